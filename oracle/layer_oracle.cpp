@@ -1,0 +1,134 @@
+// TEST INFRASTRUCTURE ONLY -- see layer_oracle.hpp.
+#include "layer_oracle.hpp"
+
+#include <algorithm>
+#include <cmath>
+
+namespace helix_oracle {
+
+Mat hash_matrix(std::uint64_t seed, HashKind kind, i64 layer, i64 rows, i64 cols, double scale,
+                bool bf16) {
+  Mat m(rows, cols);
+  const std::uint64_t stream = hash_stream(kind, layer);
+  for (i64 r = 0; r < rows; ++r)
+    for (i64 c = 0; c < cols; ++c) {
+      const double v = hash_unit(seed, stream, static_cast<std::uint64_t>(r * cols + c)) * scale;
+      m(r, c) = bf16 ? round_bf16(v) : v;
+    }
+  return m;
+}
+
+std::vector<double> rmsnorm(const std::vector<double>& x, double eps) {
+  double ss = 0.0;
+  for (double v : x) ss += v * v;
+  const double inv = 1.0 / std::sqrt(ss / static_cast<double>(x.size()) + eps);
+  std::vector<double> y(x.size());
+  for (std::size_t i = 0; i < x.size(); ++i) y[i] = x[i] * inv;
+  return y;
+}
+
+namespace {
+// y = x . W for W [in x out] row-major
+std::vector<double> vecmat(const std::vector<double>& x, const Mat& w) {
+  std::vector<double> y(static_cast<std::size_t>(w.cols), 0.0);
+  for (i64 c = 0; c < w.cols; ++c) {
+    double acc = 0.0;
+    for (i64 k = 0; k < w.rows; ++k) acc += x[static_cast<std::size_t>(k)] * w(k, c);
+    y[static_cast<std::size_t>(c)] = acc;
+  }
+  return y;
+}
+}  // namespace
+
+ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, std::uint64_t seed,
+                         QkvInit qkv_init, bool bf16)
+    : d_(d), batch_(batch), seed_(seed), bf16_(bf16) {
+  if (d.hidden != d.query_heads * d.head_size)
+    throw std::invalid_argument("hidden_dim must equal query_heads * head_size");
+  const double sh = 1.0 / std::sqrt(static_cast<double>(d.hidden));
+  const double sf = 1.0 / std::sqrt(static_cast<double>(d.ffn));
+  h_.reserve(static_cast<std::size_t>(d.layers * batch));
+  for (i64 l = 0; l < d.layers; ++l) {
+    for (i64 b = 0; b < batch; ++b) {
+      h_.emplace_back(Dims{d.query_heads, d.kv_heads, d.head_size}, tpa, kvp, chunk,
+                      seed + static_cast<std::uint64_t>(l), bf16);
+      if (qkv_init == QkvInit::Hash)
+        h_.back().set_weights(
+            hash_matrix(seed, kWq, l, d.hidden, d.query_heads * d.head_size, 1.0, bf16),
+            hash_matrix(seed, kWk, l, d.hidden, d.kv_heads * d.head_size, 1.0, bf16),
+            hash_matrix(seed, kWv, l, d.hidden, d.kv_heads * d.head_size, 1.0, bf16));
+    }
+    wo_.push_back(hash_matrix(seed, kWo, l, d.hidden, d.hidden, sh, bf16));
+    wg_.push_back(hash_matrix(seed, kWgate, l, d.hidden, d.ffn, sh, bf16));
+    wu_.push_back(hash_matrix(seed, kWup, l, d.hidden, d.ffn, sh, bf16));
+    wd_.push_back(hash_matrix(seed, kWdown, l, d.ffn, d.hidden, sf, bf16));
+  }
+  emb_ = hash_matrix(seed, kEmb, 0, d.vocab, d.hidden, 1.0, bf16);
+  lm_ = hash_matrix(seed, kLm, 0, d.hidden, d.vocab, sh, bf16);
+}
+
+void ModelOracle::grow_random(i64 layer, i64 request, i64 n, std::mt19937_64& rng) {
+  harness(layer, request).grow_random(n, rng);
+}
+
+void ModelOracle::grow_hash(i64 layer, i64 request, i64 n) {
+  DecodeHarness& h = harness(layer, request);
+  const i64 K = d_.kv_heads, w = d_.head_size;
+  for (i64 i = 0; i < n; ++i) {
+    const i64 g = h.cache().total_tokens();
+    Mat k(K, w), v(K, w);
+    for (i64 kh = 0; kh < K; ++kh)
+      for (i64 dd = 0; dd < w; ++dd) {
+        const std::uint64_t idx =
+            ((static_cast<std::uint64_t>(request * K + kh) << 32) + static_cast<std::uint64_t>(g)) *
+                static_cast<std::uint64_t>(w) +
+            static_cast<std::uint64_t>(dd);
+        const double kv = hash_unit(seed_, hash_stream(kCacheK, layer), idx);
+        const double vv = hash_unit(seed_, hash_stream(kCacheV, layer), idx);
+        k(kh, dd) = bf16_ ? round_bf16(kv) : kv;
+        v(kh, dd) = bf16_ ? round_bf16(vv) : vv;
+      }
+    h.cache().append_round_robin(k, v);
+  }
+}
+
+std::vector<double> ModelOracle::step(const std::vector<std::int64_t>& tokens,
+                                      std::vector<double>* hidden,
+                                      std::vector<std::int64_t>* next) {
+  if (static_cast<i64>(tokens.size()) != batch_)
+    throw std::invalid_argument("token batch has wrong size");
+  const i64 H = d_.hidden;
+  std::vector<double> logits(static_cast<std::size_t>(batch_ * d_.vocab));
+  if (hidden) hidden->assign(static_cast<std::size_t>((d_.layers + 1) * batch_ * H), 0.0);
+  if (next) next->assign(static_cast<std::size_t>(batch_), 0);
+  for (i64 b = 0; b < batch_; ++b) {
+    const std::int64_t tok = tokens[static_cast<std::size_t>(b)];
+    if (tok < 0 || tok >= d_.vocab) throw std::invalid_argument("token id out of range");
+    std::vector<double> x(emb_.row(tok), emb_.row(tok) + H);
+    if (hidden) std::copy(x.begin(), x.end(), hidden->begin() + b * H);
+    for (i64 l = 0; l < d_.layers; ++l) {
+      const std::vector<double> a = rmsnorm(x);
+      const Mat att = harness(l, b).step(a);  // [Q x Hsz] == flattened [H]
+      const std::vector<double> o = vecmat(att.a, wo_[static_cast<std::size_t>(l)]);
+      std::vector<double> h(static_cast<std::size_t>(H));
+      for (i64 i = 0; i < H; ++i) h[static_cast<std::size_t>(i)] = x[static_cast<std::size_t>(i)] + o[static_cast<std::size_t>(i)];
+      const std::vector<double> f = rmsnorm(h);
+      const std::vector<double> gt = vecmat(f, wg_[static_cast<std::size_t>(l)]);
+      const std::vector<double> up = vecmat(f, wu_[static_cast<std::size_t>(l)]);
+      std::vector<double> m(gt.size());
+      for (std::size_t i = 0; i < m.size(); ++i) m[i] = gt[i] / (1.0 + std::exp(-gt[i])) * up[i];
+      const std::vector<double> dn = vecmat(m, wd_[static_cast<std::size_t>(l)]);
+      for (i64 i = 0; i < H; ++i) x[static_cast<std::size_t>(i)] = h[static_cast<std::size_t>(i)] + dn[static_cast<std::size_t>(i)];
+      if (hidden)
+        std::copy(x.begin(), x.end(), hidden->begin() + ((l + 1) * batch_ + b) * H);
+    }
+    const std::vector<double> lg = vecmat(rmsnorm(x), lm_);
+    std::copy(lg.begin(), lg.end(), logits.begin() + b * d_.vocab);
+    if (next)
+      (*next)[static_cast<std::size_t>(b)] =
+          static_cast<std::int64_t>(std::max_element(lg.begin(), lg.end()) - lg.begin());
+  }
+  return logits;
+}
+
+}  // namespace helix_oracle
