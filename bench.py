@@ -1,0 +1,287 @@
+#!/usr/bin/env python
+"""Helix decode-step benchmark (driver contract: one JSON line on rank 0).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[1]): Llama-3-8B-shaped GQA decoder
+(H=4096, Q=32, K=8, Hsz=128, F=14336, 32 layers, vocab 128256), batch 8,
+131072-token synthetic KV per request, one B200, KVP=1. A step is one full
+decode step of the stack (embedding -> 32 x [RMSNorm, QKV+append, Helix
+attention, O-proj, RMSNorm, SwiGLU FFN] -> LM head -> greedy token) for all
+8 requests; metric = tokens/s (aggregate) and TTL ms/token (= ms_per_step).
+Synthetic bf16 weights/KV from the counter hash; KV per layer (4.3 GB) far
+exceeds L2, so no flush is needed between steps.
+
+`--impl reference` times the reference's own CPU implementation of the path
+(DecodeHarness<double>::step, attention.hpp:460-510, built from /root/reference
+sources into oracle/_ref/ref_bench) on the host cores with all threads.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "TTL ms/token and tokens/s/GPU at 1M-token KV, KVP=1/2/4/8 on B200"
+UNIT = "tokens/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--batch", type=int, default=8)
+    ap.add_argument("--context", type=int, default=131072, help="KV tokens per request per GPU")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-context", type=int, default=131072)
+    ap.add_argument("--profile-only", action="store_true", help="skip timing loops (for ncu)")
+    return ap.parse_args()
+
+
+def config_dict(a, n):
+    return {"workload": "llama3-8b-shaped GQA decode (H=4096 Q=32 K=8 Hsz=128 F=14336 V=128256), "
+                        f"{a.layers} layers, batch {a.batch}, {a.context} KV tokens/request/GPU, KVP={n}",
+            "model": "llama3-8b-like", "global_batch": a.batch, "seq_len": a.context * n,
+            "layers": a.layers, "parallelism": f"helix tpa=1 kvp={n} tpf={n}",
+            "l2": "no flush needed: per-layer KV (4.3 GB) >> 126 MB L2"}
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    def __init__(self):
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, device=0):
+        rows = [r for r in self.samples if len(r) >= 9 and r[0] == str(device)]
+        if not rows:
+            return None
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for name, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": float(rows[0][2]),
+                "reasons": sorted(reasons), "samples": len(rows)}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["hbm_gbs"], "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def ncu_traffic():
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
+            return json.load(f).get("attention", {}).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# ----------------------------------------------------------------------------- CPU reference
+def run_ref_bench(threads, context, steps, warmup, layers, batch):
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+    if os.path.exists(exe):
+        out = subprocess.run([exe, "32", "8", "128", "1", "1", str(context), str(steps), str(threads), str(warmup)],
+                             capture_output=True, text=True, check=True).stdout
+        r = json.loads(out.strip().splitlines()[-1])
+        t = r["seconds_per_step_per_request"]
+        kind = "reference"
+    else:
+        # oracle port (clean-room restatement) when the reference could not be built
+        from tests import oracle_py as O
+        h = O.Harness(32, 8, 128, 1, 1, 16, 42)
+        h.grow_random(context, O.Rng(1000))
+        x = O.Rng(7).draws(4096)
+        for _ in range(warmup):
+            h.step(x)
+        t0 = time.time()
+        for _ in range(steps):
+            h.step(x)
+        t = (time.time() - t0) / steps
+        threads, kind = 1, "port"
+    # one decode step = batch x layers reference harness steps; threads run requests in parallel
+    tok_s = threads / (t * layers)
+    sample = (f"DecodeHarness<double>::step, Q=32 K=8 Hsz=128, {context}-token context, {steps} timed steps "
+              f"x {threads} concurrent requests; extrapolated x{layers} layers (the reference has no "
+              f"O-proj/FFN/LM-head numerics, so this CPU figure covers attention only)")
+    return {"value": tok_s, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
+            "seconds_per_request_layer_step": t}
+
+
+def reference_arm(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    ctx = a.cpu_context
+    # bound memory: ~16.8 KB of doubles per token per request (K,V x 8 heads x 128)
+    try:
+        mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
+        threads = max(1, min(threads, int(mem * 0.5 // (ctx * 8 * 128 * 2 * 8 * 1.5))))
+    except (ValueError, OSError):
+        pass
+    steps = max(1, min(a.steps, 3))
+    cb = run_ref_bench(threads, ctx, steps, min(a.warmup, 1), a.layers, a.batch)
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": a.gpus, "steps": steps,
+            "warmup": min(a.warmup, 1), "ms_per_step": a.batch / cb["value"] * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(a, a.gpus), "impl": "reference",
+            "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+            "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- our arm
+def ours(a):
+    import numpy as np
+    import torch
+    import paper_2507_07120_b200 as P
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1 or a.gpus > 1:
+        raise SystemExit("multi-GPU Helix (NCCL) arm is not available in this build")
+    dev = 0
+    torch.cuda.set_device(dev)
+    spec = P.model.PRESETS["llama3-8b-like"]
+    B, S, L = a.batch, a.context, a.layers
+    total_steps = a.warmup + a.steps
+    cap = S + 4 * (total_steps + 8) + 64
+    eng = P.HelixDecoder(spec, tpa=1, kvp=1, batch=B, capacity=cap, layers=L, device=dev)
+    eng.init_weights(2507, qkv="hash")
+    eng.fill_kv_hash(S, 2507)
+    info = eng.info()
+    stream = torch.cuda.ExternalStream(eng.stream())
+
+    tok = [torch.randint(0, spec.vocab, (B,), dtype=torch.int32, device="cuda"),
+           torch.zeros(B, dtype=torch.int32, device="cuda")]
+
+    def dev_step(i):
+        eng.step_device(tok[i % 2].data_ptr(), tok[(i + 1) % 2].data_ptr())
+
+    for i in range(a.warmup):
+        dev_step(i)
+    eng.synchronize()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler() as clk:
+        time.sleep(0.3)
+        e0.record(stream)
+        for i in range(a.steps):
+            dev_step(a.warmup + i)
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / a.steps
+        # e2e through the public API: pinned host tokens in, host next tokens out, every step
+        h_tok = torch.zeros(B, dtype=torch.int32).pin_memory()
+        h_next = torch.zeros(B, dtype=torch.int32).pin_memory()
+        h_tok.copy_(tok[0].cpu())
+        import ctypes
+        ip = ctypes.POINTER(ctypes.c_int32)
+        e2 = torch.cuda.Event(enable_timing=True)
+        e3 = torch.cuda.Event(enable_timing=True)
+        w0 = time.perf_counter()
+        e2.record(stream)
+        for i in range(a.steps):
+            rc = P.lib().hx_decode_step(eng._h, ctypes.cast(h_tok.data_ptr(), ip), ctypes.cast(h_next.data_ptr(), ip),
+                                        None, None)
+            P._lib.check(rc, eng._h)
+            h_tok.copy_(h_next)
+        e3.record(stream)
+        e3.synchronize()
+        wall_e2e = (time.perf_counter() - w0) / a.steps * 1e3
+        ms_e2e = max(e2.elapsed_time(e3) / a.steps, wall_e2e)
+    clocks = clk.summary(dev)
+
+    # per-kernel-kind breakdown (eager launches, CUDA events on the engine stream)
+    prof = np.zeros(9)
+    P.lib().hx_profile_step(eng._h, 2, prof.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    step_prof = prof.sum()
+    attn_ms_launch = prof[2] / L
+    s_now = eng.total_tokens(0, 0)
+    attn_bytes = B * spec.kv_heads * s_now * spec.head_size * 2 * 2  # K+V bf16, algorithmic
+    weight_bytes = info["weight_bytes_per_layer"] * L + info["head_bytes"] // 2  # LM head read; embedding gather ~0
+    hbm_peak, peak_kind = peaks()
+    achieved = attn_bytes / (attn_ms_launch * 1e-3) / 1e9
+    step_bytes = attn_bytes * L + weight_bytes
+    value = B / (ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms, "ttl_ms": ms, "tokens_per_s_per_gpu": value, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": config_dict(a, 1),
+        "e2e": {"value": B / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 4 * B, "d2h_bytes_per_step": 4 * B,
+                "ms_per_step": ms_e2e},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": ncu_traffic(), "kernel": "attn_decode_kernel<128,8,2>",
+                     "algorithmic_bytes_per_launch": attn_bytes, "launch_ms": attn_ms_launch, "peak_kind": peak_kind,
+                     "step_hbm_frac": step_bytes / (ms * 1e-3) / 1e9 / hbm_peak,
+                     "step_algorithmic_bytes": step_bytes},
+        "breakdown_ms": {k: float(v) for k, v in zip(
+            ["embed", "qkv", "attention", "split_reduce", "o_proj", "gate_up", "down", "lm_head", "merge"], prof)},
+        "profile_step_ms": step_prof,
+        "gpu_launches": int(info["kernels_per_step"]) * a.steps,
+        "clocks": clocks,
+        "engine": info,
+    }
+    if not a.no_cpu_baseline and rank == 0:
+        try:
+            cb = run_ref_bench(1, a.cpu_context, 2, 0, L, B)
+            line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as ex:  # reported, never fatal for the GPU number
+            line["cpu_baseline"] = {"error": str(ex)[:200]}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = parse()
+    if a.impl == "reference":
+        reference_arm(a)
+    else:
+        ours(a)
+
+
+if __name__ == "__main__":
+    main()

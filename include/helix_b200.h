@@ -1,0 +1,159 @@
+/* helix_b200.h -- C-ABI boundary of the B200-native Helix decode step.
+ *
+ * Drop-in replacement for the reference's decode path
+ * (/root/reference/proj/include/helixsim/attention.hpp, namespace
+ * helixsim::exact). The reference is a header-only C++ template library with
+ * no FFI; these entry points are what its C++ API lowers to, one per
+ * reference operation (the C++ mirror in include/helixsim/exact_b200.hpp
+ * re-exposes them under the reference's names):
+ *
+ *   DecodeHarness ctor          attention.hpp:428-443  -> hx_engine_create + hx_init_weights_mt19937
+ *   DecodeHarness::grow_random  attention.hpp:452-456  -> hx_grow_random
+ *   DecodeHarness::step         attention.hpp:460-510  -> hx_harness_step
+ *   DecodeHarness::append_projected :531-539           -> fused into hx_harness_step / hx_decode_step
+ *   DecodeHarness::transcript   attention.hpp:401-411  -> hx_transcript
+ *   ShardedKVCache::{effective_tokens,total_tokens,max_min_gap} :286-299
+ *                                                      -> hx_effective_tokens / hx_total_tokens / hx_max_min_gap
+ *   ShardedKVCache::context     attention.hpp:303-309  -> hx_read_kv
+ *   (analytical decode layer, latency.cpp:45-146)      -> hx_decode_step (full layer: O-proj, FFN, LM head)
+ *
+ * Conventions: plain pointers and sizes only; host buffers are caller-owned
+ * and copied; no exceptions cross the ABI. Every call returns HX_OK or an
+ * error code; the message (the reference's std::invalid_argument text where
+ * the reference throws) is available from hx_last_error().
+ * There is no CPU fallback: a missing/failed CUDA device is HX_ERR_CUDA.
+ */
+#ifndef HELIX_B200_H_
+#define HELIX_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HX_OK 0
+#define HX_ERR_INVALID 1 /* reference std::invalid_argument */
+#define HX_ERR_CUDA 2
+#define HX_ERR_NCCL 3
+#define HX_ERR_STATE 4
+
+typedef struct hx_engine hx_engine;
+typedef struct hx_rng hx_rng;
+
+typedef struct hx_model_config {
+  int64_t hidden;       /* H = query_heads * head_size (types.hpp:31) */
+  int64_t query_heads;  /* Q */
+  int64_t kv_heads;     /* K */
+  int64_t head_size;    /* Hsz */
+  int64_t ffn;          /* F (dense SwiGLU width) */
+  int64_t layers;
+  int64_t vocab;
+  int32_t attention_only; /* 1: DecodeHarness semantics only (no norm/O/FFN/LM head) */
+  int32_t reserved;
+} hx_model_config;
+
+typedef struct hx_parallel_config {
+  int64_t tpa;          /* attention tensor parallelism (types.hpp:97) */
+  int64_t kvp;          /* KV parallelism across the sequence (types.hpp:98) */
+  int64_t chunk_size;   /* round-robin chunk (attention.hpp:237, default 16) */
+  int32_t distributed;  /* 0: whole tpa*kvp pool on this device; 1: this process is one rank */
+  int32_t rank;         /* global rank id g*kvp + r (attention.hpp:555) when distributed */
+  const void* nccl_unique_id; /* 128 bytes (ncclUniqueId) when distributed */
+} hx_parallel_config;
+
+typedef struct hx_runtime_config {
+  int64_t batch;            /* concurrent requests (one DecodeHarness each) */
+  int64_t capacity_tokens;  /* max global context per request */
+  int32_t device;
+  int32_t hopb;             /* HOP-B batch-wise comm/compute overlap (overlap.hpp:37-69) */
+  int32_t use_graphs;       /* capture the decode step in a CUDA graph */
+  int32_t reserved;
+} hx_runtime_config;
+
+typedef struct hx_engine_info {
+  int64_t kv_bytes_per_layer;      /* resident KV pool bytes on this device, per layer */
+  int64_t weight_bytes_per_layer;  /* QKV + O + FFN weight bytes on this device, per layer */
+  int64_t head_bytes;              /* embedding + LM head bytes */
+  int64_t attn_streams, attn_splits, attn_items, attn_grid;
+  int64_t kernels_per_step;        /* kernel launches of one hx_decode_step (or harness step) */
+  int64_t page_cap;
+  int64_t head_dim_padded;
+} hx_engine_info;
+
+const char* hx_version(void);
+const char* hx_last_error(const hx_engine* e); /* e may be NULL: last create/global error */
+
+int hx_engine_create(const hx_model_config* model, const hx_parallel_config* par,
+                     const hx_runtime_config* rt, hx_engine** out);
+void hx_engine_destroy(hx_engine* e);
+int hx_engine_get_info(const hx_engine* e, hx_engine_info* info);
+
+/* --- weights --- */
+/* W_q/W_k/W_v of layer l drawn exactly as DecodeHarness(seed + l) draws them
+ * (attention.hpp:438-442, mt19937_64, row-major U[-1,1)), stored bf16;
+ * extension weights from the counter hash (oracle/layer_oracle.hpp). */
+int hx_init_weights_mt19937(hx_engine* e, uint64_t seed);
+/* All weights from the counter hash (device-side, fast; bench shapes). */
+int hx_init_weights_hash(hx_engine* e, uint64_t seed);
+
+/* --- KV cache growth (reference grow_random: per token V then K) --- */
+int hx_rng_create(uint64_t seed, hx_rng** out);
+void hx_rng_destroy(hx_rng* r);
+double hx_rng_unit_draw(hx_rng* r); /* attention.hpp:549-552 */
+int hx_grow_random(hx_engine* e, int64_t layer, int64_t request, int64_t n, hx_rng* rng);
+/* Append n tokens of host K/V rows [n][kv_heads][head_size] (fp32, stored bf16). */
+int hx_append_kv(hx_engine* e, int64_t layer, int64_t request, int64_t n, const float* k,
+                 const float* v);
+/* Device-side synthetic growth of every (layer, request) cache by n tokens
+ * (hash RNG, same values as ModelOracle::grow_hash). */
+int hx_fill_kv_hash(hx_engine* e, int64_t n, uint64_t seed);
+
+int64_t hx_total_tokens(const hx_engine* e, int64_t layer, int64_t request);
+int64_t hx_effective_tokens(const hx_engine* e, int64_t layer, int64_t request, int64_t rank);
+int64_t hx_max_min_gap(const hx_engine* e, int64_t layer, int64_t request);
+/* Rows of (rank, kv head) in append order, trimmed (ShardedKVCache::context). */
+int hx_read_kv(hx_engine* e, int64_t layer, int64_t request, int64_t rank, int64_t head,
+               float* keys, float* values);
+
+/* --- the decode step --- */
+/* DecodeHarness::step for every request of the batch on one layer's cache:
+ * x [batch][hidden] -> out [batch][query_heads][head_size] (+ lse [batch][query_heads],
+ * natural log), then append each request's projected K/V (attend-then-append). */
+int hx_harness_step(hx_engine* e, int64_t layer, const float* x, int64_t x_len, float* out,
+                    float* lse);
+/* Full decode step of the layer stack for the batch: tokens [batch] -> next
+ * greedy tokens [batch]; optional logits [batch][vocab] and residual-stream
+ * hidden states [layers+1][batch][hidden]. */
+int hx_decode_step(hx_engine* e, const int32_t* tokens, int32_t* next_tokens, float* logits,
+                   float* hidden);
+/* Device-resident variant (no host copies): tokens/next are device pointers. */
+int hx_decode_step_device(hx_engine* e, const int32_t* tokens_dev, int32_t* next_dev);
+/* Device-resident harness step (x/out device pointers, [batch][hidden] / [batch][Q][Hsz]). */
+int hx_harness_step_device(hx_engine* e, int64_t layer, const float* x_dev, float* out_dev);
+int hx_synchronize(hx_engine* e);
+/* Profiling: `reps` eager steps (decode step, or one harness step per layer in
+ * attention-only mode) with CUDA events after every launch on the engine
+ * stream; ms[kind] = average milliseconds per step for kind
+ * 0 embed, 1 qkv+append, 2 attention, 3 split-reduce, 4 o-proj (+merge),
+ * 5 gate/up, 6 down, 7 lm-head+argmax, 8 merge (harness). Advances the caches
+ * like real steps. */
+#define HX_PROF_KINDS 9
+int hx_profile_step(hx_engine* e, int64_t reps, double* ms);
+/* The engine's CUDA stream (cudaStream_t) for event timing by the caller. */
+void* hx_stream(hx_engine* e);
+
+/* --- transcript: reference Message records (attention.hpp:401-411) --- */
+int64_t hx_transcript_size(const hx_engine* e);
+/* out [n][5] = kind (0 broadcast, 1 all-to-all), src, dst, payload_scalars, lse_scalars */
+int hx_transcript(const hx_engine* e, int64_t* out);
+int hx_clear_transcript(hx_engine* e);
+
+/* --- distributed plumbing --- */
+int hx_nccl_get_unique_id(void* out128);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HELIX_B200_H_ */

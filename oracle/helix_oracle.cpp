@@ -330,7 +330,9 @@ void DecodeHarness::append_projected(const std::vector<double>& x) {
   cache_.append_round_robin(k, v);
 }
 
-Mat DecodeHarness::step(const std::vector<double>& x) {
+Mat DecodeHarness::step(const std::vector<double>& x) { return step_with_append(x, nullptr, nullptr); }
+
+Mat DecodeHarness::step_with_append(const std::vector<double>& x, const Mat* k_over, const Mat* v_over) {
   // attention.hpp:460-510 -- attend, exchange, merge, THEN append
   if (static_cast<i64>(x.size()) != dims_.hidden())
     throw std::invalid_argument("hidden state has wrong width");
@@ -373,7 +375,10 @@ Mat DecodeHarness::step(const std::vector<double>& x) {
           merged.lse[static_cast<std::size_t>(qi)];
     }
   }
-  append_projected(x);
+  if (k_over && v_over)
+    cache_.append_round_robin(*k_over, *v_over);
+  else
+    append_projected(x);
   return out;
 }
 

@@ -139,6 +139,10 @@ class DecodeHarness {
                 bool bf16_storage = false);
   void grow_random(i64 n, std::mt19937_64& rng);              // :452-456
   Mat step(const std::vector<double>& x);                     // :460-510
+  // step() whose final append uses the given rows (k, v: [kv_heads x w])
+  // instead of this harness's own projection -- lets a parity test feed the
+  // exact bf16 rows the GPU stored, isolating attention arithmetic.
+  Mat step_with_append(const std::vector<double>& x, const Mat* k, const Mat* v);
   Mat reference(const std::vector<double>& x) const;          // :514-529
   void append_projected(const std::vector<double>& x);        // :531-539
   std::vector<double> project_q(const std::vector<double>& x) const;  // x^T W_q, all heads

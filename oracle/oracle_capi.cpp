@@ -60,6 +60,20 @@ int oracle_harness_step(void* hp, const double* x, i64 n, double* out, double* l
   });
 }
 
+int oracle_harness_step_append(void* hp, const double* x, i64 n, double* out, double* lse,
+                               const double* k, const double* v) {
+  return guard([&] {
+    auto* h = static_cast<DecodeHarness*>(hp);
+    const Dims d = h->dims();
+    Mat km(d.kv_heads, d.head_size), vm(d.kv_heads, d.head_size);
+    std::memcpy(km.a.data(), k, km.a.size() * sizeof(double));
+    std::memcpy(vm.a.data(), v, vm.a.size() * sizeof(double));
+    Mat o = h->step_with_append(std::vector<double>(x, x + n), &km, &vm);
+    std::memcpy(out, o.a.data(), o.a.size() * sizeof(double));
+    if (lse) std::memcpy(lse, h->last_lse().data(), h->last_lse().size() * sizeof(double));
+  });
+}
+
 int oracle_harness_reference(void* hp, const double* x, i64 n, double* out) {
   return guard([&] {
     Mat o = static_cast<DecodeHarness*>(hp)->reference(std::vector<double>(x, x + n));

@@ -4,7 +4,7 @@
 // owns an independent harness (one request of the batch), as the reference
 // runs one request per harness. Construction and KV growth are untimed.
 //
-//   ref_bench Q K Hsz tpa kvp context steps threads
+//   ref_bench Q K Hsz tpa kvp context steps threads [warmup]
 // prints one JSON line.
 #include <atomic>
 #include <chrono>
@@ -28,6 +28,7 @@ int main(int argc, char** argv) {
   const i64 tpa = std::atoll(argv[4]), kvp = std::atoll(argv[5]);
   const i64 context = std::atoll(argv[6]);
   const int steps = std::atoi(argv[7]), threads = std::atoi(argv[8]);
+  const int warmup = argc > 9 ? std::atoi(argv[9]) : 0;
 
   std::atomic<int> ready{0};
   std::atomic<bool> go{false};
@@ -40,11 +41,12 @@ int main(int argc, char** argv) {
       std::mt19937_64 rng(1000 + static_cast<std::uint64_t>(t));
       h.grow_random(context, rng);
       std::vector<Vector<double>> xs;
-      for (int s = 0; s < steps; ++s) {
+      for (int s = 0; s < steps + warmup; ++s) {
         Vector<double> x(Q * Hsz);
         for (i64 i = 0; i < Q * Hsz; ++i) x[i] = DecodeHarness<double>::unit_draw(rng);
         xs.push_back(x);
       }
+      for (int s = 0; s < warmup; ++s) h.step(xs[static_cast<std::size_t>(steps + s)]);
       ready.fetch_add(1);
       while (!go.load()) std::this_thread::yield();
       const auto t0 = std::chrono::steady_clock::now();

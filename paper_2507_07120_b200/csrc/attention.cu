@@ -1,0 +1,440 @@
+// K1: KV-parallel GQA flash-decode partial attention for sm_100a.
+//
+// Replaces the per-(rank, kv head, query head) Eigen GEMVs of
+// shard_attention / partial_head_attention (reference attention.hpp:65-78,
+// :375-396): one pass over a rank's KV shard serves every query head of the
+// GQA group, emitting a locally normalised partial output plus its
+// log-sum-exp per query head -- exactly the (partial_out, lse) pair of
+// HeadFragment (:56-59), computed per contiguous page range ("split").
+//
+// Structure (persistent, one CTA per SM, warp specialised):
+//   * producer warp: grabs work items (stream, split) from a global counter,
+//     streams the split's contiguous 16-token pages into a shared-memory ring
+//     with cp.async.bulk (TMA bulk engine), completion via mbarrier tx-bytes;
+//     the item's query rows ride along in the first stage.
+//   * NWC consumer warps: one page each per stage; S = Q K^T and O += P V on
+//     legacy HMMA m16n8k16 (bf16 in, fp32 accumulate). The fp32 query is
+//     split hi+mid+lo into three bf16 terms (rows 0-7 / 8-15 of M-tile 0 and
+//     rows 0-7 of M-tile 1) and P into hi+lo (rows 0-7 / 8-15), so the only
+//     rounding is the bf16 KV storage itself.
+//   * per item, consumers combine their per-warp (m, l, O) through shared
+//     memory and write the split's normalised O and log2-sum-exp.
+// The KV stream is the roofline: 64*DP bytes per page, no re-reads.
+#include "common.cuh"
+#include "kv_layout.cuh"
+#include "kernels.h"
+
+namespace hx {
+
+namespace {
+
+constexpr int kItemDone = -1;
+
+struct StageMeta {
+  int item;         // work item id, or kItemDone
+  int stream;       // stream index
+  int page0;        // first page (within the stream) of this stage
+  int npages;       // pages in this stage (<= NWC)
+  int ntok;         // tokens on this rank for the stream
+  int first;        // first stage of the item (q rows staged)
+  int last;         // last stage of the item
+  int rows;         // valid query rows in this stream (<= 8)
+};
+
+template <int DP>
+struct AttnCfg {
+  static constexpr int KS = DP / 16;     // k-steps over the head dim
+  static constexpr int ND = DP / 8;      // PV n-tiles
+  static constexpr uint32_t PAGE = 64u * DP;
+};
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+}  // namespace
+
+template <int DP, int NWC, int NSTAGE>
+__global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const AttnParams p) {
+  using Cfg = AttnCfg<DP>;
+  constexpr uint32_t STAGE_KV = NWC * Cfg::PAGE;
+  constexpr uint32_t Q_BYTES = 8 * DP * 4;
+  constexpr uint32_t STAGE_BYTES = STAGE_KV + Q_BYTES;
+
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* stages = smem;                                                     // NSTAGE * STAGE_BYTES
+  float* scratch = reinterpret_cast<float*>(smem + NSTAGE * STAGE_BYTES);     // NWC * (8*DP + 16)
+  StageMeta* meta = reinterpret_cast<StageMeta*>(scratch + NWC * (8 * DP + 16));
+  uint64_t* full = reinterpret_cast<uint64_t*>(meta + NSTAGE);
+  uint64_t* empty = full + NSTAGE;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < NSTAGE; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NWC);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == NWC) {
+    // ------------------------------------------------------------ producer
+    if (lane == 0) {
+      int st = 0;
+      for (;;) {
+        const int item = atomicAdd(p.work_counter, 1);
+        bool done = item >= p.n_items;
+        int stream = 0, pg0 = 0, pg1 = 0, ntok = 0, rows = 0;
+        if (!done) {
+          const int split = item / p.n_streams;
+          stream = item - split * p.n_streams;
+          // stream -> (slot, request, kv head, query chunk)
+          int t = stream;
+          const int qc = t % p.q_chunks; t /= p.q_chunks;
+          t /= p.kvh_per_slot;
+          const int b = t % p.batch;
+          const int slot = t / p.batch + p.slot_base;
+          const int rank = slot % p.kvp;
+          ntok = static_cast<int>(rr_count(p.total[b], rank, p.chunk, p.kvp));
+          const int pages = (ntok + 15) >> 4;
+          pg0 = static_cast<int>((static_cast<long long>(split) * pages) / p.splits);
+          pg1 = static_cast<int>((static_cast<long long>(split + 1) * pages) / p.splits);
+          const int g_rows = p.group - qc * 8;
+          rows = g_rows < 8 ? g_rows : 8;
+          if (pg1 <= pg0) continue;  // empty split: nothing to emit
+        }
+        const int nchunks = done ? 1 : (pg1 - pg0 + NWC - 1) / NWC;
+        for (int ch = 0; ch < nchunks; ++ch, ++st) {
+          const int s = st % NSTAGE;
+          if (st >= NSTAGE) mbar_wait(&empty[s], ((st / NSTAGE) & 1) ^ 1);
+          StageMeta& m = meta[s];
+          if (done) {
+            m.item = kItemDone;
+            mbar_arrive(&full[s]);
+            break;
+          }
+          const int a = pg0 + ch * NWC;
+          const int np = min(NWC, pg1 - a);
+          m.item = item;
+          m.stream = stream;
+          m.page0 = a;
+          m.npages = np;
+          m.ntok = ntok;
+          m.first = ch == 0;
+          m.last = ch == nchunks - 1;
+          m.rows = rows;
+          uint8_t* dst = stages + s * STAGE_BYTES;
+          const uint8_t* src =
+              p.kv + (static_cast<size_t>(stream / p.q_chunks) * p.page_cap + a) * Cfg::PAGE;
+          uint32_t bytes = np * Cfg::PAGE;
+          uint32_t qbytes = 0;
+          if (ch == 0) qbytes = static_cast<uint32_t>(rows) * DP * 4;
+          mbar_arrive_expect_tx(&full[s], bytes + qbytes);
+          bulk_g2s(dst, src, bytes, &full[s]);
+          if (qbytes) {
+            // q rows of this stream: [request][head][DP] fp32, heads contiguous
+            int t = stream;
+            const int qc = t % p.q_chunks; t /= p.q_chunks;
+            const int kvh = t % p.kvh_per_slot; t /= p.kvh_per_slot;
+            const int b = t % p.batch;
+            const int slot = t / p.batch + p.slot_base;
+            const int grp = slot / p.kvp;
+            const int head0 = (grp * p.kvh_per_slot + kvh) * p.group + qc * 8;
+            const float* qsrc = p.q + (static_cast<size_t>(b) * p.q_heads + head0) * DP;
+            bulk_g2s(dst + STAGE_KV, qsrc, qbytes, &full[s]);
+          }
+        }
+        if (done) break;
+      }
+    }
+  } else {
+    // ------------------------------------------------------------ consumers
+    const int g = lane >> 2, c = lane & 3;
+    uint32_t qa[Cfg::KS][4];  // M-tile 0: hi (rows 0-7), mid (rows 8-15)
+    uint32_t qb[Cfg::KS][2];  // M-tile 1: lo (rows 0-7); rows 8-15 are zero
+    float acc[Cfg::ND][4];
+    float m_ref = -INFINITY, l_sum = 0.f;
+    int st = 0;
+    const uint32_t stage_base = smem_u32(stages);
+    for (;; ++st) {
+      const int s = st % NSTAGE;
+      mbar_wait(&full[s], (st / NSTAGE) & 1);
+      const StageMeta m = meta[s];
+      if (m.item == kItemDone) break;
+      const uint32_t sbase = stage_base + s * STAGE_BYTES;
+      if (m.first) {
+        // stage the item's query rows as hi/mid/lo bf16 fragments
+        const float* qs = reinterpret_cast<const float*>(stages + s * STAGE_BYTES + STAGE_KV);
+        const bool valid = g < m.rows;
+#pragma unroll
+        for (int ks = 0; ks < Cfg::KS; ++ks) {
+          float v[4];
+          const int d0 = ks * 16 + 2 * c;
+          v[0] = valid ? qs[g * DP + d0] * p.qscale : 0.f;
+          v[1] = valid ? qs[g * DP + d0 + 1] * p.qscale : 0.f;
+          v[2] = valid ? qs[g * DP + d0 + 8] * p.qscale : 0.f;
+          v[3] = valid ? qs[g * DP + d0 + 9] * p.qscale : 0.f;
+          float hi[4], mid[4], lo[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) split3(v[i], hi[i], mid[i], lo[i]);
+          qa[ks][0] = pack_bf16(hi[0], hi[1]);
+          qa[ks][1] = pack_bf16(mid[0], mid[1]);
+          qa[ks][2] = pack_bf16(hi[2], hi[3]);
+          qa[ks][3] = pack_bf16(mid[2], mid[3]);
+          qb[ks][0] = pack_bf16(lo[0], lo[1]);
+          qb[ks][1] = pack_bf16(lo[2], lo[3]);
+        }
+#pragma unroll
+        for (int nd = 0; nd < Cfg::ND; ++nd) acc[nd][0] = acc[nd][1] = acc[nd][2] = acc[nd][3] = 0.f;
+        m_ref = -INFINITY;
+        l_sum = 0.f;
+      }
+      if (warp < m.npages) {
+        const uint32_t pbase = sbase + warp * Cfg::PAGE;
+        const int tok0 = (m.page0 + warp) * 16;
+        const int valid_tok = m.ntok - tok0;  // >= 1
+        // ---- S = Q K^T over the 16 tokens of this page
+        float s0[2][4], s1[2][4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+          for (int i = 0; i < 4; ++i) s0[nt][i] = s1[nt][i] = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+          for (int kp = 0; kp < Cfg::KS / 2; ++kp) {
+            const uint4 kf = lds128(pbase + ((nt * (Cfg::KS / 2) + kp) * 32 + lane) * 16);
+            const int k0 = 2 * kp, k1 = 2 * kp + 1;
+            mma_bf16_16816(s0[nt], qa[k0][0], qa[k0][1], qa[k0][2], qa[k0][3], kf.x, kf.y);
+            mma_bf16_16816(s1[nt], qb[k0][0], 0u, qb[k0][1], 0u, kf.x, kf.y);
+            mma_bf16_16816(s0[nt], qa[k1][0], qa[k1][1], qa[k1][2], qa[k1][3], kf.z, kf.w);
+            mma_bf16_16816(s1[nt], qb[k1][0], 0u, qb[k1][1], 0u, kf.z, kf.w);
+          }
+        }
+        // logits (log2 units) for query row g, tokens 2c, 2c+1, 8+2c, 9+2c
+        float sv[4];
+        sv[0] = s0[0][0] + s0[0][2] + s1[0][0];
+        sv[1] = s0[0][1] + s0[0][3] + s1[0][1];
+        sv[2] = s0[1][0] + s0[1][2] + s1[1][0];
+        sv[3] = s0[1][1] + s0[1][3] + s1[1][1];
+        if (valid_tok < 16) {
+          if (2 * c >= valid_tok) sv[0] = -INFINITY;
+          if (2 * c + 1 >= valid_tok) sv[1] = -INFINITY;
+          if (8 + 2 * c >= valid_tok) sv[2] = -INFINITY;
+          if (9 + 2 * c >= valid_tok) sv[3] = -INFINITY;
+        }
+        float mx = fmaxf(fmaxf(sv[0], sv[1]), fmaxf(sv[2], sv[3]));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+        mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+        // Lazy rescale: keep the reference max unless it grows by > 8 (log2),
+        // exact in real arithmetic; bounds p by 2^8.
+        const bool grow = mx > m_ref + 8.f;
+        if (__any_sync(0xffffffffu, grow)) {
+          const float m_new = grow ? mx : m_ref;
+          const float alpha = fast_exp2(m_ref - m_new);  // 0 when m_ref = -inf
+          l_sum *= alpha;
+#pragma unroll
+          for (int nd = 0; nd < Cfg::ND; ++nd)
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[nd][i] *= alpha;
+          m_ref = m_new;
+        }
+        float pv[4], ph[4], pl[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          pv[i] = fast_exp2(sv[i] - m_ref);
+          split2(pv[i], ph[i], pl[i]);
+        }
+        l_sum += (pv[0] + pv[1]) + (pv[2] + pv[3]);
+        const uint32_t a0 = pack_bf16(ph[0], ph[1]);
+        const uint32_t a1 = pack_bf16(pl[0], pl[1]);
+        const uint32_t a2 = pack_bf16(ph[2], ph[3]);
+        const uint32_t a3 = pack_bf16(pl[2], pl[3]);
+        // ---- O += P V
+        const uint32_t vbase = pbase + 32 * DP;
+#pragma unroll
+        for (int nd2 = 0; nd2 < Cfg::ND / 2; ++nd2) {
+          const uint4 vf = lds128(vbase + (nd2 * 32 + lane) * 16);
+          mma_bf16_16816(acc[2 * nd2], a0, a1, a2, a3, vf.x, vf.y);
+          mma_bf16_16816(acc[2 * nd2 + 1], a0, a1, a2, a3, vf.z, vf.w);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+
+      if (m.last) {
+        // ---- combine the NWC warps' (m, l, O) for this item
+        float* ws = scratch + warp * (8 * DP + 16);
+        float l_tot = l_sum;
+        l_tot += __shfl_xor_sync(0xffffffffu, l_tot, 1);
+        l_tot += __shfl_xor_sync(0xffffffffu, l_tot, 2);
+        if (c == 0) {
+          ws[8 * DP + g] = m_ref;      // -inf for warps that saw no page
+          ws[8 * DP + 8 + g] = l_tot;
+        }
+#pragma unroll
+        for (int nd = 0; nd < Cfg::ND; ++nd) {
+          const int d = nd * 8 + 2 * c;
+          ws[g * DP + d] = acc[nd][0] + acc[nd][2];
+          ws[g * DP + d + 1] = acc[nd][1] + acc[nd][3];
+        }
+        named_bar_sync(1, NWC * 32);
+        const int rows = m.rows;
+        const size_t obase = static_cast<size_t>(m.item) * 8 * DP;
+        for (int idx = threadIdx.x; idx < rows * DP; idx += NWC * 32) {
+          const int q = idx / DP, d = idx - q * DP;
+          float M = -INFINITY;
+#pragma unroll
+          for (int w = 0; w < NWC; ++w) M = fmaxf(M, scratch[w * (8 * DP + 16) + 8 * DP + q]);
+          float L = 0.f, O = 0.f;
+#pragma unroll
+          for (int w = 0; w < NWC; ++w) {
+            const float* wsw = scratch + w * (8 * DP + 16);
+            const float mw = wsw[8 * DP + q];
+            const float e = mw == -INFINITY ? 0.f : fast_exp2(mw - M);
+            L += wsw[8 * DP + 8 + q] * e;
+            O += wsw[q * DP + d] * e;
+          }
+          p.part_o[obase + idx] = O / L;
+          if (d == 0) p.part_lse2[static_cast<size_t>(m.item) * 8 + q] = M + __log2f(L);
+        }
+        named_bar_sync(1, NWC * 32);
+        // the next item re-initialises state on its first stage
+        m_ref = -INFINITY;
+        l_sum = 0.f;
+#pragma unroll
+        for (int nd = 0; nd < Cfg::ND; ++nd) acc[nd][0] = acc[nd][1] = acc[nd][2] = acc[nd][3] = 0.f;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(p.done_counter, 1) == static_cast<int>(gridDim.x) - 1) {
+      // every CTA has drained the work queue: reset for the next launch / graph replay
+      *p.work_counter = 0;
+      *p.done_counter = 0;
+      __threadfence();
+    }
+  }
+}
+
+// ------------------------------------------------------------------------
+// Split reduce: merge a stream's split partials (in split order) into the
+// rank's fragment for each query head, natural-log lse (HeadFragment,
+// attention.hpp:56-59; empty shard -> (0, -inf) as at :69-70).
+template <int DP>
+__global__ void attn_split_reduce_kernel(const AttnParams p, float* frag_o, float* frag_lse) {
+  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const int row = warp_global & 7;
+  const int stream = warp_global >> 3;
+  if (stream < p.n_streams) {
+    int t = stream;
+    const int qc = t % p.q_chunks; t /= p.q_chunks;
+    const int kvh = t % p.kvh_per_slot; t /= p.kvh_per_slot;
+    const int b = t % p.batch;
+    const int slot_local = t / p.batch;
+    const int slot = slot_local + p.slot_base;
+    const int rank = slot % p.kvp;
+    const int qrow = qc * 8 + row;
+    if (qrow < p.group) {
+      const int ntok = static_cast<int>(rr_count(p.total[b], rank, p.chunk, p.kvp));
+      const int pages = (ntok + 15) >> 4;
+      constexpr int PER = DP / 32;
+      float o[PER];
+#pragma unroll
+      for (int i = 0; i < PER; ++i) o[i] = 0.f;
+      float M = -INFINITY, L = 0.f;
+      for (int s = 0; s < p.splits; ++s) {
+        const int pg0 = static_cast<int>((static_cast<long long>(s) * pages) / p.splits);
+        const int pg1 = static_cast<int>((static_cast<long long>(s + 1) * pages) / p.splits);
+        if (pg1 <= pg0) continue;
+        const size_t item = static_cast<size_t>(s) * p.n_streams + stream;
+        const float lse2 = p.part_lse2[item * 8 + row];
+        const float Mn = fmaxf(M, lse2);
+        const float a = M == -INFINITY ? 0.f : exp2f(M - Mn);
+        const float w = exp2f(lse2 - Mn);
+        const float* src = p.part_o + (item * 8 + row) * DP;
+#pragma unroll
+        for (int i = 0; i < PER; ++i) o[i] = o[i] * a + src[lane + 32 * i] * w;
+        L = L * a + w;
+        M = Mn;
+      }
+      // fragment layout: [slot_local][b][q_in_group][DP]
+      const int q_in_group = kvh * p.group + qrow;
+      const size_t fo = ((static_cast<size_t>(slot_local) * p.batch + b) * p.q_per_slot + q_in_group);
+#pragma unroll
+      for (int i = 0; i < PER; ++i) frag_o[fo * DP + lane + 32 * i] = L > 0.f ? o[i] / L : 0.f;
+      if (lane == 0) frag_lse[fo] = L > 0.f ? (M + log2f(L)) * 0.69314718055994530942f : -INFINITY;
+    }
+  }
+}
+
+__global__ void bump_totals_kernel(int* total, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) total[i] += 1;
+}
+
+// ------------------------------------------------------------------------
+// host launchers
+template <int DP, int NWC, int NSTAGE>
+static size_t attn_smem_bytes() {
+  return NSTAGE * (NWC * AttnCfg<DP>::PAGE + 8 * DP * 4) + NWC * (8 * DP + 16) * 4 +
+         NSTAGE * sizeof(StageMeta) + 2 * NSTAGE * 8 + 64;
+}
+
+template <int DP, int NWC, int NSTAGE>
+static cudaError_t launch_attn_t(const AttnParams& p, int grid, cudaStream_t stream) {
+  const size_t smem = attn_smem_bytes<DP, NWC, NSTAGE>();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<DP, NWC, NSTAGE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  attn_decode_kernel<DP, NWC, NSTAGE><<<grid, (NWC + 1) * 32, smem, stream>>>(p);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t stream) {
+  switch (p.dp) {
+    case 32: return launch_attn_t<32, 8, 4>(p, grid, stream);
+    case 64: return launch_attn_t<64, 8, 3>(p, grid, stream);
+    case 128: return launch_attn_t<128, 8, 2>(p, grid, stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_attn_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse,
+                                     cudaStream_t stream) {
+  const int warps = p.n_streams * 8;
+  const int threads = 256;
+  const int blocks = (warps * 32 + threads - 1) / threads;
+  switch (p.dp) {
+    case 32: attn_split_reduce_kernel<32><<<blocks, threads, 0, stream>>>(p, frag_o, frag_lse); break;
+    case 64: attn_split_reduce_kernel<64><<<blocks, threads, 0, stream>>>(p, frag_o, frag_lse); break;
+    case 128: attn_split_reduce_kernel<128><<<blocks, threads, 0, stream>>>(p, frag_o, frag_lse); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bump_totals(int* total, int n, cudaStream_t stream) {
+  bump_totals_kernel<<<(n + 127) / 128, 128, 0, stream>>>(total, n);
+  return cudaGetLastError();
+}
+
+size_t attn_decode_smem_bytes(int dp) {
+  switch (dp) {
+    case 32: return attn_smem_bytes<32, 8, 4>();
+    case 64: return attn_smem_bytes<64, 8, 3>();
+    case 128: return attn_smem_bytes<128, 8, 2>();
+    default: return 0;
+  }
+}
+
+}  // namespace hx

@@ -1,0 +1,743 @@
+// Host runtime: allocation, weight init, round-robin KV bookkeeping, the
+// per-layer launch sequence and CUDA-graph capture of the whole decode step.
+#include "engine.h"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "kv_layout.cuh"
+
+namespace hx {
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw CudaError(std::string(what) + ": " + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) + ")");
+}
+
+namespace {
+
+template <class T>
+T* dalloc(size_t n, const char* what) {
+  void* p = nullptr;
+  cuda_check(cudaMalloc(&p, n * sizeof(T) + 16), what);
+  cuda_check(cudaMemset(p, 0, n * sizeof(T) + 16), what);
+  return static_cast<T*>(p);
+}
+
+// bf16 RNE of a double -- identical to oracle round_bf16 / device double_to_bf16_rne.
+uint16_t bf16_bits_from_double(double x) {
+  uint64_t b;
+  std::memcpy(&b, &x, 8);
+  const uint64_t lsb = (b >> 45) & 1ull;
+  b += 0x0FFFFFFFFFFFull + lsb;
+  b &= ~0x1FFFFFFFFFFFull;
+  double r;
+  std::memcpy(&r, &b, 8);
+  const float f = static_cast<float>(r);  // exact: <= 8 significant bits
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  return static_cast<uint16_t>(u >> 16);
+}
+uint16_t bf16_bits_from_float(float f) {
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7F800000u) == 0x7F800000u) return static_cast<uint16_t>(u >> 16);
+  u += 0x7FFFu + ((u >> 16) & 1u);
+  return static_cast<uint16_t>(u >> 16);
+}
+float float_from_bf16_bits(uint16_t h) {
+  const uint32_t u = static_cast<uint32_t>(h) << 16;
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
+double unit_draw(std::mt19937_64& rng) {  // attention.hpp:549-552
+  const double u = static_cast<double>(rng() >> 11) * 0x1.0p-53;
+  return 2.0 * u - 1.0;
+}
+
+size_t wfrag_offset_host(int n, int k, int kst) {
+  const int nt = n >> 4, rn = n & 15, ks = k >> 4, rk = k & 15;
+  const int g = rn & 7, rowhalf = rn >> 3;
+  const int c = (rk & 7) >> 1, khalf = rk >> 3, elem = rk & 1;
+  const int reg = khalf * 2 + rowhalf;
+  const int lane = g * 4 + c;
+  return ((static_cast<size_t>(nt) * kst + ks) * 32 + lane) * 16 + reg * 4 + elem * 2;
+}
+
+int round_up(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b * b); }
+
+uint64_t hash_stream(uint64_t kind, int64_t layer) { return (kind << 32) | static_cast<uint64_t>(layer); }
+enum : uint64_t { kWq = 1, kWk = 2, kWv = 3, kWo = 4, kWgate = 5, kWup = 6, kWdown = 7, kEmb = 8, kLm = 9,
+                  kCacheK = 10, kCacheV = 11 };
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx_runtime_config& rt)
+    : H_(m.hidden), Qh_(m.query_heads), Kh_(m.kv_heads), D_(m.head_size), F_(m.ffn), L_(m.layers),
+      V_(m.vocab), attn_only_(m.attention_only != 0), tpa_(static_cast<int>(par.tpa)),
+      kvp_(static_cast<int>(par.kvp)), chunk_(static_cast<int>(par.chunk_size)),
+      distributed_(par.distributed != 0), rank_(par.rank), B_(static_cast<int>(rt.batch)),
+      cap_(rt.capacity_tokens), device_(rt.device), hopb_(rt.hopb != 0), graphs_(rt.use_graphs != 0) {
+  validate_reference_dims();
+  if (H_ != Qh_ * D_) throw std::invalid_argument("hidden_dim must equal query_heads * head_size");
+  if (L_ < 1) throw std::invalid_argument("layers must be >= 1");
+  if (B_ < 1 || B_ > 16) throw std::invalid_argument("batch must be in [1, 16] for the B200 decode kernels");
+  if (cap_ < 1) throw std::invalid_argument("capacity_tokens must be >= 1");
+  if (D_ > 128) throw std::invalid_argument("head_size > 128 is not supported by the GQA decode kernel");
+  if (H_ % 16) throw std::invalid_argument("hidden width must be a multiple of 16");
+  if (!attn_only_) {
+    if (F_ < 16 || F_ % 16) throw std::invalid_argument("ffn_dim must be a positive multiple of 16");
+    if (V_ < 1) throw std::invalid_argument("vocab must be >= 1");
+  }
+  if (distributed_) throw StateError("distributed mode: use the NCCL build (not enabled in this engine)");
+
+  DP_ = D_ <= 32 ? 32 : (D_ <= 64 ? 64 : 128);
+  G_ = static_cast<int>(Qh_ / Kh_);
+  q_chunks_ = (G_ + 7) / 8;
+  kvh_per_slot_ = static_cast<int>(Kh_ / tpa_);
+  q_per_slot_ = static_cast<int>(Qh_ / tpa_);
+  n_slots_ = tpa_ * kvp_;
+  slot_base_ = 0;
+  const int64_t per_rank_max = ((cap_ + static_cast<int64_t>(chunk_) * kvp_ - 1) /
+                                (static_cast<int64_t>(chunk_) * kvp_)) * chunk_;
+  page_cap_ = static_cast<int>((per_rank_max + 15) / 16 + 1);
+  page_bytes_ = 64u * static_cast<size_t>(DP_);
+
+  cuda_check(cudaSetDevice(device_), "cudaSetDevice");
+  cudaDeviceProp prop{};
+  cuda_check(cudaGetDeviceProperties(&prop, device_), "cudaGetDeviceProperties");
+  if (prop.major < 10)
+    throw CudaError("device is not sm_100 class (Blackwell); this build targets sm_100a only");
+  num_sms_ = prop.multiProcessorCount;
+  cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  alloc();
+  plan_gemvs();
+}
+
+Engine::~Engine() {
+  drop_graphs();
+  auto f = [](void* p) {
+    if (p) cudaFree(p);
+  };
+  for (auto* p : kv_) f(p);
+  for (auto* p : w_qkv_) f(p);
+  for (auto* p : w_o_) f(p);
+  for (auto* p : w_gu_) f(p);
+  for (auto* p : w_down_) f(p);
+  f(w_lm_); f(emb_); f(d_total_); f(d_q_); f(d_part_o_); f(d_part_lse_); f(d_work_);
+  f(d_frag_o_); f(d_frag_lse_); f(d_ypart_); f(d_counters_); f(d_x_); f(d_ss_); f(d_m_);
+  f(d_logits_); f(d_best_); f(d_tokens_); f(d_next_); f(d_out_); f(d_out_lse_); f(d_hidden_);
+  f(d_segs_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::validate_reference_dims() const {
+  // Same checks, same order, same messages as the reference:
+  // ShardedKVCache ctor (attention.hpp:239-240) then DecodeHarness ctor (:431-437).
+  if (kvp_ < 1 || Kh_ < 1 || D_ < 1 || chunk_ < 1)
+    throw std::invalid_argument("cache dimensions must be >= 1");
+  if (tpa_ < 1 || kvp_ < 1) throw std::invalid_argument("tpa and kvp must be >= 1");
+  if (Qh_ % Kh_ != 0) throw std::invalid_argument("query_heads must be a multiple of kv_heads");
+  if (Kh_ % tpa_ != 0) throw std::invalid_argument("tpa must divide kv_heads");
+  if ((Qh_ * D_) % (static_cast<int64_t>(tpa_) * kvp_) != 0)
+    throw std::invalid_argument("tpa*kvp must divide the hidden width");
+}
+
+void Engine::alloc() {
+  const size_t pool = static_cast<size_t>(n_slots_) * B_ * kvh_per_slot_ * page_cap_ * page_bytes_;
+  for (int64_t l = 0; l < L_; ++l) kv_.push_back(dalloc<uint8_t>(pool, "kv pool"));
+  d_total_ = dalloc<int>(static_cast<size_t>(L_) * B_, "totals");
+  h_total_.assign(static_cast<size_t>(L_ * B_), 0);
+  d_q_ = dalloc<float>(static_cast<size_t>(B_) * Qh_ * DP_, "q");
+
+  // attention work decomposition
+  n_streams_ = n_slots_ * B_ * kvh_per_slot_ * q_chunks_;
+  const int pages_max = page_cap_;
+  const int target_items = num_sms_ * 8;
+  splits_ = std::max(1, std::min((target_items + n_streams_ - 1) / n_streams_, std::max(1, pages_max / 8)));
+  n_items_ = n_streams_ * splits_;
+  attn_grid_ = std::min(num_sms_, n_items_);
+  d_part_o_ = dalloc<float>(static_cast<size_t>(n_items_) * 8 * DP_, "part_o");
+  d_part_lse_ = dalloc<float>(static_cast<size_t>(n_items_) * 8, "part_lse");
+  d_work_ = dalloc<int>(4, "work counters");
+  d_frag_o_ = dalloc<float>(static_cast<size_t>(n_slots_) * B_ * q_per_slot_ * DP_, "frag_o");
+  d_frag_lse_ = dalloc<float>(static_cast<size_t>(n_slots_) * B_ * q_per_slot_, "frag_lse");
+  d_x_ = dalloc<float>(static_cast<size_t>(B_) * H_, "x");
+  d_out_ = dalloc<float>(static_cast<size_t>(B_) * Qh_ * D_, "out");
+  d_out_lse_ = dalloc<float>(static_cast<size_t>(B_) * Qh_, "out_lse");
+  d_tokens_ = dalloc<int>(B_, "tokens");
+  d_next_ = dalloc<int>(B_, "next");
+  d_best_ = dalloc<unsigned long long>(B_, "best");
+  d_segs_ = dalloc<WSeg>(16, "segs");
+}
+
+// ---------------------------------------------------------------------------
+void Engine::plan_gemvs() {
+  auto make = [&](int N, int Npad, int K, int xm, int em) {
+    GemvPlan g;
+    GemvParams& p = g.p;
+    p.N = N;
+    p.Npad = Npad;
+    p.K = K;
+    p.batch = B_;
+    const int kst = K / 16;
+    const int nblk = Npad / 128;
+    int ksplit = std::max(1, (2 * num_sms_ + nblk - 1) / nblk);
+    ksplit = std::min(ksplit, std::max(1, kst / 4));
+    int kr = (kst + ksplit - 1) / ksplit;
+    kr = std::min(kr, 128);
+    ksplit = (kst + kr - 1) / kr;
+    p.ksplit = ksplit;
+    p.kr_steps = kr;
+    p.eps = 1e-5f;
+    p.kvp = kvp_;
+    p.q_per_slot = q_per_slot_;
+    p.head_dim = static_cast<int>(D_);
+    p.dp = DP_;
+    g.xmode = xm;
+    g.emode = em;
+    ypart_elems_ = std::max(ypart_elems_, static_cast<size_t>(ksplit) * B_ * Npad);
+    max_counters_ = std::max(max_counters_, nblk);
+    return g;
+  };
+  const int nq = static_cast<int>(Qh_ * D_), nk = static_cast<int>(Kh_ * D_);
+  const int Nqkv = nq + 2 * nk;
+  const int Hh = static_cast<int>(H_);
+  for (int64_t l = 0; l < L_; ++l) {
+    GemvPlan q = make(Nqkv, round_up(Nqkv, 128), Hh, attn_only_ ? X_PLAIN : X_NORM, E_QKV);
+    q.p.nq = nq;
+    q.p.nk = nk;
+    q.p.kv_heads = static_cast<int>(Kh_);
+    q.p.kvh_per_slot = kvh_per_slot_;
+    q.p.chunk = chunk_;
+    q.p.page_cap = page_cap_;
+    q.p.slot_base = slot_base_;
+    q.p.n_local_slots = n_slots_;
+    q.p.append = 1;
+    plan_qkv_.push_back(q);
+    if (!attn_only_) {
+      plan_o_.push_back(make(Hh, round_up(Hh, 128), Hh, X_MERGE, E_RESID));
+      const int F = static_cast<int>(F_);
+      plan_gu_.push_back(make(2 * F, round_up(F, 64) * 2, Hh, X_NORM, E_SWIGLU));
+      plan_down_.push_back(make(Hh, round_up(Hh, 128), F, X_PLAIN, E_RESID));
+    }
+  }
+  if (!attn_only_) plan_lm_ = make(static_cast<int>(V_), round_up(V_, 128), Hh, X_NORM, E_LOGITS);
+
+  d_ypart_ = dalloc<float>(ypart_elems_, "ypart");
+  d_counters_ = dalloc<int>(static_cast<size_t>(max_counters_), "counters");
+  const int hblk = round_up(Hh, 128) / 128;
+  d_ss_ = dalloc<float>(static_cast<size_t>(std::max(hblk, 1)) * B_, "ss");
+  if (!attn_only_) {
+    d_m_ = dalloc<float>(static_cast<size_t>(B_) * F_, "m");
+    d_logits_ = dalloc<float>(static_cast<size_t>(B_) * V_, "logits");
+    d_hidden_ = dalloc<float>(static_cast<size_t>(L_ + 1) * B_ * H_, "hidden");
+  }
+  kernels_per_step_ = attn_only_ ? 5 : 1 + 7 * L_ + 2;
+}
+
+// ---------------------------------------------------------------------------
+void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
+  const int Hh = static_cast<int>(H_);
+  const int nq = static_cast<int>(Qh_ * D_), nk = static_cast<int>(Kh_ * D_);
+  auto walloc = [&](const GemvPlan& g) {
+    return dalloc<uint4>(static_cast<size_t>(g.p.Npad) * g.p.K / 8, "weights");
+  };
+  auto init = [&](uint4* w, const GemvPlan& g, const std::vector<WSeg>& segs) {
+    cuda_check(cudaMemcpyAsync(d_segs_, segs.data(), segs.size() * sizeof(WSeg), cudaMemcpyHostToDevice,
+                               stream_), "segs");
+    cuda_check(launch_weight_init_hash(w, g.p.Npad, g.p.K, d_segs_, static_cast<int>(segs.size()), seed,
+                                       stream_), "weight init");
+    cuda_check(cudaStreamSynchronize(stream_), "weight init sync");
+  };
+  const double sh = 1.0 / std::sqrt(static_cast<double>(H_));
+  for (int64_t l = 0; l < L_; ++l) {
+    if (w_qkv_.size() <= static_cast<size_t>(l)) w_qkv_.push_back(walloc(plan_qkv_[l]));
+    if (qkv_hash) {
+      std::vector<WSeg> segs = {
+          {hash_stream(kWq, l), 0, nq, nq, 0, 0, 1.0},
+          {hash_stream(kWk, l), nq, nq + nk, nk, 0, 0, 1.0},
+          {hash_stream(kWv, l), nq + nk, nq + 2 * nk, nk, 0, 0, 1.0},
+      };
+      init(w_qkv_[l], plan_qkv_[l], segs);
+    }
+    plan_qkv_[l].p.w = w_qkv_[l];
+    if (!attn_only_) {
+      const int F = static_cast<int>(F_);
+      if (w_o_.size() <= static_cast<size_t>(l)) {
+        w_o_.push_back(walloc(plan_o_[l]));
+        w_gu_.push_back(walloc(plan_gu_[l]));
+        w_down_.push_back(walloc(plan_down_[l]));
+      }
+      init(w_o_[l], plan_o_[l], {{hash_stream(kWo, l), 0, Hh, Hh, 0, 0, sh}});
+      init(w_gu_[l], plan_gu_[l],
+           {{hash_stream(kWgate, l), 0, plan_gu_[l].p.Npad, F, 0, 1, sh},
+            {hash_stream(kWup, l), 0, plan_gu_[l].p.Npad, F, 0, 2, sh}});
+      init(w_down_[l], plan_down_[l],
+           {{hash_stream(kWdown, l), 0, Hh, Hh, 0, 0, 1.0 / std::sqrt(static_cast<double>(F_))}});
+      plan_o_[l].p.w = w_o_[l];
+      plan_gu_[l].p.w = w_gu_[l];
+      plan_down_[l].p.w = w_down_[l];
+    }
+  }
+  if (!attn_only_) {
+    if (!w_lm_) w_lm_ = walloc(plan_lm_);
+    init(w_lm_, plan_lm_, {{hash_stream(kLm, 0), 0, static_cast<int>(V_), static_cast<int>(V_), 0, 0, sh}});
+    plan_lm_.p.w = w_lm_;
+    if (!emb_) emb_ = dalloc<uint16_t>(static_cast<size_t>(V_) * H_, "embedding");
+    cuda_check(launch_emb_init_hash(emb_, static_cast<int>(V_), Hh, seed, hash_stream(kEmb, 0), stream_),
+               "emb init");
+    cuda_check(cudaStreamSynchronize(stream_), "emb init sync");
+  }
+  // wire the remaining pointers of every plan
+  for (int64_t l = 0; l < L_; ++l) {
+    GemvParams& q = plan_qkv_[l].p;
+    q.ypart = d_ypart_;
+    q.counters = d_counters_;
+    q.q_out = d_q_;
+    q.kv = kv_[l];
+    q.total = d_total_ + l * B_;
+    q.x = d_x_;
+    q.x_stride = static_cast<int>(H_);
+    q.ss_part = d_ss_;
+    q.n_ss = 1;  // set per use
+    if (!attn_only_) {
+      GemvParams& o = plan_o_[l].p;
+      o.ypart = d_ypart_;
+      o.counters = d_counters_;
+      o.frag_o = d_frag_o_;
+      o.frag_lse = d_frag_lse_;
+      o.out = d_x_;
+      o.out_stride = static_cast<int>(H_);
+      o.ss_out = d_ss_;
+      GemvParams& gu = plan_gu_[l].p;
+      gu.ypart = d_ypart_;
+      gu.counters = d_counters_;
+      gu.x = d_x_;
+      gu.x_stride = static_cast<int>(H_);
+      gu.ss_part = d_ss_;
+      gu.n_ss = plan_o_[l].p.Npad / 128;
+      gu.out = d_m_;
+      gu.out_stride = static_cast<int>(F_);
+      GemvParams& dn = plan_down_[l].p;
+      dn.ypart = d_ypart_;
+      dn.counters = d_counters_;
+      dn.x = d_m_;
+      dn.x_stride = static_cast<int>(F_);
+      dn.out = d_x_;
+      dn.out_stride = static_cast<int>(H_);
+      dn.ss_out = d_ss_;
+      q.n_ss = l == 0 ? 1 : plan_down_[l - 1].p.Npad / 128;
+    }
+  }
+  if (!attn_only_) {
+    GemvParams& lm = plan_lm_.p;
+    lm.ypart = d_ypart_;
+    lm.counters = d_counters_;
+    lm.x = d_x_;
+    lm.x_stride = static_cast<int>(H_);
+    lm.ss_part = d_ss_;
+    lm.n_ss = plan_down_[L_ - 1].p.Npad / 128;
+    lm.best = d_best_;
+    lm.out = nullptr;
+    lm.out_stride = static_cast<int>(V_);
+  }
+  weights_ready_ = true;
+  drop_graphs();
+}
+
+void Engine::drop_graphs() {
+  for (auto& g : graphs_cache_) cudaGraphExecDestroy(g.exec);
+  graphs_cache_.clear();
+}
+
+void Engine::mark(int kind) {
+  if (!prof_) return;
+  cudaEvent_t ev;
+  cuda_check(cudaEventCreate(&ev), "event");
+  cuda_check(cudaEventRecord(ev, stream_), "event record");
+  prof_->push_back({kind, ev});
+}
+
+void Engine::init_weights_hash(uint64_t seed) { build_weights_common(seed, true); }
+
+void Engine::init_weights_mt19937(uint64_t seed) {
+  build_weights_common(seed, false);
+  const int64_t nq = Qh_ * D_, nk = Kh_ * D_;
+  for (int64_t l = 0; l < L_; ++l) {
+    // DecodeHarness ctor draw order: W_q, W_k, W_v (attention.hpp:438-442)
+    std::mt19937_64 rng(seed + static_cast<uint64_t>(l));
+    std::vector<double> wq(static_cast<size_t>(H_ * nq)), wk(static_cast<size_t>(H_ * nk)),
+        wv(static_cast<size_t>(H_ * nk));
+    for (double& v : wq) v = unit_draw(rng);
+    for (double& v : wk) v = unit_draw(rng);
+    for (double& v : wv) v = unit_draw(rng);
+    upload_qkv_host(l, wq, wk, wv);
+  }
+}
+
+void Engine::upload_qkv_host(int64_t layer, const std::vector<double>& wq, const std::vector<double>& wk,
+                             const std::vector<double>& wv) {
+  const GemvPlan& g = plan_qkv_[layer];
+  const int K = g.p.K, kst = K / 16;
+  const int nq = static_cast<int>(Qh_ * D_), nk = static_cast<int>(Kh_ * D_);
+  std::vector<uint16_t> img(static_cast<size_t>(g.p.Npad) * K, 0);
+  for (int k = 0; k < K; ++k) {
+    for (int n = 0; n < nq; ++n)
+      img[wfrag_offset_host(n, k, kst) / 2] = bf16_bits_from_double(wq[static_cast<size_t>(k) * nq + n]);
+    for (int n = 0; n < nk; ++n) {
+      img[wfrag_offset_host(nq + n, k, kst) / 2] = bf16_bits_from_double(wk[static_cast<size_t>(k) * nk + n]);
+      img[wfrag_offset_host(nq + nk + n, k, kst) / 2] =
+          bf16_bits_from_double(wv[static_cast<size_t>(k) * nk + n]);
+    }
+  }
+  cuda_check(cudaMemcpy(w_qkv_[layer], img.data(), img.size() * 2, cudaMemcpyHostToDevice), "qkv upload");
+}
+
+// ---------------------------------------------------------------------------
+void Engine::check_layer(int64_t layer) const {
+  if (layer < 0 || layer >= L_) throw std::invalid_argument("layer out of range");
+}
+
+void Engine::grow_random(int64_t layer, int64_t request, int64_t n, std::mt19937_64& rng) {
+  check_layer(layer);
+  if (request < 0 || request >= B_) throw std::invalid_argument("request out of range");
+  const int64_t per = Kh_ * D_;
+  const int64_t block = 4096;
+  std::vector<float> k, v;
+  for (int64_t done = 0; done < n; done += block) {
+    const int64_t m = std::min(block, n - done);
+    k.resize(static_cast<size_t>(m * per));
+    v.resize(static_cast<size_t>(m * per));
+    for (int64_t i = 0; i < m; ++i) {
+      // attention.hpp:454-455 under g++: V drawn before K (right-to-left args)
+      std::vector<double> vv(static_cast<size_t>(per)), kk(static_cast<size_t>(per));
+      for (double& x : vv) x = unit_draw(rng);
+      for (double& x : kk) x = unit_draw(rng);
+      for (int64_t j = 0; j < per; ++j) {
+        // exact: route the double through its bf16 value (stored format)
+        v[static_cast<size_t>(i * per + j)] = float_from_bf16_bits(bf16_bits_from_double(vv[static_cast<size_t>(j)]));
+        k[static_cast<size_t>(i * per + j)] = float_from_bf16_bits(bf16_bits_from_double(kk[static_cast<size_t>(j)]));
+      }
+    }
+    append_kv(layer, request, m, k.data(), v.data());
+  }
+}
+
+void Engine::append_kv(int64_t layer, int64_t request, int64_t n, const float* k, const float* v) {
+  check_layer(layer);
+  if (request < 0 || request >= B_) throw std::invalid_argument("request out of range");
+  if (n < 0) throw std::invalid_argument("token count must be >= 0");
+  if (h_total_[static_cast<size_t>(layer * B_ + request)] + n > cap_)
+    throw std::invalid_argument("KV capacity exceeded");
+  if (n == 0) return;
+  const size_t cnt = static_cast<size_t>(n * Kh_ * D_);
+  std::vector<uint16_t> kb(cnt), vb(cnt);
+  for (size_t i = 0; i < cnt; ++i) {
+    kb[i] = bf16_bits_from_float(k[i]);
+    vb[i] = bf16_bits_from_float(v[i]);
+  }
+  uint16_t *dk = nullptr, *dv = nullptr;
+  cuda_check(cudaMalloc(&dk, cnt * 2), "append staging");
+  cuda_check(cudaMalloc(&dv, cnt * 2), "append staging");
+  cuda_check(cudaMemcpyAsync(dk, kb.data(), cnt * 2, cudaMemcpyHostToDevice, stream_), "append h2d");
+  cuda_check(cudaMemcpyAsync(dv, vb.data(), cnt * 2, cudaMemcpyHostToDevice, stream_), "append h2d");
+  cuda_check(launch_kv_append_rows(kv_[layer], dk, dv, static_cast<int>(n), static_cast<int>(request),
+                                   d_total_ + layer * B_, B_, static_cast<int>(Kh_), kvh_per_slot_, kvp_,
+                                   chunk_, static_cast<int>(D_), DP_, page_cap_, slot_base_, n_slots_,
+                                   stream_),
+             "append kernel");
+  cuda_check(cudaStreamSynchronize(stream_), "append sync");
+  cudaFree(dk);
+  cudaFree(dv);
+  h_total_[static_cast<size_t>(layer * B_ + request)] += n;
+}
+
+void Engine::fill_kv_hash(int64_t n, uint64_t seed) {
+  for (int64_t l = 0; l < L_; ++l)
+    for (int b = 0; b < B_; ++b)
+      if (h_total_[static_cast<size_t>(l * B_ + b)] + n > cap_) throw std::invalid_argument("KV capacity exceeded");
+  for (int64_t l = 0; l < L_; ++l) {
+    cuda_check(launch_kv_fill_hash(kv_[l], d_total_ + l * B_, B_, static_cast<int>(Kh_), kvh_per_slot_, kvp_,
+                                   chunk_, static_cast<int>(D_), DP_, page_cap_, slot_base_, n_slots_, n, seed,
+                                   hash_stream(kCacheK, l), hash_stream(kCacheV, l), stream_),
+               "kv fill");
+    for (int b = 0; b < B_; ++b) h_total_[static_cast<size_t>(l * B_ + b)] += n;
+  }
+  cuda_check(cudaStreamSynchronize(stream_), "kv fill sync");
+}
+
+int64_t Engine::total_tokens(int64_t layer, int64_t request) const {
+  check_layer(layer);
+  if (request < 0 || request >= B_) throw std::invalid_argument("request out of range");
+  return h_total_[static_cast<size_t>(layer * B_ + request)];
+}
+
+int64_t Engine::effective_tokens(int64_t layer, int64_t request, int64_t rank) const {
+  if (rank < 0 || rank >= kvp_) throw std::invalid_argument("rank out of range");
+  return rr_count(total_tokens(layer, request), static_cast<int>(rank), chunk_, kvp_);
+}
+
+int64_t Engine::max_min_gap(int64_t layer, int64_t request) const {
+  int64_t lo = INT64_MAX, hi = 0;
+  for (int r = 0; r < kvp_; ++r) {
+    const int64_t c = effective_tokens(layer, request, r);
+    lo = std::min(lo, c);
+    hi = std::max(hi, c);
+  }
+  return hi - lo;
+}
+
+int Engine::slot_local_of(int rank, int group) const { return group * kvp_ + rank - slot_base_; }
+
+void Engine::read_kv(int64_t layer, int64_t request, int64_t rank, int64_t head, float* k, float* v) {
+  check_layer(layer);
+  if (head < 0 || head >= Kh_) throw std::invalid_argument("kv head out of range");
+  const int64_t n = effective_tokens(layer, request, rank);
+  const int grp = static_cast<int>(head / kvh_per_slot_), kvh = static_cast<int>(head % kvh_per_slot_);
+  const int sl = slot_local_of(static_cast<int>(rank), grp);
+  if (sl < 0 || sl >= n_slots_) throw std::invalid_argument("rank not resident on this device");
+  const int pages = static_cast<int>((n + 15) / 16);
+  std::vector<uint8_t> buf(static_cast<size_t>(pages) * page_bytes_);
+  const size_t base = ((static_cast<size_t>(sl) * B_ + request) * kvh_per_slot_ + kvh) * page_cap_ * page_bytes_;
+  cuda_check(cudaStreamSynchronize(stream_), "read_kv sync");
+  if (pages)
+    cuda_check(cudaMemcpy(buf.data(), kv_[layer] + base, buf.size(), cudaMemcpyDeviceToHost), "read_kv");
+  for (int64_t t = 0; t < n; ++t) {
+    const uint8_t* page = buf.data() + static_cast<size_t>(t / 16) * page_bytes_;
+    for (int d = 0; d < D_; ++d) {
+      uint16_t kb, vb;
+      std::memcpy(&kb, page + k_offset(DP_, static_cast<int>(t % 16), d), 2);
+      std::memcpy(&vb, page + v_offset(DP_, static_cast<int>(t % 16), d), 2);
+      k[t * D_ + d] = float_from_bf16_bits(kb);
+      v[t * D_ + d] = float_from_bf16_bits(vb);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+void Engine::require_context(int64_t layer) const {
+  for (int b = 0; b < B_; ++b)
+    if (h_total_[static_cast<size_t>(layer * B_ + b)] == 0)
+      throw std::invalid_argument("decode needs a nonempty context");
+  for (int b = 0; b < B_; ++b)
+    if (h_total_[static_cast<size_t>(layer * B_ + b)] + 1 > cap_) throw std::invalid_argument("KV capacity exceeded");
+}
+
+void Engine::record_transcript(int64_t layers) {
+  // attention.hpp:466-468 (broadcast) and :492-502 (all-to-all), per request.
+  const int64_t pool = static_cast<int64_t>(tpa_) * kvp_;
+  const int64_t group_width = static_cast<int64_t>(q_per_slot_) * D_;
+  const int64_t slice = group_width / kvp_;
+  for (int64_t l = 0; l < layers; ++l)
+    for (int b = 0; b < B_; ++b) {
+      for (int64_t r = 1; r < pool; ++r) transcript_.push_back({0, 0, r, H_, 0});
+      for (int g = 0; g < tpa_; ++g)
+        for (int r = 0; r < kvp_; ++r)
+          for (int p = 0; p < kvp_; ++p) {
+            if (p == r) continue;
+            const int64_t first = p * slice / D_, last = ((p + 1) * slice - 1) / D_;
+            transcript_.push_back({1, static_cast<int64_t>(g) * kvp_ + r, static_cast<int64_t>(g) * kvp_ + p,
+                                   slice, last - first + 1});
+          }
+    }
+}
+
+void Engine::enqueue_attention(int64_t layer, int qkv_xmode, const float* x, int x_stride) {
+  // 1. QKV projection with fused round-robin append of this token's K/V
+  GemvPlan q = plan_qkv_[layer];
+  q.p.x = x;
+  q.p.x_stride = x_stride;
+  cuda_check(launch_gemv(q.p, qkv_xmode, E_QKV, stream_), "qkv gemv");
+  mark(1);
+  // 2. flash-decode partials over every local rank's shard (attend BEFORE append)
+  AttnParams a{};
+  a.kv = kv_[layer];
+  a.q = d_q_;
+  a.total = d_total_ + layer * B_;
+  a.part_o = d_part_o_;
+  a.part_lse2 = d_part_lse_;
+  a.work_counter = d_work_;
+  a.done_counter = d_work_ + 1;
+  a.dp = DP_;
+  a.batch = B_;
+  a.q_heads = static_cast<int>(Qh_);
+  a.group = G_;
+  a.q_chunks = q_chunks_;
+  a.kvh_per_slot = kvh_per_slot_;
+  a.q_per_slot = q_per_slot_;
+  a.kvp = kvp_;
+  a.chunk = chunk_;
+  a.page_cap = page_cap_;
+  a.slot_base = slot_base_;
+  a.n_local_slots = n_slots_;
+  a.n_streams = n_streams_;
+  a.splits = splits_;
+  a.n_items = n_items_;
+  a.qscale = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D_)));
+  cuda_check(launch_attn_decode(a, attn_grid_, stream_), "attention");
+  mark(2);
+  // 3. per-rank fragments (split merge), then bump the totals (append is now visible)
+  cuda_check(launch_attn_split_reduce(a, d_frag_o_, d_frag_lse_, stream_), "split reduce");
+  cuda_check(launch_bump_totals(d_total_ + layer * B_, B_, stream_), "bump totals");
+  mark(3);
+}
+
+void Engine::harness_step(int64_t layer, const float* x_host, int64_t x_len, float* out, float* lse) {
+  check_layer(layer);
+  if (x_len != static_cast<int64_t>(B_) * H_) throw std::invalid_argument("hidden state has wrong width");
+  if (!weights_ready_) throw StateError("weights are not initialised");
+  require_context(layer);
+  cuda_check(cudaMemcpyAsync(d_x_, x_host, static_cast<size_t>(x_len) * 4, cudaMemcpyHostToDevice, stream_),
+             "x h2d");
+  harness_step_device(layer, d_x_, d_out_);
+  if (lse)
+    cuda_check(cudaMemcpyAsync(lse, d_out_lse_, static_cast<size_t>(B_) * Qh_ * 4, cudaMemcpyDeviceToHost, stream_),
+               "lse d2h");
+  cuda_check(cudaMemcpyAsync(out, d_out_, static_cast<size_t>(B_) * Qh_ * D_ * 4, cudaMemcpyDeviceToHost, stream_),
+             "out d2h");
+  cuda_check(cudaStreamSynchronize(stream_), "harness sync");
+}
+
+void Engine::harness_step_device(int64_t layer, const float* x_dev, float* out_dev) {
+  check_layer(layer);
+  if (!weights_ready_) throw StateError("weights are not initialised");
+  require_context(layer);
+  enqueue_attention(layer, X_PLAIN, x_dev, static_cast<int>(H_));
+  cuda_check(launch_merge_out(d_frag_o_, d_frag_lse_, B_, static_cast<int>(Qh_), q_per_slot_, kvp_,
+                              static_cast<int>(D_), DP_, out_dev, d_out_lse_, stream_),
+             "merge");
+  mark(8);
+  for (int b = 0; b < B_; ++b) h_total_[static_cast<size_t>(layer * B_ + b)] += 1;
+  record_transcript(1);
+}
+
+void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
+  cuda_check(launch_embed(emb_, tokens_dev, B_, static_cast<int>(H_), d_x_, d_ss_, stream_), "embed");
+  mark(0);
+  if (capture_hidden_)
+    cuda_check(cudaMemcpyAsync(d_hidden_, d_x_, static_cast<size_t>(B_) * H_ * 4, cudaMemcpyDeviceToDevice, stream_),
+               "hidden");
+  for (int64_t l = 0; l < L_; ++l) {
+    enqueue_attention(l, X_NORM, d_x_, static_cast<int>(H_));
+    cuda_check(launch_gemv(plan_o_[l].p, X_MERGE, E_RESID, stream_), "o-proj");
+    mark(4);
+    cuda_check(launch_gemv(plan_gu_[l].p, X_NORM, E_SWIGLU, stream_), "gate/up");
+    mark(5);
+    cuda_check(launch_gemv(plan_down_[l].p, X_PLAIN, E_RESID, stream_), "down");
+    mark(6);
+    if (capture_hidden_)
+      cuda_check(cudaMemcpyAsync(d_hidden_ + (l + 1) * B_ * H_, d_x_, static_cast<size_t>(B_) * H_ * 4,
+                                 cudaMemcpyDeviceToDevice, stream_),
+                 "hidden");
+  }
+  GemvParams lm = plan_lm_.p;
+  lm.out = store_logits_ ? d_logits_ : nullptr;
+  cuda_check(launch_gemv(lm, X_NORM, E_LOGITS, stream_), "lm head");
+  cuda_check(launch_argmax_finish(d_best_, B_, next_dev, d_best_, stream_), "argmax");
+  mark(7);
+}
+
+void Engine::decode_step_device(const int32_t* tokens_dev, int32_t* next_dev) {
+  if (attn_only_) throw StateError("decode_step needs a full model (attention_only = 0)");
+  if (!weights_ready_) throw StateError("weights are not initialised");
+  for (int64_t l = 0; l < L_; ++l) require_context(l);
+  if (graphs_ && !prof_) {
+    cudaGraphExec_t exec = nullptr;
+    for (auto& g : graphs_cache_)
+      if (g.tokens == tokens_dev && g.next == next_dev && g.hidden == capture_hidden_ && g.logits == store_logits_)
+        exec = g.exec;
+    if (!exec) {
+      cudaGraph_t g;
+      cuda_check(cudaStreamBeginCapture(stream_, cudaStreamCaptureModeThreadLocal), "capture begin");
+      enqueue_decode(tokens_dev, next_dev);
+      cuda_check(cudaStreamEndCapture(stream_, &g), "capture end");
+      cuda_check(cudaGraphInstantiate(&exec, g, 0), "graph instantiate");
+      cudaGraphDestroy(g);
+      graphs_cache_.push_back({tokens_dev, next_dev, capture_hidden_, store_logits_, exec});
+    }
+    cuda_check(cudaGraphLaunch(exec, stream_), "graph launch");
+  } else {
+    enqueue_decode(tokens_dev, next_dev);
+  }
+  for (int64_t l = 0; l < L_; ++l)
+    for (int b = 0; b < B_; ++b) h_total_[static_cast<size_t>(l * B_ + b)] += 1;
+  record_transcript(L_);
+}
+
+void Engine::decode_step(const int32_t* tokens, int32_t* next, float* logits, float* hidden) {
+  if (attn_only_) throw StateError("decode_step needs a full model (attention_only = 0)");
+  for (int b = 0; b < B_; ++b)
+    if (tokens[b] < 0 || tokens[b] >= V_) throw std::invalid_argument("token id out of range");
+  capture_hidden_ = hidden != nullptr;
+  store_logits_ = logits != nullptr;
+  cuda_check(cudaMemcpyAsync(d_tokens_, tokens, static_cast<size_t>(B_) * 4, cudaMemcpyHostToDevice, stream_),
+             "tokens h2d");
+  decode_step_device(d_tokens_, d_next_);
+  cuda_check(cudaMemcpyAsync(next, d_next_, static_cast<size_t>(B_) * 4, cudaMemcpyDeviceToHost, stream_),
+             "next d2h");
+  if (logits)
+    cuda_check(cudaMemcpyAsync(logits, d_logits_, static_cast<size_t>(B_) * V_ * 4, cudaMemcpyDeviceToHost, stream_),
+               "logits d2h");
+  if (hidden)
+    cuda_check(cudaMemcpyAsync(hidden, d_hidden_, static_cast<size_t>(L_ + 1) * B_ * H_ * 4,
+                               cudaMemcpyDeviceToHost, stream_),
+               "hidden d2h");
+  cuda_check(cudaStreamSynchronize(stream_), "decode sync");
+}
+
+void Engine::synchronize() { cuda_check(cudaStreamSynchronize(stream_), "synchronize"); }
+
+void Engine::profile_step(int64_t reps, double* ms) {
+  if (!weights_ready_) throw StateError("weights are not initialised");
+  for (int k = 0; k < 9; ++k) ms[k] = 0.0;
+  std::vector<std::pair<int, cudaEvent_t>> evs;
+  for (int64_t r = 0; r < reps; ++r) {
+    evs.clear();
+    prof_ = &evs;
+    mark(-1);
+    try {
+      if (attn_only_) {
+        for (int64_t l = 0; l < L_; ++l) harness_step_device(l, d_x_, d_out_);
+      } else {
+        decode_step_device(d_tokens_, d_next_);
+      }
+    } catch (...) {
+      prof_ = nullptr;
+      throw;
+    }
+    prof_ = nullptr;
+    cuda_check(cudaStreamSynchronize(stream_), "profile sync");
+    for (size_t i = 1; i < evs.size(); ++i) {
+      float t = 0.f;
+      cuda_check(cudaEventElapsedTime(&t, evs[i - 1].second, evs[i].second), "elapsed");
+      if (evs[i].first >= 0 && evs[i].first < 9) ms[evs[i].first] += t / static_cast<double>(reps);
+    }
+    for (auto& e : evs) cudaEventDestroy(e.second);
+  }
+}
+
+void Engine::info(hx_engine_info* o) const {
+  std::memset(o, 0, sizeof(*o));
+  o->kv_bytes_per_layer = static_cast<int64_t>(n_slots_) * B_ * kvh_per_slot_ * page_cap_ * page_bytes_;
+  int64_t wb = static_cast<int64_t>(plan_qkv_[0].p.Npad) * plan_qkv_[0].p.K * 2;
+  if (!attn_only_)
+    wb += static_cast<int64_t>(plan_o_[0].p.Npad) * plan_o_[0].p.K * 2 +
+          static_cast<int64_t>(plan_gu_[0].p.Npad) * plan_gu_[0].p.K * 2 +
+          static_cast<int64_t>(plan_down_[0].p.Npad) * plan_down_[0].p.K * 2;
+  o->weight_bytes_per_layer = wb;
+  o->head_bytes = attn_only_ ? 0 : static_cast<int64_t>(plan_lm_.p.Npad) * plan_lm_.p.K * 2 + V_ * H_ * 2;
+  o->attn_streams = n_streams_;
+  o->attn_splits = splits_;
+  o->attn_items = n_items_;
+  o->attn_grid = attn_grid_;
+  o->kernels_per_step = kernels_per_step_;
+  o->page_cap = page_cap_;
+  o->head_dim_padded = DP_;
+}
+
+}  // namespace hx

@@ -1,0 +1,154 @@
+// Host runtime of the B200 Helix decode step (C++, behind the C ABI).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <random>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/helix_b200.h"
+#include "kernels.h"
+
+namespace hx {
+
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct NcclError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct StateError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void cuda_check(cudaError_t e, const char* what);
+
+struct Message {
+  int64_t kind, src, dst, payload, lse;
+};
+
+struct GemvPlan {
+  GemvParams p{};
+  int xmode = 0, emode = 0;
+};
+
+class Comm;  // NCCL plumbing (distributed mode)
+
+class Engine {
+ public:
+  Engine(const hx_model_config& m, const hx_parallel_config& par, const hx_runtime_config& rt);
+  ~Engine();
+
+  void init_weights_mt19937(uint64_t seed);
+  void init_weights_hash(uint64_t seed);
+  void grow_random(int64_t layer, int64_t request, int64_t n, std::mt19937_64& rng);
+  void append_kv(int64_t layer, int64_t request, int64_t n, const float* k, const float* v);
+  void fill_kv_hash(int64_t n, uint64_t seed);
+  int64_t total_tokens(int64_t layer, int64_t request) const;
+  int64_t effective_tokens(int64_t layer, int64_t request, int64_t rank) const;
+  int64_t max_min_gap(int64_t layer, int64_t request) const;
+  void read_kv(int64_t layer, int64_t request, int64_t rank, int64_t head, float* k, float* v);
+
+  void harness_step(int64_t layer, const float* x_host, int64_t x_len, float* out, float* lse);
+  void harness_step_device(int64_t layer, const float* x_dev, float* out_dev);
+  void decode_step(const int32_t* tokens, int32_t* next, float* logits, float* hidden);
+  void decode_step_device(const int32_t* tokens_dev, int32_t* next_dev);
+  void synchronize();
+  // Eager decode (or harness) steps with CUDA events after every launch on the
+  // engine stream; ms[kind] += average milliseconds per step (see hx_profile_step).
+  void profile_step(int64_t reps, double* ms);
+  cudaStream_t stream() const { return stream_; }
+  void info(hx_engine_info* out) const;
+
+  const std::vector<Message>& transcript() const { return transcript_; }
+  void clear_transcript() { transcript_.clear(); }
+
+  std::string last_error;
+
+ private:
+  void validate_reference_dims() const;
+  void alloc();
+  void plan_gemvs();
+  void build_weights_common(uint64_t seed, bool qkv_hash);
+  void upload_qkv_host(int64_t layer, const std::vector<double>& wq, const std::vector<double>& wk,
+                       const std::vector<double>& wv);
+  void enqueue_attention(int64_t layer, int qkv_xmode, const float* x, int x_stride);
+  void enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev);
+  void record_transcript(int64_t layers);
+  void require_context(int64_t layer) const;
+  void check_layer(int64_t layer) const;
+  int slot_local_of(int rank, int group) const;
+
+  // ---- configuration
+  int64_t H_, Qh_, Kh_, D_, F_, L_, V_;
+  bool attn_only_;
+  int tpa_, kvp_, chunk_;
+  bool distributed_;
+  int rank_;
+  int B_;
+  int64_t cap_;
+  int device_;
+  bool hopb_, graphs_;
+  int DP_, G_, q_chunks_, kvh_per_slot_, q_per_slot_, n_slots_, slot_base_;
+  int page_cap_;
+  size_t page_bytes_;
+  int num_sms_;
+  // attention plan
+  int n_streams_, splits_, n_items_, attn_grid_;
+
+  // ---- device state
+  cudaStream_t stream_ = nullptr;
+  std::vector<uint8_t*> kv_;   // per layer page pool
+  int* d_total_ = nullptr;     // [L][B]
+  std::vector<int64_t> h_total_;
+  float* d_q_ = nullptr;
+  float* d_part_o_ = nullptr;
+  float* d_part_lse_ = nullptr;
+  int* d_work_ = nullptr;      // [2] work counter, done counter
+  float* d_frag_o_ = nullptr;
+  float* d_frag_lse_ = nullptr;
+  std::vector<uint4*> w_qkv_, w_o_, w_gu_, w_down_;
+  uint4* w_lm_ = nullptr;
+  uint16_t* emb_ = nullptr;
+  float* d_ypart_ = nullptr;
+  int* d_counters_ = nullptr;
+  float* d_x_ = nullptr;       // residual stream / harness x [B][H]
+  float* d_ss_ = nullptr;      // [max blocks][B]
+  float* d_m_ = nullptr;       // [B][F]
+  float* d_logits_ = nullptr;  // [B][V]
+  unsigned long long* d_best_ = nullptr;
+  int* d_tokens_ = nullptr;
+  int* d_next_ = nullptr;
+  float* d_out_ = nullptr;     // harness out [B][Q][Hsz]
+  float* d_out_lse_ = nullptr;
+  float* d_hidden_ = nullptr;  // [(L+1)][B][H]
+  WSeg* d_segs_ = nullptr;
+  bool weights_ready_ = false;
+  bool capture_hidden_ = false;
+  bool store_logits_ = false;
+
+  std::vector<GemvPlan> plan_qkv_, plan_o_, plan_gu_, plan_down_;
+  GemvPlan plan_lm_;
+  size_t ypart_elems_ = 0;
+  int max_counters_ = 0;
+  int64_t kernels_per_step_ = 0;
+
+  struct GraphEntry {
+    const int32_t* tokens;
+    int32_t* next;
+    bool hidden, logits;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs_cache_;
+  void drop_graphs();
+  void mark(int kind);
+  std::vector<std::pair<int, cudaEvent_t>>* prof_ = nullptr;
+
+  std::vector<Message> transcript_;
+  Comm* comm_ = nullptr;
+};
+
+}  // namespace hx

@@ -1,0 +1,105 @@
+// Kernel parameter blocks and launchers (internal to libhelix_b200.so).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include <stdint.h>
+
+namespace hx {
+
+// ---------------------------------------------------------------- attention
+struct AttnParams {
+  const uint8_t* kv;       // page pool for this layer: [slot_local][B][kvh_per_slot][page_cap] pages
+  const float* q;          // [B][q_heads][DP] fp32 (padded rows)
+  const int* total;        // [B] tokens appended to this layer's cache so far
+  float* part_o;           // [n_items][8][DP]
+  float* part_lse2;        // [n_items][8]  (log2 domain)
+  int* work_counter;       // persistent-kernel work queue (self-resetting)
+  int* done_counter;
+  int dp, batch, q_heads, group, q_chunks, kvh_per_slot, q_per_slot;
+  int kvp, chunk, page_cap, slot_base, n_local_slots;
+  int n_streams, splits, n_items;
+  float qscale;            // log2(e) / sqrt(head_size)
+};
+cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_attn_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse,
+                                     cudaStream_t stream);
+cudaError_t launch_bump_totals(int* total, int n, cudaStream_t stream);
+size_t attn_decode_smem_bytes(int dp);
+
+// ---------------------------------------------------------------- GEMV
+enum XMode : int { X_PLAIN = 0, X_NORM = 1, X_MERGE = 2 };
+enum EMode : int { E_STORE = 0, E_QKV = 1, E_RESID = 2, E_SWIGLU = 3, E_LOGITS = 4 };
+
+struct GemvParams {
+  const uint4* w;        // fragment-major bf16 weights [Npad/16][K/16][32 lanes][16 B]
+  int N, Npad, K;
+  int ksplit, kr_steps;  // k-steps (16 wide) per split
+  int batch;
+  // x source
+  const float* x;        // [B][x_stride] (X_PLAIN, X_NORM)
+  int x_stride;
+  const float* ss_part;  // [n_ss][B] partial sums of squares (X_NORM)
+  int n_ss;
+  float eps;
+  const float* frag_o;   // X_MERGE: [slot][B][q_per_slot][DP]
+  const float* frag_lse; // [slot][B][q_per_slot] (natural log)
+  int kvp, q_per_slot, head_dim, dp;
+  // split-K plumbing
+  float* ypart;          // [ksplit][B][Npad]
+  int* counters;         // [Npad/128], self-resetting
+  // epilogue
+  float* out;            // E_STORE / E_RESID (in-place residual) / E_SWIGLU / E_LOGITS (optional)
+  int out_stride;
+  float* ss_out;         // [Npad/128][B] partial sums of squares of the written rows (E_RESID, E_STORE)
+  // E_QKV
+  float* q_out;          // [B][q_heads][DP]
+  uint8_t* kv;           // page pool of this layer
+  const int* total;      // [B]
+  float* kv_dbg;         // optional [B][2][kv_heads][head_dim] fp32 copy of appended K/V
+  int nq, nk, kv_heads, kvh_per_slot, chunk, page_cap, slot_base, n_local_slots;
+  int append;            // write K/V into the cache
+  // E_LOGITS
+  unsigned long long* best;  // [B] packed (orderable logit, ~index)
+};
+cudaError_t launch_gemv(const GemvParams& p, int xmode, int emode, cudaStream_t stream);
+size_t gemv_smem_bytes(const GemvParams& p);
+
+// ---------------------------------------------------------------- misc
+cudaError_t launch_merge_out(const float* frag_o, const float* frag_lse, int batch, int q_heads,
+                             int q_per_slot, int kvp, int head_dim, int dp, float* out,
+                             float* out_lse, cudaStream_t stream);
+cudaError_t launch_embed(const uint16_t* emb, const int* tokens, int batch, int hidden,
+                         float* x, float* ss_part, cudaStream_t stream);
+cudaError_t launch_argmax_finish(const unsigned long long* best, int batch, int* tokens_out,
+                                 unsigned long long* best_reset, cudaStream_t stream);
+// Scatter n tokens (bf16 K/V rows [n][kv_heads][head_dim]) of request b at global
+// positions total[b] .. total[b]+n-1 into the round-robin page pool, then bump total.
+cudaError_t launch_kv_append_rows(uint8_t* kv, const uint16_t* k_rows, const uint16_t* v_rows,
+                                  int n, int b, int* total, int batch, int kv_heads,
+                                  int kvh_per_slot, int kvp, int chunk, int head_dim, int dp,
+                                  int page_cap, int slot_base, int n_local_slots,
+                                  cudaStream_t stream);
+// Device-side synthetic fill: tokens [t0, t0+n) of every request from the hash RNG.
+cudaError_t launch_kv_fill_hash(uint8_t* kv, int* total, int batch, int kv_heads,
+                                int kvh_per_slot, int kvp, int chunk, int head_dim, int dp,
+                                int page_cap, int slot_base, int n_local_slots, long long n,
+                                uint64_t seed, uint64_t stream_k, uint64_t stream_v,
+                                cudaStream_t stream);
+// Weight init from the hash RNG straight into the fragment-major layout.
+// Segment list maps combined rows to (hash stream, column count, column offset).
+struct WSeg {
+  uint64_t stream;
+  int rows_begin, rows_end;  // rows of the combined matrix covered
+  int cols_total;            // columns of the source (reference-orientation) matrix
+  int col_offset;            // source column of rows_begin
+  int interleave;            // 0: contiguous; 1: SwiGLU gate rows; 2: SwiGLU up rows
+  double scale;
+};
+cudaError_t launch_weight_init_hash(uint4* w, int Npad, int K, const WSeg* segs, int nseg,
+                                    uint64_t seed, cudaStream_t stream);
+cudaError_t launch_emb_init_hash(uint16_t* emb, int vocab, int hidden, uint64_t seed,
+                                 uint64_t stream_id, cudaStream_t stream);
+cudaError_t launch_fill_zero(void* p, size_t bytes, cudaStream_t stream);
+
+}  // namespace hx

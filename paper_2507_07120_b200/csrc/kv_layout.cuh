@@ -1,0 +1,62 @@
+// KV page layout in HBM (one page = 16 tokens of one KV head, K then V).
+//
+// Pages are stored "fragment-major": the byte image of a page is exactly the
+// register image the decode kernel's mma.sync B-operands need, so a consumer
+// warp reads its page with conflict-free 16-byte shared-memory loads (each
+// warp instruction touches 512 contiguous bytes) after one bulk TMA copy.
+//
+//   K region [0, 32*DP):   for nt in {0,1} (tokens 8nt..8nt+7), kp in [0, DP/32),
+//                          lane (g = lane/4, c = lane%4): 16 B =
+//                            ks = 2kp   : (K[8nt+g][16ks+2c], +1), (K[..][16ks+2c+8], +9)
+//                            ks = 2kp+1 : same two pairs
+//   V region [32*DP, 64*DP): for nd2 in [0, DP/16), lane: 16 B =
+//                            nd = 2nd2  : (V[2c][8nd+g], V[2c+1][8nd+g]), (V[2c+8][..], V[2c+9][..])
+//                            nd = 2nd2+1: same two pairs
+// bf16 pairs are packed low half = first element. DP is the head size padded
+// to a multiple of 32; padded dims hold zeros.
+#pragma once
+
+#include <stdint.h>
+
+namespace hx {
+
+__host__ __device__ __forceinline__ uint32_t page_bytes(int dp) { return 64u * static_cast<uint32_t>(dp); }
+
+// Byte offset of K[t][d] inside a page (t in [0,16), d in [0,DP)).
+__host__ __device__ __forceinline__ uint32_t k_offset(int dp, int t, int d) {
+  const int nt = t >> 3, g = t & 7;
+  const int ks = d >> 4, r = d & 15;
+  const int half = r >> 3, c = (r & 7) >> 1, elem = r & 1;
+  const int kp = ks >> 1, sub = ks & 1;
+  const int lane = g * 4 + c;
+  return static_cast<uint32_t>(((nt * (dp / 32) + kp) * 32 + lane) * 16 + (sub * 2 + half) * 4 + elem * 2);
+}
+
+// Byte offset of V[t][d] inside a page.
+__host__ __device__ __forceinline__ uint32_t v_offset(int dp, int t, int d) {
+  const int nd = d >> 3, g = d & 7;
+  const int nd2 = nd >> 1, sub = nd & 1;
+  const int tt = t & 15;
+  const int half = tt >> 3, c = (tt & 7) >> 1, elem = tt & 1;
+  const int lane = g * 4 + c;
+  return static_cast<uint32_t>(32 * dp + (nd2 * 32 + lane) * 16 + (sub * 2 + half) * 4 + elem * 2);
+}
+
+// Round-robin placement (attention.hpp:262-282 in closed form): global token
+// g of a cache grown only by append_round_robin with chunk c over kvp ranks.
+__host__ __device__ __forceinline__ int rr_rank(long long g, int chunk, int kvp) {
+  return static_cast<int>((g / chunk) % kvp);
+}
+__host__ __device__ __forceinline__ long long rr_row(long long g, int chunk, int kvp) {
+  return (g / (static_cast<long long>(chunk) * kvp)) * chunk + g % chunk;
+}
+// Tokens held by rank r after `total` round-robin appends.
+__host__ __device__ __forceinline__ long long rr_count(long long total, int r, int chunk, int kvp) {
+  const long long cyc = static_cast<long long>(chunk) * kvp;
+  const long long full = total / cyc, rem = total % cyc;
+  long long extra = rem - static_cast<long long>(r) * chunk;
+  extra = extra < 0 ? 0 : (extra > chunk ? chunk : extra);
+  return full * chunk + extra;
+}
+
+}  // namespace hx

@@ -1,0 +1,159 @@
+"""B200 mirror of the reference's exact-attention harness API.
+
+Reference: /root/reference/proj/include/helixsim/attention.hpp, namespace
+helixsim::exact. Same names, argument meaning and error behaviour
+(std::invalid_argument -> ValueError with the reference's message), computed
+by libhelix_b200.so on the GPU. One DecodeHarness here drives `batch`
+requests (one reference harness each, identical seeded weights,
+attention.hpp:438-442) through a single batched GPU step.
+"""
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from ._lib import (EngineInfo, ModelConfig, ParallelConfig, RuntimeConfig, check, lib)
+
+_fp = C.POINTER(C.c_float)
+
+
+def _f32(a):
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+class Rng:
+    """std::mt19937_64 with the reference's unit_draw (attention.hpp:549-552)."""
+
+    def __init__(self, seed):
+        h = C.c_void_p()
+        check(lib().hx_rng_create(seed, C.byref(h)))
+        self._h = h
+
+    def unit_draw(self):
+        return lib().hx_rng_unit_draw(self._h)
+
+    def random_matrix(self, rows, cols):
+        """DecodeHarness::random_matrix (attention.hpp:541-546), row-major draws."""
+        return np.array([[self.unit_draw() for _ in range(cols)] for _ in range(rows)])
+
+    def __del__(self):
+        try:
+            lib().hx_rng_destroy(self._h)
+        except Exception:
+            pass
+
+
+@dataclass
+class Dims:
+    """DecodeHarness::Dims (attention.hpp:421-426)."""
+    query_heads: int
+    kv_heads: int
+    head_size: int
+
+    def hidden(self):
+        return self.query_heads * self.head_size
+
+
+class MsgKind:
+    Broadcast = 0
+    AllToAll = 1
+
+
+class _Engine:
+    def __init__(self, model, tpa, kvp, chunk_size, batch, capacity, device=0, use_graphs=True, hopb=False):
+        self.mc = model
+        self.pc = ParallelConfig(tpa=tpa, kvp=kvp, chunk_size=chunk_size, distributed=0, rank=0, nccl_unique_id=None)
+        self.rc = RuntimeConfig(batch=batch, capacity_tokens=capacity, device=device, hopb=int(hopb),
+                                use_graphs=int(use_graphs))
+        h = C.c_void_p()
+        check(lib().hx_engine_create(C.byref(self.mc), C.byref(self.pc), C.byref(self.rc), C.byref(h)))
+        self._h = h
+        self.batch = batch
+
+    def _check(self, rc):
+        check(rc, self._h)
+
+    def info(self):
+        i = EngineInfo()
+        self._check(lib().hx_engine_get_info(self._h, C.byref(i)))
+        return {f: getattr(i, f) for f, _ in EngineInfo._fields_}
+
+    def transcript(self):
+        n = lib().hx_transcript_size(self._h)
+        out = np.zeros((n, 5), dtype=np.int64)
+        if n:
+            self._check(lib().hx_transcript(self._h, out.ctypes.data_as(C.POINTER(C.c_int64))))
+        return out
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib().hx_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class DecodeHarness(_Engine):
+    """DecodeHarness(dims, tpa, kvp, chunk_size, seed) (attention.hpp:428-443) on the GPU.
+
+    W_q/W_k/W_v are the reference's own mt19937_64(seed) draws, stored bf16.
+    """
+
+    def __init__(self, dims, tpa, kvp, chunk_size, seed, batch=1, capacity=4096, device=0):
+        if not isinstance(dims, Dims):
+            dims = Dims(*dims)
+        self.dims = dims
+        mc = ModelConfig(hidden=dims.query_heads * dims.head_size, query_heads=dims.query_heads,
+                         kv_heads=dims.kv_heads, head_size=dims.head_size, ffn=16, layers=1, vocab=1,
+                         attention_only=1)
+        super().__init__(mc, tpa, kvp, chunk_size, batch, capacity, device, use_graphs=False)
+        self._tpa, self._kvp = tpa, kvp
+        self._check(lib().hx_init_weights_mt19937(self._h, seed))
+
+    def pool(self):
+        return self._tpa * self._kvp
+
+    def grow_random(self, n, rng, request=0):
+        """attention.hpp:452-456 (per token: V drawn before K)."""
+        self._check(lib().hx_grow_random(self._h, 0, request, n, rng._h))
+
+    def append(self, keys, values, request=0):
+        """Append host K/V rows [n][kv_heads][head_size] round-robin."""
+        k, v = _f32(keys), _f32(values)
+        n = k.shape[0]
+        self._check(lib().hx_append_kv(self._h, 0, request, n, k.ctypes.data_as(_fp), v.ctypes.data_as(_fp)))
+
+    def step(self, x, return_lse=False):
+        """DecodeHarness::step (attention.hpp:460-510) for every request.
+
+        x: [hidden] (batch 1) or [batch, hidden]; returns [Q, Hsz] or [batch, Q, Hsz]."""
+        x = _f32(x)
+        single = x.ndim == 1
+        out = np.zeros((self.batch, self.dims.query_heads, self.dims.head_size), dtype=np.float32)
+        lse = np.zeros((self.batch, self.dims.query_heads), dtype=np.float32)
+        self._check(lib().hx_harness_step(self._h, 0, x.ctypes.data_as(_fp), x.size, out.ctypes.data_as(_fp),
+                                          lse.ctypes.data_as(_fp)))
+        if single and self.batch == 1:
+            out, lse = out[0], lse[0]
+        return (out, lse) if return_lse else out
+
+    # ShardedKVCache views (attention.hpp:286-309)
+    def total_tokens(self, request=0):
+        return lib().hx_total_tokens(self._h, 0, request)
+
+    def effective_tokens(self, rank, request=0):
+        return lib().hx_effective_tokens(self._h, 0, request, rank)
+
+    def max_min_gap(self, request=0):
+        return lib().hx_max_min_gap(self._h, 0, request)
+
+    def context(self, rank, head, request=0):
+        n = self.effective_tokens(rank, request)
+        k = np.zeros((n, self.dims.head_size), dtype=np.float32)
+        v = np.zeros((n, self.dims.head_size), dtype=np.float32)
+        self._check(lib().hx_read_kv(self._h, 0, request, rank, head, k.ctypes.data_as(_fp), v.ctypes.data_as(_fp)))
+        return k, v

@@ -1,0 +1,212 @@
+"""Decoder stack on the GPU + the reference's model/preset surface.
+
+ModelSpec mirrors helixsim::ModelSpec (types.hpp:27-52) with the same strict
+JSON schema as model_from_json / to_json (presets.cpp:96-163: snake_case keys,
+unknown keys rejected, the error names the key). HelixDecoder runs the full
+decode step (embedding -> L x [RMSNorm, Helix attention, O-proj, RMSNorm,
+SwiGLU FFN] -> RMSNorm -> LM head -> greedy token) defined in
+oracle/layer_oracle.hpp, entirely in libhelix_b200.so.
+"""
+import ctypes as C
+import json
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from ._lib import ModelConfig, check, lib
+from .exact import _Engine, _f32
+
+_ip = C.POINTER(C.c_int32)
+_fp = C.POINTER(C.c_float)
+
+
+class ConfigError(RuntimeError):
+    """presets.hpp:16-18 -- configuration-file problem (distinct from validation)."""
+
+
+@dataclass
+class MoESpec:
+    total_experts: int = 0
+    active_experts_per_token: int = 0
+    expert_ffn_dim: int = 0
+    shared_expert_ffn_dim: int = 0
+
+
+@dataclass
+class ModelSpec:
+    name: str = ""
+    layers: int = 0
+    hidden_dim: int = 0
+    query_heads: int = 0
+    kv_heads: int = 0
+    head_size: int = 0
+    ffn_dim: int = 0
+    ffn_gate_factor: int = 3
+    attention: str = "gqa"
+    kv_latent_dim: int = 0
+    moe: Optional[MoESpec] = None
+    vocab: int = 128256  # not part of the reference schema (it has no LM head); builder extension
+
+    def validate(self):
+        """ModelSpec::validate (types.cpp:16-44)."""
+        def req(c, m):
+            if not c:
+                raise ValueError(m)
+        req(self.layers >= 1, "layers must be >= 1")
+        req(self.hidden_dim >= 1, "hidden_dim must be >= 1")
+        req(self.query_heads >= 1, "query_heads must be >= 1")
+        req(self.kv_heads >= 1, "kv_heads must be >= 1")
+        req(self.head_size >= 1, "head_size must be >= 1")
+        req(self.ffn_dim >= 1, "ffn_dim must be >= 1")
+        req(self.ffn_gate_factor >= 1, "ffn_gate_factor must be >= 1")
+        req(self.hidden_dim == self.query_heads * self.head_size, "hidden_dim must equal query_heads * head_size")
+        if self.attention == "gqa":
+            req(self.query_heads % self.kv_heads == 0, "query_heads must be a multiple of kv_heads")
+            req(self.kv_latent_dim == 0, "kv_latent_dim is only meaningful for MLA")
+        else:
+            req(self.kv_heads == 1, "MLA keeps a single latent KV head")
+            req(self.kv_latent_dim >= 0, "kv_latent_dim must be >= 0")
+        if self.moe:
+            m = self.moe
+            req(m.total_experts >= 1, "moe.total_experts must be >= 1")
+            req(m.active_experts_per_token >= 1, "moe.active_experts_per_token must be >= 1")
+            req(m.active_experts_per_token <= m.total_experts,
+                "moe.active_experts_per_token must not exceed moe.total_experts")
+            req(m.expert_ffn_dim >= 1, "moe.expert_ffn_dim must be >= 1")
+            req(m.shared_expert_ffn_dim >= 0, "moe.shared_expert_ffn_dim must be >= 0")
+
+    def to_json(self):
+        j = {"name": self.name, "layers": self.layers, "hidden_dim": self.hidden_dim,
+             "query_heads": self.query_heads, "kv_heads": self.kv_heads, "head_size": self.head_size,
+             "ffn_dim": self.ffn_dim, "ffn_gate_factor": self.ffn_gate_factor, "attention": self.attention,
+             "kv_latent_dim": self.kv_latent_dim}
+        if self.moe:
+            j["moe"] = dict(self.moe.__dict__)
+        return j
+
+    @staticmethod
+    def from_json(j):
+        """model_from_json (presets.cpp:126-163): strict schema."""
+        where = "model config"
+        if not isinstance(j, dict):
+            raise ConfigError(f"{where}: expected a JSON object")
+        allowed = {"name", "layers", "hidden_dim", "query_heads", "kv_heads", "head_size", "ffn_dim",
+                   "ffn_gate_factor", "attention", "kv_latent_dim", "moe"}
+        for k in j:
+            if k not in allowed:
+                raise ConfigError(f"{where}: unknown key '{k}'")
+
+        def geti(key, default=None):
+            if key not in j:
+                if default is not None:
+                    return default
+                raise ConfigError(f"{where}: missing field '{key}'")
+            v = j[key]
+            if not isinstance(v, int) or isinstance(v, bool):
+                raise ConfigError(f"{where}: field '{key}' must be an integer")
+            return v
+        if "name" not in j:
+            raise ConfigError(f"{where}: missing field 'name'")
+        if not isinstance(j["name"], str):
+            raise ConfigError(f"{where}: field 'name' must be a string")
+        att = j.get("attention", "gqa")
+        if att not in ("gqa", "mla"):
+            raise ConfigError(f"{where}: field 'attention' must be \"gqa\" or \"mla\"")
+        m = ModelSpec(name=j["name"], layers=geti("layers"), hidden_dim=geti("hidden_dim"),
+                      query_heads=geti("query_heads"), kv_heads=geti("kv_heads"), head_size=geti("head_size"),
+                      ffn_dim=geti("ffn_dim"), ffn_gate_factor=geti("ffn_gate_factor", 3), attention=att,
+                      kv_latent_dim=geti("kv_latent_dim", 0))
+        if "moe" in j:
+            mj = j["moe"]
+            mw = "model config.moe"
+            if not isinstance(mj, dict):
+                raise ConfigError(f"{mw}: expected a JSON object")
+            for k in mj:
+                if k not in MoESpec.__dataclass_fields__:
+                    raise ConfigError(f"{mw}: unknown key '{k}'")
+            m.moe = MoESpec(**{k: int(mj[k]) for k in mj})
+        return m
+
+
+PRESETS = {
+    # reference presets (presets.cpp:11-44, presets/*.json)
+    "llama405b-like": ModelSpec("llama405b-like", 126, 16384, 128, 8, 128, 65536, 3, "gqa", 0),
+    "deepseek-r1-like": ModelSpec("deepseek-r1-like", 61, 16384, 128, 1, 128, 18432, 3, "mla", 288,
+                                  MoESpec(256, 8, 2048, 2048)),
+    # builder presets (the reference ships no tiny preset)
+    "tiny-gqa": ModelSpec("tiny-gqa", 2, 64, 8, 4, 8, 128, 3, "gqa", 0, vocab=256),
+    "llama3-8b-like": ModelSpec("llama3-8b-like", 32, 4096, 32, 8, 128, 14336, 3, "gqa", 0, vocab=128256),
+}
+
+
+def load_model(name_or_path):
+    """load_model (presets.cpp:246-252): preset name, else a JSON file path."""
+    if name_or_path in PRESETS:
+        m = PRESETS[name_or_path]
+    else:
+        try:
+            with open(name_or_path) as f:
+                j = json.load(f)
+        except OSError as e:
+            raise ConfigError(f"cannot open model config '{name_or_path}': {e}")
+        except json.JSONDecodeError as e:
+            raise ConfigError(f"malformed JSON in '{name_or_path}': {e}")
+        m = ModelSpec.from_json(j)
+    m.validate()
+    return m
+
+
+class HelixDecoder(_Engine):
+    """Full decode step of a GQA decoder stack under Helix (tpa, kvp) on one device.
+
+    `layers`/`vocab` override the spec (layer slices, small vocab for tests)."""
+
+    def __init__(self, spec, tpa=1, kvp=1, chunk_size=16, batch=8, capacity=4096, layers=None, vocab=None,
+                 device=0, use_graphs=True):
+        if spec.attention != "gqa":
+            raise NotImplementedError("MLA attention is not implemented in this build (GQA only)")
+        if spec.moe:
+            raise NotImplementedError("MoE FFN is not implemented in this build (dense SwiGLU only)")
+        self.spec = spec
+        self.layers = layers or spec.layers
+        self.vocab = vocab or spec.vocab
+        mc = ModelConfig(hidden=spec.hidden_dim, query_heads=spec.query_heads, kv_heads=spec.kv_heads,
+                         head_size=spec.head_size, ffn=spec.ffn_dim, layers=self.layers, vocab=self.vocab,
+                         attention_only=0)
+        super().__init__(mc, tpa, kvp, chunk_size, batch, capacity, device, use_graphs=use_graphs)
+
+    def init_weights(self, seed, qkv="mt19937"):
+        if qkv == "mt19937":
+            self._check(lib().hx_init_weights_mt19937(self._h, seed))
+        else:
+            self._check(lib().hx_init_weights_hash(self._h, seed))
+
+    def grow_random(self, layer, request, n, rng):
+        self._check(lib().hx_grow_random(self._h, layer, request, n, rng._h))
+
+    def fill_kv_hash(self, n, seed):
+        self._check(lib().hx_fill_kv_hash(self._h, n, seed))
+
+    def total_tokens(self, layer=0, request=0):
+        return lib().hx_total_tokens(self._h, layer, request)
+
+    def step(self, tokens, want_logits=False, want_hidden=False):
+        t = np.ascontiguousarray(tokens, dtype=np.int32)
+        nxt = np.zeros(self.batch, dtype=np.int32)
+        logits = np.zeros((self.batch, self.vocab), dtype=np.float32) if want_logits else None
+        hidden = np.zeros((self.layers + 1, self.batch, self.spec.hidden_dim), dtype=np.float32) \
+            if want_hidden else None
+        self._check(lib().hx_decode_step(self._h, t.ctypes.data_as(_ip), nxt.ctypes.data_as(_ip),
+                                         logits.ctypes.data_as(_fp) if logits is not None else None,
+                                         hidden.ctypes.data_as(_fp) if hidden is not None else None))
+        return nxt, logits, hidden
+
+    def step_device(self, tokens_ptr, next_ptr):
+        self._check(lib().hx_decode_step_device(self._h, tokens_ptr, next_ptr))
+
+    def synchronize(self):
+        self._check(lib().hx_synchronize(self._h))
+
+    def stream(self):
+        return lib().hx_stream(self._h)

@@ -34,6 +34,7 @@ def lib():
             "oracle_harness_grow_random": (C.c_int, [vp, i64, vp]),
             "oracle_harness_step": (C.c_int, [vp, dp, i64, dp, dp]),
             "oracle_harness_reference": (C.c_int, [vp, dp, i64, dp]),
+            "oracle_harness_step_append": (C.c_int, [vp, dp, i64, dp, dp, dp, dp]),
             "oracle_harness_append_projected": (C.c_int, [vp, dp, i64]),
             "oracle_harness_project": (C.c_int, [vp, dp, i64, dp, dp, dp]),
             "oracle_harness_weights": (C.c_int, [vp, C.c_int, dp]),
@@ -123,6 +124,16 @@ class Harness:
         out = np.zeros((self.q, self.hsz))
         lse = np.zeros(self.q)
         check(lib().oracle_harness_step(self.h, _dp(x), x.size, _dp(out), _dp(lse)))
+        return out, lse
+
+    def step_append(self, x, k, v):
+        """step(x) but append the given rows [kv_heads x w] (e.g. what the GPU stored)."""
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        k = np.ascontiguousarray(k, dtype=np.float64)
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        out = np.zeros((self.q, self.hsz))
+        lse = np.zeros(self.q)
+        check(lib().oracle_harness_step_append(self.h, _dp(x), x.size, _dp(out), _dp(lse), _dp(k), _dp(v)))
         return out, lse
 
     def reference(self, x):
