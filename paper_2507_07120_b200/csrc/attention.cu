@@ -346,21 +346,27 @@ __global__ void attn_split_reduce_kernel(const AttnParams p, float* frag_o, floa
       float o[PER];
 #pragma unroll
       for (int i = 0; i < PER; ++i) o[i] = 0.f;
-      float M = -INFINITY, L = 0.f;
+      // pass 1: every lane fetches a subset of the split lse values (independent loads)
+      float M = -INFINITY;
+      for (int s = lane; s < p.splits; s += 32) {
+        const int pg0 = static_cast<int>((static_cast<long long>(s) * pages) / p.splits);
+        const int pg1 = static_cast<int>((static_cast<long long>(s + 1) * pages) / p.splits);
+        if (pg1 > pg0) M = fmaxf(M, p.part_lse2[(static_cast<size_t>(s) * p.n_streams + stream) * 8 + row]);
+      }
+#pragma unroll
+      for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
+      // pass 2: weighted sum in split order (deterministic), loads unrolled by 4
+      float L = 0.f;
       for (int s = 0; s < p.splits; ++s) {
         const int pg0 = static_cast<int>((static_cast<long long>(s) * pages) / p.splits);
         const int pg1 = static_cast<int>((static_cast<long long>(s + 1) * pages) / p.splits);
         if (pg1 <= pg0) continue;
         const size_t item = static_cast<size_t>(s) * p.n_streams + stream;
-        const float lse2 = p.part_lse2[item * 8 + row];
-        const float Mn = fmaxf(M, lse2);
-        const float a = M == -INFINITY ? 0.f : exp2f(M - Mn);
-        const float w = exp2f(lse2 - Mn);
+        const float w = exp2f(p.part_lse2[item * 8 + row] - M);
         const float* src = p.part_o + (item * 8 + row) * DP;
 #pragma unroll
-        for (int i = 0; i < PER; ++i) o[i] = o[i] * a + src[lane + 32 * i] * w;
-        L = L * a + w;
-        M = Mn;
+        for (int i = 0; i < PER; ++i) o[i] += src[lane + 32 * i] * w;
+        L += w;
       }
       // fragment layout: [slot_local][b][q_in_group][DP]
       const int q_in_group = kvh * p.group + qrow;

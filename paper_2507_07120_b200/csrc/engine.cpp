@@ -58,13 +58,15 @@ double unit_draw(std::mt19937_64& rng) {  // attention.hpp:549-552
   return 2.0 * u - 1.0;
 }
 
+// Byte offset of W^T[n][k] in the CTA-tile-major fragment layout of gemv.cu:
+// [128-row block nb][k-step ks][n-tile nt (8)][lane][16 B].
 size_t wfrag_offset_host(int n, int k, int kst) {
-  const int nt = n >> 4, rn = n & 15, ks = k >> 4, rk = k & 15;
+  const int nb = n >> 7, nt = (n >> 4) & 7, rn = n & 15, ks = k >> 4, rk = k & 15;
   const int g = rn & 7, rowhalf = rn >> 3;
   const int c = (rk & 7) >> 1, khalf = rk >> 3, elem = rk & 1;
   const int reg = khalf * 2 + rowhalf;
   const int lane = g * 4 + c;
-  return ((static_cast<size_t>(nt) * kst + ks) * 32 + lane) * 16 + reg * 4 + elem * 2;
+  return (((static_cast<size_t>(nb) * kst + ks) * 8 + nt) * 32 + lane) * 16 + reg * 4 + elem * 2;
 }
 
 int round_up(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b * b); }
@@ -184,13 +186,14 @@ void Engine::plan_gemvs() {
     p.Npad = Npad;
     p.K = K;
     p.batch = B_;
+    // Each CTA streams a contiguous [128 rows x kr k-steps] weight range through
+    // its TMA ring: kr = 64 k-steps (256 KB) keeps x fragments <= 48 KB so two
+    // CTAs fit per SM; shrink kr until the grid covers >= 2 CTAs per SM.
     const int kst = K / 16;
     const int nblk = Npad / 128;
-    int ksplit = std::max(1, (2 * num_sms_ + nblk - 1) / nblk);
-    ksplit = std::min(ksplit, std::max(1, kst / 4));
-    int kr = (kst + ksplit - 1) / ksplit;
-    kr = std::min(kr, 128);
-    ksplit = (kst + kr - 1) / kr;
+    int kr = std::min(64, kst);
+    while (kr > 16 && static_cast<int64_t>(nblk) * ((kst + kr - 1) / kr) < 2 * num_sms_) kr /= 2;
+    const int ksplit = (kst + kr - 1) / kr;
     p.ksplit = ksplit;
     p.kr_steps = kr;
     p.eps = 1e-5f;

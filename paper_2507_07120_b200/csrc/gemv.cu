@@ -1,10 +1,12 @@
 // Weight-streaming GEMV / skinny GEMM for the decode step (B <= 16 rows).
 //
-// y[b][n] = sum_k x[b][k] * W[k][n] with W stored fragment-major bf16 (one
-// 16x16 tile = 512 contiguous bytes = one 16-byte load per lane), streamed
-// once from HBM with evict-first loads. x is staged in shared memory as
-// bf16 hi+lo pairs (two N=8 column groups of the m16n8k16 HMMA), so the
-// product carries ~16-bit x mantissas with fp32 accumulation.
+// y[b][n] = sum_k x[b][k] * W[k][n] with W stored fragment-major bf16 in
+// CTA-tile-major order [128-row block][k-step][8 n-tiles][512 B] (one 16x16
+// A tile = 512 contiguous bytes = one 16-byte shared load per lane), so each
+// CTA's weights are ONE contiguous range: a producer warp streams it through
+// a 4-stage shared-memory ring with cp.async.bulk (TMA bulk engine), 8
+// consumer warps run HMMA m16n8k16 against x fragments staged in shared
+// memory as bf16 hi+lo (or hi+mid+lo) terms, fp32 accumulation.
 //
 // Split-K over gridDim.y with a deterministic last-CTA reduction (partials
 // summed in split order), followed by a fused epilogue:
@@ -25,8 +27,14 @@ namespace hx {
 
 namespace {
 
-constexpr int kRows = 128;  // rows (output features) per CTA: 8 warps x 16
-constexpr int kThreads = 256;
+constexpr int kRows = 128;        // rows (output features) per CTA: 8 consumer warps x 16
+constexpr int kThreads = 256;     // consumer threads (+1 producer warp)
+constexpr int kStageSteps = 4;    // k-steps per ring stage (4 x 4 KB)
+constexpr int kStages = 4;        // ring depth: 64 KB of weights in flight per CTA
+
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 
 __device__ __forceinline__ unsigned long long logit_key(float v, int n) {
   unsigned u = __float_as_uint(v);
@@ -79,13 +87,16 @@ __device__ __forceinline__ float x_value(const GemvParams& p, const float* s_inv
 
 }  // namespace
 
-template <int NB8, int XM, int EM>
-__global__ void __launch_bounds__(kThreads) gemv_kernel(const GemvParams p) {
-  extern __shared__ __align__(16) uint8_t smem[];
-  uint2* xs = reinterpret_cast<uint2*>(smem);  // [kr][2*NB8][32]
+template <int NB8, int XM, int EM, int XS>
+__global__ void __launch_bounds__(kThreads + 32) gemv_kernel(const GemvParams p) {
+  // Shared memory: [ring: kStages x kStageSteps x 4 KB][xs fragments][mbarriers]
+  extern __shared__ __align__(128) uint8_t smem[];
+  uint8_t* ring = smem;
+  uint2* xs = reinterpret_cast<uint2*>(smem + kStages * kStageSteps * 4096);
   __shared__ float s_inv[16];
   __shared__ int s_last;
   __shared__ unsigned long long s_best[16];
+  __shared__ __align__(8) uint64_t full[kStages], empty[kStages];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nblk = blockIdx.x, ksp = blockIdx.y;
@@ -93,15 +104,42 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const GemvParams p) {
   const int ks0 = ksp * p.kr_steps;
   const int ks1 = min(ks0 + p.kr_steps, KST);
   const int nks = ks1 - ks0;
+  const int nst = (nks + kStageSteps - 1) / kStageSteps;
 
-  // ---------------------------------------------------------------- prologue
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 8);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+
+  if (warp == 8) {
+    // ------------------------------------------------------------ producer: TMA bulk weight stream
+    // the CTA's weights [nblk][ks0..ks1][8 n-tiles][512 B] are one contiguous range
+    if (lane == 0) {
+      const uint8_t* src = reinterpret_cast<const uint8_t*>(p.w) + (static_cast<size_t>(nblk) * KST + ks0) * 4096;
+      for (int st = 0; st < nst; ++st) {
+        const int s = st % kStages;
+        if (st >= kStages) mbar_wait(&empty[s], ((st / kStages) & 1) ^ 1);
+        const int steps = min(kStageSteps, nks - st * kStageSteps);
+        const uint32_t bytes = static_cast<uint32_t>(steps) * 4096u;
+        mbar_arrive_expect_tx(&full[s], bytes);
+        bulk_g2s(ring + s * kStageSteps * 4096, src + static_cast<size_t>(st) * kStageSteps * 4096, bytes, &full[s]);
+      }
+    }
+    return;  // exited threads do not block later CTA barriers
+  }
+
+  // ---------------------------------------------------------------- prologue (overlaps the stream)
   if (XM == X_NORM) {
     if (threadIdx.x < p.batch) {
       float s = 0.f;
       for (int i = 0; i < p.n_ss; ++i) s += p.ss_part[i * p.batch + threadIdx.x];
       s_inv[threadIdx.x] = rsqrtf(s / static_cast<float>(p.K) + p.eps);
     }
-    __syncthreads();
+    named_bar_sync(1, kThreads);
   }
   for (int e = threadIdx.x; e < nks * NB8 * 32; e += kThreads) {
     const int ln = e & 31;
@@ -117,46 +155,48 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const GemvParams p) {
       v[2] = x_value<XM>(p, s_inv, b, k + 8);
       v[3] = x_value<XM>(p, s_inv, b, k + 9);
     }
-    float hi[4], lo[4];
+    if (XS == 2) {
+      float hi[4], lo[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) split2(v[i], hi[i], lo[i]);
-    xs[(ksl * 2 * NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(hi[0], hi[1]), pack_bf16(hi[2], hi[3]));
-    xs[(ksl * 2 * NB8 + NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(lo[0], lo[1]), pack_bf16(lo[2], lo[3]));
+      for (int i = 0; i < 4; ++i) split2(v[i], hi[i], lo[i]);
+      xs[(ksl * 2 * NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(hi[0], hi[1]), pack_bf16(hi[2], hi[3]));
+      xs[(ksl * 2 * NB8 + NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(lo[0], lo[1]), pack_bf16(lo[2], lo[3]));
+    } else {
+      float hi[4], mid[4], lo[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) split3(v[i], hi[i], mid[i], lo[i]);
+      xs[(ksl * 3 * NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(hi[0], hi[1]), pack_bf16(hi[2], hi[3]));
+      xs[(ksl * 3 * NB8 + NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(mid[0], mid[1]), pack_bf16(mid[2], mid[3]));
+      xs[(ksl * 3 * NB8 + 2 * NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(lo[0], lo[1]), pack_bf16(lo[2], lo[3]));
+    }
   }
-  __syncthreads();
+  named_bar_sync(1, kThreads);
 
-  // ---------------------------------------------------------------- stream W
+  // ---------------------------------------------------------------- consume the weight ring
   const int ntile = nblk * 8 + warp;
-  float acc[2 * NB8][4];
+  float acc[XS * NB8][4];
 #pragma unroll
-  for (int j = 0; j < 2 * NB8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
-  const uint4* wp = p.w + (static_cast<size_t>(ntile) * KST + ks0) * 32 + lane;
+  for (int j = 0; j < XS * NB8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
   const uint32_t xs_base = smem_u32(xs) + lane * 8;
-
-  constexpr int U = 8;
-  const uint64_t pol = policy_evict_first();
-  uint4 wa[U];
+  const uint32_t ring_base = smem_u32(ring) + warp * 512 + lane * 16;
+  for (int st = 0; st < nst; ++st) {
+    const int s = st % kStages;
+    mbar_wait(&full[s], (st / kStages) & 1);
+    const int steps = min(kStageSteps, nks - st * kStageSteps);
 #pragma unroll
-  for (int u = 0; u < U; ++u)
-    if (u < nks) wa[u] = ldg_stream(wp + u * 32, pol);
-  for (int kb = 0; kb < nks; kb += U) {
-    uint4 wn[U];
+    for (int kk = 0; kk < kStageSteps; ++kk) {
+      if (kk < steps) {
+        const uint4 wa = lds128(ring_base + (s * kStageSteps + kk) * 4096);
+        const uint32_t xa = xs_base + ((st * kStageSteps + kk) * XS * NB8) * 256;
 #pragma unroll
-    for (int u = 0; u < U; ++u)
-      if (kb + U + u < nks) wn[u] = ldg_stream(wp + (kb + U + u) * 32, pol);
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (kb + u < nks) {
-        const uint32_t xa = xs_base + ((kb + u) * 2 * NB8) * 256;
-#pragma unroll
-        for (int j = 0; j < 2 * NB8; ++j) {
+        for (int j = 0; j < XS * NB8; ++j) {
           const uint2 bx = lds64(xa + j * 256);
-          mma_bf16_16816(acc[j], wa[u].x, wa[u].y, wa[u].z, wa[u].w, bx.x, bx.y);
+          mma_bf16_16816(acc[j], wa.x, wa.y, wa.z, wa.w, bx.x, bx.y);
         }
       }
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) wa[u] = wn[u];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
   }
 
   // partials: rows ntile*16 + g (+8), batches bg*8 + 2c (+1)
@@ -165,35 +205,39 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const GemvParams p) {
     const int n0 = ntile * 16 + g;
 #pragma unroll
     for (int bg = 0; bg < NB8; ++bg) {
-      const float* hi = acc[bg];
-      const float* lo = acc[NB8 + bg];
+      float y[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        y[i] = acc[bg][i] + acc[(XS - 1) * NB8 + bg][i];
+        if (XS == 3) y[i] += acc[NB8 + bg][i];
+      }
       const int b0 = bg * 8 + 2 * c;
       float* yp = p.ypart + static_cast<size_t>(ksp) * p.batch * p.Npad;
       if (b0 < p.batch) {
-        yp[static_cast<size_t>(b0) * p.Npad + n0] = hi[0] + lo[0];
-        yp[static_cast<size_t>(b0) * p.Npad + n0 + 8] = hi[2] + lo[2];
+        yp[static_cast<size_t>(b0) * p.Npad + n0] = y[0];
+        yp[static_cast<size_t>(b0) * p.Npad + n0 + 8] = y[2];
       }
       if (b0 + 1 < p.batch) {
-        yp[static_cast<size_t>(b0 + 1) * p.Npad + n0] = hi[1] + lo[1];
-        yp[static_cast<size_t>(b0 + 1) * p.Npad + n0 + 8] = hi[3] + lo[3];
+        yp[static_cast<size_t>(b0 + 1) * p.Npad + n0] = y[1];
+        yp[static_cast<size_t>(b0 + 1) * p.Npad + n0 + 8] = y[3];
       }
     }
   }
   __threadfence();  // every writer publishes its partials device-wide
-  __syncthreads();
+  named_bar_sync(1, kThreads);
   if (threadIdx.x == 0) {
     const int prev = atomicAdd(&p.counters[nblk], 1);
     s_last = prev == p.ksplit - 1;
   }
-  __syncthreads();
+  named_bar_sync(1, kThreads);
   if (!s_last) return;
   __threadfence();
 
   // ---------------------------------------------------------------- epilogue (last CTA of the n-block)
-  float* vt = reinterpret_cast<float*>(smem);  // [16][kRows] staged results (reuses xs)
+  float* vt = reinterpret_cast<float*>(smem);  // [16][kRows] staged results (reuses the ring)
   if (EM == E_LOGITS) {
     if (threadIdx.x < 16) s_best[threadIdx.x] = 0ull;
-    __syncthreads();
+    named_bar_sync(1, kThreads);
   }
   const int rows_here = EM == E_SWIGLU ? kRows / 2 : kRows;
   for (int e = threadIdx.x; e < rows_here * p.batch; e += kThreads) {
@@ -261,7 +305,7 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const GemvParams p) {
   }
   if (EM == E_STORE || EM == E_RESID) {
     if (p.ss_out) {
-      __syncthreads();
+      named_bar_sync(1, kThreads);
       for (int b = warp; b < p.batch; b += kThreads / 32) {
         float s = 0.f;
         for (int r = lane; r < kRows; r += 32) s += vt[b * kRows + r];
@@ -272,30 +316,32 @@ __global__ void __launch_bounds__(kThreads) gemv_kernel(const GemvParams p) {
     }
   }
   if (EM == E_LOGITS) {
-    __syncthreads();
+    named_bar_sync(1, kThreads);
     if (threadIdx.x < p.batch) atomicMax(&p.best[threadIdx.x], s_best[threadIdx.x]);
   }
   if (threadIdx.x == 0) p.counters[nblk] = 0;  // self-reset for the next launch
 }
 
-size_t gemv_smem_bytes(const GemvParams& p) {
+size_t gemv_smem_bytes(const GemvParams& p, int xs_terms) {
   const int nb8 = (p.batch + 7) / 8;
-  const size_t xs = static_cast<size_t>(p.kr_steps) * nb8 * 2 * 32 * 8;
-  const size_t vt = 16 * kRows * 4;
-  return xs > vt ? xs : vt;
+  const size_t xs = static_cast<size_t>(p.kr_steps) * nb8 * xs_terms * 32 * 8;
+  return static_cast<size_t>(kStages) * kStageSteps * 4096 + xs;  // epilogue staging reuses the ring
 }
 
 template <int NB8, int XM, int EM>
 static cudaError_t launch_t(const GemvParams& p, cudaStream_t stream) {
-  const size_t smem = gemv_smem_bytes(p);
+  // QKV feeds exp(q.k) with |logits| up to ~1e3 under the reference's unscaled
+  // weights: carry x at fp32 precision there (3 bf16 terms), 2 terms elsewhere.
+  constexpr int XS = EM == E_QKV ? 3 : 2;
+  const size_t smem = gemv_smem_bytes(p, XS);
   if (smem > 48 * 1024) {
-    cudaError_t e = cudaFuncSetAttribute(gemv_kernel<NB8, XM, EM>,
+    cudaError_t e = cudaFuncSetAttribute(gemv_kernel<NB8, XM, EM, XS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
   }
   dim3 grid(p.Npad / kRows, p.ksplit);
-  gemv_kernel<NB8, XM, EM><<<grid, kThreads, smem, stream>>>(p);
+  gemv_kernel<NB8, XM, EM, XS><<<grid, kThreads + 32, smem, stream>>>(p);
   return cudaGetLastError();
 }
 

@@ -63,7 +63,7 @@ struct GemvParams {
   unsigned long long* best;  // [B] packed (orderable logit, ~index)
 };
 cudaError_t launch_gemv(const GemvParams& p, int xmode, int emode, cudaStream_t stream);
-size_t gemv_smem_bytes(const GemvParams& p);
+size_t gemv_smem_bytes(const GemvParams& p, int xs_terms);
 
 // ---------------------------------------------------------------- misc
 cudaError_t launch_merge_out(const float* frag_o, const float* frag_lse, int batch, int q_heads,

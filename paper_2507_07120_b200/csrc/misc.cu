@@ -163,39 +163,81 @@ cudaError_t launch_kv_append_rows(uint8_t* kv, const uint16_t* k_rows, const uin
 }
 
 // Hash fill: element (b, h, g, d) = hash_unit(seed, stream, ((b*K + h) << 32 + g) * Hsz + d)
-// (layer_oracle.hpp ModelOracle::grow_hash). One thread per (b, h, g, 8 dims).
+// (layer_oracle.hpp ModelOracle::grow_hash). One warp per page of one stream
+// (slot, request, kv head); each lane writes whole 16-byte chunks of the
+// fragment-major page image (coalesced 512 B per warp store). Rows outside the
+// new token range keep their old contents (read-modify-write on edge pages).
+__device__ __forceinline__ long long rr_global_of_row(long long row, int rank, int chunk, int kvp) {
+  return (row / chunk) * static_cast<long long>(chunk) * kvp + static_cast<long long>(rank) * chunk + row % chunk;
+}
+
+__device__ __forceinline__ uint16_t hash_bf16_bits(uint64_t sseed, uint64_t index) {
+  const uint64_t z = splitmix64(sseed + index);
+  const double u = 2.0 * (static_cast<double>(z >> 11) * 0x1.0p-53) - 1.0;
+  const __nv_bfloat16 h = double_to_bf16_rne(u);
+  return *reinterpret_cast<const uint16_t*>(&h);
+}
+
 __global__ void kv_fill_hash_kernel(uint8_t* kv, const int* total, int batch, int kv_heads,
                                     int kvh_per_slot, int kvp, int chunk, int head_dim, int dp,
                                     int page_cap, int slot_base, int n_local_slots, long long n,
                                     uint64_t seed, uint64_t stream_k, uint64_t stream_v) {
-  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int dgroups = (head_dim + 7) / 8;
-  const long long per_b = static_cast<long long>(kv_heads) * n * dgroups;
-  if (idx >= per_b * batch) return;
-  const int b = static_cast<int>(idx / per_b);
-  long long r = idx - b * per_b;
-  const int h = static_cast<int>(r / (n * dgroups));
-  r -= static_cast<long long>(h) * n * dgroups;
-  const long long i = r / dgroups;
-  const int dg = static_cast<int>(r - i * dgroups);
-  const long long g = static_cast<long long>(total[b]) + i;
+  const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long long streams = static_cast<long long>(n_local_slots) * batch * kvh_per_slot;
+  if (warp >= streams * page_cap) return;
+  const int page = static_cast<int>(warp % page_cap);
+  const long long stream_idx = warp / page_cap;  // ((slot_local*B + b)*kvh_per_slot + kvh)
+  long long st = stream_idx;
+  const int kvh = static_cast<int>(st % kvh_per_slot);
+  st /= kvh_per_slot;
+  const int b = static_cast<int>(st % batch);
+  const int slot = static_cast<int>(st / batch) + slot_base;
+  const int rank = slot % kvp, grp = slot / kvp;
+  const int h = grp * kvh_per_slot + kvh;
+  const long long t0 = total[b], t1 = t0 + n;
+  const long long gmin = rr_global_of_row(16ll * page, rank, chunk, kvp);
+  const long long gmax = rr_global_of_row(16ll * page + 15, rank, chunk, kvp);
+  if (gmax < t0 || gmin >= t1) return;
+  const bool full = gmin >= t0 && gmax < t1;
   const uint64_t kseed = splitmix64(seed ^ (stream_k * 0xD1B54A32D192ED03ull));
   const uint64_t vseed = splitmix64(seed ^ (stream_v * 0xD1B54A32D192ED03ull));
-  for (int d = dg * 8; d < min(head_dim, dg * 8 + 8); ++d) {
-    const uint64_t index =
-        ((static_cast<uint64_t>(b * kv_heads + h) << 32) + static_cast<uint64_t>(g)) *
-            static_cast<uint64_t>(head_dim) + static_cast<uint64_t>(d);
-    const uint64_t zk = splitmix64(kseed + index);
-    const uint64_t zv = splitmix64(vseed + index);
-    const double uk = 2.0 * (static_cast<double>(zk >> 11) * 0x1.0p-53) - 1.0;
-    const double uv = 2.0 * (static_cast<double>(zv >> 11) * 0x1.0p-53) - 1.0;
-    uint8_t* pk = kv_elem_ptr(kv, g, b, h, d, 0, batch, kvh_per_slot, kvp, chunk, dp, page_cap,
-                              slot_base, n_local_slots);
-    if (!pk) continue;
-    uint8_t* pv = kv_elem_ptr(kv, g, b, h, d, 1, batch, kvh_per_slot, kvp, chunk, dp, page_cap,
-                              slot_base, n_local_slots);
-    *reinterpret_cast<__nv_bfloat16*>(pk) = double_to_bf16_rne(uk);
-    *reinterpret_cast<__nv_bfloat16*>(pv) = double_to_bf16_rne(uv);
+  const uint64_t base = static_cast<uint64_t>(b * kv_heads + h) << 32;
+  uint8_t* pg = kv + (static_cast<size_t>(stream_idx) * page_cap + page) * page_bytes(dp);
+  const int chunks = 64 * dp / 16;  // 16-byte chunks per page
+  for (int ci = lane; ci < chunks; ci += 32) {
+    uint4* dst = reinterpret_cast<uint4*>(pg + ci * 16);
+    uint4 old = full ? make_uint4(0, 0, 0, 0) : *dst;
+    uint16_t* ov = reinterpret_cast<uint16_t*>(&old);
+    const int is_v = ci >= chunks / 2;
+    const int cl = is_v ? ci - chunks / 2 : ci;
+    const int ln = cl & 31, grpi = cl >> 5;
+    const int g = ln >> 2, c = ln & 3;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      // e = sub*4 + half*2 + elem  (see kv_layout.cuh)
+      const int sub = e >> 2, half = (e >> 1) & 1, elem = e & 1;
+      int t, d;
+      if (!is_v) {  // grpi = nt*(dp/32) + kp
+        const int nt = grpi / (dp / 32), kp = grpi % (dp / 32);
+        t = nt * 8 + g;
+        d = (2 * kp + sub) * 16 + half * 8 + 2 * c + elem;
+      } else {      // grpi = nd2
+        const int nd = 2 * grpi + sub;
+        d = nd * 8 + g;
+        t = half * 8 + 2 * c + elem;
+      }
+      const long long gtok = rr_global_of_row(16ll * page + t, rank, chunk, kvp);
+      if (gtok < t0 || gtok >= t1) continue;
+      if (d >= head_dim) {
+        ov[e] = 0;
+        continue;
+      }
+      const uint64_t index = (base + static_cast<uint64_t>(gtok)) * static_cast<uint64_t>(head_dim) +
+                             static_cast<uint64_t>(d);
+      ov[e] = hash_bf16_bits(is_v ? vseed : kseed, index);
+    }
+    *dst = old;
   }
 }
 
@@ -209,8 +251,8 @@ cudaError_t launch_kv_fill_hash(uint8_t* kv, int* total, int batch, int kv_heads
                                 int page_cap, int slot_base, int n_local_slots, long long n,
                                 uint64_t seed, uint64_t stream_k, uint64_t stream_v,
                                 cudaStream_t stream) {
-  const long long work = static_cast<long long>(batch) * kv_heads * n * ((head_dim + 7) / 8);
-  if (work > 0)
+  const long long work = static_cast<long long>(n_local_slots) * batch * kvh_per_slot * page_cap * 32;
+  if (n > 0)
     kv_fill_hash_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(
         kv, total, batch, kv_heads, kvh_per_slot, kvp, chunk, head_dim, dp, page_cap, slot_base,
         n_local_slots, n, seed, stream_k, stream_v);
@@ -230,12 +272,7 @@ __host__ __device__ __forceinline__ size_t wfrag_offset(int n, int k, int kst) {
   return ((static_cast<size_t>(nt) * kst + ks) * 32 + lane) * 16 + reg * 4 + elem * 2;
 }
 
-__global__ void weight_init_hash_kernel(uint8_t* w, int Npad, int K, const WSeg* segs, int nseg,
-                                        uint64_t seed) {
-  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= static_cast<long long>(Npad) * K) return;
-  const int n = static_cast<int>(idx / K), k = static_cast<int>(idx - static_cast<long long>(n) * K);
-  double v = 0.0;
+__device__ double wseg_value(const WSeg* segs, int nseg, int n, int k, uint64_t seed) {
   for (int s = 0; s < nseg; ++s) {
     const WSeg sg = segs[s];
     if (n < sg.rows_begin || n >= sg.rows_end) continue;
@@ -246,22 +283,49 @@ __global__ void weight_init_hash_kernel(uint8_t* w, int Npad, int K, const WSeg*
       // SwiGLU: per 128-row block, rows [0,64) gate features, [64,128) up features
       const int blk = n >> 7, r = n & 127;
       if ((sg.interleave == 1) != (r < 64)) continue;
-      col = blk * 64 + (r & 63);
-      if (col >= sg.cols_total) continue;
+      col = sg.col_offset + blk * 64 + (r & 63);
+      if (col >= sg.cols_total) return 0.0;
     }
     const uint64_t index = static_cast<uint64_t>(k) * static_cast<uint64_t>(sg.cols_total) +
                            static_cast<uint64_t>(col);
-    v = hash_unit(seed, sg.stream, index) * sg.scale;
-    break;
+    return hash_unit(seed, sg.stream, index) * sg.scale;
   }
-  *reinterpret_cast<__nv_bfloat16*>(w + wfrag_offset(n, k, K >> 4)) = double_to_bf16_rne(v);
+  return 0.0;
+}
+
+// One thread per 16-byte chunk (n-tile, k-step, lane) of the fragment-major image.
+__global__ void weight_init_hash_kernel(uint4* w, int Npad, int K, const WSeg* segs, int nseg,
+                                        uint64_t seed) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int kst = K >> 4;
+  if (idx >= static_cast<long long>(Npad / 16) * kst * 32) return;
+  // chunk index = ((nb * kst + ks) * 8 + ntl) * 32 + lane  (CTA-tile-major, see gemv.cu)
+  const int lane = static_cast<int>(idx & 31);
+  long long t = idx >> 5;
+  const int ntl = static_cast<int>(t & 7);
+  t >>= 3;
+  const int ks = static_cast<int>(t % kst), nb = static_cast<int>(t / kst);
+  const int nt = nb * 8 + ntl;
+  const int g = lane >> 2, c = lane & 3;
+  uint4 out;
+  uint16_t* o = reinterpret_cast<uint16_t*>(&out);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int reg = e >> 1, elem = e & 1;          // reg = khalf*2 + rowhalf
+    const int rowhalf = reg & 1, khalf = reg >> 1;
+    const int n = nt * 16 + rowhalf * 8 + g;
+    const int k = ks * 16 + khalf * 8 + 2 * c + elem;
+    const __nv_bfloat16 h = double_to_bf16_rne(wseg_value(segs, nseg, n, k, seed));
+    o[e] = *reinterpret_cast<const uint16_t*>(&h);
+  }
+  w[idx] = out;
 }
 
 cudaError_t launch_weight_init_hash(uint4* w, int Npad, int K, const WSeg* segs, int nseg,
                                     uint64_t seed, cudaStream_t stream) {
-  const long long work = static_cast<long long>(Npad) * K;
+  const long long work = static_cast<long long>(Npad / 16) * (K / 16) * 32;
   weight_init_hash_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(
-      reinterpret_cast<uint8_t*>(w), Npad, K, segs, nseg, seed);
+      w, Npad, K, segs, nseg, seed);
   return cudaGetLastError();
 }
 

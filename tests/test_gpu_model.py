@@ -63,6 +63,18 @@ def test_hash_init_matches_oracle_weights():
     g.fill_kv_hash(20, 77)
     for b in range(2):
         o.grow_hash(0, b, 20)
+    h = O.Harness(4, 2, 32, 1, 1, 16, 77, bf16=True)  # layout reference for the readback below
+    import ctypes
+    for b in range(2):
+        for head in range(2):
+            k = np.zeros((20, 32), dtype=np.float32)
+            v = np.zeros((20, 32), dtype=np.float32)
+            rc = P.lib().hx_read_kv(g._h, 0, b, 0, head, k.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+                                    v.ctypes.data_as(ctypes.POINTER(ctypes.c_float)))
+            assert rc == 0
+            want_k = np.array([[O.hash_unit(77, (10 << 32) | 0, (((b * 2 + head) << 32) + t) * 32 + d)
+                                for d in range(32)] for t in range(20)])
+            np.testing.assert_array_equal(k, O.round_bf16(want_k).astype(np.float32))
     nxt, logits, hidden = g.step(np.array([1, 2]), want_logits=True, want_hidden=True)
     lo, ho, no = o.step(np.array([1, 2]))
     assert rel_err(hidden[0], ho[0]) == 0.0  # embedding rows are bit-identical
