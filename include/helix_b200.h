@@ -53,14 +53,23 @@ typedef struct hx_model_config {
   int32_t reserved;
 } hx_model_config;
 
+typedef struct hx_loopback hx_loopback;
+
 typedef struct hx_parallel_config {
   int64_t tpa;          /* attention tensor parallelism (types.hpp:97) */
   int64_t kvp;          /* KV parallelism across the sequence (types.hpp:98) */
   int64_t chunk_size;   /* round-robin chunk (attention.hpp:237, default 16) */
-  int32_t distributed;  /* 0: whole tpa*kvp pool on this device; 1: this process is one rank */
+  int32_t distributed;  /* HX_POOL_LOCAL: whole tpa*kvp pool on this device;
+                           HX_POOL_NCCL: this process is one rank (one GPU) of the pool;
+                           HX_POOL_LOOPBACK: one rank per host thread on one device (tests) */
   int32_t rank;         /* global rank id g*kvp + r (attention.hpp:555) when distributed */
-  const void* nccl_unique_id; /* 128 bytes (ncclUniqueId) when distributed */
+  const void* nccl_unique_id; /* 128 bytes (ncclUniqueId) for HX_POOL_NCCL */
+  hx_loopback* loopback;      /* shared group for HX_POOL_LOOPBACK */
 } hx_parallel_config;
+
+#define HX_POOL_LOCAL 0
+#define HX_POOL_NCCL 1
+#define HX_POOL_LOOPBACK 2
 
 typedef struct hx_runtime_config {
   int64_t batch;            /* concurrent requests (one DecodeHarness each) */
@@ -136,9 +145,9 @@ int hx_synchronize(hx_engine* e);
  * attention-only mode) with CUDA events after every launch on the engine
  * stream; ms[kind] = average milliseconds per step for kind
  * 0 embed, 1 qkv+append, 2 attention, 3 split-reduce, 4 o-proj (+merge),
- * 5 gate/up, 6 down, 7 lm-head+argmax, 8 merge (harness). Advances the caches
- * like real steps. */
-#define HX_PROF_KINDS 9
+ * 5 gate/up, 6 down, 7 lm-head+argmax, 8 merge (harness), 9 exchange /
+ * all-reduce / residual (distributed pools). Advances the caches like real steps. */
+#define HX_PROF_KINDS 10
 int hx_profile_step(hx_engine* e, int64_t reps, double* ms);
 /* The engine's CUDA stream (cudaStream_t) for event timing by the caller. */
 void* hx_stream(hx_engine* e);
@@ -150,7 +159,20 @@ int hx_transcript(const hx_engine* e, int64_t* out);
 int hx_clear_transcript(hx_engine* e);
 
 /* --- distributed plumbing --- */
+/* Rank 0 creates the NCCL id and shares it (e.g. torch.distributed broadcast). */
 int hx_nccl_get_unique_id(void* out128);
+/* Fragment-exchange layout of one TPA group (attention.hpp:492-502), host only:
+ * for each destination KVP rank p, out[4p..4p+3] = first flattened element,
+ * element count (= slice), first head touched, heads touched; returns the
+ * padded per-(peer, request) chunk in floats (slice + lse slots), or < 0. */
+int64_t hx_exchange_layout(int64_t q_per_group, int64_t head_size, int64_t kvp, int64_t* out);
+/* Measurement switches: HX_FLAG_SKIP_COMM = 1 replaces every collective by a
+ * local copy (exposed-communication measurement; results are then wrong). */
+#define HX_FLAG_SKIP_COMM 1
+int hx_engine_set_flag(hx_engine* e, int32_t flag, int32_t value);
+/* In-process group of n ranks on one device (one host thread per rank). */
+int hx_loopback_create(int32_t n_ranks, hx_loopback** out);
+void hx_loopback_destroy(hx_loopback* lb);
 
 #ifdef __cplusplus
 }

@@ -19,9 +19,12 @@ class ModelConfig(C.Structure):
                 ("layers", i64), ("vocab", i64), ("attention_only", i32), ("reserved", i32)]
 
 
+POOL_LOCAL, POOL_NCCL, POOL_LOOPBACK = 0, 1, 2
+
+
 class ParallelConfig(C.Structure):
     _fields_ = [("tpa", i64), ("kvp", i64), ("chunk_size", i64), ("distributed", i32), ("rank", i32),
-                ("nccl_unique_id", vp)]
+                ("nccl_unique_id", vp), ("loopback", vp)]
 
 
 class RuntimeConfig(C.Structure):
@@ -65,6 +68,10 @@ EXPORTS = {
     "hx_transcript": (C.c_int, [vp, C.POINTER(C.c_int64)]),
     "hx_clear_transcript": (C.c_int, [vp]),
     "hx_nccl_get_unique_id": (C.c_int, [vp]),
+    "hx_loopback_create": (C.c_int, [i32, C.POINTER(vp)]),
+    "hx_exchange_layout": (i64, [i64, i64, i64, C.POINTER(i64)]),
+    "hx_engine_set_flag": (C.c_int, [vp, i32, i32]),
+    "hx_loopback_destroy": (None, [vp]),
 }
 
 _lib = None

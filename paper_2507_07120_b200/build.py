@@ -23,6 +23,16 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 CXXSTD = "-std=c++17"
 
 
+def nccl_dirs():
+    """NCCL 2.28 from the torch-bundled nvidia-nccl wheel (same library torch loads)."""
+    try:
+        import nvidia.nccl
+        base = list(nvidia.nccl.__path__)[0]
+        return os.path.join(base, "include"), os.path.join(base, "lib")
+    except ImportError:
+        return "/usr/include", "/usr/lib/x86_64-linux-gnu"
+
+
 def _newer(src_list, target):
     if not os.path.exists(target):
         return True
@@ -35,8 +45,9 @@ def build(verbose=False, force=False):
     headers = glob.glob(os.path.join(CSRC, "*.h")) + glob.glob(os.path.join(CSRC, "*.cuh")) + \
         [os.path.join(ROOT, "include", "helix_b200.h")]
     objs = []
+    nccl_inc, nccl_lib = nccl_dirs()
     cu_flags = [NVCC, CXXSTD, "-O3", "-lineinfo", *ARCH, "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-                "-I", CSRC, "-I", os.path.join(ROOT, "include")]
+                "-I", CSRC, "-I", os.path.join(ROOT, "include"), "-I", nccl_inc]
     if verbose:
         cu_flags += ["-Xptxas", "-v"]
     jobs = []
@@ -57,6 +68,7 @@ def build(verbose=False, force=False):
         raise RuntimeError("nvcc compilation failed")
     if force or jobs or _newer(objs, LIB):
         link = [NVCC, "-shared", *ARCH, "-Xcompiler", "-fPIC", "-cudart", "static", "-o", LIB, *objs,
+                "-L", nccl_lib, "-l:libnccl.so.2", "-Xlinker", f"-rpath,{nccl_lib}",
                 "-Xlinker", "--no-undefined", "-lrt", "-lpthread", "-ldl"]
         subprocess.check_call(link)
     return LIB

@@ -77,11 +77,13 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
     fence_mbar_init();
   }
   __syncthreads();
+  griddep_launch_dependents();
 
   if (warp == NWC) {
     // ------------------------------------------------------------ producer
     if (lane == 0) {
       int st = 0;
+      bool waited = false;  // q rows come from the QKV kernel: wait before staging them
       for (;;) {
         const int item = atomicAdd(p.work_counter, 1);
         bool done = item >= p.n_items;
@@ -93,8 +95,8 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           int t = stream;
           const int qc = t % p.q_chunks; t /= p.q_chunks;
           t /= p.kvh_per_slot;
-          const int b = t % p.batch;
-          const int slot = t / p.batch + p.slot_base;
+          const int b = t % p.stream_batch + p.b_begin;
+          const int slot = t / p.stream_batch + p.slot_base;
           const int rank = slot % p.kvp;
           ntok = static_cast<int>(rr_count(p.total[b], rank, p.chunk, p.kvp));
           const int pages = (ntok + 15) >> 4;
@@ -110,6 +112,10 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           if (st >= NSTAGE) mbar_wait(&empty[s], ((st / NSTAGE) & 1) ^ 1);
           StageMeta& m = meta[s];
           if (done) {
+            if (!waited) {
+              griddep_wait();
+              waited = true;
+            }
             m.item = kItemDone;
             mbar_arrive(&full[s]);
             break;
@@ -125,22 +131,31 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           m.last = ch == nchunks - 1;
           m.rows = rows;
           uint8_t* dst = stages + s * STAGE_BYTES;
-          const uint8_t* src =
-              p.kv + (static_cast<size_t>(stream / p.q_chunks) * p.page_cap + a) * Cfg::PAGE;
+          // KV stream index in the page pool: ((slot_local * batch + b) * kvh_per_slot + kvh)
+          int ts = stream / p.q_chunks;
+          const int kvh_s = ts % p.kvh_per_slot;
+          ts /= p.kvh_per_slot;
+          const int b_s = ts % p.stream_batch + p.b_begin, sl_s = ts / p.stream_batch;
+          const size_t pool_stream = (static_cast<size_t>(sl_s) * p.batch + b_s) * p.kvh_per_slot + kvh_s;
+          const uint8_t* src = p.kv + (pool_stream * p.page_cap + a) * Cfg::PAGE;
           uint32_t bytes = np * Cfg::PAGE;
           uint32_t qbytes = 0;
           if (ch == 0) qbytes = static_cast<uint32_t>(rows) * DP * 4;
           mbar_arrive_expect_tx(&full[s], bytes + qbytes);
-          bulk_g2s(dst, src, bytes, &full[s]);
+          bulk_g2s(dst, src, bytes, &full[s]);  // KV pages: independent of the previous kernel
+          if (!waited) {
+            griddep_wait();
+            waited = true;
+          }
           if (qbytes) {
             // q rows of this stream: [request][head][DP] fp32, heads contiguous
             int t = stream;
             const int qc = t % p.q_chunks; t /= p.q_chunks;
             const int kvh = t % p.kvh_per_slot; t /= p.kvh_per_slot;
-            const int b = t % p.batch;
-            const int slot = t / p.batch + p.slot_base;
+            const int b = t % p.stream_batch + p.b_begin;
+            const int slot = t / p.stream_batch + p.slot_base;
             const int grp = slot / p.kvp;
-            const int head0 = (grp * p.kvh_per_slot + kvh) * p.group + qc * 8;
+            const int head0 = ((grp - p.q_grp_base) * p.kvh_per_slot + kvh) * p.group + qc * 8;
             const float* qsrc = p.q + (static_cast<size_t>(b) * p.q_heads + head0) * DP;
             bulk_g2s(dst + STAGE_KV, qsrc, qbytes, &full[s]);
           }
@@ -326,6 +341,8 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
 // attention.hpp:56-59; empty shard -> (0, -inf) as at :69-70).
 template <int DP>
 __global__ void attn_split_reduce_kernel(const AttnParams p, float* frag_o, float* frag_lse) {
+  griddep_wait();
+  griddep_launch_dependents();
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const int row = warp_global & 7;
@@ -334,8 +351,8 @@ __global__ void attn_split_reduce_kernel(const AttnParams p, float* frag_o, floa
     int t = stream;
     const int qc = t % p.q_chunks; t /= p.q_chunks;
     const int kvh = t % p.kvh_per_slot; t /= p.kvh_per_slot;
-    const int b = t % p.batch;
-    const int slot_local = t / p.batch;
+    const int b = t % p.stream_batch + p.b_begin;
+    const int slot_local = t / p.stream_batch;
     const int slot = slot_local + p.slot_base;
     const int rank = slot % p.kvp;
     const int qrow = qc * 8 + row;
@@ -355,18 +372,29 @@ __global__ void attn_split_reduce_kernel(const AttnParams p, float* frag_o, floa
       }
 #pragma unroll
       for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
-      // pass 2: weighted sum in split order (deterministic), loads unrolled by 4
+      // pass 2: weighted sum in split order (deterministic); each batch of 8
+      // splits issues all its loads before accumulating
       float L = 0.f;
-      for (int s = 0; s < p.splits; ++s) {
-        const int pg0 = static_cast<int>((static_cast<long long>(s) * pages) / p.splits);
-        const int pg1 = static_cast<int>((static_cast<long long>(s + 1) * pages) / p.splits);
-        if (pg1 <= pg0) continue;
-        const size_t item = static_cast<size_t>(s) * p.n_streams + stream;
-        const float w = exp2f(p.part_lse2[item * 8 + row] - M);
-        const float* src = p.part_o + (item * 8 + row) * DP;
+      for (int s0 = 0; s0 < p.splits; s0 += 8) {
+        float w[8], v[8][PER];
 #pragma unroll
-        for (int i = 0; i < PER; ++i) o[i] += src[lane + 32 * i] * w;
-        L += w;
+        for (int j = 0; j < 8; ++j) {
+          const int s = s0 + j;
+          const int pg0 = static_cast<int>((static_cast<long long>(s) * pages) / p.splits);
+          const int pg1 = static_cast<int>((static_cast<long long>(s + 1) * pages) / p.splits);
+          const bool ok = s < p.splits && pg1 > pg0;
+          const size_t item = static_cast<size_t>(s) * p.n_streams + stream;
+          w[j] = ok ? p.part_lse2[item * 8 + row] : -INFINITY;
+#pragma unroll
+          for (int i = 0; i < PER; ++i) v[j][i] = ok ? p.part_o[(item * 8 + row) * DP + lane + 32 * i] : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const float e = w[j] == -INFINITY ? 0.f : exp2f(w[j] - M);
+#pragma unroll
+          for (int i = 0; i < PER; ++i) o[i] += v[j][i] * e;
+          L += e;
+        }
       }
       // fragment layout: [slot_local][b][q_in_group][DP]
       const int q_in_group = kvh * p.group + qrow;
@@ -379,6 +407,8 @@ __global__ void attn_split_reduce_kernel(const AttnParams p, float* frag_o, floa
 }
 
 __global__ void bump_totals_kernel(int* total, int n) {
+  griddep_wait();
+  griddep_launch_dependents();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) total[i] += 1;
 }
@@ -402,8 +432,7 @@ static cudaError_t launch_attn_t(const AttnParams& p, int grid, cudaStream_t str
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  attn_decode_kernel<DP, NWC, NSTAGE><<<grid, (NWC + 1) * 32, smem, stream>>>(p);
-  return cudaGetLastError();
+  return launch_k(attn_decode_kernel<DP, NWC, NSTAGE>, dim3(grid), dim3((NWC + 1) * 32), smem, stream, p);
 }
 
 cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t stream) {
@@ -421,18 +450,20 @@ cudaError_t launch_attn_split_reduce(const AttnParams& p, float* frag_o, float* 
   const int threads = 256;
   const int blocks = (warps * 32 + threads - 1) / threads;
   switch (p.dp) {
-    case 32: attn_split_reduce_kernel<32><<<blocks, threads, 0, stream>>>(p, frag_o, frag_lse); break;
-    case 64: attn_split_reduce_kernel<64><<<blocks, threads, 0, stream>>>(p, frag_o, frag_lse); break;
-    case 128: attn_split_reduce_kernel<128><<<blocks, threads, 0, stream>>>(p, frag_o, frag_lse); break;
+    case 32: return launch_k(attn_split_reduce_kernel<32>, dim3(blocks), dim3(threads), 0, stream, p, frag_o, frag_lse);
+    case 64: return launch_k(attn_split_reduce_kernel<64>, dim3(blocks), dim3(threads), 0, stream, p, frag_o, frag_lse);
+    case 128: return launch_k(attn_split_reduce_kernel<128>, dim3(blocks), dim3(threads), 0, stream, p, frag_o, frag_lse);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_bump_totals(int* total, int n, cudaStream_t stream) {
-  bump_totals_kernel<<<(n + 127) / 128, 128, 0, stream>>>(total, n);
-  return cudaGetLastError();
+  return launch_k(bump_totals_kernel, dim3((n + 127) / 128), dim3(128), 0, stream, total, n);
 }
+
+static bool g_pdl = true;
+void set_pdl(bool on) { g_pdl = on; }
+bool pdl_enabled() { return g_pdl; }
 
 size_t attn_decode_smem_bytes(int dp) {
   switch (dp) {

@@ -3,6 +3,7 @@
 #include <random>
 #include <string>
 
+#include "comm.h"
 #include "engine.h"
 
 struct hx_engine {
@@ -10,6 +11,10 @@ struct hx_engine {
 };
 struct hx_rng {
   std::mt19937_64 r;
+};
+struct hx_loopback {
+  explicit hx_loopback(int n) : hub(n) {}
+  hx::LoopbackHub hub;
 };
 
 namespace {
@@ -46,7 +51,9 @@ int hx_engine_create(const hx_model_config* m, const hx_parallel_config* p, cons
                      hx_engine** out) {
   return guard(nullptr, [&] {
     if (!m || !p || !r || !out) throw std::invalid_argument("null argument");
-    auto* e = new hx::Engine(*m, *p, *r);
+    hx_parallel_config par = *p;
+    if (par.loopback) par.loopback = reinterpret_cast<hx_loopback*>(&p->loopback->hub);  // engine sees the hub
+    auto* e = new hx::Engine(*m, par, *r);
     *out = new hx_engine{e};
   });
 }
@@ -144,10 +151,26 @@ int hx_clear_transcript(hx_engine* e) {
 }
 
 int hx_nccl_get_unique_id(void* out128) {
-  return guard(nullptr, [&] {
-    (void)out128;
-    throw hx::StateError("NCCL support is not compiled into this build");
-  });
+  return guard(nullptr, [&] { hx::nccl_get_unique_id(out128); });
 }
 
+int hx_loopback_create(int32_t n, hx_loopback** out) {
+  return guard(nullptr, [&] {
+    if (n < 1) throw std::invalid_argument("loopback group needs >= 1 rank");
+    *out = new hx_loopback(n);
+  });
+}
+void hx_loopback_destroy(hx_loopback* lb) { delete lb; }
+
+}  // extern "C"
+
+extern "C" {
+int64_t hx_exchange_layout(int64_t q_per_group, int64_t head_size, int64_t kvp, int64_t* out) {
+  int64_t chunk = -1;
+  guard(nullptr, [&] { chunk = hx::exchange_layout(q_per_group, head_size, kvp, out); });
+  return chunk;
+}
+int hx_engine_set_flag(hx_engine* e, int32_t flag, int32_t value) {
+  return guard(e, [&] { e->e->set_flag(flag, value); });
+}
 }  // extern "C"

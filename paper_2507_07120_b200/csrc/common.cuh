@@ -119,6 +119,13 @@ HX_DEV void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint6
       : "memory");
 }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// A kernel launched with programmatic stream serialization may start while the
+// previous kernel drains; it must griddep_wait() before touching anything the
+// previous kernel writes. No-ops for ordinary launches.
+HX_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+HX_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- RNG (== layer_oracle.hpp)
 HX_DEV uint64_t splitmix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;

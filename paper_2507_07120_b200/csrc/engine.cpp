@@ -6,9 +6,29 @@
 #include <cmath>
 #include <cstring>
 
+#include "comm.h"
 #include "kv_layout.cuh"
 
 namespace hx {
+
+int64_t exchange_layout(int64_t q_per_group, int64_t head_size, int64_t kvp, int64_t* out) {
+  if (q_per_group < 1 || head_size < 1 || kvp < 1) throw std::invalid_argument("layout dims must be >= 1");
+  const int64_t width = q_per_group * head_size;
+  if (width % kvp) throw std::invalid_argument("tpa*kvp must divide the hidden width");
+  const int64_t slice = width / kvp;
+  int64_t nh_max = 0;
+  for (int64_t p = 0; p < kvp; ++p) {
+    const int64_t first = p * slice / head_size, last = ((p + 1) * slice - 1) / head_size;
+    if (out) {
+      out[4 * p + 0] = p * slice;
+      out[4 * p + 1] = slice;
+      out[4 * p + 2] = first;
+      out[4 * p + 3] = last - first + 1;
+    }
+    nh_max = std::max(nh_max, last - first + 1);
+  }
+  return (slice + nh_max + 3) / 4 * 4;
+}
 
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
@@ -95,15 +115,38 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
     if (F_ < 16 || F_ % 16) throw std::invalid_argument("ffn_dim must be a positive multiple of 16");
     if (V_ < 1) throw std::invalid_argument("vocab must be >= 1");
   }
-  if (distributed_) throw StateError("distributed mode: use the NCCL build (not enabled in this engine)");
+  dist_mode_ = par.distributed;
+  if (dist_mode_ != HX_POOL_LOCAL && dist_mode_ != HX_POOL_NCCL && dist_mode_ != HX_POOL_LOOPBACK)
+    throw std::invalid_argument("unknown pool mode");
 
   DP_ = D_ <= 32 ? 32 : (D_ <= 64 ? 64 : 128);
   G_ = static_cast<int>(Qh_ / Kh_);
   q_chunks_ = (G_ + 7) / 8;
   kvh_per_slot_ = static_cast<int>(Kh_ / tpa_);
   q_per_slot_ = static_cast<int>(Qh_ / tpa_);
-  n_slots_ = tpa_ * kvp_;
-  slot_base_ = 0;
+  N_ = tpa_ * kvp_;
+  F_local_ = static_cast<int>(F_);
+  V_local_ = static_cast<int>(V_);
+  if (dist_mode_ == HX_POOL_LOCAL) {
+    n_slots_ = N_;
+    slot_base_ = 0;
+  } else {
+    // One rank (r, g) of the Helix pool: its KV shard, its group's QKV slice,
+    // its H/N slice of the exchange, 1/N of O-proj/FFN/LM head (latency.cpp:45-146).
+    if (rank_ < 0 || rank_ >= N_) throw std::invalid_argument("rank out of range for tpa*kvp");
+    grp_ = rank_ / kvp_;
+    r_ = rank_ % kvp_;
+    n_slots_ = 1;
+    slot_base_ = rank_;
+    slice_ = static_cast<int>(q_per_slot_ * D_ / kvp_);
+    if (slice_ % 16) throw std::invalid_argument("distributed Helix needs hidden/(tpa*kvp) to be a multiple of 16");
+    xchunk_ = static_cast<int>(exchange_layout(q_per_slot_, D_, kvp_, nullptr));
+    if (!attn_only_) {
+      if (F_ % N_ || (F_ / N_) % 16) throw std::invalid_argument("ffn_dim/(tpa*kvp) must be a multiple of 16");
+      F_local_ = static_cast<int>(F_ / N_);
+      V_local_ = static_cast<int>((V_ + N_ - 1) / N_);
+    }
+  }
   const int64_t per_rank_max = ((cap_ + static_cast<int64_t>(chunk_) * kvp_ - 1) /
                                 (static_cast<int64_t>(chunk_) * kvp_)) * chunk_;
   page_cap_ = static_cast<int>((per_rank_max + 15) / 16 + 1);
@@ -116,6 +159,19 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
     throw CudaError("device is not sm_100 class (Blackwell); this build targets sm_100a only");
   num_sms_ = prop.multiProcessorCount;
   cuda_check(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "cudaStreamCreate");
+  if (dist_mode_ == HX_POOL_NCCL) {
+    if (!par.nccl_unique_id) throw std::invalid_argument("NCCL pool needs nccl_unique_id");
+    transport_ = make_nccl_transport(par.nccl_unique_id, rank_, tpa_, kvp_);
+  } else if (dist_mode_ == HX_POOL_LOOPBACK) {
+    if (!par.loopback) throw std::invalid_argument("loopback pool needs a loopback group");
+    transport_ = make_loopback_transport(reinterpret_cast<LoopbackHub*>(par.loopback), rank_, tpa_, kvp_);
+    graphs_ = false;  // host barriers inside the collectives cannot be captured
+  }
+  if (dist_mode_ != HX_POOL_LOCAL) {
+    cuda_check(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "comm stream");
+    hop_events_.resize(static_cast<size_t>(B_) + 1);
+    for (auto& e : hop_events_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+  }
   alloc();
   plan_gemvs();
 }
@@ -133,7 +189,10 @@ Engine::~Engine() {
   f(w_lm_); f(emb_); f(d_total_); f(d_q_); f(d_part_o_); f(d_part_lse_); f(d_work_);
   f(d_frag_o_); f(d_frag_lse_); f(d_ypart_); f(d_counters_); f(d_x_); f(d_ss_); f(d_m_);
   f(d_logits_); f(d_best_); f(d_tokens_); f(d_next_); f(d_out_); f(d_out_lse_); f(d_hidden_);
-  f(d_segs_);
+  f(d_segs_); f(d_send_); f(d_recv_); f(d_parth_);
+  for (auto& e : hop_events_) cudaEventDestroy(e);
+  delete transport_;
+  if (comm_stream_) cudaStreamDestroy(comm_stream_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
@@ -154,15 +213,22 @@ void Engine::alloc() {
   for (int64_t l = 0; l < L_; ++l) kv_.push_back(dalloc<uint8_t>(pool, "kv pool"));
   d_total_ = dalloc<int>(static_cast<size_t>(L_) * B_, "totals");
   h_total_.assign(static_cast<size_t>(L_ * B_), 0);
-  d_q_ = dalloc<float>(static_cast<size_t>(B_) * Qh_ * DP_, "q");
+  const int qh_buf = dist_mode_ == HX_POOL_LOCAL ? static_cast<int>(Qh_) : q_per_slot_;
+  d_q_ = dalloc<float>(static_cast<size_t>(B_) * qh_buf * DP_, "q");
 
-  // attention work decomposition
-  n_streams_ = n_slots_ * B_ * kvh_per_slot_ * q_chunks_;
+  // attention work decomposition (per launch: all requests, or one request under HOP-B)
+  const int launch_batch = (hopb_ && dist_mode_ != HX_POOL_LOCAL) ? 1 : B_;
+  n_streams_ = n_slots_ * launch_batch * kvh_per_slot_ * q_chunks_;
   const int pages_max = page_cap_;
   const int target_items = num_sms_ * 8;
   splits_ = std::max(1, std::min((target_items + n_streams_ - 1) / n_streams_, std::max(1, pages_max / 8)));
   n_items_ = n_streams_ * splits_;
   attn_grid_ = std::min(num_sms_, n_items_);
+  if (dist_mode_ != HX_POOL_LOCAL) {
+    d_send_ = dalloc<float>(static_cast<size_t>(kvp_) * B_ * xchunk_, "exchange send");
+    d_recv_ = dalloc<float>(static_cast<size_t>(kvp_) * B_ * xchunk_, "exchange recv");
+    d_parth_ = dalloc<float>(static_cast<size_t>(B_) * H_, "tp partial");
+  }
   d_part_o_ = dalloc<float>(static_cast<size_t>(n_items_) * 8 * DP_, "part_o");
   d_part_lse_ = dalloc<float>(static_cast<size_t>(n_items_) * 8, "part_lse");
   d_work_ = dalloc<int>(4, "work counters");
@@ -187,12 +253,15 @@ void Engine::plan_gemvs() {
     p.K = K;
     p.batch = B_;
     // Each CTA streams a contiguous [128 rows x kr k-steps] weight range through
-    // its TMA ring: kr = 64 k-steps (256 KB) keeps x fragments <= 48 KB so two
-    // CTAs fit per SM; shrink kr until the grid covers >= 2 CTAs per SM.
+    // a 32 KB TMA ring; kr <= 32 k-steps keeps a CTA <= ~56 KB of shared memory
+    // so 4 co-reside per SM (one CTA's prologue/epilogue latency overlaps the
+    // others' streams). Shrink kr until the grid covers >= 4 CTAs per SM.
     const int kst = K / 16;
     const int nblk = Npad / 128;
-    int kr = std::min(64, kst);
-    while (kr > 16 && static_cast<int64_t>(nblk) * ((kst + kr - 1) / kr) < 2 * num_sms_) kr /= 2;
+    int kr = std::min(32, kst);
+    while (kr > 8 && static_cast<int64_t>(nblk) * ((kst + kr - 1) / kr) < 4 * num_sms_) kr /= 2;
+    if (xm == X_MERGE || xm == X_RECV)  // (request, head) pairs per CTA fit the prologue's shared table
+      while (kr > 1 && (kr * 16 / D_ + 2) * B_ > 256) kr /= 2;
     const int ksplit = (kst + kr - 1) / kr;
     p.ksplit = ksplit;
     p.kr_steps = kr;
@@ -207,46 +276,76 @@ void Engine::plan_gemvs() {
     max_counters_ = std::max(max_counters_, nblk);
     return g;
   };
-  const int nq = static_cast<int>(Qh_ * D_), nk = static_cast<int>(Kh_ * D_);
+  const bool dist = dist_mode_ != HX_POOL_LOCAL;
+  const int nq = static_cast<int>((dist ? q_per_slot_ : Qh_) * D_);
+  const int nk = static_cast<int>((dist ? kvh_per_slot_ : Kh_) * D_);
   const int Nqkv = nq + 2 * nk;
   const int Hh = static_cast<int>(H_);
+  const int F = F_local_;
   for (int64_t l = 0; l < L_; ++l) {
     GemvPlan q = make(Nqkv, round_up(Nqkv, 128), Hh, attn_only_ ? X_PLAIN : X_NORM, E_QKV);
     q.p.nq = nq;
     q.p.nk = nk;
-    q.p.kv_heads = static_cast<int>(Kh_);
+    q.p.kv_heads = nk / static_cast<int>(D_);
+    q.p.kv_head_base = dist ? grp_ * kvh_per_slot_ : 0;
     q.p.kvh_per_slot = kvh_per_slot_;
-    q.p.chunk = chunk_;
+    q.p.rr_chunk = chunk_;
     q.p.page_cap = page_cap_;
     q.p.slot_base = slot_base_;
     q.p.n_local_slots = n_slots_;
     q.p.append = 1;
     plan_qkv_.push_back(q);
     if (!attn_only_) {
-      plan_o_.push_back(make(Hh, round_up(Hh, 128), Hh, X_MERGE, E_RESID));
-      const int F = static_cast<int>(F_);
-      plan_gu_.push_back(make(2 * F, round_up(F, 64) * 2, Hh, X_NORM, E_SWIGLU));
-      plan_down_.push_back(make(Hh, round_up(Hh, 128), F, X_PLAIN, E_RESID));
+      if (dist) {
+        // O-proj: this rank's exchanged slice of its group's heads x its rows of W_O
+        GemvPlan o = make(Hh, round_up(Hh, 128), slice_, X_RECV, E_STORE);
+        o.p.chunk = xchunk_;
+        o.p.slice = slice_;
+        o.p.exch_rank = r_;
+        plan_o_.push_back(o);
+        plan_gu_.push_back(make(2 * F, round_up(F, 64) * 2, Hh, X_NORM, E_SWIGLU));
+        plan_down_.push_back(make(Hh, round_up(Hh, 128), F, X_PLAIN, E_STORE));
+      } else {
+        plan_o_.push_back(make(Hh, round_up(Hh, 128), Hh, X_MERGE, E_RESID));
+        plan_gu_.push_back(make(2 * F, round_up(F, 64) * 2, Hh, X_NORM, E_SWIGLU));
+        plan_down_.push_back(make(Hh, round_up(Hh, 128), F, X_PLAIN, E_RESID));
+      }
     }
   }
-  if (!attn_only_) plan_lm_ = make(static_cast<int>(V_), round_up(V_, 128), Hh, X_NORM, E_LOGITS);
+  if (!attn_only_) {
+    plan_lm_ = make(V_local_, round_up(V_local_, 128), Hh, X_NORM, E_LOGITS);
+    plan_lm_.p.n_offset = dist ? rank_ * V_local_ : 0;
+  }
 
   d_ypart_ = dalloc<float>(ypart_elems_, "ypart");
   d_counters_ = dalloc<int>(static_cast<size_t>(max_counters_), "counters");
   const int hblk = round_up(Hh, 128) / 128;
   d_ss_ = dalloc<float>(static_cast<size_t>(std::max(hblk, 1)) * B_, "ss");
   if (!attn_only_) {
-    d_m_ = dalloc<float>(static_cast<size_t>(B_) * F_, "m");
-    d_logits_ = dalloc<float>(static_cast<size_t>(B_) * V_, "logits");
+    d_m_ = dalloc<float>(static_cast<size_t>(B_) * F_local_, "m");
+    d_logits_ = dalloc<float>(static_cast<size_t>(B_) * V_local_, "logits");
     d_hidden_ = dalloc<float>(static_cast<size_t>(L_ + 1) * B_ * H_, "hidden");
   }
-  kernels_per_step_ = attn_only_ ? 5 : 1 + 7 * L_ + 2;
+  if (attn_only_)
+    kernels_per_step_ = 5;
+  else if (!dist)
+    kernels_per_step_ = 1 + 7 * L_ + 2;
+  else  // + pack and two residual adds per layer (per-request attention launches under HOP-B)
+    kernels_per_step_ = 1 + L_ * (7 + 3 + (hopb_ ? 3 * (B_ - 1) : 0)) + 2;
 }
 
 // ---------------------------------------------------------------------------
 void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
+  const bool dist = dist_mode_ != HX_POOL_LOCAL;
   const int Hh = static_cast<int>(H_);
-  const int nq = static_cast<int>(Qh_ * D_), nk = static_cast<int>(Kh_ * D_);
+  const int Dd = static_cast<int>(D_);
+  // columns of W_q / W_k / W_v held here (all, or this rank's TPA group's heads)
+  const int nq = static_cast<int>((dist ? q_per_slot_ : Qh_) * D_);
+  const int nk = static_cast<int>((dist ? kvh_per_slot_ : Kh_) * D_);
+  const int q0 = dist ? grp_ * nq : 0, k0 = dist ? grp_ * nk : 0;
+  const int F = F_local_, f0 = dist ? rank_ * F_local_ : 0;
+  const int v0 = dist ? rank_ * V_local_ : 0;
+  const int vrows = static_cast<int>(std::min<int64_t>(V_local_, V_ - v0));
   auto walloc = [&](const GemvPlan& g) {
     return dalloc<uint4>(static_cast<size_t>(g.p.Npad) * g.p.K / 8, "weights");
   };
@@ -257,31 +356,32 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
                                        stream_), "weight init");
     cuda_check(cudaStreamSynchronize(stream_), "weight init sync");
   };
+  // WSeg: {stream, rows_begin, rows_end, cols_total, col_offset, interleave, scale, k_offset, col_limit}
   const double sh = 1.0 / std::sqrt(static_cast<double>(H_));
+  const double sf = 1.0 / std::sqrt(static_cast<double>(F_));
+  const int Qall = static_cast<int>(Qh_ * D_), Kall = static_cast<int>(Kh_ * D_);
   for (int64_t l = 0; l < L_; ++l) {
     if (w_qkv_.size() <= static_cast<size_t>(l)) w_qkv_.push_back(walloc(plan_qkv_[l]));
     if (qkv_hash) {
-      std::vector<WSeg> segs = {
-          {hash_stream(kWq, l), 0, nq, nq, 0, 0, 1.0},
-          {hash_stream(kWk, l), nq, nq + nk, nk, 0, 0, 1.0},
-          {hash_stream(kWv, l), nq + nk, nq + 2 * nk, nk, 0, 0, 1.0},
-      };
-      init(w_qkv_[l], plan_qkv_[l], segs);
+      init(w_qkv_[l], plan_qkv_[l],
+           {{hash_stream(kWq, l), 0, nq, Qall, q0, 0, 1.0, 0, 0},
+            {hash_stream(kWk, l), nq, nq + nk, Kall, k0, 0, 1.0, 0, 0},
+            {hash_stream(kWv, l), nq + nk, nq + 2 * nk, Kall, k0, 0, 1.0, 0, 0}});
     }
     plan_qkv_[l].p.w = w_qkv_[l];
     if (!attn_only_) {
-      const int F = static_cast<int>(F_);
       if (w_o_.size() <= static_cast<size_t>(l)) {
         w_o_.push_back(walloc(plan_o_[l]));
         w_gu_.push_back(walloc(plan_gu_[l]));
         w_down_.push_back(walloc(plan_down_[l]));
       }
-      init(w_o_[l], plan_o_[l], {{hash_stream(kWo, l), 0, Hh, Hh, 0, 0, sh}});
+      // O-proj input rows: this rank's slice of its group's flattened heads
+      const int ko = dist ? grp_ * q_per_slot_ * Dd + r_ * slice_ : 0;
+      init(w_o_[l], plan_o_[l], {{hash_stream(kWo, l), 0, Hh, Hh, 0, 0, sh, ko, 0}});
       init(w_gu_[l], plan_gu_[l],
-           {{hash_stream(kWgate, l), 0, plan_gu_[l].p.Npad, F, 0, 1, sh},
-            {hash_stream(kWup, l), 0, plan_gu_[l].p.Npad, F, 0, 2, sh}});
-      init(w_down_[l], plan_down_[l],
-           {{hash_stream(kWdown, l), 0, Hh, Hh, 0, 0, 1.0 / std::sqrt(static_cast<double>(F_))}});
+           {{hash_stream(kWgate, l), 0, plan_gu_[l].p.Npad, static_cast<int>(F_), f0, 1, sh, 0, f0 + F},
+            {hash_stream(kWup, l), 0, plan_gu_[l].p.Npad, static_cast<int>(F_), f0, 2, sh, 0, f0 + F}});
+      init(w_down_[l], plan_down_[l], {{hash_stream(kWdown, l), 0, Hh, Hh, 0, 0, sf, f0, 0}});
       plan_o_[l].p.w = w_o_[l];
       plan_gu_[l].p.w = w_gu_[l];
       plan_down_[l].p.w = w_down_[l];
@@ -289,7 +389,7 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
   }
   if (!attn_only_) {
     if (!w_lm_) w_lm_ = walloc(plan_lm_);
-    init(w_lm_, plan_lm_, {{hash_stream(kLm, 0), 0, static_cast<int>(V_), static_cast<int>(V_), 0, 0, sh}});
+    init(w_lm_, plan_lm_, {{hash_stream(kLm, 0), 0, vrows, static_cast<int>(V_), v0, 0, sh, 0, 0}});
     plan_lm_.p.w = w_lm_;
     if (!emb_) emb_ = dalloc<uint16_t>(static_cast<size_t>(V_) * H_, "embedding");
     cuda_check(launch_emb_init_hash(emb_, static_cast<int>(V_), Hh, seed, hash_stream(kEmb, 0), stream_),
@@ -297,6 +397,7 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
     cuda_check(cudaStreamSynchronize(stream_), "emb init sync");
   }
   // wire the remaining pointers of every plan
+  const int hblk = round_up(Hh, 128) / 128;
   for (int64_t l = 0; l < L_; ++l) {
     GemvParams& q = plan_qkv_[l].p;
     q.ypart = d_ypart_;
@@ -307,34 +408,34 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
     q.x = d_x_;
     q.x_stride = static_cast<int>(H_);
     q.ss_part = d_ss_;
-    q.n_ss = 1;  // set per use
+    q.n_ss = l == 0 ? 1 : hblk;  // embedding writes one block; residual writers write hblk
     if (!attn_only_) {
       GemvParams& o = plan_o_[l].p;
       o.ypart = d_ypart_;
       o.counters = d_counters_;
       o.frag_o = d_frag_o_;
       o.frag_lse = d_frag_lse_;
-      o.out = d_x_;
+      o.recv = d_recv_;
+      o.out = dist ? d_parth_ : d_x_;
       o.out_stride = static_cast<int>(H_);
-      o.ss_out = d_ss_;
+      o.ss_out = dist ? nullptr : d_ss_;
       GemvParams& gu = plan_gu_[l].p;
       gu.ypart = d_ypart_;
       gu.counters = d_counters_;
       gu.x = d_x_;
       gu.x_stride = static_cast<int>(H_);
       gu.ss_part = d_ss_;
-      gu.n_ss = plan_o_[l].p.Npad / 128;
+      gu.n_ss = hblk;
       gu.out = d_m_;
-      gu.out_stride = static_cast<int>(F_);
+      gu.out_stride = F;
       GemvParams& dn = plan_down_[l].p;
       dn.ypart = d_ypart_;
       dn.counters = d_counters_;
       dn.x = d_m_;
-      dn.x_stride = static_cast<int>(F_);
-      dn.out = d_x_;
+      dn.x_stride = F;
+      dn.out = dist ? d_parth_ : d_x_;
       dn.out_stride = static_cast<int>(H_);
-      dn.ss_out = d_ss_;
-      q.n_ss = l == 0 ? 1 : plan_down_[l - 1].p.Npad / 128;
+      dn.ss_out = dist ? nullptr : d_ss_;
     }
   }
   if (!attn_only_) {
@@ -344,10 +445,10 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
     lm.x = d_x_;
     lm.x_stride = static_cast<int>(H_);
     lm.ss_part = d_ss_;
-    lm.n_ss = plan_down_[L_ - 1].p.Npad / 128;
+    lm.n_ss = hblk;
     lm.best = d_best_;
     lm.out = nullptr;
-    lm.out_stride = static_cast<int>(V_);
+    lm.out_stride = V_local_;
   }
   weights_ready_ = true;
   drop_graphs();
@@ -385,17 +486,23 @@ void Engine::init_weights_mt19937(uint64_t seed) {
 
 void Engine::upload_qkv_host(int64_t layer, const std::vector<double>& wq, const std::vector<double>& wk,
                              const std::vector<double>& wv) {
+  // wq [H x Q*Hsz], wk/wv [H x K*Hsz] row-major (reference orientation); this
+  // device keeps all columns (local pool) or its TPA group's heads.
+  const bool dist = dist_mode_ != HX_POOL_LOCAL;
   const GemvPlan& g = plan_qkv_[layer];
   const int K = g.p.K, kst = K / 16;
-  const int nq = static_cast<int>(Qh_ * D_), nk = static_cast<int>(Kh_ * D_);
+  const int Qall = static_cast<int>(Qh_ * D_), Kall = static_cast<int>(Kh_ * D_);
+  const int nq = g.p.nq, nk = g.p.nk;
+  const int q0 = dist ? grp_ * nq : 0, k0 = dist ? grp_ * nk : 0;
   std::vector<uint16_t> img(static_cast<size_t>(g.p.Npad) * K, 0);
   for (int k = 0; k < K; ++k) {
     for (int n = 0; n < nq; ++n)
-      img[wfrag_offset_host(n, k, kst) / 2] = bf16_bits_from_double(wq[static_cast<size_t>(k) * nq + n]);
+      img[wfrag_offset_host(n, k, kst) / 2] = bf16_bits_from_double(wq[static_cast<size_t>(k) * Qall + q0 + n]);
     for (int n = 0; n < nk; ++n) {
-      img[wfrag_offset_host(nq + n, k, kst) / 2] = bf16_bits_from_double(wk[static_cast<size_t>(k) * nk + n]);
+      img[wfrag_offset_host(nq + n, k, kst) / 2] =
+          bf16_bits_from_double(wk[static_cast<size_t>(k) * Kall + k0 + n]);
       img[wfrag_offset_host(nq + nk + n, k, kst) / 2] =
-          bf16_bits_from_double(wv[static_cast<size_t>(k) * nk + n]);
+          bf16_bits_from_double(wv[static_cast<size_t>(k) * Kall + k0 + n]);
     }
   }
   cuda_check(cudaMemcpy(w_qkv_[layer], img.data(), img.size() * 2, cudaMemcpyHostToDevice), "qkv upload");
@@ -550,14 +657,7 @@ void Engine::record_transcript(int64_t layers) {
     }
 }
 
-void Engine::enqueue_attention(int64_t layer, int qkv_xmode, const float* x, int x_stride) {
-  // 1. QKV projection with fused round-robin append of this token's K/V
-  GemvPlan q = plan_qkv_[layer];
-  q.p.x = x;
-  q.p.x_stride = x_stride;
-  cuda_check(launch_gemv(q.p, qkv_xmode, E_QKV, stream_), "qkv gemv");
-  mark(1);
-  // 2. flash-decode partials over every local rank's shard (attend BEFORE append)
+AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) const {
   AttnParams a{};
   a.kv = kv_[layer];
   a.q = d_q_;
@@ -568,7 +668,8 @@ void Engine::enqueue_attention(int64_t layer, int qkv_xmode, const float* x, int
   a.done_counter = d_work_ + 1;
   a.dp = DP_;
   a.batch = B_;
-  a.q_heads = static_cast<int>(Qh_);
+  a.q_heads = dist_mode_ == HX_POOL_LOCAL ? static_cast<int>(Qh_) : q_per_slot_;
+  a.q_grp_base = dist_mode_ == HX_POOL_LOCAL ? 0 : grp_;
   a.group = G_;
   a.q_chunks = q_chunks_;
   a.kvh_per_slot = kvh_per_slot_;
@@ -578,16 +679,76 @@ void Engine::enqueue_attention(int64_t layer, int qkv_xmode, const float* x, int
   a.page_cap = page_cap_;
   a.slot_base = slot_base_;
   a.n_local_slots = n_slots_;
-  a.n_streams = n_streams_;
+  a.b_begin = b_begin;
+  a.stream_batch = b_count;
+  a.n_streams = n_slots_ * b_count * kvh_per_slot_ * q_chunks_;
   a.splits = splits_;
-  a.n_items = n_items_;
+  a.n_items = a.n_streams * splits_;
   a.qscale = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D_)));
+  return a;
+}
+
+void Engine::enqueue_attention(int64_t layer, int qkv_xmode, const float* x, int x_stride) {
+  // 1. QKV projection with fused round-robin append of this token's K/V
+  GemvPlan q = plan_qkv_[layer];
+  q.p.x = x;
+  q.p.x_stride = x_stride;
+  cuda_check(launch_gemv(q.p, qkv_xmode, E_QKV, stream_), "qkv gemv");
+  mark(1);
+  if (dist_mode_ != HX_POOL_LOCAL) {
+    enqueue_exchange_and_attention_dist(layer);
+    return;
+  }
+  // 2. flash-decode partials over every local rank's shard (attend BEFORE append)
+  const AttnParams a = attn_params(layer, 0, B_);
   cuda_check(launch_attn_decode(a, attn_grid_, stream_), "attention");
   mark(2);
   // 3. per-rank fragments (split merge), then bump the totals (append is now visible)
   cuda_check(launch_attn_split_reduce(a, d_frag_o_, d_frag_lse_, stream_), "split reduce");
   cuda_check(launch_bump_totals(d_total_ + layer * B_, B_, stream_), "bump totals");
   mark(3);
+}
+
+// One rank of the pool: attention over its own KV shard, pack the fragment
+// into per-peer slices, all-to-all inside the KVP group (attention.hpp:492-502).
+// HOP-B (overlap.hpp:37-69): request b's exchange runs on the comm stream while
+// request b+1's attention runs on the compute stream.
+void Engine::enqueue_exchange_and_attention_dist(int64_t layer) {
+  const size_t stride = static_cast<size_t>(B_) * xchunk_;
+  const int rounds = hopb_ ? B_ : 1;
+  const int per = hopb_ ? 1 : B_;
+  const bool side_stream = hopb_ && dist_mode_ == HX_POOL_NCCL;
+  for (int i = 0; i < rounds; ++i) {
+    const int b0 = i * per;
+    const AttnParams a = attn_params(layer, b0, per);
+    cuda_check(launch_attn_decode(a, std::min(attn_grid_, a.n_items), stream_), "attention");
+    mark(2);
+    cuda_check(launch_attn_split_reduce(a, d_frag_o_, d_frag_lse_, stream_), "split reduce");
+    cuda_check(launch_pack_exchange(d_frag_o_, d_frag_lse_, b0, per, B_, q_per_slot_, static_cast<int>(D_), DP_,
+                                    kvp_, slice_, xchunk_, d_send_, stream_),
+               "pack");
+    mark(3);
+    float* send = d_send_ + static_cast<size_t>(b0) * xchunk_;
+    float* recv = d_recv_ + static_cast<size_t>(b0) * xchunk_;
+    const size_t count = static_cast<size_t>(per) * xchunk_;
+    if (skip_comm_) {  // measurement: keep only this rank's own block, no wire traffic
+      cuda_check(cudaMemcpyAsync(recv + static_cast<size_t>(r_) * stride, send + static_cast<size_t>(r_) * stride,
+                                 count * sizeof(float), cudaMemcpyDeviceToDevice, stream_),
+                 "skip-comm copy");
+    } else if (side_stream) {
+      cuda_check(cudaEventRecord(hop_events_[static_cast<size_t>(i)], stream_), "hopb event");
+      cuda_check(cudaStreamWaitEvent(comm_stream_, hop_events_[static_cast<size_t>(i)], 0), "hopb wait");
+      transport_->all_to_all(send, recv, count, stride, comm_stream_);
+    } else {
+      transport_->all_to_all(send, recv, count, stride, stream_);
+    }
+  }
+  if (side_stream && !skip_comm_) {
+    cuda_check(cudaEventRecord(hop_events_.back(), comm_stream_), "hopb join");
+    cuda_check(cudaStreamWaitEvent(stream_, hop_events_.back(), 0), "hopb join wait");
+  }
+  cuda_check(launch_bump_totals(d_total_ + layer * B_, B_, stream_), "bump totals");
+  mark(9);
 }
 
 void Engine::harness_step(int64_t layer, const float* x_host, int64_t x_len, float* out, float* lse) {
@@ -608,6 +769,8 @@ void Engine::harness_step(int64_t layer, const float* x_host, int64_t x_len, flo
 
 void Engine::harness_step_device(int64_t layer, const float* x_dev, float* out_dev) {
   check_layer(layer);
+  if (dist_mode_ != HX_POOL_LOCAL)
+    throw StateError("the attention-only harness runs on a local pool; distributed pools use decode_step");
   if (!weights_ready_) throw StateError("weights are not initialised");
   require_context(layer);
   enqueue_attention(layer, X_PLAIN, x_dev, static_cast<int>(H_));
@@ -625,14 +788,32 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
   if (capture_hidden_)
     cuda_check(cudaMemcpyAsync(d_hidden_, d_x_, static_cast<size_t>(B_) * H_ * 4, cudaMemcpyDeviceToDevice, stream_),
                "hidden");
+  const bool dist = dist_mode_ != HX_POOL_LOCAL;
   for (int64_t l = 0; l < L_; ++l) {
     enqueue_attention(l, X_NORM, d_x_, static_cast<int>(H_));
-    cuda_check(launch_gemv(plan_o_[l].p, X_MERGE, E_RESID, stream_), "o-proj");
-    mark(4);
-    cuda_check(launch_gemv(plan_gu_[l].p, X_NORM, E_SWIGLU, stream_), "gate/up");
-    mark(5);
-    cuda_check(launch_gemv(plan_down_[l].p, X_PLAIN, E_RESID, stream_), "down");
-    mark(6);
+    if (!dist) {
+      cuda_check(launch_gemv(plan_o_[l].p, X_MERGE, E_RESID, stream_), "o-proj");
+      mark(4);
+      cuda_check(launch_gemv(plan_gu_[l].p, X_NORM, E_SWIGLU, stream_), "gate/up");
+      mark(5);
+      cuda_check(launch_gemv(plan_down_[l].p, X_PLAIN, E_RESID, stream_), "down");
+      mark(6);
+    } else {
+      // TP O-proj over this rank's exchanged slice, AllReduce over the pool (latency.cpp:85-94)
+      cuda_check(launch_gemv(plan_o_[l].p, X_RECV, E_STORE, stream_), "o-proj");
+      mark(4);
+      if (!skip_comm_) transport_->all_reduce_sum(d_parth_, static_cast<size_t>(B_) * H_, stream_);
+      cuda_check(launch_residual_add(d_x_, d_parth_, B_, static_cast<int>(H_), d_ss_, stream_), "residual");
+      mark(9);
+      // TP FFN over F/N features, AllReduce (latency.cpp:138-144)
+      cuda_check(launch_gemv(plan_gu_[l].p, X_NORM, E_SWIGLU, stream_), "gate/up");
+      mark(5);
+      cuda_check(launch_gemv(plan_down_[l].p, X_PLAIN, E_STORE, stream_), "down");
+      mark(6);
+      if (!skip_comm_) transport_->all_reduce_sum(d_parth_, static_cast<size_t>(B_) * H_, stream_);
+      cuda_check(launch_residual_add(d_x_, d_parth_, B_, static_cast<int>(H_), d_ss_, stream_), "residual");
+      mark(9);
+    }
     if (capture_hidden_)
       cuda_check(cudaMemcpyAsync(d_hidden_ + (l + 1) * B_ * H_, d_x_, static_cast<size_t>(B_) * H_ * 4,
                                  cudaMemcpyDeviceToDevice, stream_),
@@ -641,6 +822,7 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
   GemvParams lm = plan_lm_.p;
   lm.out = store_logits_ ? d_logits_ : nullptr;
   cuda_check(launch_gemv(lm, X_NORM, E_LOGITS, stream_), "lm head");
+  if (dist && !skip_comm_) transport_->all_reduce_max_u64(d_best_, static_cast<size_t>(B_), stream_);  // vocab-sharded argmax
   cuda_check(launch_argmax_finish(d_best_, B_, next_dev, d_best_, stream_), "argmax");
   mark(7);
 }
@@ -684,7 +866,8 @@ void Engine::decode_step(const int32_t* tokens, int32_t* next, float* logits, fl
   cuda_check(cudaMemcpyAsync(next, d_next_, static_cast<size_t>(B_) * 4, cudaMemcpyDeviceToHost, stream_),
              "next d2h");
   if (logits)
-    cuda_check(cudaMemcpyAsync(logits, d_logits_, static_cast<size_t>(B_) * V_ * 4, cudaMemcpyDeviceToHost, stream_),
+    cuda_check(cudaMemcpyAsync(logits, d_logits_, static_cast<size_t>(B_) * V_local_ * 4, cudaMemcpyDeviceToHost,
+                               stream_),
                "logits d2h");
   if (hidden)
     cuda_check(cudaMemcpyAsync(hidden, d_hidden_, static_cast<size_t>(L_ + 1) * B_ * H_ * 4,
@@ -693,11 +876,20 @@ void Engine::decode_step(const int32_t* tokens, int32_t* next, float* logits, fl
   cuda_check(cudaStreamSynchronize(stream_), "decode sync");
 }
 
+void Engine::set_flag(int flag, int value) {
+  if (flag == HX_FLAG_SKIP_COMM) {
+    skip_comm_ = value != 0;
+    drop_graphs();
+  } else {
+    throw std::invalid_argument("unknown engine flag");
+  }
+}
+
 void Engine::synchronize() { cuda_check(cudaStreamSynchronize(stream_), "synchronize"); }
 
 void Engine::profile_step(int64_t reps, double* ms) {
   if (!weights_ready_) throw StateError("weights are not initialised");
-  for (int k = 0; k < 9; ++k) ms[k] = 0.0;
+  for (int k = 0; k < 10; ++k) ms[k] = 0.0;
   std::vector<std::pair<int, cudaEvent_t>> evs;
   for (int64_t r = 0; r < reps; ++r) {
     evs.clear();
@@ -718,7 +910,7 @@ void Engine::profile_step(int64_t reps, double* ms) {
     for (size_t i = 1; i < evs.size(); ++i) {
       float t = 0.f;
       cuda_check(cudaEventElapsedTime(&t, evs[i - 1].second, evs[i].second), "elapsed");
-      if (evs[i].first >= 0 && evs[i].first < 9) ms[evs[i].first] += t / static_cast<double>(reps);
+      if (evs[i].first >= 0 && evs[i].first < 10) ms[evs[i].first] += t / static_cast<double>(reps);
     }
     for (auto& e : evs) cudaEventDestroy(e.second);
   }

@@ -26,6 +26,11 @@ struct StateError : std::runtime_error {
 
 void cuda_check(cudaError_t e, const char* what);
 
+// Fragment-exchange layout (attention.hpp:492-502): per destination KVP rank p,
+// out[4p..] = {first element, slice, first head, heads touched}; returns the
+// padded chunk (floats per peer and request: slice + lse slots).
+int64_t exchange_layout(int64_t q_per_group, int64_t head_size, int64_t kvp, int64_t* out);
+
 struct Message {
   int64_t kind, src, dst, payload, lse;
 };
@@ -35,7 +40,8 @@ struct GemvPlan {
   int xmode = 0, emode = 0;
 };
 
-class Comm;  // NCCL plumbing (distributed mode)
+class Transport;
+class LoopbackHub;
 
 class Engine {
  public:
@@ -62,6 +68,7 @@ class Engine {
   void profile_step(int64_t reps, double* ms);
   cudaStream_t stream() const { return stream_; }
   void info(hx_engine_info* out) const;
+  void set_flag(int flag, int value);
 
   const std::vector<Message>& transcript() const { return transcript_; }
   void clear_transcript() { transcript_.clear(); }
@@ -148,7 +155,22 @@ class Engine {
   std::vector<std::pair<int, cudaEvent_t>>* prof_ = nullptr;
 
   std::vector<Message> transcript_;
-  Comm* comm_ = nullptr;
+
+  // ---- distributed pool (one rank of tpa*kvp; comm.h)
+  int dist_mode_ = 0;          // HX_POOL_LOCAL / NCCL / LOOPBACK
+  bool skip_comm_ = false;     // HX_FLAG_SKIP_COMM (measurement only)
+  int grp_ = 0, r_ = 0, N_ = 1;
+  int slice_ = 0, xchunk_ = 0; // exchanged elements per (peer, request) and padded chunk (+ lse slots)
+  int F_local_ = 0, V_local_ = 0;
+  Transport* transport_ = nullptr;
+  float* d_send_ = nullptr;
+  float* d_recv_ = nullptr;
+  float* d_parth_ = nullptr;   // [B][H] partial products before the TP AllReduce
+  cudaStream_t comm_stream_ = nullptr;
+  std::vector<cudaEvent_t> hop_events_;
+  void enqueue_exchange_and_attention_dist(int64_t layer);
+  void init_dist_weights(uint64_t seed, bool qkv_hash);
+  AttnParams attn_params(int64_t layer, int b_begin, int b_count) const;
 };
 
 }  // namespace hx

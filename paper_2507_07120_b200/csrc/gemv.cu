@@ -29,8 +29,8 @@ namespace {
 
 constexpr int kRows = 128;        // rows (output features) per CTA: 8 consumer warps x 16
 constexpr int kThreads = 256;     // consumer threads (+1 producer warp)
-constexpr int kStageSteps = 4;    // k-steps per ring stage (4 x 4 KB)
-constexpr int kStages = 4;        // ring depth: 64 KB of weights in flight per CTA
+constexpr int kStageSteps = 2;    // k-steps per ring stage (2 x 4 KB)
+constexpr int kStages = 4;        // ring depth: 32 KB in flight per CTA, 4 CTAs per SM
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -42,50 +42,103 @@ __device__ __forceinline__ unsigned long long logit_key(float v, int n) {
   return (static_cast<unsigned long long>(u) << 32) | (0xFFFFFFFFu - static_cast<unsigned>(n));
 }
 
-// Merged attention output element (KVP fragment combine, attention.hpp:118-137):
-// canonical order = descending lse, ties broken by source rank.
-__device__ float merge_elem(const GemvParams& p, int b, int k) {
-  const int head = k / p.head_dim, d = k - head * p.head_dim;
+// KVP fragment combine (attention.hpp:118-137) for the O-projection prologue,
+// in two phases so each is one latency round trip:
+//  merge_weights: per (request, head) covered by this CTA's k-range, the
+//    canonical order (descending lse, ties by rank; attention.hpp:90-102),
+//    w_r = exp(lse_r - m) and z = sum w_r, into shared memory;
+//  merge_elem: (sum_r w_r * o_r in that order) / z.
+constexpr int kMaxKr = 32;          // k-steps per CTA (engine plan guarantees)
+constexpr int kMaxMergePairs = 256; // (request, head) pairs per CTA (engine plan guarantees)
+struct MergeSmem {
+  float w[kMaxMergePairs][8];
+  float z[kMaxMergePairs];
+  int ord[kMaxMergePairs][8];
+};
+
+// Flattened index of column k inside the merged attention output:
+// X_MERGE: k is a global hidden index; X_RECV: k is an offset into this rank's
+// exchanged slice r*slice .. of its group's flattened (heads x head_dim) block.
+template <int XM>
+__device__ __forceinline__ int merge_flat(const GemvParams& p, int k) {
+  return XM == X_RECV ? p.exch_rank * p.slice + k : k;
+}
+template <int XM>
+__device__ __forceinline__ int merge_nh(const GemvParams& p, int ks0, int nks) {
+  return merge_flat<XM>(p, (ks0 + nks) * 16 - 1) / p.head_dim - merge_flat<XM>(p, ks0 * 16) / p.head_dim + 1;
+}
+template <int XM>
+__device__ __forceinline__ float merge_lse(const GemvParams& p, int r, int b, int head) {
+  if (XM == X_RECV) {
+    const int first = (p.exch_rank * p.slice) / p.head_dim;
+    return p.recv[(static_cast<size_t>(r) * p.batch + b) * p.chunk + p.slice + head - first];
+  }
   const int grp = head / p.q_per_slot, qi = head - grp * p.q_per_slot;
-  float lse[8];
-  int ord[8];
-  const int kvp = p.kvp;
-  for (int r = 0; r < kvp; ++r) {
-    const int slot = grp * kvp + r;
-    lse[r] = p.frag_lse[(static_cast<size_t>(slot) * p.batch + b) * p.q_per_slot + qi];
-    ord[r] = r;
-  }
-  for (int i = 1; i < kvp; ++i) {  // insertion sort: lse desc, rank asc
-    const int o = ord[i];
-    int j = i - 1;
-    while (j >= 0 && lse[ord[j]] < lse[o]) {
-      ord[j + 1] = ord[j];
-      --j;
+  return p.frag_lse[(static_cast<size_t>(grp * p.kvp + r) * p.batch + b) * p.q_per_slot + qi];
+}
+template <int XM>
+__device__ __forceinline__ float merge_o(const GemvParams& p, int r, int b, int k, int head, int d) {
+  if (XM == X_RECV) return p.recv[(static_cast<size_t>(r) * p.batch + b) * p.chunk + k];
+  const int grp = head / p.q_per_slot, qi = head - grp * p.q_per_slot;
+  return p.frag_o[((static_cast<size_t>(grp * p.kvp + r) * p.batch + b) * p.q_per_slot + qi) * p.dp + d];
+}
+
+template <int XM>
+__device__ void merge_weights(const GemvParams& p, int ks0, int nks, MergeSmem* ms) {
+  const int h0 = merge_flat<XM>(p, ks0 * 16) / p.head_dim;
+  const int nh = merge_nh<XM>(p, ks0, nks);
+  for (int pr = threadIdx.x; pr < nh * p.batch; pr += 256) {
+    const int b = pr / nh, head = h0 + pr % nh;
+    float lse[8];
+    int ord[8];
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      lse[r] = r < p.kvp ? merge_lse<XM>(p, r, b, head) : -INFINITY;
+      ord[r] = r;
     }
-    ord[j + 1] = o;
+    for (int i = 1; i < p.kvp; ++i) {  // insertion sort: lse desc, rank asc
+      const int o = ord[i];
+      int j = i - 1;
+      while (j >= 0 && lse[ord[j]] < lse[o]) {
+        ord[j + 1] = ord[j];
+        --j;
+      }
+      ord[j + 1] = o;
+    }
+    const float m = lse[ord[0]];
+    float z = 0.f;
+    for (int i = 0; i < 8; ++i) {
+      const int r = ord[i];
+      const float w = (i < p.kvp && m != -INFINITY && lse[r] != -INFINITY) ? __expf(lse[r] - m) : 0.f;
+      ms->ord[pr][i] = r;
+      ms->w[pr][i] = w;
+      z += w;
+    }
+    ms->z[pr] = z;
   }
-  const float m = lse[ord[0]];
-  if (m == -INFINITY) return 0.f;
-  float acc = 0.f, z = 0.f;
-  for (int i = 0; i < kvp; ++i) {
-    const int r = ord[i];
-    if (lse[r] == -INFINITY) continue;
-    const float w = __expf(lse[r] - m);
-    const int slot = grp * kvp + r;
-    acc += w * p.frag_o[((static_cast<size_t>(slot) * p.batch + b) * p.q_per_slot + qi) * p.dp + d];
-    z += w;
+}
+
+template <int XM>
+__device__ __forceinline__ float merge_elem(const GemvParams& p, int b, int k, int ks0, int nks,
+                                            const MergeSmem* ms) {
+  const int flat = merge_flat<XM>(p, k);
+  const int head = flat / p.head_dim, d = flat - head * p.head_dim;
+  const int pr = b * merge_nh<XM>(p, ks0, nks) + head - merge_flat<XM>(p, ks0 * 16) / p.head_dim;
+  const float z = ms->z[pr];
+  if (z == 0.f) return 0.f;
+  float acc = 0.f;
+  for (int i = 0; i < p.kvp; ++i) {
+    const int r = ms->ord[pr][i];
+    acc += ms->w[pr][i] * merge_o<XM>(p, r, b, k, head, d);
   }
   return acc / z;
 }
 
-template <int XM>
-__device__ __forceinline__ float x_value(const GemvParams& p, const float* s_inv, int b, int k) {
-  if (XM == X_MERGE) return merge_elem(p, b, k);
-  const float v = p.x[static_cast<size_t>(b) * p.x_stride + k];
-  return XM == X_NORM ? v * s_inv[b] : v;
-}
-
 }  // namespace
+
+__host__ __device__ __forceinline__ size_t xs_bytes(const GemvParams& p, int nb8, int xs_terms) {
+  return static_cast<size_t>(p.kr_steps) * nb8 * xs_terms * 32 * 8;
+}
 
 template <int NB8, int XM, int EM, int XS>
 __global__ void __launch_bounds__(kThreads + 32) gemv_kernel(const GemvParams p) {
@@ -114,6 +167,7 @@ __global__ void __launch_bounds__(kThreads + 32) gemv_kernel(const GemvParams p)
     fence_mbar_init();
   }
   __syncthreads();
+  griddep_launch_dependents();
 
   if (warp == 8) {
     // ------------------------------------------------------------ producer: TMA bulk weight stream
@@ -131,43 +185,68 @@ __global__ void __launch_bounds__(kThreads + 32) gemv_kernel(const GemvParams p)
     }
     return;  // exited threads do not block later CTA barriers
   }
+  // weights are constant: the producer streams them while the previous kernel
+  // drains; everything below reads activations it produced.
+  griddep_wait();
 
   // ---------------------------------------------------------------- prologue (overlaps the stream)
+  // Every global load below is issued before any of its results is consumed
+  // (one latency round trip per phase, not one per element).
   if (XM == X_NORM) {
-    if (threadIdx.x < p.batch) {
-      float s = 0.f;
-      for (int i = 0; i < p.n_ss; ++i) s += p.ss_part[i * p.batch + threadIdx.x];
-      s_inv[threadIdx.x] = rsqrtf(s / static_cast<float>(p.K) + p.eps);
+    for (int b = warp; b < p.batch; b += 8) {
+      float ss = 0.f;
+      for (int i = lane; i < p.n_ss; i += 32) ss += p.ss_part[i * p.batch + b];
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      if (lane == 0) s_inv[b] = rsqrtf(ss / static_cast<float>(p.K) + p.eps);
     }
-    named_bar_sync(1, kThreads);
   }
-  for (int e = threadIdx.x; e < nks * NB8 * 32; e += kThreads) {
-    const int ln = e & 31;
-    const int t = e >> 5;
-    const int bg = t % NB8, ksl = t / NB8;
-    const int g = ln >> 2, c = ln & 3;
-    const int b = bg * 8 + g;
-    const int k = (ks0 + ksl) * 16 + 2 * c;
-    float v[4] = {0.f, 0.f, 0.f, 0.f};
-    if (b < p.batch) {
-      v[0] = x_value<XM>(p, s_inv, b, k);
-      v[1] = x_value<XM>(p, s_inv, b, k + 1);
-      v[2] = x_value<XM>(p, s_inv, b, k + 8);
-      v[3] = x_value<XM>(p, s_inv, b, k + 9);
+  MergeSmem* ms = reinterpret_cast<MergeSmem*>(smem + kStages * kStageSteps * 4096 + xs_bytes(p, NB8, XS));
+  if (XM == X_MERGE || XM == X_RECV) merge_weights<XM>(p, ks0, nks, ms);
+  if (XM != X_PLAIN) named_bar_sync(1, kThreads);
+  {
+    constexpr int MAXE = (kMaxKr * NB8 * 32) / kThreads;  // entries per thread (kr <= kMaxKr)
+    float v[MAXE][4];
+#pragma unroll
+    for (int j = 0; j < MAXE; ++j) {
+      const int e = threadIdx.x + j * kThreads;
+      const int ln = e & 31, t = e >> 5;
+      const int bg = t % NB8, ksl = t / NB8;
+      const int b = bg * 8 + (ln >> 2);
+      const int k = (ks0 + ksl) * 16 + 2 * (ln & 3);
+      const bool ok = ksl < nks && b < p.batch;
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int kk = k + (i & 1) + (i >> 1) * 8;
+        v[j][i] = ok ? ((XM == X_MERGE || XM == X_RECV) ? merge_elem<XM>(p, b, kk, ks0, nks, ms)
+                                                        : p.x[static_cast<size_t>(b) * p.x_stride + kk])
+                     : 0.f;
+      }
     }
-    if (XS == 2) {
-      float hi[4], lo[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) split2(v[i], hi[i], lo[i]);
-      xs[(ksl * 2 * NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(hi[0], hi[1]), pack_bf16(hi[2], hi[3]));
-      xs[(ksl * 2 * NB8 + NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(lo[0], lo[1]), pack_bf16(lo[2], lo[3]));
-    } else {
-      float hi[4], mid[4], lo[4];
+    for (int j = 0; j < MAXE; ++j) {
+      const int e = threadIdx.x + j * kThreads;
+      const int ln = e & 31, t = e >> 5;
+      const int bg = t % NB8, ksl = t / NB8;
+      if (ksl >= nks) continue;
+      const int b = bg * 8 + (ln >> 2);
+      if (XM == X_NORM && b < p.batch)
 #pragma unroll
-      for (int i = 0; i < 4; ++i) split3(v[i], hi[i], mid[i], lo[i]);
-      xs[(ksl * 3 * NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(hi[0], hi[1]), pack_bf16(hi[2], hi[3]));
-      xs[(ksl * 3 * NB8 + NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(mid[0], mid[1]), pack_bf16(mid[2], mid[3]));
-      xs[(ksl * 3 * NB8 + 2 * NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(lo[0], lo[1]), pack_bf16(lo[2], lo[3]));
+        for (int i = 0; i < 4; ++i) v[j][i] *= s_inv[b];
+      if (XS == 2) {
+        float hi[4], lo[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) split2(v[j][i], hi[i], lo[i]);
+        xs[(ksl * 2 * NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(hi[0], hi[1]), pack_bf16(hi[2], hi[3]));
+        xs[(ksl * 2 * NB8 + NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(lo[0], lo[1]), pack_bf16(lo[2], lo[3]));
+      } else {
+        float hi[4], mid[4], lo[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) split3(v[j][i], hi[i], mid[i], lo[i]);
+        xs[(ksl * 3 * NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(hi[0], hi[1]), pack_bf16(hi[2], hi[3]));
+        xs[(ksl * 3 * NB8 + NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(mid[0], mid[1]), pack_bf16(mid[2], mid[3]));
+        xs[(ksl * 3 * NB8 + 2 * NB8 + bg) * 32 + ln] = make_uint2(pack_bf16(lo[0], lo[1]), pack_bf16(lo[2], lo[3]));
+      }
     }
   }
   named_bar_sync(1, kThreads);
@@ -243,10 +322,18 @@ __global__ void __launch_bounds__(kThreads + 32) gemv_kernel(const GemvParams p)
   for (int e = threadIdx.x; e < rows_here * p.batch; e += kThreads) {
     const int r = e % rows_here, b = e / rows_here;
     auto ysum = [&](int rr) {
-      float y = 0.f;
+      // all split partials are loaded before summing (in split order: deterministic)
       const int n = nblk * kRows + rr;
-      for (int s = 0; s < p.ksplit; ++s)
-        y += __ldcg(p.ypart + (static_cast<size_t>(s) * p.batch + b) * p.Npad + n);
+      const float* base = p.ypart + static_cast<size_t>(b) * p.Npad + n;
+      const size_t stride = static_cast<size_t>(p.batch) * p.Npad;
+      float y = 0.f;
+      for (int s0 = 0; s0 < p.ksplit; s0 += 16) {
+        float v[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = s0 + j < p.ksplit ? __ldcg(base + (s0 + j) * stride) : 0.f;
+#pragma unroll
+        for (int j = 0; j < 16; ++j) y += v[j];
+      }
       return y;
     };
     if (EM == E_SWIGLU) {
@@ -269,7 +356,7 @@ __global__ void __launch_bounds__(kThreads + 32) gemv_kernel(const GemvParams p)
         *o = keep;
       } else if (EM == E_LOGITS) {
         if (p.out) p.out[static_cast<size_t>(b) * p.out_stride + n] = y;
-        atomicMax(&s_best[b], logit_key(y, n));
+        atomicMax(&s_best[b], logit_key(y, n + p.n_offset));
       } else if (EM == E_QKV) {
         if (n < p.nq) {
           const int head = n / p.head_dim, d = n - head * p.head_dim;
@@ -279,13 +366,14 @@ __global__ void __launch_bounds__(kThreads + 32) gemv_kernel(const GemvParams p)
           const int kvn = n - p.nq;
           const int is_v = kvn >= p.nk;
           const int kn = is_v ? kvn - p.nk : kvn;
-          const int h = kn / p.head_dim, d = kn - h * p.head_dim;
+          const int hl = kn / p.head_dim, d = kn - hl * p.head_dim;
+          const int h = p.kv_head_base + hl;
           if (p.kv_dbg)
-            p.kv_dbg[((static_cast<size_t>(b) * 2 + is_v) * p.kv_heads + h) * p.head_dim + d] = y;
+            p.kv_dbg[((static_cast<size_t>(b) * 2 + is_v) * p.kv_heads + hl) * p.head_dim + d] = y;
           if (p.append) {
             const long long g = p.total[b];
-            const int rank = rr_rank(g, p.chunk, p.kvp);
-            const long long row = rr_row(g, p.chunk, p.kvp);
+            const int rank = rr_rank(g, p.rr_chunk, p.kvp);
+            const long long row = rr_row(g, p.rr_chunk, p.kvp);
             const int grp = h / p.kvh_per_slot, kvh = h - grp * p.kvh_per_slot;
             const int slot_local = grp * p.kvp + rank - p.slot_base;
             if (slot_local >= 0 && slot_local < p.n_local_slots) {
@@ -322,10 +410,11 @@ __global__ void __launch_bounds__(kThreads + 32) gemv_kernel(const GemvParams p)
   if (threadIdx.x == 0) p.counters[nblk] = 0;  // self-reset for the next launch
 }
 
-size_t gemv_smem_bytes(const GemvParams& p, int xs_terms) {
+size_t gemv_smem_bytes(const GemvParams& p, int xs_terms, bool merge) {
   const int nb8 = (p.batch + 7) / 8;
-  const size_t xs = static_cast<size_t>(p.kr_steps) * nb8 * xs_terms * 32 * 8;
-  return static_cast<size_t>(kStages) * kStageSteps * 4096 + xs;  // epilogue staging reuses the ring
+  // epilogue staging reuses the ring
+  return static_cast<size_t>(kStages) * kStageSteps * 4096 + xs_bytes(p, nb8, xs_terms) +
+         (merge ? sizeof(MergeSmem) : 0);
 }
 
 template <int NB8, int XM, int EM>
@@ -333,7 +422,7 @@ static cudaError_t launch_t(const GemvParams& p, cudaStream_t stream) {
   // QKV feeds exp(q.k) with |logits| up to ~1e3 under the reference's unscaled
   // weights: carry x at fp32 precision there (3 bf16 terms), 2 terms elsewhere.
   constexpr int XS = EM == E_QKV ? 3 : 2;
-  const size_t smem = gemv_smem_bytes(p, XS);
+  const size_t smem = gemv_smem_bytes(p, XS, XM == X_MERGE || XM == X_RECV);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(gemv_kernel<NB8, XM, EM, XS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -341,8 +430,7 @@ static cudaError_t launch_t(const GemvParams& p, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
   }
   dim3 grid(p.Npad / kRows, p.ksplit);
-  gemv_kernel<NB8, XM, EM, XS><<<grid, kThreads + 32, smem, stream>>>(p);
-  return cudaGetLastError();
+  return launch_k(gemv_kernel<NB8, XM, EM, XS>, grid, dim3(kThreads + 32), smem, stream, p);
 }
 
 template <int NB8>
@@ -353,6 +441,7 @@ static cudaError_t dispatch_nb(const GemvParams& p, int xm, int em, cudaStream_t
   HX_CASE(X_NORM, E_QKV)
   HX_CASE(X_MERGE, E_RESID)
   HX_CASE(X_MERGE, E_STORE)
+  HX_CASE(X_RECV, E_STORE)
   HX_CASE(X_NORM, E_SWIGLU)
   HX_CASE(X_PLAIN, E_RESID)
   HX_CASE(X_PLAIN, E_STORE)

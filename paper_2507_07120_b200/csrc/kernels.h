@@ -7,6 +7,26 @@
 
 namespace hx {
 
+// Programmatic dependent launch for the decode-step kernels (set by the engine).
+void set_pdl(bool on);
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                     Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 // ---------------------------------------------------------------- attention
 struct AttnParams {
   const uint8_t* kv;       // page pool for this layer: [slot_local][B][kvh_per_slot][page_cap] pages
@@ -20,6 +40,9 @@ struct AttnParams {
   int kvp, chunk, page_cap, slot_base, n_local_slots;
   int n_streams, splits, n_items;
   float qscale;            // log2(e) / sqrt(head_size)
+  int q_grp_base;          // first TPA group whose query heads are in `q` (0: all groups)
+  int b_begin;             // requests [b_begin, b_begin + stream_batch) in this launch
+  int stream_batch;        // (HOP-B launches one request at a time)
 };
 cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t stream);
 cudaError_t launch_attn_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse,
@@ -28,7 +51,7 @@ cudaError_t launch_bump_totals(int* total, int n, cudaStream_t stream);
 size_t attn_decode_smem_bytes(int dp);
 
 // ---------------------------------------------------------------- GEMV
-enum XMode : int { X_PLAIN = 0, X_NORM = 1, X_MERGE = 2 };
+enum XMode : int { X_PLAIN = 0, X_NORM = 1, X_MERGE = 2, X_RECV = 3 };
 enum EMode : int { E_STORE = 0, E_QKV = 1, E_RESID = 2, E_SWIGLU = 3, E_LOGITS = 4 };
 
 struct GemvParams {
@@ -45,6 +68,8 @@ struct GemvParams {
   const float* frag_o;   // X_MERGE: [slot][B][q_per_slot][DP]
   const float* frag_lse; // [slot][B][q_per_slot] (natural log)
   int kvp, q_per_slot, head_dim, dp;
+  const float* recv;     // X_RECV: [kvp src][B][chunk] exchanged slices (+ lse slots)
+  int chunk, slice, exch_rank;
   // split-K plumbing
   float* ypart;          // [ksplit][B][Npad]
   int* counters;         // [Npad/128], self-resetting
@@ -57,13 +82,15 @@ struct GemvParams {
   uint8_t* kv;           // page pool of this layer
   const int* total;      // [B]
   float* kv_dbg;         // optional [B][2][kv_heads][head_dim] fp32 copy of appended K/V
-  int nq, nk, kv_heads, kvh_per_slot, chunk, page_cap, slot_base, n_local_slots;
+  int nq, nk, kv_heads, kvh_per_slot, rr_chunk, page_cap, slot_base, n_local_slots;
+  int kv_head_base;      // global index of the first KV head in this projection
   int append;            // write K/V into the cache
   // E_LOGITS
   unsigned long long* best;  // [B] packed (orderable logit, ~index)
+  int n_offset;              // global index of row 0 (vocabulary shard offset)
 };
 cudaError_t launch_gemv(const GemvParams& p, int xmode, int emode, cudaStream_t stream);
-size_t gemv_smem_bytes(const GemvParams& p, int xs_terms);
+size_t gemv_smem_bytes(const GemvParams& p, int xs_terms, bool merge);
 
 // ---------------------------------------------------------------- misc
 cudaError_t launch_merge_out(const float* frag_o, const float* frag_lse, int batch, int q_heads,
@@ -92,14 +119,25 @@ struct WSeg {
   uint64_t stream;
   int rows_begin, rows_end;  // rows of the combined matrix covered
   int cols_total;            // columns of the source (reference-orientation) matrix
-  int col_offset;            // source column of rows_begin
+  int col_offset;            // source column of rows_begin (interleaved: of feature 0)
   int interleave;            // 0: contiguous; 1: SwiGLU gate rows; 2: SwiGLU up rows
   double scale;
+  int k_offset;              // source row of k = 0 (tensor-parallel input shard)
+  int col_limit;             // interleaved: first source column past this shard
 };
 cudaError_t launch_weight_init_hash(uint4* w, int Npad, int K, const WSeg* segs, int nseg,
                                     uint64_t seed, cudaStream_t stream);
 cudaError_t launch_emb_init_hash(uint16_t* emb, int vocab, int hidden, uint64_t seed,
                                  uint64_t stream_id, cudaStream_t stream);
 cudaError_t launch_fill_zero(void* p, size_t bytes, cudaStream_t stream);
+// Distributed Helix exchange: pack this rank's fragment into per-destination
+// slices [kvp][batch][chunk] (chunk = slice + lse slots) for requests
+// [b_begin, b_begin + b_count).
+cudaError_t launch_pack_exchange(const float* frag_o, const float* frag_lse, int b_begin, int b_count, int batch,
+                                 int q_per_slot, int head_dim, int dp, int kvp, int slice, int chunk, float* send,
+                                 cudaStream_t s);
+// Residual add of an all-reduced partial product + RMSNorm statistics.
+cudaError_t launch_residual_add(float* x, const float* part, int batch, int hidden, float* ss_part,
+                                cudaStream_t s);
 
 }  // namespace hx

@@ -2,6 +2,8 @@
 // harness output, embedding gather, greedy-token finish, KV scatter/fill into
 // the round-robin page pool, and hash-RNG weight init directly into the
 // fragment-major layout (values identical to oracle/layer_oracle.hpp).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "kv_layout.cuh"
@@ -14,6 +16,8 @@ namespace hx {
 __global__ void merge_out_kernel(const float* frag_o, const float* frag_lse, int batch,
                                  int q_heads, int q_per_slot, int kvp, int head_dim, int dp,
                                  float* out, float* out_lse) {
+  griddep_wait();
+  griddep_launch_dependents();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= batch * q_heads) return;
   const int b = warp / q_heads, head = warp - b * q_heads;
@@ -54,22 +58,41 @@ cudaError_t launch_merge_out(const float* frag_o, const float* frag_lse, int bat
                              int q_per_slot, int kvp, int head_dim, int dp, float* out,
                              float* out_lse, cudaStream_t stream) {
   const int warps = batch * q_heads;
-  merge_out_kernel<<<(warps * 32 + 255) / 256, 256, 0, stream>>>(
-      frag_o, frag_lse, batch, q_heads, q_per_slot, kvp, head_dim, dp, out, out_lse);
-  return cudaGetLastError();
+  return launch_k(merge_out_kernel, dim3((warps * 32 + 255) / 256), dim3(256), 0, stream, frag_o, frag_lse,
+                  batch, q_heads, q_per_slot, kvp, head_dim, dp, out, out_lse);
 }
 
 // ---------------------------------------------------------------- embedding
 // x[b][:] = E[token_b][:] (bf16 -> fp32); ss_part[0][b] = sum x^2.
 __global__ void embed_kernel(const __nv_bfloat16* emb, const int* tokens, int batch, int hidden,
                              float* x, float* ss_part) {
+  griddep_wait();
+  griddep_launch_dependents();
   const int b = blockIdx.x;
   const int tok = tokens[b];
   float s = 0.f;
-  for (int i = threadIdx.x; i < hidden; i += blockDim.x) {
-    const float v = __bfloat162float(emb[static_cast<size_t>(tok) * hidden + i]);
-    x[static_cast<size_t>(b) * hidden + i] = v;
-    s += v * v;
+  // 8 bf16 per 16-byte load; every load issued before use
+  const uint4* src = reinterpret_cast<const uint4*>(emb + static_cast<size_t>(tok) * hidden);
+  const int nvec = hidden / 8;
+  for (int i0 = threadIdx.x; i0 < nvec; i0 += blockDim.x * 4) {
+    uint4 u[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + j * blockDim.x;
+      u[j] = i < nvec ? src[i] : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int i = i0 + j * blockDim.x;
+      if (i >= nvec) continue;
+      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u[j]);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float v = __bfloat162float(h[e]);
+        x[static_cast<size_t>(b) * hidden + i * 8 + e] = v;
+        s += v * v;
+      }
+    }
   }
   __shared__ float red[32];
 #pragma unroll
@@ -86,13 +109,14 @@ __global__ void embed_kernel(const __nv_bfloat16* emb, const int* tokens, int ba
 
 cudaError_t launch_embed(const uint16_t* emb, const int* tokens, int batch, int hidden, float* x,
                          float* ss_part, cudaStream_t stream) {
-  embed_kernel<<<batch, 256, 0, stream>>>(reinterpret_cast<const __nv_bfloat16*>(emb), tokens,
-                                          batch, hidden, x, ss_part);
-  return cudaGetLastError();
+  return launch_k(embed_kernel, dim3(batch), dim3(256), 0, stream, reinterpret_cast<const __nv_bfloat16*>(emb),
+                  tokens, batch, hidden, x, ss_part);
 }
 
 __global__ void argmax_finish_kernel(const unsigned long long* best, int batch, int* tokens_out,
                                      unsigned long long* best_reset) {
+  griddep_wait();
+  griddep_launch_dependents();
   const int b = threadIdx.x;
   if (b < batch) {
     const unsigned long long k = best[b];
@@ -103,8 +127,7 @@ __global__ void argmax_finish_kernel(const unsigned long long* best, int batch, 
 
 cudaError_t launch_argmax_finish(const unsigned long long* best, int batch, int* tokens_out,
                                  unsigned long long* best_reset, cudaStream_t stream) {
-  argmax_finish_kernel<<<1, 32, 0, stream>>>(best, batch, tokens_out, best_reset);
-  return cudaGetLastError();
+  return launch_k(argmax_finish_kernel, dim3(1), dim3(32), 0, stream, best, batch, tokens_out, best_reset);
 }
 
 // ---------------------------------------------------------------- KV scatter / fill
@@ -284,9 +307,9 @@ __device__ double wseg_value(const WSeg* segs, int nseg, int n, int k, uint64_t 
       const int blk = n >> 7, r = n & 127;
       if ((sg.interleave == 1) != (r < 64)) continue;
       col = sg.col_offset + blk * 64 + (r & 63);
-      if (col >= sg.cols_total) return 0.0;
+      if (col >= sg.col_limit) return 0.0;
     }
-    const uint64_t index = static_cast<uint64_t>(k) * static_cast<uint64_t>(sg.cols_total) +
+    const uint64_t index = static_cast<uint64_t>(k + sg.k_offset) * static_cast<uint64_t>(sg.cols_total) +
                            static_cast<uint64_t>(col);
     return hash_unit(seed, sg.stream, index) * sg.scale;
   }
@@ -348,4 +371,96 @@ cudaError_t launch_fill_zero(void* p, size_t bytes, cudaStream_t stream) {
   return cudaMemsetAsync(p, 0, bytes, stream);
 }
 
+}  // namespace hx
+
+// ---------------------------------------------------------------- loopback reductions (comm.h)
+namespace hx {
+__global__ void sum_buffers_kernel(const float* const* srcs, int n, float* dst, size_t count) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  float s = 0.f;
+  for (int r = 0; r < n; ++r) s += srcs[r][i];  // rank order: deterministic, identical on every rank
+  dst[i] = s;
+}
+__global__ void max_u64_buffers_kernel(const unsigned long long* const* srcs, int n, unsigned long long* dst,
+                                       size_t count) {
+  const size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  unsigned long long m = 0;
+  for (int r = 0; r < n; ++r) m = srcs[r][i] > m ? srcs[r][i] : m;
+  dst[i] = m;
+}
+cudaError_t launch_sum_buffers(const float* const* srcs, int n, float* dst, size_t count, cudaStream_t s) {
+  sum_buffers_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(srcs, n, dst, count);
+  return cudaGetLastError();
+}
+cudaError_t launch_max_u64_buffers(const unsigned long long* const* srcs, int n, unsigned long long* dst,
+                                   size_t count, cudaStream_t s) {
+  max_u64_buffers_kernel<<<static_cast<unsigned>((count + 255) / 256), 256, 0, s>>>(srcs, n, dst, count);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- Helix fragment exchange (pack side)
+// send[p][b][0:slice]           = this rank's fragment elements [p*slice, (p+1)*slice) of its
+//                                 group's flattened (heads x head_dim) output (attention.hpp:495-502)
+// send[p][b][slice:slice+nh_p]  = lse of the heads that slice touches
+__global__ void pack_exchange_kernel(const float* frag_o, const float* frag_lse, int b_begin, int b_count,
+                                     int batch, int q_per_slot, int head_dim, int dp, int kvp, int slice,
+                                     int chunk, float* send) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int per_req = slice + (chunk - slice);
+  const long long total = static_cast<long long>(kvp) * b_count * per_req;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const int e = static_cast<int>(i % per_req);
+    const long long t = i / per_req;
+    const int bl = static_cast<int>(t % b_count), p = static_cast<int>(t / b_count);
+    const int b = b_begin + bl;
+    const int first_head = (p * slice) / head_dim;
+    const int last_head = ((p + 1) * slice - 1) / head_dim;
+    float v = 0.f;
+    if (e < slice) {
+      const int flat = p * slice + e;
+      const int head = flat / head_dim, d = flat - head * head_dim;
+      v = frag_o[(static_cast<size_t>(b) * q_per_slot + head) * dp + d];
+    } else if (e - slice <= last_head - first_head) {
+      v = frag_lse[static_cast<size_t>(b) * q_per_slot + first_head + (e - slice)];
+    }
+    send[(static_cast<size_t>(p) * batch + b) * chunk + e] = v;
+  }
+}
+cudaError_t launch_pack_exchange(const float* frag_o, const float* frag_lse, int b_begin, int b_count, int batch,
+                                 int q_per_slot, int head_dim, int dp, int kvp, int slice, int chunk, float* send,
+                                 cudaStream_t s) {
+  const long long total = static_cast<long long>(kvp) * b_count * chunk;
+  const int blocks = static_cast<int>(std::min<long long>((total + 255) / 256, 1024));
+  return launch_k(pack_exchange_kernel, dim3(blocks), dim3(256), 0, s, frag_o, frag_lse, b_begin, b_count, batch,
+                  q_per_slot, head_dim, dp, kvp, slice, chunk, send);
+}
+
+// x[b][n] += part[b][n]; ss_part[blk][b] = sum over the 128-column block of x^2 (deterministic).
+__global__ void residual_add_kernel(float* x, const float* part, int batch, int hidden, float* ss_part) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int blk = blockIdx.x, b = blockIdx.y;
+  const int n = blk * 128 + threadIdx.x;
+  float v = 0.f;
+  if (n < hidden) {
+    v = x[static_cast<size_t>(b) * hidden + n] + part[static_cast<size_t>(b) * hidden + n];
+    x[static_cast<size_t>(b) * hidden + n] = v;
+  }
+  float s = v * v;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  __shared__ float red[4];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) ss_part[static_cast<size_t>(blk) * batch + b] = (red[0] + red[1]) + (red[2] + red[3]);
+}
+cudaError_t launch_residual_add(float* x, const float* part, int batch, int hidden, float* ss_part,
+                                cudaStream_t s) {
+  return launch_k(residual_add_kernel, dim3((hidden + 127) / 128, batch), dim3(128), 0, s, x, part, batch, hidden,
+                  ss_part);
+}
 }  // namespace hx

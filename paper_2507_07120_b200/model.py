@@ -163,7 +163,7 @@ class HelixDecoder(_Engine):
     `layers`/`vocab` override the spec (layer slices, small vocab for tests)."""
 
     def __init__(self, spec, tpa=1, kvp=1, chunk_size=16, batch=8, capacity=4096, layers=None, vocab=None,
-                 device=0, use_graphs=True):
+                 device=0, use_graphs=True, hopb=False, pool=0, rank=0, nccl_id=None, loopback=None):
         if spec.attention != "gqa":
             raise NotImplementedError("MLA attention is not implemented in this build (GQA only)")
         if spec.moe:
@@ -174,7 +174,11 @@ class HelixDecoder(_Engine):
         mc = ModelConfig(hidden=spec.hidden_dim, query_heads=spec.query_heads, kv_heads=spec.kv_heads,
                          head_size=spec.head_size, ffn=spec.ffn_dim, layers=self.layers, vocab=self.vocab,
                          attention_only=0)
-        super().__init__(mc, tpa, kvp, chunk_size, batch, capacity, device, use_graphs=use_graphs)
+        super().__init__(mc, tpa, kvp, chunk_size, batch, capacity, device, use_graphs=use_graphs, hopb=hopb,
+                         pool=pool, rank=rank, nccl_id=nccl_id, loopback=loopback)
+        self.n_ranks = tpa * kvp if pool else 1
+        self.rank = rank
+        self.vocab_local = -(-self.vocab // self.n_ranks)
 
     def init_weights(self, seed, qkv="mt19937"):
         if qkv == "mt19937":
@@ -194,7 +198,7 @@ class HelixDecoder(_Engine):
     def step(self, tokens, want_logits=False, want_hidden=False):
         t = np.ascontiguousarray(tokens, dtype=np.int32)
         nxt = np.zeros(self.batch, dtype=np.int32)
-        logits = np.zeros((self.batch, self.vocab), dtype=np.float32) if want_logits else None
+        logits = np.zeros((self.batch, self.vocab_local), dtype=np.float32) if want_logits else None
         hidden = np.zeros((self.layers + 1, self.batch, self.spec.hidden_dim), dtype=np.float32) \
             if want_hidden else None
         self._check(lib().hx_decode_step(self._h, t.ctypes.data_as(_ip), nxt.ctypes.data_as(_ip),
@@ -210,3 +214,26 @@ class HelixDecoder(_Engine):
 
     def stream(self):
         return lib().hx_stream(self._h)
+
+
+class Loopback:
+    """In-process group of n ranks on one device (HX_POOL_LOOPBACK): one engine
+    per host thread, collectives through device copies + a host barrier."""
+
+    def __init__(self, n):
+        h = C.c_void_p()
+        check(lib().hx_loopback_create(n, C.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        try:
+            lib().hx_loopback_destroy(self._h)
+        except Exception:
+            pass
+
+
+def nccl_unique_id():
+    """128-byte ncclUniqueId (rank 0 creates it; share it with the other ranks)."""
+    buf = (C.c_char * 128)()
+    check(lib().hx_nccl_get_unique_id(buf))
+    return bytes(buf)
