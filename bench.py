@@ -180,19 +180,42 @@ def ours(a):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    if world > 1 or a.gpus > 1:
-        raise SystemExit("multi-GPU Helix (NCCL) arm is not available in this build")
-    dev = 0
+    dev = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(dev)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     spec = P.model.PRESETS["llama3-8b-like"]
     B, S, L = a.batch, a.context, a.layers
-    total_steps = a.warmup + a.steps
-    cap = S + 4 * (total_steps + 8) + 64
-    eng = P.HelixDecoder(spec, tpa=1, kvp=1, batch=B, capacity=cap, layers=L, device=dev)
+    total_steps = 3 * (a.warmup + a.steps) + 8
+    # weak scaling: S KV tokens per request per GPU; KVP = N (global context S*N)
+    S_glob = S * world
+    cap = S_glob + 4 * (total_steps + 8) * world + 64
+    if world > 1:
+        from paper_2507_07120_b200.model import nccl_unique_id
+        uid = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        eng = P.HelixDecoder(spec, tpa=1, kvp=world, batch=B, capacity=cap, layers=L, device=dev, pool=1,
+                             rank=rank, nccl_id=uid[0], hopb=True)
+    else:
+        eng = P.HelixDecoder(spec, tpa=1, kvp=1, batch=B, capacity=cap, layers=L, device=dev)
     eng.init_weights(2507, qkv="hash")
-    eng.fill_kv_hash(S, 2507)
+    eng.fill_kv_hash(S_glob, 2507)
     info = eng.info()
     stream = torch.cuda.ExternalStream(eng.stream())
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if dist is None:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     tok = [torch.randint(0, spec.vocab, (B,), dtype=torch.int32, device="cuda"),
            torch.zeros(B, dtype=torch.int32, device="cuda")]
@@ -200,26 +223,29 @@ def ours(a):
     def dev_step(i):
         eng.step_device(tok[i % 2].data_ptr(), tok[(i + 1) % 2].data_ptr())
 
-    for i in range(a.warmup):
-        dev_step(i)
-    eng.synchronize()
-    torch.cuda.synchronize()
-    with torch.cuda.stream(stream):
+    def timed(n_steps, offset):
+        barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler() as clk:
-        time.sleep(0.3)
         e0.record(stream)
-        for i in range(a.steps):
-            dev_step(a.warmup + i)
+        for i in range(n_steps):
+            dev_step(offset + i)
         e1.record(stream)
         e1.synchronize()
-        ms = e0.elapsed_time(e1) / a.steps
+        barrier()
+        return max_over_ranks(e0.elapsed_time(e1) / n_steps)
+
+    for i in range(a.warmup):
+        dev_step(i)
+    import ctypes
+    with ClockSampler() as clk:
+        time.sleep(0.3)
+        ms = timed(a.steps, a.warmup)
         # e2e through the public API: pinned host tokens in, host next tokens out, every step
         h_tok = torch.zeros(B, dtype=torch.int32).pin_memory()
         h_next = torch.zeros(B, dtype=torch.int32).pin_memory()
         h_tok.copy_(tok[0].cpu())
-        import ctypes
         ip = ctypes.POINTER(ctypes.c_int32)
+        barrier()
         e2 = torch.cuda.Event(enable_timing=True)
         e3 = torch.cuda.Event(enable_timing=True)
         w0 = time.perf_counter()
@@ -232,11 +258,32 @@ def ours(a):
         e3.record(stream)
         e3.synchronize()
         wall_e2e = (time.perf_counter() - w0) / a.steps * 1e3
-        ms_e2e = max(e2.elapsed_time(e3) / a.steps, wall_e2e)
+        ms_e2e = max_over_ranks(max(e2.elapsed_time(e3) / a.steps, wall_e2e))
+        hopb = None
+        if world > 1:
+            # exposed all-to-all with and without HOP-B (overlap.hpp:37-69): same resident pool,
+            # runtime switches; "no a2a" replaces the exchange by a local copy (measurement only)
+            def setf(flag, v):
+                P._lib.check(P.lib().hx_engine_set_flag(eng._h, flag, v), eng._h)
+            off = a.warmup + a.steps
+            setf(2, 0)
+            for i in range(a.warmup):
+                dev_step(off + i)
+            ms_off = timed(a.steps, off + a.warmup)
+            setf(1, 1)
+            for i in range(a.warmup):
+                dev_step(off + i)
+            ms_noa2a = timed(a.steps, off + a.warmup)
+            setf(1, 0)
+            setf(2, 1)
+            exp_on, exp_off = max(0.0, ms - ms_noa2a), max(0.0, ms_off - ms_noa2a)
+            hopb = {"ms_per_step_on": ms, "ms_per_step_off": ms_off, "ms_per_step_no_a2a": ms_noa2a,
+                    "exposed_a2a_ms_on": exp_on, "exposed_a2a_ms_off": exp_off,
+                    "a2a_hidden_frac": (1.0 - exp_on / exp_off) if exp_off > 0 else None}
     clocks = clk.summary(dev)
 
     # per-kernel-kind breakdown (eager launches, CUDA events on the engine stream)
-    prof = np.zeros(9)
+    prof = np.zeros(10)
     P.lib().hx_profile_step(eng._h, 2, prof.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     step_prof = prof.sum()
     attn_ms_launch = prof[2] / L
@@ -248,10 +295,10 @@ def ours(a):
     step_bytes = attn_bytes * L + weight_bytes
     value = B / (ms * 1e-3)
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": a.steps, "warmup": a.warmup,
-        "ms_per_step": ms, "ttl_ms": ms, "tokens_per_s_per_gpu": value, "higher_is_better": True,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+        "ms_per_step": ms, "ttl_ms": ms, "tokens_per_s_per_gpu": value / world, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": config_dict(a, 1),
+        "config": config_dict(a, world),
         "e2e": {"value": B / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 4 * B, "d2h_bytes_per_step": 4 * B,
                 "ms_per_step": ms_e2e},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
@@ -266,13 +313,20 @@ def ours(a):
         "clocks": clocks,
         "engine": info,
     }
-    if not a.no_cpu_baseline and rank == 0:
+    if hopb is not None:
+        line["hopb"] = hopb
+    if not a.no_cpu_baseline and rank == 0 and world == 1:
         try:
             cb = run_ref_bench(1, a.cpu_context, 2, 0, L, B)
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as ex:  # reported, never fatal for the GPU number
             line["cpu_baseline"] = {"error": str(ex)[:200]}
-    print(json.dumps(line), flush=True)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        eng.close()
+        dist.destroy_process_group()
 
 
 def main():

@@ -166,9 +166,11 @@ int hx_nccl_get_unique_id(void* out128);
  * element count (= slice), first head touched, heads touched; returns the
  * padded per-(peer, request) chunk in floats (slice + lse slots), or < 0. */
 int64_t hx_exchange_layout(int64_t q_per_group, int64_t head_size, int64_t kvp, int64_t* out);
-/* Measurement switches: HX_FLAG_SKIP_COMM = 1 replaces every collective by a
- * local copy (exposed-communication measurement; results are then wrong). */
+/* Runtime switches. HX_FLAG_HOPB: HOP-B on/off. HX_FLAG_SKIP_COMM (measurement
+ * only, results are then wrong): bitmask 1 = replace the all-to-all by a local
+ * copy, 2 = skip the all-reduces -- exposed-communication measurement. */
 #define HX_FLAG_SKIP_COMM 1
+#define HX_FLAG_HOPB 2
 int hx_engine_set_flag(hx_engine* e, int32_t flag, int32_t value);
 /* In-process group of n ranks on one device (one host thread per rank). */
 int hx_loopback_create(int32_t n_ranks, hx_loopback** out);

@@ -216,13 +216,18 @@ void Engine::alloc() {
   const int qh_buf = dist_mode_ == HX_POOL_LOCAL ? static_cast<int>(Qh_) : q_per_slot_;
   d_q_ = dalloc<float>(static_cast<size_t>(B_) * qh_buf * DP_, "q");
 
-  // attention work decomposition (per launch: all requests, or one request under HOP-B)
-  const int launch_batch = (hopb_ && dist_mode_ != HX_POOL_LOCAL) ? 1 : B_;
-  n_streams_ = n_slots_ * launch_batch * kvh_per_slot_ * q_chunks_;
+  // attention work decomposition: balanced page ranges ("splits") per stream,
+  // ~8 work items per SM for a full-batch launch and for a one-request (HOP-B) launch
   const int pages_max = page_cap_;
   const int target_items = num_sms_ * 8;
-  splits_ = std::max(1, std::min((target_items + n_streams_ - 1) / n_streams_, std::max(1, pages_max / 8)));
-  n_items_ = n_streams_ * splits_;
+  auto splits_for = [&](int streams) {
+    return std::max(1, std::min((target_items + streams - 1) / streams, std::max(1, pages_max / 8)));
+  };
+  n_streams_ = n_slots_ * B_ * kvh_per_slot_ * q_chunks_;
+  splits_ = splits_for(n_streams_);
+  const int req_streams = n_slots_ * kvh_per_slot_ * q_chunks_;
+  splits_req_ = splits_for(req_streams);
+  n_items_ = std::max(n_streams_ * splits_, req_streams * splits_req_);
   attn_grid_ = std::min(num_sms_, n_items_);
   if (dist_mode_ != HX_POOL_LOCAL) {
     d_send_ = dalloc<float>(static_cast<size_t>(kvp_) * B_ * xchunk_, "exchange send");
@@ -682,7 +687,7 @@ AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) const {
   a.b_begin = b_begin;
   a.stream_batch = b_count;
   a.n_streams = n_slots_ * b_count * kvh_per_slot_ * q_chunks_;
-  a.splits = splits_;
+  a.splits = b_count == B_ ? splits_ : splits_req_;
   a.n_items = a.n_streams * splits_;
   a.qscale = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D_)));
   return a;
@@ -731,7 +736,7 @@ void Engine::enqueue_exchange_and_attention_dist(int64_t layer) {
     float* send = d_send_ + static_cast<size_t>(b0) * xchunk_;
     float* recv = d_recv_ + static_cast<size_t>(b0) * xchunk_;
     const size_t count = static_cast<size_t>(per) * xchunk_;
-    if (skip_comm_) {  // measurement: keep only this rank's own block, no wire traffic
+    if (skip_comm_ & 1) {  // measurement: keep only this rank's own block, no wire traffic
       cuda_check(cudaMemcpyAsync(recv + static_cast<size_t>(r_) * stride, send + static_cast<size_t>(r_) * stride,
                                  count * sizeof(float), cudaMemcpyDeviceToDevice, stream_),
                  "skip-comm copy");
@@ -743,7 +748,7 @@ void Engine::enqueue_exchange_and_attention_dist(int64_t layer) {
       transport_->all_to_all(send, recv, count, stride, stream_);
     }
   }
-  if (side_stream && !skip_comm_) {
+  if (side_stream && !(skip_comm_ & 1)) {
     cuda_check(cudaEventRecord(hop_events_.back(), comm_stream_), "hopb join");
     cuda_check(cudaStreamWaitEvent(stream_, hop_events_.back(), 0), "hopb join wait");
   }
@@ -802,7 +807,7 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
       // TP O-proj over this rank's exchanged slice, AllReduce over the pool (latency.cpp:85-94)
       cuda_check(launch_gemv(plan_o_[l].p, X_RECV, E_STORE, stream_), "o-proj");
       mark(4);
-      if (!skip_comm_) transport_->all_reduce_sum(d_parth_, static_cast<size_t>(B_) * H_, stream_);
+      if (!(skip_comm_ & 2)) transport_->all_reduce_sum(d_parth_, static_cast<size_t>(B_) * H_, stream_);
       cuda_check(launch_residual_add(d_x_, d_parth_, B_, static_cast<int>(H_), d_ss_, stream_), "residual");
       mark(9);
       // TP FFN over F/N features, AllReduce (latency.cpp:138-144)
@@ -810,7 +815,7 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
       mark(5);
       cuda_check(launch_gemv(plan_down_[l].p, X_PLAIN, E_STORE, stream_), "down");
       mark(6);
-      if (!skip_comm_) transport_->all_reduce_sum(d_parth_, static_cast<size_t>(B_) * H_, stream_);
+      if (!(skip_comm_ & 2)) transport_->all_reduce_sum(d_parth_, static_cast<size_t>(B_) * H_, stream_);
       cuda_check(launch_residual_add(d_x_, d_parth_, B_, static_cast<int>(H_), d_ss_, stream_), "residual");
       mark(9);
     }
@@ -822,7 +827,7 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
   GemvParams lm = plan_lm_.p;
   lm.out = store_logits_ ? d_logits_ : nullptr;
   cuda_check(launch_gemv(lm, X_NORM, E_LOGITS, stream_), "lm head");
-  if (dist && !skip_comm_) transport_->all_reduce_max_u64(d_best_, static_cast<size_t>(B_), stream_);  // vocab-sharded argmax
+  if (dist && !(skip_comm_ & 2)) transport_->all_reduce_max_u64(d_best_, static_cast<size_t>(B_), stream_);  // vocab-sharded argmax
   cuda_check(launch_argmax_finish(d_best_, B_, next_dev, d_best_, stream_), "argmax");
   mark(7);
 }
@@ -878,7 +883,10 @@ void Engine::decode_step(const int32_t* tokens, int32_t* next, float* logits, fl
 
 void Engine::set_flag(int flag, int value) {
   if (flag == HX_FLAG_SKIP_COMM) {
-    skip_comm_ = value != 0;
+    skip_comm_ = value;
+    drop_graphs();
+  } else if (flag == HX_FLAG_HOPB) {
+    hopb_ = value != 0;
     drop_graphs();
   } else {
     throw std::invalid_argument("unknown engine flag");
@@ -931,6 +939,8 @@ void Engine::info(hx_engine_info* o) const {
   o->attn_items = n_items_;
   o->attn_grid = attn_grid_;
   o->kernels_per_step = kernels_per_step_;
+  if (!attn_only_ && dist_mode_ != HX_POOL_LOCAL)  // + pack and two residual adds per layer
+    o->kernels_per_step = 1 + L_ * (7 + 3 + (hopb_ ? 3 * (B_ - 1) : 0)) + 2;
   o->page_cap = page_cap_;
   o->head_dim_padded = DP_;
 }

@@ -105,6 +105,7 @@ class Engine {
   int num_sms_;
   // attention plan
   int n_streams_, splits_, n_items_, attn_grid_;
+  int splits_req_ = 1;  // splits per stream for per-request (HOP-B) launches
 
   // ---- device state
   cudaStream_t stream_ = nullptr;
@@ -158,7 +159,7 @@ class Engine {
 
   // ---- distributed pool (one rank of tpa*kvp; comm.h)
   int dist_mode_ = 0;          // HX_POOL_LOCAL / NCCL / LOOPBACK
-  bool skip_comm_ = false;     // HX_FLAG_SKIP_COMM (measurement only)
+  int skip_comm_ = 0;          // HX_FLAG_SKIP_COMM bitmask: 1 all-to-all, 2 all-reduces (measurement only)
   int grp_ = 0, r_ = 0, N_ = 1;
   int slice_ = 0, xchunk_ = 0; // exchanged elements per (peer, request) and padded chunk (+ lse slots)
   int F_local_ = 0, V_local_ = 0;

@@ -423,11 +423,13 @@ static cudaError_t launch_t(const GemvParams& p, cudaStream_t stream) {
   // weights: carry x at fp32 precision there (3 bf16 terms), 2 terms elsewhere.
   constexpr int XS = EM == E_QKV ? 3 : 2;
   const size_t smem = gemv_smem_bytes(p, XS, XM == X_MERGE || XM == X_RECV);
-  if (smem > 48 * 1024) {
+  static size_t configured = 0;  // opt in once per instantiation (static smem adds to the 48 KB default)
+  if (smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(gemv_kernel<NB8, XM, EM, XS>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
+    configured = smem;
   }
   dim3 grid(p.Npad / kRows, p.ksplit);
   return launch_k(gemv_kernel<NB8, XM, EM, XS>, grid, dim3(kThreads + 32), smem, stream, p);
