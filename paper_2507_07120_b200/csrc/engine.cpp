@@ -189,7 +189,7 @@ Engine::~Engine() {
   f(w_lm_); f(emb_); f(d_total_); f(d_q_); f(d_part_o_); f(d_part_lse_); f(d_work_);
   f(d_frag_o_); f(d_frag_lse_); f(d_ypart_); f(d_counters_); f(d_x_); f(d_ss_); f(d_m_);
   f(d_logits_); f(d_best_); f(d_tokens_); f(d_next_); f(d_out_); f(d_out_lse_); f(d_hidden_);
-  f(d_segs_); f(d_send_); f(d_recv_); f(d_parth_);
+  f(d_segs_); f(d_send_); f(d_recv_); f(d_parth_); f(d_xf_resid_); f(d_xf_attn_); f(d_xf_m_); f(d_plan_ctr_);
   for (auto& e : hop_events_) cudaEventDestroy(e);
   delete transport_;
   if (comm_stream_) cudaStreamDestroy(comm_stream_);
@@ -250,32 +250,32 @@ void Engine::alloc() {
 
 // ---------------------------------------------------------------------------
 void Engine::plan_gemvs() {
-  auto make = [&](int N, int Npad, int K, int xm, int em) {
+  d_plan_ctr_ = dalloc<int>(static_cast<size_t>(2 * (4 * L_ + 2)), "plan counters");
+  int plan_idx = 0;
+  auto make = [&](int N, int Npad, int K, int norm, int em) {
     GemvPlan g;
     GemvParams& p = g.p;
     p.N = N;
     p.Npad = Npad;
     p.K = K;
     p.batch = B_;
-    // Each CTA streams a contiguous [128 rows x kr k-steps] weight range through
-    // a 32 KB TMA ring; kr <= 32 k-steps keeps a CTA <= ~56 KB of shared memory
-    // so 4 co-reside per SM (one CTA's prologue/epilogue latency overlaps the
-    // others' streams). Shrink kr until the grid covers >= 4 CTAs per SM.
+    // Persistent GEMV: tiles = (128-row block, k-chunk of kr k-steps) pulled
+    // from a queue by one CTA per SM. kr shrinks until there are >= 4 tiles per
+    // SM (dynamic balance, <= one short tile of tail); kr >= 8 keeps a tile >= 32 KB.
     const int kst = K / 16;
     const int nblk = Npad / 128;
-    int kr = std::min(32, kst);
+    int kr = std::min(64, kst);
     while (kr > 8 && static_cast<int64_t>(nblk) * ((kst + kr - 1) / kr) < 4 * num_sms_) kr /= 2;
-    if (xm == X_MERGE || xm == X_RECV)  // (request, head) pairs per CTA fit the prologue's shared table
-      while (kr > 1 && (kr * 16 / D_ + 2) * B_ > 256) kr /= 2;
     const int ksplit = (kst + kr - 1) / kr;
     p.ksplit = ksplit;
     p.kr_steps = kr;
+    p.n_tiles = nblk * ksplit;
+    p.work_counter = d_plan_ctr_ + 2 * plan_idx++;
     p.eps = 1e-5f;
     p.kvp = kvp_;
-    p.q_per_slot = q_per_slot_;
     p.head_dim = static_cast<int>(D_);
     p.dp = DP_;
-    g.xmode = xm;
+    g.xmode = norm;
     g.emode = em;
     ypart_elems_ = std::max(ypart_elems_, static_cast<size_t>(ksplit) * B_ * Npad);
     max_counters_ = std::max(max_counters_, nblk);
@@ -288,7 +288,7 @@ void Engine::plan_gemvs() {
   const int Hh = static_cast<int>(H_);
   const int F = F_local_;
   for (int64_t l = 0; l < L_; ++l) {
-    GemvPlan q = make(Nqkv, round_up(Nqkv, 128), Hh, attn_only_ ? X_PLAIN : X_NORM, E_QKV);
+    GemvPlan q = make(Nqkv, round_up(Nqkv, 128), Hh, attn_only_ ? 0 : 1, E_QKV);
     q.p.nq = nq;
     q.p.nk = nk;
     q.p.kv_heads = nk / static_cast<int>(D_);
@@ -303,26 +303,29 @@ void Engine::plan_gemvs() {
     if (!attn_only_) {
       if (dist) {
         // O-proj: this rank's exchanged slice of its group's heads x its rows of W_O
-        GemvPlan o = make(Hh, round_up(Hh, 128), slice_, X_RECV, E_STORE);
-        o.p.chunk = xchunk_;
-        o.p.slice = slice_;
-        o.p.exch_rank = r_;
-        plan_o_.push_back(o);
-        plan_gu_.push_back(make(2 * F, round_up(F, 64) * 2, Hh, X_NORM, E_SWIGLU));
-        plan_down_.push_back(make(Hh, round_up(Hh, 128), F, X_PLAIN, E_STORE));
+        plan_o_.push_back(make(Hh, round_up(Hh, 128), slice_, 0, E_STORE));
+        plan_gu_.push_back(make(2 * F, round_up(F, 64) * 2, Hh, 1, E_SWIGLU));
+        plan_down_.push_back(make(Hh, round_up(Hh, 128), F, 0, E_STORE));
       } else {
-        plan_o_.push_back(make(Hh, round_up(Hh, 128), Hh, X_MERGE, E_RESID));
-        plan_gu_.push_back(make(2 * F, round_up(F, 64) * 2, Hh, X_NORM, E_SWIGLU));
-        plan_down_.push_back(make(Hh, round_up(Hh, 128), F, X_PLAIN, E_RESID));
+        plan_o_.push_back(make(Hh, round_up(Hh, 128), Hh, 0, E_RESID));
+        plan_gu_.push_back(make(2 * F, round_up(F, 64) * 2, Hh, 1, E_SWIGLU));
+        plan_down_.push_back(make(Hh, round_up(Hh, 128), F, 0, E_RESID));
       }
     }
   }
   if (!attn_only_) {
-    plan_lm_ = make(V_local_, round_up(V_local_, 128), Hh, X_NORM, E_LOGITS);
+    plan_lm_ = make(V_local_, round_up(V_local_, 128), Hh, 1, E_LOGITS);
     plan_lm_.p.n_offset = dist ? rank_ * V_local_ : 0;
   }
 
   d_ypart_ = dalloc<float>(ypart_elems_, "ypart");
+  {
+    const int nb8 = (B_ + 7) / 8;
+    auto xf_alloc = [&](int K) { return dalloc<uint8_t>(static_cast<size_t>(K / 16) * 3 * nb8 * 256, "xf"); };
+    d_xf_resid_ = xf_alloc(static_cast<int>(H_));
+    d_xf_attn_ = xf_alloc(dist ? slice_ : static_cast<int>(H_));
+    d_xf_m_ = xf_alloc(std::max(16, F_local_));
+  }
   d_counters_ = dalloc<int>(static_cast<size_t>(max_counters_), "counters");
   const int hblk = round_up(Hh, 128) / 128;
   d_ss_ = dalloc<float>(static_cast<size_t>(std::max(hblk, 1)) * B_, "ss");
@@ -331,12 +334,13 @@ void Engine::plan_gemvs() {
     d_logits_ = dalloc<float>(static_cast<size_t>(B_) * V_local_, "logits");
     d_hidden_ = dalloc<float>(static_cast<size_t>(L_ + 1) * B_ * H_, "hidden");
   }
+  // launches per step (each GEMV = streaming kernel + epilogue kernel)
   if (attn_only_)
-    kernels_per_step_ = 5;
+    kernels_per_step_ = 7;  // xprep, qkv x2, attention, split-reduce, bump, merge
   else if (!dist)
-    kernels_per_step_ = 1 + 7 * L_ + 2;
-  else  // + pack and two residual adds per layer (per-request attention launches under HOP-B)
-    kernels_per_step_ = 1 + L_ * (7 + 3 + (hopb_ ? 3 * (B_ - 1) : 0)) + 2;
+    kernels_per_step_ = 1 + 12 * L_ + 3;
+  else  // + pack and two residual adds per layer; per-request attention launches under HOP-B
+    kernels_per_step_ = 1 + L_ * (14 + (hopb_ ? 3 * (B_ - 1) : 0)) + 3;
 }
 
 // ---------------------------------------------------------------------------
@@ -410,45 +414,40 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
     q.q_out = d_q_;
     q.kv = kv_[l];
     q.total = d_total_ + l * B_;
-    q.x = d_x_;
-    q.x_stride = static_cast<int>(H_);
+    q.xf = d_xf_resid_;  // harness: the host x prepared into the same buffer
     q.ss_part = d_ss_;
     q.n_ss = l == 0 ? 1 : hblk;  // embedding writes one block; residual writers write hblk
     if (!attn_only_) {
       GemvParams& o = plan_o_[l].p;
       o.ypart = d_ypart_;
       o.counters = d_counters_;
-      o.frag_o = d_frag_o_;
-      o.frag_lse = d_frag_lse_;
-      o.recv = d_recv_;
+      o.xf = d_xf_attn_;
       o.out = dist ? d_parth_ : d_x_;
       o.out_stride = static_cast<int>(H_);
       o.ss_out = dist ? nullptr : d_ss_;
+      o.xf_out = d_xf_resid_;
       GemvParams& gu = plan_gu_[l].p;
       gu.ypart = d_ypart_;
       gu.counters = d_counters_;
-      gu.x = d_x_;
-      gu.x_stride = static_cast<int>(H_);
+      gu.xf = d_xf_resid_;
       gu.ss_part = d_ss_;
       gu.n_ss = hblk;
-      gu.out = d_m_;
-      gu.out_stride = F;
+      gu.xf_out = d_xf_m_;
       GemvParams& dn = plan_down_[l].p;
       dn.ypart = d_ypart_;
       dn.counters = d_counters_;
-      dn.x = d_m_;
-      dn.x_stride = F;
+      dn.xf = d_xf_m_;
       dn.out = dist ? d_parth_ : d_x_;
       dn.out_stride = static_cast<int>(H_);
       dn.ss_out = dist ? nullptr : d_ss_;
+      dn.xf_out = d_xf_resid_;
     }
   }
   if (!attn_only_) {
     GemvParams& lm = plan_lm_.p;
     lm.ypart = d_ypart_;
     lm.counters = d_counters_;
-    lm.x = d_x_;
-    lm.x_stride = static_cast<int>(H_);
+    lm.xf = d_xf_resid_;
     lm.ss_part = d_ss_;
     lm.n_ss = hblk;
     lm.best = d_best_;
@@ -693,12 +692,11 @@ AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) const {
   return a;
 }
 
-void Engine::enqueue_attention(int64_t layer, int qkv_xmode, const float* x, int x_stride) {
-  // 1. QKV projection with fused round-robin append of this token's K/V
-  GemvPlan q = plan_qkv_[layer];
-  q.p.x = x;
-  q.p.x_stride = x_stride;
-  cuda_check(launch_gemv(q.p, qkv_xmode, E_QKV, stream_), "qkv gemv");
+void Engine::enqueue_attention(int64_t layer) {
+  // 1. QKV projection (input fragments already in d_xf_resid_) with fused
+  //    round-robin append of this token's K/V
+  const GemvPlan& q = plan_qkv_[layer];
+  cuda_check(launch_gemv(q.p, q.xmode, E_QKV, num_sms_, stream_), "qkv gemv");
   mark(1);
   if (dist_mode_ != HX_POOL_LOCAL) {
     enqueue_exchange_and_attention_dist(layer);
@@ -778,7 +776,9 @@ void Engine::harness_step_device(int64_t layer, const float* x_dev, float* out_d
     throw StateError("the attention-only harness runs on a local pool; distributed pools use decode_step");
   if (!weights_ready_) throw StateError("weights are not initialised");
   require_context(layer);
-  enqueue_attention(layer, X_PLAIN, x_dev, static_cast<int>(H_));
+  cuda_check(launch_xprep_plain(x_dev, B_, static_cast<int>(H_), static_cast<int>(H_), d_xf_resid_, stream_),
+             "xprep");
+  enqueue_attention(layer);
   cuda_check(launch_merge_out(d_frag_o_, d_frag_lse_, B_, static_cast<int>(Qh_), q_per_slot_, kvp_,
                               static_cast<int>(D_), DP_, out_dev, d_out_lse_, stream_),
              "merge");
@@ -788,35 +788,45 @@ void Engine::harness_step_device(int64_t layer, const float* x_dev, float* out_d
 }
 
 void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
-  cuda_check(launch_embed(emb_, tokens_dev, B_, static_cast<int>(H_), d_x_, d_ss_, stream_), "embed");
+  cuda_check(launch_embed(emb_, tokens_dev, B_, static_cast<int>(H_), d_x_, d_ss_, d_xf_resid_, stream_), "embed");
   mark(0);
   if (capture_hidden_)
     cuda_check(cudaMemcpyAsync(d_hidden_, d_x_, static_cast<size_t>(B_) * H_ * 4, cudaMemcpyDeviceToDevice, stream_),
                "hidden");
   const bool dist = dist_mode_ != HX_POOL_LOCAL;
   for (int64_t l = 0; l < L_; ++l) {
-    enqueue_attention(l, X_NORM, d_x_, static_cast<int>(H_));
+    enqueue_attention(l);
     if (!dist) {
-      cuda_check(launch_gemv(plan_o_[l].p, X_MERGE, E_RESID, stream_), "o-proj");
+      // LSE-rescale combine of the KVP fragments -> O-proj activations (attention.hpp:118-175)
+      cuda_check(launch_xprep_merge_local(d_frag_o_, d_frag_lse_, B_, q_per_slot_, kvp_, static_cast<int>(D_), DP_,
+                                          static_cast<int>(H_), d_xf_attn_, stream_),
+                 "merge");
+      cuda_check(launch_gemv(plan_o_[l].p, 0, E_RESID, num_sms_, stream_), "o-proj");
       mark(4);
-      cuda_check(launch_gemv(plan_gu_[l].p, X_NORM, E_SWIGLU, stream_), "gate/up");
+      cuda_check(launch_gemv(plan_gu_[l].p, 1, E_SWIGLU, num_sms_, stream_), "gate/up");
       mark(5);
-      cuda_check(launch_gemv(plan_down_[l].p, X_PLAIN, E_RESID, stream_), "down");
+      cuda_check(launch_gemv(plan_down_[l].p, 0, E_RESID, num_sms_, stream_), "down");
       mark(6);
     } else {
-      // TP O-proj over this rank's exchanged slice, AllReduce over the pool (latency.cpp:85-94)
-      cuda_check(launch_gemv(plan_o_[l].p, X_RECV, E_STORE, stream_), "o-proj");
+      // merge of the exchanged slices, then TP O-proj over this rank's slice and
+      // AllReduce over the pool (latency.cpp:85-94)
+      cuda_check(launch_xprep_merge_recv(d_recv_, B_, kvp_, xchunk_, slice_, r_, static_cast<int>(D_), d_xf_attn_,
+                                         stream_),
+                 "merge");
+      cuda_check(launch_gemv(plan_o_[l].p, 0, E_STORE, num_sms_, stream_), "o-proj");
       mark(4);
       if (!(skip_comm_ & 2)) transport_->all_reduce_sum(d_parth_, static_cast<size_t>(B_) * H_, stream_);
-      cuda_check(launch_residual_add(d_x_, d_parth_, B_, static_cast<int>(H_), d_ss_, stream_), "residual");
+      cuda_check(launch_residual_add(d_x_, d_parth_, B_, static_cast<int>(H_), d_ss_, d_xf_resid_, stream_),
+                 "residual");
       mark(9);
       // TP FFN over F/N features, AllReduce (latency.cpp:138-144)
-      cuda_check(launch_gemv(plan_gu_[l].p, X_NORM, E_SWIGLU, stream_), "gate/up");
+      cuda_check(launch_gemv(plan_gu_[l].p, 1, E_SWIGLU, num_sms_, stream_), "gate/up");
       mark(5);
-      cuda_check(launch_gemv(plan_down_[l].p, X_PLAIN, E_STORE, stream_), "down");
+      cuda_check(launch_gemv(plan_down_[l].p, 0, E_STORE, num_sms_, stream_), "down");
       mark(6);
       if (!(skip_comm_ & 2)) transport_->all_reduce_sum(d_parth_, static_cast<size_t>(B_) * H_, stream_);
-      cuda_check(launch_residual_add(d_x_, d_parth_, B_, static_cast<int>(H_), d_ss_, stream_), "residual");
+      cuda_check(launch_residual_add(d_x_, d_parth_, B_, static_cast<int>(H_), d_ss_, d_xf_resid_, stream_),
+                 "residual");
       mark(9);
     }
     if (capture_hidden_)
@@ -826,7 +836,7 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
   }
   GemvParams lm = plan_lm_.p;
   lm.out = store_logits_ ? d_logits_ : nullptr;
-  cuda_check(launch_gemv(lm, X_NORM, E_LOGITS, stream_), "lm head");
+  cuda_check(launch_gemv(lm, 1, E_LOGITS, num_sms_, stream_), "lm head");
   if (dist && !(skip_comm_ & 2)) transport_->all_reduce_max_u64(d_best_, static_cast<size_t>(B_), stream_);  // vocab-sharded argmax
   cuda_check(launch_argmax_finish(d_best_, B_, next_dev, d_best_, stream_), "argmax");
   mark(7);
@@ -940,7 +950,7 @@ void Engine::info(hx_engine_info* o) const {
   o->attn_grid = attn_grid_;
   o->kernels_per_step = kernels_per_step_;
   if (!attn_only_ && dist_mode_ != HX_POOL_LOCAL)  // + pack and two residual adds per layer
-    o->kernels_per_step = 1 + L_ * (7 + 3 + (hopb_ ? 3 * (B_ - 1) : 0)) + 2;
+    o->kernels_per_step = 1 + L_ * (14 + (hopb_ ? 3 * (B_ - 1) : 0)) + 3;
   o->page_cap = page_cap_;
   o->head_dim_padded = DP_;
 }

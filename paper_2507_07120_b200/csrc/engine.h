@@ -37,7 +37,7 @@ struct Message {
 
 struct GemvPlan {
   GemvParams p{};
-  int xmode = 0, emode = 0;
+  int xmode = 0, emode = 0;  // xmode: 1 = RMSNorm consumer (scale y by the row's rsqrt(mean x^2))
 };
 
 class Transport;
@@ -82,7 +82,7 @@ class Engine {
   void build_weights_common(uint64_t seed, bool qkv_hash);
   void upload_qkv_host(int64_t layer, const std::vector<double>& wq, const std::vector<double>& wk,
                        const std::vector<double>& wv);
-  void enqueue_attention(int64_t layer, int qkv_xmode, const float* x, int x_stride);
+  void enqueue_attention(int64_t layer);
   void enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev);
   void record_transcript(int64_t layers);
   void require_context(int64_t layer) const;
@@ -133,6 +133,10 @@ class Engine {
   float* d_out_ = nullptr;     // harness out [B][Q][Hsz]
   float* d_out_lse_ = nullptr;
   float* d_hidden_ = nullptr;  // [(L+1)][B][H]
+  uint8_t* d_xf_resid_ = nullptr;  // x-fragments of the residual stream (QKV / gate-up / LM head input)
+  uint8_t* d_xf_attn_ = nullptr;   // x-fragments of the merged attention output (O-proj input)
+  uint8_t* d_xf_m_ = nullptr;      // x-fragments of silu(gate)*up (down-proj input)
+  int* d_plan_ctr_ = nullptr;      // per-GEMV persistent tile queues
   WSeg* d_segs_ = nullptr;
   bool weights_ready_ = false;
   bool capture_hidden_ = false;

@@ -51,32 +51,28 @@ cudaError_t launch_bump_totals(int* total, int n, cudaStream_t stream);
 size_t attn_decode_smem_bytes(int dp);
 
 // ---------------------------------------------------------------- GEMV
-enum XMode : int { X_PLAIN = 0, X_NORM = 1, X_MERGE = 2, X_RECV = 3 };
 enum EMode : int { E_STORE = 0, E_QKV = 1, E_RESID = 2, E_SWIGLU = 3, E_LOGITS = 4 };
 
 struct GemvParams {
-  const uint4* w;        // fragment-major bf16 weights [Npad/16][K/16][32 lanes][16 B]
+  const uint4* w;        // bf16 weights, CTA-tile-major fragments [Npad/128][K/16][8][32 lanes][16 B]
+  const uint8_t* xf;     // input activation fragments for K (xfrag.cuh)
   int N, Npad, K;
-  int ksplit, kr_steps;  // k-steps (16 wide) per split
+  int ksplit, kr_steps;  // k-chunks per 128-row block and k-steps per chunk
+  int n_tiles;           // (Npad/128) * ksplit
+  int* work_counter;     // [2] persistent tile queue (self-resetting), one pair per plan
   int batch;
-  // x source
-  const float* x;        // [B][x_stride] (X_PLAIN, X_NORM)
-  int x_stride;
-  const float* ss_part;  // [n_ss][B] partial sums of squares (X_NORM)
+  // RMSNorm statistics of the input (norm consumers scale y by rsqrt(mean(x^2) + eps))
+  const float* ss_part;  // [n_ss][B]
   int n_ss;
   float eps;
-  const float* frag_o;   // X_MERGE: [slot][B][q_per_slot][DP]
-  const float* frag_lse; // [slot][B][q_per_slot] (natural log)
-  int kvp, q_per_slot, head_dim, dp;
-  const float* recv;     // X_RECV: [kvp src][B][chunk] exchanged slices (+ lse slots)
-  int chunk, slice, exch_rank;
   // split-K plumbing
   float* ypart;          // [ksplit][B][Npad]
   int* counters;         // [Npad/128], self-resetting
   // epilogue
-  float* out;            // E_STORE / E_RESID (in-place residual) / E_SWIGLU / E_LOGITS (optional)
+  float* out;            // E_STORE / E_RESID (in-place residual) / E_LOGITS (optional)
   int out_stride;
   float* ss_out;         // [Npad/128][B] partial sums of squares of the written rows (E_RESID, E_STORE)
+  uint8_t* xf_out;       // E_RESID: fragments of the new residual; E_SWIGLU: fragments of m
   // E_QKV
   float* q_out;          // [B][q_heads][DP]
   uint8_t* kv;           // page pool of this layer
@@ -85,19 +81,30 @@ struct GemvParams {
   int nq, nk, kv_heads, kvh_per_slot, rr_chunk, page_cap, slot_base, n_local_slots;
   int kv_head_base;      // global index of the first KV head in this projection
   int append;            // write K/V into the cache
+  int kvp, head_dim, dp;
   // E_LOGITS
   unsigned long long* best;  // [B] packed (orderable logit, ~index)
   int n_offset;              // global index of row 0 (vocabulary shard offset)
 };
-cudaError_t launch_gemv(const GemvParams& p, int xmode, int emode, cudaStream_t stream);
-size_t gemv_smem_bytes(const GemvParams& p, int xs_terms, bool merge);
+cudaError_t launch_gemv(const GemvParams& p, int norm, int emode, int grid, cudaStream_t stream);
+size_t gemv_smem_bytes(const GemvParams& p);
+
+// x-fragment producers (xfrag.cuh layout; nb8 = ceil(batch / 8))
+cudaError_t launch_xprep_plain(const float* x, int batch, int K, int x_stride, uint8_t* xf, cudaStream_t s);
+// Merged attention output (canonical LSE merge over KVP fragments, attention.hpp:90-137):
+//  local pool: frag_o [slot][B][q_per_slot][DP], frag_lse [slot][B][q_per_slot]; K = hidden
+//  exchanged:  recv [kvp src][B][chunk] (slice + lse slots); K = slice of rank exch_rank
+cudaError_t launch_xprep_merge_local(const float* frag_o, const float* frag_lse, int batch, int q_per_slot,
+                                     int kvp, int head_dim, int dp, int K, uint8_t* xf, cudaStream_t s);
+cudaError_t launch_xprep_merge_recv(const float* recv, int batch, int kvp, int chunk, int slice, int exch_rank,
+                                    int head_dim, uint8_t* xf, cudaStream_t s);
 
 // ---------------------------------------------------------------- misc
 cudaError_t launch_merge_out(const float* frag_o, const float* frag_lse, int batch, int q_heads,
                              int q_per_slot, int kvp, int head_dim, int dp, float* out,
                              float* out_lse, cudaStream_t stream);
 cudaError_t launch_embed(const uint16_t* emb, const int* tokens, int batch, int hidden,
-                         float* x, float* ss_part, cudaStream_t stream);
+                         float* x, float* ss_part, uint8_t* xf, cudaStream_t stream);
 cudaError_t launch_argmax_finish(const unsigned long long* best, int batch, int* tokens_out,
                                  unsigned long long* best_reset, cudaStream_t stream);
 // Scatter n tokens (bf16 K/V rows [n][kv_heads][head_dim]) of request b at global
@@ -138,6 +145,6 @@ cudaError_t launch_pack_exchange(const float* frag_o, const float* frag_lse, int
                                  cudaStream_t s);
 // Residual add of an all-reduced partial product + RMSNorm statistics.
 cudaError_t launch_residual_add(float* x, const float* part, int batch, int hidden, float* ss_part,
-                                cudaStream_t s);
+                                uint8_t* xf, cudaStream_t s);
 
 }  // namespace hx

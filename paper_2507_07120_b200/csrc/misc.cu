@@ -7,6 +7,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "kv_layout.cuh"
+#include "xfrag.cuh"
 
 namespace hx {
 
@@ -65,7 +66,7 @@ cudaError_t launch_merge_out(const float* frag_o, const float* frag_lse, int bat
 // ---------------------------------------------------------------- embedding
 // x[b][:] = E[token_b][:] (bf16 -> fp32); ss_part[0][b] = sum x^2.
 __global__ void embed_kernel(const __nv_bfloat16* emb, const int* tokens, int batch, int hidden,
-                             float* x, float* ss_part) {
+                             float* x, float* ss_part, uint8_t* xf) {
   griddep_wait();
   griddep_launch_dependents();
   const int b = blockIdx.x;
@@ -90,6 +91,7 @@ __global__ void embed_kernel(const __nv_bfloat16* emb, const int* tokens, int ba
       for (int e = 0; e < 8; ++e) {
         const float v = __bfloat162float(h[e]);
         x[static_cast<size_t>(b) * hidden + i * 8 + e] = v;
+        xf_write(xf, (batch + 7) / 8, b, i * 8 + e, v);
         s += v * v;
       }
     }
@@ -108,9 +110,9 @@ __global__ void embed_kernel(const __nv_bfloat16* emb, const int* tokens, int ba
 }
 
 cudaError_t launch_embed(const uint16_t* emb, const int* tokens, int batch, int hidden, float* x,
-                         float* ss_part, cudaStream_t stream) {
+                         float* ss_part, uint8_t* xf, cudaStream_t stream) {
   return launch_k(embed_kernel, dim3(batch), dim3(256), 0, stream, reinterpret_cast<const __nv_bfloat16*>(emb),
-                  tokens, batch, hidden, x, ss_part);
+                  tokens, batch, hidden, x, ss_part, xf);
 }
 
 __global__ void argmax_finish_kernel(const unsigned long long* best, int batch, int* tokens_out,
@@ -440,7 +442,8 @@ cudaError_t launch_pack_exchange(const float* frag_o, const float* frag_lse, int
 }
 
 // x[b][n] += part[b][n]; ss_part[blk][b] = sum over the 128-column block of x^2 (deterministic).
-__global__ void residual_add_kernel(float* x, const float* part, int batch, int hidden, float* ss_part) {
+__global__ void residual_add_kernel(float* x, const float* part, int batch, int hidden, float* ss_part,
+                                    uint8_t* xf) {
   griddep_wait();
   griddep_launch_dependents();
   const int blk = blockIdx.x, b = blockIdx.y;
@@ -449,6 +452,7 @@ __global__ void residual_add_kernel(float* x, const float* part, int batch, int 
   if (n < hidden) {
     v = x[static_cast<size_t>(b) * hidden + n] + part[static_cast<size_t>(b) * hidden + n];
     x[static_cast<size_t>(b) * hidden + n] = v;
+    xf_write(xf, (batch + 7) / 8, b, n, v);
   }
   float s = v * v;
 #pragma unroll
@@ -459,8 +463,105 @@ __global__ void residual_add_kernel(float* x, const float* part, int batch, int 
   if (threadIdx.x == 0) ss_part[static_cast<size_t>(blk) * batch + b] = (red[0] + red[1]) + (red[2] + red[3]);
 }
 cudaError_t launch_residual_add(float* x, const float* part, int batch, int hidden, float* ss_part,
-                                cudaStream_t s) {
+                                uint8_t* xf, cudaStream_t s) {
   return launch_k(residual_add_kernel, dim3((hidden + 127) / 128, batch), dim3(128), 0, s, x, part, batch, hidden,
-                  ss_part);
+                  ss_part, xf);
+}
+}  // namespace hx
+
+// ---------------------------------------------------------------- x-fragment producers
+namespace hx {
+__global__ void xprep_plain_kernel(const float* x, int batch, int K, int x_stride, uint8_t* xf) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<long long>(batch) * K) return;
+  const int b = static_cast<int>(i / K), k = static_cast<int>(i % K);
+  xf_write(xf, (batch + 7) / 8, b, k, x[static_cast<size_t>(b) * x_stride + k]);
+}
+cudaError_t launch_xprep_plain(const float* x, int batch, int K, int x_stride, uint8_t* xf, cudaStream_t s) {
+  const long long n = static_cast<long long>(batch) * K;
+  return launch_k(xprep_plain_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, x, batch, K,
+                  x_stride, xf);
+}
+
+// Canonical merge (attention.hpp:90-137): descending lse, ties by source rank.
+__device__ __forceinline__ float merge_sources(const float* lse, const float* o, int kvp) {
+  int ord[8];
+  for (int r = 0; r < kvp; ++r) ord[r] = r;
+  for (int i = 1; i < kvp; ++i) {
+    const int v = ord[i];
+    int j = i - 1;
+    while (j >= 0 && lse[ord[j]] < lse[v]) {
+      ord[j + 1] = ord[j];
+      --j;
+    }
+    ord[j + 1] = v;
+  }
+  const float m = lse[ord[0]];
+  if (m == -INFINITY) return 0.f;
+  float acc = 0.f, z = 0.f;
+  for (int i = 0; i < kvp; ++i) {
+    const int r = ord[i];
+    if (lse[r] == -INFINITY) continue;
+    const float w = __expf(lse[r] - m);
+    acc += w * o[r];
+    z += w;
+  }
+  return acc / z;
+}
+
+__global__ void xprep_merge_local_kernel(const float* frag_o, const float* frag_lse, int batch, int q_per_slot,
+                                         int kvp, int head_dim, int dp, int K, uint8_t* xf) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<long long>(batch) * K) return;
+  const int b = static_cast<int>(i / K), k = static_cast<int>(i % K);
+  const int head = k / head_dim, d = k - head * head_dim;
+  const int grp = head / q_per_slot, qi = head - grp * q_per_slot;
+  float lse[8], o[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    if (r < kvp) {
+      const size_t f = (static_cast<size_t>(grp * kvp + r) * batch + b) * q_per_slot + qi;
+      lse[r] = frag_lse[f];
+      o[r] = frag_o[f * dp + d];
+    }
+  }
+  xf_write(xf, (batch + 7) / 8, b, k, merge_sources(lse, o, kvp));
+}
+cudaError_t launch_xprep_merge_local(const float* frag_o, const float* frag_lse, int batch, int q_per_slot,
+                                     int kvp, int head_dim, int dp, int K, uint8_t* xf, cudaStream_t s) {
+  const long long n = static_cast<long long>(batch) * K;
+  return launch_k(xprep_merge_local_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, frag_o,
+                  frag_lse, batch, q_per_slot, kvp, head_dim, dp, K, xf);
+}
+
+__global__ void xprep_merge_recv_kernel(const float* recv, int batch, int kvp, int chunk, int slice, int exch_rank,
+                                        int head_dim, uint8_t* xf) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<long long>(batch) * slice) return;
+  const int b = static_cast<int>(i / slice), k = static_cast<int>(i % slice);
+  const int first = (exch_rank * slice) / head_dim;
+  const int head = (exch_rank * slice + k) / head_dim;
+  float lse[8], o[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    if (r < kvp) {
+      const float* src = recv + (static_cast<size_t>(r) * batch + b) * chunk;
+      lse[r] = src[slice + head - first];
+      o[r] = src[k];
+    }
+  }
+  xf_write(xf, (batch + 7) / 8, b, k, merge_sources(lse, o, kvp));
+}
+cudaError_t launch_xprep_merge_recv(const float* recv, int batch, int kvp, int chunk, int slice, int exch_rank,
+                                    int head_dim, uint8_t* xf, cudaStream_t s) {
+  const long long n = static_cast<long long>(batch) * slice;
+  return launch_k(xprep_merge_recv_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, recv,
+                  batch, kvp, chunk, slice, exch_rank, head_dim, xf);
 }
 }  // namespace hx

@@ -1,0 +1,40 @@
+// Activation fragments ("xf"): the B x K activation matrix pre-split into bf16
+// terms in the exact register image of the GEMV's mma.sync B operand, written
+// ONCE by whoever produces the activation (embedding, residual epilogues,
+// SwiGLU epilogue, the attention merge) and streamed by the GEMV next to its
+// weights with the TMA bulk engine.
+//
+// Layout: [k-step ks][term t < 3][batch group bg < NB8][lane][2 x u32]
+//   lane (g = lane/4, c = lane%4), batch b = 8*bg + g:
+//   u32 0 = (x[b][16ks+2c], x[b][16ks+2c+1]), u32 1 = (x[b][16ks+2c+8], x[b][16ks+2c+9])
+//   terms: hi = bf16(x), mid = bf16(x - hi), lo = bf16(x - hi - mid); a GEMV
+//   that needs ~16-bit activations reads hi+mid, the QKV projection all three.
+#pragma once
+
+#include "common.cuh"
+
+namespace hx {
+
+constexpr int kXfTerms = 3;
+
+__host__ __device__ __forceinline__ size_t xf_step_bytes(int nb8) {
+  return static_cast<size_t>(kXfTerms) * nb8 * 32 * 8;
+}
+
+// Write activation value v of (batch b, column k) into the fragment buffer.
+HX_DEV void xf_write(uint8_t* xf, int nb8, int b, int k, float v) {
+  const int ks = k >> 4, r = k & 15;
+  const int half = r >> 3, c = (r & 7) >> 1, elem = r & 1;
+  const int g = b & 7, bg = b >> 3;
+  const int lane = g * 4 + c;
+  float t[3];
+  split3(v, t[0], t[1], t[2]);
+#pragma unroll
+  for (int term = 0; term < kXfTerms; ++term) {
+    const size_t off = ((static_cast<size_t>(ks) * kXfTerms + term) * nb8 + bg) * 32 * 8 + lane * 8 + half * 4 +
+                       elem * 2;
+    *reinterpret_cast<__nv_bfloat16*>(xf + off) = __float2bfloat16_rn(t[term]);
+  }
+}
+
+}  // namespace hx
