@@ -336,11 +336,11 @@ void Engine::plan_gemvs() {
   }
   // launches per step (each GEMV = streaming kernel + epilogue kernel)
   if (attn_only_)
-    kernels_per_step_ = 7;  // xprep, qkv x2, attention, split-reduce, bump, merge
+    kernels_per_step_ = 6;  // xprep, qkv x2, attention, split-reduce, merge(+bump)
   else if (!dist)
-    kernels_per_step_ = 1 + 12 * L_ + 3;
+    kernels_per_step_ = 1 + 11 * L_ + 3;
   else  // + pack and two residual adds per layer; per-request attention launches under HOP-B
-    kernels_per_step_ = 1 + L_ * (14 + (hopb_ ? 3 * (B_ - 1) : 0)) + 3;
+    kernels_per_step_ = 1 + L_ * (13 + (hopb_ ? 3 * (B_ - 1) : 0)) + 3;
 }
 
 // ---------------------------------------------------------------------------
@@ -706,9 +706,9 @@ void Engine::enqueue_attention(int64_t layer) {
   const AttnParams a = attn_params(layer, 0, B_);
   cuda_check(launch_attn_decode(a, attn_grid_, stream_), "attention");
   mark(2);
-  // 3. per-rank fragments (split merge), then bump the totals (append is now visible)
+  // 3. per-rank fragments (split merge); the token totals are bumped by the
+  //    next kernel (merge), after which the appended token counts
   cuda_check(launch_attn_split_reduce(a, d_frag_o_, d_frag_lse_, stream_), "split reduce");
-  cuda_check(launch_bump_totals(d_total_ + layer * B_, B_, stream_), "bump totals");
   mark(3);
 }
 
@@ -750,7 +750,6 @@ void Engine::enqueue_exchange_and_attention_dist(int64_t layer) {
     cuda_check(cudaEventRecord(hop_events_.back(), comm_stream_), "hopb join");
     cuda_check(cudaStreamWaitEvent(stream_, hop_events_.back(), 0), "hopb join wait");
   }
-  cuda_check(launch_bump_totals(d_total_ + layer * B_, B_, stream_), "bump totals");
   mark(9);
 }
 
@@ -780,7 +779,7 @@ void Engine::harness_step_device(int64_t layer, const float* x_dev, float* out_d
              "xprep");
   enqueue_attention(layer);
   cuda_check(launch_merge_out(d_frag_o_, d_frag_lse_, B_, static_cast<int>(Qh_), q_per_slot_, kvp_,
-                              static_cast<int>(D_), DP_, out_dev, d_out_lse_, stream_),
+                              static_cast<int>(D_), DP_, out_dev, d_out_lse_, d_total_ + layer * B_, stream_),
              "merge");
   mark(8);
   for (int b = 0; b < B_; ++b) h_total_[static_cast<size_t>(layer * B_ + b)] += 1;
@@ -799,7 +798,7 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
     if (!dist) {
       // LSE-rescale combine of the KVP fragments -> O-proj activations (attention.hpp:118-175)
       cuda_check(launch_xprep_merge_local(d_frag_o_, d_frag_lse_, B_, q_per_slot_, kvp_, static_cast<int>(D_), DP_,
-                                          static_cast<int>(H_), d_xf_attn_, stream_),
+                                          static_cast<int>(H_), d_xf_attn_, d_total_ + l * B_, stream_),
                  "merge");
       cuda_check(launch_gemv(plan_o_[l].p, 0, E_RESID, num_sms_, stream_), "o-proj");
       mark(4);
@@ -811,7 +810,7 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
       // merge of the exchanged slices, then TP O-proj over this rank's slice and
       // AllReduce over the pool (latency.cpp:85-94)
       cuda_check(launch_xprep_merge_recv(d_recv_, B_, kvp_, xchunk_, slice_, r_, static_cast<int>(D_), d_xf_attn_,
-                                         stream_),
+                                         d_total_ + l * B_, stream_),
                  "merge");
       cuda_check(launch_gemv(plan_o_[l].p, 0, E_STORE, num_sms_, stream_), "o-proj");
       mark(4);
@@ -950,7 +949,7 @@ void Engine::info(hx_engine_info* o) const {
   o->attn_grid = attn_grid_;
   o->kernels_per_step = kernels_per_step_;
   if (!attn_only_ && dist_mode_ != HX_POOL_LOCAL)  // + pack and two residual adds per layer
-    o->kernels_per_step = 1 + L_ * (14 + (hopb_ ? 3 * (B_ - 1) : 0)) + 3;
+    o->kernels_per_step = 1 + L_ * (13 + (hopb_ ? 3 * (B_ - 1) : 0)) + 3;
   o->page_cap = page_cap_;
   o->head_dim_padded = DP_;
 }

@@ -20,6 +20,8 @@
 //   E_STORE  plain store (tensor-parallel partial products before AllReduce)
 // RMSNorm without a weight is a per-row scalar: (x * s) W = s * (x W), so
 // normalised consumers multiply y by s = rsqrt(mean(x^2) + eps) in the epilogue.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "kv_layout.cuh"
@@ -201,16 +203,19 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemv_kernel(const GemvParams
 // Epilogue: one CTA per 128-row block reduces the split-K partials in split
 // order (deterministic) and applies the fused epilogue.
 template <int NB8, int EM, bool NORM>
-__global__ void __launch_bounds__(kThreads) gemv_epilogue_kernel(const GemvParams p) {
+__global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p) {
+  // One thread per (row, request) element of a 128-row block; every global load
+  // an element needs (its split partials, the old residual) is issued before use.
   __shared__ float s_inv[16];
   __shared__ float vt[16][kRows];
   __shared__ unsigned long long s_best[16];
+  __shared__ long long s_pos[16][2];  // E_QKV: append (rank, local row) per request
   griddep_wait();
   griddep_launch_dependents();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const int nb = blockIdx.x;
   if (NORM) {
-    for (int b = warp; b < p.batch; b += kThreads / 32) {
+    for (int b = warp; b < p.batch; b += nwarps) {
       float ss = 0.f;
       for (int i = lane; i < p.n_ss; i += 32) ss += p.ss_part[i * p.batch + b];
 #pragma unroll
@@ -218,82 +223,92 @@ __global__ void __launch_bounds__(kThreads) gemv_epilogue_kernel(const GemvParam
       if (lane == 0) s_inv[b] = rsqrtf(ss / static_cast<float>(p.K) + p.eps);
     }
   }
+  if (EM == E_QKV && threadIdx.x < p.batch) {
+    const long long g = p.total[threadIdx.x];
+    s_pos[threadIdx.x][0] = rr_rank(g, p.rr_chunk, p.kvp);
+    s_pos[threadIdx.x][1] = rr_row(g, p.rr_chunk, p.kvp);
+  }
   if (EM == E_LOGITS && threadIdx.x < 16) s_best[threadIdx.x] = 0ull;
+  if (EM == E_STORE || EM == E_RESID)
+    for (int i = threadIdx.x; i < 16 * kRows; i += blockDim.x) vt[i / kRows][i % kRows] = 0.f;
   __syncthreads();
   const int rows_here = EM == E_SWIGLU ? kRows / 2 : kRows;
-  for (int e = threadIdx.x; e < rows_here * p.batch; e += kThreads) {
+  const size_t stride = static_cast<size_t>(p.batch) * p.Npad;
+  constexpr int NP = 2;  // partial streams per element (SwiGLU: gate + up)
+  for (int e = threadIdx.x; e < rows_here * p.batch; e += blockDim.x) {
     const int r = e % rows_here, b = e / rows_here;
-    auto ysum = [&](int rr) {
-      // all split partials are loaded before summing (split order: deterministic)
-      const float* base = p.ypart + static_cast<size_t>(b) * p.Npad + nb * kRows + rr;
-      const size_t stride = static_cast<size_t>(p.batch) * p.Npad;
-      float y = 0.f;
-      for (int s0 = 0; s0 < p.ksplit; s0 += 16) {
-        float v[16];
+    const int np = EM == E_SWIGLU ? 2 : 1;
+    float y[NP] = {0.f, 0.f};
+    float old = 0.f;
+    const int n = nb * kRows + r;
+    if (EM == E_RESID && n < p.N) old = p.out[static_cast<size_t>(b) * p.out_stride + n];
+    for (int s0 = 0; s0 < p.ksplit; s0 += 16) {
+      float v[NP][16];
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = s0 + j < p.ksplit ? __ldcg(base + (s0 + j) * stride) : 0.f;
+      for (int q = 0; q < NP; ++q) {
+        const float* base = p.ypart + static_cast<size_t>(b) * p.Npad + nb * kRows + r + q * (kRows / 2);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) y += v[j];
+        for (int j = 0; j < 16; ++j) v[q][j] = (q < np && s0 + j < p.ksplit) ? __ldcg(base + (s0 + j) * stride) : 0.f;
       }
-      return NORM ? y * s_inv[b] : y;
-    };
+#pragma unroll
+      for (int q = 0; q < NP; ++q)
+#pragma unroll
+        for (int j = 0; j < 16; ++j) y[q] += v[q][j];  // split order: deterministic
+    }
+    if (NORM) {
+      y[0] *= s_inv[b];
+      y[1] *= s_inv[b];
+    }
     if (EM == E_SWIGLU) {
-      const float gt = ysum(r), up = ysum(r + kRows / 2);
       const int f = nb * (kRows / 2) + r;
-      if (f < p.N / 2) xf_write(p.xf_out, NB8, b, f, gt / (1.f + __expf(-gt)) * up);
+      if (f < p.N / 2) xf_write(p.xf_out, NB8, b, f, y[0] / (1.f + __expf(-y[0])) * y[1]);
       continue;
     }
-    const float y = ysum(r);
-    const int n = nb * kRows + r;
-    float keep = 0.f;
-    if (n < p.N) {
-      if (EM == E_STORE) {
-        p.out[static_cast<size_t>(b) * p.out_stride + n] = y;
-        keep = y;
-      } else if (EM == E_RESID) {
-        float* o = p.out + static_cast<size_t>(b) * p.out_stride + n;
-        keep = *o + y;
-        *o = keep;
-        xf_write(p.xf_out, NB8, b, n, keep);
-      } else if (EM == E_LOGITS) {
-        if (p.out) p.out[static_cast<size_t>(b) * p.out_stride + n] = y;
-        atomicMax(&s_best[b], logit_key(y, n + p.n_offset));
-      } else if (EM == E_QKV) {
-        if (n < p.nq) {
-          const int head = n / p.head_dim, d = n - head * p.head_dim;
-          const int q_heads = p.nq / p.head_dim;
-          p.q_out[(static_cast<size_t>(b) * q_heads + head) * p.dp + d] = y;
-        } else {
-          const int kvn = n - p.nq;
-          const int is_v = kvn >= p.nk;
-          const int kn = is_v ? kvn - p.nk : kvn;
-          const int hl = kn / p.head_dim, d = kn - hl * p.head_dim;
-          const int h = p.kv_head_base + hl;
-          if (p.kv_dbg)
-            p.kv_dbg[((static_cast<size_t>(b) * 2 + is_v) * p.kv_heads + hl) * p.head_dim + d] = y;
-          if (p.append) {
-            const long long g = p.total[b];
-            const int rank = rr_rank(g, p.rr_chunk, p.kvp);
-            const long long row = rr_row(g, p.rr_chunk, p.kvp);
-            const int grp = h / p.kvh_per_slot, kvh = h - grp * p.kvh_per_slot;
-            const int slot_local = grp * p.kvp + rank - p.slot_base;
-            if (slot_local >= 0 && slot_local < p.n_local_slots) {
-              const size_t page =
-                  ((static_cast<size_t>(slot_local) * p.batch + b) * p.kvh_per_slot + kvh) * p.page_cap +
-                  static_cast<size_t>(row >> 4);
-              const uint32_t off = is_v ? v_offset(p.dp, static_cast<int>(row & 15), d)
-                                        : k_offset(p.dp, static_cast<int>(row & 15), d);
-              *reinterpret_cast<__nv_bfloat16*>(p.kv + page * page_bytes(p.dp) + off) = __float2bfloat16_rn(y);
-            }
+    if (n >= p.N) continue;
+    if (EM == E_STORE) {
+      p.out[static_cast<size_t>(b) * p.out_stride + n] = y[0];
+      vt[b][r] = y[0] * y[0];
+    } else if (EM == E_RESID) {
+      const float keep = old + y[0];
+      p.out[static_cast<size_t>(b) * p.out_stride + n] = keep;
+      xf_write(p.xf_out, NB8, b, n, keep);
+      vt[b][r] = keep * keep;
+    } else if (EM == E_LOGITS) {
+      if (p.out) p.out[static_cast<size_t>(b) * p.out_stride + n] = y[0];
+      atomicMax(&s_best[b], logit_key(y[0], n + p.n_offset));
+    } else if (EM == E_QKV) {
+      if (n < p.nq) {
+        const int head = n / p.head_dim, d = n - head * p.head_dim;
+        const int q_heads = p.nq / p.head_dim;
+        p.q_out[(static_cast<size_t>(b) * q_heads + head) * p.dp + d] = y[0];
+      } else {
+        const int kvn = n - p.nq;
+        const int is_v = kvn >= p.nk;
+        const int kn = is_v ? kvn - p.nk : kvn;
+        const int hl = kn / p.head_dim, d = kn - hl * p.head_dim;
+        const int h = p.kv_head_base + hl;
+        if (p.kv_dbg)
+          p.kv_dbg[((static_cast<size_t>(b) * 2 + is_v) * p.kv_heads + hl) * p.head_dim + d] = y[0];
+        if (p.append) {
+          const int rank = static_cast<int>(s_pos[b][0]);
+          const long long row = s_pos[b][1];
+          const int grp = h / p.kvh_per_slot, kvh = h - grp * p.kvh_per_slot;
+          const int slot_local = grp * p.kvp + rank - p.slot_base;
+          if (slot_local >= 0 && slot_local < p.n_local_slots) {
+            const size_t page =
+                ((static_cast<size_t>(slot_local) * p.batch + b) * p.kvh_per_slot + kvh) * p.page_cap +
+                static_cast<size_t>(row >> 4);
+            const uint32_t off = is_v ? v_offset(p.dp, static_cast<int>(row & 15), d)
+                                      : k_offset(p.dp, static_cast<int>(row & 15), d);
+            *reinterpret_cast<__nv_bfloat16*>(p.kv + page * page_bytes(p.dp) + off) = __float2bfloat16_rn(y[0]);
           }
         }
       }
     }
-    if (EM == E_STORE || EM == E_RESID) vt[b][r] = keep * keep;
   }
   if ((EM == E_STORE || EM == E_RESID) && p.ss_out) {
     __syncthreads();
-    for (int b = warp; b < p.batch; b += kThreads / 32) {
+    for (int b = warp; b < p.batch; b += nwarps) {
       float s = 0.f;
       for (int r = lane; r < kRows; r += 32) s += vt[b][r];
 #pragma unroll
@@ -324,7 +339,9 @@ static cudaError_t launch_t(const GemvParams& p, int grid, cudaStream_t stream) 
   }
   cudaError_t e = launch_k(gemv_kernel<NB8, EM, XS, NORM>, dim3(grid), dim3(kThreads + 32), smem, stream, p);
   if (e != cudaSuccess) return e;
-  return launch_k(gemv_epilogue_kernel<NB8, EM, NORM>, dim3(p.Npad / kRows), dim3(kThreads), 0, stream, p);
+  const int rows_here = EM == E_SWIGLU ? kRows / 2 : kRows;
+  const int threads = std::min(1024, (rows_here * p.batch + 31) / 32 * 32);
+  return launch_k(gemv_epilogue_kernel<NB8, EM, NORM>, dim3(p.Npad / kRows), dim3(threads), 0, stream, p);
 }
 
 template <int NB8>

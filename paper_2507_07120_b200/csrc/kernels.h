@@ -94,15 +94,18 @@ cudaError_t launch_xprep_plain(const float* x, int batch, int K, int x_stride, u
 // Merged attention output (canonical LSE merge over KVP fragments, attention.hpp:90-137):
 //  local pool: frag_o [slot][B][q_per_slot][DP], frag_lse [slot][B][q_per_slot]; K = hidden
 //  exchanged:  recv [kvp src][B][chunk] (slice + lse slots); K = slice of rank exch_rank
+// Both also bump the layer's per-request token totals (bump_total may be null):
+// the attention has read them, so the token appended by the QKV epilogue now counts.
 cudaError_t launch_xprep_merge_local(const float* frag_o, const float* frag_lse, int batch, int q_per_slot,
-                                     int kvp, int head_dim, int dp, int K, uint8_t* xf, cudaStream_t s);
+                                     int kvp, int head_dim, int dp, int K, uint8_t* xf, int* bump_total,
+                                     cudaStream_t s);
 cudaError_t launch_xprep_merge_recv(const float* recv, int batch, int kvp, int chunk, int slice, int exch_rank,
-                                    int head_dim, uint8_t* xf, cudaStream_t s);
+                                    int head_dim, uint8_t* xf, int* bump_total, cudaStream_t s);
 
 // ---------------------------------------------------------------- misc
 cudaError_t launch_merge_out(const float* frag_o, const float* frag_lse, int batch, int q_heads,
                              int q_per_slot, int kvp, int head_dim, int dp, float* out,
-                             float* out_lse, cudaStream_t stream);
+                             float* out_lse, int* bump_total, cudaStream_t stream);
 cudaError_t launch_embed(const uint16_t* emb, const int* tokens, int batch, int hidden,
                          float* x, float* ss_part, uint8_t* xf, cudaStream_t stream);
 cudaError_t launch_argmax_finish(const unsigned long long* best, int batch, int* tokens_out,

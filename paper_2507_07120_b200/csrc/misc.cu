@@ -16,10 +16,12 @@ namespace hx {
 // (merge_fragments / merge_head_fragments, attention.hpp:118-175).
 __global__ void merge_out_kernel(const float* frag_o, const float* frag_lse, int batch,
                                  int q_heads, int q_per_slot, int kvp, int head_dim, int dp,
-                                 float* out, float* out_lse) {
+                                 float* out, float* out_lse, int* bump_total) {
   griddep_wait();
   griddep_launch_dependents();
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int gi = blockIdx.x * blockDim.x + threadIdx.x;
+  if (bump_total && gi < batch) bump_total[gi] += 1;  // attend-then-append: the new token now counts
+  const int warp = gi >> 5, lane = threadIdx.x & 31;
   if (warp >= batch * q_heads) return;
   const int b = warp / q_heads, head = warp - b * q_heads;
   const int grp = head / q_per_slot, qi = head - grp * q_per_slot;
@@ -57,10 +59,10 @@ __global__ void merge_out_kernel(const float* frag_o, const float* frag_lse, int
 
 cudaError_t launch_merge_out(const float* frag_o, const float* frag_lse, int batch, int q_heads,
                              int q_per_slot, int kvp, int head_dim, int dp, float* out,
-                             float* out_lse, cudaStream_t stream) {
+                             float* out_lse, int* bump_total, cudaStream_t stream) {
   const int warps = batch * q_heads;
   return launch_k(merge_out_kernel, dim3((warps * 32 + 255) / 256), dim3(256), 0, stream, frag_o, frag_lse,
-                  batch, q_heads, q_per_slot, kvp, head_dim, dp, out, out_lse);
+                  batch, q_heads, q_per_slot, kvp, head_dim, dp, out, out_lse, bump_total);
 }
 
 // ---------------------------------------------------------------- embedding
@@ -512,10 +514,12 @@ __device__ __forceinline__ float merge_sources(const float* lse, const float* o,
 }
 
 __global__ void xprep_merge_local_kernel(const float* frag_o, const float* frag_lse, int batch, int q_per_slot,
-                                         int kvp, int head_dim, int dp, int K, uint8_t* xf) {
+                                         int kvp, int head_dim, int dp, int K, uint8_t* xf, int* bump_total) {
   griddep_wait();
   griddep_launch_dependents();
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  // the attention of this layer has read its token totals: the appended token now counts
+  if (bump_total && i < batch) bump_total[i] += 1;
   if (i >= static_cast<long long>(batch) * K) return;
   const int b = static_cast<int>(i / K), k = static_cast<int>(i % K);
   const int head = k / head_dim, d = k - head * head_dim;
@@ -532,17 +536,19 @@ __global__ void xprep_merge_local_kernel(const float* frag_o, const float* frag_
   xf_write(xf, (batch + 7) / 8, b, k, merge_sources(lse, o, kvp));
 }
 cudaError_t launch_xprep_merge_local(const float* frag_o, const float* frag_lse, int batch, int q_per_slot,
-                                     int kvp, int head_dim, int dp, int K, uint8_t* xf, cudaStream_t s) {
+                                     int kvp, int head_dim, int dp, int K, uint8_t* xf, int* bump_total,
+                                     cudaStream_t s) {
   const long long n = static_cast<long long>(batch) * K;
   return launch_k(xprep_merge_local_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, frag_o,
-                  frag_lse, batch, q_per_slot, kvp, head_dim, dp, K, xf);
+                  frag_lse, batch, q_per_slot, kvp, head_dim, dp, K, xf, bump_total);
 }
 
 __global__ void xprep_merge_recv_kernel(const float* recv, int batch, int kvp, int chunk, int slice, int exch_rank,
-                                        int head_dim, uint8_t* xf) {
+                                        int head_dim, uint8_t* xf, int* bump_total) {
   griddep_wait();
   griddep_launch_dependents();
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (bump_total && i < batch) bump_total[i] += 1;
   if (i >= static_cast<long long>(batch) * slice) return;
   const int b = static_cast<int>(i / slice), k = static_cast<int>(i % slice);
   const int first = (exch_rank * slice) / head_dim;
@@ -559,9 +565,9 @@ __global__ void xprep_merge_recv_kernel(const float* recv, int batch, int kvp, i
   xf_write(xf, (batch + 7) / 8, b, k, merge_sources(lse, o, kvp));
 }
 cudaError_t launch_xprep_merge_recv(const float* recv, int batch, int kvp, int chunk, int slice, int exch_rank,
-                                    int head_dim, uint8_t* xf, cudaStream_t s) {
+                                    int head_dim, uint8_t* xf, int* bump_total, cudaStream_t s) {
   const long long n = static_cast<long long>(batch) * slice;
   return launch_k(xprep_merge_recv_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, recv,
-                  batch, kvp, chunk, slice, exch_rank, head_dim, xf);
+                  batch, kvp, chunk, slice, exch_rank, head_dim, xf, bump_total);
 }
 }  // namespace hx
