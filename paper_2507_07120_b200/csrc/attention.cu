@@ -86,17 +86,23 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
       bool waited = false;  // q rows come from the QKV kernel: wait before staging them
       for (;;) {
         const int item = atomicAdd(p.work_counter, 1);
-        bool done = item >= p.n_items;
+        const bool done = item >= p.n_items;
         int stream = 0, pg0 = 0, pg1 = 0, ntok = 0, rows = 0;
+        const uint8_t* kv_base = nullptr;
+        const float* q_src = nullptr;
         if (!done) {
+          // decode the item once: (split, stream) -> (slot, request, kv head, query chunk)
           const int split = item / p.n_streams;
           stream = item - split * p.n_streams;
-          // stream -> (slot, request, kv head, query chunk)
           int t = stream;
-          const int qc = t % p.q_chunks; t /= p.q_chunks;
+          const int qc = t % p.q_chunks;
+          t /= p.q_chunks;
+          const int kvh = t % p.kvh_per_slot;
           t /= p.kvh_per_slot;
-          const int b = t % p.stream_batch + p.b_begin;
-          const int slot = t / p.stream_batch + p.slot_base;
+          const int bl = t % p.stream_batch;
+          const int sl = t / p.stream_batch;
+          const int b = bl + p.b_begin;
+          const int slot = sl + p.slot_base;
           const int rank = slot % p.kvp;
           ntok = static_cast<int>(rr_count(p.total[b], rank, p.chunk, p.kvp));
           const int pages = (ntok + 15) >> 4;
@@ -105,6 +111,11 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           const int g_rows = p.group - qc * 8;
           rows = g_rows < 8 ? g_rows : 8;
           if (pg1 <= pg0) continue;  // empty split: nothing to emit
+          const size_t pool_stream = (static_cast<size_t>(sl) * p.batch + b) * p.kvh_per_slot + kvh;
+          kv_base = p.kv + pool_stream * p.page_cap * static_cast<size_t>(Cfg::PAGE);
+          const int grp = slot / p.kvp;
+          const int head0 = ((grp - p.q_grp_base) * p.kvh_per_slot + kvh) * p.group + qc * 8;
+          q_src = p.q + (static_cast<size_t>(b) * p.q_heads + head0) * DP;
         }
         const int nchunks = done ? 1 : (pg1 - pg0 + NWC - 1) / NWC;
         for (int ch = 0; ch < nchunks; ++ch, ++st) {
@@ -131,34 +142,15 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           m.last = ch == nchunks - 1;
           m.rows = rows;
           uint8_t* dst = stages + s * STAGE_BYTES;
-          // KV stream index in the page pool: ((slot_local * batch + b) * kvh_per_slot + kvh)
-          int ts = stream / p.q_chunks;
-          const int kvh_s = ts % p.kvh_per_slot;
-          ts /= p.kvh_per_slot;
-          const int b_s = ts % p.stream_batch + p.b_begin, sl_s = ts / p.stream_batch;
-          const size_t pool_stream = (static_cast<size_t>(sl_s) * p.batch + b_s) * p.kvh_per_slot + kvh_s;
-          const uint8_t* src = p.kv + (pool_stream * p.page_cap + a) * Cfg::PAGE;
-          uint32_t bytes = np * Cfg::PAGE;
-          uint32_t qbytes = 0;
-          if (ch == 0) qbytes = static_cast<uint32_t>(rows) * DP * 4;
+          const uint32_t bytes = np * Cfg::PAGE;
+          const uint32_t qbytes = ch == 0 ? static_cast<uint32_t>(rows) * DP * 4 : 0u;
           mbar_arrive_expect_tx(&full[s], bytes + qbytes);
-          bulk_g2s(dst, src, bytes, &full[s]);  // KV pages: independent of the previous kernel
+          bulk_g2s(dst, kv_base + static_cast<size_t>(a) * Cfg::PAGE, bytes, &full[s]);  // KV: no dependency
           if (!waited) {
             griddep_wait();
             waited = true;
           }
-          if (qbytes) {
-            // q rows of this stream: [request][head][DP] fp32, heads contiguous
-            int t = stream;
-            const int qc = t % p.q_chunks; t /= p.q_chunks;
-            const int kvh = t % p.kvh_per_slot; t /= p.kvh_per_slot;
-            const int b = t % p.stream_batch + p.b_begin;
-            const int slot = t / p.stream_batch + p.slot_base;
-            const int grp = slot / p.kvp;
-            const int head0 = ((grp - p.q_grp_base) * p.kvh_per_slot + kvh) * p.group + qc * 8;
-            const float* qsrc = p.q + (static_cast<size_t>(b) * p.q_heads + head0) * DP;
-            bulk_g2s(dst + STAGE_KV, qsrc, qbytes, &full[s]);
-          }
+          if (qbytes) bulk_g2s(dst + STAGE_KV, q_src, qbytes, &full[s]);
         }
         if (done) break;
       }
