@@ -51,6 +51,11 @@ typedef struct hx_model_config {
   int64_t vocab;
   int32_t attention_only; /* 1: DecodeHarness semantics only (no norm/O/FFN/LM head) */
   int32_t reserved;
+  /* MoE FFN (types.hpp:19-25): n_experts > 0 replaces the dense FFN by top_k-of-n_experts
+   * routed SwiGLU experts of width expert_ffn plus a shared expert of width `ffn` (0: none). */
+  int64_t n_experts;
+  int64_t top_k;
+  int64_t expert_ffn;
 } hx_model_config;
 
 typedef struct hx_loopback hx_loopback;
@@ -65,6 +70,7 @@ typedef struct hx_parallel_config {
   int32_t rank;         /* global rank id g*kvp + r (attention.hpp:555) when distributed */
   const void* nccl_unique_id; /* 128 bytes (ncclUniqueId) for HX_POOL_NCCL */
   hx_loopback* loopback;      /* shared group for HX_POOL_LOOPBACK */
+  int64_t ep;           /* MoE expert parallelism (types.hpp:100); tpf = tpa*kvp/ep. 0 or 1: ep = 1 */
 } hx_parallel_config;
 
 #define HX_POOL_LOCAL 0

@@ -3,6 +3,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <numeric>
 
 namespace helix_oracle {
 
@@ -45,8 +46,10 @@ ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, st
     : d_(d), batch_(batch), seed_(seed), bf16_(bf16) {
   if (d.hidden != d.query_heads * d.head_size)
     throw std::invalid_argument("hidden_dim must equal query_heads * head_size");
+  if (d.n_experts > 0 && (d.top_k < 1 || d.top_k > d.n_experts || d.expert_ffn < 1))
+    throw std::invalid_argument("invalid MoE shape");
   const double sh = 1.0 / std::sqrt(static_cast<double>(d.hidden));
-  const double sf = 1.0 / std::sqrt(static_cast<double>(d.ffn));
+  const double sf = 1.0 / std::sqrt(static_cast<double>(std::max<i64>(d.ffn, 1)));
   h_.reserve(static_cast<std::size_t>(d.layers * batch));
   for (i64 l = 0; l < d.layers; ++l) {
     for (i64 b = 0; b < batch; ++b) {
@@ -59,10 +62,40 @@ ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, st
             hash_matrix(seed, kWv, l, d.hidden, d.kv_heads * d.head_size, 1.0, bf16));
     }
     wo_.push_back(hash_matrix(seed, kWo, l, d.hidden, d.hidden, sh, bf16));
-    wg_.push_back(hash_matrix(seed, kWgate, l, d.hidden, d.ffn, sh, bf16));
-    wu_.push_back(hash_matrix(seed, kWup, l, d.hidden, d.ffn, sh, bf16));
-    wd_.push_back(hash_matrix(seed, kWdown, l, d.ffn, d.hidden, sf, bf16));
+    if (d.ffn > 0) {  // dense FFN, or the MoE shared expert
+      wg_.push_back(hash_matrix(seed, kWgate, l, d.hidden, d.ffn, sh, bf16));
+      wu_.push_back(hash_matrix(seed, kWup, l, d.hidden, d.ffn, sh, bf16));
+      wd_.push_back(hash_matrix(seed, kWdown, l, d.ffn, d.hidden, sf, bf16));
+    } else {
+      wg_.emplace_back();
+      wu_.emplace_back();
+      wd_.emplace_back();
+    }
+    if (d.n_experts > 0) {
+      wr_.push_back(hash_matrix(seed, kWrouter, l, d.hidden, d.n_experts, sh, bf16));
+      const double se = 1.0 / std::sqrt(static_cast<double>(d.expert_ffn));
+      eg_.emplace_back();
+      eu_.emplace_back();
+      ed_.emplace_back();
+      for (i64 e = 0; e < d.n_experts; ++e) {
+        auto em = [&](HashKind k, i64 rows, i64 cols, double sc) {
+          Mat m(rows, cols);
+          const std::uint64_t st = expert_stream(k, l, e);
+          for (i64 r = 0; r < rows; ++r)
+            for (i64 c = 0; c < cols; ++c) {
+              const double v = hash_unit(seed, st, static_cast<std::uint64_t>(r * cols + c)) * sc;
+              m(r, c) = bf16 ? round_bf16(v) : v;
+            }
+          return m;
+        };
+        eg_.back().push_back(em(kEgate, d.hidden, d.expert_ffn, sh));
+        eu_.back().push_back(em(kEup, d.hidden, d.expert_ffn, sh));
+        ed_.back().push_back(em(kEdown, d.expert_ffn, d.hidden, se));
+      }
+    }
   }
+  routes_.assign(static_cast<std::size_t>(d.layers * batch), {});
+  gaps_.assign(static_cast<std::size_t>(d.layers * batch), 1e30);
   emb_ = hash_matrix(seed, kEmb, 0, d.vocab, d.hidden, 1.0, bf16);
   lm_ = hash_matrix(seed, kLm, 0, d.hidden, d.vocab, sh, bf16);
 }
@@ -92,6 +125,46 @@ void ModelOracle::grow_hash(i64 layer, i64 request, i64 n) {
   }
 }
 
+std::vector<double> ModelOracle::ffn(i64 l, i64 b, const std::vector<double>& f) {
+  const i64 H = d_.hidden;
+  std::vector<double> y(static_cast<std::size_t>(H), 0.0);
+  auto swiglu_ffn = [&](const Mat& wg, const Mat& wu, const Mat& wd, double scale) {
+    const std::vector<double> gt = vecmat(f, wg);
+    const std::vector<double> up = vecmat(f, wu);
+    std::vector<double> m(gt.size());
+    for (std::size_t i = 0; i < m.size(); ++i) m[i] = gt[i] / (1.0 + std::exp(-gt[i])) * up[i];
+    const std::vector<double> dn = vecmat(m, wd);
+    for (i64 i = 0; i < H; ++i) y[static_cast<std::size_t>(i)] += scale * dn[static_cast<std::size_t>(i)];
+  };
+  if (d_.n_experts > 0) {
+    const std::vector<double> r = vecmat(f, wr_[static_cast<std::size_t>(l)]);
+    std::vector<i64> idx(static_cast<std::size_t>(d_.n_experts));
+    std::iota(idx.begin(), idx.end(), 0);
+    std::stable_sort(idx.begin(), idx.end(), [&](i64 a, i64 c) {
+      return r[static_cast<std::size_t>(a)] > r[static_cast<std::size_t>(c)];
+    });
+    gaps_[static_cast<std::size_t>(l * batch_ + b)] =
+        d_.top_k < d_.n_experts ? r[static_cast<std::size_t>(idx[static_cast<std::size_t>(d_.top_k - 1)])] -
+                                      r[static_cast<std::size_t>(idx[static_cast<std::size_t>(d_.top_k)])]
+                                : 1e30;
+    idx.resize(static_cast<std::size_t>(d_.top_k));
+    const double m = r[static_cast<std::size_t>(idx[0])];
+    double z = 0.0;
+    for (i64 e : idx) z += std::exp(r[static_cast<std::size_t>(e)] - m);
+    for (i64 e : idx) {
+      const double w = std::exp(r[static_cast<std::size_t>(e)] - m) / z;
+      swiglu_ffn(eg_[static_cast<std::size_t>(l)][static_cast<std::size_t>(e)],
+                 eu_[static_cast<std::size_t>(l)][static_cast<std::size_t>(e)],
+                 ed_[static_cast<std::size_t>(l)][static_cast<std::size_t>(e)], w);
+    }
+    routes_[static_cast<std::size_t>(l * batch_ + b)] = idx;
+  }
+  if (d_.ffn > 0)
+    swiglu_ffn(wg_[static_cast<std::size_t>(l)], wu_[static_cast<std::size_t>(l)], wd_[static_cast<std::size_t>(l)],
+               1.0);
+  return y;
+}
+
 std::vector<double> ModelOracle::step(const std::vector<std::int64_t>& tokens,
                                       std::vector<double>* hidden,
                                       std::vector<std::int64_t>* next) {
@@ -112,12 +185,7 @@ std::vector<double> ModelOracle::step(const std::vector<std::int64_t>& tokens,
       const std::vector<double> o = vecmat(att.a, wo_[static_cast<std::size_t>(l)]);
       std::vector<double> h(static_cast<std::size_t>(H));
       for (i64 i = 0; i < H; ++i) h[static_cast<std::size_t>(i)] = x[static_cast<std::size_t>(i)] + o[static_cast<std::size_t>(i)];
-      const std::vector<double> f = rmsnorm(h);
-      const std::vector<double> gt = vecmat(f, wg_[static_cast<std::size_t>(l)]);
-      const std::vector<double> up = vecmat(f, wu_[static_cast<std::size_t>(l)]);
-      std::vector<double> m(gt.size());
-      for (std::size_t i = 0; i < m.size(); ++i) m[i] = gt[i] / (1.0 + std::exp(-gt[i])) * up[i];
-      const std::vector<double> dn = vecmat(m, wd_[static_cast<std::size_t>(l)]);
+      const std::vector<double> dn = ffn(l, b, rmsnorm(h));
       for (i64 i = 0; i < H; ++i) x[static_cast<std::size_t>(i)] = h[static_cast<std::size_t>(i)] + dn[static_cast<std::size_t>(i)];
       if (hidden)
         std::copy(x.begin(), x.end(), hidden->begin() + ((l + 1) * batch_ + b) * H);

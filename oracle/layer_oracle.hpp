@@ -43,14 +43,25 @@ inline double hash_unit(std::uint64_t seed, std::uint64_t stream, std::uint64_t 
 }
 enum HashKind : std::uint64_t {
   kWq = 1, kWk = 2, kWv = 3, kWo = 4, kWgate = 5, kWup = 6, kWdown = 7, kEmb = 8, kLm = 9,
-  kCacheK = 10, kCacheV = 11
+  kCacheK = 10, kCacheV = 11, kWrouter = 12, kEgate = 13, kEup = 14, kEdown = 15
 };
 inline std::uint64_t hash_stream(HashKind kind, std::int64_t layer) {
   return (static_cast<std::uint64_t>(kind) << 32) | static_cast<std::uint64_t>(layer);
 }
+// Routed-expert weights: one stream per (layer, expert).
+inline std::uint64_t expert_stream(HashKind kind, std::int64_t layer, std::int64_t expert) {
+  return (static_cast<std::uint64_t>(kind) << 32) | (static_cast<std::uint64_t>(layer) << 16) |
+         static_cast<std::uint64_t>(expert);
+}
 
+// MoE FFN (types.hpp:19-25 MoESpec; latency.cpp:110-137 analytic shape):
+//   f = rmsnorm(h); r = f . W_router [H x E] (scale 1/sqrt(H));
+//   top-k experts by r (ties: lower index); w = softmax over the k selected r;
+//   y = sum_i w_i * E_i(f) + S(f),  E_i(f) = (silu(f Wg_i) * (f Wu_i)) Wd_i  [H x Fe, Fe x H]
+//   S = the dense SwiGLU weights (kWgate/kWup/kWdown) of width shared_ffn (0: none).
 struct ModelDims {
   i64 hidden, query_heads, kv_heads, head_size, ffn, layers, vocab;
+  i64 n_experts = 0, top_k = 0, expert_ffn = 0;  // n_experts == 0: dense FFN of width `ffn`
 };
 
 enum class QkvInit { MT19937 = 0, Hash = 1 };
@@ -78,6 +89,12 @@ class ModelOracle {
   const Mat& wdown(i64 l) const { return wd_[static_cast<std::size_t>(l)]; }
   const Mat& emb() const { return emb_; }
   const Mat& lm() const { return lm_; }
+  const Mat& router(i64 l) const { return wr_[static_cast<std::size_t>(l)]; }
+  // Last step's routing: [B][top_k] expert ids per layer (for kernel parity)
+  const std::vector<std::vector<i64>>& routes() const { return routes_; }
+  // Last step's router margin per (layer, request): r[k-th] - r[(k+1)-th]
+  // (a kernel whose logits differ by more than this may legally pick another set)
+  const std::vector<double>& route_gaps() const { return gaps_; }
 
  private:
   ModelDims d_;
@@ -85,8 +102,12 @@ class ModelOracle {
   std::uint64_t seed_;
   bool bf16_;
   std::vector<DecodeHarness> h_;
-  std::vector<Mat> wo_, wg_, wu_, wd_;
+  std::vector<Mat> wo_, wg_, wu_, wd_, wr_;
+  std::vector<std::vector<Mat>> eg_, eu_, ed_;  // [layer][expert]
+  std::vector<std::vector<i64>> routes_;        // [layer*B + b] -> selected experts
+  std::vector<double> gaps_;                    // [layer*B + b] -> top-k margin
   Mat emb_, lm_;
+  std::vector<double> ffn(i64 l, i64 b, const std::vector<double>& f);
 };
 
 // Hash-initialised matrix [rows x cols], row-major index r*cols + c, times scale.

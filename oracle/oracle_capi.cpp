@@ -205,6 +205,37 @@ int oracle_model_create(i64 hidden, i64 q, i64 k, i64 hsz, i64 ffn, i64 layers, 
                            qkv_hash ? QkvInit::Hash : QkvInit::MT19937, bf16 != 0);
   });
 }
+
+// MoE model: ffn = shared-expert width (0: none), n_experts / top_k / expert_ffn routed.
+int oracle_model_create_moe(i64 hidden, i64 q, i64 k, i64 hsz, i64 shared_ffn, i64 layers, i64 vocab,
+                            i64 n_experts, i64 top_k, i64 expert_ffn, i64 tpa, i64 kvp, i64 chunk, i64 batch,
+                            std::uint64_t seed, int qkv_hash, int bf16, void** out) {
+  return guard([&] {
+    ModelDims d{hidden, q, k, hsz, shared_ffn, layers, vocab};
+    d.n_experts = n_experts;
+    d.top_k = top_k;
+    d.expert_ffn = expert_ffn;
+    *out = new ModelOracle(d, tpa, kvp, chunk, batch, seed, qkv_hash ? QkvInit::Hash : QkvInit::MT19937,
+                           bf16 != 0);
+  });
+}
+
+// routes of the last step: [layers][B][top_k]
+int oracle_model_routes(void* mp, std::int64_t* out) {
+  return guard([&] {
+    auto* m = static_cast<ModelOracle*>(mp);
+    std::size_t o = 0;
+    for (const auto& r : m->routes())
+      for (i64 e : r) out[o++] = e;
+  });
+}
+// router top-k margins of the last step: [layers][B]
+int oracle_model_route_gaps(void* mp, double* out) {
+  return guard([&] {
+    const auto& g = static_cast<ModelOracle*>(mp)->route_gaps();
+    std::copy(g.begin(), g.end(), out);
+  });
+}
 void oracle_model_free(void* m) { delete static_cast<ModelOracle*>(m); }
 
 int oracle_model_grow_random(void* m, i64 layer, i64 request, i64 n, void* rng) {

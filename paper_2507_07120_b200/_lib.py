@@ -16,7 +16,8 @@ i64, u64, i32, dp, fp, vp = C.c_int64, C.c_uint64, C.c_int32, C.POINTER(C.c_doub
 
 class ModelConfig(C.Structure):
     _fields_ = [("hidden", i64), ("query_heads", i64), ("kv_heads", i64), ("head_size", i64), ("ffn", i64),
-                ("layers", i64), ("vocab", i64), ("attention_only", i32), ("reserved", i32)]
+                ("layers", i64), ("vocab", i64), ("attention_only", i32), ("reserved", i32),
+                ("n_experts", i64), ("top_k", i64), ("expert_ffn", i64)]
 
 
 POOL_LOCAL, POOL_NCCL, POOL_LOOPBACK = 0, 1, 2
@@ -24,7 +25,7 @@ POOL_LOCAL, POOL_NCCL, POOL_LOOPBACK = 0, 1, 2
 
 class ParallelConfig(C.Structure):
     _fields_ = [("tpa", i64), ("kvp", i64), ("chunk_size", i64), ("distributed", i32), ("rank", i32),
-                ("nccl_unique_id", vp), ("loopback", vp)]
+                ("nccl_unique_id", vp), ("loopback", vp), ("ep", i64)]
 
 
 class RuntimeConfig(C.Structure):

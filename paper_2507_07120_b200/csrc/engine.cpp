@@ -93,7 +93,11 @@ int round_up(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b * b
 
 uint64_t hash_stream(uint64_t kind, int64_t layer) { return (kind << 32) | static_cast<uint64_t>(layer); }
 enum : uint64_t { kWq = 1, kWk = 2, kWv = 3, kWo = 4, kWgate = 5, kWup = 6, kWdown = 7, kEmb = 8, kLm = 9,
-                  kCacheK = 10, kCacheV = 11 };
+                  kCacheK = 10, kCacheV = 11, kWrouter = 12, kEgate = 13, kEup = 14, kEdown = 15 };
+// routed-expert weights: one stream per (layer, expert) -- oracle/layer_oracle.hpp expert_stream
+uint64_t expert_stream(uint64_t kind, int64_t layer, int64_t expert) {
+  return (kind << 32) | (static_cast<uint64_t>(layer) << 16) | static_cast<uint64_t>(expert);
+}
 
 }  // namespace
 
@@ -107,12 +111,22 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
   validate_reference_dims();
   if (H_ != Qh_ * D_) throw std::invalid_argument("hidden_dim must equal query_heads * head_size");
   if (L_ < 1) throw std::invalid_argument("layers must be >= 1");
-  if (B_ < 1 || B_ > 16) throw std::invalid_argument("batch must be in [1, 16] for the B200 decode kernels");
+  if (B_ < 1 || B_ > 64) throw std::invalid_argument("batch must be in [1, 64] for the B200 decode kernels");
   if (cap_ < 1) throw std::invalid_argument("capacity_tokens must be >= 1");
   if (D_ > 128) throw std::invalid_argument("head_size > 128 is not supported by the GQA decode kernel");
   if (H_ % 16) throw std::invalid_argument("hidden width must be a multiple of 16");
+  moe_ = !attn_only_ && m.n_experts > 0;
+  if (moe_) {
+    E_ = m.n_experts;
+    topk_ = m.top_k;
+    Fe_ = m.expert_ffn;
+    if (topk_ < 1 || topk_ > 16 || topk_ > E_) throw std::invalid_argument("moe top_k must be in [1, min(16, experts)]");
+    if (Fe_ < 16 || Fe_ % 16) throw std::invalid_argument("moe expert_ffn_dim must be a positive multiple of 16");
+    if (E_ > 4096) throw std::invalid_argument("at most 4096 experts");
+  }
   if (!attn_only_) {
-    if (F_ < 16 || F_ % 16) throw std::invalid_argument("ffn_dim must be a positive multiple of 16");
+    const bool shared_ok = moe_ && F_ == 0;  // MoE without a shared expert
+    if (!shared_ok && (F_ < 16 || F_ % 16)) throw std::invalid_argument("ffn_dim must be a positive multiple of 16");
     if (V_ < 1) throw std::invalid_argument("vocab must be >= 1");
   }
   dist_mode_ = par.distributed;
@@ -127,6 +141,21 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
   N_ = tpa_ * kvp_;
   F_local_ = static_cast<int>(F_);
   V_local_ = static_cast<int>(V_);
+  if (moe_) {  // expert parallelism (types.hpp:100): ep x tpf = tpa x kvp in a distributed pool
+    ep_ = dist_mode_ == HX_POOL_LOCAL ? 1 : static_cast<int>(std::max<int64_t>(1, par.ep));
+    if (N_ % ep_) throw std::invalid_argument("helix re-provisions one pool: kvp*tpa must equal tpf*ep");
+    tpf_ = dist_mode_ == HX_POOL_LOCAL ? 1 : N_ / ep_;
+    if (E_ % ep_) throw std::invalid_argument("ep must divide total_experts");
+    if (Fe_ % tpf_ || (Fe_ / tpf_) % 16) throw std::invalid_argument("tpf must divide expert_ffn_dim (x16)");
+    if (dist_mode_ != HX_POOL_LOCAL) {
+      ep_rank_ = rank_ / tpf_;
+      tpf_rank_ = rank_ % tpf_;
+    }
+    E_local_ = static_cast<int>(E_ / ep_);
+    e_begin_ = ep_rank_ * E_local_;
+    Fe_local_ = static_cast<int>(Fe_ / tpf_);
+    n_groups_max_ = static_cast<int>(std::min<int64_t>(E_local_, static_cast<int64_t>(B_) * topk_));
+  }
   if (dist_mode_ == HX_POOL_LOCAL) {
     n_slots_ = N_;
     slot_base_ = 0;
@@ -142,7 +171,8 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
     if (slice_ % 16) throw std::invalid_argument("distributed Helix needs hidden/(tpa*kvp) to be a multiple of 16");
     xchunk_ = static_cast<int>(exchange_layout(q_per_slot_, D_, kvp_, nullptr));
     if (!attn_only_) {
-      if (F_ % N_ || (F_ / N_) % 16) throw std::invalid_argument("ffn_dim/(tpa*kvp) must be a multiple of 16");
+      if (F_ % N_ || (F_ > 0 && (F_ / N_) % 16))
+        throw std::invalid_argument("ffn_dim/(tpa*kvp) must be a multiple of 16");
       F_local_ = static_cast<int>(F_ / N_);
       V_local_ = static_cast<int>((V_ + N_ - 1) / N_);
     }
@@ -186,6 +216,10 @@ Engine::~Engine() {
   for (auto* p : w_o_) f(p);
   for (auto* p : w_gu_) f(p);
   for (auto* p : w_down_) f(p);
+  for (auto* p : w_router_) f(p);
+  for (auto* p : w_egu_) f(p);
+  for (auto* p : w_edown_) f(p);
+  f(d_rlog_); f(d_route_w_); f(d_gids_); f(d_gcount_); f(d_xf_em_); f(d_moe_y_);
   f(w_lm_); f(emb_); f(d_total_); f(d_q_); f(d_part_o_); f(d_part_lse_); f(d_work_);
   f(d_frag_o_); f(d_frag_lse_); f(d_ypart_); f(d_counters_); f(d_x_); f(d_ss_); f(d_m_);
   f(d_logits_); f(d_best_); f(d_tokens_); f(d_next_); f(d_out_); f(d_out_lse_); f(d_hidden_);
@@ -250,9 +284,10 @@ void Engine::alloc() {
 
 // ---------------------------------------------------------------------------
 void Engine::plan_gemvs() {
-  d_plan_ctr_ = dalloc<int>(static_cast<size_t>(2 * (4 * L_ + 2)), "plan counters");
+  d_plan_ctr_ = dalloc<int>(static_cast<size_t>(2 * (7 * L_ + 2)), "plan counters");
   int plan_idx = 0;
-  auto make = [&](int N, int Npad, int K, int norm, int em) {
+  // groups: expected concurrent weight blocks (MoE: active experts) for tile sizing
+  auto make = [&](int N, int Npad, int K, int norm, int em, int groups = 1) {
     GemvPlan g;
     GemvParams& p = g.p;
     p.N = N;
@@ -265,7 +300,7 @@ void Engine::plan_gemvs() {
     const int kst = K / 16;
     const int nblk = Npad / 128;
     int kr = std::min(64, kst);
-    while (kr > 8 && static_cast<int64_t>(nblk) * ((kst + kr - 1) / kr) < 4 * num_sms_) kr /= 2;
+    while (kr > 8 && static_cast<int64_t>(nblk) * groups * ((kst + kr - 1) / kr) < 4 * num_sms_) kr /= 2;
     const int ksplit = (kst + kr - 1) / kr;
     p.ksplit = ksplit;
     p.kr_steps = kr;
@@ -277,7 +312,7 @@ void Engine::plan_gemvs() {
     p.dp = DP_;
     g.xmode = norm;
     g.emode = em;
-    ypart_elems_ = std::max(ypart_elems_, static_cast<size_t>(ksplit) * B_ * Npad);
+    ypart_elems_ = std::max(ypart_elems_, static_cast<size_t>(groups) * ksplit * B_ * Npad);
     max_counters_ = std::max(max_counters_, nblk);
     return g;
   };
@@ -304,14 +339,49 @@ void Engine::plan_gemvs() {
       if (dist) {
         // O-proj: this rank's exchanged slice of its group's heads x its rows of W_O
         plan_o_.push_back(make(Hh, round_up(Hh, 128), slice_, 0, E_STORE));
-        plan_gu_.push_back(make(2 * F, round_up(F, 64) * 2, Hh, 1, E_SWIGLU));
-        plan_down_.push_back(make(Hh, round_up(Hh, 128), F, 0, E_STORE));
       } else {
         plan_o_.push_back(make(Hh, round_up(Hh, 128), Hh, 0, E_RESID));
+      }
+      if (F > 0) {  // dense FFN, or the MoE shared expert
         plan_gu_.push_back(make(2 * F, round_up(F, 64) * 2, Hh, 1, E_SWIGLU));
-        plan_down_.push_back(make(Hh, round_up(Hh, 128), F, 0, E_RESID));
+        plan_down_.push_back(make(Hh, round_up(Hh, 128), F, 0, dist ? E_STORE : E_RESID));
       }
     }
+  }
+  if (moe_) {
+    // router -> top-k -> grouped expert GEMVs whose tile queue covers only the
+    // experts some request selected (group list written by the routing kernel)
+    const int E = static_cast<int>(E_), Fe = Fe_local_, G = n_groups_max_;
+    const int nb8 = xf_nb8(B_);
+    const long long xfe = static_cast<long long>(Fe / 16) * 3 * nb8 * 256;
+    const bool shared = F_ > 0;
+    for (int64_t l = 0; l < L_; ++l) {
+      GemvPlan r = make(E, round_up(E, 128), Hh, 1, E_STORE);
+      r.p.out_stride = E;
+      plan_router_.push_back(r);
+      GemvPlan gu = make(2 * Fe, round_up(Fe, 64) * 2, Hh, 1, E_SWIGLU, G);
+      GemvPlan dn = make(Hh, round_up(Hh, 128), Fe, 0, (dist || shared) ? E_STORE : E_RESID, G);
+      for (GemvPlan* g : {&gu, &dn}) {
+        GemvParams& p = g->p;
+        p.tiles_per_group = p.n_tiles;
+        p.n_groups_max = G;
+        p.group_base = e_begin_;
+        p.w_group_stride = static_cast<long long>(p.Npad) * p.K * 2;
+        p.part_group_stride = static_cast<long long>(p.ksplit) * B_ * p.Npad;
+        p.n_experts = E;
+      }
+      gu.p.xf_group_stride = 0;  // every expert reads the same normalised h
+      gu.p.xf_out_group_stride = xfe;
+      dn.p.xf_group_stride = xfe;
+      plan_egu_.push_back(gu);
+      plan_edown_.push_back(dn);
+    }
+    d_rlog_ = dalloc<float>(static_cast<size_t>(B_) * E, "router logits");
+    d_route_w_ = dalloc<float>(static_cast<size_t>(B_) * E, "route weights");
+    d_gids_ = dalloc<int>(static_cast<size_t>(std::max(G, 1)), "expert list");
+    d_gcount_ = dalloc<int>(1, "expert count");
+    d_xf_em_ = dalloc<uint8_t>(static_cast<size_t>(std::max(G, 1)) * xfe, "expert xf");
+    if (shared) d_moe_y_ = dalloc<float>(static_cast<size_t>(B_) * H_, "moe y");
   }
   if (!attn_only_) {
     plan_lm_ = make(V_local_, round_up(V_local_, 128), Hh, 1, E_LOGITS);
@@ -320,7 +390,7 @@ void Engine::plan_gemvs() {
 
   d_ypart_ = dalloc<float>(ypart_elems_, "ypart");
   {
-    const int nb8 = (B_ + 7) / 8;
+    const int nb8 = xf_nb8(B_);
     auto xf_alloc = [&](int K) { return dalloc<uint8_t>(static_cast<size_t>(K / 16) * 3 * nb8 * 256, "xf"); };
     d_xf_resid_ = xf_alloc(static_cast<int>(H_));
     d_xf_attn_ = xf_alloc(dist ? slice_ : static_cast<int>(H_));
@@ -335,12 +405,14 @@ void Engine::plan_gemvs() {
     d_hidden_ = dalloc<float>(static_cast<size_t>(L_ + 1) * B_ * H_, "hidden");
   }
   // launches per step (each GEMV = streaming kernel + epilogue kernel)
+  // FFN per layer: dense 4; MoE router 2 + route 1 + experts 4 (+ shared 4)
+  const int64_t ffn_k = moe_ ? 7 + (F_ > 0 ? 4 : 0) : 4;
   if (attn_only_)
     kernels_per_step_ = 6;  // xprep, qkv x2, attention, split-reduce, merge(+bump)
   else if (!dist)
-    kernels_per_step_ = 1 + 11 * L_ + 3;
+    kernels_per_step_ = 1 + (7 + ffn_k) * L_ + 3;
   else  // + pack and two residual adds per layer; per-request attention launches under HOP-B
-    kernels_per_step_ = 1 + L_ * (13 + (hopb_ ? 3 * (B_ - 1) : 0)) + 3;
+    kernels_per_step_ = 1 + L_ * (9 + ffn_k + (hopb_ ? 3 * (B_ - 1) : 0)) + 3;
 }
 
 // ---------------------------------------------------------------------------
@@ -381,19 +453,49 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
     if (!attn_only_) {
       if (w_o_.size() <= static_cast<size_t>(l)) {
         w_o_.push_back(walloc(plan_o_[l]));
-        w_gu_.push_back(walloc(plan_gu_[l]));
-        w_down_.push_back(walloc(plan_down_[l]));
+        if (F > 0) {
+          w_gu_.push_back(walloc(plan_gu_[l]));
+          w_down_.push_back(walloc(plan_down_[l]));
+        }
       }
       // O-proj input rows: this rank's slice of its group's flattened heads
       const int ko = dist ? grp_ * q_per_slot_ * Dd + r_ * slice_ : 0;
       init(w_o_[l], plan_o_[l], {{hash_stream(kWo, l), 0, Hh, Hh, 0, 0, sh, ko, 0}});
-      init(w_gu_[l], plan_gu_[l],
-           {{hash_stream(kWgate, l), 0, plan_gu_[l].p.Npad, static_cast<int>(F_), f0, 1, sh, 0, f0 + F},
-            {hash_stream(kWup, l), 0, plan_gu_[l].p.Npad, static_cast<int>(F_), f0, 2, sh, 0, f0 + F}});
-      init(w_down_[l], plan_down_[l], {{hash_stream(kWdown, l), 0, Hh, Hh, 0, 0, sf, f0, 0}});
       plan_o_[l].p.w = w_o_[l];
-      plan_gu_[l].p.w = w_gu_[l];
-      plan_down_[l].p.w = w_down_[l];
+      if (F > 0) {
+        init(w_gu_[l], plan_gu_[l],
+             {{hash_stream(kWgate, l), 0, plan_gu_[l].p.Npad, static_cast<int>(F_), f0, 1, sh, 0, f0 + F},
+              {hash_stream(kWup, l), 0, plan_gu_[l].p.Npad, static_cast<int>(F_), f0, 2, sh, 0, f0 + F}});
+        init(w_down_[l], plan_down_[l], {{hash_stream(kWdown, l), 0, Hh, Hh, 0, 0, sf, f0, 0}});
+        plan_gu_[l].p.w = w_gu_[l];
+        plan_down_[l].p.w = w_down_[l];
+      }
+    }
+    if (moe_) {
+      // router replicated; experts [e_begin, e_begin + E_local) of this EP group,
+      // each sliced to this rank's tpf share of the expert FFN width
+      GemvPlan& r = plan_router_[l];
+      GemvPlan& gu = plan_egu_[l];
+      GemvPlan& dn = plan_edown_[l];
+      if (w_router_.size() <= static_cast<size_t>(l)) {
+        w_router_.push_back(walloc(r));
+        w_egu_.push_back(dalloc<uint4>(static_cast<size_t>(E_local_) * gu.p.Npad * gu.p.K / 8, "expert gate/up"));
+        w_edown_.push_back(dalloc<uint4>(static_cast<size_t>(E_local_) * dn.p.Npad * dn.p.K / 8, "expert down"));
+      }
+      const int E = static_cast<int>(E_), Fe = Fe_local_, fe0 = tpf_rank_ * Fe_local_;
+      const double se = 1.0 / std::sqrt(static_cast<double>(Fe_));
+      init(w_router_[l], r, {{hash_stream(kWrouter, l), 0, E, E, 0, 0, sh, 0, 0}});
+      for (int el = 0; el < E_local_; ++el) {
+        const int64_t e = e_begin_ + el;
+        init(w_egu_[l] + static_cast<size_t>(el) * gu.p.Npad * gu.p.K / 8, gu,
+             {{expert_stream(kEgate, l, e), 0, gu.p.Npad, static_cast<int>(Fe_), fe0, 1, sh, 0, fe0 + Fe},
+              {expert_stream(kEup, l, e), 0, gu.p.Npad, static_cast<int>(Fe_), fe0, 2, sh, 0, fe0 + Fe}});
+        init(w_edown_[l] + static_cast<size_t>(el) * dn.p.Npad * dn.p.K / 8, dn,
+             {{expert_stream(kEdown, l, e), 0, Hh, Hh, 0, 0, se, fe0, 0}});
+      }
+      r.p.w = w_router_[l];
+      gu.p.w = w_egu_[l];
+      dn.p.w = w_edown_[l];
     }
   }
   if (!attn_only_) {
@@ -426,21 +528,60 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
       o.out_stride = static_cast<int>(H_);
       o.ss_out = dist ? nullptr : d_ss_;
       o.xf_out = d_xf_resid_;
-      GemvParams& gu = plan_gu_[l].p;
-      gu.ypart = d_ypart_;
-      gu.counters = d_counters_;
-      gu.xf = d_xf_resid_;
-      gu.ss_part = d_ss_;
-      gu.n_ss = hblk;
-      gu.xf_out = d_xf_m_;
-      GemvParams& dn = plan_down_[l].p;
-      dn.ypart = d_ypart_;
-      dn.counters = d_counters_;
-      dn.xf = d_xf_m_;
-      dn.out = dist ? d_parth_ : d_x_;
-      dn.out_stride = static_cast<int>(H_);
-      dn.ss_out = dist ? nullptr : d_ss_;
-      dn.xf_out = d_xf_resid_;
+      // the FFN's last GEMV writes the residual (local) or the TP partial (dist)
+      float* ffn_out = dist ? d_parth_ : d_x_;
+      float* ffn_ss = dist ? nullptr : d_ss_;
+      if (F_ > 0) {
+        GemvParams& gu = plan_gu_[l].p;
+        gu.ypart = d_ypart_;
+        gu.counters = d_counters_;
+        gu.xf = d_xf_resid_;
+        gu.ss_part = d_ss_;
+        gu.n_ss = hblk;
+        gu.xf_out = d_xf_m_;
+        GemvParams& dn = plan_down_[l].p;
+        dn.ypart = d_ypart_;
+        dn.counters = d_counters_;
+        dn.xf = d_xf_m_;
+        dn.out = ffn_out;
+        dn.out_stride = static_cast<int>(H_);
+        dn.ss_out = ffn_ss;
+        dn.xf_out = d_xf_resid_;
+        dn.addend = moe_ ? d_moe_y_ : nullptr;  // shared expert + routed experts
+      }
+      if (moe_) {
+        GemvParams& r = plan_router_[l].p;
+        r.ypart = d_ypart_;
+        r.counters = d_counters_;
+        r.xf = d_xf_resid_;
+        r.ss_part = d_ss_;
+        r.n_ss = hblk;
+        r.out = d_rlog_;
+        GemvParams& gu = plan_egu_[l].p;
+        gu.ypart = d_ypart_;
+        gu.counters = d_counters_;
+        gu.xf = d_xf_resid_;
+        gu.ss_part = d_ss_;
+        gu.n_ss = hblk;
+        gu.xf_out = d_xf_em_;
+        gu.group_count = d_gcount_;
+        gu.group_ids = d_gids_;
+        GemvParams& dn = plan_edown_[l].p;
+        dn.ypart = d_ypart_;
+        dn.counters = d_counters_;
+        dn.xf = d_xf_em_;
+        dn.group_count = d_gcount_;
+        dn.group_ids = d_gids_;
+        dn.route_w = d_route_w_;
+        dn.out_stride = static_cast<int>(H_);
+        if (F_ > 0) {
+          dn.out = d_moe_y_;
+        } else {
+          dn.out = ffn_out;
+          dn.ss_out = ffn_ss;
+          dn.xf_out = d_xf_resid_;
+        }
+      }
     }
   }
   if (!attn_only_) {
@@ -802,10 +943,7 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
                  "merge");
       cuda_check(launch_gemv(plan_o_[l].p, 0, E_RESID, num_sms_, stream_), "o-proj");
       mark(4);
-      cuda_check(launch_gemv(plan_gu_[l].p, 1, E_SWIGLU, num_sms_, stream_), "gate/up");
-      mark(5);
-      cuda_check(launch_gemv(plan_down_[l].p, 0, E_RESID, num_sms_, stream_), "down");
-      mark(6);
+      enqueue_ffn(l);
     } else {
       // merge of the exchanged slices, then TP O-proj over this rank's slice and
       // AllReduce over the pool (latency.cpp:85-94)
@@ -818,11 +956,8 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
       cuda_check(launch_residual_add(d_x_, d_parth_, B_, static_cast<int>(H_), d_ss_, d_xf_resid_, stream_),
                  "residual");
       mark(9);
-      // TP FFN over F/N features, AllReduce (latency.cpp:138-144)
-      cuda_check(launch_gemv(plan_gu_[l].p, 1, E_SWIGLU, num_sms_, stream_), "gate/up");
-      mark(5);
-      cuda_check(launch_gemv(plan_down_[l].p, 0, E_STORE, num_sms_, stream_), "down");
-      mark(6);
+      // TP FFN over F/N features (or EP x TPF experts), AllReduce (latency.cpp:110-144)
+      enqueue_ffn(l);
       if (!(skip_comm_ & 2)) transport_->all_reduce_sum(d_parth_, static_cast<size_t>(B_) * H_, stream_);
       cuda_check(launch_residual_add(d_x_, d_parth_, B_, static_cast<int>(H_), d_ss_, d_xf_resid_, stream_),
                  "residual");
@@ -839,6 +974,38 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
   if (dist && !(skip_comm_ & 2)) transport_->all_reduce_max_u64(d_best_, static_cast<size_t>(B_), stream_);  // vocab-sharded argmax
   cuda_check(launch_argmax_finish(d_best_, B_, next_dev, d_best_, stream_), "argmax");
   mark(7);
+}
+
+// FFN of one layer: input = rmsnorm(x) via d_xf_resid_ + d_ss_; output into the
+// residual (local pool) or the TP partial d_parth_ (distributed pool).
+//   dense: gate/up (SwiGLU epilogue) -> down
+//   MoE (latency.cpp:110-137): router GEMV -> top-k routing kernel -> grouped
+//   expert gate/up over the active experts only -> grouped expert down whose
+//   epilogue combines the experts with the routing weights in ascending expert
+//   order -> [shared expert gate/up -> down, adding the routed output]
+void Engine::enqueue_ffn(int64_t l) {
+  const bool dist = dist_mode_ != HX_POOL_LOCAL;
+  const int em_last = dist ? E_STORE : E_RESID;
+  if (moe_) {
+    cuda_check(launch_gemv(plan_router_[l].p, 1, E_STORE, num_sms_, stream_), "router");
+    cuda_check(launch_moe_route(d_rlog_, B_, static_cast<int>(E_), static_cast<int>(topk_), e_begin_,
+                                e_begin_ + E_local_, d_route_w_, d_gids_, d_gcount_, stream_),
+               "route");
+    cuda_check(launch_gemv(plan_egu_[l].p, 1, E_SWIGLU, num_sms_, stream_), "expert gate/up");
+    mark(5);
+    const bool shared = F_ > 0;
+    cuda_check(launch_gemv(plan_edown_[l].p, 0, shared ? E_STORE : em_last, num_sms_, stream_), "expert down");
+    if (shared) {
+      cuda_check(launch_gemv(plan_gu_[l].p, 1, E_SWIGLU, num_sms_, stream_), "shared gate/up");
+      cuda_check(launch_gemv(plan_down_[l].p, 0, em_last, num_sms_, stream_), "shared down");
+    }
+    mark(6);
+    return;
+  }
+  cuda_check(launch_gemv(plan_gu_[l].p, 1, E_SWIGLU, num_sms_, stream_), "gate/up");
+  mark(5);
+  cuda_check(launch_gemv(plan_down_[l].p, 0, em_last, num_sms_, stream_), "down");
+  mark(6);
 }
 
 void Engine::decode_step_device(const int32_t* tokens_dev, int32_t* next_dev) {
@@ -937,10 +1104,13 @@ void Engine::info(hx_engine_info* o) const {
   std::memset(o, 0, sizeof(*o));
   o->kv_bytes_per_layer = static_cast<int64_t>(n_slots_) * B_ * kvh_per_slot_ * page_cap_ * page_bytes_;
   int64_t wb = static_cast<int64_t>(plan_qkv_[0].p.Npad) * plan_qkv_[0].p.K * 2;
-  if (!attn_only_)
-    wb += static_cast<int64_t>(plan_o_[0].p.Npad) * plan_o_[0].p.K * 2 +
-          static_cast<int64_t>(plan_gu_[0].p.Npad) * plan_gu_[0].p.K * 2 +
-          static_cast<int64_t>(plan_down_[0].p.Npad) * plan_down_[0].p.K * 2;
+  auto bytes = [](const GemvPlan& g) { return static_cast<int64_t>(g.p.Npad) * g.p.K * 2; };
+  if (!attn_only_) {
+    wb += bytes(plan_o_[0]);
+    if (F_ > 0) wb += bytes(plan_gu_[0]) + bytes(plan_down_[0]);
+    if (moe_)  // all experts held here (only the routed ones are read per step)
+      wb += bytes(plan_router_[0]) + static_cast<int64_t>(E_local_) * (bytes(plan_egu_[0]) + bytes(plan_edown_[0]));
+  }
   o->weight_bytes_per_layer = wb;
   o->head_bytes = attn_only_ ? 0 : static_cast<int64_t>(plan_lm_.p.Npad) * plan_lm_.p.K * 2 + V_ * H_ * 2;
   o->attn_streams = n_streams_;

@@ -176,6 +176,21 @@ class Engine {
   void enqueue_exchange_and_attention_dist(int64_t layer);
   void init_dist_weights(uint64_t seed, bool qkv_hash);
   AttnParams attn_params(int64_t layer, int b_begin, int b_count) const;
+
+  // ---- MoE FFN (router -> top-k -> grouped expert GEMVs over the active list)
+  bool moe_ = false;
+  int64_t E_ = 0, topk_ = 0, Fe_ = 0;
+  int ep_ = 1, tpf_ = 1, ep_rank_ = 0, tpf_rank_ = 0, E_local_ = 0, e_begin_ = 0, Fe_local_ = 0;
+  int n_groups_max_ = 0;
+  std::vector<GemvPlan> plan_router_, plan_egu_, plan_edown_;
+  std::vector<uint4*> w_router_, w_egu_, w_edown_;
+  float* d_rlog_ = nullptr;     // [B][E] router logits
+  float* d_route_w_ = nullptr;  // [B][E] routing weights (dense, zeros off the top-k)
+  int* d_gids_ = nullptr;       // active local experts (ascending global ids)
+  int* d_gcount_ = nullptr;
+  uint8_t* d_xf_em_ = nullptr;  // [active slot] x-fragments of silu(gate)*up per expert
+  float* d_moe_y_ = nullptr;    // [B][H] routed-expert output (when a shared expert follows)
+  void enqueue_ffn(int64_t layer);
 };
 
 }  // namespace hx

@@ -1,4 +1,4 @@
-// Weight-streaming GEMV / skinny GEMM for the decode step (B <= 16 rows).
+// Weight-streaming GEMV / skinny GEMM for the decode step (B <= 64 rows).
 //
 // y[b][n] = sum_k x[b][k] * W[k][n]. W is bf16, fragment-major in CTA-tile
 // order [128-row block][k-step][8 n-tiles][512 B] (one 16x16 HMMA A tile = 512
@@ -33,14 +33,18 @@ namespace {
 
 constexpr int kRows = 128;        // rows (output features) per tile: 8 consumer warps x 16
 constexpr int kThreads = 256;     // consumer threads (+1 producer warp)
-constexpr int kStageSteps = 8;    // k-steps per ring stage: 32 KB of weights + x slice
 constexpr int kStages = 4;        // ring depth (~150 KB in flight per SM)
+// k-steps per ring stage: 32 KB of weights (+ x slice) for B <= 16; fewer
+// k-steps when the x slice grows with the batch (B <= 64) so 4 stages fit.
+template <int NB8>
+constexpr int stage_steps() { return NB8 <= 2 ? 8 : (NB8 <= 4 ? 4 : 2); }
 constexpr int kDone = -1;
 
 struct TileMeta {
   int tile, nb, ks0, nks;  // stage covers k-steps [ks0, ks0 + nks) of row block nb
   int last;                // last stage of its tile
-  int pad[3];
+  int kc, gi;              // k-chunk and group (expert slot) of the tile
+  int pad;
 };
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
@@ -53,8 +57,9 @@ __device__ __forceinline__ unsigned long long logit_key(float v, int n) {
   return (static_cast<unsigned long long>(u) << 32) | (0xFFFFFFFFu - static_cast<unsigned>(n));
 }
 
+__host__ __device__ __forceinline__ int stage_steps_rt(int nb8) { return nb8 <= 2 ? 8 : (nb8 <= 4 ? 4 : 2); }
 __host__ __device__ __forceinline__ size_t stage_bytes(int nb8) {
-  return static_cast<size_t>(kStageSteps) * (4096 + xf_step_bytes(nb8));
+  return static_cast<size_t>(stage_steps_rt(nb8)) * (4096 + xf_step_bytes(nb8));
 }
 
 }  // namespace
@@ -62,6 +67,7 @@ __host__ __device__ __forceinline__ size_t stage_bytes(int nb8) {
 template <int NB8, int EM, int XS, bool NORM>
 __global__ void __launch_bounds__(kThreads + 32, 1) gemv_kernel(const GemvParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
+  constexpr int kStageSteps = stage_steps<NB8>();
   constexpr size_t SW = kStageSteps * 4096;                   // weight bytes per stage
   constexpr size_t SX = kStageSteps * kXfTerms * NB8 * 256;   // x-fragment bytes per stage
   constexpr size_t SB = SW + SX;
@@ -87,14 +93,28 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemv_kernel(const GemvParams
     if (lane == 0) {
       int st = 0;
       bool waited = false;  // x fragments come from the previous kernel; weights are constant
+      int n_tiles = p.n_tiles;
+      if (p.group_count) {  // the active-expert list is produced by the routing kernel
+        griddep_wait();
+        waited = true;
+        n_tiles = *p.group_count * p.tiles_per_group;
+      }
       for (;;) {
         const int tile = atomicAdd(p.work_counter, 1);
-        const bool done = tile >= p.n_tiles;
-        const int nb = done ? 0 : tile / p.ksplit;  // row-block-major: a block's k-chunks finish together
-        const int kc = done ? 0 : tile - nb * p.ksplit;
+        const bool done = tile >= n_tiles;
+        const int gi = (done || !p.group_count) ? 0 : tile / p.tiles_per_group;
+        const int rem = done ? 0 : tile - gi * p.tiles_per_group;
+        const int nb = rem / p.ksplit;  // row-block-major: a block's k-chunks finish together
+        const int kc = rem - nb * p.ksplit;
         const int k0 = kc * p.kr_steps;
         const int k1 = min(k0 + p.kr_steps, KST);
         const int nstage = done ? 1 : (k1 - k0 + kStageSteps - 1) / kStageSteps;
+        const uint8_t* wg = reinterpret_cast<const uint8_t*>(p.w);
+        const uint8_t* xg = p.xf;
+        if (!done && p.group_count) {
+          wg += static_cast<size_t>(p.group_ids[gi] - p.group_base) * p.w_group_stride;
+          xg += static_cast<size_t>(gi) * p.xf_group_stride;
+        }
         for (int si = 0; si < nstage; ++si, ++st) {
           const int s = st % kStages;
           if (st >= kStages) mbar_wait(&empty[s], ((st / kStages) & 1) ^ 1);
@@ -113,15 +133,16 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemv_kernel(const GemvParams
           m.ks0 = a;
           m.nks = n;
           m.last = si == nstage - 1;
+          m.kc = kc;
+          m.gi = gi;
           uint8_t* dst = ring + s * SB;
           mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(n) * (4096u + kXfTerms * NB8 * 256u));
-          bulk_g2s(dst, reinterpret_cast<const uint8_t*>(p.w) + (static_cast<size_t>(nb) * KST + a) * 4096,
-                   static_cast<uint32_t>(n) * 4096u, &full[s]);
+          bulk_g2s(dst, wg + (static_cast<size_t>(nb) * KST + a) * 4096, static_cast<uint32_t>(n) * 4096u, &full[s]);
           if (!waited) {
             griddep_wait();
             waited = true;
           }
-          bulk_g2s(dst + SW, p.xf + static_cast<size_t>(a) * kXfTerms * NB8 * 256,
+          bulk_g2s(dst + SW, xg + static_cast<size_t>(a) * kXfTerms * NB8 * 256,
                    static_cast<uint32_t>(n) * kXfTerms * NB8 * 256u, &full[s]);
         }
         if (done) break;
@@ -159,10 +180,10 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemv_kernel(const GemvParams
 
       // ---- tile complete: store the split-K partial of rows nb*128 + warp*16 + g (+8).
       // Plain stores: the epilogue kernel (next in stream order) reduces them.
-      const int kc = m.tile - m.nb * p.ksplit;
       const int g = lane >> 2, c = lane & 3;
       const int n0 = m.nb * kRows + warp * 16 + g;
-      float* yp = p.ypart + static_cast<size_t>(kc) * p.batch * p.Npad;
+      float* yp = p.ypart + static_cast<size_t>(m.gi) * p.part_group_stride +
+                  static_cast<size_t>(m.kc) * p.batch * p.Npad;
 #pragma unroll
       for (int bg = 0; bg < NB8; ++bg) {
         float y[4];
@@ -206,10 +227,10 @@ template <int NB8, int EM, bool NORM>
 __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p) {
   // One thread per (row, request) element of a 128-row block; every global load
   // an element needs (its split partials, the old residual) is issued before use.
-  __shared__ float s_inv[16];
-  __shared__ float vt[16][kRows];
-  __shared__ unsigned long long s_best[16];
-  __shared__ long long s_pos[16][2];  // E_QKV: append (rank, local row) per request
+  __shared__ float s_inv[64];
+  __shared__ float vt[64][kRows];
+  __shared__ unsigned long long s_best[64];
+  __shared__ long long s_pos[64][2];  // E_QKV: append (rank, local row) per request
   griddep_wait();
   griddep_launch_dependents();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
@@ -228,13 +249,19 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
     s_pos[threadIdx.x][0] = rr_rank(g, p.rr_chunk, p.kvp);
     s_pos[threadIdx.x][1] = rr_row(g, p.rr_chunk, p.kvp);
   }
-  if (EM == E_LOGITS && threadIdx.x < 16) s_best[threadIdx.x] = 0ull;
+  if (EM == E_LOGITS && threadIdx.x < 64) s_best[threadIdx.x] = 0ull;
   if (EM == E_STORE || EM == E_RESID)
-    for (int i = threadIdx.x; i < 16 * kRows; i += blockDim.x) vt[i / kRows][i % kRows] = 0.f;
+    for (int i = threadIdx.x; i < 64 * kRows; i += blockDim.x) vt[i / kRows][i % kRows] = 0.f;
   __syncthreads();
   const int rows_here = EM == E_SWIGLU ? kRows / 2 : kRows;
   const size_t stride = static_cast<size_t>(p.batch) * p.Npad;
   constexpr int NP = 2;  // partial streams per element (SwiGLU: gate + up)
+  // grouped SwiGLU: one grid row per active expert slot
+  const int gi_epi = (p.group_count && EM == E_SWIGLU) ? static_cast<int>(blockIdx.y) : 0;
+  if (p.group_count && EM == E_SWIGLU && gi_epi >= *p.group_count) return;
+  const bool combine = p.group_count && EM != E_SWIGLU;  // MoE combine (possibly of zero experts)
+  const int n_comb = combine ? *p.group_count : 0;
+  uint8_t* xf_out = p.xf_out + static_cast<size_t>(gi_epi) * p.xf_out_group_stride;
   for (int e = threadIdx.x; e < rows_here * p.batch; e += blockDim.x) {
     const int r = e % rows_here, b = e / rows_here;
     const int np = EM == E_SWIGLU ? 2 : 1;
@@ -242,18 +269,32 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
     float old = 0.f;
     const int n = nb * kRows + r;
     if (EM == E_RESID && n < p.N) old = p.out[static_cast<size_t>(b) * p.out_stride + n];
-    for (int s0 = 0; s0 < p.ksplit; s0 += 16) {
-      float v[NP][16];
+    const int ngrp = combine ? n_comb : 1;
+    for (int gq = 0; gq < ngrp; ++gq) {
+      const int gsl = combine ? gq : gi_epi;
+      float yg[NP] = {0.f, 0.f};
+      for (int s0 = 0; s0 < p.ksplit; s0 += 16) {
+        float v[NP][16];
 #pragma unroll
-      for (int q = 0; q < NP; ++q) {
-        const float* base = p.ypart + static_cast<size_t>(b) * p.Npad + nb * kRows + r + q * (kRows / 2);
+        for (int q = 0; q < NP; ++q) {
+          const float* base = p.ypart + static_cast<size_t>(gsl) * p.part_group_stride +
+                              static_cast<size_t>(b) * p.Npad + nb * kRows + r + q * (kRows / 2);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) v[q][j] = (q < np && s0 + j < p.ksplit) ? __ldcg(base + (s0 + j) * stride) : 0.f;
+          for (int j = 0; j < 16; ++j)
+            v[q][j] = (q < np && s0 + j < p.ksplit) ? __ldcg(base + (s0 + j) * stride) : 0.f;
+        }
+#pragma unroll
+        for (int q = 0; q < NP; ++q)
+#pragma unroll
+          for (int j = 0; j < 16; ++j) yg[q] += v[q][j];  // split order: deterministic
       }
-#pragma unroll
-      for (int q = 0; q < NP; ++q)
-#pragma unroll
-        for (int j = 0; j < 16; ++j) y[q] += v[q][j];  // split order: deterministic
+      if (combine) {  // MoE combine in ascending expert order (deterministic)
+        const float w = p.route_w[static_cast<size_t>(b) * p.n_experts + p.group_ids[gq]];
+        y[0] += w * yg[0];
+      } else {
+        y[0] = yg[0];
+        y[1] = yg[1];
+      }
     }
     if (NORM) {
       y[0] *= s_inv[b];
@@ -261,10 +302,11 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
     }
     if (EM == E_SWIGLU) {
       const int f = nb * (kRows / 2) + r;
-      if (f < p.N / 2) xf_write(p.xf_out, NB8, b, f, y[0] / (1.f + __expf(-y[0])) * y[1]);
+      if (f < p.N / 2) xf_write(xf_out, NB8, b, f, y[0] / (1.f + __expf(-y[0])) * y[1]);
       continue;
     }
     if (n >= p.N) continue;
+    if (p.addend) y[0] += p.addend[static_cast<size_t>(b) * p.out_stride + n];
     if (EM == E_STORE) {
       p.out[static_cast<size_t>(b) * p.out_stride + n] = y[0];
       vt[b][r] = y[0] * y[0];
@@ -323,7 +365,7 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
 }
 
 size_t gemv_smem_bytes(const GemvParams& p) {
-  const int nb8 = (p.batch + 7) / 8;
+  const int nb8 = xf_nb8(p.batch);
   return static_cast<size_t>(kStages) * stage_bytes(nb8) + kStages * sizeof(TileMeta) + 2 * kStages * 8 + 64;
 }
 
@@ -341,7 +383,8 @@ static cudaError_t launch_t(const GemvParams& p, int grid, cudaStream_t stream) 
   if (e != cudaSuccess) return e;
   const int rows_here = EM == E_SWIGLU ? kRows / 2 : kRows;
   const int threads = std::min(1024, (rows_here * p.batch + 31) / 32 * 32);
-  return launch_k(gemv_epilogue_kernel<NB8, EM, NORM>, dim3(p.Npad / kRows), dim3(threads), 0, stream, p);
+  const int gy = (p.group_count && EM == E_SWIGLU) ? p.n_groups_max : 1;
+  return launch_k(gemv_epilogue_kernel<NB8, EM, NORM>, dim3(p.Npad / kRows, gy), dim3(threads), 0, stream, p);
 }
 
 template <int NB8>
@@ -354,6 +397,7 @@ static cudaError_t dispatch_nb(const GemvParams& p, int norm, int em, int grid, 
   HX_CASE(E_QKV, 3, false)
   HX_CASE(E_RESID, 2, false)
   HX_CASE(E_STORE, 2, false)
+  HX_CASE(E_STORE, 3, true)  // MoE router: fp32-accurate logits keep top-k ties rare
   HX_CASE(E_SWIGLU, 2, true)
   HX_CASE(E_LOGITS, 2, true)
 #undef HX_CASE
@@ -361,9 +405,11 @@ static cudaError_t dispatch_nb(const GemvParams& p, int norm, int em, int grid, 
 }
 
 cudaError_t launch_gemv(const GemvParams& p, int norm, int emode, int grid, cudaStream_t stream) {
-  if (p.batch < 1 || p.batch > 16 || (p.K & 15) || (p.Npad % kRows)) return cudaErrorInvalidValue;
+  if (p.batch < 1 || p.batch > 64 || (p.K & 15) || (p.Npad % kRows)) return cudaErrorInvalidValue;
   if (p.batch <= 8) return dispatch_nb<1>(p, norm, emode, grid, stream);
-  return dispatch_nb<2>(p, norm, emode, grid, stream);
+  if (p.batch <= 16) return dispatch_nb<2>(p, norm, emode, grid, stream);
+  if (p.batch <= 32) return dispatch_nb<4>(p, norm, emode, grid, stream);
+  return dispatch_nb<8>(p, norm, emode, grid, stream);
 }
 
 }  // namespace hx

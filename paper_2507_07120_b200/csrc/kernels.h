@@ -7,6 +7,16 @@
 
 namespace hx {
 
+#ifdef __CUDACC__
+#define HX_HD __host__ __device__
+#else
+#define HX_HD
+#endif
+// Batch groups of 8 in the x-fragment image (xfrag.cuh): the GEMV instantiates
+// 1, 2, 4 or 8 groups, so writers, readers and allocations use the padded count.
+HX_HD inline int xf_nb8(int batch) { return batch <= 8 ? 1 : (batch <= 16 ? 2 : (batch <= 32 ? 4 : 8)); }
+
+
 // Programmatic dependent launch for the decode-step kernels (set by the engine).
 void set_pdl(bool on);
 bool pdl_enabled();
@@ -85,6 +95,18 @@ struct GemvParams {
   // E_LOGITS
   unsigned long long* best;  // [B] packed (orderable logit, ~index)
   int n_offset;              // global index of row 0 (vocabulary shard offset)
+  // Grouped GEMV (MoE experts): tiles run over the device-side active-expert list
+  const int* group_count;    // active groups (nullptr: one ungrouped GEMV)
+  const int* group_ids;      // [group] -> global expert id (ascending)
+  int group_base;            // first expert id held here (weight block = id - group_base)
+  int n_groups_max, tiles_per_group;
+  long long w_group_stride;      // bytes between experts' weight blocks
+  long long xf_group_stride;     // bytes between groups' input fragments (0: shared input)
+  long long part_group_stride;   // floats between groups' split-K partials
+  long long xf_out_group_stride; // bytes between groups' output fragments (E_SWIGLU)
+  const float* route_w;      // [B][n_experts] routing weights: the epilogue combines groups
+  int n_experts;
+  const float* addend;       // optional [B][out_stride] added by E_RESID / E_STORE
 };
 cudaError_t launch_gemv(const GemvParams& p, int norm, int emode, int grid, cudaStream_t stream);
 size_t gemv_smem_bytes(const GemvParams& p);
@@ -146,6 +168,11 @@ cudaError_t launch_fill_zero(void* p, size_t bytes, cudaStream_t stream);
 cudaError_t launch_pack_exchange(const float* frag_o, const float* frag_lse, int b_begin, int b_count, int batch,
                                  int q_per_slot, int head_dim, int dp, int kvp, int slice, int chunk, float* send,
                                  cudaStream_t s);
+// MoE routing (one block): per request, top-k of router logits [B][E] (ties:
+// lower index), softmax over the selected -> dense weights route_w [B][E];
+// ascending list of selected experts within [e_begin, e_end) -> group_ids, count.
+cudaError_t launch_moe_route(const float* logits, int batch, int n_experts, int top_k, int e_begin, int e_end,
+                             float* route_w, int* group_ids, int* group_count, cudaStream_t s);
 // Residual add of an all-reduced partial product + RMSNorm statistics.
 cudaError_t launch_residual_add(float* x, const float* part, int batch, int hidden, float* ss_part,
                                 uint8_t* xf, cudaStream_t s);

@@ -93,7 +93,7 @@ __global__ void embed_kernel(const __nv_bfloat16* emb, const int* tokens, int ba
       for (int e = 0; e < 8; ++e) {
         const float v = __bfloat162float(h[e]);
         x[static_cast<size_t>(b) * hidden + i * 8 + e] = v;
-        xf_write(xf, (batch + 7) / 8, b, i * 8 + e, v);
+        xf_write(xf, xf_nb8(batch), b, i * 8 + e, v);
         s += v * v;
       }
     }
@@ -131,7 +131,7 @@ __global__ void argmax_finish_kernel(const unsigned long long* best, int batch, 
 
 cudaError_t launch_argmax_finish(const unsigned long long* best, int batch, int* tokens_out,
                                  unsigned long long* best_reset, cudaStream_t stream) {
-  return launch_k(argmax_finish_kernel, dim3(1), dim3(32), 0, stream, best, batch, tokens_out, best_reset);
+  return launch_k(argmax_finish_kernel, dim3(1), dim3(64), 0, stream, best, batch, tokens_out, best_reset);
 }
 
 // ---------------------------------------------------------------- KV scatter / fill
@@ -269,8 +269,7 @@ __global__ void kv_fill_hash_kernel(uint8_t* kv, const int* total, int batch, in
 }
 
 __global__ void add_total_all_kernel(int* total, int batch, int n) {
-  const int b = threadIdx.x;
-  if (b < batch) total[b] += n;
+  for (int b = threadIdx.x; b < batch; b += blockDim.x) total[b] += n;
 }
 
 cudaError_t launch_kv_fill_hash(uint8_t* kv, int* total, int batch, int kv_heads,
@@ -283,7 +282,7 @@ cudaError_t launch_kv_fill_hash(uint8_t* kv, int* total, int batch, int kv_heads
     kv_fill_hash_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(
         kv, total, batch, kv_heads, kvh_per_slot, kvp, chunk, head_dim, dp, page_cap, slot_base,
         n_local_slots, n, seed, stream_k, stream_v);
-  add_total_all_kernel<<<1, 32, 0, stream>>>(total, batch, static_cast<int>(n));
+  add_total_all_kernel<<<1, 64, 0, stream>>>(total, batch, static_cast<int>(n));
   return cudaGetLastError();
 }
 
@@ -454,7 +453,7 @@ __global__ void residual_add_kernel(float* x, const float* part, int batch, int 
   if (n < hidden) {
     v = x[static_cast<size_t>(b) * hidden + n] + part[static_cast<size_t>(b) * hidden + n];
     x[static_cast<size_t>(b) * hidden + n] = v;
-    xf_write(xf, (batch + 7) / 8, b, n, v);
+    xf_write(xf, xf_nb8(batch), b, n, v);
   }
   float s = v * v;
 #pragma unroll
@@ -479,7 +478,7 @@ __global__ void xprep_plain_kernel(const float* x, int batch, int K, int x_strid
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= static_cast<long long>(batch) * K) return;
   const int b = static_cast<int>(i / K), k = static_cast<int>(i % K);
-  xf_write(xf, (batch + 7) / 8, b, k, x[static_cast<size_t>(b) * x_stride + k]);
+  xf_write(xf, xf_nb8(batch), b, k, x[static_cast<size_t>(b) * x_stride + k]);
 }
 cudaError_t launch_xprep_plain(const float* x, int batch, int K, int x_stride, uint8_t* xf, cudaStream_t s) {
   const long long n = static_cast<long long>(batch) * K;
@@ -533,7 +532,7 @@ __global__ void xprep_merge_local_kernel(const float* frag_o, const float* frag_
       o[r] = frag_o[f * dp + d];
     }
   }
-  xf_write(xf, (batch + 7) / 8, b, k, merge_sources(lse, o, kvp));
+  xf_write(xf, xf_nb8(batch), b, k, merge_sources(lse, o, kvp));
 }
 cudaError_t launch_xprep_merge_local(const float* frag_o, const float* frag_lse, int batch, int q_per_slot,
                                      int kvp, int head_dim, int dp, int K, uint8_t* xf, int* bump_total,
@@ -562,12 +561,78 @@ __global__ void xprep_merge_recv_kernel(const float* recv, int batch, int kvp, i
       o[r] = src[k];
     }
   }
-  xf_write(xf, (batch + 7) / 8, b, k, merge_sources(lse, o, kvp));
+  xf_write(xf, xf_nb8(batch), b, k, merge_sources(lse, o, kvp));
 }
 cudaError_t launch_xprep_merge_recv(const float* recv, int batch, int kvp, int chunk, int slice, int exch_rank,
                                     int head_dim, uint8_t* xf, int* bump_total, cudaStream_t s) {
   const long long n = static_cast<long long>(batch) * slice;
   return launch_k(xprep_merge_recv_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, recv,
                   batch, kvp, chunk, slice, exch_rank, head_dim, xf, bump_total);
+}
+}  // namespace hx
+
+// ---------------------------------------------------------------- MoE routing
+namespace hx {
+__global__ void moe_route_kernel(const float* logits, int batch, int n_experts, int top_k, int e_begin, int e_end,
+                                 float* route_w, int* group_ids, int* group_count) {
+  griddep_wait();
+  griddep_launch_dependents();
+  extern __shared__ int s_flag[];  // [n_experts]
+  for (int i = threadIdx.x; i < n_experts; i += blockDim.x) s_flag[i] = 0;
+  for (int i = threadIdx.x; i < batch * n_experts; i += blockDim.x) route_w[i] = 0.f;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int b = warp; b < batch; b += nw) {
+    const float* r = logits + static_cast<size_t>(b) * n_experts;
+    float sel_v[16];
+    int sel_i[16];
+    for (int k = 0; k < top_k; ++k) {
+      // warp argmax over experts not yet selected (ties: lower index)
+      float bv = -INFINITY;
+      int bi = 0x7fffffff;
+      for (int e = lane; e < n_experts; e += 32) {
+        bool taken = false;
+        for (int j = 0; j < k; ++j) taken |= sel_i[j] == e;
+        const float v = r[e];
+        if (!taken && (v > bv || (v == bv && e < bi))) {
+          bv = v;
+          bi = e;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      sel_v[k] = bv;
+      sel_i[k] = bi;
+    }
+    if (lane == 0) {
+      const float m = sel_v[0];
+      float z = 0.f;
+      for (int k = 0; k < top_k; ++k) z += expf(sel_v[k] - m);
+      for (int k = 0; k < top_k; ++k) {
+        route_w[static_cast<size_t>(b) * n_experts + sel_i[k]] = expf(sel_v[k] - m) / z;
+        s_flag[sel_i[k]] = 1;
+      }
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {  // ascending list of active local experts
+    int c = 0;
+    for (int e = e_begin; e < e_end; ++e)
+      if (s_flag[e]) group_ids[c++] = e;
+    *group_count = c;
+  }
+}
+cudaError_t launch_moe_route(const float* logits, int batch, int n_experts, int top_k, int e_begin, int e_end,
+                             float* route_w, int* group_ids, int* group_count, cudaStream_t s) {
+  if (top_k > 16) return cudaErrorInvalidValue;
+  return launch_k(moe_route_kernel, dim3(1), dim3(512), static_cast<size_t>(n_experts) * sizeof(int), s, logits,
+                  batch, n_experts, top_k, e_begin, e_end, route_w, group_ids, group_count);
 }
 }  // namespace hx

@@ -12,6 +12,7 @@
 #pragma once
 
 #include "common.cuh"
+#include "kernels.h"  // xf_nb8
 
 namespace hx {
 

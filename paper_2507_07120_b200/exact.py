@@ -61,13 +61,13 @@ class MsgKind:
 
 class _Engine:
     def __init__(self, model, tpa, kvp, chunk_size, batch, capacity, device=0, use_graphs=True, hopb=False,
-                 pool=0, rank=0, nccl_id=None, loopback=None):
+                 pool=0, rank=0, nccl_id=None, loopback=None, ep=1):
         self.mc = model
         self._nccl_buf = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         self._loopback = loopback  # the group must outlive its engines
         self.pc = ParallelConfig(tpa=tpa, kvp=kvp, chunk_size=chunk_size, distributed=pool, rank=rank,
                                  nccl_unique_id=C.cast(self._nccl_buf, C.c_void_p) if nccl_id is not None else None,
-                                 loopback=loopback._h if loopback is not None else None)
+                                 loopback=loopback._h if loopback is not None else None, ep=ep)
         self.rc = RuntimeConfig(batch=batch, capacity_tokens=capacity, device=device, hopb=int(hopb),
                                 use_graphs=int(use_graphs))
         h = C.c_void_p()

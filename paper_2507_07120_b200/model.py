@@ -160,22 +160,27 @@ def load_model(name_or_path):
 class HelixDecoder(_Engine):
     """Full decode step of a GQA decoder stack under Helix (tpa, kvp) on one device.
 
-    `layers`/`vocab` override the spec (layer slices, small vocab for tests)."""
+    `layers`/`vocab` override the spec (layer slices, small vocab for tests).
+    With `spec.moe` every layer's FFN is the routed MoE (top-k of total_experts,
+    SwiGLU experts of expert_ffn_dim) plus a shared expert of
+    shared_expert_ffn_dim (0: none); in a distributed pool the FFN runs on the
+    re-provisioned ep x tpf grid (types.hpp:100), tpf = tpa*kvp/ep."""
 
     def __init__(self, spec, tpa=1, kvp=1, chunk_size=16, batch=8, capacity=4096, layers=None, vocab=None,
-                 device=0, use_graphs=True, hopb=False, pool=0, rank=0, nccl_id=None, loopback=None):
+                 device=0, use_graphs=True, hopb=False, pool=0, rank=0, nccl_id=None, loopback=None, ep=1):
         if spec.attention != "gqa":
             raise NotImplementedError("MLA attention is not implemented in this build (GQA only)")
-        if spec.moe:
-            raise NotImplementedError("MoE FFN is not implemented in this build (dense SwiGLU only)")
         self.spec = spec
         self.layers = layers or spec.layers
         self.vocab = vocab or spec.vocab
+        m = spec.moe
         mc = ModelConfig(hidden=spec.hidden_dim, query_heads=spec.query_heads, kv_heads=spec.kv_heads,
-                         head_size=spec.head_size, ffn=spec.ffn_dim, layers=self.layers, vocab=self.vocab,
-                         attention_only=0)
+                         head_size=spec.head_size, ffn=m.shared_expert_ffn_dim if m else spec.ffn_dim,
+                         layers=self.layers, vocab=self.vocab, attention_only=0,
+                         n_experts=m.total_experts if m else 0, top_k=m.active_experts_per_token if m else 0,
+                         expert_ffn=m.expert_ffn_dim if m else 0)
         super().__init__(mc, tpa, kvp, chunk_size, batch, capacity, device, use_graphs=use_graphs, hopb=hopb,
-                         pool=pool, rank=rank, nccl_id=nccl_id, loopback=loopback)
+                         pool=pool, rank=rank, nccl_id=nccl_id, loopback=loopback, ep=ep)
         self.n_ranks = tpa * kvp if pool else 1
         self.rank = rank
         self.vocab_local = -(-self.vocab // self.n_ranks)

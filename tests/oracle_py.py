@@ -49,6 +49,9 @@ def lib():
             "oracle_reference_attention": (C.c_int, [dp, dp, dp, i64, i64, dp]),
             "oracle_merge_head_fragments": (C.c_int, [i64, i64, dp, dp, dp, dp]),
             "oracle_model_create": (C.c_int, [i64] * 11 + [u64, C.c_int, C.c_int, C.POINTER(vp)]),
+            "oracle_model_create_moe": (C.c_int, [i64] * 14 + [u64, C.c_int, C.c_int, C.POINTER(vp)]),
+            "oracle_model_routes": (C.c_int, [vp, ip]),
+            "oracle_model_route_gaps": (C.c_int, [vp, dp]),
             "oracle_model_free": (None, [vp]),
             "oracle_model_grow_random": (C.c_int, [vp, i64, i64, i64, vp]),
             "oracle_model_grow_hash": (C.c_int, [vp, i64, i64, i64]),
@@ -229,13 +232,33 @@ class Model:
     WEIGHTS = {"wq": 0, "wk": 1, "wv": 2, "wo": 3, "wgate": 4, "wup": 5, "wdown": 6, "emb": 7, "lm": 8}
 
     def __init__(self, hidden, q, k, hsz, ffn, layers, vocab, tpa=1, kvp=1, chunk=16, batch=1,
-                 seed=0, qkv_hash=False, bf16=True):
+                 seed=0, qkv_hash=False, bf16=True, moe=None):
+        """moe = (n_experts, top_k, expert_ffn): every layer's FFN is routed MoE,
+        `ffn` is then the shared expert width (0: none)."""
         self.dims = dict(hidden=hidden, q=q, k=k, hsz=hsz, ffn=ffn, layers=layers, vocab=vocab)
         self.batch = batch
+        self.moe = moe
         h = C.c_void_p()
-        check(lib().oracle_model_create(hidden, q, k, hsz, ffn, layers, vocab, tpa, kvp, chunk, batch,
-                                        seed, int(qkv_hash), int(bf16), C.byref(h)))
+        if moe:
+            check(lib().oracle_model_create_moe(hidden, q, k, hsz, ffn, layers, vocab, moe[0], moe[1], moe[2],
+                                                tpa, kvp, chunk, batch, seed, int(qkv_hash), int(bf16),
+                                                C.byref(h)))
+        else:
+            check(lib().oracle_model_create(hidden, q, k, hsz, ffn, layers, vocab, tpa, kvp, chunk, batch,
+                                            seed, int(qkv_hash), int(bf16), C.byref(h)))
         self.h = h
+
+    def routes(self):
+        """Last step's selected experts [layers][B][top_k] (descending router logit)."""
+        out = np.zeros((self.dims["layers"], self.batch, self.moe[1]), dtype=np.int64)
+        check(lib().oracle_model_routes(self.h, _ip(out)))
+        return out
+
+    def route_gaps(self):
+        """Last step's router margin r[k-th] - r[(k+1)-th], [layers][B]."""
+        out = np.zeros((self.dims["layers"], self.batch))
+        check(lib().oracle_model_route_gaps(self.h, _dp(out)))
+        return out
 
     def grow_random(self, layer, request, n, rng):
         check(lib().oracle_model_grow_random(self.h, layer, request, n, rng.h))

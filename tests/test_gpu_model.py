@@ -79,3 +79,21 @@ def test_hash_init_matches_oracle_weights():
     lo, ho, no = o.step(np.array([1, 2]))
     assert rel_err(hidden[0], ho[0]) == 0.0  # embedding rows are bit-identical
     assert rel_err(logits, lo) <= TOL_STEP0
+
+
+@pytest.mark.parametrize("batch", [24, 64])
+def test_large_batch_decode(batch):
+    """B up to 64 (the HOP-B sweep's batch range): 4 and 8 batch groups per HMMA tile."""
+    import paper_2507_07120_b200 as P
+    spec = P.model.ModelSpec("t", 1, 128, 4, 2, 32, 256, 3, "gqa", 0, vocab=500)
+    g = P.HelixDecoder(spec, batch=batch, capacity=128, layers=1, vocab=500)
+    g.init_weights(31, qkv="hash")
+    g.fill_kv_hash(40, 31)
+    o = O.Model(128, 4, 2, 32, 256, 1, 500, batch=batch, seed=31, qkv_hash=True, bf16=True)
+    for b in range(batch):
+        o.grow_hash(0, b, 40)
+    toks = np.arange(batch) * 7 % 500
+    nxt, logits, hidden = g.step(toks, want_logits=True, want_hidden=True)
+    lo, ho, no = o.step(toks)
+    assert rel_err(hidden, ho) <= TOL_STEP0
+    assert rel_err(logits, lo) <= TOL_STEP0

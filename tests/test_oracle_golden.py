@@ -125,3 +125,22 @@ def test_bf16_rounding_is_rne():
     b = np.array([f32]).view(np.uint32)[0]
     b = (b + 0x7FFF + ((b >> 16) & 1)) & 0xFFFF0000
     assert np.array([b], dtype=np.uint32).view(np.float32)[0] == np.float32(r[3])
+
+
+def test_oracle_moe_routing_invariants():
+    """MoE oracle: k distinct in-range experts per (layer, request), listed by
+    descending router logit (margins >= 0); top_k == E selects every expert."""
+    for E, k in [(8, 3), (4, 4)]:
+        m = O.Model(64, 4, 2, 16, 0, 2, 50, batch=3, seed=5, qkv_hash=True, bf16=True, moe=(E, k, 32))
+        for l in range(2):
+            for b in range(3):
+                m.grow_hash(l, b, 9)
+        lo, ho, no = m.step(np.array([1, 2, 3]))
+        r = m.routes()
+        assert r.shape == (2, 3, k)
+        for l in range(2):
+            for b in range(3):
+                assert len(set(r[l, b])) == k and r[l, b].min() >= 0 and r[l, b].max() < E
+        g = m.route_gaps()
+        assert (g >= 0).all()
+        assert np.isfinite(lo).all() and np.abs(ho[-1] - ho[0]).max() > 0
