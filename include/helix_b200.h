@@ -56,6 +56,10 @@ typedef struct hx_model_config {
   int64_t n_experts;
   int64_t top_k;
   int64_t expert_ffn;
+  /* MLA attention (types.hpp:37-49): kv_latent > 0 gives one latent KV head of width
+   * 2*kv_latent (must be 576 = 512 value dims + 64 rope dims), kv_heads = 1, tpa = 1,
+   * query_heads <= 128, absorbed projections (oracle/layer_oracle.hpp). */
+  int64_t kv_latent;
 } hx_model_config;
 
 typedef struct hx_loopback hx_loopback;

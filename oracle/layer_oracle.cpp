@@ -48,11 +48,23 @@ ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, st
     throw std::invalid_argument("hidden_dim must equal query_heads * head_size");
   if (d.n_experts > 0 && (d.top_k < 1 || d.top_k > d.n_experts || d.expert_ffn < 1))
     throw std::invalid_argument("invalid MoE shape");
+  const bool mla = d.kv_latent > 0;
+  if (mla && (d.kv_heads != 1 || tpa != 1 || mla_width(d.kv_latent) <= 64))
+    throw std::invalid_argument("MLA needs kv_heads == 1, tpa == 1 and a latent wider than the 64 rope dims");
+  const i64 W = mla ? mla_width(d.kv_latent) : 0, DV = mla ? mla_value_width(d.kv_latent) : 0;
   const double sh = 1.0 / std::sqrt(static_cast<double>(d.hidden));
   const double sf = 1.0 / std::sqrt(static_cast<double>(std::max<i64>(d.ffn, 1)));
   h_.reserve(static_cast<std::size_t>(d.layers * batch));
   for (i64 l = 0; l < d.layers; ++l) {
-    for (i64 b = 0; b < batch; ++b) {
+    if (mla) {
+      for (i64 b = 0; b < batch; ++b) mla_.emplace_back(kvp, 1, W, chunk);
+      wq_mla_.push_back(hash_matrix(seed, kWq, l, d.hidden, d.query_heads * W,
+                                    8.0 / std::sqrt(static_cast<double>(d.hidden)), bf16));
+      wdkv_.push_back(hash_matrix(seed, kWk, l, d.hidden, W, sh, bf16));
+      wo_.push_back(hash_matrix(seed, kWo, l, d.query_heads * DV, d.hidden,
+                                1.0 / std::sqrt(static_cast<double>(d.query_heads * DV)), bf16));
+    }
+    for (i64 b = 0; b < batch && !mla; ++b) {
       h_.emplace_back(Dims{d.query_heads, d.kv_heads, d.head_size}, tpa, kvp, chunk,
                       seed + static_cast<std::uint64_t>(l), bf16);
       if (qkv_init == QkvInit::Hash)
@@ -61,7 +73,7 @@ ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, st
             hash_matrix(seed, kWk, l, d.hidden, d.kv_heads * d.head_size, 1.0, bf16),
             hash_matrix(seed, kWv, l, d.hidden, d.kv_heads * d.head_size, 1.0, bf16));
     }
-    wo_.push_back(hash_matrix(seed, kWo, l, d.hidden, d.hidden, sh, bf16));
+    if (!mla) wo_.push_back(hash_matrix(seed, kWo, l, d.hidden, d.hidden, sh, bf16));
     if (d.ffn > 0) {  // dense FFN, or the MoE shared expert
       wg_.push_back(hash_matrix(seed, kWgate, l, d.hidden, d.ffn, sh, bf16));
       wu_.push_back(hash_matrix(seed, kWup, l, d.hidden, d.ffn, sh, bf16));
@@ -101,10 +113,29 @@ ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, st
 }
 
 void ModelOracle::grow_random(i64 layer, i64 request, i64 n, std::mt19937_64& rng) {
+  if (d_.kv_latent > 0) throw std::invalid_argument("MLA caches are grown with the counter hash");
   harness(layer, request).grow_random(n, rng);
 }
 
 void ModelOracle::grow_hash(i64 layer, i64 request, i64 n) {
+  if (d_.kv_latent > 0) {
+    const i64 W = mla_width(d_.kv_latent);
+    ShardedKVCache& c = mla_[static_cast<std::size_t>(layer * batch_ + request)];
+    for (i64 i = 0; i < n; ++i) {
+      const i64 g = c.total_tokens();
+      Mat row(1, W);
+      for (i64 dd = 0; dd < W; ++dd) {
+        const std::uint64_t idx =
+            ((static_cast<std::uint64_t>(request) << 32) + static_cast<std::uint64_t>(g)) *
+                static_cast<std::uint64_t>(W) +
+            static_cast<std::uint64_t>(dd);
+        const double v = hash_unit(seed_, hash_stream(kCacheK, layer), idx);
+        row(0, dd) = bf16_ ? round_bf16(v) : v;
+      }
+      c.append_round_robin(row, row);
+    }
+    return;
+  }
   DecodeHarness& h = harness(layer, request);
   const i64 K = d_.kv_heads, w = d_.head_size;
   for (i64 i = 0; i < n; ++i) {
@@ -165,6 +196,26 @@ std::vector<double> ModelOracle::ffn(i64 l, i64 b, const std::vector<double>& f)
   return y;
 }
 
+std::vector<double> ModelOracle::attend_mla(i64 l, i64 b, const std::vector<double>& a) {
+  const i64 Qh = d_.query_heads, W = mla_width(d_.kv_latent), DV = mla_value_width(d_.kv_latent);
+  const std::vector<double> qf = vecmat(a, wq_mla_[static_cast<std::size_t>(l)]);
+  Mat q(Qh, W);
+  for (i64 i = 0; i < Qh * W; ++i) q.a[static_cast<std::size_t>(i)] = round_bf16(qf[static_cast<std::size_t>(i)]);
+  ShardedKVCache& cache = mla_[static_cast<std::size_t>(l * batch_ + b)];
+  std::vector<AttentionFragment> frags;
+  for (i64 r = 0; r < cache.kvp(); ++r) frags.push_back(shard_attention(q, cache, r, 0, 1, Qh));
+  const AttentionFragment m = merge_fragments(frags);
+  std::vector<double> att(static_cast<std::size_t>(Qh * DV));
+  for (i64 h = 0; h < Qh; ++h)
+    for (i64 dd = 0; dd < DV; ++dd) att[static_cast<std::size_t>(h * DV + dd)] = m.out(h, dd);
+  // attend-then-append: this token's latent joins the cache after the merge
+  const std::vector<double> c = vecmat(a, wdkv_[static_cast<std::size_t>(l)]);
+  Mat row(1, W);
+  for (i64 dd = 0; dd < W; ++dd) row(0, dd) = bf16_ ? round_bf16(c[static_cast<std::size_t>(dd)]) : c[static_cast<std::size_t>(dd)];
+  cache.append_round_robin(row, row);
+  return att;
+}
+
 std::vector<double> ModelOracle::step(const std::vector<std::int64_t>& tokens,
                                       std::vector<double>* hidden,
                                       std::vector<std::int64_t>* next) {
@@ -181,8 +232,9 @@ std::vector<double> ModelOracle::step(const std::vector<std::int64_t>& tokens,
     if (hidden) std::copy(x.begin(), x.end(), hidden->begin() + b * H);
     for (i64 l = 0; l < d_.layers; ++l) {
       const std::vector<double> a = rmsnorm(x);
-      const Mat att = harness(l, b).step(a);  // [Q x Hsz] == flattened [H]
-      const std::vector<double> o = vecmat(att.a, wo_[static_cast<std::size_t>(l)]);
+      // GQA: [Q x Hsz] == flattened [H]; MLA: [Q x DV]
+      const std::vector<double> att = d_.kv_latent > 0 ? attend_mla(l, b, a) : harness(l, b).step(a).a;
+      const std::vector<double> o = vecmat(att, wo_[static_cast<std::size_t>(l)]);
       std::vector<double> h(static_cast<std::size_t>(H));
       for (i64 i = 0; i < H; ++i) h[static_cast<std::size_t>(i)] = x[static_cast<std::size_t>(i)] + o[static_cast<std::size_t>(i)];
       const std::vector<double> dn = ffn(l, b, rmsnorm(h));

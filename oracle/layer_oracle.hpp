@@ -62,7 +62,26 @@ inline std::uint64_t expert_stream(HashKind kind, std::int64_t layer, std::int64
 struct ModelDims {
   i64 hidden, query_heads, kv_heads, head_size, ffn, layers, vocab;
   i64 n_experts = 0, top_k = 0, expert_ffn = 0;  // n_experts == 0: dense FFN of width `ffn`
+  i64 kv_latent = 0;  // > 0: MLA attention (types.hpp:37-49), latent width W = 2 * kv_latent
 };
+
+// MLA attention in the absorbed decode form (types.hpp:37-49: K_eff = 1, one
+// latent "KV head" of width W = 2 * kv_latent_dim = 576 for deepseek-r1-like,
+// 512 latent + 64 rope dims). Per request, with a = rmsnorm(x):
+//   q_h = bf16(a . Wq[:, h*W:(h+1)*W])   (absorbed W_UK; hash kWq, scale 8/sqrt(H);
+//                                          the B200 MMA consumes q in bf16)
+//   c   = a . Wdkv                        (hash kWk, scale 1/sqrt(H); stored bf16)
+//   o_h = partial_head_attention / merge_head_fragments (attention.hpp:65-78,
+//         :118-137, via shard_attention / merge_fragments) with keys = values =
+//         the rank's latent rows, scale logit_scale(W) = 1/sqrt(W); keep
+//         o_h[0:DV], DV = W - 64 (the value part of the latent)
+//   h   = x + concat_h(o_h) . Wo          (absorbed W_UV W_O: [Q*DV x H], hash kWo,
+//                                          scale 1/sqrt(Q*DV))
+// then append c round-robin (attend-then-append, attention.hpp:504-508).
+// Cache fill: latent element d of token g of (layer, request) =
+//   hash_unit(seed, (kCacheK<<32)|layer, ((request << 32) + g) * W + d).
+inline i64 mla_width(i64 kv_latent) { return 2 * kv_latent; }
+inline i64 mla_value_width(i64 kv_latent) { return 2 * kv_latent - 64; }
 
 enum class QkvInit { MT19937 = 0, Hash = 1 };
 
@@ -105,6 +124,9 @@ class ModelOracle {
   std::vector<Mat> wo_, wg_, wu_, wd_, wr_;
   std::vector<std::vector<Mat>> eg_, eu_, ed_;  // [layer][expert]
   std::vector<std::vector<i64>> routes_;        // [layer*B + b] -> selected experts
+  std::vector<ShardedKVCache> mla_;             // [layer*B + b] latent caches (MLA)
+  std::vector<Mat> wq_mla_, wdkv_;              // [layer]
+  std::vector<double> attend_mla(i64 l, i64 b, const std::vector<double>& a);
   std::vector<double> gaps_;                    // [layer*B + b] -> top-k margin
   Mat emb_, lm_;
   std::vector<double> ffn(i64 l, i64 b, const std::vector<double>& f);

@@ -220,6 +220,21 @@ int oracle_model_create_moe(i64 hidden, i64 q, i64 k, i64 hsz, i64 shared_ffn, i
   });
 }
 
+// General model: MoE when n_experts > 0, MLA attention when kv_latent > 0.
+int oracle_model_create_ex(i64 hidden, i64 q, i64 k, i64 hsz, i64 ffn, i64 layers, i64 vocab, i64 n_experts,
+                           i64 top_k, i64 expert_ffn, i64 kv_latent, i64 tpa, i64 kvp, i64 chunk, i64 batch,
+                           std::uint64_t seed, int qkv_hash, int bf16, void** out) {
+  return guard([&] {
+    ModelDims d{hidden, q, k, hsz, ffn, layers, vocab};
+    d.n_experts = n_experts;
+    d.top_k = top_k;
+    d.expert_ffn = expert_ffn;
+    d.kv_latent = kv_latent;
+    *out = new ModelOracle(d, tpa, kvp, chunk, batch, seed, qkv_hash ? QkvInit::Hash : QkvInit::MT19937,
+                           bf16 != 0);
+  });
+}
+
 // routes of the last step: [layers][B][top_k]
 int oracle_model_routes(void* mp, std::int64_t* out) {
   return guard([&] {

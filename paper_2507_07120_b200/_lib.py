@@ -17,7 +17,7 @@ i64, u64, i32, dp, fp, vp = C.c_int64, C.c_uint64, C.c_int32, C.POINTER(C.c_doub
 class ModelConfig(C.Structure):
     _fields_ = [("hidden", i64), ("query_heads", i64), ("kv_heads", i64), ("head_size", i64), ("ffn", i64),
                 ("layers", i64), ("vocab", i64), ("attention_only", i32), ("reserved", i32),
-                ("n_experts", i64), ("top_k", i64), ("expert_ffn", i64)]
+                ("n_experts", i64), ("top_k", i64), ("expert_ffn", i64), ("kv_latent", i64)]
 
 
 POOL_LOCAL, POOL_NCCL, POOL_LOOPBACK = 0, 1, 2

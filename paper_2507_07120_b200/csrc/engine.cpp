@@ -113,7 +113,19 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
   if (L_ < 1) throw std::invalid_argument("layers must be >= 1");
   if (B_ < 1 || B_ > 64) throw std::invalid_argument("batch must be in [1, 64] for the B200 decode kernels");
   if (cap_ < 1) throw std::invalid_argument("capacity_tokens must be >= 1");
-  if (D_ > 128) throw std::invalid_argument("head_size > 128 is not supported by the GQA decode kernel");
+  mla_ = m.kv_latent > 0;
+  if (mla_) {
+    // types.hpp:43-49: MLA keeps one latent KV head; Helix needs tpa <= K_eff = 1 (types.cpp:122-139)
+    W_ = static_cast<int>(2 * m.kv_latent);
+    DV_ = W_ - 64;
+    if (W_ != kMlaW) throw std::invalid_argument("MLA kernel supports kv_latent_dim = 288 (576-wide latent)");
+    if (Kh_ != 1) throw std::invalid_argument("MLA keeps a single latent KV head");
+    if (tpa_ != 1) throw std::invalid_argument("MLA needs tpa = 1 (tpa <= effective KV heads)");
+    if (Qh_ > kMlaHeads) throw std::invalid_argument("MLA kernel supports at most 128 query heads");
+    if (m.attention_only) throw std::invalid_argument("the attention-only harness is GQA (DecodeHarness)");
+  } else if (D_ > 128) {
+    throw std::invalid_argument("head_size > 128 is not supported by the GQA decode kernel");
+  }
   if (H_ % 16) throw std::invalid_argument("hidden width must be a multiple of 16");
   moe_ = !attn_only_ && m.n_experts > 0;
   if (moe_) {
@@ -134,8 +146,10 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
     throw std::invalid_argument("unknown pool mode");
 
   DP_ = D_ <= 32 ? 32 : (D_ <= 64 ? 64 : 128);
+  AD_ = mla_ ? DV_ : static_cast<int>(D_);   // per-head attention output width
+  ADP_ = mla_ ? DV_ : DP_;                    // its stride in the fragment buffers
   G_ = static_cast<int>(Qh_ / Kh_);
-  q_chunks_ = (G_ + 7) / 8;
+  q_chunks_ = mla_ ? 1 : (G_ + 7) / 8;
   kvh_per_slot_ = static_cast<int>(Kh_ / tpa_);
   q_per_slot_ = static_cast<int>(Qh_ / tpa_);
   N_ = tpa_ * kvp_;
@@ -167,9 +181,10 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
     r_ = rank_ % kvp_;
     n_slots_ = 1;
     slot_base_ = rank_;
-    slice_ = static_cast<int>(q_per_slot_ * D_ / kvp_);
-    if (slice_ % 16) throw std::invalid_argument("distributed Helix needs hidden/(tpa*kvp) to be a multiple of 16");
-    xchunk_ = static_cast<int>(exchange_layout(q_per_slot_, D_, kvp_, nullptr));
+    slice_ = static_cast<int>(q_per_slot_ * AD_ / kvp_);
+    if ((q_per_slot_ * AD_) % kvp_ || slice_ % 16)
+      throw std::invalid_argument("distributed Helix needs hidden/(tpa*kvp) to be a multiple of 16");
+    xchunk_ = static_cast<int>(exchange_layout(q_per_slot_, AD_, kvp_, nullptr));
     if (!attn_only_) {
       if (F_ % N_ || (F_ > 0 && (F_ / N_) % 16))
         throw std::invalid_argument("ffn_dim/(tpa*kvp) must be a multiple of 16");
@@ -179,8 +194,13 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
   }
   const int64_t per_rank_max = ((cap_ + static_cast<int64_t>(chunk_) * kvp_ - 1) /
                                 (static_cast<int64_t>(chunk_) * kvp_)) * chunk_;
-  page_cap_ = static_cast<int>((per_rank_max + 15) / 16 + 1);
-  page_bytes_ = 64u * static_cast<size_t>(DP_);
+  if (mla_) {
+    page_cap_ = static_cast<int>((per_rank_max + kMlaPageRows - 1) / kMlaPageRows + 1);
+    page_bytes_ = mla_page_bytes();
+  } else {
+    page_cap_ = static_cast<int>((per_rank_max + 15) / 16 + 1);
+    page_bytes_ = 64u * static_cast<size_t>(DP_);
+  }
 
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   cudaDeviceProp prop{};
@@ -219,6 +239,7 @@ Engine::~Engine() {
   for (auto* p : w_router_) f(p);
   for (auto* p : w_egu_) f(p);
   for (auto* p : w_edown_) f(p);
+  f(d_qimg_);
   f(d_rlog_); f(d_route_w_); f(d_gids_); f(d_gcount_); f(d_xf_em_); f(d_moe_y_);
   f(w_lm_); f(emb_); f(d_total_); f(d_q_); f(d_part_o_); f(d_part_lse_); f(d_work_);
   f(d_frag_o_); f(d_frag_lse_); f(d_ypart_); f(d_counters_); f(d_x_); f(d_ss_); f(d_m_);
@@ -258,20 +279,33 @@ void Engine::alloc() {
     return std::max(1, std::min((target_items + streams - 1) / streams, std::max(1, pages_max / 8)));
   };
   n_streams_ = n_slots_ * B_ * kvh_per_slot_ * q_chunks_;
-  splits_ = splits_for(n_streams_);
   const int req_streams = n_slots_ * kvh_per_slot_ * q_chunks_;
-  splits_req_ = splits_for(req_streams);
-  n_items_ = std::max(n_streams_ * splits_, req_streams * splits_req_);
+  if (mla_) {
+    // one item per SM: (split, stream, value half), statically strided over the grid
+    auto mla_splits = [&](int streams) {
+      return std::max(1, std::min(num_sms_ / (2 * streams), pages_max));
+    };
+    splits_ = mla_splits(n_streams_);
+    splits_req_ = mla_splits(req_streams);
+    n_items_ = 2 * std::max(n_streams_ * splits_, req_streams * splits_req_);
+    d_qimg_ = dalloc<uint8_t>(static_cast<size_t>(B_) * mla_q_bytes(), "mla query images");
+  } else {
+    splits_ = splits_for(n_streams_);
+    splits_req_ = splits_for(req_streams);
+    n_items_ = std::max(n_streams_ * splits_, req_streams * splits_req_);
+  }
   attn_grid_ = std::min(num_sms_, n_items_);
   if (dist_mode_ != HX_POOL_LOCAL) {
     d_send_ = dalloc<float>(static_cast<size_t>(kvp_) * B_ * xchunk_, "exchange send");
     d_recv_ = dalloc<float>(static_cast<size_t>(kvp_) * B_ * xchunk_, "exchange recv");
     d_parth_ = dalloc<float>(static_cast<size_t>(B_) * H_, "tp partial");
   }
-  d_part_o_ = dalloc<float>(static_cast<size_t>(n_items_) * 8 * DP_, "part_o");
-  d_part_lse_ = dalloc<float>(static_cast<size_t>(n_items_) * 8, "part_lse");
+  const size_t part_rows = mla_ ? static_cast<size_t>(kMlaHeads) : 8;  // rows per item
+  const size_t part_w = mla_ ? static_cast<size_t>(DV_ / 2) : static_cast<size_t>(DP_);
+  d_part_o_ = dalloc<float>(static_cast<size_t>(n_items_) * part_rows * part_w, "part_o");
+  d_part_lse_ = dalloc<float>(static_cast<size_t>(n_items_) * part_rows, "part_lse");
   d_work_ = dalloc<int>(4, "work counters");
-  d_frag_o_ = dalloc<float>(static_cast<size_t>(n_slots_) * B_ * q_per_slot_ * DP_, "frag_o");
+  d_frag_o_ = dalloc<float>(static_cast<size_t>(n_slots_) * B_ * q_per_slot_ * ADP_, "frag_o");
   d_frag_lse_ = dalloc<float>(static_cast<size_t>(n_slots_) * B_ * q_per_slot_, "frag_lse");
   d_x_ = dalloc<float>(static_cast<size_t>(B_) * H_, "x");
   d_out_ = dalloc<float>(static_cast<size_t>(B_) * Qh_ * D_, "out");
@@ -317,16 +351,20 @@ void Engine::plan_gemvs() {
     return g;
   };
   const bool dist = dist_mode_ != HX_POOL_LOCAL;
-  const int nq = static_cast<int>((dist ? q_per_slot_ : Qh_) * D_);
-  const int nk = static_cast<int>((dist ? kvh_per_slot_ : Kh_) * D_);
-  const int Nqkv = nq + 2 * nk;
+  // MLA: absorbed q for every head (W wide) + one latent row (types.hpp:43-49)
+  const int qw = mla_ ? W_ : static_cast<int>(D_);
+  const int nq = static_cast<int>((dist ? q_per_slot_ : Qh_) * qw);
+  const int nk = mla_ ? W_ : static_cast<int>((dist ? kvh_per_slot_ : Kh_) * D_);
+  const int Nqkv = nq + (mla_ ? 1 : 2) * nk;
   const int Hh = static_cast<int>(H_);
+  const int AW = static_cast<int>(Qh_) * AD_;  // merged attention width (GQA: = H)
   const int F = F_local_;
   for (int64_t l = 0; l < L_; ++l) {
     GemvPlan q = make(Nqkv, round_up(Nqkv, 128), Hh, attn_only_ ? 0 : 1, E_QKV);
     q.p.nq = nq;
     q.p.nk = nk;
-    q.p.kv_heads = nk / static_cast<int>(D_);
+    q.p.kv_heads = nk / qw;
+    q.p.mla = mla_ ? 1 : 0;
     q.p.kv_head_base = dist ? grp_ * kvh_per_slot_ : 0;
     q.p.kvh_per_slot = kvh_per_slot_;
     q.p.rr_chunk = chunk_;
@@ -334,13 +372,14 @@ void Engine::plan_gemvs() {
     q.p.slot_base = slot_base_;
     q.p.n_local_slots = n_slots_;
     q.p.append = 1;
+    if (mla_) q.p.head_dim = W_;
     plan_qkv_.push_back(q);
     if (!attn_only_) {
       if (dist) {
         // O-proj: this rank's exchanged slice of its group's heads x its rows of W_O
         plan_o_.push_back(make(Hh, round_up(Hh, 128), slice_, 0, E_STORE));
       } else {
-        plan_o_.push_back(make(Hh, round_up(Hh, 128), Hh, 0, E_RESID));
+        plan_o_.push_back(make(Hh, round_up(Hh, 128), AW, 0, E_RESID));
       }
       if (F > 0) {  // dense FFN, or the MoE shared expert
         plan_gu_.push_back(make(2 * F, round_up(F, 64) * 2, Hh, 1, E_SWIGLU));
@@ -393,7 +432,7 @@ void Engine::plan_gemvs() {
     const int nb8 = xf_nb8(B_);
     auto xf_alloc = [&](int K) { return dalloc<uint8_t>(static_cast<size_t>(K / 16) * 3 * nb8 * 256, "xf"); };
     d_xf_resid_ = xf_alloc(static_cast<int>(H_));
-    d_xf_attn_ = xf_alloc(dist ? slice_ : static_cast<int>(H_));
+    d_xf_attn_ = xf_alloc(dist ? slice_ : AW);
     d_xf_m_ = xf_alloc(std::max(16, F_local_));
   }
   d_counters_ = dalloc<int>(static_cast<size_t>(max_counters_), "counters");
@@ -419,7 +458,6 @@ void Engine::plan_gemvs() {
 void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
   const bool dist = dist_mode_ != HX_POOL_LOCAL;
   const int Hh = static_cast<int>(H_);
-  const int Dd = static_cast<int>(D_);
   // columns of W_q / W_k / W_v held here (all, or this rank's TPA group's heads)
   const int nq = static_cast<int>((dist ? q_per_slot_ : Qh_) * D_);
   const int nk = static_cast<int>((dist ? kvh_per_slot_ : Kh_) * D_);
@@ -443,7 +481,12 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
   const int Qall = static_cast<int>(Qh_ * D_), Kall = static_cast<int>(Kh_ * D_);
   for (int64_t l = 0; l < L_; ++l) {
     if (w_qkv_.size() <= static_cast<size_t>(l)) w_qkv_.push_back(walloc(plan_qkv_[l]));
-    if (qkv_hash) {
+    if (mla_) {  // absorbed W_q (kWq, 8/sqrt(H)) and the latent down-projection (kWk, 1/sqrt(H))
+      const int nqm = static_cast<int>(Qh_) * W_;
+      init(w_qkv_[l], plan_qkv_[l],
+           {{hash_stream(kWq, l), 0, nqm, nqm, 0, 0, 8.0 / std::sqrt(static_cast<double>(H_)), 0, 0},
+            {hash_stream(kWk, l), nqm, nqm + W_, W_, 0, 0, sh, 0, 0}});
+    } else if (qkv_hash) {
       init(w_qkv_[l], plan_qkv_[l],
            {{hash_stream(kWq, l), 0, nq, Qall, q0, 0, 1.0, 0, 0},
             {hash_stream(kWk, l), nq, nq + nk, Kall, k0, 0, 1.0, 0, 0},
@@ -459,8 +502,9 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
         }
       }
       // O-proj input rows: this rank's slice of its group's flattened heads
-      const int ko = dist ? grp_ * q_per_slot_ * Dd + r_ * slice_ : 0;
-      init(w_o_[l], plan_o_[l], {{hash_stream(kWo, l), 0, Hh, Hh, 0, 0, sh, ko, 0}});
+      const int ko = dist ? grp_ * q_per_slot_ * AD_ + r_ * slice_ : 0;
+      const double so = mla_ ? 1.0 / std::sqrt(static_cast<double>(Qh_ * AD_)) : sh;  // MLA: W_o is [Q*DV x H]
+      init(w_o_[l], plan_o_[l], {{hash_stream(kWo, l), 0, Hh, Hh, 0, 0, so, ko, 0}});
       plan_o_[l].p.w = w_o_[l];
       if (F > 0) {
         init(w_gu_[l], plan_gu_[l],
@@ -514,6 +558,7 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
     q.ypart = d_ypart_;
     q.counters = d_counters_;
     q.q_out = d_q_;
+    q.q_img = d_qimg_;
     q.kv = kv_[l];
     q.total = d_total_ + l * B_;
     q.xf = d_xf_resid_;  // harness: the host x prepared into the same buffer
@@ -615,6 +660,7 @@ void Engine::mark(int kind) {
 void Engine::init_weights_hash(uint64_t seed) { build_weights_common(seed, true); }
 
 void Engine::init_weights_mt19937(uint64_t seed) {
+  if (mla_) throw std::invalid_argument("MLA weights come from the counter hash (the reference has no MLA draws)");
   build_weights_common(seed, false);
   const int64_t nq = Qh_ * D_, nk = Kh_ * D_;
   for (int64_t l = 0; l < L_; ++l) {
@@ -660,6 +706,7 @@ void Engine::check_layer(int64_t layer) const {
 
 void Engine::grow_random(int64_t layer, int64_t request, int64_t n, std::mt19937_64& rng) {
   check_layer(layer);
+  if (mla_) throw std::invalid_argument("MLA caches are grown with the counter hash (fill_kv_hash)");
   if (request < 0 || request >= B_) throw std::invalid_argument("request out of range");
   const int64_t per = Kh_ * D_;
   const int64_t block = 4096;
@@ -685,6 +732,7 @@ void Engine::grow_random(int64_t layer, int64_t request, int64_t n, std::mt19937
 
 void Engine::append_kv(int64_t layer, int64_t request, int64_t n, const float* k, const float* v) {
   check_layer(layer);
+  if (mla_) throw std::invalid_argument("append_kv takes GQA K/V rows; MLA caches hold latents");
   if (request < 0 || request >= B_) throw std::invalid_argument("request out of range");
   if (n < 0) throw std::invalid_argument("token count must be >= 0");
   if (h_total_[static_cast<size_t>(layer * B_ + request)] + n > cap_)
@@ -716,7 +764,13 @@ void Engine::fill_kv_hash(int64_t n, uint64_t seed) {
   for (int64_t l = 0; l < L_; ++l)
     for (int b = 0; b < B_; ++b)
       if (h_total_[static_cast<size_t>(l * B_ + b)] + n > cap_) throw std::invalid_argument("KV capacity exceeded");
-  for (int64_t l = 0; l < L_; ++l) {
+  for (int64_t l = 0; l < L_ && mla_; ++l) {
+    cuda_check(launch_kv_fill_hash_mla(kv_[l], d_total_ + l * B_, B_, kvp_, chunk_, page_cap_, slot_base_, n_slots_,
+                                       n, seed, hash_stream(kCacheK, l), stream_),
+               "kv fill");
+    for (int b = 0; b < B_; ++b) h_total_[static_cast<size_t>(l * B_ + b)] += n;
+  }
+  for (int64_t l = 0; l < L_ && !mla_; ++l) {
     cuda_check(launch_kv_fill_hash(kv_[l], d_total_ + l * B_, B_, static_cast<int>(Kh_), kvh_per_slot_, kvp_,
                                    chunk_, static_cast<int>(D_), DP_, page_cap_, slot_base_, n_slots_, n, seed,
                                    hash_stream(kCacheK, l), hash_stream(kCacheV, l), stream_),
@@ -751,6 +805,28 @@ int Engine::slot_local_of(int rank, int group) const { return group * kvp_ + ran
 
 void Engine::read_kv(int64_t layer, int64_t request, int64_t rank, int64_t head, float* k, float* v) {
   check_layer(layer);
+  if (mla_) {  // latent rows: k = [n x W], v = [n x DV] (the value part of the same rows)
+    if (head != 0) throw std::invalid_argument("kv head out of range");
+    const int64_t n = effective_tokens(layer, request, rank);
+    const int sl = slot_local_of(static_cast<int>(rank), 0);
+    if (sl < 0 || sl >= n_slots_) throw std::invalid_argument("rank not resident on this device");
+    const int pages = static_cast<int>((n + kMlaPageRows - 1) / kMlaPageRows);
+    std::vector<uint8_t> buf(static_cast<size_t>(pages) * page_bytes_);
+    const size_t base = (static_cast<size_t>(sl) * B_ + request) * page_cap_ * page_bytes_;
+    cuda_check(cudaStreamSynchronize(stream_), "read_kv sync");
+    if (pages)
+      cuda_check(cudaMemcpy(buf.data(), kv_[layer] + base, buf.size(), cudaMemcpyDeviceToHost), "read_kv");
+    for (int64_t t = 0; t < n; ++t) {
+      const uint8_t* page = buf.data() + static_cast<size_t>(t / kMlaPageRows) * page_bytes_;
+      for (int d = 0; d < W_; ++d) {
+        uint16_t kb;
+        std::memcpy(&kb, page + mla_kv_offset(static_cast<int>(t % kMlaPageRows), d), 2);
+        k[t * W_ + d] = float_from_bf16_bits(kb);
+        if (d < DV_) v[t * DV_ + d] = float_from_bf16_bits(kb);
+      }
+    }
+    return;
+  }
   if (head < 0 || head >= Kh_) throw std::invalid_argument("kv head out of range");
   const int64_t n = effective_tokens(layer, request, rank);
   const int grp = static_cast<int>(head / kvh_per_slot_), kvh = static_cast<int>(head % kvh_per_slot_);
@@ -791,6 +867,7 @@ void Engine::record_transcript(int64_t layers) {
   for (int64_t l = 0; l < layers; ++l)
     for (int b = 0; b < B_; ++b) {
       for (int64_t r = 1; r < pool; ++r) transcript_.push_back({0, 0, r, H_, 0});
+      if (mla_) continue;  // the message records are DecodeHarness (GQA) semantics
       for (int g = 0; g < tpa_; ++g)
         for (int r = 0; r < kvp_; ++r)
           for (int p = 0; p < kvp_; ++p) {
@@ -829,8 +906,28 @@ AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) const {
   a.n_streams = n_slots_ * b_count * kvh_per_slot_ * q_chunks_;
   a.splits = b_count == B_ ? splits_ : splits_req_;
   a.n_items = a.n_streams * splits_;
-  a.qscale = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(D_)));
+  a.qscale = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(mla_ ? W_ : D_)));
+  if (mla_) {
+    a.qimg = d_qimg_;
+    a.n_items = 2 * a.n_streams * a.splits;
+    a.dp = DV_;
+  }
   return a;
+}
+
+// 2-3: flash-decode partials over every local rank's shard (attend BEFORE
+// append), then per-rank fragments (split merge); the token totals are bumped
+// by the merge kernel, after which the appended token counts.
+void Engine::launch_attention_kernels(const AttnParams& a) {
+  if (mla_) {
+    cuda_check(launch_mla_decode(a, std::min(attn_grid_, a.n_items), stream_), "mla attention");
+    mark(2);
+    cuda_check(launch_mla_split_reduce(a, d_frag_o_, d_frag_lse_, stream_), "mla split reduce");
+  } else {
+    cuda_check(launch_attn_decode(a, std::min(attn_grid_, a.n_items), stream_), "attention");
+    mark(2);
+    cuda_check(launch_attn_split_reduce(a, d_frag_o_, d_frag_lse_, stream_), "split reduce");
+  }
 }
 
 void Engine::enqueue_attention(int64_t layer) {
@@ -845,11 +942,7 @@ void Engine::enqueue_attention(int64_t layer) {
   }
   // 2. flash-decode partials over every local rank's shard (attend BEFORE append)
   const AttnParams a = attn_params(layer, 0, B_);
-  cuda_check(launch_attn_decode(a, attn_grid_, stream_), "attention");
-  mark(2);
-  // 3. per-rank fragments (split merge); the token totals are bumped by the
-  //    next kernel (merge), after which the appended token counts
-  cuda_check(launch_attn_split_reduce(a, d_frag_o_, d_frag_lse_, stream_), "split reduce");
+  launch_attention_kernels(a);
   mark(3);
 }
 
@@ -865,10 +958,8 @@ void Engine::enqueue_exchange_and_attention_dist(int64_t layer) {
   for (int i = 0; i < rounds; ++i) {
     const int b0 = i * per;
     const AttnParams a = attn_params(layer, b0, per);
-    cuda_check(launch_attn_decode(a, std::min(attn_grid_, a.n_items), stream_), "attention");
-    mark(2);
-    cuda_check(launch_attn_split_reduce(a, d_frag_o_, d_frag_lse_, stream_), "split reduce");
-    cuda_check(launch_pack_exchange(d_frag_o_, d_frag_lse_, b0, per, B_, q_per_slot_, static_cast<int>(D_), DP_,
+    launch_attention_kernels(a);
+    cuda_check(launch_pack_exchange(d_frag_o_, d_frag_lse_, b0, per, B_, q_per_slot_, AD_, ADP_,
                                     kvp_, slice_, xchunk_, d_send_, stream_),
                "pack");
     mark(3);
@@ -912,6 +1003,7 @@ void Engine::harness_step(int64_t layer, const float* x_host, int64_t x_len, flo
 
 void Engine::harness_step_device(int64_t layer, const float* x_dev, float* out_dev) {
   check_layer(layer);
+  if (mla_) throw StateError("the attention-only harness is DecodeHarness (GQA); MLA runs through decode_step");
   if (dist_mode_ != HX_POOL_LOCAL)
     throw StateError("the attention-only harness runs on a local pool; distributed pools use decode_step");
   if (!weights_ready_) throw StateError("weights are not initialised");
@@ -938,8 +1030,8 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
     enqueue_attention(l);
     if (!dist) {
       // LSE-rescale combine of the KVP fragments -> O-proj activations (attention.hpp:118-175)
-      cuda_check(launch_xprep_merge_local(d_frag_o_, d_frag_lse_, B_, q_per_slot_, kvp_, static_cast<int>(D_), DP_,
-                                          static_cast<int>(H_), d_xf_attn_, d_total_ + l * B_, stream_),
+      cuda_check(launch_xprep_merge_local(d_frag_o_, d_frag_lse_, B_, q_per_slot_, kvp_, AD_, ADP_,
+                                          static_cast<int>(Qh_) * AD_, d_xf_attn_, d_total_ + l * B_, stream_),
                  "merge");
       cuda_check(launch_gemv(plan_o_[l].p, 0, E_RESID, num_sms_, stream_), "o-proj");
       mark(4);
@@ -947,7 +1039,7 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
     } else {
       // merge of the exchanged slices, then TP O-proj over this rank's slice and
       // AllReduce over the pool (latency.cpp:85-94)
-      cuda_check(launch_xprep_merge_recv(d_recv_, B_, kvp_, xchunk_, slice_, r_, static_cast<int>(D_), d_xf_attn_,
+      cuda_check(launch_xprep_merge_recv(d_recv_, B_, kvp_, xchunk_, slice_, r_, AD_, d_xf_attn_,
                                          d_total_ + l * B_, stream_),
                  "merge");
       cuda_check(launch_gemv(plan_o_[l].p, 0, E_STORE, num_sms_, stream_), "o-proj");

@@ -53,8 +53,16 @@ struct AttnParams {
   int q_grp_base;          // first TPA group whose query heads are in `q` (0: all groups)
   int b_begin;             // requests [b_begin, b_begin + stream_batch) in this launch
   int stream_batch;        // (HOP-B launches one request at a time)
+  const uint8_t* qimg;     // MLA: [B] absorbed-query images (kv_layout.cuh mla_q_offset)
 };
 cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t stream);
+// MLA (tcgen05): items = (split, stream, value half); part_o [n_items][128][256],
+// part_lse2 [n_items][128]; the split reduce writes frag_o [slot][b][q][512].
+cudaError_t launch_mla_decode(const AttnParams& p, int grid, cudaStream_t stream);
+cudaError_t launch_mla_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse, cudaStream_t stream);
+cudaError_t launch_kv_fill_hash_mla(uint8_t* kv, int* total, int batch, int kvp, int chunk, int page_cap,
+                                    int slot_base, int n_local_slots, long long n, uint64_t seed, uint64_t stream_k,
+                                    cudaStream_t stream);
 cudaError_t launch_attn_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse,
                                      cudaStream_t stream);
 cudaError_t launch_bump_totals(int* total, int n, cudaStream_t stream);
@@ -91,6 +99,8 @@ struct GemvParams {
   int nq, nk, kv_heads, kvh_per_slot, rr_chunk, page_cap, slot_base, n_local_slots;
   int kv_head_base;      // global index of the first KV head in this projection
   int append;            // write K/V into the cache
+  uint8_t* q_img;        // MLA (mla = 1): q -> bf16 query images, latent -> MLA pages
+  int mla;
   int kvp, head_dim, dp;
   // E_LOGITS
   unsigned long long* best;  // [B] packed (orderable logit, ~index)

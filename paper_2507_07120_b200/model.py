@@ -158,7 +158,9 @@ def load_model(name_or_path):
 
 
 class HelixDecoder(_Engine):
-    """Full decode step of a GQA decoder stack under Helix (tpa, kvp) on one device.
+    """Full decode step of a decoder stack under Helix (tpa, kvp): GQA attention, or
+    MLA (attention == "mla": one 2*kv_latent_dim-wide latent KV head, absorbed
+    projections, tcgen05 attention kernel; oracle/layer_oracle.hpp).
 
     `layers`/`vocab` override the spec (layer slices, small vocab for tests).
     With `spec.moe` every layer's FFN is the routed MoE (top-k of total_experts,
@@ -168,8 +170,6 @@ class HelixDecoder(_Engine):
 
     def __init__(self, spec, tpa=1, kvp=1, chunk_size=16, batch=8, capacity=4096, layers=None, vocab=None,
                  device=0, use_graphs=True, hopb=False, pool=0, rank=0, nccl_id=None, loopback=None, ep=1):
-        if spec.attention != "gqa":
-            raise NotImplementedError("MLA attention is not implemented in this build (GQA only)")
         self.spec = spec
         self.layers = layers or spec.layers
         self.vocab = vocab or spec.vocab
@@ -178,7 +178,8 @@ class HelixDecoder(_Engine):
                          head_size=spec.head_size, ffn=m.shared_expert_ffn_dim if m else spec.ffn_dim,
                          layers=self.layers, vocab=self.vocab, attention_only=0,
                          n_experts=m.total_experts if m else 0, top_k=m.active_experts_per_token if m else 0,
-                         expert_ffn=m.expert_ffn_dim if m else 0)
+                         expert_ffn=m.expert_ffn_dim if m else 0,
+                         kv_latent=spec.kv_latent_dim if spec.attention == "mla" else 0)
         super().__init__(mc, tpa, kvp, chunk_size, batch, capacity, device, use_graphs=use_graphs, hopb=hopb,
                          pool=pool, rank=rank, nccl_id=nccl_id, loopback=loopback, ep=ep)
         self.n_ranks = tpa * kvp if pool else 1
