@@ -64,20 +64,20 @@ __host__ __device__ __forceinline__ long long rr_count(long long total, int r, i
 // ---------------------------------------------------------------------------
 // MLA latent pages (types.hpp:37-49: one latent "KV head" of width W = 576 per
 // token; keys = the whole latent, values = its first DV = 512 dims).
-// One page = 256 local rows of one (rank shard, request). Layout = UMMA
+// One page = 128 local rows of one (rank shard, request). Layout = UMMA
 // canonical no-swizzle core matrices, d-group major:
-//   [dg = d/8 : 72][tg = row/8 : 32][row%8 : 8][d%8 : 8] bf16
-// so 64 consecutive latent dims of all 256 rows are one contiguous 32 KB
+//   [dg = d/8 : 72][tg = row/8 : 16][row%8 : 8][d%8 : 8] bf16
+// so 64 consecutive latent dims of all 128 rows are one contiguous 16 KB
 // block: a K-major B operand (rows = tokens) for S = Q . C^T and, read with
 // the other stride pair, an MN-major B operand (rows = tokens, N = dims) for
 // O = P . V -- the same bytes, no transpose.
 constexpr int kMlaW = 576;
 constexpr int kMlaDV = 512;
-constexpr int kMlaPageRows = 256;
+constexpr int kMlaPageRows = 128;
 constexpr int kMlaHeads = 128;  // UMMA M: query heads per CTA (zero-padded)
 __host__ __device__ __forceinline__ uint32_t mla_page_bytes() { return kMlaPageRows * kMlaW * 2; }
 __host__ __device__ __forceinline__ uint32_t mla_kv_offset(int r, int d) {
-  return static_cast<uint32_t>((((d >> 3) * 32 + (r >> 3)) * 64 + (r & 7) * 8 + (d & 7)) * 2);
+  return static_cast<uint32_t>((((d >> 3) * (kMlaPageRows / 8) + (r >> 3)) * 64 + (r & 7) * 8 + (d & 7)) * 2);
 }
 // Per-request absorbed-query image [dg : 72][head group : 16][head%8][d%8] bf16
 // (K-major A operand, M = 128 heads): written by the QKV epilogue.

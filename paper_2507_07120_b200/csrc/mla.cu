@@ -9,24 +9,28 @@
 //
 // At ~242 FLOP per KV byte MLA sits at the B200 ridge, so both GEMMs run on
 // tcgen05 (UMMA M = 128 heads, fp32 accumulators in TMEM). The fp32 output
-// [128 x 512] alone fills all 512 TMEM columns, so a work item owns one
+// [128 x 512] alone would fill all 512 TMEM columns, so a work item owns one
 // VALUE HALF (256 dims): the two items of a (split, stream) pair each compute
 // S for the whole tile and accumulate their half of O (the QK^T product is
 // issued twice; the KV bytes come from HBM once and from L2 twice).
 //
-// TMEM (512 columns x 128 lanes fp32):  S / P  [0, 256)   O half [256, 512)
-// Shared memory: Q image (147,456 B, K-major A operand, loaded once per item)
-//                + 2 x 32 KB ring of latent chunks (64 dims x 256 tokens).
+// TMEM (512 columns x 128 lanes fp32):
+//   S/P buffer 0 [0, 128)   S/P buffer 1 [128, 256)   O half [256, 512)
+// Tiles are 128-row pages; S of tile t+1 is computed while the softmax of
+// tile t runs, and P.V(t) follows. Shared memory: the Q image (147,456 B,
+// K-major A operand, once per item) + a 5 x 16 KB ring of latent chunks
+// (64 dims x 128 rows, contiguous in the page layout).
 // Roles (192 threads):
 //   warps 0-3  softmax: thread = head row = TMEM lane. Row max, lazy rescale
-//              of O (only when the max grows by > 2^8, FA4-style), P = exp2
-//              in bf16 written back into TMEM over S (A operand of P.V), row
-//              sum of the bf16-rounded P, final O / z and log2-domain LSE.
-//   warp 4     producer: cp.async.bulk of the Q image and latent chunks.
+//              of O (only when the max grows by > 2^8, FA4-style; decided per
+//              warp), P = exp2 in bf16 written into TMEM over S (the A operand
+//              of P.V), row sum of the bf16-rounded P, final O / z and LSE.
+//   warp 4     producer: cp.async.bulk of the Q image and latent chunks in
+//              the MMA's consumption order.
 //   warp 5     TMEM allocation + MMA issue (one thread):
-//                S(t)  = 36 x UMMA SS  M128 N256 K16 (Q smem, latent K-major)
-//                O    += 64 x UMMA TS  M128 N64  K16 (P in TMEM, latent MN-major)
-// Tile = one 256-row page; items are statically strided over the grid.
+//                S(t)  = 36 x UMMA SS  M128 N128 K16 (Q smem, latent K-major)
+//                O    += 32 x UMMA TS  M128 N64  K16 (P in TMEM, latent MN-major)
+// Items (split, stream, value half) are statically strided over the grid.
 #include "common.cuh"
 #include "kernels.h"
 #include "kv_layout.cuh"
@@ -36,11 +40,12 @@ namespace hx {
 
 namespace {
 constexpr uint32_t kQBytes = kMlaW * kMlaHeads * 2;  // 147456
-constexpr uint32_t kChunk = 64 * kMlaPageRows * 2;   // 32768: 64 latent dims x 256 rows
+constexpr uint32_t kChunk = 64 * kMlaPageRows * 2;   // 16384: 64 latent dims x 128 rows
 constexpr int kSChunks = kMlaW / 64;                 // 9
 constexpr int kVChunks = kMlaDV / 2 / 64;            // 4 per value half
-constexpr int kSlots = 2;
-constexpr uint32_t kIdescS = umma_idesc_bf16(128, 256, false, false);
+constexpr int kSlots = 5;
+constexpr uint32_t kDgStride = kMlaPageRows / 8 * 128;  // bytes between 8-dim groups of a chunk
+constexpr uint32_t kIdescS = umma_idesc_bf16(128, kMlaPageRows, false, false);
 constexpr uint32_t kIdescPV = umma_idesc_bf16(128, 64, false, true);
 constexpr int kThreads = 192;
 
@@ -64,6 +69,29 @@ __device__ __forceinline__ MlaItem decode_item(const AttnParams& p, int item) {
   it.pg1 = static_cast<int>((static_cast<long long>(split + 1) * pages) / p.splits);
   return it;
 }
+
+// Consumption order of an item's chunks (producer and MMA agree on it):
+//   S(0), S(1), V(0), S(2), V(1), S(3), ..., V(n-1)
+// step k of an item with n tiles -> (tile, is_value)
+__device__ __forceinline__ void mla_step(int k, int n, int& tile, bool& value) {
+  if (k < 2 || n == 1) {
+    if (n == 1) {
+      tile = 0;
+      value = k == 1;
+    } else {
+      tile = k;
+      value = false;
+    }
+    return;
+  }
+  const int j = k - 2;  // V(j/2) then S(j/2 + 2)
+  tile = j / 2 + ((j & 1) ? 2 : 0);
+  value = (j & 1) == 0;
+  if (tile >= n) {  // past the last S: only V remains
+    tile = n - 1;
+    value = true;
+  }
+}
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParams p) {
@@ -71,15 +99,15 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
   uint8_t* qs = smem;
   uint8_t* ring = smem + kQBytes;
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kSlots * kChunk);
-  uint64_t* full = bars;       // [2]
-  uint64_t* empty = bars + 2;  // [2]
-  uint64_t* q_full = bars + 4;
-  uint64_t* q_free = bars + 5;
-  uint64_t* s_full = bars + 6;
-  uint64_t* p_full = bars + 7;
-  uint64_t* pv_done = bars + 8;
-  uint64_t* o_free = bars + 9;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 10);
+  uint64_t* full = bars;                // [kSlots]
+  uint64_t* empty = bars + kSlots;      // [kSlots]
+  uint64_t* q_full = bars + 2 * kSlots;
+  uint64_t* q_free = q_full + 1;
+  uint64_t* s_full = q_full + 2;   // [2] per S buffer
+  uint64_t* p_full = q_full + 4;   // [2]
+  uint64_t* pv_done = q_full + 6;  // [2]
+  uint64_t* o_free = q_full + 8;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 9);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -89,9 +117,11 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
     }
     mbar_init(q_full, 1);
     mbar_init(q_free, 1);
-    mbar_init(s_full, 1);
-    mbar_init(p_full, 128);
-    mbar_init(pv_done, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&s_full[i], 1);
+      mbar_init(&p_full[i], 128);
+      mbar_init(&pv_done[i], 1);
+    }
     mbar_init(o_free, 128);
     fence_mbar_init();
   }
@@ -120,11 +150,15 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
         ++qcount;
         const uint8_t* kvb =
             p.kv + (static_cast<size_t>(it.sl) * p.batch + it.b) * p.page_cap * static_cast<size_t>(mla_page_bytes());
-        for (int pg = it.pg0; pg < it.pg1; ++pg) {
-          const uint8_t* page = kvb + static_cast<size_t>(pg) * mla_page_bytes();
-          for (int j = 0; j < kSChunks + kVChunks; ++j) {
-            // S chunks: dims [64j, 64j+64); value chunks: this item's half
-            const int blk = j < kSChunks ? j : 4 * it.half + (j - kSChunks);
+        const int n = it.pg1 - it.pg0;
+        for (int k = 0; k < 2 * n; ++k) {
+          int tile;
+          bool value;
+          mla_step(k, n, tile, value);
+          const uint8_t* page = kvb + static_cast<size_t>(it.pg0 + tile) * mla_page_bytes();
+          const int nch = value ? kVChunks : kSChunks;
+          for (int j = 0; j < nch; ++j) {
+            const int blk = value ? 4 * it.half + j : j;  // 64-dim block of the page
             const int s = it_slot % kSlots;
             if (it_slot >= kSlots) mbar_wait(&empty[s], ((it_slot / kSlots) - 1) & 1);
             mbar_arrive_expect_tx(&full[s], kChunk);
@@ -139,52 +173,59 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
     // ------------------------------------------------------------ MMA issuer
     if (lane == 0) {
       const uint32_t q_addr = smem_u32(qs), ring_addr = smem_u32(ring);
-      int it_slot = 0, qcount = 0, tiles = 0, items = 0;
+      int it_slot = 0, qcount = 0, g0 = 0, items = 0;  // g0: global index of the item's first tile
       for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
         const MlaItem it = decode_item(p, item);
         if (it.pg1 <= it.pg0) continue;
         mbar_wait(q_full, qcount & 1);
         ++qcount;
-        const int ntiles = it.pg1 - it.pg0;
-        for (int t = 0; t < ntiles; ++t) {
-          if (t > 0)
-            mbar_wait(pv_done, (tiles - 1) & 1);  // P of the previous tile consumed
-          else if (items > 0)
-            mbar_wait(o_free, (items - 1) & 1);   // previous item's O read out
-          tc_fence_after();
-          for (int j = 0; j < kSChunks; ++j) {
-            const int s = it_slot % kSlots;
-            mbar_wait(&full[s], (it_slot / kSlots) & 1);
+        tc_fence_after();
+        const int n = it.pg1 - it.pg0;
+        for (int k = 0; k < 2 * n; ++k) {
+          int tile;
+          bool value;
+          mla_step(k, n, tile, value);
+          const int g = g0 + tile, buf = g & 1;
+          if (!value) {
+            // S(tile) into buffer buf: the P.V that last read this buffer must be done
+            if (g >= 2) mbar_wait(&pv_done[buf], ((g >> 1) - 1) & 1);
             tc_fence_after();
+            for (int j = 0; j < kSChunks; ++j) {
+              const int s = it_slot % kSlots;
+              mbar_wait(&full[s], (it_slot / kSlots) & 1);
+              tc_fence_after();
 #pragma unroll
-            for (int kk = 0; kk < 4; ++kk) {
-              const int ks = 4 * j + kk;  // 16-dim k-step of the latent
-              const uint64_t a = umma_desc(q_addr + ks * 4096, 2048, 128);
-              const uint64_t bd = umma_desc(ring_addr + s * kChunk + kk * 8192, 4096, 128);
-              umma_ss(tbase, a, bd, kIdescS, (j | kk) != 0);
+              for (int kk = 0; kk < 4; ++kk) {
+                const uint64_t a = umma_desc(q_addr + (4 * j + kk) * 4096, 2048, 128);
+                const uint64_t bd = umma_desc(ring_addr + s * kChunk + kk * 2 * kDgStride, kDgStride, 128);
+                umma_ss(tbase + buf * 128, a, bd, kIdescS, (j | kk) != 0);
+              }
+              umma_commit(&empty[s]);
+              ++it_slot;
             }
-            umma_commit(&empty[s]);
-            ++it_slot;
-          }
-          if (t == ntiles - 1) umma_commit(q_free);
-          umma_commit(s_full);
-          mbar_wait(p_full, tiles & 1);
-          tc_fence_after();
-          for (int v = 0; v < kVChunks; ++v) {
-            const int s = it_slot % kSlots;
-            mbar_wait(&full[s], (it_slot / kSlots) & 1);
+            if (tile == n - 1) umma_commit(q_free);
+            umma_commit(&s_full[buf]);
+          } else {
+            mbar_wait(&p_full[buf], (g >> 1) & 1);
+            if (tile == 0 && items > 0) mbar_wait(o_free, (items - 1) & 1);  // previous O read out
             tc_fence_after();
-#pragma unroll 4
-            for (int kk = 0; kk < kMlaPageRows / 16; ++kk) {
-              const uint64_t bd = umma_desc(ring_addr + s * kChunk + kk * 256, 128, 4096);
-              umma_ts(tbase + 256 + 64 * v, tbase + 8 * kk, bd, kIdescPV, (t > 0 || kk > 0) ? 1u : 0u);
+            for (int v = 0; v < kVChunks; ++v) {
+              const int s = it_slot % kSlots;
+              mbar_wait(&full[s], (it_slot / kSlots) & 1);
+              tc_fence_after();
+#pragma unroll
+              for (int kk = 0; kk < kMlaPageRows / 16; ++kk) {
+                const uint64_t bd = umma_desc(ring_addr + s * kChunk + kk * 256, 128, kDgStride);
+                umma_ts(tbase + 256 + 64 * v, tbase + buf * 128 + 8 * kk, bd, kIdescPV,
+                        (tile > 0 || kk > 0) ? 1u : 0u);
+              }
+              umma_commit(&empty[s]);
+              ++it_slot;
             }
-            umma_commit(&empty[s]);
-            ++it_slot;
+            umma_commit(&pv_done[buf]);
           }
-          umma_commit(pv_done);
-          ++tiles;
         }
+        g0 += n;
         ++items;
       }
     }
@@ -192,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
     // ------------------------------------------------------------ softmax (warps 0-3)
     const int h = threadIdx.x;  // head row == TMEM lane
     const uint32_t lrow = tbase + (static_cast<uint32_t>(warp * 32) << 16);
-    int tiles = 0, items = 0;
+    int g = 0;
     for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
       const MlaItem it = decode_item(p, item);
       float* po = p.part_o + (static_cast<size_t>(item) * kMlaHeads + h) * 256;
@@ -205,29 +246,34 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
         continue;
       }
       float m = -INFINITY, z = 0.f;
-      const int ntiles = it.pg1 - it.pg0;
-      for (int t = 0; t < ntiles; ++t) {
+      const int n = it.pg1 - it.pg0;
+      for (int t = 0; t < n; ++t, ++g) {
+        const int buf = g & 1;
+        const uint32_t sb = lrow + buf * 128;
         const int valid = min(kMlaPageRows, it.ntok - (it.pg0 + t) * kMlaPageRows);
-        mbar_wait(s_full, tiles & 1);
+        mbar_wait(&s_full[buf], (g >> 1) & 1);
         tc_fence_after();
         float mt = -INFINITY;
 #pragma unroll 1
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < kMlaPageRows / 32; ++c) {
           float v[32];
-          tmem_ld32(lrow + 32 * c, v);
+          tmem_ld32(sb + 32 * c, v);
 #pragma unroll
           for (int i = 0; i < 32; ++i)
             if (32 * c + i < valid) mt = fmaxf(mt, v[i]);
         }
         mt *= p.qscale;
         // Lazy rescale: a row keeps its reference max unless the tile max exceeds
-        // it by 2^8. The decision is made per warp (tcgen05.ld/st are warp-collective);
-        // rows that did not grow rescale by exactly 1.
+        // it by 2^8. Decided per warp (tcgen05.ld/st are warp-collective); rows
+        // that did not grow rescale by exactly 1.
         const bool grow = mt > m + 8.f;
         if (__any_sync(0xffffffffu, grow)) {
           const float m_new = grow ? mt : m;
           const float alpha = grow ? exp2f(m - m_new) : 1.f;  // 0 on the first tile
-          if (t > 0) {  // O holds earlier tiles (their P.V completed before S(t) was issued)
+          if (t > 0) {
+            // O holds tiles < t: wait for P.V(t-1), then rescale it in TMEM
+            mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+            tc_fence_after();
 #pragma unroll 1
             for (int c = 0; c < 8; ++c) {
               float v[32];
@@ -241,9 +287,9 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
           m = m_new;
         }
 #pragma unroll 1
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < kMlaPageRows / 32; ++c) {
           float v[32];
-          tmem_ld32(lrow + 32 * c, v);
+          tmem_ld32(sb + 32 * c, v);
           uint32_t pk[16];
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
@@ -253,14 +299,13 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
             z += __low2float(pb) + __high2float(pb);
             pk[i] = *reinterpret_cast<const uint32_t*>(&pb);
           }
-          tmem_st16(lrow + 16 * c, pk);  // P over the S columns already read
+          tmem_st16(sb + 16 * c, pk);  // P over the S columns already read
         }
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(p_full);
-        ++tiles;
+        mbar_arrive(&p_full[buf]);
       }
-      mbar_wait(pv_done, (tiles - 1) & 1);
+      mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
       tc_fence_after();
       const float inv = z > 0.f ? 1.f / z : 0.f;
 #pragma unroll 1
@@ -276,7 +321,6 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
       if (h < p.q_heads) *pl = z > 0.f ? m + log2f(z) : -INFINITY;
       tc_fence_before();
       mbar_arrive(o_free);
-      ++items;
     }
   }
   tc_fence_before();
@@ -326,7 +370,7 @@ __global__ void mla_split_reduce_kernel(const AttnParams p, float* frag_o, float
   if (lane == 0) frag_lse[fo] = L > 0.f ? (M + log2f(L)) * 0.69314718055994530942f : -INFINITY;
 }
 
-size_t mla_smem_bytes() { return kQBytes + kSlots * kChunk + 16 * 8; }
+size_t mla_smem_bytes() { return kQBytes + kSlots * kChunk + (2 * kSlots + 12) * 8; }
 
 cudaError_t launch_mla_decode(const AttnParams& p, int grid, cudaStream_t stream) {
   if (p.q_heads > kMlaHeads || p.q_heads < 1) return cudaErrorInvalidValue;
@@ -367,8 +411,8 @@ __global__ void kv_fill_hash_mla_kernel(uint8_t* kv, const int* total, int batch
   const long long st = idx / per_stream;  // slot_local * B + b
   const long long rem = idx - st * per_stream;
   const int page = static_cast<int>(rem / kRowsPerPage);
-  const int ci = static_cast<int>(rem % kRowsPerPage);  // (dg * 32 + tg) * 8 + r8
-  const int r8 = ci & 7, tg = (ci >> 3) & 31, dg = ci >> 8;
+  const int ci = static_cast<int>(rem % kRowsPerPage);  // (dg * 16 + tg) * 8 + r8
+  const int r8 = ci & 7, tg = (ci >> 3) & 15, dg = ci >> 7;
   const int b = static_cast<int>(st % batch);
   const int rank = (static_cast<int>(st / batch) + slot_base) % kvp;
   const long long row = static_cast<long long>(page) * kMlaPageRows + tg * 8 + r8;
