@@ -44,6 +44,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-context", type=int, default=131072)
     ap.add_argument("--profile-only", action="store_true", help="skip timing loops (for ncu)")
+    ap.add_argument("--no-deepseek", action="store_true", help="skip the deepseek-r1-like (MLA + MoE) slice")
+    ap.add_argument("--deepseek-context", type=int, default=125000,
+                    help="latent tokens per request on this GPU (1M context / KVP 8)")
     return ap.parse_args()
 
 
@@ -108,6 +111,82 @@ def peaks():
         return p["hbm_gbs"], "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def peak_tensor():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops_sustained"], "measured (sustained)"
+    except Exception:
+        return 1393.0, "fallback"
+
+
+def deepseek_slice(a):
+    """C4: deepseek-r1-like layer as ONE GPU of a KVP=8, EP=8 (tpf=1)
+    Helix pool: 128 heads over a B x 125,000-token latent shard (MLA, tcgen05),
+    32 of 256 experts (top-8) + 1/8 of the shared expert, 1/8 of W_O. Runs one
+    rank of an 8-rank loopback pool with the collectives switched off (a single
+    B200 here), so the number is this GPU's compute per layer; the reference's
+    NVLink terms are not included."""
+    import ctypes
+    import numpy as np
+    import torch
+    import paper_2507_07120_b200 as P
+    from paper_2507_07120_b200.model import Loopback
+    spec = P.model.PRESETS["deepseek-r1-like"]
+    B, S, N = a.batch, a.deepseek_context, 8
+    lb = Loopback(N)
+    eng = P.HelixDecoder(spec, tpa=1, kvp=N, batch=B, capacity=S * N + 64 * N, layers=1, vocab=4096,
+                         use_graphs=False, pool=2, rank=0, loopback=lb, ep=8)
+    P._lib.check(P.lib().hx_engine_set_flag(eng._h, 1, 3), eng._h)  # HX_FLAG_SKIP_COMM: no a2a / all-reduce
+    eng.init_weights(2507, qkv="hash")
+    eng.fill_kv_hash(S * N, 2507)  # rank 0 keeps S of the S*N global tokens
+    s_loc = int(P.lib().hx_effective_tokens(eng._h, 0, 0, 0))
+    tok = torch.randint(0, 4096, (B,), dtype=torch.int32, device="cuda")
+    nxt = torch.zeros(B, dtype=torch.int32, device="cuda")
+    for _ in range(a.warmup):
+        eng.step_device(tok.data_ptr(), nxt.data_ptr())
+    eng.synchronize()
+    prof = np.zeros(10)
+    reps = max(3, a.steps)
+    P.lib().hx_profile_step(eng._h, reps, prof.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    eng.synchronize()
+    # timed steps (eager; CUDA events on the engine stream)
+    stream = torch.cuda.ExternalStream(eng.stream())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(a.steps):
+        eng.step_device(tok.data_ptr(), nxt.data_ptr())
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    info = eng.info()
+    att_ms = prof[2]
+    kv_bytes = B * s_loc * 576 * 2
+    flops = B * s_loc * spec.query_heads * (576 + 512) * 2
+    hbm, _ = peaks()
+    tc, tc_kind = peak_tensor()
+    out = {
+        "workload": "deepseek-r1-like layer, one GPU of KVP=8 x EP=8 (tpf=1): 128 heads x %d latent tokens x B=%d; "
+                    "32/256 experts top-8 + shared 2048/8; collectives off (1 GPU)" % (s_loc, B),
+        "ms_per_layer": ms, "eager_launches": True,
+        "breakdown_ms": {k: float(v) for k, v in zip(
+            ["embed", "qkv", "attention", "split_reduce", "o_proj", "ffn_router_to_gate_up", "ffn_down_combine",
+             "lm_head", "merge"], prof)},
+        "mla_attention": {
+            "kernel": "mla_decode_kernel (tcgen05 SS + TS, TMEM accumulators)", "launch_ms": att_ms,
+            "algorithmic_kv_bytes": kv_bytes, "algorithmic_flops": flops,
+            "roofline": {"bound": "tensor", "achieved": flops / (att_ms * 1e-3) / 1e12, "peak": tc, "unit": "TFLOP/s",
+                         "frac": flops / (att_ms * 1e-3) / 1e12 / tc, "peak_kind": tc_kind,
+                         "hbm_achieved_gbs": kv_bytes / (att_ms * 1e-3) / 1e9,
+                         "hbm_frac": kv_bytes / (att_ms * 1e-3) / 1e9 / hbm,
+                         "t_roof_ms": max(kv_bytes / hbm / 1e6, flops / tc / 1e9)}},
+        "engine": info,
+    }
+    eng.close()
+    return out
 
 
 def ncu_traffic():
@@ -321,6 +400,12 @@ def ours(a):
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as ex:  # reported, never fatal for the GPU number
             line["cpu_baseline"] = {"error": str(ex)[:200]}
+    if world == 1 and not a.no_deepseek:
+        eng.close()  # free the 150 GB pool before the deepseek slice
+        try:
+            line["deepseek_slice"] = deepseek_slice(a)
+        except Exception as ex:  # reported, never fatal for the headline number
+            line["deepseek_slice"] = {"error": str(ex)[:300]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
