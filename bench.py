@@ -163,6 +163,7 @@ def deepseek_slice(a):
     e1.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
     info = eng.info()
+    active = int(P.lib().hx_moe_active_experts(eng._h))
     att_ms = prof[2]
     kv_bytes = B * s_loc * 576 * 2
     flops = B * s_loc * spec.query_heads * (576 + 512) * 2
@@ -183,6 +184,8 @@ def deepseek_slice(a):
                          "hbm_achieved_gbs": kv_bytes / (att_ms * 1e-3) / 1e9,
                          "hbm_frac": kv_bytes / (att_ms * 1e-3) / 1e9 / hbm,
                          "t_roof_ms": max(kv_bytes / hbm / 1e6, flops / tc / 1e9)}},
+        "moe": {"local_experts": 32, "active_local_experts_last_step": active,
+                "expert_bytes_streamed": active * 3 * spec.hidden_dim * spec.moe.expert_ffn_dim * 2},
         "engine": info,
     }
     eng.close()

@@ -182,6 +182,10 @@ int64_t hx_exchange_layout(int64_t q_per_group, int64_t head_size, int64_t kvp, 
 #define HX_FLAG_SKIP_COMM 1
 #define HX_FLAG_HOPB 2
 int hx_engine_set_flag(hx_engine* e, int32_t flag, int32_t value);
+/* MoE: experts held by this device that the last step's router selected in the
+ * last layer (the grouped GEMVs streamed exactly these weight blocks); 0 for
+ * dense models. Synchronises the engine stream. */
+int64_t hx_moe_active_experts(hx_engine* e);
 /* In-process group of n ranks on one device (one host thread per rank). */
 int hx_loopback_create(int32_t n_ranks, hx_loopback** out);
 void hx_loopback_destroy(hx_loopback* lb);

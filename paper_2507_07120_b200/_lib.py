@@ -72,6 +72,7 @@ EXPORTS = {
     "hx_loopback_create": (C.c_int, [i32, C.POINTER(vp)]),
     "hx_exchange_layout": (i64, [i64, i64, i64, C.POINTER(i64)]),
     "hx_engine_set_flag": (C.c_int, [vp, i32, i32]),
+    "hx_moe_active_experts": (i64, [vp]),
     "hx_loopback_destroy": (None, [vp]),
 }
 

@@ -173,4 +173,9 @@ int64_t hx_exchange_layout(int64_t q_per_group, int64_t head_size, int64_t kvp, 
 int hx_engine_set_flag(hx_engine* e, int32_t flag, int32_t value) {
   return guard(e, [&] { e->e->set_flag(flag, value); });
 }
+int64_t hx_moe_active_experts(hx_engine* e) {
+  int64_t n = -1;
+  guard(e, [&] { n = e->e->moe_active_experts(); });
+  return n;
+}
 }  // extern "C"

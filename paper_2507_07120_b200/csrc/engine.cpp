@@ -1161,6 +1161,14 @@ void Engine::set_flag(int flag, int value) {
   }
 }
 
+int64_t Engine::moe_active_experts() {
+  if (!moe_) return 0;
+  int n = 0;
+  cuda_check(cudaStreamSynchronize(stream_), "sync");
+  cuda_check(cudaMemcpy(&n, d_gcount_, sizeof(int), cudaMemcpyDeviceToHost), "expert count");
+  return n;
+}
+
 void Engine::synchronize() { cuda_check(cudaStreamSynchronize(stream_), "synchronize"); }
 
 void Engine::profile_step(int64_t reps, double* ms) {

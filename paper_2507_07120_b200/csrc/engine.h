@@ -69,6 +69,7 @@ class Engine {
   cudaStream_t stream() const { return stream_; }
   void info(hx_engine_info* out) const;
   void set_flag(int flag, int value);
+  int64_t moe_active_experts();
 
   const std::vector<Message>& transcript() const { return transcript_; }
   void clear_transcript() { transcript_.clear(); }

@@ -43,6 +43,39 @@ def test_sass_uses_bulk_copy_and_hmma():
     assert "HMMA.16816.F32.BF16" in sass
 
 
+def test_mla_kernel_uses_tcgen05():
+    """The MLA kernel issues 5th-gen tensor-core MMAs (UTCHMMA), moves TMEM
+    with tcgen05.ld/st (LDTM/STTM) and commits to mbarriers (UTCBAR)."""
+    so = os.path.join(ROOT, "paper_2507_07120_b200", "libhelix_b200.so")
+    sass = subprocess.run(["cuobjdump", "-sass", "-fun", "_ZN2hx17mla_decode_kernelENS_10AttnParamsE", so],
+                          capture_output=True, text=True).stdout
+    for op in ("UTCHMMA", "LDTM", "STTM", "UTCBAR", "UBLKCP"):
+        assert op in sass, op
+
+
+def test_ctypes_structs_match_c_header(tmp_path):
+    """The Python binding's struct layouts equal the C ABI's (sizeof + offsets)."""
+    from paper_2507_07120_b200 import _lib
+    src = tmp_path / "sz.c"
+    src.write_text("""#include <stdio.h>
+#include <stddef.h>
+#include "helix_b200.h"
+int main(void) {
+  printf("%zu %zu %zu %zu %zu %zu\\n", sizeof(hx_model_config), sizeof(hx_parallel_config),
+         sizeof(hx_runtime_config), sizeof(hx_engine_info), offsetof(hx_model_config, kv_latent),
+         offsetof(hx_parallel_config, ep));
+  return 0;
+}
+""")
+    exe = tmp_path / "sz"
+    subprocess.check_call(["gcc", "-I", os.path.join(ROOT, "include"), str(src), "-o", str(exe)])
+    got = [int(x) for x in subprocess.check_output([str(exe)], text=True).split()]
+    import ctypes as C
+    want = [C.sizeof(_lib.ModelConfig), C.sizeof(_lib.ParallelConfig), C.sizeof(_lib.RuntimeConfig),
+            C.sizeof(_lib.EngineInfo), _lib.ModelConfig.kv_latent.offset, _lib.ParallelConfig.ep.offset]
+    assert got == want
+
+
 @pytest.mark.parametrize("dims,tpa,kvp,msg", [
     ((4, 3, 8), 1, 1, "multiple of kv_heads"),
     ((4, 2, 8), 4, 1, "tpa must divide kv_heads"),
