@@ -144,3 +144,26 @@ def test_oracle_moe_routing_invariants():
         g = m.route_gaps()
         assert (g >= 0).all()
         assert np.isfinite(lo).all() and np.abs(ho[-1] - ho[0]).max() > 0
+
+
+@pytest.mark.parametrize("kvp", [2, 3])
+def test_oracle_mla_sharding_invariance(kvp):
+    """MLA through the reference's shard_attention + merge_fragments: hidden
+    states and logits do not depend on the KVP width (the Helix exactness
+    property, attention.hpp:118-175), to rounding."""
+    def run(k):
+        m = O.Model(128, 8, 1, 16, 64, 2, 50, kvp=k, batch=2, seed=4, qkv_hash=True, bf16=True, kv_latent=288)
+        for l in range(2):
+            for b in range(2):
+                m.grow_hash(l, b, 37 + 5 * b)
+        out = []
+        toks = np.array([1, 2])
+        for _ in range(2):
+            lo, ho, no = m.step(toks)
+            out.append((lo, ho))
+            toks = no
+        return out
+    a, b = run(1), run(kvp)
+    for (la, ha), (lb, hb) in zip(a, b):
+        assert np.abs(la - lb).max() <= 1e-10 * np.abs(la).max()
+        assert np.abs(ha - hb).max() <= 1e-10 * np.abs(ha).max()
