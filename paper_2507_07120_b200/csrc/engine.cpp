@@ -281,27 +281,27 @@ void Engine::alloc() {
   n_streams_ = n_slots_ * B_ * kvh_per_slot_ * q_chunks_;
   const int req_streams = n_slots_ * kvh_per_slot_ * q_chunks_;
   if (mla_) {
-    // one item per SM: (split, stream, value half), statically strided over the grid
+    // one item per CTA pair: (split, stream), statically strided over the pairs
     auto mla_splits = [&](int streams) {
-      return std::max(1, std::min(num_sms_ / (2 * streams), pages_max));
+      return std::max(1, std::min((num_sms_ / 2) / streams, std::max(1, pages_max / 2)));
     };
     splits_ = mla_splits(n_streams_);
     splits_req_ = mla_splits(req_streams);
-    n_items_ = 2 * std::max(n_streams_ * splits_, req_streams * splits_req_);
+    n_items_ = std::max(n_streams_ * splits_, req_streams * splits_req_);
     d_qimg_ = dalloc<uint8_t>(static_cast<size_t>(B_) * mla_q_bytes(), "mla query images");
   } else {
     splits_ = splits_for(n_streams_);
     splits_req_ = splits_for(req_streams);
     n_items_ = std::max(n_streams_ * splits_, req_streams * splits_req_);
   }
-  attn_grid_ = std::min(num_sms_, n_items_);
+  attn_grid_ = std::min(mla_ ? num_sms_ / 2 : num_sms_, n_items_);  // MLA: CTA pairs
   if (dist_mode_ != HX_POOL_LOCAL) {
     d_send_ = dalloc<float>(static_cast<size_t>(kvp_) * B_ * xchunk_, "exchange send");
     d_recv_ = dalloc<float>(static_cast<size_t>(kvp_) * B_ * xchunk_, "exchange recv");
     d_parth_ = dalloc<float>(static_cast<size_t>(B_) * H_, "tp partial");
   }
   const size_t part_rows = mla_ ? static_cast<size_t>(kMlaHeads) : 8;  // rows per item
-  const size_t part_w = mla_ ? static_cast<size_t>(DV_ / 2) : static_cast<size_t>(DP_);
+  const size_t part_w = mla_ ? static_cast<size_t>(DV_) : static_cast<size_t>(DP_);
   d_part_o_ = dalloc<float>(static_cast<size_t>(n_items_) * part_rows * part_w, "part_o");
   d_part_lse_ = dalloc<float>(static_cast<size_t>(n_items_) * part_rows, "part_lse");
   d_work_ = dalloc<int>(4, "work counters");
@@ -909,7 +909,7 @@ AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) const {
   a.qscale = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(mla_ ? W_ : D_)));
   if (mla_) {
     a.qimg = d_qimg_;
-    a.n_items = 2 * a.n_streams * a.splits;
+    a.n_items = a.n_streams * a.splits;
     a.dp = DV_;
   }
   return a;

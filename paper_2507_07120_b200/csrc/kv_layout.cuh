@@ -79,9 +79,12 @@ __host__ __device__ __forceinline__ uint32_t mla_page_bytes() { return kMlaPageR
 __host__ __device__ __forceinline__ uint32_t mla_kv_offset(int r, int d) {
   return static_cast<uint32_t>((((d >> 3) * (kMlaPageRows / 8) + (r >> 3)) * 64 + (r & 7) * 8 + (d & 7)) * 2);
 }
-// Per-request absorbed-query image [dg : 72][head group : 16][head%8][d%8] bf16
-// (K-major A operand, M = 128 heads): written by the QKV epilogue.
+// Per-request absorbed-query image, split in two head halves (one per CTA of
+// the MLA pair): [head/64 : 2][dg : 72][(head%64)/8 : 8][head%8][d%8] bf16 --
+// each half is the K-major B operand (N = 64 heads) of S^T = C . Q^T and one
+// contiguous 73,728-byte block. Written by the QKV epilogue.
 __host__ __device__ __forceinline__ uint32_t mla_q_bytes() { return kMlaW * kMlaHeads * 2; }
 __host__ __device__ __forceinline__ uint32_t mla_q_offset(int head, int d) {
-  return static_cast<uint32_t>((((d >> 3) * 16 + (head >> 3)) * 64 + (head & 7) * 8 + (d & 7)) * 2);
+  return static_cast<uint32_t>(((((head >> 6) * 72 + (d >> 3)) * 8 + ((head & 63) >> 3)) * 8 + (head & 7)) * 16 +
+                               (d & 7) * 2);
 }

@@ -1,36 +1,41 @@
-// MLA decode attention on the 5th-generation tensor cores (tcgen05 + TMEM).
+// MLA decode attention on the 5th-generation tensor cores (tcgen05 + TMEM),
+// one CTA PAIR (cluster of 2, cta_group::2) per work item.
 //
-// Per (rank shard, request): 128 query heads (zero-padded) share one latent
-// KV "head" of width W = 576 (keys = the latent, values = its first 512 dims):
-//   S = Q . C^T * (1/sqrt(W)),  P = exp(S - m),  O = P . C[:, :512]
-// -- partial_head_attention (attention.hpp:65-78) for every head of the
-// rank, with the LSE of each head (HeadFragment) so the fragments merge
-// exactly as merge_head_fragments (:118-137).
+// Per (rank shard, request): 128 query heads share one latent KV "head" of
+// width W = 576 (keys = the latent, values = its first 512 dims):
+//   S = Q . C^T / sqrt(W),  P = exp(S - m),  O = P . C[:, :512]
+// -- partial_head_attention (attention.hpp:65-78) for every head of the rank
+// with each head's LSE (HeadFragment), so the fragments merge exactly as
+// merge_head_fragments (:118-137). ~242 FLOP per KV byte: at the B200 ridge.
 //
-// At ~242 FLOP per KV byte MLA sits at the B200 ridge, so both GEMMs run on
-// tcgen05 (UMMA M = 128 heads, fp32 accumulators in TMEM). The fp32 output
-// [128 x 512] alone would fill all 512 TMEM columns, so a work item owns one
-// VALUE HALF (256 dims): the two items of a (split, stream) pair each compute
-// S for the whole tile and accumulate their half of O (the QK^T product is
-// issued twice; the KV bytes come from HBM once and from L2 twice).
+// Transposed, paired formulation (exact FLOPs, each latent byte staged once
+// per pair):
+//   S^T = C . Q^T   UMMA M = 256 tokens (128 per CTA: each CTA stages ONLY its
+//                   own 128-row page), N = 128 heads (the B operand is split by
+//                   N: each CTA holds HALF the query image, 73.7 KB), K = 576
+//   softmax per head = per COLUMN of S^T: warp redux.max over token lanes,
+//                   4 warps through shared memory, the pair through DSMEM
+//   O^T += V^T . P^T  M = 256 value dims (128 per CTA, two blocks cover 512),
+//                   N = 128 heads (each CTA holds P^T for its 64 heads; every
+//                   thread writes its token's P to both CTAs), K = 256 tokens
+// The fp32 O^T [512 dims x 128 heads] is split across the pair's TMEM (256
+// columns each); per-head row sums are kept per thread and reduced at the end.
 //
-// TMEM (512 columns x 128 lanes fp32):
-//   S/P buffer 0 [0, 128)   S/P buffer 1 [128, 256)   O half [256, 512)
-// Tiles are 128-row pages; S of tile t+1 is computed while the softmax of
-// tile t runs, and P.V(t) follows. Shared memory: the Q image (147,456 B,
-// K-major A operand, once per item) + a 5 x 16 KB ring of latent chunks
-// (64 dims x 128 rows, contiguous in the page layout).
-// Roles (192 threads):
-//   warps 0-3  softmax: thread = head row = TMEM lane. Row max, lazy rescale
-//              of O (only when the max grows by > 2^8, FA4-style; decided per
-//              warp), P = exp2 in bf16 written into TMEM over S (the A operand
-//              of P.V), row sum of the bf16-rounded P, final O / z and LSE.
-//   warp 4     producer: cp.async.bulk of the Q image and latent chunks in
-//              the MMA's consumption order.
-//   warp 5     TMEM allocation + MMA issue (one thread):
-//                S(t)  = 36 x UMMA SS  M128 N128 K16 (Q smem, latent K-major)
-//                O    += 32 x UMMA TS  M128 N64  K16 (P in TMEM, latent MN-major)
-// Items (split, stream, value half) are statically strided over the grid.
+// TMEM (per CTA, 512 columns x 128 lanes):
+//   S^T buffer 0 [0,128)   S^T buffer 1 [128,256)   O^T block 0 [256,384)   block 1 [384,512)
+// Shared memory (per CTA, same offsets in both): Q^T half 73,728 B | S ring
+// 3 x 16 KB (64 dims x 128 own rows) | V ring 2 x 32 KB (128 dims x 128 rows)
+// | P^T 32 KB [tokens 256 x this CTA's 64 heads] | exchange arrays + barriers.
+// Roles (192 threads per CTA):
+//   warps 0-3  softmax / correction (thread = token lane of S^T, = dim lane of O^T)
+//   warp 4     S producer: cp.async.bulk of the Q^T half and the S chunks
+//   warp 6     V producer: cp.async.bulk of the V blocks (own ring, runs ahead)
+//   warp 5     TMEM alloc (pair); leader CTA: MMA issue (one thread), in the
+//              order S(0) S(1) V(0) S(2) V(1) ...; peer CTA: forwards its
+//              "stage landed" events to the leader (relaxed cluster arrives).
+// Per-tile pair exchanges avoid cluster-scope fences: the column maxima and
+// the peer's half of P^T travel as st.async (completing tx on the peer's
+// mbarrier); only the per-item head sums use release/acquire.
 #include "common.cuh"
 #include "kernels.h"
 #include "kv_layout.cuh"
@@ -39,26 +44,39 @@
 namespace hx {
 
 namespace {
-constexpr uint32_t kQBytes = kMlaW * kMlaHeads * 2;  // 147456
-constexpr uint32_t kChunk = 64 * kMlaPageRows * 2;   // 16384: 64 latent dims x 128 rows
+constexpr uint32_t kQHalf = kMlaW * 64 * 2;          // 73728: query image half
+constexpr uint32_t kSChunk = 64 * kMlaPageRows * 2;  // 16384: 64 dims x 128 rows
+constexpr uint32_t kVBlock = 128 * kMlaPageRows * 2; // 32768: 128 dims x 128 rows
+constexpr uint32_t kPT = 256 * 64 * 2;               // 32768: P^T, 256 tokens x 64 heads
 constexpr int kSChunks = kMlaW / 64;                 // 9
-constexpr int kVChunks = kMlaDV / 2 / 64;            // 4 per value half
-constexpr int kSlots = 5;
-constexpr uint32_t kDgStride = kMlaPageRows / 8 * 128;  // bytes between 8-dim groups of a chunk
-constexpr uint32_t kIdescS = umma_idesc_bf16(128, kMlaPageRows, false, false);
-constexpr uint32_t kIdescPV = umma_idesc_bf16(128, 64, false, true);
-constexpr int kThreads = 192;
+constexpr int kSSlots = 3, kVSlots = 2;
+constexpr uint32_t kIdescST = umma_idesc_bf16(256, 128, false, false);
+constexpr uint32_t kIdescOT = umma_idesc_bf16(256, 128, true, true);
+constexpr int kThreads = 224;
+
+// shared-memory carve-up
+constexpr uint32_t kOffQ = 0;
+constexpr uint32_t kOffS = kOffQ + kQHalf;
+constexpr uint32_t kOffV = kOffS + kSSlots * kSChunk;
+constexpr uint32_t kOffPT = kOffV + kVSlots * kVBlock;
+constexpr uint32_t kOffRed = kOffPT + kPT;         // float [4][128] (max / sum per warp)
+constexpr uint32_t kOffMin = kOffRed + 4 * 128 * 4; // float [2][128] peer maxima
+constexpr uint32_t kOffMuse = kOffMin + 2 * 128 * 4;
+constexpr uint32_t kOffAlpha = kOffMuse + 128 * 4;
+constexpr uint32_t kOffZin = kOffAlpha + 128 * 4;   // float [2][128] peer sums
+constexpr uint32_t kOffZs = kOffZin + 2 * 128 * 4;
+constexpr uint32_t kOffBar = kOffZs + 128 * 4;
+constexpr int kNumBars = 32;
+constexpr uint32_t kSmem = kOffBar + kNumBars * 8 + 16;
 
 struct MlaItem {
-  int b, sl, half, pg0, pg1, ntok;
+  int b, sl, pg0, pg1, ntok;
 };
 
 __device__ __forceinline__ MlaItem decode_item(const AttnParams& p, int item) {
   MlaItem it;
-  it.half = item & 1;
-  const int ps = item >> 1;  // split * n_streams + stream
-  const int split = ps / p.n_streams;
-  const int stream = ps - split * p.n_streams;
+  const int split = item / p.n_streams;
+  const int stream = item - split * p.n_streams;
   const int bl = stream % p.stream_batch;
   it.sl = stream / p.stream_batch;
   it.b = bl + p.b_begin;
@@ -70,24 +88,23 @@ __device__ __forceinline__ MlaItem decode_item(const AttnParams& p, int item) {
   return it;
 }
 
-// Consumption order of an item's chunks (producer and MMA agree on it):
-//   S(0), S(1), V(0), S(2), V(1), S(3), ..., V(n-1)
-// step k of an item with n tiles -> (tile, is_value)
+// Consumption order of an item's stages (producer, forwarder and MMA agree):
+//   S(0), S(1), V(0), S(2), V(1), ..., S(n-1), V(n-2), V(n-1)
 __device__ __forceinline__ void mla_step(int k, int n, int& tile, bool& value) {
-  if (k < 2 || n == 1) {
-    if (n == 1) {
-      tile = 0;
-      value = k == 1;
-    } else {
-      tile = k;
-      value = false;
-    }
+  if (n == 1) {
+    tile = 0;
+    value = k == 1;
     return;
   }
-  const int j = k - 2;  // V(j/2) then S(j/2 + 2)
+  if (k < 2) {
+    tile = k;
+    value = false;
+    return;
+  }
+  const int j = k - 2;
   tile = j / 2 + ((j & 1) ? 2 : 0);
   value = (j & 1) == 0;
-  if (tile >= n) {  // past the last S: only V remains
+  if (tile >= n) {
     tile = n - 1;
     value = true;
   }
@@ -95,134 +112,207 @@ __device__ __forceinline__ void mla_step(int k, int n, int& tile, bool& value) {
 }  // namespace
 
 __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParams p) {
-  extern __shared__ __align__(1024) uint8_t smem[];
-  uint8_t* qs = smem;
-  uint8_t* ring = smem + kQBytes;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + kSlots * kChunk);
-  uint64_t* full = bars;                // [kSlots]
-  uint64_t* empty = bars + kSlots;      // [kSlots]
-  uint64_t* q_full = bars + 2 * kSlots;
-  uint64_t* q_free = q_full + 1;
-  uint64_t* s_full = q_full + 2;   // [2] per S buffer
-  uint64_t* p_full = q_full + 4;   // [2]
-  uint64_t* pv_done = q_full + 6;  // [2]
-  uint64_t* o_free = q_full + 8;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 9);
+  extern __shared__ __align__(128) uint8_t smem[];
+  const uint32_t sbase = smem_u32(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
+  uint64_t* full_s = bars + 0;       // [3]
+  uint64_t* empty_s = bars + 3;      // [3]
+  uint64_t* pfull_s = bars + 6;      // [3] leader: peer's S stage landed
+  uint64_t* full_v = bars + 9;       // [2]
+  uint64_t* empty_v = bars + 11;     // [2]
+  uint64_t* pfull_v = bars + 13;     // [2]
+  uint64_t* q_full = bars + 15;
+  uint64_t* q_free = bars + 16;
+  uint64_t* pq_full = bars + 17;     // leader: peer's Q half landed
+  uint64_t* s_full = bars + 18;      // [2] per S^T buffer
+  uint64_t* pt_full = bars + 20;     // P^T of this CTA complete (local 128 + peer st.async bytes
+                                     // [+ leader: the peer's forward])
+  uint64_t* pv_done = bars + 21;
+  uint64_t* o_free = bars + 22;      // leader: both CTAs read O^T (256 arrivals)
+  uint64_t* mx_bar = bars + 23;      // [2] peer maxima arrived (128 arrivals)
+  uint64_t* zx_bar = bars + 25;      // [2] peer sums arrived (128 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
+  float* red = reinterpret_cast<float*>(smem + kOffRed);
+  float* m_in = reinterpret_cast<float*>(smem + kOffMin);
+  float* m_use = reinterpret_cast<float*>(smem + kOffMuse);
+  float* alpha_s = reinterpret_cast<float*>(smem + kOffAlpha);
+  float* z_in = reinterpret_cast<float*>(smem + kOffZin);
+  float* zs = reinterpret_cast<float*>(smem + kOffZs);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t cta = cluster_ctarank();
+  const uint32_t peer = cta ^ 1u;
+  const bool leader = cta == 0;
+  const int cluster_id = blockIdx.x >> 1, n_clusters = gridDim.x >> 1;
+
   if (threadIdx.x == 0) {
-    for (int s = 0; s < kSlots; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    for (int s = 0; s < kSSlots; ++s) {
+      mbar_init(&full_s[s], 1);
+      mbar_init(&empty_s[s], 1);
+      mbar_init(&pfull_s[s], 1);
+    }
+    for (int s = 0; s < kVSlots; ++s) {
+      mbar_init(&full_v[s], 1);
+      mbar_init(&empty_v[s], 1);
+      mbar_init(&pfull_v[s], 1);
     }
     mbar_init(q_full, 1);
     mbar_init(q_free, 1);
+    mbar_init(pq_full, 1);
+    mbar_init(&s_full[0], 1);
+    mbar_init(&s_full[1], 1);
+    mbar_init(pt_full, leader ? 129 : 128);
+    mbar_init(pv_done, 1);
+    mbar_init(o_free, 256);
     for (int i = 0; i < 2; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&p_full[i], 128);
-      mbar_init(&pv_done[i], 1);
+      mbar_init(&mx_bar[i], 1);  // + 512 tx bytes of peer maxima per phase
+      mbar_init(&zx_bar[i], 128);
     }
-    mbar_init(o_free, 128);
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc(tmem_slot, 512);
+  if (warp == 5) tmem_alloc_pair(tmem_slot, 512);
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
   griddep_launch_dependents();
 
-  if (warp == 4) {
-    // ------------------------------------------------------------ producer
+  if (warp == 4 || warp == 6) {
+    // ------------------------------------------------------------ producers (S: warp 4, V: warp 6)
     if (lane == 0) {
-      int it_slot = 0, qcount = 0;
+      const bool sprod = warp == 4;
+      int us = 0, uv = 0, qcount = 0;
       bool waited = false;
-      for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+      for (int item = cluster_id; item < p.n_items; item += n_clusters) {
         const MlaItem it = decode_item(p, item);
         if (it.pg1 <= it.pg0) continue;
-        if (!waited) {  // the query images come from the QKV kernel
+        if (!waited) {  // query images and the appended latent come from the QKV kernel
           griddep_wait();
           waited = true;
         }
-        if (qcount > 0) mbar_wait(q_free, (qcount - 1) & 1);
-        mbar_arrive_expect_tx(q_full, kQBytes);
-        bulk_g2s(qs, p.qimg + static_cast<size_t>(it.b) * kQBytes, kQBytes, q_full);
-        ++qcount;
         const uint8_t* kvb =
             p.kv + (static_cast<size_t>(it.sl) * p.batch + it.b) * p.page_cap * static_cast<size_t>(mla_page_bytes());
-        const int n = it.pg1 - it.pg0;
-        for (int k = 0; k < 2 * n; ++k) {
-          int tile;
-          bool value;
-          mla_step(k, n, tile, value);
-          const uint8_t* page = kvb + static_cast<size_t>(it.pg0 + tile) * mla_page_bytes();
-          const int nch = value ? kVChunks : kSChunks;
-          for (int j = 0; j < nch; ++j) {
-            const int blk = value ? 4 * it.half + j : j;  // 64-dim block of the page
-            const int s = it_slot % kSlots;
-            if (it_slot >= kSlots) mbar_wait(&empty[s], ((it_slot / kSlots) - 1) & 1);
-            mbar_arrive_expect_tx(&full[s], kChunk);
-            bulk_g2s(ring + s * kChunk, page + static_cast<size_t>(blk) * kChunk, kChunk, &full[s]);
-            ++it_slot;
+        const int n = (it.pg1 - it.pg0 + 1) / 2;
+        auto page_of = [&](int tile, int c) {
+          const int pg = it.pg0 + 2 * tile + c;
+          return kvb + static_cast<size_t>(pg < it.pg1 ? pg : it.pg0) * mla_page_bytes();  // ghost: masked
+        };
+        if (sprod) {
+          if (qcount > 0) mbar_wait(q_free, (qcount - 1) & 1);
+          mbar_arrive_expect_tx(q_full, kQHalf);
+          bulk_g2s(smem + kOffQ, p.qimg + static_cast<size_t>(it.b) * mla_q_bytes() + cta * kQHalf, kQHalf, q_full);
+          ++qcount;
+          for (int tile = 0; tile < n; ++tile) {
+            const uint8_t* page = page_of(tile, static_cast<int>(cta));
+            for (int j = 0; j < kSChunks; ++j, ++us) {
+              const int s = us % kSSlots;
+              if (us >= kSSlots) mbar_wait(&empty_s[s], ((us / kSSlots) - 1) & 1);
+              mbar_arrive_expect_tx(&full_s[s], kSChunk);
+              bulk_g2s(smem + kOffS + s * kSChunk, page + static_cast<size_t>(j) * kSChunk, kSChunk, &full_s[s]);
+            }
           }
+        } else {
+          for (int tile = 0; tile < n; ++tile)
+            for (int jb = 0; jb < 2; ++jb)
+              for (int pp = 0; pp < 2; ++pp, ++uv) {
+                const int s = uv % kVSlots;
+                if (uv >= kVSlots) mbar_wait(&empty_v[s], ((uv / kVSlots) - 1) & 1);
+                mbar_arrive_expect_tx(&full_v[s], kVBlock);
+                // this CTA's 128 value dims of block jb: [256 jb + 128 cta, +128), rows of CTA pp's page
+                bulk_g2s(smem + kOffV + s * kVBlock, page_of(tile, pp) + static_cast<size_t>(2 * jb + cta) * kVBlock,
+                         kVBlock, &full_v[s]);
+              }
         }
       }
       if (!waited) griddep_wait();
     }
   } else if (warp == 5) {
-    // ------------------------------------------------------------ MMA issuer
-    if (lane == 0) {
-      const uint32_t q_addr = smem_u32(qs), ring_addr = smem_u32(ring);
-      int it_slot = 0, qcount = 0, g0 = 0, items = 0;  // g0: global index of the item's first tile
-      for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+    if (lane == 0 && !leader) {
+      // ---------------------------------------------------------- peer: forward "stage landed"
+      const uint32_t l_pfull_s = mapa_shared(smem_u32(pfull_s), 0), l_pfull_v = mapa_shared(smem_u32(pfull_v), 0);
+      const uint32_t l_pq = mapa_shared(smem_u32(pq_full), 0);
+      int us = 0, uv = 0, qcount = 0;
+      for (int item = cluster_id; item < p.n_items; item += n_clusters) {
         const MlaItem it = decode_item(p, item);
         if (it.pg1 <= it.pg0) continue;
         mbar_wait(q_full, qcount & 1);
         ++qcount;
-        tc_fence_after();
-        const int n = it.pg1 - it.pg0;
+        mbar_arrive_cluster_relaxed(l_pq);
+        const int n = (it.pg1 - it.pg0 + 1) / 2;
         for (int k = 0; k < 2 * n; ++k) {
           int tile;
           bool value;
           mla_step(k, n, tile, value);
-          const int g = g0 + tile, buf = g & 1;
           if (!value) {
-            // S(tile) into buffer buf: the P.V that last read this buffer must be done
-            if (g >= 2) mbar_wait(&pv_done[buf], ((g >> 1) - 1) & 1);
-            tc_fence_after();
-            for (int j = 0; j < kSChunks; ++j) {
-              const int s = it_slot % kSlots;
-              mbar_wait(&full[s], (it_slot / kSlots) & 1);
+            for (int j = 0; j < kSChunks; ++j, ++us) {
+              const int s = us % kSSlots;
+              mbar_wait(&full_s[s], (us / kSSlots) & 1);
+              mbar_arrive_cluster_relaxed(l_pfull_s + s * 8);
+            }
+          } else {
+            for (int q = 0; q < 4; ++q, ++uv) {
+              const int s = uv % kVSlots;
+              mbar_wait(&full_v[s], (uv / kVSlots) & 1);
+              mbar_arrive_cluster_relaxed(l_pfull_v + s * 8);
+            }
+          }
+        }
+      }
+    } else if (lane == 0) {
+      // ---------------------------------------------------------- leader: MMA issue
+      int us = 0, uv = 0, qcount = 0, g0 = 0, items = 0;
+      for (int item = cluster_id; item < p.n_items; item += n_clusters) {
+        const MlaItem it = decode_item(p, item);
+        if (it.pg1 <= it.pg0) continue;
+        mbar_wait(q_full, qcount & 1);
+        mbar_wait(pq_full, qcount & 1);
+        ++qcount;
+        tc_fence_after();
+        const int n = (it.pg1 - it.pg0 + 1) / 2;
+        for (int k = 0; k < 2 * n; ++k) {
+          int tile;
+          bool value;
+          mla_step(k, n, tile, value);
+          const int g = g0 + tile;
+          if (!value) {
+            // S^T(g) -> buffer g&1 (its previous reader, softmax(g-2), completed pt_full(g-2),
+            // which this thread waited before issuing P.V(g-2))
+            const uint32_t d = tbase + 128u * (g & 1);
+            for (int j = 0; j < kSChunks; ++j, ++us) {
+              const int s = us % kSSlots;
+              mbar_wait(&full_s[s], (us / kSSlots) & 1);
+              mbar_wait(&pfull_s[s], (us / kSSlots) & 1);
               tc_fence_after();
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) {
-                const uint64_t a = umma_desc(q_addr + (4 * j + kk) * 4096, 2048, 128);
-                const uint64_t bd = umma_desc(ring_addr + s * kChunk + kk * 2 * kDgStride, kDgStride, 128);
-                umma_ss(tbase + buf * 128, a, bd, kIdescS, (j | kk) != 0);
+                const uint64_t a = umma_desc(sbase + kOffS + s * kSChunk + kk * 4096, 2048, 128);
+                const uint64_t bd = umma_desc(sbase + kOffQ + (4 * j + kk) * 2048, 1024, 128);
+                umma_ss_pair(d, a, bd, kIdescST, (j | kk) != 0);
               }
-              umma_commit(&empty[s]);
-              ++it_slot;
+              umma_commit_pair(&empty_s[s]);
             }
-            if (tile == n - 1) umma_commit(q_free);
-            umma_commit(&s_full[buf]);
+            if (tile == n - 1) umma_commit_pair(q_free);
+            umma_commit_pair(&s_full[g & 1]);
           } else {
-            mbar_wait(&p_full[buf], (g >> 1) & 1);
-            if (tile == 0 && items > 0) mbar_wait(o_free, (items - 1) & 1);  // previous O read out
+            mbar_wait(pt_full, g & 1);
+            if (tile == 0 && items > 0) mbar_wait_cluster(o_free, (items - 1) & 1);
+            fence_proxy_async();
             tc_fence_after();
-            for (int v = 0; v < kVChunks; ++v) {
-              const int s = it_slot % kSlots;
-              mbar_wait(&full[s], (it_slot / kSlots) & 1);
-              tc_fence_after();
+            for (int jb = 0; jb < 2; ++jb)
+              for (int pp = 0; pp < 2; ++pp, ++uv) {
+                const int s = uv % kVSlots;
+                mbar_wait(&full_v[s], (uv / kVSlots) & 1);
+                mbar_wait(&pfull_v[s], (uv / kVSlots) & 1);
+                tc_fence_after();
 #pragma unroll
-              for (int kk = 0; kk < kMlaPageRows / 16; ++kk) {
-                const uint64_t bd = umma_desc(ring_addr + s * kChunk + kk * 256, 128, kDgStride);
-                umma_ts(tbase + 256 + 64 * v, tbase + buf * 128 + 8 * kk, bd, kIdescPV,
-                        (tile > 0 || kk > 0) ? 1u : 0u);
+                for (int kk = 0; kk < kMlaPageRows / 16; ++kk) {
+                  const uint64_t a = umma_desc(sbase + kOffV + s * kVBlock + kk * 256, 128, 2048);
+                  const uint64_t bd = umma_desc(sbase + kOffPT + (8 * pp + kk) * 2048, 1024, 128);
+                  umma_ss_pair(tbase + 256 + 128 * jb, a, bd, kIdescOT, (tile > 0 || pp > 0 || kk > 0) ? 1u : 0u);
+                }
+                umma_commit_pair(&empty_v[s]);
               }
-              umma_commit(&empty[s]);
-              ++it_slot;
-            }
-            umma_commit(&pv_done[buf]);
+            umma_commit_pair(pv_done);
           }
         }
         g0 += n;
@@ -230,103 +320,177 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
       }
     }
   } else {
-    // ------------------------------------------------------------ softmax (warps 0-3)
-    const int h = threadIdx.x;  // head row == TMEM lane
+    // ------------------------------------------------------------ softmax / correction (warps 0-3)
+    const int t = threadIdx.x;  // token lane of S^T, dim lane of O^T, head index in exchanges
     const uint32_t lrow = tbase + (static_cast<uint32_t>(warp * 32) << 16);
-    int g = 0;
-    for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+    const uint32_t peer_min = mapa_shared(sbase + kOffMin, peer), peer_zin = mapa_shared(sbase + kOffZin, peer);
+    const uint32_t peer_mx = mapa_shared(smem_u32(mx_bar), peer), peer_zx = mapa_shared(smem_u32(zx_bar), peer);
+    const uint32_t peer_pt = mapa_shared(sbase + kOffPT, peer), peer_ptfull = mapa_shared(smem_u32(pt_full), peer);
+    const uint32_t l_ptfull = mapa_shared(smem_u32(pt_full), 0), l_ofree = mapa_shared(smem_u32(o_free), 0);
+    const uint32_t pt_local = sbase + kOffPT;
+    int g = 0, items = 0;
+    for (int item = cluster_id; item < p.n_items; item += n_clusters) {
       const MlaItem it = decode_item(p, item);
-      float* po = p.part_o + (static_cast<size_t>(item) * kMlaHeads + h) * 256;
-      float* pl = p.part_lse2 + static_cast<size_t>(item) * kMlaHeads + h;
-      if (it.pg1 <= it.pg0) {
-        if (h < p.q_heads) {
-          for (int i = 0; i < 256; i += 4) *reinterpret_cast<float4*>(po + i) = make_float4(0.f, 0.f, 0.f, 0.f);
-          *pl = -INFINITY;
+      if (it.pg1 <= it.pg0) {  // empty split: zero fragment rows, LSE -inf
+        for (int jb = 0; jb < 2; ++jb) {
+          const int dim = 256 * jb + 128 * static_cast<int>(cta) + t;
+          for (int h = 0; h < p.q_heads; ++h) p.part_o[(static_cast<size_t>(item) * kMlaHeads + h) * kMlaDV + dim] = 0.f;
         }
+        if (leader && t < p.q_heads) p.part_lse2[static_cast<size_t>(item) * kMlaHeads + t] = -INFINITY;
         continue;
       }
-      float m = -INFINITY, z = 0.f;
-      const int n = it.pg1 - it.pg0;
-      for (int t = 0; t < n; ++t, ++g) {
+      float z[128];
+#pragma unroll
+      for (int h = 0; h < 128; ++h) z[h] = 0.f;
+      float m_run = -INFINITY;  // reference max of head t (log2 units)
+      const int n = (it.pg1 - it.pg0 + 1) / 2;
+      for (int tile = 0; tile < n; ++tile, ++g) {
         const int buf = g & 1;
-        const uint32_t sb = lrow + buf * 128;
-        const int valid = min(kMlaPageRows, it.ntok - (it.pg0 + t) * kMlaPageRows);
+        const int pg = it.pg0 + 2 * tile + static_cast<int>(cta);
+        const int valid = pg < it.pg1 ? min(kMlaPageRows, it.ntok - pg * kMlaPageRows) : 0;
+        const bool mine = t < valid;
+        const uint32_t srow = lrow + 128u * buf;
+        if (t == 0) mbar_arrive_expect_tx(&mx_bar[buf], 128 * 4);  // the peer's maxima for this tile
         mbar_wait(&s_full[buf], (g >> 1) & 1);
         tc_fence_after();
-        float mt = -INFINITY;
+        // ---- column (per-head) maxima over this CTA's 128 tokens
 #pragma unroll 1
-        for (int c = 0; c < kMlaPageRows / 32; ++c) {
+        for (int j = 0; j < 4; ++j) {
           float v[32];
-          tmem_ld32(sb + 32 * c, v);
+          tmem_ld32(srow + 32 * j, v);
+          float keep = -INFINITY;
 #pragma unroll
-          for (int i = 0; i < 32; ++i)
-            if (32 * c + i < valid) mt = fmaxf(mt, v[i]);
+          for (int i = 0; i < 32; ++i) {
+            const float r = redux_max_f32(mine ? v[i] : -INFINITY);
+            if (lane == i) keep = r;
+          }
+          red[warp * 128 + 32 * j + lane] = keep;
         }
-        mt *= p.qscale;
-        // Lazy rescale: a row keeps its reference max unless the tile max exceeds
-        // it by 2^8. Decided per warp (tcgen05.ld/st are warp-collective); rows
-        // that did not grow rescale by exactly 1.
-        const bool grow = mt > m + 8.f;
-        if (__any_sync(0xffffffffu, grow)) {
-          const float m_new = grow ? mt : m;
-          const float alpha = grow ? exp2f(m - m_new) : 1.f;  // 0 on the first tile
-          if (t > 0) {
-            // O holds tiles < t: wait for P.V(t-1), then rescale it in TMEM
-            mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+        named_bar(1, 128);
+        float mc = fmaxf(fmaxf(red[t], red[128 + t]), fmaxf(red[256 + t], red[384 + t]));
+        mc *= p.qscale;
+        st_async_f32(peer_min + (buf * 128 + t) * 4, mc, peer_mx + buf * 8);
+        mbar_wait(&mx_bar[buf], (g >> 1) & 1);
+        const float mt = fmaxf(mc, m_in[buf * 128 + t]);
+        const bool grow = mt > m_run + 8.f;  // lazy: keep the reference max within 2^8
+        const float m_new = grow ? mt : m_run;
+        alpha_s[t] = grow ? exp2f(m_run - m_new) : 1.f;
+        m_use[t] = m_new;
+        m_run = m_new;
+        const bool any = bar_red_or(2, 128, grow);  // also publishes m_use / alpha_s
+        bool pv_waited = false;
+        if (any) {
+#pragma unroll
+          for (int h = 0; h < 128; ++h) z[h] *= alpha_s[h];
+          if (tile > 0) {  // O^T holds tiles < tile: wait for P.V(g-1), rescale its head columns
+            mbar_wait(pv_done, (g - 1) & 1);
             tc_fence_after();
+            pv_waited = true;
 #pragma unroll 1
             for (int c = 0; c < 8; ++c) {
               float v[32];
               tmem_ld32(lrow + 256 + 32 * c, v);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] *= alpha;
+              for (int i = 0; i < 32; ++i) v[i] *= alpha_s[(32 * c + i) & 127];
               tmem_st32(lrow + 256 + 32 * c, v);
             }
+            tmem_wait_st();
           }
-          z *= alpha;
-          m = m_new;
         }
-#pragma unroll 1
-        for (int c = 0; c < kMlaPageRows / 32; ++c) {
+        if (tile > 0 && !pv_waited) mbar_wait(pv_done, (g - 1) & 1);  // P^T buffers free
+        // ---- P for this token, all 128 heads: own heads -> local P^T, the peer's -> st.async
+        const int k = 128 * static_cast<int>(cta) + t;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
           float v[32];
-          tmem_ld32(sb + 32 * c, v);
-          uint32_t pk[16];
+          tmem_ld32(srow + 32 * j, v);
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float p0 = (32 * c + 2 * i < valid) ? exp2f(fmaf(v[2 * i], p.qscale, -m)) : 0.f;
-            const float p1 = (32 * c + 2 * i + 1 < valid) ? exp2f(fmaf(v[2 * i + 1], p.qscale, -m)) : 0.f;
-            const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);  // .x = low half = even token
-            z += __low2float(pb) + __high2float(pb);
-            pk[i] = *reinterpret_cast<const uint32_t*>(&pb);
+          for (int q = 0; q < 4; ++q) {
+            uint32_t w4[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int h0 = 32 * j + 8 * q + 2 * e;
+              const float p0 = mine ? exp2f(fmaf(v[8 * q + 2 * e], p.qscale, -m_use[h0])) : 0.f;
+              const float p1 = mine ? exp2f(fmaf(v[8 * q + 2 * e + 1], p.qscale, -m_use[h0 + 1])) : 0.f;
+              const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
+              z[h0] += __low2float(pb);
+              z[h0 + 1] += __high2float(pb);
+              w4[e] = *reinterpret_cast<const uint32_t*>(&pb);
+            }
+            const int h8 = 32 * j + 8 * q;
+            const uint32_t off = ((static_cast<uint32_t>(k >> 3) * 8 + ((h8 & 63) >> 3)) * 8 + (k & 7)) * 16;
+            const uint4 val = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+            if ((h8 >> 6) == static_cast<int>(cta))
+              sts128(pt_local + off, val);
+            else
+              st_async_v4(peer_pt + off, val, peer_ptfull);
           }
-          tmem_st16(sb + 16 * c, pk);  // P over the S columns already read
         }
-        tmem_wait_st();
+        fence_proxy_async();
         tc_fence_before();
-        mbar_arrive(&p_full[buf]);
+        if (t == 0)
+          mbar_arrive_expect_tx(pt_full, 128 * 64 * 2);  // + the peer's half of this CTA's P^T
+        else
+          mbar_arrive(pt_full);
+        if (!leader && t == 0) {  // forward "peer P^T complete" to the leader's MMA issuer
+          mbar_wait(pt_full, g & 1);
+          fence_proxy_async();
+          mbar_arrive_cluster_relaxed(l_ptfull);
+        }
       }
-      mbar_wait(&pv_done[(g - 1) & 1], ((g - 1) >> 1) & 1);
+      // ---- item done: head sums over the pair, then O^T / z
+      mbar_wait(pv_done, (g - 1) & 1);
       tc_fence_after();
-      const float inv = z > 0.f ? 1.f / z : 0.f;
-#pragma unroll 1
-      for (int c = 0; c < 8; ++c) {
-        float v[32];
-        tmem_ld32(lrow + 256 + 32 * c, v);
-        if (h < p.q_heads)
+      // transpose-reduce the 128 per-head partials across the warp: lane ends with heads [hb, hb+4)
+      int hb = 0;
 #pragma unroll
-          for (int i = 0; i < 32; i += 4)
-            *reinterpret_cast<float4*>(po + 32 * c + i) =
-                make_float4(v[i] * inv, v[i + 1] * inv, v[i + 2] * inv, v[i + 3] * inv);
+      for (int o = 16, cnt = 64; o >= 1; o >>= 1, cnt >>= 1) {
+        const bool up = (lane & o) != 0;
+#pragma unroll
+        for (int i = 0; i < cnt; ++i) {
+          const float send = up ? z[i] : z[i + cnt];
+          const float keep = up ? z[i + cnt] : z[i];
+          z[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+        }
+        if (up) hb += cnt;
       }
-      if (h < p.q_heads) *pl = z > 0.f ? m + log2f(z) : -INFINITY;
+      named_bar(1, 128);  // red[] free (last tile's maxima consumed)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) red[warp * 128 + hb + i] = z[i];
+      named_bar(1, 128);
+      const float zc = (red[t] + red[128 + t]) + (red[256 + t] + red[384 + t]);
+      const int zb = items & 1;
+      st_cluster_f32(peer_zin + (zb * 128 + t) * 4, zc);
+      mbar_arrive_cluster(peer_zx + zb * 8);
+      mbar_wait_cluster(&zx_bar[zb], (items >> 1) & 1);
+      const float ztot = leader ? zc + z_in[zb * 128 + t] : z_in[zb * 128 + t] + zc;  // CTA 0's sum first
+      zs[t] = ztot > 0.f ? 1.f / ztot : 0.f;
+      if (leader && t < p.q_heads)
+        p.part_lse2[static_cast<size_t>(item) * kMlaHeads + t] = ztot > 0.f ? m_run + log2f(ztot) : -INFINITY;
+      named_bar(1, 128);
+#pragma unroll 1
+      for (int jb = 0; jb < 2; ++jb) {
+        const int dim = 256 * jb + 128 * static_cast<int>(cta) + t;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          float v[32];
+          tmem_ld32(lrow + 256 + 128 * jb + 32 * c, v);
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int h = 32 * c + i;
+            if (h < p.q_heads) p.part_o[(static_cast<size_t>(item) * kMlaHeads + h) * kMlaDV + dim] = v[i] * zs[h];
+          }
+        }
+      }
       tc_fence_before();
-      mbar_arrive(o_free);
+      mbar_arrive_cluster(l_ofree);
+      ++items;
     }
   }
   tc_fence_before();
-  __syncthreads();
+  cluster_sync_all();
   tc_fence_after();
-  if (warp == 5) tmem_dealloc(tbase, 512);
+  if (warp == 5) tmem_dealloc_pair(tbase, 512);
 }
 
 // Merge a stream's split partials (split order, deterministic) into the
@@ -346,8 +510,7 @@ __global__ void mla_split_reduce_kernel(const AttnParams p, float* frag_o, float
   for (int s = 0; s < p.splits; ++s) {
     const int pg0 = static_cast<int>((static_cast<long long>(s) * pages) / p.splits);
     const int pg1 = static_cast<int>((static_cast<long long>(s + 1) * pages) / p.splits);
-    if (pg1 > pg0)
-      M = fmaxf(M, p.part_lse2[static_cast<size_t>(((s * p.n_streams + stream) * 2) * kMlaHeads) + h]);
+    if (pg1 > pg0) M = fmaxf(M, p.part_lse2[static_cast<size_t>(s * p.n_streams + stream) * kMlaHeads + h]);
   }
   float o[16] = {};
   float L = 0.f;
@@ -355,14 +518,11 @@ __global__ void mla_split_reduce_kernel(const AttnParams p, float* frag_o, float
     const int pg0 = static_cast<int>((static_cast<long long>(s) * pages) / p.splits);
     const int pg1 = static_cast<int>((static_cast<long long>(s + 1) * pages) / p.splits);
     if (pg1 <= pg0) continue;
-    const size_t i0 = static_cast<size_t>((s * p.n_streams + stream) * 2);
-    const float w = exp2f(p.part_lse2[i0 * kMlaHeads + h] - M);
+    const size_t item = static_cast<size_t>(s * p.n_streams + stream);
+    const float w = exp2f(p.part_lse2[item * kMlaHeads + h] - M);
     L += w;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int d = lane + 32 * i, half = d >> 8;
-      o[i] += w * p.part_o[((i0 + half) * kMlaHeads + h) * 256 + (d & 255)];
-    }
+    for (int i = 0; i < 16; ++i) o[i] += w * p.part_o[(item * kMlaHeads + h) * kMlaDV + lane + 32 * i];
   }
   const size_t fo = (static_cast<size_t>(sl) * p.batch + b) * p.q_per_slot + h;
 #pragma unroll
@@ -370,19 +530,32 @@ __global__ void mla_split_reduce_kernel(const AttnParams p, float* frag_o, float
   if (lane == 0) frag_lse[fo] = L > 0.f ? (M + log2f(L)) * 0.69314718055994530942f : -INFINITY;
 }
 
-size_t mla_smem_bytes() { return kQBytes + kSlots * kChunk + (2 * kSlots + 12) * 8; }
+size_t mla_smem_bytes() { return kSmem; }
 
 cudaError_t launch_mla_decode(const AttnParams& p, int grid, cudaStream_t stream) {
   if (p.q_heads > kMlaHeads || p.q_heads < 1) return cudaErrorInvalidValue;
   static bool configured = false;
-  const size_t smem = mla_smem_bytes();
   if (!configured) {
     cudaError_t e =
-        cudaFuncSetAttribute(mla_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        cudaFuncSetAttribute(mla_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  return launch_k(mla_decode_kernel, dim3(grid), dim3(kThreads), smem, stream, p);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>(2 * grid));  // grid = number of CTA pairs
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, mla_decode_kernel, p);
 }
 
 cudaError_t launch_mla_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse, cudaStream_t stream) {
