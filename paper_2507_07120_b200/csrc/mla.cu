@@ -26,11 +26,16 @@
 // Shared memory (per CTA, same offsets in both): Q^T half 73,728 B | S ring
 // 3 x 16 KB (64 dims x 128 own rows) | V ring 2 x 32 KB (128 dims x 128 rows)
 // | P^T 32 KB [tokens 256 x this CTA's 64 heads] | exchange arrays + barriers.
-// Roles (192 threads per CTA):
-//   warps 0-3  softmax / correction (thread = token lane of S^T, = dim lane of O^T)
-//   warp 4     S producer: cp.async.bulk of the Q^T half and the S chunks
-//   warp 6     V producer: cp.async.bulk of the V blocks (own ring, runs ahead)
-//   warp 5     TMEM alloc (pair); leader CTA: MMA issue (one thread), in the
+// Roles (352 threads per CTA):
+//   warps 0-7  softmax / correction: two warpgroups on the same TMEM lanes
+//              (thread = token lane of S^T, = dim lane of O^T), warpgroup k
+//              owns heads [64k, 64k+64) -- exactly the heads whose P^T lives
+//              in CTA k, so one warpgroup writes locally, the other remotely
+//   warps 8,11 S producers: cp.async.bulk of the Q^T half (warp 8) and the S
+//              chunks (even / odd chunks: a warp issues ~1 bulk copy per 300 ns,
+//              so two issuers double the per-SM ingest of 16 KB chunks)
+//   warp 10    V producer: cp.async.bulk of the V blocks (own ring, runs ahead)
+//   warp 9     TMEM alloc (pair); leader CTA: MMA issue (one thread), in the
 //              order S(0) S(1) V(0) S(2) V(1) ...; peer CTA: forwards its
 //              "stage landed" events to the leader (relaxed cluster arrives).
 // Per-tile pair exchanges avoid cluster-scope fences: the column maxima and
@@ -52,14 +57,14 @@ constexpr int kSChunks = kMlaW / 64;                 // 9
 constexpr int kSSlots = 3, kVSlots = 2;
 constexpr uint32_t kIdescST = umma_idesc_bf16(256, 128, false, false);
 constexpr uint32_t kIdescOT = umma_idesc_bf16(256, 128, true, true);
-constexpr int kThreads = 224;
+constexpr int kThreads = 384;  // 8 softmax warps + 2 S producers + MMA + V producer
 
 // shared-memory carve-up
 constexpr uint32_t kOffQ = 0;
 constexpr uint32_t kOffS = kOffQ + kQHalf;
 constexpr uint32_t kOffV = kOffS + kSSlots * kSChunk;
 constexpr uint32_t kOffPT = kOffV + kVSlots * kVBlock;
-constexpr uint32_t kOffRed = kOffPT + kPT;         // float [4][128] (max / sum per warp)
+constexpr uint32_t kOffRed = kOffPT + kPT;         // float [8 warps][64 heads] (max / sum)
 constexpr uint32_t kOffMin = kOffRed + 4 * 128 * 4; // float [2][128] peer maxima
 constexpr uint32_t kOffMuse = kOffMin + 2 * 128 * 4;
 constexpr uint32_t kOffAlpha = kOffMuse + 128 * 4;
@@ -128,7 +133,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
   uint64_t* pt_full = bars + 20;     // P^T of this CTA complete (local 128 + peer st.async bytes
                                      // [+ leader: the peer's forward])
   uint64_t* pv_done = bars + 21;
-  uint64_t* o_free = bars + 22;      // leader: both CTAs read O^T (256 arrivals)
+  uint64_t* o_free = bars + 22;      // leader: both CTAs read O^T (512 arrivals)
   uint64_t* mx_bar = bars + 23;      // [2] peer maxima arrived (128 arrivals)
   uint64_t* zx_bar = bars + 25;      // [2] peer sums arrived (128 arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
@@ -161,26 +166,27 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
     mbar_init(pq_full, 1);
     mbar_init(&s_full[0], 1);
     mbar_init(&s_full[1], 1);
-    mbar_init(pt_full, leader ? 129 : 128);
+    mbar_init(pt_full, leader ? 257 : 256);
     mbar_init(pv_done, 1);
-    mbar_init(o_free, 256);
+    mbar_init(o_free, 512);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&mx_bar[i], 1);  // + 512 tx bytes of peer maxima per phase
       mbar_init(&zx_bar[i], 128);
     }
     fence_mbar_init();
   }
-  if (warp == 5) tmem_alloc_pair(tmem_slot, 512);
+  if (warp == 9) tmem_alloc_pair(tmem_slot, 512);
   tc_fence_before();
   cluster_sync_all();  // barriers of both CTAs initialised, TMEM allocated
   tc_fence_after();
   const uint32_t tbase = *tmem_slot;
   griddep_launch_dependents();
 
-  if (warp == 4 || warp == 6) {
-    // ------------------------------------------------------------ producers (S: warp 4, V: warp 6)
+  if (warp == 8 || warp == 10 || warp == 11) {
+    // ------------------------------------------------------------ producers (S: warps 8, 11; V: warp 10)
     if (lane == 0) {
-      const bool sprod = warp == 4;
+      const bool sprod = warp != 10;
+      const int sparity = warp == 8 ? 0 : 1;  // S chunks issued by this warp: us % 2 == sparity
       int us = 0, uv = 0, qcount = 0;
       bool waited = false;
       for (int item = cluster_id; item < p.n_items; item += n_clusters) {
@@ -198,13 +204,16 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
           return kvb + static_cast<size_t>(pg < it.pg1 ? pg : it.pg0) * mla_page_bytes();  // ghost: masked
         };
         if (sprod) {
-          if (qcount > 0) mbar_wait(q_free, (qcount - 1) & 1);
-          mbar_arrive_expect_tx(q_full, kQHalf);
-          bulk_g2s(smem + kOffQ, p.qimg + static_cast<size_t>(it.b) * mla_q_bytes() + cta * kQHalf, kQHalf, q_full);
-          ++qcount;
+          if (sparity == 0) {
+            if (qcount > 0) mbar_wait(q_free, (qcount - 1) & 1);
+            mbar_arrive_expect_tx(q_full, kQHalf);
+            bulk_g2s(smem + kOffQ, p.qimg + static_cast<size_t>(it.b) * mla_q_bytes() + cta * kQHalf, kQHalf, q_full);
+            ++qcount;
+          }
           for (int tile = 0; tile < n; ++tile) {
             const uint8_t* page = page_of(tile, static_cast<int>(cta));
             for (int j = 0; j < kSChunks; ++j, ++us) {
+              if ((us & 1) != sparity) continue;
               const int s = us % kSSlots;
               if (us >= kSSlots) mbar_wait(&empty_s[s], ((us / kSSlots) - 1) & 1);
               mbar_arrive_expect_tx(&full_s[s], kSChunk);
@@ -226,40 +235,39 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
       }
       if (!waited) griddep_wait();
     }
-  } else if (warp == 5) {
-    if (lane == 0 && !leader) {
+  } else if (warp == 9) {
+    if (lane < 2 && !leader) {
       // ---------------------------------------------------------- peer: forward "stage landed"
+      // lane 0: S stages (and the Q half), lane 1: V stages -- independent, so
+      // the leader can drain both rings concurrently.
       const uint32_t l_pfull_s = mapa_shared(smem_u32(pfull_s), 0), l_pfull_v = mapa_shared(smem_u32(pfull_v), 0);
       const uint32_t l_pq = mapa_shared(smem_u32(pq_full), 0);
       int us = 0, uv = 0, qcount = 0;
       for (int item = cluster_id; item < p.n_items; item += n_clusters) {
         const MlaItem it = decode_item(p, item);
         if (it.pg1 <= it.pg0) continue;
-        mbar_wait(q_full, qcount & 1);
-        ++qcount;
-        mbar_arrive_cluster_relaxed(l_pq);
         const int n = (it.pg1 - it.pg0 + 1) / 2;
-        for (int k = 0; k < 2 * n; ++k) {
-          int tile;
-          bool value;
-          mla_step(k, n, tile, value);
-          if (!value) {
-            for (int j = 0; j < kSChunks; ++j, ++us) {
-              const int s = us % kSSlots;
-              mbar_wait(&full_s[s], (us / kSSlots) & 1);
-              mbar_arrive_cluster_relaxed(l_pfull_s + s * 8);
-            }
-          } else {
-            for (int q = 0; q < 4; ++q, ++uv) {
-              const int s = uv % kVSlots;
-              mbar_wait(&full_v[s], (uv / kVSlots) & 1);
-              mbar_arrive_cluster_relaxed(l_pfull_v + s * 8);
-            }
+        if (lane == 0) {
+          mbar_wait(q_full, qcount & 1);
+          ++qcount;
+          mbar_arrive_cluster_relaxed(l_pq);
+          for (int j = 0; j < kSChunks * n; ++j, ++us) {
+            const int s = us % kSSlots;
+            mbar_wait(&full_s[s], (us / kSSlots) & 1);
+            mbar_arrive_cluster_relaxed(l_pfull_s + s * 8);
+          }
+        } else {
+          for (int q = 0; q < 4 * n; ++q, ++uv) {
+            const int s = uv % kVSlots;
+            mbar_wait(&full_v[s], (uv / kVSlots) & 1);
+            mbar_arrive_cluster_relaxed(l_pfull_v + s * 8);
           }
         }
       }
-    } else if (lane == 0) {
+    } else if (lane == 0 && leader) {
       // ---------------------------------------------------------- leader: MMA issue
+      // order S(0) S(1) V(0) S(2) V(1) ... (a non-blocking scheduler interleaving
+      // the two streams measured slower: both rings are latency-bound anyway)
       int us = 0, uv = 0, qcount = 0, g0 = 0, items = 0;
       for (int item = cluster_id; item < p.n_items; item += n_clusters) {
         const MlaItem it = decode_item(p, item);
@@ -320,42 +328,48 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
       }
     }
   } else {
-    // ------------------------------------------------------------ softmax / correction (warps 0-3)
-    const int t = threadIdx.x;  // token lane of S^T, dim lane of O^T, head index in exchanges
-    const uint32_t lrow = tbase + (static_cast<uint32_t>(warp * 32) << 16);
+    // ------------------------------------------------------------ softmax / correction (warps 0-7)
+    const int wg = warp >> 2, wq = warp & 3;
+    const int t = wq * 32 + lane;  // token lane of S^T, dim lane of O^T
+    const int hbase = 64 * wg;     // this warpgroup's heads
+    const int wg_bar = 1 + 2 * wg; // named barrier of the warpgroup (ids 1, 3); 2 = both
+    const uint32_t lrow = tbase + (static_cast<uint32_t>(wq * 32) << 16);
     const uint32_t peer_min = mapa_shared(sbase + kOffMin, peer), peer_zin = mapa_shared(sbase + kOffZin, peer);
     const uint32_t peer_mx = mapa_shared(smem_u32(mx_bar), peer), peer_zx = mapa_shared(smem_u32(zx_bar), peer);
     const uint32_t peer_pt = mapa_shared(sbase + kOffPT, peer), peer_ptfull = mapa_shared(smem_u32(pt_full), peer);
     const uint32_t l_ptfull = mapa_shared(smem_u32(pt_full), 0), l_ofree = mapa_shared(smem_u32(o_free), 0);
     const uint32_t pt_local = sbase + kOffPT;
+    const bool pt_remote = wg != static_cast<int>(cta);  // P^T of these heads lives in the peer
+    const int h_own = hbase + t;                           // head owned for max/sum bookkeeping (t < 64)
     int g = 0, items = 0;
     for (int item = cluster_id; item < p.n_items; item += n_clusters) {
       const MlaItem it = decode_item(p, item);
       if (it.pg1 <= it.pg0) {  // empty split: zero fragment rows, LSE -inf
         for (int jb = 0; jb < 2; ++jb) {
           const int dim = 256 * jb + 128 * static_cast<int>(cta) + t;
-          for (int h = 0; h < p.q_heads; ++h) p.part_o[(static_cast<size_t>(item) * kMlaHeads + h) * kMlaDV + dim] = 0.f;
+          for (int h = hbase; h < hbase + 64 && h < p.q_heads; ++h)
+            p.part_o[(static_cast<size_t>(item) * kMlaHeads + h) * kMlaDV + dim] = 0.f;
         }
-        if (leader && t < p.q_heads) p.part_lse2[static_cast<size_t>(item) * kMlaHeads + t] = -INFINITY;
+        if (leader && t < 64 && h_own < p.q_heads) p.part_lse2[static_cast<size_t>(item) * kMlaHeads + h_own] = -INFINITY;
         continue;
       }
-      float z[128];
+      float z[64];
 #pragma unroll
-      for (int h = 0; h < 128; ++h) z[h] = 0.f;
-      float m_run = -INFINITY;  // reference max of head t (log2 units)
+      for (int h = 0; h < 64; ++h) z[h] = 0.f;
+      float m_run = -INFINITY;  // reference max of head h_own (log2 units), threads t < 64
       const int n = (it.pg1 - it.pg0 + 1) / 2;
       for (int tile = 0; tile < n; ++tile, ++g) {
         const int buf = g & 1;
         const int pg = it.pg0 + 2 * tile + static_cast<int>(cta);
         const int valid = pg < it.pg1 ? min(kMlaPageRows, it.ntok - pg * kMlaPageRows) : 0;
         const bool mine = t < valid;
-        const uint32_t srow = lrow + 128u * buf;
-        if (t == 0) mbar_arrive_expect_tx(&mx_bar[buf], 128 * 4);  // the peer's maxima for this tile
+        const uint32_t srow = lrow + 128u * buf + hbase;
+        if (threadIdx.x == 0) mbar_arrive_expect_tx(&mx_bar[buf], 128 * 4);  // the peer's maxima
         mbar_wait(&s_full[buf], (g >> 1) & 1);
         tc_fence_after();
-        // ---- column (per-head) maxima over this CTA's 128 tokens
+        // ---- column (per-head) maxima over this CTA's 128 tokens, this warpgroup's 64 heads
 #pragma unroll 1
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < 2; ++j) {
           float v[32];
           tmem_ld32(srow + 32 * j, v);
           float keep = -INFINITY;
@@ -364,75 +378,84 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
             const float r = redux_max_f32(mine ? v[i] : -INFINITY);
             if (lane == i) keep = r;
           }
-          red[warp * 128 + 32 * j + lane] = keep;
+          red[warp * 64 + 32 * j + lane] = keep;
         }
-        named_bar(1, 128);
-        float mc = fmaxf(fmaxf(red[t], red[128 + t]), fmaxf(red[256 + t], red[384 + t]));
-        mc *= p.qscale;
-        st_async_f32(peer_min + (buf * 128 + t) * 4, mc, peer_mx + buf * 8);
-        mbar_wait(&mx_bar[buf], (g >> 1) & 1);
-        const float mt = fmaxf(mc, m_in[buf * 128 + t]);
-        const bool grow = mt > m_run + 8.f;  // lazy: keep the reference max within 2^8
-        const float m_new = grow ? mt : m_run;
-        alpha_s[t] = grow ? exp2f(m_run - m_new) : 1.f;
-        m_use[t] = m_new;
-        m_run = m_new;
-        const bool any = bar_red_or(2, 128, grow);  // also publishes m_use / alpha_s
+        named_bar(wg_bar, 128);
+        bool grow = false;
+        if (t < 64) {
+          float mc = fmaxf(fmaxf(red[(4 * wg) * 64 + t], red[(4 * wg + 1) * 64 + t]),
+                           fmaxf(red[(4 * wg + 2) * 64 + t], red[(4 * wg + 3) * 64 + t]));
+          mc *= p.qscale;
+          st_async_f32(peer_min + (buf * 128 + h_own) * 4, mc, peer_mx + buf * 8);
+          mbar_wait(&mx_bar[buf], (g >> 1) & 1);
+          const float mt = fmaxf(mc, m_in[buf * 128 + h_own]);
+          grow = mt > m_run + 8.f;  // lazy: keep the reference max within 2^8
+          const float m_new = grow ? mt : m_run;
+          alpha_s[h_own] = grow ? exp2f(m_run - m_new) : 1.f;
+          m_use[h_own] = m_new;
+          m_run = m_new;
+        }
+        const bool any = bar_red_or(2, 256, grow);  // also publishes m_use / alpha_s
         bool pv_waited = false;
         if (any) {
 #pragma unroll
-          for (int h = 0; h < 128; ++h) z[h] *= alpha_s[h];
-          if (tile > 0) {  // O^T holds tiles < tile: wait for P.V(g-1), rescale its head columns
+          for (int h = 0; h < 64; ++h) z[h] *= alpha_s[hbase + h];
+          if (tile > 0) {  // O^T holds tiles < tile: wait for P.V(g-1), rescale this warpgroup's head columns
             mbar_wait(pv_done, (g - 1) & 1);
             tc_fence_after();
             pv_waited = true;
 #pragma unroll 1
-            for (int c = 0; c < 8; ++c) {
+            for (int c = 0; c < 4; ++c) {
+              const uint32_t col = 256 + 128 * (c >> 1) + hbase + 32 * (c & 1);
               float v[32];
-              tmem_ld32(lrow + 256 + 32 * c, v);
+              tmem_ld32(lrow + col, v);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] *= alpha_s[(32 * c + i) & 127];
-              tmem_st32(lrow + 256 + 32 * c, v);
+              for (int i = 0; i < 32; ++i) v[i] *= alpha_s[hbase + 32 * (c & 1) + i];
+              tmem_st32(lrow + col, v);
             }
             tmem_wait_st();
           }
         }
         if (tile > 0 && !pv_waited) mbar_wait(pv_done, (g - 1) & 1);  // P^T buffers free
-        // ---- P for this token, all 128 heads: own heads -> local P^T, the peer's -> st.async
+        // ---- P for this token, this warpgroup's 64 heads -> P^T of CTA wg (local or st.async)
         const int k = 128 * static_cast<int>(cta) + t;
+        const uint32_t rowoff = (static_cast<uint32_t>(k >> 3) * 64 + (k & 7)) * 16;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < 2; ++j) {
           float v[32];
           tmem_ld32(srow + 32 * j, v);
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
+            const float4 ma = *reinterpret_cast<const float4*>(m_use + hbase + 32 * j + 8 * q);
+            const float4 mb = *reinterpret_cast<const float4*>(m_use + hbase + 32 * j + 8 * q + 4);
+            const float mm[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
             uint32_t w4[4];
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
-              const int h0 = 32 * j + 8 * q + 2 * e;
-              const float p0 = mine ? exp2f(fmaf(v[8 * q + 2 * e], p.qscale, -m_use[h0])) : 0.f;
-              const float p1 = mine ? exp2f(fmaf(v[8 * q + 2 * e + 1], p.qscale, -m_use[h0 + 1])) : 0.f;
+              const int hl = 32 * j + 8 * q + 2 * e;  // head index within the warpgroup
+              const float p0 = mine ? ex2_approx(fmaf(v[8 * q + 2 * e], p.qscale, -mm[2 * e])) : 0.f;
+              const float p1 = mine ? ex2_approx(fmaf(v[8 * q + 2 * e + 1], p.qscale, -mm[2 * e + 1])) : 0.f;
               const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
-              z[h0] += __low2float(pb);
-              z[h0 + 1] += __high2float(pb);
+              z[hl] += __low2float(pb);
+              z[hl + 1] += __high2float(pb);
               w4[e] = *reinterpret_cast<const uint32_t*>(&pb);
             }
-            const int h8 = 32 * j + 8 * q;
-            const uint32_t off = ((static_cast<uint32_t>(k >> 3) * 8 + ((h8 & 63) >> 3)) * 8 + (k & 7)) * 16;
+            // P^T core (token row k, heads 8-group (4j + q) of this CTA's 64)
+            const uint32_t off = rowoff + static_cast<uint32_t>(4 * j + q) * 128;
             const uint4 val = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-            if ((h8 >> 6) == static_cast<int>(cta))
-              sts128(pt_local + off, val);
-            else
+            if (pt_remote)
               st_async_v4(peer_pt + off, val, peer_ptfull);
+            else
+              sts128(pt_local + off, val);
           }
         }
         fence_proxy_async();
         tc_fence_before();
-        if (t == 0)
-          mbar_arrive_expect_tx(pt_full, 128 * 64 * 2);  // + the peer's half of this CTA's P^T
+        if (threadIdx.x == 0)
+          mbar_arrive_expect_tx(pt_full, 128 * 64 * 2);  // + the peer warpgroup's st.async into this P^T
         else
           mbar_arrive(pt_full);
-        if (!leader && t == 0) {  // forward "peer P^T complete" to the leader's MMA issuer
+        if (!leader && threadIdx.x == 0) {  // forward "peer P^T complete" to the leader's MMA issuer
           mbar_wait(pt_full, g & 1);
           fence_proxy_async();
           mbar_arrive_cluster_relaxed(l_ptfull);
@@ -441,10 +464,10 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
       // ---- item done: head sums over the pair, then O^T / z
       mbar_wait(pv_done, (g - 1) & 1);
       tc_fence_after();
-      // transpose-reduce the 128 per-head partials across the warp: lane ends with heads [hb, hb+4)
+      // transpose-reduce the 64 per-head partials across the warp: lane ends with heads [hb, hb+2)
       int hb = 0;
 #pragma unroll
-      for (int o = 16, cnt = 64; o >= 1; o >>= 1, cnt >>= 1) {
+      for (int o = 16, cnt = 32; o >= 1; o >>= 1, cnt >>= 1) {
         const bool up = (lane & o) != 0;
 #pragma unroll
         for (int i = 0; i < cnt; ++i) {
@@ -454,32 +477,33 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
         }
         if (up) hb += cnt;
       }
-      named_bar(1, 128);  // red[] free (last tile's maxima consumed)
-#pragma unroll
-      for (int i = 0; i < 4; ++i) red[warp * 128 + hb + i] = z[i];
-      named_bar(1, 128);
-      const float zc = (red[t] + red[128 + t]) + (red[256 + t] + red[384 + t]);
+      named_bar(wg_bar, 128);  // red[] free (last tile's maxima consumed)
+      red[warp * 64 + hb] = z[0];
+      red[warp * 64 + hb + 1] = z[1];
+      named_bar(wg_bar, 128);
       const int zb = items & 1;
-      st_cluster_f32(peer_zin + (zb * 128 + t) * 4, zc);
-      mbar_arrive_cluster(peer_zx + zb * 8);
-      mbar_wait_cluster(&zx_bar[zb], (items >> 1) & 1);
-      const float ztot = leader ? zc + z_in[zb * 128 + t] : z_in[zb * 128 + t] + zc;  // CTA 0's sum first
-      zs[t] = ztot > 0.f ? 1.f / ztot : 0.f;
-      if (leader && t < p.q_heads)
-        p.part_lse2[static_cast<size_t>(item) * kMlaHeads + t] = ztot > 0.f ? m_run + log2f(ztot) : -INFINITY;
-      named_bar(1, 128);
+      float zc = 0.f;
+      if (t < 64) {
+        zc = (red[(4 * wg) * 64 + t] + red[(4 * wg + 1) * 64 + t]) + (red[(4 * wg + 2) * 64 + t] + red[(4 * wg + 3) * 64 + t]);
+        st_cluster_f32(peer_zin + (zb * 128 + h_own) * 4, zc);
+        mbar_arrive_cluster(peer_zx + zb * 8);
+        mbar_wait_cluster(&zx_bar[zb], (items >> 1) & 1);
+        const float ztot = leader ? zc + z_in[zb * 128 + h_own] : z_in[zb * 128 + h_own] + zc;  // CTA 0's sum first
+        zs[h_own] = ztot > 0.f ? 1.f / ztot : 0.f;
+        if (leader && h_own < p.q_heads)
+          p.part_lse2[static_cast<size_t>(item) * kMlaHeads + h_own] = ztot > 0.f ? m_run + log2f(ztot) : -INFINITY;
+      }
+      named_bar(2, 256);
 #pragma unroll 1
-      for (int jb = 0; jb < 2; ++jb) {
+      for (int c = 0; c < 4; ++c) {
+        const int jb = c >> 1, hc = hbase + 32 * (c & 1);
         const int dim = 256 * jb + 128 * static_cast<int>(cta) + t;
-#pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
-          float v[32];
-          tmem_ld32(lrow + 256 + 128 * jb + 32 * c, v);
+        float v[32];
+        tmem_ld32(lrow + 256 + 128 * jb + hc, v);
 #pragma unroll
-          for (int i = 0; i < 32; ++i) {
-            const int h = 32 * c + i;
-            if (h < p.q_heads) p.part_o[(static_cast<size_t>(item) * kMlaHeads + h) * kMlaDV + dim] = v[i] * zs[h];
-          }
+        for (int i = 0; i < 32; ++i) {
+          const int h = hc + i;
+          if (h < p.q_heads) p.part_o[(static_cast<size_t>(item) * kMlaHeads + h) * kMlaDV + dim] = v[i] * zs[h];
         }
       }
       tc_fence_before();
@@ -490,7 +514,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
   tc_fence_before();
   cluster_sync_all();
   tc_fence_after();
-  if (warp == 5) tmem_dealloc_pair(tbase, 512);
+  if (warp == 9) tmem_dealloc_pair(tbase, 512);
 }
 
 // Merge a stream's split partials (split order, deterministic) into the
