@@ -564,7 +564,7 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
     q.total = d_total_ + l * B_;
     q.xf = d_xf_resid_;  // harness: the host x prepared into the same buffer
     q.ss_part = d_ss_;
-    q.n_ss = l == 0 ? 1 : hblk;  // embedding writes one block; residual writers write hblk
+    q.n_ss = hblk;  // per-128-column-block partials from the embedding / residual writers
     if (!attn_only_) {
       GemvParams& o = plan_o_[l].p;
       o.ypart = d_ypart_;

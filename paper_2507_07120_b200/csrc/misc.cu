@@ -66,55 +66,34 @@ cudaError_t launch_merge_out(const float* frag_o, const float* frag_lse, int bat
 }
 
 // ---------------------------------------------------------------- embedding
-// x[b][:] = E[token_b][:] (bf16 -> fp32); ss_part[0][b] = sum x^2.
+// x[b][:] = E[token_b][:] (bf16 -> fp32) with its x-fragments; one CTA per
+// (128-column block, request), ss_part[blk][b] = sum of x^2 over the block --
+// the same RMSNorm partials the residual epilogues write.
 __global__ void embed_kernel(const __nv_bfloat16* emb, const int* tokens, int batch, int hidden,
                              float* x, float* ss_part, uint8_t* xf) {
   griddep_wait();
   griddep_launch_dependents();
-  const int b = blockIdx.x;
-  const int tok = tokens[b];
-  float s = 0.f;
-  // 8 bf16 per 16-byte load; every load issued before use
-  const uint4* src = reinterpret_cast<const uint4*>(emb + static_cast<size_t>(tok) * hidden);
-  const int nvec = hidden / 8;
-  for (int i0 = threadIdx.x; i0 < nvec; i0 += blockDim.x * 4) {
-    uint4 u[4];
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int i = i0 + j * blockDim.x;
-      u[j] = i < nvec ? src[i] : make_uint4(0, 0, 0, 0);
-    }
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const int i = i0 + j * blockDim.x;
-      if (i >= nvec) continue;
-      const __nv_bfloat16* h = reinterpret_cast<const __nv_bfloat16*>(&u[j]);
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float v = __bfloat162float(h[e]);
-        x[static_cast<size_t>(b) * hidden + i * 8 + e] = v;
-        xf_write(xf, xf_nb8(batch), b, i * 8 + e, v);
-        s += v * v;
-      }
-    }
+  const int nb = blockIdx.x, b = blockIdx.y;
+  const int col = nb * 128 + threadIdx.x;
+  float v = 0.f;
+  if (col < hidden) {
+    v = __bfloat162float(emb[static_cast<size_t>(tokens[b]) * hidden + col]);
+    x[static_cast<size_t>(b) * hidden + col] = v;
+    xf_write(xf, xf_nb8(batch), b, col, v);
   }
-  __shared__ float red[32];
+  float s = v * v;
+  __shared__ float red[4];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    s = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    if (threadIdx.x == 0) ss_part[b] = s;
-  }
+  if (threadIdx.x == 0) ss_part[static_cast<size_t>(nb) * batch + b] = (red[0] + red[1]) + (red[2] + red[3]);
 }
 
 cudaError_t launch_embed(const uint16_t* emb, const int* tokens, int batch, int hidden, float* x,
                          float* ss_part, uint8_t* xf, cudaStream_t stream) {
-  return launch_k(embed_kernel, dim3(batch), dim3(256), 0, stream, reinterpret_cast<const __nv_bfloat16*>(emb),
-                  tokens, batch, hidden, x, ss_part, xf);
+  return launch_k(embed_kernel, dim3((hidden + 127) / 128, batch), dim3(128), 0, stream,
+                  reinterpret_cast<const __nv_bfloat16*>(emb), tokens, batch, hidden, x, ss_part, xf);
 }
 
 __global__ void argmax_finish_kernel(const unsigned long long* best, int batch, int* tokens_out,
