@@ -22,6 +22,8 @@
 // The KV stream is the roofline: 64*DP bytes per page, no re-reads.
 #include "common.cuh"
 #include "kv_layout.cuh"
+#include "xfrag.cuh"
+#include "merge.cuh"
 #include "kernels.h"
 
 namespace hx {

@@ -1031,6 +1031,7 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
     enqueue_attention(l);
     if (!dist) {
       // LSE-rescale combine of the KVP fragments -> O-proj activations (attention.hpp:118-175)
+      // (a fused split+KVP merge kernel measured 0.2 ms/step slower than this pair)
       cuda_check(launch_xprep_merge_local(d_frag_o_, d_frag_lse_, B_, q_per_slot_, kvp_, AD_, ADP_,
                                           static_cast<int>(Qh_) * AD_, d_xf_attn_, d_total_ + l * B_, stream_),
                  "merge");
