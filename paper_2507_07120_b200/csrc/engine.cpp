@@ -267,6 +267,11 @@ void Engine::validate_reference_dims() const {
 void Engine::alloc() {
   const size_t pool = static_cast<size_t>(n_slots_) * B_ * kvh_per_slot_ * page_cap_ * page_bytes_;
   for (int64_t l = 0; l < L_; ++l) kv_.push_back(dalloc<uint8_t>(pool, "kv pool"));
+  if (mla_) {  // 2-SM TMA views of each layer's latent pool (mla.cu)
+    mla_tm_.resize(static_cast<size_t>(L_));
+    for (int64_t l = 0; l < L_; ++l)
+      cuda_check(make_mla_tensor_maps(kv_[l], pool, mla_tm_[l].s, mla_tm_[l].v), "mla tensor maps");
+  }
   d_total_ = dalloc<int>(static_cast<size_t>(L_) * B_, "totals");
   h_total_.assign(static_cast<size_t>(L_ * B_), 0);
   const int qh_buf = dist_mode_ == HX_POOL_LOCAL ? static_cast<int>(Qh_) : q_per_slot_;
@@ -880,7 +885,8 @@ void Engine::record_transcript(int64_t layers) {
     }
 }
 
-AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) const {
+AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) {
+  attn_layer_ = layer;
   AttnParams a{};
   a.kv = kv_[layer];
   a.q = d_q_;
@@ -921,7 +927,9 @@ AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) const {
 // by the merge kernel, after which the appended token counts.
 void Engine::launch_attention_kernels(const AttnParams& a) {
   if (mla_) {
-    cuda_check(launch_mla_decode(a, std::min(attn_grid_, a.n_items), stream_), "mla attention");
+    cuda_check(launch_mla_decode(a, std::min(attn_grid_, a.n_items), stream_, mla_tm_[attn_layer_].s,
+                                 mla_tm_[attn_layer_].v),
+               "mla attention");
     mark(2);
     cuda_check(launch_mla_split_reduce(a, d_frag_o_, d_frag_lse_, stream_), "mla split reduce");
   } else {

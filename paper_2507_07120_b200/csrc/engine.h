@@ -176,7 +176,7 @@ class Engine {
   std::vector<cudaEvent_t> hop_events_;
   void enqueue_exchange_and_attention_dist(int64_t layer);
   void init_dist_weights(uint64_t seed, bool qkv_hash);
-  AttnParams attn_params(int64_t layer, int b_begin, int b_count) const;
+  AttnParams attn_params(int64_t layer, int b_begin, int b_count);
   void launch_attention_kernels(const AttnParams& a);
 
   // ---- MoE FFN (router -> top-k -> grouped expert GEMVs over the active list)
@@ -185,6 +185,11 @@ class Engine {
   int W_ = 0, DV_ = 0;           // latent width (576) and value width (512)
   int AD_ = 0, ADP_ = 0;         // attention output width per head and its padded stride
   uint8_t* d_qimg_ = nullptr;    // [B] bf16 absorbed-query images
+  struct alignas(64) MlaTmaps {  // CUtensorMap x 2 per layer over the latent pool
+    unsigned char s[128], v[128];
+  };
+  std::vector<MlaTmaps> mla_tm_;
+  int64_t attn_layer_ = 0;       // layer whose attention is being enqueued
   bool moe_ = false;
   int64_t E_ = 0, topk_ = 0, Fe_ = 0;
   int ep_ = 1, tpf_ = 1, ep_rank_ = 0, tpf_rank_ = 0, E_local_ = 0, e_begin_ = 0, Fe_local_ = 0;

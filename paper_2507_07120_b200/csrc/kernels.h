@@ -58,7 +58,11 @@ struct AttnParams {
 cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t stream);
 // MLA (tcgen05): items = (split, stream, value half); part_o [n_items][128][256],
 // part_lse2 [n_items][128]; the split reduce writes frag_o [slot][b][q][512].
-cudaError_t launch_mla_decode(const AttnParams& p, int grid, cudaStream_t stream);
+// tm_s / tm_v: CUtensorMap (128 B each) over the layer's latent pool viewed as
+// [rows of 2 KB] x [256 x u64], boxes of 8 rows (16 KB chunk) / 16 rows (32 KB block).
+cudaError_t launch_mla_decode(const AttnParams& p, int grid, cudaStream_t stream, const void* tm_s, const void* tm_v);
+// Encode the two tensor maps for a latent pool of `bytes` bytes (multiple of 2 KB).
+cudaError_t make_mla_tensor_maps(const void* pool, size_t bytes, void* tm_s, void* tm_v);
 cudaError_t launch_mla_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse, cudaStream_t stream);
 cudaError_t launch_kv_fill_hash_mla(uint8_t* kv, int* total, int batch, int kvp, int chunk, int page_cap,
                                     int slot_base, int n_local_slots, long long n, uint64_t seed, uint64_t stream_k,

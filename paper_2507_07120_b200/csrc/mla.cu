@@ -36,8 +36,10 @@
 //              so two issuers double the per-SM ingest of 16 KB chunks)
 //   warp 10    V producer: cp.async.bulk of the V blocks (own ring, runs ahead)
 //   warp 9     TMEM alloc (pair); leader CTA: MMA issue (one thread), in the
-//              order S(0) S(1) V(0) S(2) V(1) ...; peer CTA: forwards its
-//              "stage landed" events to the leader (relaxed cluster arrives).
+//              order S(0) S(1) V(0) S(2) V(1) ...; peer CTA: forwards "Q half
+//              landed" to the leader. Latent chunks are loaded with 2-SM tensor
+//              TMA (UTMALDG.2CTA) by both CTAs and complete on the LEADER's
+//              barriers, so no per-chunk relay is needed.
 // Per-tile pair exchanges avoid cluster-scope fences: the column maxima and
 // the peer's half of P^T travel as st.async (completing tx on the peer's
 // mbarrier); only the per-item head sums use release/acquire.
@@ -116,25 +118,24 @@ __device__ __forceinline__ void mla_step(int k, int n, int& tile, bool& value) {
 }
 }  // namespace
 
-__global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParams p) {
+__global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tm_s,
+                                                                   const __grid_constant__ CUtensorMap tm_v) {
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
   uint64_t* full_s = bars + 0;       // [3]
   uint64_t* empty_s = bars + 3;      // [3]
-  uint64_t* pfull_s = bars + 6;      // [3] leader: peer's S stage landed
   uint64_t* full_v = bars + 9;       // [2]
   uint64_t* empty_v = bars + 11;     // [2]
-  uint64_t* pfull_v = bars + 13;     // [2]
   uint64_t* q_full = bars + 15;
   uint64_t* q_free = bars + 16;
   uint64_t* pq_full = bars + 17;     // leader: peer's Q half landed
   uint64_t* s_full = bars + 18;      // [2] per S^T buffer
-  uint64_t* pt_full = bars + 20;     // P^T of this CTA complete (local 128 + peer st.async bytes
-                                     // [+ leader: the peer's forward])
+  uint64_t* pt_full = bars + 20;     // P^T of this CTA complete: 256 local arrivals + the peer's st.async bytes
+                                     // (+1: the peer's forward, leader only)
   uint64_t* pv_done = bars + 21;
   uint64_t* o_free = bars + 22;      // leader: both CTAs read O^T (512 arrivals)
-  uint64_t* mx_bar = bars + 23;      // [2] peer maxima arrived (128 arrivals)
+  uint64_t* mx_bar = bars + 23;      // [2] peer maxima arrived (1 arrival + 512 tx bytes)
   uint64_t* zx_bar = bars + 25;      // [2] peer sums arrived (128 arrivals)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + kNumBars);
   float* red = reinterpret_cast<float*>(smem + kOffRed);
@@ -154,12 +155,10 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
     for (int s = 0; s < kSSlots; ++s) {
       mbar_init(&full_s[s], 1);
       mbar_init(&empty_s[s], 1);
-      mbar_init(&pfull_s[s], 1);
     }
     for (int s = 0; s < kVSlots; ++s) {
       mbar_init(&full_v[s], 1);
       mbar_init(&empty_v[s], 1);
-      mbar_init(&pfull_v[s], 1);
     }
     mbar_init(q_full, 1);
     mbar_init(q_free, 1);
@@ -186,6 +185,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
     // ------------------------------------------------------------ producers (S: warps 8, 11; V: warp 10)
     if (lane == 0) {
       const bool sprod = warp != 10;
+      const uint32_t l_full_s = mapa_shared(smem_u32(full_s), 0), l_full_v = mapa_shared(smem_u32(full_v), 0);
       const int sparity = warp == 8 ? 0 : 1;  // S chunks issued by this warp: us % 2 == sparity
       int us = 0, uv = 0, qcount = 0;
       bool waited = false;
@@ -211,13 +211,14 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
             ++qcount;
           }
           for (int tile = 0; tile < n; ++tile) {
-            const uint8_t* page = page_of(tile, static_cast<int>(cta));
+            const int row0 = static_cast<int>((page_of(tile, static_cast<int>(cta)) - p.kv) >> 11);  // 2 KB rows
             for (int j = 0; j < kSChunks; ++j, ++us) {
               if ((us & 1) != sparity) continue;
               const int s = us % kSSlots;
               if (us >= kSSlots) mbar_wait(&empty_s[s], ((us / kSSlots) - 1) & 1);
-              mbar_arrive_expect_tx(&full_s[s], kSChunk);
-              bulk_g2s(smem + kOffS + s * kSChunk, page + static_cast<size_t>(j) * kSChunk, kSChunk, &full_s[s]);
+              // both CTAs' chunks complete on the LEADER's full barrier (2-SM TMA)
+              if (leader) mbar_arrive_expect_tx(&full_s[s], 2 * kSChunk);
+              tma_load_2d_pair(sbase + kOffS + s * kSChunk, &tm_s, 0, row0 + j * 8, l_full_s + s * 8);
             }
           }
         } else {
@@ -226,43 +227,27 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
               for (int pp = 0; pp < 2; ++pp, ++uv) {
                 const int s = uv % kVSlots;
                 if (uv >= kVSlots) mbar_wait(&empty_v[s], ((uv / kVSlots) - 1) & 1);
-                mbar_arrive_expect_tx(&full_v[s], kVBlock);
+                if (leader) mbar_arrive_expect_tx(&full_v[s], 2 * kVBlock);
                 // this CTA's 128 value dims of block jb: [256 jb + 128 cta, +128), rows of CTA pp's page
-                bulk_g2s(smem + kOffV + s * kVBlock, page_of(tile, pp) + static_cast<size_t>(2 * jb + cta) * kVBlock,
-                         kVBlock, &full_v[s]);
+                const int row0 = static_cast<int>((page_of(tile, pp) - p.kv) >> 11) + (2 * jb + static_cast<int>(cta)) * 16;
+                tma_load_2d_pair(sbase + kOffV + s * kVBlock, &tm_v, 0, row0, l_full_v + s * 8);
               }
         }
       }
       if (!waited) griddep_wait();
     }
   } else if (warp == 9) {
-    if (lane < 2 && !leader) {
-      // ---------------------------------------------------------- peer: forward "stage landed"
-      // lane 0: S stages (and the Q half), lane 1: V stages -- independent, so
-      // the leader can drain both rings concurrently.
-      const uint32_t l_pfull_s = mapa_shared(smem_u32(pfull_s), 0), l_pfull_v = mapa_shared(smem_u32(pfull_v), 0);
+    if (lane == 0 && !leader) {
+      // ---------------------------------------------------------- peer: forward "Q half landed"
+      // (latent chunks complete directly on the leader's barriers through 2-SM TMA)
       const uint32_t l_pq = mapa_shared(smem_u32(pq_full), 0);
-      int us = 0, uv = 0, qcount = 0;
+      int qcount = 0;
       for (int item = cluster_id; item < p.n_items; item += n_clusters) {
         const MlaItem it = decode_item(p, item);
         if (it.pg1 <= it.pg0) continue;
-        const int n = (it.pg1 - it.pg0 + 1) / 2;
-        if (lane == 0) {
-          mbar_wait(q_full, qcount & 1);
-          ++qcount;
-          mbar_arrive_cluster_relaxed(l_pq);
-          for (int j = 0; j < kSChunks * n; ++j, ++us) {
-            const int s = us % kSSlots;
-            mbar_wait(&full_s[s], (us / kSSlots) & 1);
-            mbar_arrive_cluster_relaxed(l_pfull_s + s * 8);
-          }
-        } else {
-          for (int q = 0; q < 4 * n; ++q, ++uv) {
-            const int s = uv % kVSlots;
-            mbar_wait(&full_v[s], (uv / kVSlots) & 1);
-            mbar_arrive_cluster_relaxed(l_pfull_v + s * 8);
-          }
-        }
+        mbar_wait(q_full, qcount & 1);
+        ++qcount;
+        mbar_arrive_cluster_relaxed(l_pq);
       }
     } else if (lane == 0 && leader) {
       // ---------------------------------------------------------- leader: MMA issue
@@ -288,8 +273,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
             const uint32_t d = tbase + 128u * (g & 1);
             for (int j = 0; j < kSChunks; ++j, ++us) {
               const int s = us % kSSlots;
-              mbar_wait(&full_s[s], (us / kSSlots) & 1);
-              mbar_wait(&pfull_s[s], (us / kSSlots) & 1);
+              mbar_wait(&full_s[s], (us / kSSlots) & 1);  // both CTAs' chunks (2-SM TMA)
               tc_fence_after();
 #pragma unroll
               for (int kk = 0; kk < 4; ++kk) {
@@ -309,8 +293,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
             for (int jb = 0; jb < 2; ++jb)
               for (int pp = 0; pp < 2; ++pp, ++uv) {
                 const int s = uv % kVSlots;
-                mbar_wait(&full_v[s], (uv / kVSlots) & 1);
-                mbar_wait(&pfull_v[s], (uv / kVSlots) & 1);
+                mbar_wait(&full_v[s], (uv / kVSlots) & 1);  // both CTAs' blocks (2-SM TMA)
                 tc_fence_after();
 #pragma unroll
                 for (int kk = 0; kk < kMlaPageRows / 16; ++kk) {
@@ -556,7 +539,7 @@ __global__ void mla_split_reduce_kernel(const AttnParams p, float* frag_o, float
 
 size_t mla_smem_bytes() { return kSmem; }
 
-cudaError_t launch_mla_decode(const AttnParams& p, int grid, cudaStream_t stream) {
+cudaError_t launch_mla_decode(const AttnParams& p, int grid, cudaStream_t stream, const void* tm_s, const void* tm_v) {
   if (p.q_heads > kMlaHeads || p.q_heads < 1) return cudaErrorInvalidValue;
   static bool configured = false;
   if (!configured) {
@@ -579,7 +562,35 @@ cudaError_t launch_mla_decode(const AttnParams& p, int grid, cudaStream_t stream
   attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, mla_decode_kernel, p);
+  return cudaLaunchKernelEx(&cfg, mla_decode_kernel, p, *static_cast<const CUtensorMap*>(tm_s),
+                            *static_cast<const CUtensorMap*>(tm_v));
+}
+
+cudaError_t make_mla_tensor_maps(const void* pool, size_t bytes, void* tm_s, void* tm_v) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn encode = nullptr;
+  if (!encode) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || !fn) return e != cudaSuccess ? e : cudaErrorNotSupported;
+    encode = reinterpret_cast<EncodeFn>(fn);
+  }
+  if (bytes % 2048) return cudaErrorInvalidValue;
+  const cuuint64_t dims[2] = {256, bytes / 2048};  // u64 elements per 2 KB row, rows
+  const cuuint64_t strides[1] = {2048};
+  const cuuint32_t estr[2] = {1, 1};
+  const cuuint32_t box_s[2] = {256, 8}, box_v[2] = {256, 16};
+  CUresult r = encode(static_cast<CUtensorMap*>(tm_s), CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(pool), dims,
+                      strides, box_s, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+  r = encode(static_cast<CUtensorMap*>(tm_v), CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(pool), dims, strides,
+             box_v, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
 cudaError_t launch_mla_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse, cudaStream_t stream) {

@@ -12,6 +12,8 @@
 //       SBO = byte stride between M/N-adjacent core matrices
 #pragma once
 
+#include <cuda.h>
+
 #include "common.cuh"
 
 namespace hx {
@@ -227,5 +229,17 @@ HX_DEV bool mbar_test(uint64_t* bar, uint32_t parity) {
       : "r"(smem_u32(bar)), "r"(parity)
       : "memory");
   return r != 0;
+}
+}  // namespace hx
+
+namespace hx {
+// 2-D tensor TMA load issued by either CTA of a pair; completes tx on `mbar`,
+// which may live in the peer (leader) CTA (the 2-SM load pattern).
+HX_DEV void tma_load_2d_pair(uint32_t smem_dst, const CUtensorMap* tm, int c0, int c1, uint32_t cluster_mbar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];" ::"r"(smem_dst),
+      "l"(tm), "r"(c0), "r"(c1), "r"(cluster_mbar)
+      : "memory");
 }
 }  // namespace hx
