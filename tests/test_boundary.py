@@ -44,13 +44,16 @@ def test_sass_uses_bulk_copy_and_hmma():
 
 
 def test_mla_kernel_uses_tcgen05():
-    """The MLA kernel issues 5th-gen tensor-core MMAs (UTCHMMA), moves TMEM
-    with tcgen05.ld/st (LDTM/STTM) and commits to mbarriers (UTCBAR)."""
+    """The MLA kernel issues paired 5th-gen tensor-core MMAs (UTCHMMA.2CTA),
+    moves TMEM with tcgen05.ld/st (LDTM/STTM), commits to mbarriers (UTCBAR)
+    and loads latent chunks with 2-SM tensor TMA (UTMALDG.2D.2CTA)."""
     so = os.path.join(ROOT, "paper_2507_07120_b200", "libhelix_b200.so")
-    sass = subprocess.run(["cuobjdump", "-sass", "-fun", "_ZN2hx17mla_decode_kernelENS_10AttnParamsE", so],
-                          capture_output=True, text=True).stdout
-    for op in ("UTCHMMA", "LDTM", "STTM", "UTCBAR", "UBLKCP"):
-        assert op in sass, op
+    sass = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
+    funcs = sass.split("Function : ")
+    mla = [f for f in funcs if f.startswith("_ZN2hx17mla_decode_kernel")]
+    assert len(mla) == 1
+    for op in ("UTCHMMA.2CTA", "LDTM", "STTM", "UTCBAR", "UTMALDG.2D.2CTA", "REDUX.MAX.F32"):
+        assert op in mla[0], op
 
 
 def test_ctypes_structs_match_c_header(tmp_path):
