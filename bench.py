@@ -177,7 +177,7 @@ def deepseek_slice(a):
             ["embed", "qkv", "attention", "split_reduce", "o_proj", "ffn_router_to_gate_up", "ffn_down_combine",
              "lm_head", "merge"], prof)},
         "mla_attention": {
-            "kernel": "mla_decode_kernel (tcgen05 SS + TS, TMEM accumulators)", "launch_ms": att_ms,
+            "kernel": "mla_decode_kernel (tcgen05 cta_group::2 CTA pair, TMEM accumulators, 2-SM TMA)", "launch_ms": att_ms,
             "algorithmic_kv_bytes": kv_bytes, "algorithmic_flops": flops,
             "roofline": {"bound": "tensor", "achieved": flops / (att_ms * 1e-3) / 1e12, "peak": tc, "unit": "TFLOP/s",
                          "frac": flops / (att_ms * 1e-3) / 1e12 / tc, "peak_kind": tc_kind,
