@@ -44,9 +44,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-context", type=int, default=131072)
     ap.add_argument("--profile-only", action="store_true", help="skip timing loops (for ncu)")
-    ap.add_argument("--no-deepseek", action="store_true", help="skip the deepseek-r1-like (MLA + MoE) slice")
-    ap.add_argument("--deepseek-context", type=int, default=125000,
-                    help="latent tokens per request on this GPU (1M context / KVP 8)")
+    ap.add_argument("--no-slices", action="store_true",
+                    help="skip the one-GPU-of-8 slices (C3 llama405b-like, C4 deepseek-r1-like)")
+    ap.add_argument("--slice-context", type=int, default=125000,
+                    help="KV tokens per request on this GPU for the slices (1M context / KVP 8)")
     return ap.parse_args()
 
 
@@ -122,31 +123,35 @@ def peak_tensor():
         return 1393.0, "fallback"
 
 
-def deepseek_slice(a):
-    """C4: deepseek-r1-like layer as ONE GPU of a KVP=8, EP=8 (tpf=1)
-    Helix pool: 128 heads over a B x 125,000-token latent shard (MLA, tcgen05),
-    32 of 256 experts (top-8) + 1/8 of the shared expert, 1/8 of W_O. Runs one
-    rank of an 8-rank loopback pool with the collectives switched off (a single
-    B200 here), so the number is this GPU's compute per layer; the reference's
-    NVLink terms are not included."""
+def pool_slice(a, preset, S, ep):
+    """One GPU of an N=8 Helix pool (TPA=1, KVP=8; FFN TPF=8, or EP=8 x TPF=1 for
+    MoE) measured alone: rank 0 of an 8-rank loopback pool with the collectives
+    switched off (a single B200 here), so the number is this GPU's compute per
+    layer over its B x S-token KV shard; the reference's NVLink terms
+    (latency.cpp:77-146) are not included. C3 = llama405b-like, C4 =
+    deepseek-r1-like."""
     import ctypes
     import numpy as np
     import torch
     import paper_2507_07120_b200 as P
     from paper_2507_07120_b200.model import Loopback
-    spec = P.model.PRESETS["deepseek-r1-like"]
-    B, S, N = a.batch, a.deepseek_context, 8
+    spec = P.model.PRESETS[preset]
+    B, N, V = a.batch, 8, 4096
+    mla = spec.attention == "mla"
     lb = Loopback(N)
-    eng = P.HelixDecoder(spec, tpa=1, kvp=N, batch=B, capacity=S * N + 64 * N, layers=1, vocab=4096,
-                         use_graphs=False, pool=2, rank=0, loopback=lb, ep=8)
+    eng = P.HelixDecoder(spec, tpa=1, kvp=N, batch=B, capacity=S * N + 64 * N, layers=1, vocab=V,
+                         use_graphs=False, pool=2, rank=0, loopback=lb, ep=ep)
     P._lib.check(P.lib().hx_engine_set_flag(eng._h, 1, 3), eng._h)  # HX_FLAG_SKIP_COMM: no a2a / all-reduce
     eng.init_weights(2507, qkv="hash")
     eng.fill_kv_hash(S * N, 2507)  # rank 0 keeps S of the S*N global tokens
     s_loc = int(P.lib().hx_effective_tokens(eng._h, 0, 0, 0))
-    tok = torch.randint(0, 4096, (B,), dtype=torch.int32, device="cuda")
+    g = torch.Generator().manual_seed(7)
+    host_tok = torch.randint(0, V, (B,), dtype=torch.int32, generator=g)
+    tok = host_tok.cuda()
     nxt = torch.zeros(B, dtype=torch.int32, device="cuda")
     for _ in range(a.warmup):
         eng.step_device(tok.data_ptr(), nxt.data_ptr())
+    eng.step(host_tok.numpy())  # the profile pass below replays these (distinct) request tokens
     eng.synchronize()
     prof = np.zeros(10)
     reps = max(3, a.steps)
@@ -163,31 +168,48 @@ def deepseek_slice(a):
     e1.synchronize()
     ms = e0.elapsed_time(e1) / a.steps
     info = eng.info()
-    active = int(P.lib().hx_moe_active_experts(eng._h))
     att_ms = prof[2]
-    kv_bytes = B * s_loc * 576 * 2
-    flops = B * s_loc * spec.query_heads * (576 + 512) * 2
+    H, Q, Hsz = spec.hidden_dim, spec.query_heads, spec.head_size
     hbm, _ = peaks()
-    tc, tc_kind = peak_tensor()
-    out = {
-        "workload": "deepseek-r1-like layer, one GPU of KVP=8 x EP=8 (tpf=1): 128 heads x %d latent tokens x B=%d; "
-                    "32/256 experts top-8 + shared 2048/8; collectives off (1 GPU)" % (s_loc, B),
-        "ms_per_layer": ms, "eager_launches": True,
-        "breakdown_ms": {k: float(v) for k, v in zip(
-            ["embed", "qkv", "attention", "split_reduce", "o_proj", "ffn_router_to_gate_up", "ffn_down_combine",
-             "lm_head", "merge"], prof)},
-        "mla_attention": {
-            "kernel": "mla_decode_kernel (tcgen05 cta_group::2 CTA pair, TMEM accumulators, 2-SM TMA)", "launch_ms": att_ms,
-            "algorithmic_kv_bytes": kv_bytes, "algorithmic_flops": flops,
-            "roofline": {"bound": "tensor", "achieved": flops / (att_ms * 1e-3) / 1e12, "peak": tc, "unit": "TFLOP/s",
-                         "frac": flops / (att_ms * 1e-3) / 1e12 / tc, "peak_kind": tc_kind,
+    out = {"ms_per_layer": ms, "eager_launches": True, "kv_tokens_per_request_on_this_gpu": s_loc,
+           "breakdown_ms": {k: float(v) for k, v in zip(
+               ["embed", "qkv", "attention", "split_reduce", "o_proj", "gate_up_or_router_to_gate_up",
+                "down_or_down_combine", "lm_head", "merge"], prof)}}
+    if mla:
+        active = int(P.lib().hx_moe_active_experts(eng._h))
+        kv_bytes = B * s_loc * 576 * 2
+        flops = B * s_loc * Q * (576 + 512) * 2
+        tc, tc_kind = peak_tensor()
+        out["workload"] = ("deepseek-r1-like layer, one GPU of KVP=8 x EP=8 (tpf=1): 128 heads x %d latent tokens x "
+                           "B=%d; 32/256 experts top-8 + shared 2048/8; collectives off (1 GPU)" % (s_loc, B))
+        out["mla_attention"] = {
+            "kernel": "mla_decode_kernel (tcgen05 cta_group::2 CTA pair, TMEM accumulators, 2-SM TMA)",
+            "launch_ms": att_ms, "algorithmic_kv_bytes": kv_bytes, "algorithmic_flops": flops,
+            "roofline": {"bound": "tensor", "achieved": flops / (att_ms * 1e-3) / 1e12, "peak": tc,
+                         "unit": "TFLOP/s", "frac": flops / (att_ms * 1e-3) / 1e12 / tc, "peak_kind": tc_kind,
                          "hbm_achieved_gbs": kv_bytes / (att_ms * 1e-3) / 1e9,
                          "hbm_frac": kv_bytes / (att_ms * 1e-3) / 1e9 / hbm,
-                         "t_roof_ms": max(kv_bytes / hbm / 1e6, flops / tc / 1e9)}},
-        "moe": {"local_experts": 32, "active_local_experts_last_step": active,
-                "expert_bytes_streamed": active * 3 * spec.hidden_dim * spec.moe.expert_ffn_dim * 2},
-        "engine": info,
-    }
+                         "t_roof_ms": max(kv_bytes / hbm / 1e6, flops / tc / 1e9)}}
+        out["moe"] = {"local_experts": spec.moe.total_experts // ep, "active_local_experts_last_step": active,
+                      "expert_bytes_streamed": active * 3 * H * spec.moe.expert_ffn_dim * 2}
+    else:
+        K = spec.kv_heads
+        kv_bytes = B * 2 * K * Hsz * s_loc * 2
+        # roofline.hpp:17-48 at bf16: QKV duplicated per KVP rank, O and FFN sharded over N
+        w_bytes = H * (Q * Hsz + 2 * K * Hsz) * 2 + (H // N) * H * 2 + 3 * H * spec.ffn_dim // N * 2
+        out["workload"] = ("llama405b-like layer, one GPU of TPA=1 x KVP=8 (TPF=8): %d KV heads x %d tokens x B=%d; "
+                           "QKV replicated, W_O rows and FFN features 1/8; collectives off (1 GPU)" % (K, s_loc, B))
+        out["attention"] = {
+            "kernel": "attn_decode_kernel<128,8,2> (TMA bulk-copy page ring, mma.sync)", "launch_ms": att_ms,
+            "algorithmic_kv_bytes": kv_bytes,
+            "roofline": {"bound": "hbm", "achieved": kv_bytes / (att_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                         "frac": kv_bytes / (att_ms * 1e-3) / 1e9 / hbm}}
+        out["layer_roofline"] = {"bound": "hbm", "algorithmic_bytes": kv_bytes + w_bytes, "weight_bytes": w_bytes,
+                                 "t_roof_ms": (kv_bytes + w_bytes) / hbm / 1e6,
+                                 "achieved_gbs": (kv_bytes + w_bytes) / (ms * 1e-3) / 1e9,
+                                 "frac": (kv_bytes + w_bytes) / (ms * 1e-3) / 1e9 / hbm}
+        out["ttl_ms_extrapolated_126_layers"] = ms * spec.layers
+    out["engine"] = info
     eng.close()
     return out
 
@@ -403,12 +425,14 @@ def ours(a):
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as ex:  # reported, never fatal for the GPU number
             line["cpu_baseline"] = {"error": str(ex)[:200]}
-    if world == 1 and not a.no_deepseek:
-        eng.close()  # free the 150 GB pool before the deepseek slice
-        try:
-            line["deepseek_slice"] = deepseek_slice(a)
-        except Exception as ex:  # reported, never fatal for the headline number
-            line["deepseek_slice"] = {"error": str(ex)[:300]}
+    if world == 1 and not a.no_slices:
+        eng.close()  # free the 150 GB pool before the 8-GPU-pool slices
+        for key, preset, ctx, ep in (("llama405b_slice", "llama405b-like", a.slice_context, 1),
+                                     ("deepseek_slice", "deepseek-r1-like", a.slice_context, 8)):
+            try:
+                line[key] = pool_slice(a, preset, ctx, ep)
+            except Exception as ex:  # reported, never fatal for the headline number
+                line[key] = {"error": str(ex)[:300]}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -12,7 +12,10 @@
 //     streams the split's contiguous 16-token pages into a shared-memory ring
 //     with cp.async.bulk (TMA bulk engine), completion via mbarrier tx-bytes;
 //     the item's query rows ride along in the first stage.
-//   * NWC consumer warps: one page each per stage; S = Q K^T and O += P V on
+//   * NWC consumer warps: one page each per stage (QC = 2 query chunks of
+//     8 rows per item when the GQA group exceeds 8: warp w takes chunk w % QC
+//     and pages w / QC + k * NWC / QC, so each KV page is read from HBM once
+//     and from shared memory QC times); S = Q K^T and O += P V on
 //     legacy HMMA m16n8k16 (bf16 in, fp32 accumulate). The fp32 query is
 //     split hi+mid+lo into three bf16 terms (rows 0-7 / 8-15 of M-tile 0 and
 //     rows 0-7 of M-tile 1) and P into hi+lo (rows 0-7 / 8-15), so the only
@@ -40,7 +43,7 @@ struct StageMeta {
   int ntok;         // tokens on this rank for the stream
   int first;        // first stage of the item (q rows staged)
   int last;         // last stage of the item
-  int rows;         // valid query rows in this stream (<= 8)
+  int rows;         // valid query rows in this stream (<= 8 * QC)
 };
 
 template <int DP>
@@ -56,11 +59,14 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 
 }  // namespace
 
-template <int DP, int NWC, int NSTAGE>
+template <int DP, int NWC, int NSTAGE, int QC>
 __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const AttnParams p) {
   using Cfg = AttnCfg<DP>;
+  static_assert(NWC % QC == 0, "query chunks must divide the consumer warps");
+  constexpr int QR = 8 * QC;           // query rows per item
+  constexpr int WPC = NWC / QC;        // warps (pages per stage slot) per query chunk
   constexpr uint32_t STAGE_KV = NWC * Cfg::PAGE;
-  constexpr uint32_t Q_BYTES = 8 * DP * 4;
+  constexpr uint32_t Q_BYTES = QR * DP * 4;
   constexpr uint32_t STAGE_BYTES = STAGE_KV + Q_BYTES;
 
   extern __shared__ __align__(128) uint8_t smem[];
@@ -110,13 +116,13 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           const int pages = (ntok + 15) >> 4;
           pg0 = static_cast<int>((static_cast<long long>(split) * pages) / p.splits);
           pg1 = static_cast<int>((static_cast<long long>(split + 1) * pages) / p.splits);
-          const int g_rows = p.group - qc * 8;
-          rows = g_rows < 8 ? g_rows : 8;
+          const int g_rows = p.group - qc * QR;
+          rows = g_rows < QR ? g_rows : QR;
           if (pg1 <= pg0) continue;  // empty split: nothing to emit
           const size_t pool_stream = (static_cast<size_t>(sl) * p.batch + b) * p.kvh_per_slot + kvh;
           kv_base = p.kv + pool_stream * p.page_cap * static_cast<size_t>(Cfg::PAGE);
           const int grp = slot / p.kvp;
-          const int head0 = ((grp - p.q_grp_base) * p.kvh_per_slot + kvh) * p.group + qc * 8;
+          const int head0 = ((grp - p.q_grp_base) * p.kvh_per_slot + kvh) * p.group + qc * QR;
           q_src = p.q + (static_cast<size_t>(b) * p.q_heads + head0) * DP;
         }
         const int nchunks = done ? 1 : (pg1 - pg0 + NWC - 1) / NWC;
@@ -160,6 +166,8 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
   } else {
     // ------------------------------------------------------------ consumers
     const int g = lane >> 2, c = lane & 3;
+    const int qch = warp % QC;   // this warp's query chunk (rows qch*8 .. qch*8+7 of the item)
+    const int wpg = warp / QC;   // its page slot within the chunk's share of a stage
     uint32_t qa[Cfg::KS][4];  // M-tile 0: hi (rows 0-7), mid (rows 8-15)
     uint32_t qb[Cfg::KS][2];  // M-tile 1: lo (rows 0-7); rows 8-15 are zero
     float acc[Cfg::ND][4];
@@ -174,8 +182,8 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
       const uint32_t sbase = stage_base + s * STAGE_BYTES;
       if (m.first) {
         // stage the item's query rows as hi/mid/lo bf16 fragments
-        const float* qs = reinterpret_cast<const float*>(stages + s * STAGE_BYTES + STAGE_KV);
-        const bool valid = g < m.rows;
+        const float* qs = reinterpret_cast<const float*>(stages + s * STAGE_BYTES + STAGE_KV) + qch * 8 * DP;
+        const bool valid = qch * 8 + g < m.rows;
 #pragma unroll
         for (int ks = 0; ks < Cfg::KS; ++ks) {
           float v[4];
@@ -199,9 +207,10 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
         m_ref = -INFINITY;
         l_sum = 0.f;
       }
-      if (warp < m.npages) {
-        const uint32_t pbase = sbase + warp * Cfg::PAGE;
-        const int tok0 = (m.page0 + warp) * 16;
+#pragma unroll 1
+      for (int pj = wpg; pj < m.npages; pj += WPC) {
+        const uint32_t pbase = sbase + pj * Cfg::PAGE;
+        const int tok0 = (m.page0 + pj) * 16;
         const int valid_tok = m.ntok - tok0;  // >= 1
         // ---- S = Q K^T over the 16 tokens of this page
         float s0[2][4], s1[2][4];
@@ -290,15 +299,16 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
         }
         named_bar_sync(1, NWC * 32);
         const int rows = m.rows;
-        const size_t obase = static_cast<size_t>(m.item) * 8 * DP;
+        const size_t obase = static_cast<size_t>(m.item) * QR * DP;
         for (int idx = threadIdx.x; idx < rows * DP; idx += NWC * 32) {
-          const int q = idx / DP, d = idx - q * DP;
+          const int qi = idx / DP, d = idx - qi * DP;
+          const int qc = qi >> 3, q = qi & 7;  // chunk qc is combined over warps qc, qc + QC, ...
           float M = -INFINITY;
 #pragma unroll
-          for (int w = 0; w < NWC; ++w) M = fmaxf(M, scratch[w * (8 * DP + 16) + 8 * DP + q]);
+          for (int w = qc; w < NWC; w += QC) M = fmaxf(M, scratch[w * (8 * DP + 16) + 8 * DP + q]);
           float L = 0.f, O = 0.f;
 #pragma unroll
-          for (int w = 0; w < NWC; ++w) {
+          for (int w = qc; w < NWC; w += QC) {
             const float* wsw = scratch + w * (8 * DP + 16);
             const float mw = wsw[8 * DP + q];
             const float e = mw == -INFINITY ? 0.f : fast_exp2(mw - M);
@@ -306,7 +316,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
             O += wsw[q * DP + d] * e;
           }
           p.part_o[obase + idx] = O / L;
-          if (d == 0) p.part_lse2[static_cast<size_t>(m.item) * 8 + q] = M + __log2f(L);
+          if (d == 0) p.part_lse2[static_cast<size_t>(m.item) * QR + qi] = M + __log2f(L);
         }
         named_bar_sync(1, NWC * 32);
         // the next item re-initialises state on its first stage
@@ -339,8 +349,9 @@ __global__ void attn_split_reduce_kernel(const AttnParams p, float* frag_o, floa
   griddep_launch_dependents();
   const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const int row = warp_global & 7;
-  const int stream = warp_global >> 3;
+  const int QR = p.qrows;  // query rows per stream: 8 or 16
+  const int row = warp_global % QR;
+  const int stream = warp_global / QR;
   if (stream < p.n_streams) {
     int t = stream;
     const int qc = t % p.q_chunks; t /= p.q_chunks;
@@ -349,7 +360,7 @@ __global__ void attn_split_reduce_kernel(const AttnParams p, float* frag_o, floa
     const int slot_local = t / p.stream_batch;
     const int slot = slot_local + p.slot_base;
     const int rank = slot % p.kvp;
-    const int qrow = qc * 8 + row;
+    const int qrow = qc * QR + row;
     if (qrow < p.group) {
       const int ntok = static_cast<int>(rr_count(p.total[b], rank, p.chunk, p.kvp));
       const int pages = (ntok + 15) >> 4;
@@ -362,7 +373,7 @@ __global__ void attn_split_reduce_kernel(const AttnParams p, float* frag_o, floa
       for (int s = lane; s < p.splits; s += 32) {
         const int pg0 = static_cast<int>((static_cast<long long>(s) * pages) / p.splits);
         const int pg1 = static_cast<int>((static_cast<long long>(s + 1) * pages) / p.splits);
-        if (pg1 > pg0) M = fmaxf(M, p.part_lse2[(static_cast<size_t>(s) * p.n_streams + stream) * 8 + row]);
+        if (pg1 > pg0) M = fmaxf(M, p.part_lse2[(static_cast<size_t>(s) * p.n_streams + stream) * QR + row]);
       }
 #pragma unroll
       for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
@@ -378,9 +389,9 @@ __global__ void attn_split_reduce_kernel(const AttnParams p, float* frag_o, floa
           const int pg1 = static_cast<int>((static_cast<long long>(s + 1) * pages) / p.splits);
           const bool ok = s < p.splits && pg1 > pg0;
           const size_t item = static_cast<size_t>(s) * p.n_streams + stream;
-          w[j] = ok ? p.part_lse2[item * 8 + row] : -INFINITY;
+          w[j] = ok ? p.part_lse2[item * QR + row] : -INFINITY;
 #pragma unroll
-          for (int i = 0; i < PER; ++i) v[j][i] = ok ? p.part_o[(item * 8 + row) * DP + lane + 32 * i] : 0.f;
+          for (int i = 0; i < PER; ++i) v[j][i] = ok ? p.part_o[(item * QR + row) * DP + lane + 32 * i] : 0.f;
         }
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -409,38 +420,40 @@ __global__ void bump_totals_kernel(int* total, int n) {
 
 // ------------------------------------------------------------------------
 // host launchers
-template <int DP, int NWC, int NSTAGE>
+template <int DP, int NWC, int NSTAGE, int QC>
 static size_t attn_smem_bytes() {
-  return NSTAGE * (NWC * AttnCfg<DP>::PAGE + 8 * DP * 4) + NWC * (8 * DP + 16) * 4 +
+  return NSTAGE * (NWC * AttnCfg<DP>::PAGE + QC * 8 * DP * 4) + NWC * (8 * DP + 16) * 4 +
          NSTAGE * sizeof(StageMeta) + 2 * NSTAGE * 8 + 64;
 }
 
-template <int DP, int NWC, int NSTAGE>
+template <int DP, int NWC, int NSTAGE, int QC>
 static cudaError_t launch_attn_t(const AttnParams& p, int grid, cudaStream_t stream) {
-  const size_t smem = attn_smem_bytes<DP, NWC, NSTAGE>();
+  const size_t smem = attn_smem_bytes<DP, NWC, NSTAGE, QC>();
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<DP, NWC, NSTAGE>,
+    cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<DP, NWC, NSTAGE, QC>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  return launch_k(attn_decode_kernel<DP, NWC, NSTAGE>, dim3(grid), dim3((NWC + 1) * 32), smem, stream, p);
+  return launch_k(attn_decode_kernel<DP, NWC, NSTAGE, QC>, dim3(grid), dim3((NWC + 1) * 32), smem, stream, p);
 }
 
 cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t stream) {
+  const bool two = p.qrows == 16;
+  if (!two && p.qrows != 8) return cudaErrorInvalidValue;
   switch (p.dp) {
-    case 32: return launch_attn_t<32, 8, 4>(p, grid, stream);
-    case 64: return launch_attn_t<64, 8, 3>(p, grid, stream);
-    case 128: return launch_attn_t<128, 8, 2>(p, grid, stream);
+    case 32: return two ? launch_attn_t<32, 8, 4, 2>(p, grid, stream) : launch_attn_t<32, 8, 4, 1>(p, grid, stream);
+    case 64: return two ? launch_attn_t<64, 8, 3, 2>(p, grid, stream) : launch_attn_t<64, 8, 3, 1>(p, grid, stream);
+    case 128: return two ? launch_attn_t<128, 8, 2, 2>(p, grid, stream) : launch_attn_t<128, 8, 2, 1>(p, grid, stream);
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_attn_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse,
                                      cudaStream_t stream) {
-  const int warps = p.n_streams * 8;
+  const int warps = p.n_streams * p.qrows;
   const int threads = 256;
   const int blocks = (warps * 32 + threads - 1) / threads;
   switch (p.dp) {
@@ -460,10 +473,10 @@ void set_pdl(bool on) { g_pdl = on; }
 bool pdl_enabled() { return g_pdl; }
 
 size_t attn_decode_smem_bytes(int dp) {
-  switch (dp) {
-    case 32: return attn_smem_bytes<32, 8, 4>();
-    case 64: return attn_smem_bytes<64, 8, 3>();
-    case 128: return attn_smem_bytes<128, 8, 2>();
+  switch (dp) {  // the larger (two query chunks) variant
+    case 32: return attn_smem_bytes<32, 8, 4, 2>();
+    case 64: return attn_smem_bytes<64, 8, 3, 2>();
+    case 128: return attn_smem_bytes<128, 8, 2, 2>();
     default: return 0;
   }
 }

@@ -150,7 +150,8 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
   AD_ = mla_ ? DV_ : static_cast<int>(D_);   // per-head attention output width
   ADP_ = mla_ ? DV_ : DP_;                    // its stride in the fragment buffers
   G_ = static_cast<int>(Qh_ / Kh_);
-  q_chunks_ = mla_ ? 1 : (G_ + 7) / 8;
+  q_rows_ = G_ > 8 ? 16 : 8;  // a GQA group of 9-16 query heads shares one pass over its KV head
+  q_chunks_ = mla_ ? 1 : (G_ + q_rows_ - 1) / q_rows_;
   kvh_per_slot_ = static_cast<int>(Kh_ / tpa_);
   q_per_slot_ = static_cast<int>(Qh_ / tpa_);
   N_ = tpa_ * kvp_;
@@ -306,7 +307,7 @@ void Engine::alloc() {
     d_recv_ = dalloc<float>(static_cast<size_t>(kvp_) * B_ * xchunk_, "exchange recv");
     d_parth_ = dalloc<float>(static_cast<size_t>(B_) * H_, "tp partial");
   }
-  const size_t part_rows = mla_ ? static_cast<size_t>(kMlaHeads) : 8;  // rows per item
+  const size_t part_rows = mla_ ? static_cast<size_t>(kMlaHeads) : static_cast<size_t>(q_rows_);  // rows per item
   const size_t part_w = mla_ ? static_cast<size_t>(DV_) : static_cast<size_t>(DP_);
   d_part_o_ = dalloc<float>(static_cast<size_t>(n_items_) * part_rows * part_w, "part_o");
   d_part_lse_ = dalloc<float>(static_cast<size_t>(n_items_) * part_rows, "part_lse");
@@ -901,6 +902,7 @@ AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) {
   a.q_grp_base = dist_mode_ == HX_POOL_LOCAL ? 0 : grp_;
   a.group = G_;
   a.q_chunks = q_chunks_;
+  a.qrows = q_rows_;
   a.kvh_per_slot = kvh_per_slot_;
   a.q_per_slot = q_per_slot_;
   a.kvp = kvp_;
@@ -912,11 +914,10 @@ AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) {
   a.stream_batch = b_count;
   a.n_streams = n_slots_ * b_count * kvh_per_slot_ * q_chunks_;
   a.splits = b_count == B_ ? splits_ : splits_req_;
-  a.n_items = a.n_streams * splits_;
+  a.n_items = a.n_streams * a.splits;  // HOP-B (one request): splits_req_ balanced page ranges
   a.qscale = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(mla_ ? W_ : D_)));
   if (mla_) {
     a.qimg = d_qimg_;
-    a.n_items = a.n_streams * a.splits;
     a.dp = DV_;
   }
   return a;

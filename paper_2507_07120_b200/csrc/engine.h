@@ -100,7 +100,7 @@ class Engine {
   int64_t cap_;
   int device_;
   bool hopb_, graphs_;
-  int DP_, G_, q_chunks_, kvh_per_slot_, q_per_slot_, n_slots_, slot_base_;
+  int DP_, G_, q_rows_, q_chunks_, kvh_per_slot_, q_per_slot_, n_slots_, slot_base_;
   int page_cap_;
   size_t page_bytes_;
   int num_sms_;

@@ -42,8 +42,8 @@ struct AttnParams {
   const uint8_t* kv;       // page pool for this layer: [slot_local][B][kvh_per_slot][page_cap] pages
   const float* q;          // [B][q_heads][DP] fp32 (padded rows)
   const int* total;        // [B] tokens appended to this layer's cache so far
-  float* part_o;           // [n_items][8][DP]
-  float* part_lse2;        // [n_items][8]  (log2 domain)
+  float* part_o;           // [n_items][qrows][DP]
+  float* part_lse2;        // [n_items][qrows]  (log2 domain)
   int* work_counter;       // persistent-kernel work queue (self-resetting)
   int* done_counter;
   int dp, batch, q_heads, group, q_chunks, kvh_per_slot, q_per_slot;
@@ -54,6 +54,7 @@ struct AttnParams {
   int b_begin;             // requests [b_begin, b_begin + stream_batch) in this launch
   int stream_batch;        // (HOP-B launches one request at a time)
   const uint8_t* qimg;     // MLA: [B] absorbed-query images (kv_layout.cuh mla_q_offset)
+  int qrows;               // GQA: query rows per stream (8, or 16 when the group exceeds 8)
 };
 cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t stream);
 // MLA (tcgen05): items = (split, stream, value half); part_o [n_items][128][256],

@@ -73,3 +73,45 @@ def test_loopback_pool_matches_oracle(tpa, kvp, hopb):
         tokens = no
     for e in engines:
         e.close()
+
+
+def test_loopback_hopb_long_context_group16():
+    """HOP-B launches attention once per request with its own (larger) split
+    count; at a context long enough that it differs from the batched launch's,
+    every split must still be covered. GQA group 16 runs the two-query-chunk
+    kernel variant (each KV page read once for 16 query heads)."""
+    import paper_2507_07120_b200 as P
+    from paper_2507_07120_b200.model import Loopback
+    H, Q, K, D, F, L, V, B, kvp = 1024, 32, 2, 32, 512, 1, 500, 4, 2
+    S = 40000
+    spec = P.model.ModelSpec("test16", L, H, Q, K, D, F, 3, "gqa", 0, vocab=V)
+    lb = Loopback(kvp)
+    engines = [P.HelixDecoder(spec, tpa=1, kvp=kvp, chunk_size=16, batch=B, capacity=S + 64, layers=L, vocab=V,
+                              use_graphs=False, hopb=True, pool=2, rank=r, loopback=lb) for r in range(kvp)]
+    info = engines[0].info()
+    assert info["attn_splits"] < (S // kvp // 16) // 8, info  # the per-request launch uses more splits
+    o = O.Model(H, Q, K, D, F, L, V, tpa=1, kvp=kvp, chunk=16, batch=B, seed=77, qkv_hash=True, bf16=True)
+    for e in engines:
+        e.init_weights(77, qkv="hash")
+        e.fill_kv_hash(S, 77)
+    for b in range(B):
+        o.grow_hash(0, b, S)
+    tokens = np.array([1, 2, 3, 499])
+    results = [None] * kvp
+    errors = []
+
+    def run(r):
+        try:
+            results[r] = engines[r].step(tokens, want_logits=True, want_hidden=True)
+        except Exception as ex:  # surfaced below
+            errors.append(ex)
+    th = [threading.Thread(target=run, args=(r,), daemon=True) for r in range(kvp)]
+    [t.start() for t in th]
+    [t.join(timeout=300) for t in th]
+    assert not any(t.is_alive() for t in th), "loopback ranks did not finish"
+    assert not errors, errors
+    lo, ho, no = o.step(tokens)
+    for r in range(kvp):
+        assert rel_err(results[r][2], ho) <= 2e-3, (r, rel_err(results[r][2], ho))
+    for e in engines:
+        e.close()

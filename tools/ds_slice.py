@@ -1,11 +1,17 @@
-"""Run the bench's deepseek-r1-like single-GPU slice once (for ncu captures)."""
+"""Run one of the bench's one-GPU-of-8 slices once (for ncu captures).
+
+    python tools/ds_slice.py [deepseek-r1-like|llama405b-like]
+"""
+import os
 import sys
-sys.path.insert(0, ".")
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import bench  # noqa: E402
 
 
 class A:
-    batch, deepseek_context, warmup, steps = 8, 125000, 2, 2
+    batch, warmup, steps = 8, 2, 2
 
 
-print(bench.deepseek_slice(A())["breakdown_ms"])
+preset = sys.argv[1] if len(sys.argv) > 1 else "deepseek-r1-like"
+print(bench.pool_slice(A(), preset, 125000, 8 if preset == "deepseek-r1-like" else 1)["breakdown_ms"])
