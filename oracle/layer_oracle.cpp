@@ -58,11 +58,12 @@ ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, st
   for (i64 l = 0; l < d.layers; ++l) {
     if (mla) {
       for (i64 b = 0; b < batch; ++b) mla_.emplace_back(kvp, 1, W, chunk);
-      wq_mla_.push_back(hash_matrix(seed, kWq, l, d.hidden, d.query_heads * W,
-                                    8.0 / std::sqrt(static_cast<double>(d.hidden)), bf16));
+      wq_mla_.push_back(hash_matrix(seed, kWq, l, d.hidden, d.query_heads * d.head_size, sh, bf16));
+      wuk_.push_back(hash_matrix(seed, kWuk, l, d.query_heads * d.head_size, W,
+                                 16.0 / std::sqrt(static_cast<double>(d.head_size)), bf16));
       wdkv_.push_back(hash_matrix(seed, kWk, l, d.hidden, W, sh, bf16));
-      wo_.push_back(hash_matrix(seed, kWo, l, d.query_heads * DV, d.hidden,
-                                1.0 / std::sqrt(static_cast<double>(d.query_heads * DV)), bf16));
+      wuv_.push_back(hash_matrix(seed, kWuv, l, d.query_heads * DV, d.head_size,
+                                 1.0 / std::sqrt(static_cast<double>(DV)), bf16));
     }
     for (i64 b = 0; b < batch && !mla; ++b) {
       h_.emplace_back(Dims{d.query_heads, d.kv_heads, d.head_size}, tpa, kvp, chunk,
@@ -73,7 +74,7 @@ ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, st
             hash_matrix(seed, kWk, l, d.hidden, d.kv_heads * d.head_size, 1.0, bf16),
             hash_matrix(seed, kWv, l, d.hidden, d.kv_heads * d.head_size, 1.0, bf16));
     }
-    if (!mla) wo_.push_back(hash_matrix(seed, kWo, l, d.hidden, d.hidden, sh, bf16));
+    wo_.push_back(hash_matrix(seed, kWo, l, d.hidden, d.hidden, sh, bf16));
     if (d.ffn > 0) {  // dense FFN, or the MoE shared expert
       wg_.push_back(hash_matrix(seed, kWgate, l, d.hidden, d.ffn, sh, bf16));
       wu_.push_back(hash_matrix(seed, kWup, l, d.hidden, d.ffn, sh, bf16));
@@ -198,16 +199,28 @@ std::vector<double> ModelOracle::ffn(i64 l, i64 b, const std::vector<double>& f)
 
 std::vector<double> ModelOracle::attend_mla(i64 l, i64 b, const std::vector<double>& a) {
   const i64 Qh = d_.query_heads, W = mla_width(d_.kv_latent), DV = mla_value_width(d_.kv_latent);
-  const std::vector<double> qf = vecmat(a, wq_mla_[static_cast<std::size_t>(l)]);
+  const i64 hs = d_.head_size;
+  const std::vector<double> qn = vecmat(a, wq_mla_[static_cast<std::size_t>(l)]);
+  const Mat& wuk = wuk_[static_cast<std::size_t>(l)];
   Mat q(Qh, W);
-  for (i64 i = 0; i < Qh * W; ++i) q.a[static_cast<std::size_t>(i)] = round_bf16(qf[static_cast<std::size_t>(i)]);
+  for (i64 h = 0; h < Qh; ++h)
+    for (i64 j = 0; j < W; ++j) {
+      double acc = 0.0;
+      for (i64 dd = 0; dd < hs; ++dd) acc += qn[static_cast<std::size_t>(h * hs + dd)] * wuk(h * hs + dd, j);
+      q(h, j) = round_bf16(acc);
+    }
   ShardedKVCache& cache = mla_[static_cast<std::size_t>(l * batch_ + b)];
   std::vector<AttentionFragment> frags;
   for (i64 r = 0; r < cache.kvp(); ++r) frags.push_back(shard_attention(q, cache, r, 0, 1, Qh));
   const AttentionFragment m = merge_fragments(frags);
-  std::vector<double> att(static_cast<std::size_t>(Qh * DV));
+  const Mat& wuv = wuv_[static_cast<std::size_t>(l)];
+  std::vector<double> att(static_cast<std::size_t>(Qh * hs));
   for (i64 h = 0; h < Qh; ++h)
-    for (i64 dd = 0; dd < DV; ++dd) att[static_cast<std::size_t>(h * DV + dd)] = m.out(h, dd);
+    for (i64 j = 0; j < hs; ++j) {
+      double acc = 0.0;
+      for (i64 dd = 0; dd < DV; ++dd) acc += m.out(h, dd) * wuv(h * DV + dd, j);
+      att[static_cast<std::size_t>(h * hs + j)] = acc;
+    }
   // attend-then-append: this token's latent joins the cache after the merge
   const std::vector<double> c = vecmat(a, wdkv_[static_cast<std::size_t>(l)]);
   Mat row(1, W);
@@ -232,7 +245,7 @@ std::vector<double> ModelOracle::step(const std::vector<std::int64_t>& tokens,
     if (hidden) std::copy(x.begin(), x.end(), hidden->begin() + b * H);
     for (i64 l = 0; l < d_.layers; ++l) {
       const std::vector<double> a = rmsnorm(x);
-      // GQA: [Q x Hsz] == flattened [H]; MLA: [Q x DV]
+      // [Q x Hsz] == flattened [H] (MLA: after the per-head W_UV)
       const std::vector<double> att = d_.kv_latent > 0 ? attend_mla(l, b, a) : harness(l, b).step(a).a;
       const std::vector<double> o = vecmat(att, wo_[static_cast<std::size_t>(l)]);
       std::vector<double> h(static_cast<std::size_t>(H));

@@ -43,7 +43,7 @@ inline double hash_unit(std::uint64_t seed, std::uint64_t stream, std::uint64_t 
 }
 enum HashKind : std::uint64_t {
   kWq = 1, kWk = 2, kWv = 3, kWo = 4, kWgate = 5, kWup = 6, kWdown = 7, kEmb = 8, kLm = 9,
-  kCacheK = 10, kCacheV = 11, kWrouter = 12, kEgate = 13, kEup = 14, kEdown = 15
+  kCacheK = 10, kCacheV = 11, kWrouter = 12, kEgate = 13, kEup = 14, kEdown = 15, kWuk = 16, kWuv = 17
 };
 inline std::uint64_t hash_stream(HashKind kind, std::int64_t layer) {
   return (static_cast<std::uint64_t>(kind) << 32) | static_cast<std::uint64_t>(layer);
@@ -65,18 +65,24 @@ struct ModelDims {
   i64 kv_latent = 0;  // > 0: MLA attention (types.hpp:37-49), latent width W = 2 * kv_latent
 };
 
-// MLA attention in the absorbed decode form (types.hpp:37-49: K_eff = 1, one
-// latent "KV head" of width W = 2 * kv_latent_dim = 576 for deepseek-r1-like,
-// 512 latent + 64 rope dims). Per request, with a = rmsnorm(x):
-//   q_h = bf16(a . Wq[:, h*W:(h+1)*W])   (absorbed W_UK; hash kWq, scale 8/sqrt(H);
-//                                          the B200 MMA consumes q in bf16)
-//   c   = a . Wdkv                        (hash kWk, scale 1/sqrt(H); stored bf16)
+// MLA attention in the weight-absorbed decode form (types.hpp:37-49: K_eff = 1,
+// one latent "KV head" of width W = 2 * kv_latent_dim = 576 for
+// deepseek-r1-like, 512 latent + 64 rope dims). The projections keep the
+// reference's weight shapes (roofline.hpp:17-48 counts W_q as H x Q*Hsz, the
+// latent as H x W and W_O as (H/N) x H) plus the two small per-head
+// up-projections absorbed at decode time. Per request, with a = rmsnorm(x):
+//   n_h = (a . Wq)[h*Hsz:(h+1)*Hsz]     (hash kWq [H x Q*Hsz], scale 1/sqrt(H))
+//   q_h = bf16(n_h . Wuk_h)               (W_UK absorbed into the query: hash kWuk
+//                                          [Q*Hsz x W] = Q blocks [Hsz x W], scale
+//                                          16/sqrt(Hsz); the B200 MMA consumes q in bf16)
+//   c   = a . Wdkv                        (hash kWk [H x W], scale 1/sqrt(H); stored bf16)
 //   o_h = partial_head_attention / merge_head_fragments (attention.hpp:65-78,
 //         :118-137, via shard_attention / merge_fragments) with keys = values =
 //         the rank's latent rows, scale logit_scale(W) = 1/sqrt(W); keep
 //         o_h[0:DV], DV = W - 64 (the value part of the latent)
-//   h   = x + concat_h(o_h) . Wo          (absorbed W_UV W_O: [Q*DV x H], hash kWo,
-//                                          scale 1/sqrt(Q*DV))
+//   v_h = o_h . Wuv_h                     (W_UV: hash kWuv [Q*DV x Hsz] = Q blocks
+//                                          [DV x Hsz], scale 1/sqrt(DV))
+//   h   = x + concat_h(v_h) . Wo          (hash kWo [H x H], scale 1/sqrt(H), as GQA)
 // then append c round-robin (attend-then-append, attention.hpp:504-508).
 // Cache fill: latent element d of token g of (layer, request) =
 //   hash_unit(seed, (kCacheK<<32)|layer, ((request << 32) + g) * W + d).
@@ -125,7 +131,7 @@ class ModelOracle {
   std::vector<std::vector<Mat>> eg_, eu_, ed_;  // [layer][expert]
   std::vector<std::vector<i64>> routes_;        // [layer*B + b] -> selected experts
   std::vector<ShardedKVCache> mla_;             // [layer*B + b] latent caches (MLA)
-  std::vector<Mat> wq_mla_, wdkv_;              // [layer]
+  std::vector<Mat> wq_mla_, wdkv_, wuk_, wuv_;  // [layer]
   std::vector<double> attend_mla(i64 l, i64 b, const std::vector<double>& a);
   std::vector<double> gaps_;                    // [layer*B + b] -> top-k margin
   Mat emb_, lm_;

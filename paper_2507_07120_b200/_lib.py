@@ -7,7 +7,8 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libhelix_b200.so")
+# HX_LIB_PATH: A/B measurement of another in-tree build (tools only)
+LIB_PATH = os.environ.get("HX_LIB_PATH") or os.path.join(HERE, "libhelix_b200.so")
 
 HX_OK, HX_ERR_INVALID, HX_ERR_CUDA, HX_ERR_NCCL, HX_ERR_STATE = 0, 1, 2, 3, 4
 

@@ -207,8 +207,10 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
         m_ref = -INFINITY;
         l_sum = 0.f;
       }
-#pragma unroll 1
-      for (int pj = wpg; pj < m.npages; pj += WPC) {
+#pragma unroll
+      for (int kq = 0; kq < QC; ++kq) {
+        const int pj = QC == 1 ? warp : wpg + kq * WPC;
+        if (pj >= m.npages) break;
         const uint32_t pbase = sbase + pj * Cfg::PAGE;
         const int tok0 = (m.page0 + pj) * 16;
         const int valid_tok = m.ntok - tok0;  // >= 1

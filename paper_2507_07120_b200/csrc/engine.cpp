@@ -94,7 +94,8 @@ int round_up(int64_t a, int64_t b) { return static_cast<int>((a + b - 1) / b * b
 
 uint64_t hash_stream(uint64_t kind, int64_t layer) { return (kind << 32) | static_cast<uint64_t>(layer); }
 enum : uint64_t { kWq = 1, kWk = 2, kWv = 3, kWo = 4, kWgate = 5, kWup = 6, kWdown = 7, kEmb = 8, kLm = 9,
-                  kCacheK = 10, kCacheV = 11, kWrouter = 12, kEgate = 13, kEup = 14, kEdown = 15 };
+                  kCacheK = 10, kCacheV = 11, kWrouter = 12, kEgate = 13, kEup = 14, kEdown = 15,
+                  kWuk = 16, kWuv = 17 };
 // routed-expert weights: one stream per (layer, expert) -- oracle/layer_oracle.hpp expert_stream
 uint64_t expert_stream(uint64_t kind, int64_t layer, int64_t expert) {
   return (kind << 32) | (static_cast<uint64_t>(layer) << 16) | static_cast<uint64_t>(expert);
@@ -124,6 +125,8 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
     if (tpa_ != 1) throw std::invalid_argument("MLA needs tpa = 1 (tpa <= effective KV heads)");
     if (Qh_ > kMlaHeads) throw std::invalid_argument("MLA kernel supports at most 128 query heads");
     if (m.attention_only) throw std::invalid_argument("the attention-only harness is GQA (DecodeHarness)");
+    if (par.distributed != HX_POOL_LOCAL && Qh_ % par.kvp)
+      throw std::invalid_argument("MLA needs kvp to divide query_heads (the O-projection shards whole heads)");
   } else if (D_ > 128) {
     throw std::invalid_argument("head_size > 128 is not supported by the GQA decode kernel");
   }
@@ -135,7 +138,7 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
     Fe_ = m.expert_ffn;
     if (topk_ < 1 || topk_ > 16 || topk_ > E_) throw std::invalid_argument("moe top_k must be in [1, min(16, experts)]");
     if (Fe_ < 16 || Fe_ % 16) throw std::invalid_argument("moe expert_ffn_dim must be a positive multiple of 16");
-    if (E_ > 4096) throw std::invalid_argument("at most 4096 experts");
+    if (E_ > 512) throw std::invalid_argument("at most 512 experts (register-resident routing)");
   }
   if (!attn_only_) {
     const bool shared_ok = moe_ && F_ == 0;  // MoE without a shared expert
@@ -187,6 +190,10 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
     if ((q_per_slot_ * AD_) % kvp_ || slice_ % 16)
       throw std::invalid_argument("distributed Helix needs hidden/(tpa*kvp) to be a multiple of 16");
     xchunk_ = static_cast<int>(exchange_layout(q_per_slot_, AD_, kvp_, nullptr));
+    if (mla_) {
+      uv_heads_ = static_cast<int>(Qh_ / kvp_);
+      uv_h0_ = r_ * uv_heads_;
+    }
     if (!attn_only_) {
       if (F_ % N_ || (F_ > 0 && (F_ / N_) % 16))
         throw std::invalid_argument("ffn_dim/(tpa*kvp) must be a multiple of 16");
@@ -194,6 +201,11 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
       V_local_ = static_cast<int>((V_ + N_ - 1) / N_);
     }
   }
+  if (mla_ && dist_mode_ == HX_POOL_LOCAL) uv_heads_ = static_cast<int>(Qh_);
+  // O-projection input: GQA the merged heads (all, or this rank's exchanged slice);
+  // MLA the W_UV outputs of the heads held here (H, or H/N)
+  K_o_ = mla_ ? uv_heads_ * static_cast<int>(D_)
+              : (dist_mode_ == HX_POOL_LOCAL ? static_cast<int>(Qh_) * AD_ : slice_);
   const int64_t per_rank_max = ((cap_ + static_cast<int64_t>(chunk_) * kvp_ - 1) /
                                 (static_cast<int64_t>(chunk_) * kvp_)) * chunk_;
   if (mla_) {
@@ -242,6 +254,9 @@ Engine::~Engine() {
   for (auto* p : w_egu_) f(p);
   for (auto* p : w_edown_) f(p);
   f(d_qimg_);
+  f(d_att_);
+  for (auto* p : w_uk_) f(p);
+  for (auto* p : w_uv_) f(p);
   f(d_rlog_); f(d_route_w_); f(d_gids_); f(d_gcount_); f(d_xf_em_); f(d_moe_y_);
   f(w_lm_); f(emb_); f(d_total_); f(d_q_); f(d_part_o_); f(d_part_lse_); f(d_work_);
   f(d_frag_o_); f(d_frag_lse_); f(d_ypart_); f(d_counters_); f(d_x_); f(d_ss_); f(d_m_);
@@ -296,6 +311,8 @@ void Engine::alloc() {
     splits_req_ = mla_splits(req_streams);
     n_items_ = std::max(n_streams_ * splits_, req_streams * splits_req_);
     d_qimg_ = dalloc<uint8_t>(static_cast<size_t>(B_) * mla_q_bytes(), "mla query images");
+    d_att_ = dalloc<float>(static_cast<size_t>(B_) * (dist_mode_ == HX_POOL_LOCAL ? Qh_ * DV_ : slice_),
+                           "mla merged latent output");
   } else {
     splits_ = splits_for(n_streams_);
     splits_req_ = splits_for(req_streams);
@@ -337,11 +354,15 @@ void Engine::plan_gemvs() {
     p.batch = B_;
     // Persistent GEMV: tiles = (128-row block, k-chunk of kr k-steps) pulled
     // from a queue by one CTA per SM. kr shrinks until there are >= 4 tiles per
-    // SM (dynamic balance, <= one short tile of tail); kr >= 8 keeps a tile >= 32 KB.
+    // SM (dynamic balance, <= one short tile of tail); kr >= 8 keeps a tile >= 32 KB,
+    // and <= 32 k-chunks keep the epilogue's split-K sum short for narrow outputs
+    // (router, sharded LM head: a few row blocks over a long K).
     const int kst = K / 16;
     const int nblk = Npad / 128;
     int kr = std::min(64, kst);
-    while (kr > 8 && static_cast<int64_t>(nblk) * groups * ((kst + kr - 1) / kr) < 4 * num_sms_) kr /= 2;
+    while (kr > 8 && (kst + kr / 2 - 1) / (kr / 2) <= 32 &&
+           static_cast<int64_t>(nblk) * groups * ((kst + kr - 1) / kr) < 4 * num_sms_)
+      kr /= 2;
     const int ksplit = (kst + kr - 1) / kr;
     p.ksplit = ksplit;
     p.kr_steps = kr;
@@ -358,19 +379,17 @@ void Engine::plan_gemvs() {
     return g;
   };
   const bool dist = dist_mode_ != HX_POOL_LOCAL;
-  // MLA: absorbed q for every head (W wide) + one latent row (types.hpp:43-49)
-  const int qw = mla_ ? W_ : static_cast<int>(D_);
-  const int nq = static_cast<int>((dist ? q_per_slot_ : Qh_) * qw);
+  // MLA: q (head_size per head, absorbed into the latent by mla_absorb_q) + one latent row
+  const int nq = static_cast<int>((dist ? q_per_slot_ : Qh_) * D_);
   const int nk = mla_ ? W_ : static_cast<int>((dist ? kvh_per_slot_ : Kh_) * D_);
   const int Nqkv = nq + (mla_ ? 1 : 2) * nk;
   const int Hh = static_cast<int>(H_);
-  const int AW = static_cast<int>(Qh_) * AD_;  // merged attention width (GQA: = H)
   const int F = F_local_;
   for (int64_t l = 0; l < L_; ++l) {
     GemvPlan q = make(Nqkv, round_up(Nqkv, 128), Hh, attn_only_ ? 0 : 1, E_QKV);
     q.p.nq = nq;
     q.p.nk = nk;
-    q.p.kv_heads = nk / qw;
+    q.p.kv_heads = mla_ ? 1 : nk / static_cast<int>(D_);
     q.p.mla = mla_ ? 1 : 0;
     q.p.kv_head_base = dist ? grp_ * kvh_per_slot_ : 0;
     q.p.kvh_per_slot = kvh_per_slot_;
@@ -379,14 +398,13 @@ void Engine::plan_gemvs() {
     q.p.slot_base = slot_base_;
     q.p.n_local_slots = n_slots_;
     q.p.append = 1;
-    if (mla_) q.p.head_dim = W_;
     plan_qkv_.push_back(q);
     if (!attn_only_) {
       if (dist) {
         // O-proj: this rank's exchanged slice of its group's heads x its rows of W_O
-        plan_o_.push_back(make(Hh, round_up(Hh, 128), slice_, 0, E_STORE));
+        plan_o_.push_back(make(Hh, round_up(Hh, 128), K_o_, 0, E_STORE));
       } else {
-        plan_o_.push_back(make(Hh, round_up(Hh, 128), AW, 0, E_RESID));
+        plan_o_.push_back(make(Hh, round_up(Hh, 128), K_o_, 0, E_RESID));
       }
       if (F > 0) {  // dense FFN, or the MoE shared expert
         plan_gu_.push_back(make(2 * F, round_up(F, 64) * 2, Hh, 1, E_SWIGLU));
@@ -439,7 +457,7 @@ void Engine::plan_gemvs() {
     const int nb8 = xf_nb8(B_);
     auto xf_alloc = [&](int K) { return dalloc<uint8_t>(static_cast<size_t>(K / 16) * 3 * nb8 * 256, "xf"); };
     d_xf_resid_ = xf_alloc(static_cast<int>(H_));
-    d_xf_attn_ = xf_alloc(dist ? slice_ : AW);
+    d_xf_attn_ = xf_alloc(K_o_);
     d_xf_m_ = xf_alloc(std::max(16, F_local_));
   }
   d_counters_ = dalloc<int>(static_cast<size_t>(max_counters_), "counters");
@@ -456,9 +474,9 @@ void Engine::plan_gemvs() {
   if (attn_only_)
     kernels_per_step_ = 6;  // xprep, qkv x2, attention, split-reduce, merge(+bump)
   else if (!dist)
-    kernels_per_step_ = 1 + (7 + ffn_k) * L_ + 3;
+    kernels_per_step_ = 1 + (7 + ffn_k + (mla_ ? 2 : 0)) * L_ + 3;  // MLA: + absorb_q, uv
   else  // + pack and two residual adds per layer; per-request attention launches under HOP-B
-    kernels_per_step_ = 1 + L_ * (9 + ffn_k + (hopb_ ? 3 * (B_ - 1) : 0)) + 3;
+    kernels_per_step_ = 1 + L_ * (9 + ffn_k + (mla_ ? 2 : 0) + (hopb_ ? 3 * (B_ - 1) : 0)) + 3;
 }
 
 // ---------------------------------------------------------------------------
@@ -488,11 +506,21 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
   const int Qall = static_cast<int>(Qh_ * D_), Kall = static_cast<int>(Kh_ * D_);
   for (int64_t l = 0; l < L_; ++l) {
     if (w_qkv_.size() <= static_cast<size_t>(l)) w_qkv_.push_back(walloc(plan_qkv_[l]));
-    if (mla_) {  // absorbed W_q (kWq, 8/sqrt(H)) and the latent down-projection (kWk, 1/sqrt(H))
-      const int nqm = static_cast<int>(Qh_) * W_;
+    if (mla_) {  // W_q [H x Q*Hsz] (kWq) and the latent down-projection (kWk), both 1/sqrt(H)
       init(w_qkv_[l], plan_qkv_[l],
-           {{hash_stream(kWq, l), 0, nqm, nqm, 0, 0, 8.0 / std::sqrt(static_cast<double>(H_)), 0, 0},
-            {hash_stream(kWk, l), nqm, nqm + W_, W_, 0, 0, sh, 0, 0}});
+           {{hash_stream(kWq, l), 0, nq, nq, 0, 0, sh, 0, 0},
+            {hash_stream(kWk, l), nq, nq + W_, W_, 0, 0, sh, 0, 0}});
+      // per-head absorptions: W_UK for every head, W_UV for the heads held here
+      const long long uk = Qh_ * D_ * W_, uv = static_cast<long long>(uv_heads_) * DV_ * D_;
+      if (w_uk_.size() <= static_cast<size_t>(l)) {
+        w_uk_.push_back(dalloc<uint16_t>(static_cast<size_t>(uk), "w_uk"));
+        w_uv_.push_back(dalloc<uint16_t>(static_cast<size_t>(uv), "w_uv"));
+      }
+      cuda_check(launch_plain_init_hash(w_uk_[l], uk, seed, hash_stream(kWuk, l), 0,
+                                        16.0 / std::sqrt(static_cast<double>(D_)), stream_), "w_uk init");
+      cuda_check(launch_plain_init_hash(w_uv_[l], uv, seed, hash_stream(kWuv, l),
+                                        static_cast<long long>(uv_h0_) * DV_ * D_,
+                                        1.0 / std::sqrt(static_cast<double>(DV_)), stream_), "w_uv init");
     } else if (qkv_hash) {
       init(w_qkv_[l], plan_qkv_[l],
            {{hash_stream(kWq, l), 0, nq, Qall, q0, 0, 1.0, 0, 0},
@@ -509,9 +537,9 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
         }
       }
       // O-proj input rows: this rank's slice of its group's flattened heads
-      const int ko = dist ? grp_ * q_per_slot_ * AD_ + r_ * slice_ : 0;
-      const double so = mla_ ? 1.0 / std::sqrt(static_cast<double>(Qh_ * AD_)) : sh;  // MLA: W_o is [Q*DV x H]
-      init(w_o_[l], plan_o_[l], {{hash_stream(kWo, l), 0, Hh, Hh, 0, 0, so, ko, 0}});
+      // (MLA: the rows of the W_UV outputs of this rank's heads)
+      const int ko = !dist ? 0 : (mla_ ? uv_h0_ * static_cast<int>(D_) : grp_ * q_per_slot_ * AD_ + r_ * slice_);
+      init(w_o_[l], plan_o_[l], {{hash_stream(kWo, l), 0, Hh, Hh, 0, 0, sh, ko, 0}});
       plan_o_[l].p.w = w_o_[l];
       if (F > 0) {
         init(w_gu_[l], plan_gu_[l],
@@ -945,6 +973,10 @@ void Engine::enqueue_attention(int64_t layer) {
   //    round-robin append of this token's K/V
   const GemvPlan& q = plan_qkv_[layer];
   cuda_check(launch_gemv(q.p, q.xmode, E_QKV, num_sms_, stream_), "qkv gemv");
+  if (mla_)  // W_UK absorption: q heads -> the 576-wide latent query image
+    cuda_check(launch_mla_absorb_q(d_q_, w_uk_[layer], B_, static_cast<int>(Qh_), static_cast<int>(D_), DP_,
+                                   d_qimg_, stream_),
+               "mla absorb q");
   mark(1);
   if (dist_mode_ != HX_POOL_LOCAL) {
     enqueue_exchange_and_attention_dist(layer);
@@ -1042,8 +1074,12 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
       // LSE-rescale combine of the KVP fragments -> O-proj activations (attention.hpp:118-175)
       // (a fused split+KVP merge kernel measured 0.2 ms/step slower than this pair)
       cuda_check(launch_xprep_merge_local(d_frag_o_, d_frag_lse_, B_, q_per_slot_, kvp_, AD_, ADP_,
-                                          static_cast<int>(Qh_) * AD_, d_xf_attn_, d_total_ + l * B_, stream_),
+                                          static_cast<int>(Qh_) * AD_, d_xf_attn_, d_total_ + l * B_, stream_,
+                                          mla_ ? d_att_ : nullptr),
                  "merge");
+      if (mla_)
+        cuda_check(launch_mla_uv(d_att_, w_uv_[l], B_, uv_heads_, static_cast<int>(D_), d_xf_attn_, stream_),
+                   "mla uv");
       cuda_check(launch_gemv(plan_o_[l].p, 0, E_RESID, num_sms_, stream_), "o-proj");
       mark(4);
       enqueue_ffn(l);
@@ -1051,8 +1087,11 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
       // merge of the exchanged slices, then TP O-proj over this rank's slice and
       // AllReduce over the pool (latency.cpp:85-94)
       cuda_check(launch_xprep_merge_recv(d_recv_, B_, kvp_, xchunk_, slice_, r_, AD_, d_xf_attn_,
-                                         d_total_ + l * B_, stream_),
+                                         d_total_ + l * B_, stream_, mla_ ? d_att_ : nullptr),
                  "merge");
+      if (mla_)
+        cuda_check(launch_mla_uv(d_att_, w_uv_[l], B_, uv_heads_, static_cast<int>(D_), d_xf_attn_, stream_),
+                   "mla uv");
       cuda_check(launch_gemv(plan_o_[l].p, 0, E_STORE, num_sms_, stream_), "o-proj");
       mark(4);
       if (!(skip_comm_ & 2)) transport_->all_reduce_sum(d_parth_, static_cast<size_t>(B_) * H_, stream_);
@@ -1215,6 +1254,7 @@ void Engine::info(hx_engine_info* o) const {
   std::memset(o, 0, sizeof(*o));
   o->kv_bytes_per_layer = static_cast<int64_t>(n_slots_) * B_ * kvh_per_slot_ * page_cap_ * page_bytes_;
   int64_t wb = static_cast<int64_t>(plan_qkv_[0].p.Npad) * plan_qkv_[0].p.K * 2;
+  if (mla_) wb += (Qh_ * D_ * W_ + static_cast<int64_t>(uv_heads_) * DV_ * D_) * 2;  // W_UK + W_UV
   auto bytes = [](const GemvPlan& g) { return static_cast<int64_t>(g.p.Npad) * g.p.K * 2; };
   if (!attn_only_) {
     wb += bytes(plan_o_[0]);

@@ -184,6 +184,12 @@ class Engine {
   bool mla_ = false;
   int W_ = 0, DV_ = 0;           // latent width (576) and value width (512)
   int AD_ = 0, ADP_ = 0;         // attention output width per head and its padded stride
+  // MLA weight absorption (layer_oracle.hpp): W_UK [Q][Hsz][576] per layer (all heads),
+  // W_UV [uv_heads][512][Hsz] per layer (the heads whose O-projection rows are held here)
+  std::vector<uint16_t*> w_uk_, w_uv_;
+  float* d_att_ = nullptr;       // MLA merged latent attention output [B][Q*512 or slice]
+  int uv_heads_ = 0, uv_h0_ = 0;
+  int K_o_ = 0;                  // O-projection input width on this device
   uint8_t* d_qimg_ = nullptr;    // [B] bf16 absorbed-query images
   struct alignas(64) MlaTmaps {  // CUtensorMap x 2 per layer over the latent pool
     unsigned char s[128], v[128];

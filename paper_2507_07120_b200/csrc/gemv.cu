@@ -318,15 +318,12 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
     } else if (EM == E_LOGITS) {
       if (p.out) p.out[static_cast<size_t>(b) * p.out_stride + n] = y[0];
       atomicMax(&s_best[b], logit_key(y[0], n + p.n_offset));
-    } else if (EM == E_QKV && p.mla) {
-      // MLA: absorbed q -> bf16 query image (the tcgen05 A operand); latent -> page
-      if (n < p.nq) {
-        const int head = n / p.head_dim, d = n - head * p.head_dim;
-        *reinterpret_cast<__nv_bfloat16*>(p.q_img + static_cast<size_t>(b) * mla_q_bytes() + mla_q_offset(head, d)) =
-            __float2bfloat16_rn(y[0]);
-      } else {
+    } else if (EM == E_QKV && p.mla && n >= p.nq) {
+      // MLA latent row -> its round-robin page (q heads: the GQA branch below,
+      // then mla_absorb_q_kernel builds the tcgen05 query image)
+      {
         const int d = n - p.nq;
-        if (p.kv_dbg) p.kv_dbg[static_cast<size_t>(b) * 2 * p.head_dim + d] = y[0];
+        if (p.kv_dbg) p.kv_dbg[static_cast<size_t>(b) * 2 * kMlaW + d] = y[0];
         if (p.append) {
           const int slot_local = static_cast<int>(s_pos[b][0]) - p.slot_base;
           const long long row = s_pos[b][1];

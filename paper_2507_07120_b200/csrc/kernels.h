@@ -65,6 +65,14 @@ cudaError_t launch_mla_decode(const AttnParams& p, int grid, cudaStream_t stream
 // Encode the two tensor maps for a latent pool of `bytes` bytes (multiple of 2 KB).
 cudaError_t make_mla_tensor_maps(const void* pool, size_t bytes, void* tm_s, void* tm_v);
 cudaError_t launch_mla_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse, cudaStream_t stream);
+// MLA weight absorption (layer_oracle.hpp): q image = bf16(n_h . Wuk_h) from the
+// QKV epilogue's n [B][Q][dp] and wuk [Q][hs][576]; v = o_h . Wuv_h from the merged
+// latent output att [B][n_heads*512] and wuv [n_heads][512][hs] -> x-fragments of
+// v [B][n_heads*hs] for the O-projection.
+cudaError_t launch_mla_absorb_q(const float* n, const uint16_t* wuk, int batch, int q_heads, int hs, int dp,
+                                uint8_t* qimg, cudaStream_t stream);
+cudaError_t launch_mla_uv(const float* att, const uint16_t* wuv, int batch, int n_heads, int hs, uint8_t* xf,
+                          cudaStream_t stream);
 cudaError_t launch_kv_fill_hash_mla(uint8_t* kv, int* total, int batch, int kvp, int chunk, int page_cap,
                                     int slot_base, int n_local_slots, long long n, uint64_t seed, uint64_t stream_k,
                                     cudaStream_t stream);
@@ -133,11 +141,13 @@ cudaError_t launch_xprep_plain(const float* x, int batch, int K, int x_stride, u
 //  exchanged:  recv [kvp src][B][chunk] (slice + lse slots); K = slice of rank exch_rank
 // Both also bump the layer's per-request token totals (bump_total may be null):
 // the attention has read them, so the token appended by the QKV epilogue now counts.
+// plain != null: write the merged output as fp32 [B][K] there instead of x-fragments.
 cudaError_t launch_xprep_merge_local(const float* frag_o, const float* frag_lse, int batch, int q_per_slot,
                                      int kvp, int head_dim, int dp, int K, uint8_t* xf, int* bump_total,
-                                     cudaStream_t s);
+                                     cudaStream_t s, float* plain = nullptr);
 cudaError_t launch_xprep_merge_recv(const float* recv, int batch, int kvp, int chunk, int slice, int exch_rank,
-                                    int head_dim, uint8_t* xf, int* bump_total, cudaStream_t s);
+                                    int head_dim, uint8_t* xf, int* bump_total, cudaStream_t s,
+                                    float* plain = nullptr);
 
 // ---------------------------------------------------------------- misc
 cudaError_t launch_merge_out(const float* frag_o, const float* frag_lse, int batch, int q_heads,
@@ -176,6 +186,9 @@ cudaError_t launch_weight_init_hash(uint4* w, int Npad, int K, const WSeg* segs,
                                     uint64_t seed, cudaStream_t stream);
 cudaError_t launch_emb_init_hash(uint16_t* emb, int vocab, int hidden, uint64_t seed,
                                  uint64_t stream_id, cudaStream_t stream);
+// Plain row-major bf16: w[i] = bf16(hash_unit(seed, stream_id, idx0 + i) * scale), i < n.
+cudaError_t launch_plain_init_hash(uint16_t* w, long long n, uint64_t seed, uint64_t stream_id, long long idx0,
+                                   double scale, cudaStream_t stream);
 cudaError_t launch_fill_zero(void* p, size_t bytes, cudaStream_t stream);
 // Distributed Helix exchange: pack this rank's fragment into per-destination
 // slices [kvp][batch][chunk] (chunk = slice + lse slots) for requests

@@ -335,19 +335,24 @@ cudaError_t launch_weight_init_hash(uint4* w, int Npad, int K, const WSeg* segs,
   return cudaGetLastError();
 }
 
-__global__ void emb_init_hash_kernel(__nv_bfloat16* emb, int vocab, int hidden, uint64_t seed,
-                                     uint64_t stream_id) {
+// Plain row-major bf16 array: w[i] = bf16(hash_unit(seed, stream, idx0 + i) * scale).
+__global__ void plain_init_hash_kernel(__nv_bfloat16* w, long long n, uint64_t seed, uint64_t stream_id,
+                                       long long idx0, double scale) {
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (idx >= static_cast<long long>(vocab) * hidden) return;
-  emb[idx] = double_to_bf16_rne(hash_unit(seed, stream_id, static_cast<uint64_t>(idx)));
+  if (idx >= n) return;
+  w[idx] = double_to_bf16_rne(hash_unit(seed, stream_id, static_cast<uint64_t>(idx0 + idx)) * scale);
+}
+
+cudaError_t launch_plain_init_hash(uint16_t* w, long long n, uint64_t seed, uint64_t stream_id, long long idx0,
+                                   double scale, cudaStream_t stream) {
+  plain_init_hash_kernel<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream>>>(
+      reinterpret_cast<__nv_bfloat16*>(w), n, seed, stream_id, idx0, scale);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_emb_init_hash(uint16_t* emb, int vocab, int hidden, uint64_t seed,
                                  uint64_t stream_id, cudaStream_t stream) {
-  const long long work = static_cast<long long>(vocab) * hidden;
-  emb_init_hash_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(
-      reinterpret_cast<__nv_bfloat16*>(emb), vocab, hidden, seed, stream_id);
-  return cudaGetLastError();
+  return launch_plain_init_hash(emb, static_cast<long long>(vocab) * hidden, seed, stream_id, 0, 1.0, stream);
 }
 
 cudaError_t launch_fill_zero(void* p, size_t bytes, cudaStream_t stream) {
@@ -468,7 +473,8 @@ cudaError_t launch_xprep_plain(const float* x, int batch, int K, int x_stride, u
 
 
 __global__ void xprep_merge_local_kernel(const float* frag_o, const float* frag_lse, int batch, int q_per_slot,
-                                         int kvp, int head_dim, int dp, int K, uint8_t* xf, int* bump_total) {
+                                         int kvp, int head_dim, int dp, int K, uint8_t* xf, int* bump_total,
+                                         float* plain) {
   griddep_wait();
   griddep_launch_dependents();
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -487,18 +493,22 @@ __global__ void xprep_merge_local_kernel(const float* frag_o, const float* frag_
       o[r] = frag_o[f * dp + d];
     }
   }
-  xf_write(xf, xf_nb8(batch), b, k, merge_sources(lse, o, kvp));
+  const float v = merge_sources(lse, o, kvp);
+  if (plain)
+    plain[i] = v;
+  else
+    xf_write(xf, xf_nb8(batch), b, k, v);
 }
 cudaError_t launch_xprep_merge_local(const float* frag_o, const float* frag_lse, int batch, int q_per_slot,
                                      int kvp, int head_dim, int dp, int K, uint8_t* xf, int* bump_total,
-                                     cudaStream_t s) {
+                                     cudaStream_t s, float* plain) {
   const long long n = static_cast<long long>(batch) * K;
   return launch_k(xprep_merge_local_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, frag_o,
-                  frag_lse, batch, q_per_slot, kvp, head_dim, dp, K, xf, bump_total);
+                  frag_lse, batch, q_per_slot, kvp, head_dim, dp, K, xf, bump_total, plain);
 }
 
 __global__ void xprep_merge_recv_kernel(const float* recv, int batch, int kvp, int chunk, int slice, int exch_rank,
-                                        int head_dim, uint8_t* xf, int* bump_total) {
+                                        int head_dim, uint8_t* xf, int* bump_total, float* plain) {
   griddep_wait();
   griddep_launch_dependents();
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -516,18 +526,27 @@ __global__ void xprep_merge_recv_kernel(const float* recv, int batch, int kvp, i
       o[r] = src[k];
     }
   }
-  xf_write(xf, xf_nb8(batch), b, k, merge_sources(lse, o, kvp));
+  const float v = merge_sources(lse, o, kvp);
+  if (plain)
+    plain[i] = v;
+  else
+    xf_write(xf, xf_nb8(batch), b, k, v);
 }
 cudaError_t launch_xprep_merge_recv(const float* recv, int batch, int kvp, int chunk, int slice, int exch_rank,
-                                    int head_dim, uint8_t* xf, int* bump_total, cudaStream_t s) {
+                                    int head_dim, uint8_t* xf, int* bump_total, cudaStream_t s, float* plain) {
   const long long n = static_cast<long long>(batch) * slice;
   return launch_k(xprep_merge_recv_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, recv,
-                  batch, kvp, chunk, slice, exch_rank, head_dim, xf, bump_total);
+                  batch, kvp, chunk, slice, exch_rank, head_dim, xf, bump_total, plain);
 }
 }  // namespace hx
 
 // ---------------------------------------------------------------- MoE routing
 namespace hx {
+// One warp per request: its logits live in registers (lane holds experts
+// lane, lane+32, ...; E <= 32 * kRouteSlots), k rounds of warp argmax (ties: lower
+// index) knock the winner out in place; softmax over the selected; then warp 0
+// compacts the ascending list of active local experts with ballots.
+constexpr int kRouteSlots = 16;
 __global__ void moe_route_kernel(const float* logits, int batch, int n_experts, int top_k, int e_begin, int e_end,
                                  float* route_w, int* group_ids, int* group_count) {
   griddep_wait();
@@ -539,18 +558,22 @@ __global__ void moe_route_kernel(const float* logits, int batch, int n_experts, 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   for (int b = warp; b < batch; b += nw) {
     const float* r = logits + static_cast<size_t>(b) * n_experts;
-    float sel_v[16];
-    int sel_i[16];
+    float v[kRouteSlots];
+#pragma unroll
+    for (int i = 0; i < kRouteSlots; ++i) {
+      const int e = lane + 32 * i;
+      v[i] = e < n_experts ? r[e] : -INFINITY;
+    }
+    float sel_v = 0.f, top = 0.f, z = 0.f;
+    int sel_i = 0;
     for (int k = 0; k < top_k; ++k) {
-      // warp argmax over experts not yet selected (ties: lower index)
       float bv = -INFINITY;
       int bi = 0x7fffffff;
-      for (int e = lane; e < n_experts; e += 32) {
-        bool taken = false;
-        for (int j = 0; j < k; ++j) taken |= sel_i[j] == e;
-        const float v = r[e];
-        if (!taken && (v > bv || (v == bv && e < bi))) {
-          bv = v;
+#pragma unroll
+      for (int i = 0; i < kRouteSlots; ++i) {
+        const int e = lane + 32 * i;
+        if (e < n_experts && (v[i] > bv || (v[i] == bv && e < bi))) {
+          bv = v[i];
           bi = e;
         }
       }
@@ -563,30 +586,39 @@ __global__ void moe_route_kernel(const float* logits, int batch, int n_experts, 
           bi = oi;
         }
       }
-      sel_v[k] = bv;
-      sel_i[k] = bi;
-    }
-    if (lane == 0) {
-      const float m = sel_v[0];
-      float z = 0.f;
-      for (int k = 0; k < top_k; ++k) z += expf(sel_v[k] - m);
-      for (int k = 0; k < top_k; ++k) {
-        route_w[static_cast<size_t>(b) * n_experts + sel_i[k]] = expf(sel_v[k] - m) / z;
-        s_flag[sel_i[k]] = 1;
+      if ((bi & 31) == lane) {  // knock the winner out (its owning lane, static slot index)
+#pragma unroll
+        for (int i = 0; i < kRouteSlots; ++i)
+          if (i == (bi >> 5)) v[i] = -INFINITY;
       }
+      if (k == 0) top = bv;
+      z += expf(bv - top);  // same order as the oracle's sum over the selected
+      if (lane == k) {      // lane k keeps the k-th selection
+        sel_v = bv;
+        sel_i = bi;
+      }
+    }
+    if (lane < top_k) {
+      route_w[static_cast<size_t>(b) * n_experts + sel_i] = expf(sel_v - top) / z;
+      s_flag[sel_i] = 1;
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {  // ascending list of active local experts
+  if (warp == 0) {  // ascending list of active local experts
     int c = 0;
-    for (int e = e_begin; e < e_end; ++e)
-      if (s_flag[e]) group_ids[c++] = e;
-    *group_count = c;
+    for (int e0 = e_begin; e0 < e_end; e0 += 32) {
+      const int e = e0 + lane;
+      const bool on = e < e_end && s_flag[e];
+      const unsigned m = __ballot_sync(0xffffffffu, on);
+      if (on) group_ids[c + __popc(m & ((1u << lane) - 1u))] = e;
+      c += __popc(m);
+    }
+    if (lane == 0) *group_count = c;
   }
 }
 cudaError_t launch_moe_route(const float* logits, int batch, int n_experts, int top_k, int e_begin, int e_end,
                              float* route_w, int* group_ids, int* group_count, cudaStream_t s) {
-  if (top_k > 16) return cudaErrorInvalidValue;
+  if (top_k > 16 || n_experts > 32 * kRouteSlots) return cudaErrorInvalidValue;
   return launch_k(moe_route_kernel, dim3(1), dim3(512), static_cast<size_t>(n_experts) * sizeof(int), s, logits,
                   batch, n_experts, top_k, e_begin, e_end, route_w, group_ids, group_count);
 }

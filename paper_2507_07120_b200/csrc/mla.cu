@@ -47,6 +47,7 @@
 #include "kernels.h"
 #include "kv_layout.cuh"
 #include "tc05.cuh"
+#include "xfrag.cuh"
 
 namespace hx {
 
@@ -662,6 +663,150 @@ cudaError_t launch_kv_fill_hash_mla(uint8_t* kv, int* total, int batch, int kvp,
         kv, total, batch, kvp, chunk, page_cap, slot_base, n_local_slots, n, seed, stream_k);
   add_total_mla_kernel<<<1, 64, 0, stream>>>(total, batch, static_cast<int>(n));
   return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------
+// Decode-time weight absorption around the latent attention (layer_oracle.hpp):
+// the QKV GEMV streams the reference-shaped W_q [H x Q*Hsz] (roofline.hpp:17-48),
+// these two small per-head products turn its output into the 576-wide latent
+// query and the 512-wide latent attention output back into head_size values.
+
+// One per-head product out[b][h][j] = sum_d in[b][h][d] * W[h][d][j] (d < din,
+// j < dout), used twice:
+//   ABSORB: in = n [B][Q][dp] (QKV epilogue), W = W_UK [Q][hs][576], out -> bf16 q image;
+//   UV:     in = att [B][nh*512] (merged latent output), W = W_UV [nh][512][hs],
+//           out -> x-fragments of v [B][nh*hs] (the O-projection's K operand).
+// Grid (head, column chunk); thread = (8-column group, d-slice): one 16-byte
+// weight load per d feeds 8 requests x 8 columns of FMAs, eight loads in flight
+// per thread; the DS d-slice partials are summed in slice order (deterministic).
+// Requests in passes of 8, staged in shared memory as [d][8].
+template <bool ABSORB, int DS>
+__global__ void __launch_bounds__(512) mla_head_gemm_kernel(const float* in, int in_head_stride, int in_row_stride,
+                                                             const __nv_bfloat16* w, int din, int dout, int batch,
+                                                             uint8_t* out) {
+  constexpr int NB = 8;
+  extern __shared__ __align__(16) float hsm[];
+  float* s_in = hsm;                    // [din][NB]
+  const int cols = dout / gridDim.y, c0 = blockIdx.y * cols;
+  float* red = hsm + din * NB;          // [DS][NB][cols]
+  const int h = blockIdx.x;
+  const int groups = cols / 8;
+  const int cg = threadIdx.x % groups, ds = threadIdx.x / groups;
+  const int dper = din / DS, d0 = ds * dper;
+  const __nv_bfloat16* wh = w + static_cast<size_t>(h) * din * dout + c0 + cg * 8;
+  griddep_wait();
+  griddep_launch_dependents();
+  for (int bc = 0; bc < batch; bc += NB) {
+    const int nb = min(NB, batch - bc);
+    // stage the inputs: 8 independent loads per thread in flight before any store
+    for (int i0 = threadIdx.x; i0 < NB * din; i0 += 8 * blockDim.x) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * blockDim.x;
+        const int b = i / din, d = i - b * din;
+        v[u] = (i < NB * din && b < nb)
+                   ? in[static_cast<size_t>(bc + b) * in_row_stride + static_cast<size_t>(h) * in_head_stride + d]
+                   : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < NB * din) s_in[(i % din) * NB + i / din] = v[u];
+      }
+    }
+    __syncthreads();
+    if (ds < DS) {
+      float acc[NB][8];
+#pragma unroll
+      for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) acc[b][c] = 0.f;
+      for (int dc = d0; dc < d0 + dper; dc += 8) {
+        uint4 wv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          wv[u] = dc + u < d0 + dper ? __ldg(reinterpret_cast<const uint4*>(wh + static_cast<size_t>(dc + u) * dout))
+                                     : make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (dc + u >= d0 + dper) break;
+          float wf[8];
+          const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&wv[u]);
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            wf[2 * c] = __low2float(w2[c]);
+            wf[2 * c + 1] = __high2float(w2[c]);
+          }
+          const float4* x4 = reinterpret_cast<const float4*>(s_in + (dc + u) * NB);
+#pragma unroll
+          for (int b4 = 0; b4 < NB / 4; ++b4) {
+            const float4 x = x4[b4];
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              acc[4 * b4 + 0][c] += x.x * wf[c];
+              acc[4 * b4 + 1][c] += x.y * wf[c];
+              acc[4 * b4 + 2][c] += x.z * wf[c];
+              acc[4 * b4 + 3][c] += x.w * wf[c];
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int b = 0; b < NB; ++b) {
+        float4* r4 = reinterpret_cast<float4*>(red + (static_cast<size_t>(ds) * NB + b) * cols + cg * 8);
+        r4[0] = make_float4(acc[b][0], acc[b][1], acc[b][2], acc[b][3]);
+        r4[1] = make_float4(acc[b][4], acc[b][5], acc[b][6], acc[b][7]);
+      }
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < nb * cols; e += blockDim.x) {
+      const int b = e / cols, jc = e - b * cols, jj = c0 + jc;
+      float v = 0.f;
+#pragma unroll
+      for (int s = 0; s < DS; ++s) v += red[(s * NB + b) * cols + jc];
+      if (ABSORB)
+        *reinterpret_cast<__nv_bfloat16*>(out + static_cast<size_t>(bc + b) * mla_q_bytes() + mla_q_offset(h, jj)) =
+            __float2bfloat16_rn(v);
+      else
+        xf_write(out, xf_nb8(batch), bc + b, h * dout + jj, v);
+    }
+    __syncthreads();
+  }
+}
+
+template <bool ABSORB, int DS>
+static cudaError_t launch_head_gemm_t(const float* in, int in_head_stride, int in_row_stride, const uint16_t* w,
+                                      int din, int dout, int batch, int heads, int col_chunks, uint8_t* out,
+                                      cudaStream_t stream) {
+  while (col_chunks > 1 && dout % (8 * col_chunks)) --col_chunks;
+  const int cols = dout / col_chunks;
+  if (cols % 8 || din % DS || (cols / 8) * DS > 512) return cudaErrorInvalidValue;
+  const size_t smem = (static_cast<size_t>(din) * 8 + static_cast<size_t>(DS) * 8 * cols) * sizeof(float);
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(mla_head_gemm_kernel<ABSORB, DS>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = smem;
+  }
+  const int threads = (cols / 8) * DS;
+  return launch_k(mla_head_gemm_kernel<ABSORB, DS>, dim3(heads, col_chunks), dim3((threads + 31) / 32 * 32), smem,
+                  stream, in,
+                  in_head_stride, in_row_stride, reinterpret_cast<const __nv_bfloat16*>(w), din, dout, batch, out);
+}
+
+cudaError_t launch_mla_absorb_q(const float* n, const uint16_t* wuk, int batch, int q_heads, int hs, int dp,
+                                uint8_t* qimg, cudaStream_t stream) {
+  if (hs > 128) return cudaErrorInvalidValue;  // 3 chunks of 24 column groups x 8 d-slices
+  return launch_head_gemm_t<true, 8>(n, dp, q_heads * dp, wuk, hs, kMlaW, batch, q_heads, 3, qimg, stream);
+}
+
+cudaError_t launch_mla_uv(const float* att, const uint16_t* wuv, int batch, int n_heads, int hs, uint8_t* xf,
+                          cudaStream_t stream) {
+  if (hs > 128) return cudaErrorInvalidValue;  // 4 chunks of hs/32 column groups x 32 d-slices of 16
+  return launch_head_gemm_t<false, 32>(att, kMlaDV, n_heads * kMlaDV, wuv, kMlaDV, hs, batch, n_heads, 4, xf,
+                                       stream);
 }
 
 }  // namespace hx
