@@ -342,74 +342,94 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
 }
 
 // ------------------------------------------------------------------------
-// Split reduce: merge a stream's split partials (in split order) into the
-// rank's fragment for each query head, natural-log lse (HeadFragment,
-// attention.hpp:56-59; empty shard -> (0, -inf) as at :69-70).
+// Split reduce: merge a stream's split partials into the rank's fragment for
+// each query head, natural-log lse (HeadFragment, attention.hpp:56-59; empty
+// shard -> (0, -inf) as at :69-70). One CTA per (stream, query row): warp w
+// takes splits w, w+8, ... in order (all its loads in flight together), the 8
+// warp partials are combined in warp order -- deterministic, one load round.
+constexpr int kSrWarps = 8;
 template <int DP>
-__global__ void attn_split_reduce_kernel(const AttnParams p, float* frag_o, float* frag_lse) {
+__global__ void __launch_bounds__(kSrWarps * 32) attn_split_reduce_kernel(const AttnParams p, float* frag_o,
+                                                                          float* frag_lse) {
   griddep_wait();
   griddep_launch_dependents();
-  const int warp_global = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
+  __shared__ float s_m[kSrWarps], s_l[kSrWarps];
+  __shared__ float s_o[kSrWarps][DP];
   const int QR = p.qrows;  // query rows per stream: 8 or 16
-  const int row = warp_global % QR;
-  const int stream = warp_global / QR;
-  if (stream < p.n_streams) {
-    int t = stream;
-    const int qc = t % p.q_chunks; t /= p.q_chunks;
-    const int kvh = t % p.kvh_per_slot; t /= p.kvh_per_slot;
-    const int b = t % p.stream_batch + p.b_begin;
-    const int slot_local = t / p.stream_batch;
-    const int slot = slot_local + p.slot_base;
-    const int rank = slot % p.kvp;
-    const int qrow = qc * QR + row;
-    if (qrow < p.group) {
-      const int ntok = static_cast<int>(rr_count(p.total[b], rank, p.chunk, p.kvp));
-      const int pages = (ntok + 15) >> 4;
-      constexpr int PER = DP / 32;
-      float o[PER];
+  const int row = blockIdx.x % QR;
+  const int stream = blockIdx.x / QR;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int t = stream;
+  const int qc = t % p.q_chunks; t /= p.q_chunks;
+  const int kvh = t % p.kvh_per_slot; t /= p.kvh_per_slot;
+  const int b = t % p.stream_batch + p.b_begin;
+  const int slot_local = t / p.stream_batch;
+  const int slot = slot_local + p.slot_base;
+  const int rank = slot % p.kvp;
+  const int qrow = qc * QR + row;
+  if (qrow >= p.group) return;  // whole CTA
+  const int ntok = static_cast<int>(rr_count(p.total[b], rank, p.chunk, p.kvp));
+  const int pages = (ntok + 15) >> 4;
+  constexpr int PER = DP / 32;
+  auto valid = [&](int s) {
+    const int pg0 = static_cast<int>((static_cast<long long>(s) * pages) / p.splits);
+    const int pg1 = static_cast<int>((static_cast<long long>(s + 1) * pages) / p.splits);
+    return pg1 > pg0;
+  };
+  // pass 1: max lse over the non-empty splits
+  float M = -INFINITY;
+  for (int s = warp * 32 + lane; s < p.splits; s += kSrWarps * 32)
+    if (valid(s)) M = fmaxf(M, p.part_lse2[(static_cast<size_t>(s) * p.n_streams + stream) * QR + row]);
 #pragma unroll
-      for (int i = 0; i < PER; ++i) o[i] = 0.f;
-      // pass 1: every lane fetches a subset of the split lse values (independent loads)
-      float M = -INFINITY;
-      for (int s = lane; s < p.splits; s += 32) {
-        const int pg0 = static_cast<int>((static_cast<long long>(s) * pages) / p.splits);
-        const int pg1 = static_cast<int>((static_cast<long long>(s + 1) * pages) / p.splits);
-        if (pg1 > pg0) M = fmaxf(M, p.part_lse2[(static_cast<size_t>(s) * p.n_streams + stream) * QR + row]);
-      }
+  for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
+  if (lane == 0) s_m[warp] = M;
+  __syncthreads();
+  M = s_m[0];
 #pragma unroll
-      for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
-      // pass 2: weighted sum in split order (deterministic); each batch of 8
-      // splits issues all its loads before accumulating
-      float L = 0.f;
-      for (int s0 = 0; s0 < p.splits; s0 += 8) {
-        float w[8], v[8][PER];
+  for (int w = 1; w < kSrWarps; ++w) M = fmaxf(M, s_m[w]);
+  // pass 2: this warp's splits in order, 4 at a time with every load issued first
+  float o[PER], L = 0.f;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int s = s0 + j;
-          const int pg0 = static_cast<int>((static_cast<long long>(s) * pages) / p.splits);
-          const int pg1 = static_cast<int>((static_cast<long long>(s + 1) * pages) / p.splits);
-          const bool ok = s < p.splits && pg1 > pg0;
-          const size_t item = static_cast<size_t>(s) * p.n_streams + stream;
-          w[j] = ok ? p.part_lse2[item * QR + row] : -INFINITY;
+  for (int i = 0; i < PER; ++i) o[i] = 0.f;
+  for (int s0 = warp; s0 < p.splits; s0 += 4 * kSrWarps) {
+    float w4[4], v[4][PER];
 #pragma unroll
-          for (int i = 0; i < PER; ++i) v[j][i] = ok ? p.part_o[(item * QR + row) * DP + lane + 32 * i] : 0.f;
-        }
+    for (int j = 0; j < 4; ++j) {
+      const int s = s0 + j * kSrWarps;
+      const bool ok = s < p.splits && valid(s);
+      const size_t item = static_cast<size_t>(s) * p.n_streams + stream;
+      w4[j] = ok ? p.part_lse2[item * QR + row] : -INFINITY;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const float e = w[j] == -INFINITY ? 0.f : exp2f(w[j] - M);
-#pragma unroll
-          for (int i = 0; i < PER; ++i) o[i] += v[j][i] * e;
-          L += e;
-        }
-      }
-      // fragment layout: [slot_local][b][q_in_group][DP]
-      const int q_in_group = kvh * p.group + qrow;
-      const size_t fo = ((static_cast<size_t>(slot_local) * p.batch + b) * p.q_per_slot + q_in_group);
-#pragma unroll
-      for (int i = 0; i < PER; ++i) frag_o[fo * DP + lane + 32 * i] = L > 0.f ? o[i] / L : 0.f;
-      if (lane == 0) frag_lse[fo] = L > 0.f ? (M + log2f(L)) * 0.69314718055994530942f : -INFINITY;
+      for (int i = 0; i < PER; ++i) v[j][i] = ok ? p.part_o[(item * QR + row) * DP + lane + 32 * i] : 0.f;
     }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float e = w4[j] == -INFINITY ? 0.f : exp2f(w4[j] - M);
+#pragma unroll
+      for (int i = 0; i < PER; ++i) o[i] += v[j][i] * e;
+      L += e;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < PER; ++i) s_o[warp][lane + 32 * i] = o[i];
+  if (lane == 0) s_l[warp] = L;
+  __syncthreads();
+  if (warp == 0) {
+    float Lt = 0.f, ot[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) ot[i] = 0.f;
+#pragma unroll
+    for (int w = 0; w < kSrWarps; ++w) {
+      Lt += s_l[w];
+#pragma unroll
+      for (int i = 0; i < PER; ++i) ot[i] += s_o[w][lane + 32 * i];
+    }
+    // fragment layout: [slot_local][b][q_in_group][DP]
+    const int q_in_group = kvh * p.group + qrow;
+    const size_t fo = ((static_cast<size_t>(slot_local) * p.batch + b) * p.q_per_slot + q_in_group);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) frag_o[fo * DP + lane + 32 * i] = Lt > 0.f ? ot[i] / Lt : 0.f;
+    if (lane == 0) frag_lse[fo] = Lt > 0.f ? (M + log2f(Lt)) * 0.69314718055994530942f : -INFINITY;
   }
 }
 
@@ -455,9 +475,8 @@ cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t strea
 
 cudaError_t launch_attn_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse,
                                      cudaStream_t stream) {
-  const int warps = p.n_streams * p.qrows;
-  const int threads = 256;
-  const int blocks = (warps * 32 + threads - 1) / threads;
+  const int blocks = p.n_streams * p.qrows;  // one CTA per (stream, query row)
+  const int threads = kSrWarps * 32;
   switch (p.dp) {
     case 32: return launch_k(attn_split_reduce_kernel<32>, dim3(blocks), dim3(threads), 0, stream, p, frag_o, frag_lse);
     case 64: return launch_k(attn_split_reduce_kernel<64>, dim3(blocks), dim3(threads), 0, stream, p, frag_o, frag_lse);

@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -296,9 +297,15 @@ void Engine::alloc() {
   // attention work decomposition: balanced page ranges ("splits") per stream,
   // ~8 work items per SM for a full-batch launch and for a one-request (HOP-B) launch
   const int pages_max = page_cap_;
-  const int target_items = num_sms_ * 8;
+  // ~8 items per SM balance the persistent queue, but an item must stay >= 32
+  // pages (256 KB at Hsz 128): below that the per-item query staging and
+  // cross-warp combine dominate (measured: one 131k-token request of the
+  // 405B-like shard 0.196 -> 0.131 ms; profiles/r01_hopb_sweep.md).
+  int ips = 8, min_pages = 32;  // HX_ATTN_SPLIT="items_per_sm,min_pages_per_item" (tuning experiments)
+  if (const char* e = std::getenv("HX_ATTN_SPLIT")) std::sscanf(e, "%d,%d", &ips, &min_pages);
+  const int target_items = num_sms_ * std::max(1, ips);
   auto splits_for = [&](int streams) {
-    return std::max(1, std::min((target_items + streams - 1) / streams, std::max(1, pages_max / 8)));
+    return std::max(1, std::min((target_items + streams - 1) / streams, std::max(1, pages_max / std::max(1, min_pages))));
   };
   n_streams_ = n_slots_ * B_ * kvh_per_slot_ * q_chunks_;
   const int req_streams = n_slots_ * kvh_per_slot_ * q_chunks_;
@@ -996,7 +1003,10 @@ void Engine::enqueue_exchange_and_attention_dist(int64_t layer) {
   const size_t stride = static_cast<size_t>(B_) * xchunk_;
   const int rounds = hopb_ ? B_ : 1;
   const int per = hopb_ ? 1 : B_;
-  const bool side_stream = hopb_ && dist_mode_ == HX_POOL_NCCL;
+  // HOP-B: each request's exchange (or its measurement stand-in, the local copy)
+  // runs on the comm stream behind an event; the loopback transport
+  // synchronises on the host, so it stays on the compute stream
+  const bool side_stream = hopb_ && (dist_mode_ == HX_POOL_NCCL || (skip_comm_ & 1));
   for (int i = 0; i < rounds; ++i) {
     const int b0 = i * per;
     const AttnParams a = attn_params(layer, b0, per);
@@ -1008,19 +1018,21 @@ void Engine::enqueue_exchange_and_attention_dist(int64_t layer) {
     float* send = d_send_ + static_cast<size_t>(b0) * xchunk_;
     float* recv = d_recv_ + static_cast<size_t>(b0) * xchunk_;
     const size_t count = static_cast<size_t>(per) * xchunk_;
-    if (skip_comm_ & 1) {  // measurement: keep only this rank's own block, no wire traffic
-      cuda_check(cudaMemcpyAsync(recv + static_cast<size_t>(r_) * stride, send + static_cast<size_t>(r_) * stride,
-                                 count * sizeof(float), cudaMemcpyDeviceToDevice, stream_),
-                 "skip-comm copy");
-    } else if (side_stream) {
+    cudaStream_t cs = stream_;
+    if (side_stream) {
       cuda_check(cudaEventRecord(hop_events_[static_cast<size_t>(i)], stream_), "hopb event");
       cuda_check(cudaStreamWaitEvent(comm_stream_, hop_events_[static_cast<size_t>(i)], 0), "hopb wait");
-      transport_->all_to_all(send, recv, count, stride, comm_stream_);
+      cs = comm_stream_;
+    }
+    if (skip_comm_ & 1) {  // measurement: keep only this rank's own block, no wire traffic
+      cuda_check(cudaMemcpyAsync(recv + static_cast<size_t>(r_) * stride, send + static_cast<size_t>(r_) * stride,
+                                 count * sizeof(float), cudaMemcpyDeviceToDevice, cs),
+                 "skip-comm copy");
     } else {
-      transport_->all_to_all(send, recv, count, stride, stream_);
+      transport_->all_to_all(send, recv, count, stride, cs);
     }
   }
-  if (side_stream && !(skip_comm_ & 1)) {
+  if (side_stream) {
     cuda_check(cudaEventRecord(hop_events_.back(), comm_stream_), "hopb join");
     cuda_check(cudaStreamWaitEvent(stream_, hop_events_.back(), 0), "hopb join wait");
   }

@@ -503,39 +503,74 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
 
 // Merge a stream's split partials (split order, deterministic) into the
 // rank's fragment [slot][b][head][512] + natural-log lse (HeadFragment).
-__global__ void mla_split_reduce_kernel(const AttnParams p, float* frag_o, float* frag_lse) {
+// One CTA per (stream, head): warp w merges splits w, w+8, ... in order (all its
+// loads issued together), the 8 warp partials are combined in warp order
+// (deterministic). part_o of a launch (<= 19 MB at the C4 shard) is L2-resident.
+__global__ void __launch_bounds__(256) mla_split_reduce_kernel(const AttnParams p, float* frag_o, float* frag_lse) {
   griddep_wait();
   griddep_launch_dependents();
-  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  const int h = wg % p.q_heads, stream = wg / p.q_heads;
-  if (stream >= p.n_streams) return;
+  __shared__ float s_m[8], s_l[8];
+  __shared__ float s_o[8][kMlaDV];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = blockIdx.x % p.q_heads, stream = blockIdx.x / p.q_heads;
   const int bl = stream % p.stream_batch, sl = stream / p.stream_batch, b = bl + p.b_begin;
   const int rank = (sl + p.slot_base) % p.kvp;
   const int ntok = static_cast<int>(rr_count(p.total[b], rank, p.chunk, p.kvp));
   const int pages = (ntok + kMlaPageRows - 1) / kMlaPageRows;
-  float M = -INFINITY;
-  for (int s = 0; s < p.splits; ++s) {
+  auto valid = [&](int s) {
     const int pg0 = static_cast<int>((static_cast<long long>(s) * pages) / p.splits);
     const int pg1 = static_cast<int>((static_cast<long long>(s + 1) * pages) / p.splits);
-    if (pg1 > pg0) M = fmaxf(M, p.part_lse2[static_cast<size_t>(s * p.n_streams + stream) * kMlaHeads + h]);
-  }
+    return pg1 > pg0;
+  };
+  float M = -INFINITY;
+  for (int s = warp * 32 + lane; s < p.splits; s += 256)
+    if (valid(s)) M = fmaxf(M, p.part_lse2[static_cast<size_t>(s * p.n_streams + stream) * kMlaHeads + h]);
+#pragma unroll
+  for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
+  if (lane == 0) s_m[warp] = M;
+  __syncthreads();
+  M = s_m[0];
+#pragma unroll
+  for (int w = 1; w < 8; ++w) M = fmaxf(M, s_m[w]);
   float o[16] = {};
   float L = 0.f;
-  for (int s = 0; s < p.splits; ++s) {
-    const int pg0 = static_cast<int>((static_cast<long long>(s) * pages) / p.splits);
-    const int pg1 = static_cast<int>((static_cast<long long>(s + 1) * pages) / p.splits);
-    if (pg1 <= pg0) continue;
-    const size_t item = static_cast<size_t>(s * p.n_streams + stream);
-    const float w = exp2f(p.part_lse2[item * kMlaHeads + h] - M);
-    L += w;
+  for (int s0 = warp; s0 < p.splits; s0 += 16) {
+    float w2[2], v[2][16];
 #pragma unroll
-    for (int i = 0; i < 16; ++i) o[i] += w * p.part_o[(item * kMlaHeads + h) * kMlaDV + lane + 32 * i];
+    for (int j = 0; j < 2; ++j) {
+      const int s = s0 + 8 * j;
+      const bool ok = s < p.splits && valid(s);
+      const size_t item = static_cast<size_t>(s * p.n_streams + stream);
+      w2[j] = ok ? p.part_lse2[item * kMlaHeads + h] : -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) v[j][i] = ok ? p.part_o[(item * kMlaHeads + h) * kMlaDV + lane + 32 * i] : 0.f;
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const float e = w2[j] == -INFINITY ? 0.f : exp2f(w2[j] - M);
+      L += e;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) o[i] += e * v[j][i];
+    }
   }
+#pragma unroll
+  for (int i = 0; i < 16; ++i) s_o[warp][lane + 32 * i] = o[i];
+  if (lane == 0) s_l[warp] = L;
+  __syncthreads();
+  // all 8 warps write: warp w finalises dims [64w, 64w + 64)
+  float Lt = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) Lt += s_l[w];
   const size_t fo = (static_cast<size_t>(sl) * p.batch + b) * p.q_per_slot + h;
 #pragma unroll
-  for (int i = 0; i < 16; ++i) frag_o[fo * kMlaDV + lane + 32 * i] = L > 0.f ? o[i] / L : 0.f;
-  if (lane == 0) frag_lse[fo] = L > 0.f ? (M + log2f(L)) * 0.69314718055994530942f : -INFINITY;
+  for (int i = 0; i < 2; ++i) {
+    const int d = warp * 64 + lane + 32 * i;
+    float ot = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) ot += s_o[w][d];
+    frag_o[fo * kMlaDV + d] = Lt > 0.f ? ot / Lt : 0.f;
+  }
+  if (threadIdx.x == 0) frag_lse[fo] = Lt > 0.f ? (M + log2f(Lt)) * 0.69314718055994530942f : -INFINITY;
 }
 
 size_t mla_smem_bytes() { return kSmem; }
@@ -595,10 +630,9 @@ cudaError_t make_mla_tensor_maps(const void* pool, size_t bytes, void* tm_s, voi
 }
 
 cudaError_t launch_mla_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse, cudaStream_t stream) {
-  const long long warps = static_cast<long long>(p.n_streams) * p.q_heads;
-  const int threads = 256;
-  return launch_k(mla_split_reduce_kernel, dim3(static_cast<unsigned>((warps * 32 + threads - 1) / threads)),
-                  dim3(threads), 0, stream, p, frag_o, frag_lse);
+  const long long ctas = static_cast<long long>(p.n_streams) * p.q_heads;  // one per (stream, head)
+  return launch_k(mla_split_reduce_kernel, dim3(static_cast<unsigned>(ctas)), dim3(256), 0, stream, p, frag_o,
+                  frag_lse);
 }
 
 // ---------------------------------------------------------------------------

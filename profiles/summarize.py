@@ -1,6 +1,7 @@
 """Summarise ncu outputs into profiles/ (tracked). Usage:
     python profiles/summarize.py launches <launches.csv> <out.md>
     python profiles/summarize.py full <report.ncu-rep> <out.md> [<summary.json>]
+    python profiles/summarize.py hopb <hopb_sweep.jsonl> <out.md>
 """
 import csv
 import io
@@ -60,8 +61,30 @@ def full(rep, out, summary=None):
             json.dump({"attention": {"dram_bytes_per_launch": att.get("dram_bytes_read_total")}}, open(summary, "w"))
 
 
+def hopb(path, out):
+    rows = [json.loads(l) for l in open(path) if l.strip()]
+    ok = [r for r in rows if "attn_batched_ms" in r]
+    lines = ["| KVP | context | B | KV tok/GPU | attn batched (ms) | attn per-request (ms) | layer off (ms) | "
+             "layer on (ms) | a2a modeled (us) | exposed off (us) | exposed on (us) | hidden | HOP-B net (us) |",
+             "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
+    for r in ok:
+        hf = r.get("a2a_hidden_frac")
+        lines.append(f"| {r['kvp']} | {r['context']} | {r['batch']} | {r['kv_tokens_per_gpu']} | "
+                     f"{r['attn_batched_ms']:.3f} | {r['attn_hopb_ms']:.3f} | {r['layer_ms_off']:.3f} | "
+                     f"{r['layer_ms_on']:.3f} | {r['a2a_ms_modeled'] * 1e3:.2f} | {r['exposed_a2a_ms_off'] * 1e3:.2f} | "
+                     f"{r['exposed_a2a_ms_on'] * 1e3:.2f} | {'-' if hf is None else f'{hf:.2f}'} | "
+                     f"{r['hopb_gain_ms'] * 1e3:+.1f} |")
+    for r in rows:
+        if "skipped" in r or "error" in r:
+            lines.append(f"| {r['kvp']} | {r['context']} | {r['batch']} | {r.get('skipped') or r.get('error')} |"
+                         " | | | | | | | | |")
+    open(out, "w").write("\n".join(lines) + "\n")
+
+
 if __name__ == "__main__":
-    if sys.argv[1] == "launches":
+    if sys.argv[1] == "hopb":
+        hopb(sys.argv[2], sys.argv[3])
+    elif sys.argv[1] == "launches":
         launches(sys.argv[2], sys.argv[3])
     else:
         full(sys.argv[2], sys.argv[3], sys.argv[4] if len(sys.argv) > 4 else None)

@@ -86,8 +86,17 @@ def test_loopback_hopb_long_context_group16():
     S = 40000
     spec = P.model.ModelSpec("test16", L, H, Q, K, D, F, 3, "gqa", 0, vocab=V)
     lb = Loopback(kvp)
-    engines = [P.HelixDecoder(spec, tpa=1, kvp=kvp, chunk_size=16, batch=B, capacity=S + 64, layers=L, vocab=V,
-                              use_graphs=False, hopb=True, pool=2, rank=r, loopback=lb) for r in range(kvp)]
+    import os
+    old = os.environ.get("HX_ATTN_SPLIT")
+    os.environ["HX_ATTN_SPLIT"] = "8,8"  # small items: per-request split count (156) != batched (148)
+    try:
+        engines = [P.HelixDecoder(spec, tpa=1, kvp=kvp, chunk_size=16, batch=B, capacity=S + 64, layers=L, vocab=V,
+                                  use_graphs=False, hopb=True, pool=2, rank=r, loopback=lb) for r in range(kvp)]
+    finally:
+        if old is None:
+            del os.environ["HX_ATTN_SPLIT"]
+        else:
+            os.environ["HX_ATTN_SPLIT"] = old
     info = engines[0].info()
     assert info["attn_splits"] < (S // kvp // 16) // 8, info  # the per-request launch uses more splits
     o = O.Model(H, Q, K, D, F, L, V, tpa=1, kvp=kvp, chunk=16, batch=B, seed=77, qkv_hash=True, bf16=True)

@@ -1,0 +1,144 @@
+"""C5: HOP-B sweep -- batch x context x KVP, overlap on vs off.
+
+    python tools/hopb_sweep.py [--model llama405b-like] [--kvp 2 4 8]
+                               [--contexts 131072 ...] [--batches 1 2 ...]
+                               [--out gpurun_out/hopb_sweep.jsonl]
+
+One GPU of a KVP-sharded Helix pool (TPA = 1, TPF = KVP; one layer of the
+model) is measured alone: rank 0 of a KVP-rank loopback pool with the
+collectives switched off, so every number here is this GPU's real compute:
+
+  * attn_batched_ms -- attention + split-reduce + exchange pack for the whole
+    batch in one launch (HOP-B off);
+  * attn_hopb_ms    -- the same work launched per request (HOP-B on: request
+    b's exchange would overlap request b+1's attention, overlap.hpp:37-69);
+    the difference is the compute-side price of HOP-B's finer launches;
+  * layer_ms_off / layer_ms_on -- the whole layer (QKV .. FFN), eager launches.
+
+The all-to-all itself needs peers (one B200 here), so its duration comes from
+the reference's own alpha-beta model (comm.hpp:28-45, a2a_payload_per_destination
+:60-69; payload in fp32 as this engine sends it) with the reference's
+gb200-like link figures (900 GB/s, 0.1 us) -- "modeled" in the output -- and
+the exposed time with and without HOP-B from the reference's hopb_schedule
+(overlap.hpp:37-69, composition latency.cpp:216-234) applied to the MEASURED
+per-request compute. On a multi-GPU box `bench.py --gpus N` measures the real
+NCCL exposure (its `hopb` key) on the same engine.
+
+Points whose KV shard does not fit (1-layer slice: KV + weights > 170 GB) are
+reported as skipped.
+"""
+import argparse
+import ctypes
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+LINK_BW, LINK_LAT = 9e11, 1e-7  # reference presets/gb200-like.json:5-6
+
+
+def hopb_schedule(requests, compute, comm, enabled):
+    """overlap.hpp:37-69: total span of R requests' compute + comm."""
+    if not enabled:
+        return requests * (compute + comm)
+    prev = 0.0
+    for i in range(requests):
+        ce = (i + 1) * compute
+        ms = ce if i == 0 else max(ce, prev)
+        prev = ms + comm
+    return prev
+
+
+def a2a_time(hidden, head_size, batch, kvp, bytes_per_elem=4):
+    """comm_time(AllToAll, kvp, per_dest * kvp) with the reference payload (comm.hpp)."""
+    if kvp == 1:
+        return 0.0
+    per_dest = batch * hidden / kvp * (1.0 + 1.0 / head_size) * bytes_per_elem
+    return LINK_LAT + per_dest * kvp * (kvp - 1) / kvp / LINK_BW
+
+
+def point(P, Loopback, spec, kvp, S, B, steps=5):
+    import numpy as np
+    import torch
+    s_loc = S // kvp
+    K, Hsz, H, F = spec.kv_heads, spec.head_size, spec.hidden_dim, spec.ffn_dim
+    kv_bytes = B * s_loc * 2 * K * Hsz * 2
+    w_bytes = H * (spec.query_heads * Hsz + 2 * K * Hsz) * 2 + (H // kvp) * H * 2 + 3 * H * F // kvp * 2
+    if kv_bytes + w_bytes > 170e9:
+        return {"kvp": kvp, "context": S, "batch": B, "skipped": "KV shard + weights exceed 170 GB"}
+    lb = Loopback(kvp)
+    eng = P.HelixDecoder(spec, tpa=1, kvp=kvp, batch=B, capacity=S + 64 * kvp, layers=1, vocab=4096,
+                         use_graphs=False, pool=2, rank=0, loopback=lb, hopb=True)
+    lib = P.lib()
+    lib.hx_engine_set_flag(eng._h, 1, 3)  # collectives off (no peers on one GPU)
+    eng.init_weights(2507, qkv="hash")
+    eng.fill_kv_hash(S, 2507)
+    tok = torch.randint(0, 4096, (B,), dtype=torch.int32, device="cuda")
+    nxt = torch.zeros(B, dtype=torch.int32, device="cuda")
+    stream = torch.cuda.ExternalStream(eng.stream())
+    out = {"kvp": kvp, "context": S, "batch": B, "kv_tokens_per_gpu": s_loc}
+    for hopb in (0, 1):
+        lib.hx_engine_set_flag(eng._h, 2, hopb)
+        for _ in range(2):
+            eng.step_device(tok.data_ptr(), nxt.data_ptr())
+        prof = np.zeros(10)
+        lib.hx_profile_step(eng._h, 3, prof.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for _ in range(steps):
+            eng.step_device(tok.data_ptr(), nxt.data_ptr())
+        e1.record(stream)
+        e1.synchronize()
+        key = "on" if hopb else "off"
+        # attention kernel + split reduce + pack (kinds 2, 3): the compute HOP-B overlaps
+        out[f"attn_{'hopb' if hopb else 'batched'}_ms"] = float(prof[2] + prof[3])
+        out[f"layer_ms_{key}"] = e0.elapsed_time(e1) / steps
+    eng.close()
+    t = a2a_time(H, Hsz, B, kvp) * 1e3  # ms, whole batch
+    c_on = out["attn_hopb_ms"] / B
+    c_off = out["attn_batched_ms"] / B
+    span_on = hopb_schedule(B, c_on, t / B, True)
+    span_off = hopb_schedule(B, c_off, t / B, False)
+    out.update({
+        "a2a_ms_modeled": t,
+        "exposed_a2a_ms_off": max(0.0, span_off - out["attn_batched_ms"]),
+        "exposed_a2a_ms_on": max(0.0, span_on - out["attn_hopb_ms"]),
+        # what HOP-B buys end to end at this point: (off span) - (on span), incl. its launch price
+        "hopb_gain_ms": span_off - span_on,
+    })
+    out["a2a_hidden_frac"] = 1.0 - out["exposed_a2a_ms_on"] / t if t > 0 else None
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--model", default="llama405b-like")
+    ap.add_argument("--kvp", type=int, nargs="+", default=[2, 4, 8])
+    ap.add_argument("--contexts", type=int, nargs="+",
+                    default=[131072, 262144, 524288, 1048576, 2097152, 4194304])
+    ap.add_argument("--batches", type=int, nargs="+", default=[1, 2, 4, 8, 16, 32, 64])
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "hopb_sweep.jsonl"))
+    a = ap.parse_args()
+    import paper_2507_07120_b200 as P
+    from paper_2507_07120_b200.model import Loopback
+    spec = P.model.PRESETS[a.model]
+    os.makedirs(os.path.dirname(a.out), exist_ok=True)
+    with open(a.out, "w") as f:
+        for kvp in a.kvp:
+            for S in a.contexts:
+                for B in a.batches:
+                    try:
+                        r = point(P, Loopback, spec, kvp, S, B)
+                    except Exception as ex:  # recorded, the sweep goes on
+                        r = {"kvp": kvp, "context": S, "batch": B, "error": str(ex)[:200]}
+                    r["model"] = a.model
+                    f.write(json.dumps(r) + "\n")
+                    f.flush()
+                    print(json.dumps(r), flush=True)
+
+
+if __name__ == "__main__":
+    main()
