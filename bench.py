@@ -189,7 +189,8 @@ def pool_slice(a, preset, S, ep):
                          "unit": "TFLOP/s", "frac": flops / (att_ms * 1e-3) / 1e12 / tc, "peak_kind": tc_kind,
                          "hbm_achieved_gbs": kv_bytes / (att_ms * 1e-3) / 1e9,
                          "hbm_frac": kv_bytes / (att_ms * 1e-3) / 1e9 / hbm,
-                         "t_roof_ms": max(kv_bytes / hbm / 1e6, flops / tc / 1e9)}}
+                         "t_roof_ms": max(kv_bytes / hbm / 1e6, flops / tc / 1e9),
+                         "traffic": ncu_traffic("mla")}}
         out["moe"] = {"local_experts": spec.moe.total_experts // ep, "active_local_experts_last_step": active,
                       "expert_bytes_streamed": active * 3 * H * spec.moe.expert_ffn_dim * 2}
     else:
@@ -203,7 +204,8 @@ def pool_slice(a, preset, S, ep):
             "kernel": "attn_decode_kernel<128,8,2> (TMA bulk-copy page ring, mma.sync)", "launch_ms": att_ms,
             "algorithmic_kv_bytes": kv_bytes,
             "roofline": {"bound": "hbm", "achieved": kv_bytes / (att_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
-                         "frac": kv_bytes / (att_ms * 1e-3) / 1e9 / hbm}}
+                         "frac": kv_bytes / (att_ms * 1e-3) / 1e9 / hbm,
+                         "traffic": ncu_traffic("attention_405b_slice")}}
         out["layer_roofline"] = {"bound": "hbm", "algorithmic_bytes": kv_bytes + w_bytes, "weight_bytes": w_bytes,
                                  "t_roof_ms": (kv_bytes + w_bytes) / hbm / 1e6,
                                  "achieved_gbs": (kv_bytes + w_bytes) / (ms * 1e-3) / 1e9,
@@ -214,10 +216,12 @@ def pool_slice(a, preset, S, ep):
     return out
 
 
-def ncu_traffic():
+def ncu_traffic(key="attention"):
+    """DRAM bytes per launch (read + write) of the kernel from the committed
+    `ncu --set full` capture (profiles/ncu_summary.json), or None."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_summary.json")) as f:
-            return json.load(f).get("attention", {}).get("dram_bytes_per_launch")
+            return json.load(f).get(key, {}).get("dram_bytes_per_launch")
     except Exception:
         return None
 
