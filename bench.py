@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-context", type=int, default=131072)
     ap.add_argument("--profile-only", action="store_true", help="skip timing loops (for ncu)")
+    ap.add_argument("--no-fp8", action="store_true", help="skip the FP8-KV variant of the headline workload")
     ap.add_argument("--no-slices", action="store_true",
                     help="skip the one-GPU-of-8 slices (C3 llama405b-like, C4 deepseek-r1-like)")
     ap.add_argument("--slice-context", type=int, default=125000,
@@ -214,6 +215,54 @@ def pool_slice(a, preset, S, ep):
     out["engine"] = info
     eng.close()
     return out
+
+
+def fp8_kv_line(a):
+    """the configs[1] workload with FP8 (e4m3) KV pages
+    (kv_dtype="fp8"; weights stay bf16, attention MMAs in f16 on the exact
+    widened values). Same timing method as the headline (graph replay, CUDA
+    events on the engine stream); a separate key, never the headline number
+    (the headline stores KV in bf16)."""
+    import ctypes
+    import numpy as np
+    import torch
+    import paper_2507_07120_b200 as P
+    spec = P.model.PRESETS["llama3-8b-like"]
+    B, S, L = a.batch, a.context, a.layers
+    eng = P.HelixDecoder(spec, tpa=1, kvp=1, batch=B, capacity=S + 4 * (a.warmup + a.steps + 16) + 64, layers=L,
+                         kv_dtype="fp8")
+    eng.init_weights(2507, qkv="hash")
+    eng.fill_kv_hash(S, 2507)
+    stream = torch.cuda.ExternalStream(eng.stream())
+    tok = [torch.randint(0, spec.vocab, (B,), dtype=torch.int32, device="cuda"),
+           torch.zeros(B, dtype=torch.int32, device="cuda")]
+    for i in range(a.warmup):
+        eng.step_device(tok[i % 2].data_ptr(), tok[(i + 1) % 2].data_ptr())
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(a.steps):
+        eng.step_device(tok[i % 2].data_ptr(), tok[(i + 1) % 2].data_ptr())
+    e1.record(stream)
+    e1.synchronize()
+    ms = e0.elapsed_time(e1) / a.steps
+    prof = np.zeros(10)
+    P.lib().hx_profile_step(eng._h, 2, prof.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
+    att = prof[2] / L
+    s_now = eng.total_tokens(0, 0)
+    kv_bytes = B * spec.kv_heads * s_now * spec.head_size * 2 * 1  # K+V, 1 byte per element
+    hbm, _ = peaks()
+    info = eng.info()
+    eng.close()
+    return {"kv_dtype": "fp8_e4m3", "ms_per_step": ms, "value": B / (ms * 1e-3), "unit": UNIT,
+            "breakdown_ms": {k: float(v) for k, v in zip(
+                ["embed", "qkv", "attention", "split_reduce", "o_proj", "gate_up", "down", "lm_head", "merge"], prof)},
+            "attention_roofline": {"bound": "hbm", "kernel": "attn_decode_kernel<128,8,4,1,fp8>",
+                                   "algorithmic_bytes_per_launch": kv_bytes, "launch_ms": att,
+                                   "achieved": kv_bytes / (att * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
+                                   "frac": kv_bytes / (att * 1e-3) / 1e9 / hbm,
+                                   "traffic": ncu_traffic("attention_fp8")},
+            "kv_bytes_per_layer": info["kv_bytes_per_layer"]}
 
 
 def ncu_traffic(key="attention"):
@@ -429,6 +478,12 @@ def ours(a):
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as ex:  # reported, never fatal for the GPU number
             line["cpu_baseline"] = {"error": str(ex)[:200]}
+    if world == 1 and not a.no_fp8:
+        eng.close()  # free the 150 GB pool
+        try:
+            line["fp8_kv"] = fp8_kv_line(a)
+        except Exception as ex:  # reported, never fatal for the headline number
+            line["fp8_kv"] = {"error": str(ex)[:300]}
     if world == 1 and not a.no_slices:
         eng.close()  # free the 150 GB pool before the 8-GPU-pool slices
         for key, preset, ctx, ep in (("llama405b_slice", "llama405b-like", a.slice_context, 1),

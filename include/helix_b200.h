@@ -87,8 +87,12 @@ typedef struct hx_runtime_config {
   int32_t device;
   int32_t hopb;             /* HOP-B batch-wise comm/compute overlap (overlap.hpp:37-69) */
   int32_t use_graphs;       /* capture the decode step in a CUDA graph */
-  int32_t reserved;
+  int32_t kv_dtype;         /* KV page storage: HX_KV_BF16, or HX_KV_FP8_E4M3 (GQA; e4m3 RNE,
+                               saturating at +-448, unit scale -- SURVEY 8f rank 2) */
 } hx_runtime_config;
+
+#define HX_KV_BF16 0
+#define HX_KV_FP8_E4M3 1
 
 typedef struct hx_engine_info {
   int64_t kv_bytes_per_layer;      /* resident KV pool bytes on this device, per layer */
@@ -98,6 +102,7 @@ typedef struct hx_engine_info {
   int64_t kernels_per_step;        /* kernel launches of one hx_decode_step (or harness step) */
   int64_t page_cap;
   int64_t head_dim_padded;
+  int64_t kv_dtype;                /* HX_KV_BF16 / HX_KV_FP8_E4M3 */
 } hx_engine_info;
 
 const char* hx_version(void);

@@ -28,6 +28,18 @@ double round_bf16(double x) {
   return std::ldexp(r, e - 8);
 }
 
+double round_e4m3(double x) {
+  if (x == 0.0 || std::isnan(x)) return x;
+  const double a = std::fabs(x);
+  int e = 0;
+  std::frexp(a, &e);                                   // a in [2^(e-1), 2^e)
+  const int unb = std::max(e - 1, -6);                 // subnormals share the 2^-6 quantum
+  const double q = std::ldexp(1.0, unb - 3);           // 3 mantissa bits
+  double r = std::nearbyint(a / q) * q;                // RNE (default rounding mode)
+  if (r > 448.0) r = 448.0;                            // satfinite
+  return std::copysign(r, x);
+}
+
 double logit_scale(i64 width) { return 1.0 / std::sqrt(static_cast<double>(width)); }
 
 namespace {
@@ -286,8 +298,8 @@ void DecodeHarness::grow_random(i64 n, std::mt19937_64& rng) {
   for (i64 i = 0; i < n; ++i) {
     Mat v = random_matrix(rng, dims_.kv_heads, dims_.head_size);
     Mat k = random_matrix(rng, dims_.kv_heads, dims_.head_size);
-    maybe_round(k, bf16_);
-    maybe_round(v, bf16_);
+    for (double& e : k.a) e = round_kv(e);
+    for (double& e : v.a) e = round_kv(e);
     cache_.append_round_robin(k, v);
   }
 }
@@ -325,8 +337,8 @@ void DecodeHarness::project_kv(const std::vector<double>& x, Mat& k, Mat& v) con
 void DecodeHarness::append_projected(const std::vector<double>& x) {
   Mat k, v;
   project_kv(x, k, v);
-  maybe_round(k, bf16_);
-  maybe_round(v, bf16_);
+  for (double& e : k.a) e = round_kv(e);
+  for (double& e : v.a) e = round_kv(e);
   cache_.append_round_robin(k, v);
 }
 

@@ -51,6 +51,10 @@ Mat random_matrix(std::mt19937_64& rng, i64 rows, i64 cols);
 // Round to the nearest bf16 value (round-to-nearest-even on the double).
 // Models the B200 path's bf16 storage of weights and KV.
 double round_bf16(double x);
+// Round to the nearest FP8 E4M3 ("e4m3fn": bias 7, 3 mantissa bits, max finite
+// 448, no infinities) value, ties to even, saturating at +-448 -- the B200
+// path's optional FP8 KV storage.
+double round_e4m3(double x);
 
 // ---- single-head primitives (attention.hpp:35-78) ----
 struct HeadFragment {
@@ -162,6 +166,11 @@ class DecodeHarness {
     wv_ = std::move(wv);
   }
   bool bf16_storage() const { return bf16_; }
+  // KV storage rounding: bf16 (bf16_storage) or, with kv_fp8, e4m3 (round_e4m3);
+  // weights stay bf16. Applies to KV grown or appended after the call.
+  void set_kv_fp8(bool on) { kv_fp8_ = on; }
+  bool kv_fp8() const { return kv_fp8_; }
+  double round_kv(double x) const { return kv_fp8_ ? round_e4m3(x) : (bf16_ ? round_bf16(x) : x); }
   // Last step's merged lse per query head (natural log), for kernel parity.
   const std::vector<double>& last_lse() const { return last_lse_; }
 
@@ -170,6 +179,7 @@ class DecodeHarness {
   Dims dims_;
   i64 tpa_, kvp_;
   bool bf16_;
+  bool kv_fp8_ = false;
   Mat wq_, wk_, wv_;
   ShardedKVCache cache_;
   std::vector<Message> transcript_;

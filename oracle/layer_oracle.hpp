@@ -120,12 +120,18 @@ class ModelOracle {
   // Last step's router margin per (layer, request): r[k-th] - r[(k+1)-th]
   // (a kernel whose logits differ by more than this may legally pick another set)
   const std::vector<double>& route_gaps() const { return gaps_; }
+  // FP8 (e4m3) KV storage for the GQA caches (DecodeHarness::set_kv_fp8).
+  void set_kv_fp8(bool on) {
+    kv_fp8_ = on;
+    for (auto& h : h_) h.set_kv_fp8(on);
+  }
 
  private:
   ModelDims d_;
   i64 batch_;
   std::uint64_t seed_;
   bool bf16_;
+  bool kv_fp8_ = false;
   std::vector<DecodeHarness> h_;
   std::vector<Mat> wo_, wg_, wu_, wd_, wr_;
   std::vector<std::vector<Mat>> eg_, eu_, ed_;  // [layer][expert]

@@ -36,6 +36,7 @@ void oracle_rng_free(void* r) { delete static_cast<std::mt19937_64*>(r); }
 double oracle_rng_unit_draw(void* r) { return unit_draw(*static_cast<std::mt19937_64*>(r)); }
 std::uint64_t oracle_rng_next(void* r) { return (*static_cast<std::mt19937_64*>(r))(); }
 double oracle_round_bf16(double x) { return round_bf16(x); }
+double oracle_round_e4m3(double x) { return round_e4m3(x); }
 
 int oracle_harness_create(i64 q, i64 k, i64 hsz, i64 tpa, i64 kvp, i64 chunk, std::uint64_t seed,
                           int bf16, void** out) {
@@ -44,6 +45,7 @@ int oracle_harness_create(i64 q, i64 k, i64 hsz, i64 tpa, i64 kvp, i64 chunk, st
   });
 }
 void oracle_harness_free(void* h) { delete static_cast<DecodeHarness*>(h); }
+void oracle_harness_set_kv_fp8(void* h, int on) { static_cast<DecodeHarness*>(h)->set_kv_fp8(on != 0); }
 
 int oracle_harness_grow_random(void* h, i64 n, void* rng) {
   return guard([&] {
@@ -252,6 +254,7 @@ int oracle_model_route_gaps(void* mp, double* out) {
   });
 }
 void oracle_model_free(void* m) { delete static_cast<ModelOracle*>(m); }
+void oracle_model_set_kv_fp8(void* m, int on) { static_cast<ModelOracle*>(m)->set_kv_fp8(on != 0); }
 
 int oracle_model_grow_random(void* m, i64 layer, i64 request, i64 n, void* rng) {
   return guard([&] {

@@ -46,12 +46,44 @@ struct StageMeta {
   int rows;         // valid query rows in this stream (<= 8 * QC)
 };
 
-template <int DP>
+template <int DP, bool KV8>
 struct AttnCfg {
   static constexpr int KS = DP / 16;     // k-steps over the head dim
   static constexpr int ND = DP / 8;      // PV n-tiles
-  static constexpr uint32_t PAGE = 64u * DP;
+  static constexpr uint32_t PAGE = (KV8 ? 32u : 64u) * DP;  // kv_layout.cuh
 };
+
+// KV8: FP8 e4m3 pages; each lane's 8-byte chunk widens to the f16 register image
+// of the bf16 path's 16-byte chunk, and the MMAs run in f16 (q and P split into
+// f16 terms) -- e4m3 values are exact in f16, so the only rounding is the e4m3
+// storage itself.
+template <bool KV8>
+__device__ __forceinline__ uint4 load_kv_frag(uint32_t addr16, uint32_t addr8) {
+  if constexpr (KV8) {
+    const uint2 b = lds64(addr8);
+    uint4 r;
+    e4m3x4_to_f16x2x2(b.x, r.x, r.y);
+    e4m3x4_to_f16x2x2(b.y, r.z, r.w);
+    return r;
+  } else {
+    return lds128(addr16);
+  }
+}
+template <bool KV8>
+__device__ __forceinline__ void mma_kv(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                                       uint32_t b0, uint32_t b1) {
+  if constexpr (KV8)
+    mma_f16_16816(d, a0, a1, a2, a3, b0, b1);
+  else
+    mma_bf16_16816(d, a0, a1, a2, a3, b0, b1);
+}
+template <bool KV8>
+__device__ __forceinline__ uint32_t pack_kv(float lo, float hi) {
+  if constexpr (KV8)
+    return pack_f16(lo, hi);
+  else
+    return pack_bf16(lo, hi);
+}
 
 __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
@@ -59,9 +91,9 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 
 }  // namespace
 
-template <int DP, int NWC, int NSTAGE, int QC>
+template <int DP, int NWC, int NSTAGE, int QC, bool KV8>
 __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const AttnParams p) {
-  using Cfg = AttnCfg<DP>;
+  using Cfg = AttnCfg<DP, KV8>;
   static_assert(NWC % QC == 0, "query chunks must divide the consumer warps");
   constexpr int QR = 8 * QC;           // query rows per item
   constexpr int WPC = NWC / QC;        // warps (pages per stage slot) per query chunk
@@ -194,13 +226,21 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           v[3] = valid ? qs[g * DP + d0 + 9] * p.qscale : 0.f;
           float hi[4], mid[4], lo[4];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) split3(v[i], hi[i], mid[i], lo[i]);
-          qa[ks][0] = pack_bf16(hi[0], hi[1]);
-          qa[ks][1] = pack_bf16(mid[0], mid[1]);
-          qa[ks][2] = pack_bf16(hi[2], hi[3]);
-          qa[ks][3] = pack_bf16(mid[2], mid[3]);
-          qb[ks][0] = pack_bf16(lo[0], lo[1]);
-          qb[ks][1] = pack_bf16(lo[2], lo[3]);
+          for (int i = 0; i < 4; ++i) {
+            if constexpr (KV8) {
+              // f16 hi + lo carries 22 significant bits (~fp32): one M-tile [hi; lo]
+              split2h(v[i], hi[i], mid[i]);
+              lo[i] = 0.f;
+            } else {
+              split3(v[i], hi[i], mid[i], lo[i]);
+            }
+          }
+          qa[ks][0] = pack_kv<KV8>(hi[0], hi[1]);
+          qa[ks][1] = pack_kv<KV8>(mid[0], mid[1]);
+          qa[ks][2] = pack_kv<KV8>(hi[2], hi[3]);
+          qa[ks][3] = pack_kv<KV8>(mid[2], mid[3]);
+          qb[ks][0] = pack_kv<KV8>(lo[0], lo[1]);
+          qb[ks][1] = pack_kv<KV8>(lo[2], lo[3]);
         }
 #pragma unroll
         for (int nd = 0; nd < Cfg::ND; ++nd) acc[nd][0] = acc[nd][1] = acc[nd][2] = acc[nd][3] = 0.f;
@@ -224,12 +264,13 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
         for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
           for (int kp = 0; kp < Cfg::KS / 2; ++kp) {
-            const uint4 kf = lds128(pbase + ((nt * (Cfg::KS / 2) + kp) * 32 + lane) * 16);
+            const int ci = (nt * (Cfg::KS / 2) + kp) * 32 + lane;
+            const uint4 kf = load_kv_frag<KV8>(pbase + ci * 16, pbase + ci * 8);
             const int k0 = 2 * kp, k1 = 2 * kp + 1;
-            mma_bf16_16816(s0[nt], qa[k0][0], qa[k0][1], qa[k0][2], qa[k0][3], kf.x, kf.y);
-            mma_bf16_16816(s1[nt], qb[k0][0], 0u, qb[k0][1], 0u, kf.x, kf.y);
-            mma_bf16_16816(s0[nt], qa[k1][0], qa[k1][1], qa[k1][2], qa[k1][3], kf.z, kf.w);
-            mma_bf16_16816(s1[nt], qb[k1][0], 0u, qb[k1][1], 0u, kf.z, kf.w);
+            mma_kv<KV8>(s0[nt], qa[k0][0], qa[k0][1], qa[k0][2], qa[k0][3], kf.x, kf.y);
+            if constexpr (!KV8) mma_kv<KV8>(s1[nt], qb[k0][0], 0u, qb[k0][1], 0u, kf.x, kf.y);
+            mma_kv<KV8>(s0[nt], qa[k1][0], qa[k1][1], qa[k1][2], qa[k1][3], kf.z, kf.w);
+            if constexpr (!KV8) mma_kv<KV8>(s1[nt], qb[k1][0], 0u, qb[k1][1], 0u, kf.z, kf.w);
           }
         }
         // logits (log2 units) for query row g, tokens 2c, 2c+1, 8+2c, 9+2c
@@ -260,24 +301,31 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
             for (int i = 0; i < 4; ++i) acc[nd][i] *= alpha;
           m_ref = m_new;
         }
-        float pv[4], ph[4], pl[4];
+        float pv[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          pv[i] = fast_exp2(sv[i] - m_ref);
-          split2(pv[i], ph[i], pl[i]);
-        }
+        for (int i = 0; i < 4; ++i) pv[i] = fast_exp2(sv[i] - m_ref);
         l_sum += (pv[0] + pv[1]) + (pv[2] + pv[3]);
-        const uint32_t a0 = pack_bf16(ph[0], ph[1]);
-        const uint32_t a1 = pack_bf16(pl[0], pl[1]);
-        const uint32_t a2 = pack_bf16(ph[2], ph[3]);
-        const uint32_t a3 = pack_bf16(pl[2], pl[3]);
+        uint32_t a0, a1, a2, a3;
+        if constexpr (KV8) {
+          split2h_pack(pv[0], pv[1], a0, a1);
+          split2h_pack(pv[2], pv[3], a2, a3);
+        } else {
+          float ph[4], pl[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) split2(pv[i], ph[i], pl[i]);
+          a0 = pack_bf16(ph[0], ph[1]);
+          a1 = pack_bf16(pl[0], pl[1]);
+          a2 = pack_bf16(ph[2], ph[3]);
+          a3 = pack_bf16(pl[2], pl[3]);
+        }
         // ---- O += P V
-        const uint32_t vbase = pbase + 32 * DP;
+        const uint32_t vbase = pbase + Cfg::PAGE / 2;
 #pragma unroll
         for (int nd2 = 0; nd2 < Cfg::ND / 2; ++nd2) {
-          const uint4 vf = lds128(vbase + (nd2 * 32 + lane) * 16);
-          mma_bf16_16816(acc[2 * nd2], a0, a1, a2, a3, vf.x, vf.y);
-          mma_bf16_16816(acc[2 * nd2 + 1], a0, a1, a2, a3, vf.z, vf.w);
+          const int ci = nd2 * 32 + lane;
+          const uint4 vf = load_kv_frag<KV8>(vbase + ci * 16, vbase + ci * 8);
+          mma_kv<KV8>(acc[2 * nd2], a0, a1, a2, a3, vf.x, vf.y);
+          mma_kv<KV8>(acc[2 * nd2 + 1], a0, a1, a2, a3, vf.z, vf.w);
         }
       }
       __syncwarp();
@@ -442,35 +490,41 @@ __global__ void bump_totals_kernel(int* total, int n) {
 
 // ------------------------------------------------------------------------
 // host launchers
-template <int DP, int NWC, int NSTAGE, int QC>
+template <int DP, int NWC, int NSTAGE, int QC, bool KV8>
 static size_t attn_smem_bytes() {
-  return NSTAGE * (NWC * AttnCfg<DP>::PAGE + QC * 8 * DP * 4) + NWC * (8 * DP + 16) * 4 +
+  return NSTAGE * (NWC * AttnCfg<DP, KV8>::PAGE + QC * 8 * DP * 4) + NWC * (8 * DP + 16) * 4 +
          NSTAGE * sizeof(StageMeta) + 2 * NSTAGE * 8 + 64;
 }
 
-template <int DP, int NWC, int NSTAGE, int QC>
+template <int DP, int NWC, int NSTAGE, int QC, bool KV8>
 static cudaError_t launch_attn_t(const AttnParams& p, int grid, cudaStream_t stream) {
-  const size_t smem = attn_smem_bytes<DP, NWC, NSTAGE, QC>();
+  const size_t smem = attn_smem_bytes<DP, NWC, NSTAGE, QC, KV8>();
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<DP, NWC, NSTAGE, QC>,
+    cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<DP, NWC, NSTAGE, QC, KV8>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  return launch_k(attn_decode_kernel<DP, NWC, NSTAGE, QC>, dim3(grid), dim3((NWC + 1) * 32), smem, stream, p);
+  return launch_k(attn_decode_kernel<DP, NWC, NSTAGE, QC, KV8>, dim3(grid), dim3((NWC + 1) * 32), smem, stream, p);
+}
+
+// bf16 pages: 2-4 stages of 8 pages; FP8 pages are half the bytes, so twice the stages in flight
+template <int QC, bool KV8>
+static cudaError_t launch_attn_dp(const AttnParams& p, int grid, cudaStream_t stream) {
+  switch (p.dp) {
+    case 32: return launch_attn_t<32, 8, KV8 ? 8 : 4, QC, KV8>(p, grid, stream);
+    case 64: return launch_attn_t<64, 8, KV8 ? 6 : 3, QC, KV8>(p, grid, stream);
+    case 128: return launch_attn_t<128, 8, KV8 ? 4 : 2, QC, KV8>(p, grid, stream);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t stream) {
-  const bool two = p.qrows == 16;
-  if (!two && p.qrows != 8) return cudaErrorInvalidValue;
-  switch (p.dp) {
-    case 32: return two ? launch_attn_t<32, 8, 4, 2>(p, grid, stream) : launch_attn_t<32, 8, 4, 1>(p, grid, stream);
-    case 64: return two ? launch_attn_t<64, 8, 3, 2>(p, grid, stream) : launch_attn_t<64, 8, 3, 1>(p, grid, stream);
-    case 128: return two ? launch_attn_t<128, 8, 2, 2>(p, grid, stream) : launch_attn_t<128, 8, 2, 1>(p, grid, stream);
-    default: return cudaErrorInvalidValue;
-  }
+  if (p.qrows != 8 && p.qrows != 16) return cudaErrorInvalidValue;
+  if (p.kv8) return p.qrows == 16 ? launch_attn_dp<2, true>(p, grid, stream) : launch_attn_dp<1, true>(p, grid, stream);
+  return p.qrows == 16 ? launch_attn_dp<2, false>(p, grid, stream) : launch_attn_dp<1, false>(p, grid, stream);
 }
 
 cudaError_t launch_attn_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse,
@@ -495,9 +549,9 @@ bool pdl_enabled() { return g_pdl; }
 
 size_t attn_decode_smem_bytes(int dp) {
   switch (dp) {  // the larger (two query chunks) variant
-    case 32: return attn_smem_bytes<32, 8, 4, 2>();
-    case 64: return attn_smem_bytes<64, 8, 3, 2>();
-    case 128: return attn_smem_bytes<128, 8, 2, 2>();
+    case 32: return attn_smem_bytes<32, 8, 4, 2, false>();
+    case 64: return attn_smem_bytes<64, 8, 3, 2, false>();
+    case 128: return attn_smem_bytes<128, 8, 2, 2, false>();
     default: return 0;
   }
 }

@@ -5,6 +5,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -43,6 +44,44 @@ HX_DEV float fast_exp2(float x) {
 // D(16x8, f32) += A(16x16, bf16, row) * B(16x8, bf16, col). Legacy HMMA path:
 // the GQA/GEMV operands here are 8-16 rows wide, far from a dense tcgen05
 // M=128 tile, and the kernels are HBM-bound.
+// f16 variants (FP8 KV pages widen to f16: every e4m3 value is exact in f16)
+HX_DEV uint32_t pack_f16(float lo, float hi) {
+  __half2 v = __floats2half2_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+HX_DEV float round_f16f(float x) { return __half2float(__float2half_rn(x)); }
+HX_DEV void split3h(float x, float& hi, float& mid, float& lo) {
+  hi = round_f16f(x);
+  const float r1 = x - hi;
+  mid = round_f16f(r1);
+  lo = round_f16f(r1 - mid);
+}
+HX_DEV void split2h(float x, float& hi, float& lo) {
+  hi = round_f16f(x);
+  lo = round_f16f(x - hi);
+}
+// four e4m3 bytes (byte i = element i) -> two f16x2 (elements 0,1 and 2,3; low half first)
+HX_DEV void e4m3x4_to_f16x2x2(uint32_t four, uint32_t& lo, uint32_t& hi) {
+  asm("{\n .reg .b16 a, b;\n mov.b32 {a, b}, %2;\n cvt.rn.f16x2.e4m3x2 %0, a;\n cvt.rn.f16x2.e4m3x2 %1, b;\n}"
+      : "=r"(lo), "=r"(hi)
+      : "r"(four));
+}
+// x = hi + lo with both halves f16 (22 significant bits), packed per pair
+HX_DEV void split2h_pack(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  const __half2 h = __floats2half2_rn(x0, x1);
+  const float2 hf = __half22float2(h);
+  const __half2 l = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+  hi = *reinterpret_cast<const uint32_t*>(&h);
+  lo = *reinterpret_cast<const uint32_t*>(&l);
+}
+HX_DEV void mma_f16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                          uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 "
+      "{%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
 HX_DEV void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                            uint32_t b0, uint32_t b1) {
   asm volatile(

@@ -117,6 +117,9 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
   if (B_ < 1 || B_ > 64) throw std::invalid_argument("batch must be in [1, 64] for the B200 decode kernels");
   if (cap_ < 1) throw std::invalid_argument("capacity_tokens must be >= 1");
   mla_ = m.kv_latent > 0;
+  if (rt.kv_dtype != HX_KV_BF16 && rt.kv_dtype != HX_KV_FP8_E4M3) throw std::invalid_argument("unknown kv_dtype");
+  kv8_ = rt.kv_dtype == HX_KV_FP8_E4M3;
+  if (kv8_ && mla_) throw std::invalid_argument("FP8 KV pages are implemented for GQA caches (MLA latents stay bf16)");
   if (mla_) {
     // types.hpp:43-49: MLA keeps one latent KV head; Helix needs tpa <= K_eff = 1 (types.cpp:122-139)
     W_ = static_cast<int>(2 * m.kv_latent);
@@ -214,7 +217,7 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
     page_bytes_ = mla_page_bytes();
   } else {
     page_cap_ = static_cast<int>((per_rank_max + 15) / 16 + 1);
-    page_bytes_ = 64u * static_cast<size_t>(DP_);
+    page_bytes_ = page_bytes_kv(DP_, kv8_);
   }
 
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
@@ -405,6 +408,7 @@ void Engine::plan_gemvs() {
     q.p.slot_base = slot_base_;
     q.p.n_local_slots = n_slots_;
     q.p.append = 1;
+    q.p.kv8 = kv8_ ? 1 : 0;
     plan_qkv_.push_back(q);
     if (!attn_only_) {
       if (dist) {
@@ -763,9 +767,12 @@ void Engine::grow_random(int64_t layer, int64_t request, int64_t n, std::mt19937
       for (double& x : vv) x = unit_draw(rng);
       for (double& x : kk) x = unit_draw(rng);
       for (int64_t j = 0; j < per; ++j) {
-        // exact: route the double through its bf16 value (stored format)
-        v[static_cast<size_t>(i * per + j)] = float_from_bf16_bits(bf16_bits_from_double(vv[static_cast<size_t>(j)]));
-        k[static_cast<size_t>(i * per + j)] = float_from_bf16_bits(bf16_bits_from_double(kk[static_cast<size_t>(j)]));
+        // exact: route the double through its stored value (bf16, or e4m3 -- both exact in float)
+        const double dv = vv[static_cast<size_t>(j)], dk = kk[static_cast<size_t>(j)];
+        v[static_cast<size_t>(i * per + j)] =
+            kv8_ ? e4m3_to_float(e4m3_from_double(dv)) : float_from_bf16_bits(bf16_bits_from_double(dv));
+        k[static_cast<size_t>(i * per + j)] =
+            kv8_ ? e4m3_to_float(e4m3_from_double(dk)) : float_from_bf16_bits(bf16_bits_from_double(dk));
       }
     }
     append_kv(layer, request, m, k.data(), v.data());
@@ -781,19 +788,26 @@ void Engine::append_kv(int64_t layer, int64_t request, int64_t n, const float* k
     throw std::invalid_argument("KV capacity exceeded");
   if (n == 0) return;
   const size_t cnt = static_cast<size_t>(n * Kh_ * D_);
-  std::vector<uint16_t> kb(cnt), vb(cnt);
+  const size_t esz = kv8_ ? 1 : 2;  // stored element bytes
+  std::vector<uint8_t> kb(cnt * esz), vb(cnt * esz);
   for (size_t i = 0; i < cnt; ++i) {
-    kb[i] = bf16_bits_from_float(k[i]);
-    vb[i] = bf16_bits_from_float(v[i]);
+    if (kv8_) {  // e4m3 RNE of the float value (fp8.cuh)
+      kb[i] = e4m3_from_double(static_cast<double>(k[i]));
+      vb[i] = e4m3_from_double(static_cast<double>(v[i]));
+    } else {
+      const uint16_t kh = bf16_bits_from_float(k[i]), vh = bf16_bits_from_float(v[i]);
+      std::memcpy(&kb[2 * i], &kh, 2);
+      std::memcpy(&vb[2 * i], &vh, 2);
+    }
   }
-  uint16_t *dk = nullptr, *dv = nullptr;
-  cuda_check(cudaMalloc(&dk, cnt * 2), "append staging");
-  cuda_check(cudaMalloc(&dv, cnt * 2), "append staging");
-  cuda_check(cudaMemcpyAsync(dk, kb.data(), cnt * 2, cudaMemcpyHostToDevice, stream_), "append h2d");
-  cuda_check(cudaMemcpyAsync(dv, vb.data(), cnt * 2, cudaMemcpyHostToDevice, stream_), "append h2d");
+  uint8_t *dk = nullptr, *dv = nullptr;
+  cuda_check(cudaMalloc(&dk, cnt * esz), "append staging");
+  cuda_check(cudaMalloc(&dv, cnt * esz), "append staging");
+  cuda_check(cudaMemcpyAsync(dk, kb.data(), cnt * esz, cudaMemcpyHostToDevice, stream_), "append h2d");
+  cuda_check(cudaMemcpyAsync(dv, vb.data(), cnt * esz, cudaMemcpyHostToDevice, stream_), "append h2d");
   cuda_check(launch_kv_append_rows(kv_[layer], dk, dv, static_cast<int>(n), static_cast<int>(request),
                                    d_total_ + layer * B_, B_, static_cast<int>(Kh_), kvh_per_slot_, kvp_,
-                                   chunk_, static_cast<int>(D_), DP_, page_cap_, slot_base_, n_slots_,
+                                   chunk_, static_cast<int>(D_), DP_, page_cap_, slot_base_, n_slots_, kv8_,
                                    stream_),
              "append kernel");
   cuda_check(cudaStreamSynchronize(stream_), "append sync");
@@ -815,7 +829,7 @@ void Engine::fill_kv_hash(int64_t n, uint64_t seed) {
   for (int64_t l = 0; l < L_ && !mla_; ++l) {
     cuda_check(launch_kv_fill_hash(kv_[l], d_total_ + l * B_, B_, static_cast<int>(Kh_), kvh_per_slot_, kvp_,
                                    chunk_, static_cast<int>(D_), DP_, page_cap_, slot_base_, n_slots_, n, seed,
-                                   hash_stream(kCacheK, l), hash_stream(kCacheV, l), stream_),
+                                   hash_stream(kCacheK, l), hash_stream(kCacheV, l), kv8_, stream_),
                "kv fill");
     for (int b = 0; b < B_; ++b) h_total_[static_cast<size_t>(l * B_ + b)] += n;
   }
@@ -883,11 +897,18 @@ void Engine::read_kv(int64_t layer, int64_t request, int64_t rank, int64_t head,
   for (int64_t t = 0; t < n; ++t) {
     const uint8_t* page = buf.data() + static_cast<size_t>(t / 16) * page_bytes_;
     for (int d = 0; d < D_; ++d) {
-      uint16_t kb, vb;
-      std::memcpy(&kb, page + k_offset(DP_, static_cast<int>(t % 16), d), 2);
-      std::memcpy(&vb, page + v_offset(DP_, static_cast<int>(t % 16), d), 2);
-      k[t * D_ + d] = float_from_bf16_bits(kb);
-      v[t * D_ + d] = float_from_bf16_bits(vb);
+      const uint8_t* pk = page + kv_offset(DP_, static_cast<int>(t % 16), d, false, kv8_);
+      const uint8_t* pv = page + kv_offset(DP_, static_cast<int>(t % 16), d, true, kv8_);
+      if (kv8_) {
+        k[t * D_ + d] = e4m3_to_float(*pk);
+        v[t * D_ + d] = e4m3_to_float(*pv);
+      } else {
+        uint16_t kb, vb;
+        std::memcpy(&kb, pk, 2);
+        std::memcpy(&vb, pv, 2);
+        k[t * D_ + d] = float_from_bf16_bits(kb);
+        v[t * D_ + d] = float_from_bf16_bits(vb);
+      }
     }
   }
 }
@@ -938,6 +959,7 @@ AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) {
   a.group = G_;
   a.q_chunks = q_chunks_;
   a.qrows = q_rows_;
+  a.kv8 = kv8_ ? 1 : 0;
   a.kvh_per_slot = kvh_per_slot_;
   a.q_per_slot = q_per_slot_;
   a.kvp = kvp_;
@@ -1285,6 +1307,7 @@ void Engine::info(hx_engine_info* o) const {
     o->kernels_per_step = 1 + L_ * (13 + (hopb_ ? 3 * (B_ - 1) : 0)) + 3;
   o->page_cap = page_cap_;
   o->head_dim_padded = DP_;
+  o->kv_dtype = kv8_ ? HX_KV_FP8_E4M3 : HX_KV_BF16;
 }
 
 }  // namespace hx

@@ -100,6 +100,7 @@ class Engine {
   int64_t cap_;
   int device_;
   bool hopb_, graphs_;
+  bool kv8_ = false;  // FP8 e4m3 GQA pages (hx_runtime_config.kv_dtype)
   int DP_, G_, q_rows_, q_chunks_, kvh_per_slot_, q_per_slot_, n_slots_, slot_base_;
   int page_cap_;
   size_t page_bytes_;

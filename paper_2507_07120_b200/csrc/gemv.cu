@@ -358,9 +358,12 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
             const size_t page =
                 ((static_cast<size_t>(slot_local) * p.batch + b) * p.kvh_per_slot + kvh) * p.page_cap +
                 static_cast<size_t>(row >> 4);
-            const uint32_t off = is_v ? v_offset(p.dp, static_cast<int>(row & 15), d)
-                                      : k_offset(p.dp, static_cast<int>(row & 15), d);
-            *reinterpret_cast<__nv_bfloat16*>(p.kv + page * page_bytes(p.dp) + off) = __float2bfloat16_rn(y[0]);
+            uint8_t* dst = p.kv + page * page_bytes_kv(p.dp, p.kv8 != 0) +
+                           kv_offset(p.dp, static_cast<int>(row & 15), d, is_v != 0, p.kv8 != 0);
+            if (p.kv8)
+              *dst = e4m3_from_double(static_cast<double>(y[0]));
+            else
+              *reinterpret_cast<__nv_bfloat16*>(dst) = __float2bfloat16_rn(y[0]);
           }
         }
       }

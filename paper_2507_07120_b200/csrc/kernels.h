@@ -55,6 +55,7 @@ struct AttnParams {
   int stream_batch;        // (HOP-B launches one request at a time)
   const uint8_t* qimg;     // MLA: [B] absorbed-query images (kv_layout.cuh mla_q_offset)
   int qrows;               // GQA: query rows per stream (8, or 16 when the group exceeds 8)
+  int kv8;                 // GQA: FP8 (e4m3) pages (kv_layout.cuh), f16 MMAs
 };
 cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t stream);
 // MLA (tcgen05): items = (split, stream, value half); part_o [n_items][128][256],
@@ -112,6 +113,7 @@ struct GemvParams {
   int nq, nk, kv_heads, kvh_per_slot, rr_chunk, page_cap, slot_base, n_local_slots;
   int kv_head_base;      // global index of the first KV head in this projection
   int append;            // write K/V into the cache
+  int kv8;               // GQA cache pages are FP8 e4m3 (fp8.cuh), else bf16
   uint8_t* q_img;        // MLA (mla = 1): q -> bf16 query images, latent -> MLA pages
   int mla;
   int kvp, head_dim, dp;
@@ -159,16 +161,16 @@ cudaError_t launch_argmax_finish(const unsigned long long* best, int batch, int*
                                  unsigned long long* best_reset, cudaStream_t stream);
 // Scatter n tokens (bf16 K/V rows [n][kv_heads][head_dim]) of request b at global
 // positions total[b] .. total[b]+n-1 into the round-robin page pool, then bump total.
-cudaError_t launch_kv_append_rows(uint8_t* kv, const uint16_t* k_rows, const uint16_t* v_rows,
+cudaError_t launch_kv_append_rows(uint8_t* kv, const void* k_rows, const void* v_rows,
                                   int n, int b, int* total, int batch, int kv_heads,
                                   int kvh_per_slot, int kvp, int chunk, int head_dim, int dp,
-                                  int page_cap, int slot_base, int n_local_slots,
+                                  int page_cap, int slot_base, int n_local_slots, bool fp8,
                                   cudaStream_t stream);
 // Device-side synthetic fill: tokens [t0, t0+n) of every request from the hash RNG.
 cudaError_t launch_kv_fill_hash(uint8_t* kv, int* total, int batch, int kv_heads,
                                 int kvh_per_slot, int kvp, int chunk, int head_dim, int dp,
                                 int page_cap, int slot_base, int n_local_slots, long long n,
-                                uint64_t seed, uint64_t stream_k, uint64_t stream_v,
+                                uint64_t seed, uint64_t stream_k, uint64_t stream_v, bool fp8,
                                 cudaStream_t stream);
 // Weight init from the hash RNG straight into the fragment-major layout.
 // Segment list maps combined rows to (hash stream, column count, column offset).

@@ -18,6 +18,8 @@
 
 #include <stdint.h>
 
+#include "fp8.cuh"
+
 namespace hx {
 
 __host__ __device__ __forceinline__ uint32_t page_bytes(int dp) { return 64u * static_cast<uint32_t>(dp); }
@@ -40,6 +42,19 @@ __host__ __device__ __forceinline__ uint32_t v_offset(int dp, int t, int d) {
   const int half = tt >> 3, c = (tt & 7) >> 1, elem = tt & 1;
   const int lane = g * 4 + c;
   return static_cast<uint32_t>(32 * dp + (nd2 * 32 + lane) * 16 + (sub * 2 + half) * 4 + elem * 2);
+}
+
+// FP8 (e4m3, fp8.cuh) pages: the same fragment order with 1-byte elements --
+// every lane's 16-byte bf16 chunk becomes an 8-byte chunk, so each offset is
+// exactly half of its bf16 offset and a page is 32*DP bytes. A consumer lane
+// reads its 8 bytes and widens them (cvt e4m3x2 -> f16x2) into the register
+// image the f16 mma.sync B-operands need.
+__host__ __device__ __forceinline__ uint32_t page_bytes_kv(int dp, bool fp8) {
+  return (fp8 ? 32u : 64u) * static_cast<uint32_t>(dp);
+}
+__host__ __device__ __forceinline__ uint32_t kv_offset(int dp, int t, int d, bool is_v, bool fp8) {
+  const uint32_t off = is_v ? v_offset(dp, t, d) : k_offset(dp, t, d);
+  return fp8 ? off >> 1 : off;
 }
 
 // Round-robin placement (attention.hpp:262-282 in closed form): global token

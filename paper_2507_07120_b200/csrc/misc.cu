@@ -118,7 +118,7 @@ cudaError_t launch_argmax_finish(const unsigned long long* best, int batch, int*
 __device__ __forceinline__ uint8_t* kv_elem_ptr(uint8_t* kv, long long g, int b, int h, int d,
                                                 int is_v, int batch, int kvh_per_slot, int kvp,
                                                 int chunk, int dp, int page_cap, int slot_base,
-                                                int n_local_slots) {
+                                                int n_local_slots, bool fp8) {
   const int rank = rr_rank(g, chunk, kvp);
   const long long row = rr_row(g, chunk, kvp);
   const int grp = h / kvh_per_slot, kvh = h - grp * kvh_per_slot;
@@ -127,15 +127,14 @@ __device__ __forceinline__ uint8_t* kv_elem_ptr(uint8_t* kv, long long g, int b,
   const size_t page =
       ((static_cast<size_t>(slot_local) * batch + b) * kvh_per_slot + kvh) * page_cap +
       static_cast<size_t>(row >> 4);
-  const uint32_t off = is_v ? v_offset(dp, static_cast<int>(row & 15), d)
-                            : k_offset(dp, static_cast<int>(row & 15), d);
-  return kv + page * page_bytes(dp) + off;
+  return kv + page * page_bytes_kv(dp, fp8) + kv_offset(dp, static_cast<int>(row & 15), d, is_v != 0, fp8);
 }
 
-__global__ void kv_append_rows_kernel(uint8_t* kv, const uint16_t* k_rows, const uint16_t* v_rows,
+// k_rows / v_rows: bf16 bits (2 bytes per element) or e4m3 codes (fp8 pages, 1 byte)
+__global__ void kv_append_rows_kernel(uint8_t* kv, const void* k_rows, const void* v_rows,
                                       int n, int b, const int* total, int batch, int kv_heads,
                                       int kvh_per_slot, int kvp, int chunk, int head_dim, int dp,
-                                      int page_cap, int slot_base, int n_local_slots) {
+                                      int page_cap, int slot_base, int n_local_slots, bool fp8) {
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long per_tok = static_cast<long long>(kv_heads) * head_dim;
   if (idx >= n * per_tok) return;
@@ -144,26 +143,31 @@ __global__ void kv_append_rows_kernel(uint8_t* kv, const uint16_t* k_rows, const
   const int h = hd / head_dim, d = hd - h * head_dim;
   const long long g = static_cast<long long>(total[b]) + i;
   uint8_t* pk = kv_elem_ptr(kv, g, b, h, d, 0, batch, kvh_per_slot, kvp, chunk, dp, page_cap,
-                            slot_base, n_local_slots);
+                            slot_base, n_local_slots, fp8);
   if (!pk) return;
   uint8_t* pv = kv_elem_ptr(kv, g, b, h, d, 1, batch, kvh_per_slot, kvp, chunk, dp, page_cap,
-                            slot_base, n_local_slots);
-  *reinterpret_cast<uint16_t*>(pk) = k_rows[idx];
-  *reinterpret_cast<uint16_t*>(pv) = v_rows[idx];
+                            slot_base, n_local_slots, fp8);
+  if (fp8) {
+    *pk = static_cast<const uint8_t*>(k_rows)[idx];
+    *pv = static_cast<const uint8_t*>(v_rows)[idx];
+  } else {
+    *reinterpret_cast<uint16_t*>(pk) = static_cast<const uint16_t*>(k_rows)[idx];
+    *reinterpret_cast<uint16_t*>(pv) = static_cast<const uint16_t*>(v_rows)[idx];
+  }
 }
 
 __global__ void add_total_kernel(int* total, int b, int n) { total[b] += n; }
 
-cudaError_t launch_kv_append_rows(uint8_t* kv, const uint16_t* k_rows, const uint16_t* v_rows,
+cudaError_t launch_kv_append_rows(uint8_t* kv, const void* k_rows, const void* v_rows,
                                   int n, int b, int* total, int batch, int kv_heads,
                                   int kvh_per_slot, int kvp, int chunk, int head_dim, int dp,
-                                  int page_cap, int slot_base, int n_local_slots,
+                                  int page_cap, int slot_base, int n_local_slots, bool fp8,
                                   cudaStream_t stream) {
   const long long work = static_cast<long long>(n) * kv_heads * head_dim;
   if (work > 0) {
     kv_append_rows_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(
         kv, k_rows, v_rows, n, b, total, batch, kv_heads, kvh_per_slot, kvp, chunk, head_dim, dp,
-        page_cap, slot_base, n_local_slots);
+        page_cap, slot_base, n_local_slots, fp8);
   }
   add_total_kernel<<<1, 1, 0, stream>>>(total, b, n);
   return cudaGetLastError();
@@ -178,17 +182,19 @@ __device__ __forceinline__ long long rr_global_of_row(long long row, int rank, i
   return (row / chunk) * static_cast<long long>(chunk) * kvp + static_cast<long long>(rank) * chunk + row % chunk;
 }
 
-__device__ __forceinline__ uint16_t hash_bf16_bits(uint64_t sseed, uint64_t index) {
+__device__ __forceinline__ double hash_kv_unit(uint64_t sseed, uint64_t index) {
   const uint64_t z = splitmix64(sseed + index);
-  const double u = 2.0 * (static_cast<double>(z >> 11) * 0x1.0p-53) - 1.0;
-  const __nv_bfloat16 h = double_to_bf16_rne(u);
+  return 2.0 * (static_cast<double>(z >> 11) * 0x1.0p-53) - 1.0;
+}
+__device__ __forceinline__ uint16_t hash_bf16_bits(uint64_t sseed, uint64_t index) {
+  const __nv_bfloat16 h = double_to_bf16_rne(hash_kv_unit(sseed, index));
   return *reinterpret_cast<const uint16_t*>(&h);
 }
 
 __global__ void kv_fill_hash_kernel(uint8_t* kv, const int* total, int batch, int kv_heads,
                                     int kvh_per_slot, int kvp, int chunk, int head_dim, int dp,
                                     int page_cap, int slot_base, int n_local_slots, long long n,
-                                    uint64_t seed, uint64_t stream_k, uint64_t stream_v) {
+                                    uint64_t seed, uint64_t stream_k, uint64_t stream_v, bool fp8) {
   const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const long long streams = static_cast<long long>(n_local_slots) * batch * kvh_per_slot;
@@ -210,12 +216,14 @@ __global__ void kv_fill_hash_kernel(uint8_t* kv, const int* total, int batch, in
   const uint64_t kseed = splitmix64(seed ^ (stream_k * 0xD1B54A32D192ED03ull));
   const uint64_t vseed = splitmix64(seed ^ (stream_v * 0xD1B54A32D192ED03ull));
   const uint64_t base = static_cast<uint64_t>(b * kv_heads + h) << 32;
-  uint8_t* pg = kv + (static_cast<size_t>(stream_idx) * page_cap + page) * page_bytes(dp);
-  const int chunks = 64 * dp / 16;  // 16-byte chunks per page
+  uint8_t* pg = kv + (static_cast<size_t>(stream_idx) * page_cap + page) * page_bytes_kv(dp, fp8);
+  const int chunks = 64 * dp / 16;  // 8-element lane chunks per page (16 B bf16, 8 B fp8)
   for (int ci = lane; ci < chunks; ci += 32) {
     uint4* dst = reinterpret_cast<uint4*>(pg + ci * 16);
-    uint4 old = full ? make_uint4(0, 0, 0, 0) : *dst;
+    uint2* dst8 = reinterpret_cast<uint2*>(pg + ci * 8);
+    uint4 old = full ? make_uint4(0, 0, 0, 0) : (fp8 ? make_uint4(dst8->x, dst8->y, 0, 0) : *dst);
     uint16_t* ov = reinterpret_cast<uint16_t*>(&old);
+    uint8_t* ov8 = reinterpret_cast<uint8_t*>(&old);
     const int is_v = ci >= chunks / 2;
     const int cl = is_v ? ci - chunks / 2 : ci;
     const int ln = cl & 31, grpi = cl >> 5;
@@ -237,14 +245,23 @@ __global__ void kv_fill_hash_kernel(uint8_t* kv, const int* total, int batch, in
       const long long gtok = rr_global_of_row(16ll * page + t, rank, chunk, kvp);
       if (gtok < t0 || gtok >= t1) continue;
       if (d >= head_dim) {
-        ov[e] = 0;
+        if (fp8)
+          ov8[e] = 0;
+        else
+          ov[e] = 0;
         continue;
       }
       const uint64_t index = (base + static_cast<uint64_t>(gtok)) * static_cast<uint64_t>(head_dim) +
                              static_cast<uint64_t>(d);
-      ov[e] = hash_bf16_bits(is_v ? vseed : kseed, index);
+      if (fp8)
+        ov8[e] = e4m3_from_double(hash_kv_unit(is_v ? vseed : kseed, index));
+      else
+        ov[e] = hash_bf16_bits(is_v ? vseed : kseed, index);
     }
-    *dst = old;
+    if (fp8)
+      *dst8 = make_uint2(old.x, old.y);
+    else
+      *dst = old;
   }
 }
 
@@ -255,13 +272,13 @@ __global__ void add_total_all_kernel(int* total, int batch, int n) {
 cudaError_t launch_kv_fill_hash(uint8_t* kv, int* total, int batch, int kv_heads,
                                 int kvh_per_slot, int kvp, int chunk, int head_dim, int dp,
                                 int page_cap, int slot_base, int n_local_slots, long long n,
-                                uint64_t seed, uint64_t stream_k, uint64_t stream_v,
+                                uint64_t seed, uint64_t stream_k, uint64_t stream_v, bool fp8,
                                 cudaStream_t stream) {
   const long long work = static_cast<long long>(n_local_slots) * batch * kvh_per_slot * page_cap * 32;
   if (n > 0)
     kv_fill_hash_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(
         kv, total, batch, kv_heads, kvh_per_slot, kvp, chunk, head_dim, dp, page_cap, slot_base,
-        n_local_slots, n, seed, stream_k, stream_v);
+        n_local_slots, n, seed, stream_k, stream_v, fp8);
   add_total_all_kernel<<<1, 64, 0, stream>>>(total, batch, static_cast<int>(n));
   return cudaGetLastError();
 }

@@ -12,7 +12,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from ._lib import (EngineInfo, ModelConfig, ParallelConfig, RuntimeConfig, check, lib)
+from ._lib import (KV_DTYPES, EngineInfo, ModelConfig, ParallelConfig, RuntimeConfig, check, lib)
 
 _fp = C.POINTER(C.c_float)
 
@@ -61,15 +61,17 @@ class MsgKind:
 
 class _Engine:
     def __init__(self, model, tpa, kvp, chunk_size, batch, capacity, device=0, use_graphs=True, hopb=False,
-                 pool=0, rank=0, nccl_id=None, loopback=None, ep=1):
+                 pool=0, rank=0, nccl_id=None, loopback=None, ep=1, kv_dtype="bf16"):
         self.mc = model
         self._nccl_buf = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         self._loopback = loopback  # the group must outlive its engines
         self.pc = ParallelConfig(tpa=tpa, kvp=kvp, chunk_size=chunk_size, distributed=pool, rank=rank,
                                  nccl_unique_id=C.cast(self._nccl_buf, C.c_void_p) if nccl_id is not None else None,
                                  loopback=loopback._h if loopback is not None else None, ep=ep)
+        if kv_dtype not in KV_DTYPES:
+            raise ValueError(f"kv_dtype must be one of {sorted(KV_DTYPES)}")
         self.rc = RuntimeConfig(batch=batch, capacity_tokens=capacity, device=device, hopb=int(hopb),
-                                use_graphs=int(use_graphs))
+                                use_graphs=int(use_graphs), kv_dtype=KV_DTYPES[kv_dtype])
         h = C.c_void_p()
         check(lib().hx_engine_create(C.byref(self.mc), C.byref(self.pc), C.byref(self.rc), C.byref(h)))
         self._h = h
@@ -108,14 +110,14 @@ class DecodeHarness(_Engine):
     W_q/W_k/W_v are the reference's own mt19937_64(seed) draws, stored bf16.
     """
 
-    def __init__(self, dims, tpa, kvp, chunk_size, seed, batch=1, capacity=4096, device=0):
+    def __init__(self, dims, tpa, kvp, chunk_size, seed, batch=1, capacity=4096, device=0, kv_dtype="bf16"):
         if not isinstance(dims, Dims):
             dims = Dims(*dims)
         self.dims = dims
         mc = ModelConfig(hidden=dims.query_heads * dims.head_size, query_heads=dims.query_heads,
                          kv_heads=dims.kv_heads, head_size=dims.head_size, ffn=16, layers=1, vocab=1,
                          attention_only=1)
-        super().__init__(mc, tpa, kvp, chunk_size, batch, capacity, device, use_graphs=False)
+        super().__init__(mc, tpa, kvp, chunk_size, batch, capacity, device, use_graphs=False, kv_dtype=kv_dtype)
         self._tpa, self._kvp = tpa, kvp
         self._check(lib().hx_init_weights_mt19937(self._h, seed))
 

@@ -29,6 +29,9 @@ def lib():
             "oracle_rng_unit_draw": (C.c_double, [vp]),
             "oracle_rng_next": (u64, [vp]),
             "oracle_round_bf16": (C.c_double, [C.c_double]),
+            "oracle_round_e4m3": (C.c_double, [C.c_double]),
+            "oracle_harness_set_kv_fp8": (None, [vp, C.c_int]),
+            "oracle_model_set_kv_fp8": (None, [vp, C.c_int]),
             "oracle_harness_create": (C.c_int, [i64, i64, i64, i64, i64, i64, u64, C.c_int, C.POINTER(vp)]),
             "oracle_harness_free": (None, [vp]),
             "oracle_harness_grow_random": (C.c_int, [vp, i64, vp]),
@@ -102,6 +105,11 @@ class Rng:
             pass
 
 
+def round_e4m3(a):
+    f = np.vectorize(lib().oracle_round_e4m3)
+    return f(np.asarray(a, dtype=np.float64))
+
+
 def round_bf16(a):
     f = np.vectorize(lib().oracle_round_bf16)
     return f(np.asarray(a, dtype=np.float64))
@@ -110,10 +118,12 @@ def round_bf16(a):
 class Harness:
     """Oracle DecodeHarness<double> (attention.hpp:419-563)."""
 
-    def __init__(self, q, k, hsz, tpa, kvp, chunk, seed, bf16=False):
+    def __init__(self, q, k, hsz, tpa, kvp, chunk, seed, bf16=False, kv_fp8=False):
         self.q, self.k, self.hsz, self.tpa, self.kvp = q, k, hsz, tpa, kvp
         h = C.c_void_p()
         check(lib().oracle_harness_create(q, k, hsz, tpa, kvp, chunk, seed, int(bf16), C.byref(h)))
+        if kv_fp8:
+            lib().oracle_harness_set_kv_fp8(h, 1)
         self.h = h
 
     @property
@@ -233,7 +243,7 @@ class Model:
     WEIGHTS = {"wq": 0, "wk": 1, "wv": 2, "wo": 3, "wgate": 4, "wup": 5, "wdown": 6, "emb": 7, "lm": 8}
 
     def __init__(self, hidden, q, k, hsz, ffn, layers, vocab, tpa=1, kvp=1, chunk=16, batch=1,
-                 seed=0, qkv_hash=False, bf16=True, moe=None, kv_latent=0):
+                 seed=0, qkv_hash=False, bf16=True, moe=None, kv_latent=0, kv_fp8=False):
         """moe = (n_experts, top_k, expert_ffn): every layer's FFN is routed MoE,
         `ffn` is then the shared expert width (0: none). kv_latent > 0: MLA
         attention with latent width 2*kv_latent (layer_oracle.hpp)."""
@@ -252,6 +262,8 @@ class Model:
         else:
             check(lib().oracle_model_create(hidden, q, k, hsz, ffn, layers, vocab, tpa, kvp, chunk, batch,
                                             seed, int(qkv_hash), int(bf16), C.byref(h)))
+        if kv_fp8:
+            lib().oracle_model_set_kv_fp8(h, 1)
         self.h = h
 
     def routes(self):
