@@ -91,20 +91,32 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 
 }  // namespace
 
-template <int DP, int NWC, int NSTAGE, int QC, bool KV8>
+// W16 (bf16 pages, 9-16 query heads per KV head): every consumer warp takes
+// one page per stage for ALL 16 query rows. The three bf16 terms of the query
+// (hi/mid/lo) are three 16-row M-tiles accumulated into ONE S fragment (rows =
+// queries), and P's hi/lo tiles into one O fragment, so a page costs
+// 3·2·KS + 2·ND MMAs (80 at Hsz 128) instead of two 8-row passes (96); the
+// per-item query fragment image (3 terms x KS k-steps x 32 lanes x 16 B) lives
+// in shared memory, keeping registers at the 8-row path's level.
+template <int DP, int NWC, int NSTAGE, int QC, bool KV8, bool W16>
 __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const AttnParams p) {
   using Cfg = AttnCfg<DP, KV8>;
   static_assert(NWC % QC == 0, "query chunks must divide the consumer warps");
+  static_assert(!W16 || (QC == 2 && !KV8), "W16: 16 query rows of bf16 pages");
   constexpr int QR = 8 * QC;           // query rows per item
   constexpr int WPC = NWC / QC;        // warps (pages per stage slot) per query chunk
+  constexpr int SR = W16 ? 16 : 8;     // query rows per warp
   constexpr uint32_t STAGE_KV = NWC * Cfg::PAGE;
   constexpr uint32_t Q_BYTES = QR * DP * 4;
   constexpr uint32_t STAGE_BYTES = STAGE_KV + Q_BYTES;
+  constexpr int WS = SR * DP + 2 * SR; // per-warp combine scratch (floats): O rows, m, l
+  constexpr uint32_t QIMG_BYTES = W16 ? 3u * Cfg::KS * 32u * 16u : 0u;
 
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem;                                                     // NSTAGE * STAGE_BYTES
-  float* scratch = reinterpret_cast<float*>(smem + NSTAGE * STAGE_BYTES);     // NWC * (8*DP + 16)
-  StageMeta* meta = reinterpret_cast<StageMeta*>(scratch + NWC * (8 * DP + 16));
+  float* scratch = reinterpret_cast<float*>(smem + NSTAGE * STAGE_BYTES);     // NWC * WS
+  uint4* qimg = reinterpret_cast<uint4*>(scratch + NWC * WS);                 // W16: [3][KS][32]
+  StageMeta* meta = reinterpret_cast<StageMeta*>(reinterpret_cast<uint8_t*>(qimg) + QIMG_BYTES);
   uint64_t* full = reinterpret_cast<uint64_t*>(meta + NSTAGE);
   uint64_t* empty = full + NSTAGE;
 
@@ -193,6 +205,189 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           if (qbytes) bulk_g2s(dst + STAGE_KV, q_src, qbytes, &full[s]);
         }
         if (done) break;
+      }
+    }
+  } else if constexpr (W16) {
+    // ------------------------------------------------------------ consumers, 16 query rows per warp
+    const int g = lane >> 2, c = lane & 3;
+    float acc[Cfg::ND][4];           // rows g (query g) and g+8 (query g+8)
+    float m_ref[2] = {-INFINITY, -INFINITY}, l_sum[2] = {0.f, 0.f};
+    const uint32_t stage_base = smem_u32(stages);
+    const uint32_t qimg_base = smem_u32(qimg);
+    for (int st = 0;; ++st) {
+      const int s = st % NSTAGE;
+      mbar_wait(&full[s], (st / NSTAGE) & 1);
+      const StageMeta m = meta[s];
+      if (m.item == kItemDone) break;
+      const uint32_t sbase = stage_base + s * STAGE_BYTES;
+      if (m.first) {
+        // query fragment image: warp w builds k-steps w, w + NWC, ... of all three terms
+        const float* qs = reinterpret_cast<const float*>(stages + s * STAGE_BYTES + STAGE_KV);
+        for (int ks = warp; ks < Cfg::KS; ks += NWC) {
+          float t[3][2][4];  // [term][row g / g+8][d0, d0+1, d0+8, d0+9]
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const int row = g + 8 * r;
+            const bool valid = row < m.rows;
+            const int d0 = ks * 16 + 2 * c;
+            const int dd[4] = {d0, d0 + 1, d0 + 8, d0 + 9};
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+              const float v = valid ? qs[row * DP + dd[i]] * p.qscale : 0.f;
+              split3(v, t[0][r][i], t[1][r][i], t[2][r][i]);
+            }
+          }
+#pragma unroll
+          for (int term = 0; term < 3; ++term)
+            qimg[(term * Cfg::KS + ks) * 32 + lane] =
+                make_uint4(pack_bf16(t[term][0][0], t[term][0][1]), pack_bf16(t[term][1][0], t[term][1][1]),
+                           pack_bf16(t[term][0][2], t[term][0][3]), pack_bf16(t[term][1][2], t[term][1][3]));
+        }
+        named_bar_sync(1, NWC * 32);  // image complete before any warp's first page
+#pragma unroll
+        for (int nd = 0; nd < Cfg::ND; ++nd) acc[nd][0] = acc[nd][1] = acc[nd][2] = acc[nd][3] = 0.f;
+        m_ref[0] = m_ref[1] = -INFINITY;
+        l_sum[0] = l_sum[1] = 0.f;
+      }
+      if (warp < m.npages) {
+        const uint32_t pbase = sbase + warp * Cfg::PAGE;
+        const int tok0 = (m.page0 + warp) * 16;
+        const int valid_tok = m.ntok - tok0;  // >= 1
+        // ---- S = Q K^T: three query terms accumulate into one fragment
+        float sacc[2][4];
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) sacc[nt][0] = sacc[nt][1] = sacc[nt][2] = sacc[nt][3] = 0.f;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+#pragma unroll
+          for (int kp = 0; kp < Cfg::KS / 2; ++kp) {
+            const uint4 kf = lds128(pbase + ((nt * (Cfg::KS / 2) + kp) * 32 + lane) * 16);
+#pragma unroll
+            for (int term = 0; term < 3; ++term) {
+              const uint4 qa = lds128(qimg_base + ((term * Cfg::KS + 2 * kp) * 32 + lane) * 16);
+              mma_bf16_16816(sacc[nt], qa.x, qa.y, qa.z, qa.w, kf.x, kf.y);
+              const uint4 qb = lds128(qimg_base + ((term * Cfg::KS + 2 * kp + 1) * 32 + lane) * 16);
+              mma_bf16_16816(sacc[nt], qb.x, qb.y, qb.z, qb.w, kf.z, kf.w);
+            }
+          }
+        }
+        // logits (log2 units): query g -> sacc[nt][0..1], query g+8 -> sacc[nt][2..3];
+        // tokens 2c, 2c+1 (nt 0) and 8+2c, 9+2c (nt 1)
+        float sv[2][4];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          sv[r][0] = sacc[0][2 * r];
+          sv[r][1] = sacc[0][2 * r + 1];
+          sv[r][2] = sacc[1][2 * r];
+          sv[r][3] = sacc[1][2 * r + 1];
+          if (valid_tok < 16) {
+            if (2 * c >= valid_tok) sv[r][0] = -INFINITY;
+            if (2 * c + 1 >= valid_tok) sv[r][1] = -INFINITY;
+            if (8 + 2 * c >= valid_tok) sv[r][2] = -INFINITY;
+            if (9 + 2 * c >= valid_tok) sv[r][3] = -INFINITY;
+          }
+        }
+        float mx[2];
+        bool grow[2];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          mx[r] = fmaxf(fmaxf(sv[r][0], sv[r][1]), fmaxf(sv[r][2], sv[r][3]));
+          mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 1));
+          mx[r] = fmaxf(mx[r], __shfl_xor_sync(0xffffffffu, mx[r], 2));
+          grow[r] = mx[r] > m_ref[r] + 8.f;  // lazy rescale, as the 8-row path
+        }
+        if (__any_sync(0xffffffffu, grow[0] || grow[1])) {
+          float alpha[2];
+#pragma unroll
+          for (int r = 0; r < 2; ++r) {
+            const float m_new = grow[r] ? mx[r] : m_ref[r];
+            alpha[r] = fast_exp2(m_ref[r] - m_new);  // 0 when m_ref = -inf
+            l_sum[r] *= alpha[r];
+            m_ref[r] = m_new;
+          }
+#pragma unroll
+          for (int nd = 0; nd < Cfg::ND; ++nd) {
+            acc[nd][0] *= alpha[0];
+            acc[nd][1] *= alpha[0];
+            acc[nd][2] *= alpha[1];
+            acc[nd][3] *= alpha[1];
+          }
+        }
+        float ph[2][4], pl[2][4];
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float pv = fast_exp2(sv[r][i] - m_ref[r]);
+            l_sum[r] += pv;
+            split2(pv, ph[r][i], pl[r][i]);
+          }
+        }
+        // P A-fragments (rows = queries g, g+8; k = tokens): hi tile and lo tile
+        const uint32_t h0 = pack_bf16(ph[0][0], ph[0][1]), h1 = pack_bf16(ph[1][0], ph[1][1]);
+        const uint32_t h2 = pack_bf16(ph[0][2], ph[0][3]), h3 = pack_bf16(ph[1][2], ph[1][3]);
+        const uint32_t q0 = pack_bf16(pl[0][0], pl[0][1]), q1 = pack_bf16(pl[1][0], pl[1][1]);
+        const uint32_t q2 = pack_bf16(pl[0][2], pl[0][3]), q3 = pack_bf16(pl[1][2], pl[1][3]);
+        // ---- O += P V
+        const uint32_t vbase = pbase + Cfg::PAGE / 2;
+#pragma unroll
+        for (int nd2 = 0; nd2 < Cfg::ND / 2; ++nd2) {
+          const uint4 vf = lds128(vbase + (nd2 * 32 + lane) * 16);
+          mma_bf16_16816(acc[2 * nd2], h0, h1, h2, h3, vf.x, vf.y);
+          mma_bf16_16816(acc[2 * nd2], q0, q1, q2, q3, vf.x, vf.y);
+          mma_bf16_16816(acc[2 * nd2 + 1], h0, h1, h2, h3, vf.z, vf.w);
+          mma_bf16_16816(acc[2 * nd2 + 1], q0, q1, q2, q3, vf.z, vf.w);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+
+      if (m.last) {
+        // ---- combine the NWC warps' (m, l, O) for the item's 16 rows
+        float* ws = scratch + warp * WS;
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+          float l_tot = l_sum[r];
+          l_tot += __shfl_xor_sync(0xffffffffu, l_tot, 1);
+          l_tot += __shfl_xor_sync(0xffffffffu, l_tot, 2);
+          if (c == 0) {
+            ws[SR * DP + g + 8 * r] = m_ref[r];  // -inf for warps that saw no page
+            ws[SR * DP + SR + g + 8 * r] = l_tot;
+          }
+        }
+#pragma unroll
+        for (int nd = 0; nd < Cfg::ND; ++nd) {
+          const int d = nd * 8 + 2 * c;
+          ws[g * DP + d] = acc[nd][0];
+          ws[g * DP + d + 1] = acc[nd][1];
+          ws[(g + 8) * DP + d] = acc[nd][2];
+          ws[(g + 8) * DP + d + 1] = acc[nd][3];
+        }
+        named_bar_sync(1, NWC * 32);
+        const int rows = m.rows;
+        const size_t obase = static_cast<size_t>(m.item) * QR * DP;
+        for (int idx = threadIdx.x; idx < rows * DP; idx += NWC * 32) {
+          const int q = idx / DP, d = idx - q * DP;
+          float M = -INFINITY;
+#pragma unroll
+          for (int w = 0; w < NWC; ++w) M = fmaxf(M, scratch[w * WS + SR * DP + q]);
+          float L = 0.f, O = 0.f;
+#pragma unroll
+          for (int w = 0; w < NWC; ++w) {
+            const float* wsw = scratch + w * WS;
+            const float mw = wsw[SR * DP + q];
+            const float e = mw == -INFINITY ? 0.f : fast_exp2(mw - M);
+            L += wsw[SR * DP + SR + q] * e;
+            O += wsw[q * DP + d] * e;
+          }
+          p.part_o[obase + idx] = O / L;
+          if (d == 0) p.part_lse2[static_cast<size_t>(m.item) * QR + q] = M + __log2f(L);
+        }
+        named_bar_sync(1, NWC * 32);
+        m_ref[0] = m_ref[1] = -INFINITY;
+        l_sum[0] = l_sum[1] = 0.f;
+#pragma unroll
+        for (int nd = 0; nd < Cfg::ND; ++nd) acc[nd][0] = acc[nd][1] = acc[nd][2] = acc[nd][3] = 0.f;
       }
     }
   } else {
@@ -333,7 +528,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
 
       if (m.last) {
         // ---- combine the NWC warps' (m, l, O) for this item
-        float* ws = scratch + warp * (8 * DP + 16);
+        float* ws = scratch + warp * WS;
         float l_tot = l_sum;
         l_tot += __shfl_xor_sync(0xffffffffu, l_tot, 1);
         l_tot += __shfl_xor_sync(0xffffffffu, l_tot, 2);
@@ -355,11 +550,11 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           const int qc = qi >> 3, q = qi & 7;  // chunk qc is combined over warps qc, qc + QC, ...
           float M = -INFINITY;
 #pragma unroll
-          for (int w = qc; w < NWC; w += QC) M = fmaxf(M, scratch[w * (8 * DP + 16) + 8 * DP + q]);
+          for (int w = qc; w < NWC; w += QC) M = fmaxf(M, scratch[w * WS + 8 * DP + q]);
           float L = 0.f, O = 0.f;
 #pragma unroll
           for (int w = qc; w < NWC; w += QC) {
-            const float* wsw = scratch + w * (8 * DP + 16);
+            const float* wsw = scratch + w * WS;
             const float mw = wsw[8 * DP + q];
             const float e = mw == -INFINITY ? 0.f : fast_exp2(mw - M);
             L += wsw[8 * DP + 8 + q] * e;
@@ -490,33 +685,37 @@ __global__ void bump_totals_kernel(int* total, int n) {
 
 // ------------------------------------------------------------------------
 // host launchers
-template <int DP, int NWC, int NSTAGE, int QC, bool KV8>
+template <int DP, int NWC, int NSTAGE, int QC, bool KV8, bool W16>
 static size_t attn_smem_bytes() {
-  return NSTAGE * (NWC * AttnCfg<DP, KV8>::PAGE + QC * 8 * DP * 4) + NWC * (8 * DP + 16) * 4 +
-         NSTAGE * sizeof(StageMeta) + 2 * NSTAGE * 8 + 64;
+  constexpr int SR = W16 ? 16 : 8;
+  return NSTAGE * (NWC * AttnCfg<DP, KV8>::PAGE + QC * 8 * DP * 4) + NWC * (SR * DP + 2 * SR) * 4 +
+         (W16 ? 3 * (DP / 16) * 32 * 16 : 0) + NSTAGE * sizeof(StageMeta) + 2 * NSTAGE * 8 + 64;
 }
 
-template <int DP, int NWC, int NSTAGE, int QC, bool KV8>
+template <int DP, int NWC, int NSTAGE, int QC, bool KV8, bool W16>
 static cudaError_t launch_attn_t(const AttnParams& p, int grid, cudaStream_t stream) {
-  const size_t smem = attn_smem_bytes<DP, NWC, NSTAGE, QC, KV8>();
+  const size_t smem = attn_smem_bytes<DP, NWC, NSTAGE, QC, KV8, W16>();
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<DP, NWC, NSTAGE, QC, KV8>,
+    cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<DP, NWC, NSTAGE, QC, KV8, W16>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  return launch_k(attn_decode_kernel<DP, NWC, NSTAGE, QC, KV8>, dim3(grid), dim3((NWC + 1) * 32), smem, stream, p);
+  return launch_k(attn_decode_kernel<DP, NWC, NSTAGE, QC, KV8, W16>, dim3(grid), dim3((NWC + 1) * 32), smem, stream,
+                  p);
 }
 
-// bf16 pages: 2-4 stages of 8 pages; FP8 pages are half the bytes, so twice the stages in flight
+// bf16 pages: 2-4 stages of 8 pages; FP8 pages are half the bytes, so twice the
+// stages in flight. 9-16 query rows of bf16 pages take the W16 consumers.
 template <int QC, bool KV8>
 static cudaError_t launch_attn_dp(const AttnParams& p, int grid, cudaStream_t stream) {
+  constexpr bool W16 = QC == 2 && !KV8;
   switch (p.dp) {
-    case 32: return launch_attn_t<32, 8, KV8 ? 8 : 4, QC, KV8>(p, grid, stream);
-    case 64: return launch_attn_t<64, 8, KV8 ? 6 : 3, QC, KV8>(p, grid, stream);
-    case 128: return launch_attn_t<128, 8, KV8 ? 4 : 2, QC, KV8>(p, grid, stream);
+    case 32: return launch_attn_t<32, 8, KV8 ? 8 : 4, QC, KV8, W16>(p, grid, stream);
+    case 64: return launch_attn_t<64, 8, KV8 ? 6 : 3, QC, KV8, W16>(p, grid, stream);
+    case 128: return launch_attn_t<128, 8, KV8 ? 4 : 2, QC, KV8, W16>(p, grid, stream);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -549,9 +748,9 @@ bool pdl_enabled() { return g_pdl; }
 
 size_t attn_decode_smem_bytes(int dp) {
   switch (dp) {  // the larger (two query chunks) variant
-    case 32: return attn_smem_bytes<32, 8, 4, 2, false>();
-    case 64: return attn_smem_bytes<64, 8, 3, 2, false>();
-    case 128: return attn_smem_bytes<128, 8, 2, 2, false>();
+    case 32: return attn_smem_bytes<32, 8, 4, 2, false, true>();
+    case 64: return attn_smem_bytes<64, 8, 3, 2, false, true>();
+    case 128: return attn_smem_bytes<128, 8, 2, 2, false, true>();
     default: return 0;
   }
 }
