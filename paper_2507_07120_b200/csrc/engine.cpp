@@ -43,7 +43,11 @@ template <class T>
 T* dalloc(size_t n, const char* what) {
   void* p = nullptr;
   cuda_check(cudaMalloc(&p, n * sizeof(T) + 16), what);
+  // cudaMemset runs on the legacy default stream, which does NOT order against
+  // the engine's non-blocking streams: wait for it, or a large clear (the KV
+  // pool: tens of GB, milliseconds) can land after the first kernels' writes
   cuda_check(cudaMemset(p, 0, n * sizeof(T) + 16), what);
+  cuda_check(cudaDeviceSynchronize(), what);
   return static_cast<T*>(p);
 }
 
@@ -220,6 +224,7 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
     page_bytes_ = page_bytes_kv(DP_, kv8_);
   }
 
+  if (std::getenv("HX_NO_PDL")) set_pdl(false);  // debugging: serialise every launch
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   cudaDeviceProp prop{};
   cuda_check(cudaGetDeviceProperties(&prop, device_), "cudaGetDeviceProperties");
