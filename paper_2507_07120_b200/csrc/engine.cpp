@@ -747,7 +747,11 @@ void Engine::upload_qkv_host(int64_t layer, const std::vector<double>& wq, const
           bf16_bits_from_double(wv[static_cast<size_t>(k) * Kall + k0 + n]);
     }
   }
-  cuda_check(cudaMemcpy(w_qkv_[layer], img.data(), img.size() * 2, cudaMemcpyHostToDevice), "qkv upload");
+  // on the engine stream (a legacy-stream copy from pageable memory may still be
+  // in flight when later kernels on the non-blocking engine stream run)
+  cuda_check(cudaMemcpyAsync(w_qkv_[layer], img.data(), img.size() * 2, cudaMemcpyHostToDevice, stream_),
+             "qkv upload");
+  cuda_check(cudaStreamSynchronize(stream_), "qkv upload sync");
 }
 
 // ---------------------------------------------------------------------------
