@@ -354,7 +354,7 @@ def ours(a):
         uid = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(uid, src=0)
         eng = P.HelixDecoder(spec, tpa=1, kvp=world, batch=B, capacity=cap, layers=L, device=dev, pool=1,
-                             rank=rank, nccl_id=uid[0], hopb=True)
+                             rank=rank, nccl_id=uid[0], hopb=False)  # HOP-B measured below (profiles/r01_hopb_sweep.md)
     else:
         eng = P.HelixDecoder(spec, tpa=1, kvp=1, batch=B, capacity=cap, layers=L, device=dev)
     eng.init_weights(2507, qkv="hash")
@@ -423,20 +423,23 @@ def ours(a):
             def setf(flag, v):
                 P._lib.check(P.lib().hx_engine_set_flag(eng._h, flag, v), eng._h)
             off = a.warmup + a.steps
-            setf(2, 0)
-            for i in range(a.warmup):
-                dev_step(off + i)
-            ms_off = timed(a.steps, off + a.warmup)
-            setf(1, 1)
-            for i in range(a.warmup):
-                dev_step(off + i)
-            ms_noa2a = timed(a.steps, off + a.warmup)
+
+            def run_mode(hopb_on, skip_a2a):
+                setf(2, int(hopb_on))
+                setf(1, int(skip_a2a))
+                for i in range(a.warmup):
+                    dev_step(off + i)
+                return timed(a.steps, off + a.warmup)
+            ms_on = run_mode(True, False)
+            ms_on_noa2a = run_mode(True, True)   # same per-request launches, exchange replaced by a local copy
+            ms_off_noa2a = run_mode(False, True)
             setf(1, 0)
-            setf(2, 1)
-            exp_on, exp_off = max(0.0, ms - ms_noa2a), max(0.0, ms_off - ms_noa2a)
-            hopb = {"ms_per_step_on": ms, "ms_per_step_off": ms_off, "ms_per_step_no_a2a": ms_noa2a,
-                    "exposed_a2a_ms_on": exp_on, "exposed_a2a_ms_off": exp_off,
-                    "a2a_hidden_frac": (1.0 - exp_on / exp_off) if exp_off > 0 else None}
+            setf(2, 0)
+            exp_on, exp_off = max(0.0, ms_on - ms_on_noa2a), max(0.0, ms - ms_off_noa2a)
+            hopb = {"ms_per_step_off": ms, "ms_per_step_on": ms_on, "ms_per_step_no_a2a_off": ms_off_noa2a,
+                    "ms_per_step_no_a2a_on": ms_on_noa2a, "exposed_a2a_ms_on": exp_on, "exposed_a2a_ms_off": exp_off,
+                    "a2a_hidden_frac": (1.0 - exp_on / exp_off) if exp_off > 0 else None,
+                    "hopb_net_ms": ms - ms_on, "headline": "HOP-B off"}
     clocks = clk.summary(dev)
 
     # per-kernel-kind breakdown (eager launches, CUDA events on the engine stream)
