@@ -167,7 +167,8 @@ int hx_profile_step(hx_engine* e, int64_t reps, double* ms);
 /* The engine's CUDA stream (cudaStream_t) for event timing by the caller. */
 void* hx_stream(hx_engine* e);
 
-/* --- transcript: reference Message records (attention.hpp:401-411) --- */
+/* --- transcript: reference Message records (attention.hpp:401-411) ---
+ * Bounded: the first 2^20 records are kept (hx_clear_transcript opens a new window). */
 int64_t hx_transcript_size(const hx_engine* e);
 /* out [n][5] = kind (0 broadcast, 1 all-to-all), src, dst, payload_scalars, lse_scalars */
 int hx_transcript(const hx_engine* e, int64_t* out);

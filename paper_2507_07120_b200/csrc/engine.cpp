@@ -936,6 +936,11 @@ void Engine::record_transcript(int64_t layers) {
   const int64_t pool = static_cast<int64_t>(tpa_) * kvp_;
   const int64_t group_width = static_cast<int64_t>(q_per_slot_) * D_;
   const int64_t slice = group_width / kvp_;
+  // bounded for long serving runs: the first kMaxTranscript records are kept
+  // (hx_clear_transcript starts a new window)
+  constexpr size_t kMaxTranscript = size_t{1} << 20;
+  const size_t per_step = static_cast<size_t>(layers) * B_ * (pool - 1 + (mla_ ? 0 : tpa_ * kvp_ * (kvp_ - 1)));
+  if (transcript_.size() + per_step > kMaxTranscript) return;
   for (int64_t l = 0; l < layers; ++l)
     for (int b = 0; b < B_; ++b) {
       for (int64_t r = 1; r < pool; ++r) transcript_.push_back({0, 0, r, H_, 0});
