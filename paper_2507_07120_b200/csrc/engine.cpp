@@ -1213,6 +1213,7 @@ void Engine::decode_step_device(const int32_t* tokens_dev, int32_t* next_dev) {
       enqueue_decode(tokens_dev, next_dev);
       cuda_check(cudaStreamEndCapture(stream_, &g), "capture end");
       cuda_check(cudaGraphInstantiate(&exec, g, 0), "graph instantiate");
+      cuda_check(cudaGraphUpload(exec, stream_), "graph upload");  // device-side setup once, not per launch
       cudaGraphDestroy(g);
       graphs_cache_.push_back({tokens_dev, next_dev, capture_hidden_, store_logits_, exec});
     }
