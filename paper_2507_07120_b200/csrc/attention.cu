@@ -676,6 +676,59 @@ __global__ void __launch_bounds__(kSrWarps * 32) attn_split_reduce_kernel(const 
   }
 }
 
+// Few splits (<= 8, e.g. large batches): one WARP per (stream, query row),
+// lanes across the head dim, splits merged in order with all loads issued
+// first -- the 8-warp CTA above would idle most of its warps.
+template <int DP>
+__global__ void __launch_bounds__(256) attn_split_reduce_small_kernel(const AttnParams p, float* frag_o,
+                                                                      float* frag_lse) {
+  griddep_wait();
+  griddep_launch_dependents();
+  const int QR = p.qrows;
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int row = wg % QR, stream = wg / QR;
+  if (stream >= p.n_streams) return;
+  int t = stream;
+  const int qc = t % p.q_chunks; t /= p.q_chunks;
+  const int kvh = t % p.kvh_per_slot; t /= p.kvh_per_slot;
+  const int b = t % p.stream_batch + p.b_begin;
+  const int slot_local = t / p.stream_batch;
+  const int rank = (slot_local + p.slot_base) % p.kvp;
+  const int qrow = qc * QR + row;
+  if (qrow >= p.group) return;
+  const int ntok = static_cast<int>(rr_count(p.total[b], rank, p.chunk, p.kvp));
+  const int pages = (ntok + 15) >> 4;
+  constexpr int PER = DP / 32;
+  float w[8], v[8][PER];
+  float M = -INFINITY;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int pg0 = static_cast<int>((static_cast<long long>(j) * pages) / p.splits);
+    const int pg1 = static_cast<int>((static_cast<long long>(j + 1) * pages) / p.splits);
+    const bool ok = j < p.splits && pg1 > pg0;
+    const size_t item = static_cast<size_t>(j) * p.n_streams + stream;
+    w[j] = ok ? p.part_lse2[item * QR + row] : -INFINITY;
+#pragma unroll
+    for (int i = 0; i < PER; ++i) v[j][i] = ok ? p.part_o[(item * QR + row) * DP + lane + 32 * i] : 0.f;
+    M = fmaxf(M, w[j]);
+  }
+  float o[PER], L = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) o[i] = 0.f;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float e = w[j] == -INFINITY ? 0.f : exp2f(w[j] - M);
+#pragma unroll
+    for (int i = 0; i < PER; ++i) o[i] += v[j][i] * e;
+    L += e;
+  }
+  const int q_in_group = kvh * p.group + qrow;
+  const size_t fo = ((static_cast<size_t>(slot_local) * p.batch + b) * p.q_per_slot + q_in_group);
+#pragma unroll
+  for (int i = 0; i < PER; ++i) frag_o[fo * DP + lane + 32 * i] = L > 0.f ? o[i] / L : 0.f;
+  if (lane == 0) frag_lse[fo] = L > 0.f ? (M + log2f(L)) * 0.69314718055994530942f : -INFINITY;
+}
+
 __global__ void bump_totals_kernel(int* total, int n) {
   griddep_wait();
   griddep_launch_dependents();
@@ -728,6 +781,15 @@ cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t strea
 
 cudaError_t launch_attn_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse,
                                      cudaStream_t stream) {
+  if (p.splits <= 8) {  // one warp per (stream, query row)
+    const int blocks = (p.n_streams * p.qrows + 7) / 8;
+    switch (p.dp) {
+      case 32: return launch_k(attn_split_reduce_small_kernel<32>, dim3(blocks), dim3(256), 0, stream, p, frag_o, frag_lse);
+      case 64: return launch_k(attn_split_reduce_small_kernel<64>, dim3(blocks), dim3(256), 0, stream, p, frag_o, frag_lse);
+      case 128: return launch_k(attn_split_reduce_small_kernel<128>, dim3(blocks), dim3(256), 0, stream, p, frag_o, frag_lse);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   const int blocks = p.n_streams * p.qrows;  // one CTA per (stream, query row)
   const int threads = kSrWarps * 32;
   switch (p.dp) {

@@ -86,6 +86,12 @@ double unit_draw(std::mt19937_64& rng) {  // attention.hpp:549-552
 
 // Byte offset of W^T[n][k] in the CTA-tile-major fragment layout of gemv.cu:
 // [128-row block nb][k-step ks][n-tile nt (8)][lane][16 B].
+// tcgen05 GEMV image (gemv_tc.cu): per (row block, k-step) 4 KB of K-major core
+// matrices [row group 16][k-half 2][row 8][8 k]
+size_t wtc_offset_host(int n, int k, int kst) {
+  const int nb = n >> 7, rg = (n & 127) >> 3, r = n & 7, ks = k >> 4, kh = (k & 15) >> 3;
+  return ((static_cast<size_t>(nb) * kst + ks) * 256 + (rg * 2 + kh) * 8 + r) * 16 + (k & 7) * 2;
+}
 size_t wfrag_offset_host(int n, int k, int kst) {
   const int nb = n >> 7, nt = (n >> 4) & 7, rn = n & 15, ks = k >> 4, rk = k & 15;
   const int g = rn & 7, rowhalf = rn >> 3;
@@ -225,6 +231,9 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
   }
 
   if (std::getenv("HX_NO_PDL")) set_pdl(false);  // debugging: serialise every launch
+  // batches above 16 make the GEMV contraction dense enough for tcgen05 (gemv_tc.cu);
+  // HX_TC_GEMV=0 keeps the mma.sync path (A/B measurements)
+  tc_ = B_ > 16 && !(std::getenv("HX_TC_GEMV") && std::getenv("HX_TC_GEMV")[0] == '0');
   cuda_check(cudaSetDevice(device_), "cudaSetDevice");
   cudaDeviceProp prop{};
   cuda_check(cudaGetDeviceProperties(&prop, device_), "cudaGetDeviceProperties");
@@ -363,6 +372,10 @@ void Engine::plan_gemvs() {
   auto make = [&](int N, int Npad, int K, int norm, int em, int groups = 1) {
     GemvPlan g;
     GemvParams& p = g.p;
+    if (tc_) {  // tcgen05 tiles are row-block PAIRS over k-chunks of whole 4-k-step x blocks
+      Npad = round_up(Npad, 256);
+      if (K % 64) throw std::invalid_argument("batches above 16 need GEMV input widths that are multiples of 64");
+    }
     p.N = N;
     p.Npad = Npad;
     p.K = K;
@@ -374,19 +387,26 @@ void Engine::plan_gemvs() {
     // (router, sharded LM head: a few row blocks over a long K).
     const int kst = K / 16;
     const int nblk = Npad / 128;
-    int kr = std::min(64, kst);
-    while (kr > 8 && (kst + kr / 2 - 1) / (kr / 2) <= 32 &&
-           static_cast<int64_t>(nblk) * groups * ((kst + kr - 1) / kr) < 4 * num_sms_)
+    const int tile_blks = tc_ ? nblk / 2 : nblk;  // row blocks (tc: pairs) per k-chunk
+    // tcgen05 plans (batch > 16): the split-K partials grow with the batch
+    // (ksplit x B x Npad fp32), so cap them at ~1/4 of the weight bytes
+    // (ksplit <= K / (8 B)) and let a tile span the whole K when that suffices
+    const int max_ks = tc_ ? std::max(1, std::min(32, static_cast<int>(K / (8 * B_)))) : 32;
+    const int target = (tc_ ? 2 : 4) * num_sms_;
+    int kr = tc_ ? kst : std::min(64, kst);
+    while (kr > 8 && (!tc_ || (kr / 2) % 4 == 0) && (kst + kr / 2 - 1) / (kr / 2) <= max_ks &&
+           static_cast<int64_t>(tile_blks) * groups * ((kst + kr - 1) / kr) < target)
       kr /= 2;
     const int ksplit = (kst + kr - 1) / kr;
     p.ksplit = ksplit;
     p.kr_steps = kr;
-    p.n_tiles = nblk * ksplit;
+    p.n_tiles = tile_blks * ksplit;
     p.work_counter = d_plan_ctr_ + 2 * plan_idx++;
     p.eps = 1e-5f;
     p.kvp = kvp_;
     p.head_dim = static_cast<int>(D_);
     p.dp = DP_;
+    p.tc = tc_ ? 1 : 0;
     g.xmode = norm;
     g.emode = em;
     ypart_elems_ = std::max(ypart_elems_, static_cast<size_t>(groups) * ksplit * B_ * Npad);
@@ -513,7 +533,7 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
     cuda_check(cudaMemcpyAsync(d_segs_, segs.data(), segs.size() * sizeof(WSeg), cudaMemcpyHostToDevice,
                                stream_), "segs");
     cuda_check(launch_weight_init_hash(w, g.p.Npad, g.p.K, d_segs_, static_cast<int>(segs.size()), seed,
-                                       stream_), "weight init");
+                                       stream_, tc_ ? 1 : 0), "weight init");
     cuda_check(cudaStreamSynchronize(stream_), "weight init sync");
   };
   // WSeg: {stream, rows_begin, rows_end, cols_total, col_offset, interleave, scale, k_offset, col_limit}
@@ -737,13 +757,14 @@ void Engine::upload_qkv_host(int64_t layer, const std::vector<double>& wq, const
   const int nq = g.p.nq, nk = g.p.nk;
   const int q0 = dist ? grp_ * nq : 0, k0 = dist ? grp_ * nk : 0;
   std::vector<uint16_t> img(static_cast<size_t>(g.p.Npad) * K, 0);
+  auto woff = [&](int n, int k, int kst_) { return tc_ ? wtc_offset_host(n, k, kst_) : wfrag_offset_host(n, k, kst_); };
   for (int k = 0; k < K; ++k) {
     for (int n = 0; n < nq; ++n)
-      img[wfrag_offset_host(n, k, kst) / 2] = bf16_bits_from_double(wq[static_cast<size_t>(k) * Qall + q0 + n]);
+      img[woff(n, k, kst) / 2] = bf16_bits_from_double(wq[static_cast<size_t>(k) * Qall + q0 + n]);
     for (int n = 0; n < nk; ++n) {
-      img[wfrag_offset_host(nq + n, k, kst) / 2] =
+      img[woff(nq + n, k, kst) / 2] =
           bf16_bits_from_double(wk[static_cast<size_t>(k) * Kall + k0 + n]);
-      img[wfrag_offset_host(nq + nk + n, k, kst) / 2] =
+      img[woff(nq + nk + n, k, kst) / 2] =
           bf16_bits_from_double(wv[static_cast<size_t>(k) * Kall + k0 + n]);
     }
   }

@@ -235,8 +235,11 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
   griddep_launch_dependents();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nwarps = blockDim.x >> 5;
   const int nb = blockIdx.x;
+  // batches above 8: one grid layer per 8 requests (more CTAs in flight; every
+  // per-request reduction below stays inside its layer)
+  const int bz0 = static_cast<int>(blockIdx.z) * 8, bz1 = min(p.batch, bz0 + (gridDim.z > 1 ? 8 : p.batch));
   if (NORM) {
-    for (int b = warp; b < p.batch; b += nwarps) {
+    for (int b = bz0 + warp; b < bz1; b += nwarps) {
       float ss = 0.f;
       for (int i = lane; i < p.n_ss; i += 32) ss += p.ss_part[i * p.batch + b];
 #pragma unroll
@@ -244,10 +247,11 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
       if (lane == 0) s_inv[b] = rsqrtf(ss / static_cast<float>(p.K) + p.eps);
     }
   }
-  if (EM == E_QKV && threadIdx.x < p.batch) {
-    const long long g = p.total[threadIdx.x];
-    s_pos[threadIdx.x][0] = rr_rank(g, p.rr_chunk, p.kvp);
-    s_pos[threadIdx.x][1] = rr_row(g, p.rr_chunk, p.kvp);
+  if (EM == E_QKV && bz0 + static_cast<int>(threadIdx.x) < bz1) {
+    const int b = bz0 + threadIdx.x;
+    const long long g = p.total[b];
+    s_pos[b][0] = rr_rank(g, p.rr_chunk, p.kvp);
+    s_pos[b][1] = rr_row(g, p.rr_chunk, p.kvp);
   }
   if (EM == E_LOGITS && threadIdx.x < 64) s_best[threadIdx.x] = 0ull;
   if (EM == E_STORE || EM == E_RESID)
@@ -262,8 +266,8 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
   const bool combine = p.group_count && EM != E_SWIGLU;  // MoE combine (possibly of zero experts)
   const int n_comb = combine ? *p.group_count : 0;
   uint8_t* xf_out = p.xf_out + static_cast<size_t>(gi_epi) * p.xf_out_group_stride;
-  for (int e = threadIdx.x; e < rows_here * p.batch; e += blockDim.x) {
-    const int r = e % rows_here, b = e / rows_here;
+  for (int e = threadIdx.x; e < rows_here * (bz1 - bz0); e += blockDim.x) {
+    const int r = e % rows_here, b = bz0 + e / rows_here;
     const int np = EM == E_SWIGLU ? 2 : 1;
     float y[NP] = {0.f, 0.f};
     float old = 0.f;
@@ -371,7 +375,7 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
   }
   if ((EM == E_STORE || EM == E_RESID) && p.ss_out) {
     __syncthreads();
-    for (int b = warp; b < p.batch; b += nwarps) {
+    for (int b = bz0 + warp; b < bz1; b += nwarps) {
       float s = 0.f;
       for (int r = lane; r < kRows; r += 32) s += vt[b][r];
 #pragma unroll
@@ -381,7 +385,8 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
   }
   if (EM == E_LOGITS) {
     __syncthreads();
-    if (threadIdx.x < p.batch) atomicMax(&p.best[threadIdx.x], s_best[threadIdx.x]);
+    if (bz0 + static_cast<int>(threadIdx.x) < bz1)
+      atomicMax(&p.best[bz0 + threadIdx.x], s_best[bz0 + threadIdx.x]);
   }
 }
 
@@ -394,18 +399,21 @@ template <int NB8, int EM, int XS, bool NORM>
 static cudaError_t launch_t(const GemvParams& p, int grid, cudaStream_t stream) {
   const size_t smem = gemv_smem_bytes(p);
   static size_t configured = 0;  // opt in once per instantiation
-  if (smem > configured) {
+  if (!p.tc && smem > configured) {
     cudaError_t e = cudaFuncSetAttribute(gemv_kernel<NB8, EM, XS, NORM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = smem;
   }
-  cudaError_t e = launch_k(gemv_kernel<NB8, EM, XS, NORM>, dim3(grid), dim3(kThreads + 32), smem, stream, p);
+  cudaError_t e = p.tc ? launch_gemv_tc(p, NB8, XS, grid, stream)
+                       : launch_k(gemv_kernel<NB8, EM, XS, NORM>, dim3(grid), dim3(kThreads + 32), smem, stream, p);
   if (e != cudaSuccess) return e;
   const int rows_here = EM == E_SWIGLU ? kRows / 2 : kRows;
-  const int threads = std::min(1024, (rows_here * p.batch + 31) / 32 * 32);
+  const int gz = p.batch > 8 ? (p.batch + 7) / 8 : 1;  // one grid layer per 8 requests
+  const int per = p.batch > 8 ? 8 : p.batch;
+  const int threads = std::min(1024, (rows_here * per + 31) / 32 * 32);
   const int gy = (p.group_count && EM == E_SWIGLU) ? p.n_groups_max : 1;
-  return launch_k(gemv_epilogue_kernel<NB8, EM, NORM>, dim3(p.Npad / kRows, gy), dim3(threads), 0, stream, p);
+  return launch_k(gemv_epilogue_kernel<NB8, EM, NORM>, dim3(p.Npad / kRows, gy, gz), dim3(threads), 0, stream, p);
 }
 
 template <int NB8>
@@ -427,6 +435,7 @@ static cudaError_t dispatch_nb(const GemvParams& p, int norm, int em, int grid, 
 
 cudaError_t launch_gemv(const GemvParams& p, int norm, int emode, int grid, cudaStream_t stream) {
   if (p.batch < 1 || p.batch > 64 || (p.K & 15) || (p.Npad % kRows)) return cudaErrorInvalidValue;
+  if (p.tc && p.batch <= 16) return cudaErrorInvalidValue;  // tcgen05 path: N = 32 or 64 batch rows
   if (p.batch <= 8) return dispatch_nb<1>(p, norm, emode, grid, stream);
   if (p.batch <= 16) return dispatch_nb<2>(p, norm, emode, grid, stream);
   if (p.batch <= 32) return dispatch_nb<4>(p, norm, emode, grid, stream);

@@ -87,6 +87,8 @@ enum EMode : int { E_STORE = 0, E_QKV = 1, E_RESID = 2, E_SWIGLU = 3, E_LOGITS =
 
 struct GemvParams {
   const uint4* w;        // bf16 weights, CTA-tile-major fragments [Npad/128][K/16][8][32 lanes][16 B]
+                         // (tc: [Npad/128][K/16][16 row groups][2 k-halves][8 rows][16 B], gemv_tc.cu)
+  int tc;                // batch > 16: tcgen05 GEMV (weights and x-fragments in its operand layouts)
   const uint8_t* xf;     // input activation fragments for K (xfrag.cuh)
   int N, Npad, K;
   int ksplit, kr_steps;  // k-chunks per 128-row block and k-steps per chunk
@@ -134,6 +136,8 @@ struct GemvParams {
   const float* addend;       // optional [B][out_stride] added by E_RESID / E_STORE
 };
 cudaError_t launch_gemv(const GemvParams& p, int norm, int emode, int grid, cudaStream_t stream);
+// tcgen05 inner product for p.tc plans (gemv_tc.cu); the epilogue kernel is shared.
+cudaError_t launch_gemv_tc(const GemvParams& p, int nb8, int xs, int grid, cudaStream_t stream);
 size_t gemv_smem_bytes(const GemvParams& p);
 
 // x-fragment producers (xfrag.cuh layout; nb8 = ceil(batch / 8))
@@ -185,7 +189,7 @@ struct WSeg {
   int col_limit;             // interleaved: first source column past this shard
 };
 cudaError_t launch_weight_init_hash(uint4* w, int Npad, int K, const WSeg* segs, int nseg,
-                                    uint64_t seed, cudaStream_t stream);
+                                    uint64_t seed, cudaStream_t stream, int tc = 0);
 cudaError_t launch_emb_init_hash(uint16_t* emb, int vocab, int hidden, uint64_t seed,
                                  uint64_t stream_id, cudaStream_t stream);
 // Plain row-major bf16: w[i] = bf16(hash_unit(seed, stream_id, idx0 + i) * scale), i < n.

@@ -316,9 +316,11 @@ __device__ double wseg_value(const WSeg* segs, int nseg, int n, int k, uint64_t 
   return 0.0;
 }
 
-// One thread per 16-byte chunk (n-tile, k-step, lane) of the fragment-major image.
+// One thread per 16-byte chunk (n-tile, k-step, lane) of the fragment-major image;
+// tc: the tcgen05 GEMV's image instead -- per (row block, k-step) 4 KB of
+// canonical K-major core matrices [row group 16][k-half 2][row 8][8 k] (gemv_tc.cu).
 __global__ void weight_init_hash_kernel(uint4* w, int Npad, int K, const WSeg* segs, int nseg,
-                                        uint64_t seed) {
+                                        uint64_t seed, int tc) {
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const int kst = K >> 4;
   if (idx >= static_cast<long long>(Npad / 16) * kst * 32) return;
@@ -332,6 +334,18 @@ __global__ void weight_init_hash_kernel(uint4* w, int Npad, int K, const WSeg* s
   const int g = lane >> 2, c = lane & 3;
   uint4 out;
   uint16_t* o = reinterpret_cast<uint16_t*>(&out);
+  if (tc) {
+    const int j = static_cast<int>(idx & 255);  // chunk within the (row block, k-step) 4 KB block
+    const int n = nb * 128 + (j >> 4) * 8 + (j & 7);
+    const int k0 = ks * 16 + ((j >> 3) & 1) * 8;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      const __nv_bfloat16 h = double_to_bf16_rne(wseg_value(segs, nseg, n, k0 + e, seed));
+      o[e] = *reinterpret_cast<const uint16_t*>(&h);
+    }
+    w[idx] = out;
+    return;
+  }
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     const int reg = e >> 1, elem = e & 1;          // reg = khalf*2 + rowhalf
@@ -345,10 +359,10 @@ __global__ void weight_init_hash_kernel(uint4* w, int Npad, int K, const WSeg* s
 }
 
 cudaError_t launch_weight_init_hash(uint4* w, int Npad, int K, const WSeg* segs, int nseg,
-                                    uint64_t seed, cudaStream_t stream) {
+                                    uint64_t seed, cudaStream_t stream, int tc) {
   const long long work = static_cast<long long>(Npad / 16) * (K / 16) * 32;
   weight_init_hash_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(
-      w, Npad, K, segs, nseg, seed);
+      w, Npad, K, segs, nseg, seed, tc);
   return cudaGetLastError();
 }
 

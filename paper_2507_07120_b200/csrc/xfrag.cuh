@@ -9,6 +9,13 @@
 //   u32 0 = (x[b][16ks+2c], x[b][16ks+2c+1]), u32 1 = (x[b][16ks+2c+8], x[b][16ks+2c+9])
 //   terms: hi = bf16(x), mid = bf16(x - hi), lo = bf16(x - hi - mid); a GEMV
 //   that needs ~16-bit activations reads hi+mid, the QKV projection all three.
+//
+// Batches above 16 (nb8 >= 4) run the tcgen05 GEMV (gemv_tc.cu), whose B
+// operand is K-major in canonical core matrices: layout
+//   [k-step][term][batch group bg][k-half][batch row g][8 k] bf16
+// -- per k-step the terms' batch groups are consecutive 256-byte pairs of core
+// matrices (UMMA descriptor LBO = 128 B along K, SBO = 256 B per 8 rows), so
+// one MMA with N = 2 * 8 * nb8 multiplies the hi and mid terms at once.
 #pragma once
 
 #include "common.cuh"
@@ -30,10 +37,11 @@ HX_DEV void xf_write(uint8_t* xf, int nb8, int b, int k, float v) {
   const int lane = g * 4 + c;
   float t[3];
   split3(v, t[0], t[1], t[2]);
+  const bool tc = nb8 >= 4;
 #pragma unroll
   for (int term = 0; term < kXfTerms; ++term) {
-    const size_t off = ((static_cast<size_t>(ks) * kXfTerms + term) * nb8 + bg) * 32 * 8 + lane * 8 + half * 4 +
-                       elem * 2;
+    const size_t blk = ((static_cast<size_t>(ks) * kXfTerms + term) * nb8 + bg) * 32 * 8;
+    const size_t off = tc ? blk + half * 128 + g * 16 + (r & 7) * 2 : blk + lane * 8 + half * 4 + elem * 2;
     *reinterpret_cast<__nv_bfloat16*>(xf + off) = __float2bfloat16_rn(t[term]);
   }
 }

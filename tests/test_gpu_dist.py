@@ -124,3 +124,39 @@ def test_loopback_hopb_long_context_group16():
         assert rel_err(results[r][2], ho) <= 2e-3, (r, rel_err(results[r][2], ho))
     for e in engines:
         e.close()
+
+
+def test_loopback_pool_large_batch_tcgen05():
+    """Batch 20 (> 16): the sharded pool's GEMVs (TP partial stores, residual adds
+    after the AllReduce) run on tcgen05 with the tcgen05 x-fragment layout."""
+    import paper_2507_07120_b200 as P
+    from paper_2507_07120_b200.model import Loopback
+    H, Q, K, D, F, L, V, B, kvp = 256, 8, 2, 32, 512, 1, 1000, 20, 2
+    spec = P.model.ModelSpec("test", L, H, Q, K, D, F, 3, "gqa", 0, vocab=V)
+    lb = Loopback(kvp)
+    engines = [P.HelixDecoder(spec, tpa=1, kvp=kvp, chunk_size=16, batch=B, capacity=300, layers=L, vocab=V,
+                              use_graphs=False, pool=2, rank=r, loopback=lb) for r in range(kvp)]
+    o = O.Model(H, Q, K, D, F, L, V, tpa=1, kvp=kvp, chunk=16, batch=B, seed=55, qkv_hash=True, bf16=True)
+    for e in engines:
+        e.init_weights(55, qkv="hash")
+        e.fill_kv_hash(200, 55)
+    for b in range(B):
+        o.grow_hash(0, b, 200)
+    tokens = (np.arange(B) * 37 + 1) % V
+    results = [None] * kvp
+    errors = []
+
+    def run(r):
+        try:
+            results[r] = engines[r].step(tokens, want_logits=True, want_hidden=True)
+        except Exception as ex:  # surfaced below
+            errors.append(ex)
+    th = [threading.Thread(target=run, args=(r,), daemon=True) for r in range(kvp)]
+    [t.start() for t in th]
+    [t.join(timeout=120) for t in th]
+    assert not errors, errors
+    lo, ho, no = o.step(tokens)
+    for r in range(kvp):
+        assert rel_err(results[r][2], ho) <= 2e-3, (r, rel_err(results[r][2], ho))
+    for e in engines:
+        e.close()

@@ -31,7 +31,7 @@ def _spec(P, moe=None, q=Q, h=H, hsz=HSZ):
     return P.model.ModelSpec("mla", L, h, q, 1, hsz, 256, 3, "mla", LAT, moe, vocab=V)
 
 
-@pytest.mark.parametrize("kvp,B,ctx", [(1, 2, 40), (1, 3, 700), (2, 2, 300), (4, 1, 1100), (1, 8, 2000)])
+@pytest.mark.parametrize("kvp,B,ctx", [(1, 2, 40), (1, 3, 700), (2, 2, 300), (4, 1, 1100), (1, 8, 2000), (2, 20, 300)])
 def test_mla_decode_matches_oracle(kvp, B, ctx):
     import paper_2507_07120_b200 as P
     seed = 77 + kvp

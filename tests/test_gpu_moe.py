@@ -36,6 +36,8 @@ def _routing_clear(o):
     (1, 1, 16, 4, 64, 256, 5),
     (2, 2, 8, 8, 96, 128, 2),     # top_k == E: every expert active
     (1, 2, 32, 6, 128, 0, 16),    # many distinct experts, 2 batch groups
+    (1, 1, 16, 4, 128, 256, 24),  # batch > 16: tcgen05 GEMVs (grouped experts + shared expert)
+    (1, 2, 32, 6, 128, 0, 40),    # 64-row tcgen05 tiles
 ])
 def test_moe_decode_matches_oracle(tpa, kvp, E, k, Fe, shared, B):
     import paper_2507_07120_b200 as P
