@@ -56,6 +56,22 @@ def test_mla_kernel_uses_tcgen05():
         assert op in mla[0], op
 
 
+def test_large_batch_gemv_uses_tcgen05():
+    """Batches above 16 run the weight-streaming GEMV on tcgen05 (UTCHMMA with
+    TMEM drains, LDTM) fed by TMA bulk copies (UBLKCP); FP8 KV pages widen with
+    the e4m3 -> f16 converter (F2FP.F16.E4M3.UNPACK_B)."""
+    so = os.path.join(ROOT, "paper_2507_07120_b200", "libhelix_b200.so")
+    sass = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
+    funcs = sass.split("Function : ")
+    tc = [f for f in funcs if f.startswith("_ZN2hx14gemv_tc_kernel")]
+    assert len(tc) == 4  # N = 32 / 64 batch rows x (2 or 3 activation terms)
+    for f in tc:
+        for op in ("UTCHMMA", "LDTM", "UBLKCP", "UTCBAR"):
+            assert op in f, op
+    fp8 = [f for f in funcs if f.startswith("_ZN2hx18attn_decode_kernel") and "Lb1ELb0E" in f.split("\n", 1)[0]]
+    assert fp8 and all("F2FP.F16.E4M3.UNPACK_B" in f and "HMMA.16816.F32 " in f for f in fp8)
+
+
 def test_ctypes_structs_match_c_header(tmp_path):
     """The Python binding's struct layouts equal the C ABI's (sizeof + offsets)."""
     from paper_2507_07120_b200 import _lib
