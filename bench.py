@@ -217,6 +217,61 @@ def pool_slice(a, preset, S, ep):
     return out
 
 
+def kvp_slices(a):
+    """configs[1]'s model at KVP = 2/4/8 (weak scaling: S tokens per request per
+    GPU, global context S x KVP; TPF = KVP): ONE GPU of the pool measured alone
+    -- rank 0 of a loopback pool with both collectives switched off (so the
+    step is CUDA-graph captured like the headline) -- plus the pool's
+    communication from the reference's alpha-beta model (comm.hpp:28-45;
+    fp32 payloads as this engine sends them; gb200-like link 900 GB/s,
+    0.1 us) for the combined HBM + NVLink figure. The real NCCL numbers come
+    from `bench.py --gpus N` on an N-GPU box."""
+    import torch
+    import paper_2507_07120_b200 as P
+    from paper_2507_07120_b200.model import Loopback
+    spec = P.model.PRESETS["llama3-8b-like"]
+    B, S, L = a.batch, a.context, a.layers
+    H, Q, K, Hsz, F, V = spec.hidden_dim, spec.query_heads, spec.kv_heads, spec.head_size, spec.ffn_dim, spec.vocab
+    hbm, _ = peaks()
+    out = {}
+    for n in (2, 4, 8):
+        lb = Loopback(n)
+        eng = P.HelixDecoder(spec, tpa=1, kvp=n, batch=B, capacity=S * n + 64 * n, layers=L, pool=2, rank=0,
+                             loopback=lb, use_graphs=True)
+        P._lib.check(P.lib().hx_engine_set_flag(eng._h, 1, 3), eng._h)
+        eng.init_weights(2507, qkv="hash")
+        eng.fill_kv_hash(S * n, 2507)
+        tok = [torch.randint(0, V, (B,), dtype=torch.int32, device="cuda"),
+               torch.zeros(B, dtype=torch.int32, device="cuda")]
+        for i in range(a.warmup):
+            eng.step_device(tok[i % 2].data_ptr(), tok[(i + 1) % 2].data_ptr())
+        stream = torch.cuda.ExternalStream(eng.stream())
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        e0.record(stream)
+        for i in range(a.steps):
+            eng.step_device(tok[i % 2].data_ptr(), tok[(i + 1) % 2].data_ptr())
+        e1.record(stream)
+        e1.synchronize()
+        ms = e0.elapsed_time(e1) / a.steps
+        s_loc = int(P.lib().hx_effective_tokens(eng._h, 0, 0, 0))
+        eng.close()
+        kv = B * 2 * K * Hsz * s_loc * 2 * L
+        w = (H * (Q + 2 * K) * Hsz * 2 + (H // n) * H * 2 + 3 * H * F // n * 2) * L + (V // n) * H * 2
+        # reference comm model per layer: all-to-all of the fragment slices + two TP all-reduces
+        per_dest = B * H / n * (1 + 1 / Hsz) * 4
+        a2a = 1e-7 + per_dest * n * (n - 1) / n / 9e11
+        ar = 1e-7 * 2 * (n - 1) + 2 * (B * H * 4) * (n - 1) / n / 9e11
+        comm_ms = (a2a + 2 * ar) * L * 1e3
+        t_roof = (kv + w) / hbm / 1e6
+        out[str(n)] = {"kv_tokens_per_request_per_gpu": s_loc, "global_context": s_loc * n,
+                       "ttl_ms_compute": ms, "comm_ms_modeled": comm_ms, "ttl_ms_with_modeled_comm": ms + comm_ms,
+                       "tokens_per_s_per_gpu": B / ((ms + comm_ms) * 1e-3) / n,
+                       "hbm_bytes_per_gpu": kv + w, "t_roof_ms": t_roof + comm_ms,
+                       "roofline_frac": (t_roof + comm_ms) / (ms + comm_ms)}
+    return out
+
+
 def fp8_kv_line(a):
     """the configs[1] workload with FP8 (e4m3) KV pages
     (kv_dtype="fp8"; weights stay bf16, attention MMAs in f16 on the exact
@@ -489,6 +544,10 @@ def ours(a):
             line["fp8_kv"] = {"error": str(ex)[:300]}
     if world == 1 and not a.no_slices:
         eng.close()  # free the 150 GB pool before the 8-GPU-pool slices
+        try:
+            line["kvp_slices"] = kvp_slices(a)
+        except Exception as ex:  # reported, never fatal for the headline number
+            line["kvp_slices"] = {"error": str(ex)[:300]}
         for key, preset, ctx, ep in (("llama405b_slice", "llama405b-like", a.slice_context, 1),
                                      ("deepseek_slice", "deepseek-r1-like", a.slice_context, 8)):
             try:

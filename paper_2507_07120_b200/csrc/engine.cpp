@@ -247,7 +247,9 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
   } else if (dist_mode_ == HX_POOL_LOOPBACK) {
     if (!par.loopback) throw std::invalid_argument("loopback pool needs a loopback group");
     transport_ = make_loopback_transport(reinterpret_cast<LoopbackHub*>(par.loopback), rank_, tpa_, kvp_);
-    graphs_ = false;  // host barriers inside the collectives cannot be captured
+    // host barriers inside the loopback collectives cannot be captured; graphs
+    // stay possible only while both collectives are switched off (measurement)
+    loopback_ = true;
   }
   if (dist_mode_ != HX_POOL_LOCAL) {
     cuda_check(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "comm stream");
@@ -1223,7 +1225,7 @@ void Engine::decode_step_device(const int32_t* tokens_dev, int32_t* next_dev) {
   if (attn_only_) throw StateError("decode_step needs a full model (attention_only = 0)");
   if (!weights_ready_) throw StateError("weights are not initialised");
   for (int64_t l = 0; l < L_; ++l) require_context(l);
-  if (graphs_ && !prof_) {
+  if (graphs_ && !(loopback_ && skip_comm_ != 3) && !prof_) {
     cudaGraphExec_t exec = nullptr;
     for (auto& g : graphs_cache_)
       if (g.tokens == tokens_dev && g.next == next_dev && g.hidden == capture_hidden_ && g.logits == store_logits_)

@@ -100,6 +100,7 @@ class Engine {
   int64_t cap_;
   int device_;
   bool hopb_, graphs_;
+  bool loopback_ = false;
   bool kv8_ = false;  // FP8 e4m3 GQA pages (hx_runtime_config.kv_dtype)
   bool tc_ = false;   // batch > 16: tcgen05 GEMVs (weights / x-fragments in their operand images)
   int DP_, G_, q_rows_, q_chunks_, kvh_per_slot_, q_per_slot_, n_slots_, slot_base_;
