@@ -321,10 +321,29 @@ void Engine::alloc() {
   // cross-warp combine dominate (measured: one 131k-token request of the
   // 405B-like shard 0.196 -> 0.131 ms; profiles/r01_hopb_sweep.md).
   int ips = 8, min_pages = 32;  // HX_ATTN_SPLIT="items_per_sm,min_pages_per_item" (tuning experiments)
-  if (const char* e = std::getenv("HX_ATTN_SPLIT")) std::sscanf(e, "%d,%d", &ips, &min_pages);
+  const char* split_env = std::getenv("HX_ATTN_SPLIT");
+  if (split_env) std::sscanf(split_env, "%d,%d", &ips, &min_pages);
   const int target_items = num_sms_ * std::max(1, ips);
+  // Equal-size items pulled by one persistent CTA per SM: the step costs
+  // waves x (pages per item + per-item overhead ~16 pages: query staging and
+  // the cross-warp combine), waves = ceil(items / SMs). Minimise that over the
+  // split count (items >= 32 pages): an item count that is a multiple of the
+  // SM count leaves no tail (configs[1]: 64 streams x 37 splits = 16 x 148;
+  // measured 20.5 -> 20.0 ms of attention per step vs 19 splits).
   auto splits_for = [&](int streams) {
-    return std::max(1, std::min((target_items + streams - 1) / streams, std::max(1, pages_max / std::max(1, min_pages))));
+    const int smax = std::max(1, pages_max / std::max(1, min_pages));
+    if (split_env) return std::max(1, std::min((target_items + streams - 1) / streams, smax));
+    int best = 1;
+    double best_cost = 1e300;
+    for (int sp = 1; sp <= smax && sp <= 8192; ++sp) {
+      const long long waves = (static_cast<long long>(streams) * sp + num_sms_ - 1) / num_sms_;
+      const double cost = static_cast<double>(waves) * ((pages_max + sp - 1) / sp + 16.0);
+      if (cost < best_cost) {
+        best_cost = cost;
+        best = sp;
+      }
+    }
+    return best;
   };
   n_streams_ = n_slots_ * B_ * kvh_per_slot_ * q_chunks_;
   const int req_streams = n_slots_ * kvh_per_slot_ * q_chunks_;
