@@ -402,7 +402,7 @@ void Engine::plan_gemvs() {
     p.K = K;
     p.batch = B_;
     // Persistent GEMV: tiles = (128-row block, k-chunk of kr k-steps) pulled
-    // from a queue by one CTA per SM. kr shrinks until there are >= 4 tiles per
+    // from a queue by one CTA per SM. kr shrinks until there are >= 2 tiles per
     // SM (dynamic balance, <= one short tile of tail); kr >= 8 keeps a tile >= 32 KB,
     // and <= 32 k-chunks keep the epilogue's split-K sum short for narrow outputs
     // (router, sharded LM head: a few row blocks over a long K).
@@ -413,7 +413,11 @@ void Engine::plan_gemvs() {
     // (ksplit x B x Npad fp32), so cap them at ~1/4 of the weight bytes
     // (ksplit <= K / (8 B)) and let a tile span the whole K when that suffices
     const int max_ks = tc_ ? std::max(1, std::min(32, static_cast<int>(K / (8 * B_)))) : 32;
-    const int target = (tc_ ? 2 : 4) * num_sms_;
+    // >= 2 tiles per SM: measured against 4 and 1 at configs[1] (O-proj 0.95 -> 0.75 ms and
+    // down 1.27 -> 1.13 ms per step: fewer split-K partials for the epilogue to reduce)
+    int tiles_per_sm = 2;  // HX_GEMV_TILES="tiles_per_sm" (tuning experiments)
+    if (const char* e = std::getenv("HX_GEMV_TILES")) tiles_per_sm = std::max(1, std::atoi(e));
+    const int target = tiles_per_sm * num_sms_;
     int kr = tc_ ? kst : std::min(64, kst);
     while (kr > 8 && (!tc_ || (kr / 2) % 4 == 0) && (kst + kr / 2 - 1) / (kr / 2) <= max_ks &&
            static_cast<int64_t>(tile_blks) * groups * ((kst + kr - 1) / kr) < target)
