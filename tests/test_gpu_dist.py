@@ -160,3 +160,27 @@ def test_loopback_pool_large_batch_tcgen05():
         assert rel_err(results[r][2], ho) <= 2e-3, (r, rel_err(results[r][2], ho))
     for e in engines:
         e.close()
+
+
+@pytest.mark.parametrize("hopb,graphs", [(False, False), (True, False), (False, True), (True, True)])
+def test_nccl_pool_single_rank_matches_local(hopb, graphs):
+    """The NCCL transport itself on the one GPU available: a one-rank NCCL pool
+    (ncclCommInitRank + ncclCommSplit, grouped send/recv all-to-all to itself,
+    ncclAllReduce sum and max) runs the distributed code path end to end and
+    must agree with the local pool on the same weights and cache."""
+    import paper_2507_07120_b200 as P
+    from paper_2507_07120_b200.model import nccl_unique_id
+    H, Q, K, D, F, L, V, B = 256, 8, 2, 32, 512, 2, 1000, 3
+    spec = P.model.ModelSpec("test", L, H, Q, K, D, F, 3, "gqa", 0, vocab=V)
+    outs = []
+    for pool in (0, 1):
+        kw = dict(pool=1, rank=0, nccl_id=nccl_unique_id(), hopb=hopb) if pool else {}
+        g = P.HelixDecoder(spec, tpa=1, kvp=1, batch=B, capacity=400, layers=L, vocab=V, use_graphs=graphs, **kw)
+        g.init_weights(77, qkv="hash")
+        g.fill_kv_hash(300, 77)
+        g.step(np.array([3, 4, 5]))  # a first step (captures the graph when enabled)
+        outs.append(g.step(np.array([3, 4, 5]), want_logits=True, want_hidden=True))
+        g.close()
+    assert rel_err(outs[1][2], outs[0][2]) <= 1e-5
+    assert rel_err(outs[1][1], outs[0][1]) <= 1e-5
+    np.testing.assert_array_equal(outs[1][0], outs[0][0])
