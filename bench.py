@@ -141,8 +141,10 @@ def pool_slice(a, preset, S, ep):
     mla = spec.attention == "mla"
     lb = Loopback(N)
     eng = P.HelixDecoder(spec, tpa=1, kvp=N, batch=B, capacity=S * N + 64 * N, layers=1, vocab=V,
-                         use_graphs=False, pool=2, rank=0, loopback=lb, ep=ep)
-    P._lib.check(P.lib().hx_engine_set_flag(eng._h, 1, 3), eng._h)  # HX_FLAG_SKIP_COMM: no a2a / all-reduce
+                         use_graphs=True, pool=2, rank=0, loopback=lb, ep=ep)
+    # HX_FLAG_SKIP_COMM: no a2a / all-reduce (no peers here) -- the step is then
+    # CUDA-graph captured like the headline (and like the NCCL pool)
+    P._lib.check(P.lib().hx_engine_set_flag(eng._h, 1, 3), eng._h)
     eng.init_weights(2507, qkv="hash")
     eng.fill_kv_hash(S * N, 2507)  # rank 0 keeps S of the S*N global tokens
     s_loc = int(P.lib().hx_effective_tokens(eng._h, 0, 0, 0))
@@ -172,7 +174,7 @@ def pool_slice(a, preset, S, ep):
     att_ms = prof[2]
     H, Q, Hsz = spec.hidden_dim, spec.query_heads, spec.head_size
     hbm, _ = peaks()
-    out = {"ms_per_layer": ms, "eager_launches": True, "kv_tokens_per_request_on_this_gpu": s_loc,
+    out = {"ms_per_layer": ms, "graph_replay": True, "kv_tokens_per_request_on_this_gpu": s_loc,
            "breakdown_ms": {k: float(v) for k, v in zip(
                ["embed", "qkv", "attention", "split_reduce", "o_proj", "gate_up_or_router_to_gate_up",
                 "down_or_down_combine", "lm_head", "merge"], prof)}}

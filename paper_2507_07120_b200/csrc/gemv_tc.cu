@@ -22,6 +22,8 @@
 // issue, warps 0-3 drain finished tiles (tcgen05.ld, TMEM lane = feature row)
 // into the split-K partials while the next tile accumulates in the other TMEM
 // buffer.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "tc05.cuh"
@@ -32,30 +34,31 @@ namespace hx {
 namespace {
 constexpr int kTcThreads = 224;
 constexpr int kTcDone = -1;
-constexpr int kTcSteps = 4;   // k-steps per stage (= the x-fragment block)
-constexpr int kTcStages = 4;
+// ring geometry: KSTEPS k-steps per stage x NSTAGE stages (4 x 4 by default;
+// HX_TC_RING=2 selects 2 x 8 -- the same bytes in flight at finer granularity)
 struct TcMeta {
   int tile, pb, kc, gi, nks, first, last, k0;
 };
-template <int NB8, int XS>
+template <int NB8, int KSTEPS>
 constexpr uint32_t tc_stage_bytes() {
-  return kTcSteps * (2 * 4096u + kXfTerms * NB8 * 256u);  // all three terms: one x copy per stage
+  return KSTEPS * (2 * 4096u + kXfTerms * NB8 * 256u);  // all three terms: one x copy per stage
 }
-template <int NB8, int XS>
+template <int NB8, int KSTEPS, int NSTAGE>
 constexpr size_t tc_smem_bytes() {
-  return kTcStages * tc_stage_bytes<NB8, XS>() + kTcStages * sizeof(TcMeta) + 8 * sizeof(int) +
-         (3 * kTcStages + 6) * 8 + 16 + 128;
+  return NSTAGE * tc_stage_bytes<NB8, KSTEPS>() + NSTAGE * sizeof(TcMeta) + 8 * sizeof(int) + (3 * NSTAGE + 6) * 8 +
+         16 + 128;
 }
 }  // namespace
 
-template <int NB8, int XS>
+template <int NB8, int XS, int KSTEPS, int NSTAGE>
 __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvParams p) {
   static_assert(NB8 == 4 || NB8 == 8, "tcgen05 GEMV: N = 32 or 64 batch rows");
-  constexpr int NST = kTcStages;
+  constexpr int NST = NSTAGE;
+  constexpr int kTcSteps = KSTEPS;
   constexpr uint32_t XT = NB8 * 256u;                     // x bytes per (k-step, term)
   constexpr uint32_t XSTEP = kXfTerms * XT;               // x bytes per k-step (all terms)
   constexpr uint32_t SW = kTcSteps * 4096u;               // weight bytes per stage and row block
-  constexpr uint32_t SB = tc_stage_bytes<NB8, XS>();
+  constexpr uint32_t SB = tc_stage_bytes<NB8, KSTEPS>();
   constexpr int N = 8 * NB8;                              // batch rows
   constexpr int NC = 2 * N;                               // accumulator columns: [hi | mid]
   constexpr uint32_t COLS = 4 * NC;                       // 2 buffers x 2 row blocks
@@ -244,24 +247,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvParams
   }
 }
 
-template <int NB8, int XS>
+template <int NB8, int XS, int KSTEPS, int NSTAGE>
 static cudaError_t launch_tc_t(const GemvParams& p, int grid, cudaStream_t stream) {
-  constexpr size_t smem = tc_smem_bytes<NB8, XS>();
+  constexpr size_t smem = tc_smem_bytes<NB8, KSTEPS, NSTAGE>();
   static_assert(smem <= 227 * 1024, "tcgen05 GEMV ring exceeds shared memory");
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemv_tc_kernel<NB8, XS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
+    cudaError_t e = cudaFuncSetAttribute(gemv_tc_kernel<NB8, XS, KSTEPS, NSTAGE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  return launch_k(gemv_tc_kernel<NB8, XS>, dim3(grid), dim3(kTcThreads), smem, stream, p);
+  return launch_k(gemv_tc_kernel<NB8, XS, KSTEPS, NSTAGE>, dim3(grid), dim3(kTcThreads), smem, stream, p);
+}
+
+template <int NB8, int XS>
+static cudaError_t launch_tc_ring(const GemvParams& p, int grid, cudaStream_t stream) {
+  static const bool fine = std::getenv("HX_TC_RING") && std::getenv("HX_TC_RING")[0] == '2';
+  return fine ? launch_tc_t<NB8, XS, 2, 8>(p, grid, stream) : launch_tc_t<NB8, XS, 4, 4>(p, grid, stream);
 }
 
 cudaError_t launch_gemv_tc(const GemvParams& p, int nb8, int xs, int grid, cudaStream_t stream) {
-  if ((p.Npad % 256) || ((p.K >> 4) % kTcSteps) || (p.kr_steps % kTcSteps)) return cudaErrorInvalidValue;
-  if (nb8 == 4) return xs == 3 ? launch_tc_t<4, 3>(p, grid, stream) : launch_tc_t<4, 2>(p, grid, stream);
-  if (nb8 == 8) return xs == 3 ? launch_tc_t<8, 3>(p, grid, stream) : launch_tc_t<8, 2>(p, grid, stream);
+  if ((p.Npad % 256) || ((p.K >> 4) % 4) || (p.kr_steps % 4)) return cudaErrorInvalidValue;
+  if (nb8 == 4) return xs == 3 ? launch_tc_ring<4, 3>(p, grid, stream) : launch_tc_ring<4, 2>(p, grid, stream);
+  if (nb8 == 8) return xs == 3 ? launch_tc_ring<8, 3>(p, grid, stream) : launch_tc_ring<8, 2>(p, grid, stream);
   return cudaErrorInvalidValue;
 }
 
