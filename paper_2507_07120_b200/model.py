@@ -157,6 +157,187 @@ def load_model(name_or_path):
     return m
 
 
+# --------------------------------------------------------------------------- hardware / parallelism
+@dataclass
+class HardwareSpec:
+    """helixsim::HardwareSpec (types.hpp:56-67); JSON keys as hardware_to_json
+    (presets.cpp:115-124). The b200-measured preset carries this pod's measured
+    copy bandwidth and sustained bf16 throughput (MEASURED_PEAKS.json) at bf16."""
+    name: str = ""
+    mem_bw: float = 8.0e12
+    compute_throughput: float = 5.0e15
+    link_bw: float = 9.0e11
+    link_latency: float = 1.0e-7
+    max_gpus: int = 64
+    bytes_per_param: float = 0.5
+    dram_capacity: float = 192.0e9
+
+    _KEYS = {"name": "name", "mem_bw_bytes_per_s": "mem_bw", "compute_flops": "compute_throughput",
+             "link_bw_bytes_per_s": "link_bw", "link_latency_s": "link_latency", "max_gpus": "max_gpus",
+             "bytes_per_param": "bytes_per_param", "dram_capacity_bytes": "dram_capacity"}
+
+    def to_json(self):
+        return {k: getattr(self, a) for k, a in self._KEYS.items()}
+
+    @staticmethod
+    def from_json(j):
+        where = "hardware config"
+        if not isinstance(j, dict):
+            raise ConfigError(f"{where}: expected a JSON object")
+        for k in j:
+            if k not in HardwareSpec._KEYS:
+                raise ConfigError(f"{where}: unknown key '{k}'")
+        hw = HardwareSpec()
+        for k, a in HardwareSpec._KEYS.items():
+            if k not in j:
+                raise ConfigError(f"{where}: missing field '{k}'")
+            v = j[k]
+            if a == "name":
+                if not isinstance(v, str):
+                    raise ConfigError(f"{where}: field '{k}' must be a string")
+            elif a == "max_gpus":
+                if isinstance(v, bool) or not isinstance(v, int):
+                    raise ConfigError(f"{where}: field '{k}' must be an integer")
+            elif isinstance(v, bool) or not isinstance(v, (int, float)):
+                raise ConfigError(f"{where}: field '{k}' must be a number")
+            setattr(hw, a, v)
+        return hw
+
+
+HARDWARE_PRESETS = {
+    "gb200-like": HardwareSpec("gb200-like", 8e12, 5e15, 9e11, 1e-7, 64, 0.5, 192e9),  # presets.cpp:45-51
+    # this pod's B200 at the precision this engine stores (bf16): MEASURED_PEAKS.json copy
+    # bandwidth and sustained cuBLAS bf16; NVLink 5 at 900 GB/s per direction, 180 GB HBM3e
+    "b200-measured": HardwareSpec("b200-measured", 6.5562e12, 1.393e15, 9e11, 1e-7, 8, 2.0, 180e9),
+}
+
+
+def load_hardware(name_or_path):
+    """load_hardware (presets.cpp): preset name, else a JSON file path."""
+    if name_or_path in HARDWARE_PRESETS:
+        return HARDWARE_PRESETS[name_or_path]
+    try:
+        with open(name_or_path) as f:
+            j = json.load(f)
+    except OSError as e:
+        raise ConfigError(f"cannot open hardware config '{name_or_path}': {e}")
+    except json.JSONDecodeError as e:
+        raise ConfigError(f"malformed JSON in '{name_or_path}': {e}")
+    return HardwareSpec.from_json(j)
+
+
+STRATEGIES = ("helix", "tp", "tp_pp", "ep_dp", "medha_kvp")  # strategy_name (types.cpp)
+
+
+@dataclass
+class ParallelismConfig:
+    """helixsim::ParallelismConfig (types.hpp:84-102)."""
+    strategy: str = "tp"
+    tpa: int = 1
+    kvp: int = 1
+    tpf: int = 1
+    ep: int = 1
+    pp: int = 1
+
+    def stage_pool(self):
+        return self.tpf * self.ep if self.strategy == "ep_dp" else self.kvp * self.tpa
+
+    def total_gpus(self):
+        return self.stage_pool() * self.pp
+
+    def __str__(self):
+        return f"{self.strategy}(tpa={self.tpa},kvp={self.kvp},tpf={self.tpf},ep={self.ep},pp={self.pp})"
+
+    def to_json(self):
+        return {"strategy": self.strategy, "tpa": self.tpa, "kvp": self.kvp, "tpf": self.tpf, "ep": self.ep,
+                "pp": self.pp}
+
+    @staticmethod
+    def from_json(j):
+        where = "parallelism config"
+        if not isinstance(j, dict):
+            raise ConfigError(f"{where}: expected a JSON object")
+        keys = ("strategy", "tpa", "kvp", "tpf", "ep", "pp")
+        for k in j:
+            if k not in keys:
+                raise ConfigError(f"{where}: unknown key '{k}'")
+        for k in keys:
+            if k not in j:
+                raise ConfigError(f"{where}: missing field '{k}'")
+        if not isinstance(j["strategy"], str):
+            raise ConfigError(f"{where}: field 'strategy' must be a string")
+        if j["strategy"] not in STRATEGIES:
+            raise ConfigError(f"{where}: field 'strategy' has unknown value '{j['strategy']}'")
+        for k in keys[1:]:
+            if isinstance(j[k], bool) or not isinstance(j[k], int):
+                raise ConfigError(f"{where}: field '{k}' must be an integer")
+        return ParallelismConfig(*(j[k] for k in keys))
+
+
+@dataclass
+class Validity:
+    """types.hpp:105-110: validity is a value; `rule` names the first broken rule."""
+    ok: bool = True
+    rule: str = ""
+
+    def __bool__(self):
+        return self.ok
+
+
+def validate_config(cfg, model, hw):
+    """validate_config (types.cpp:86-141): the reference's rules, in its order and
+    with its diagnostics (the first broken rule wins)."""
+    def fail(rule):
+        return Validity(False, rule)
+    if min(cfg.tpa, cfg.kvp, cfg.tpf, cfg.ep, cfg.pp) < 1:
+        return fail("all parallelism widths must be >= 1")
+    if cfg.total_gpus() > hw.max_gpus:
+        return fail("total GPUs exceed max_gpus")
+    k_eff = 1 if model.attention == "mla" else model.kv_heads
+    if cfg.strategy == "helix":
+        if cfg.pp != 1:
+            return fail("helix runs as a single pipeline stage")
+        if cfg.tpa > k_eff:
+            return fail("helix requires tpa <= effective KV heads")
+        if cfg.kvp * cfg.tpa != cfg.tpf * cfg.ep:
+            return fail("helix re-provisions one pool: kvp*tpa must equal tpf*ep")
+    elif cfg.strategy in ("tp", "tp_pp"):
+        if cfg.strategy == "tp" and cfg.pp != 1:
+            return fail("tp has no pipeline stages")
+        if cfg.kvp != 1:
+            return fail("tp keeps the whole sequence per GPU (kvp=1)")
+        if cfg.ep != 1:
+            return fail("tp shards experts with tensor parallelism (ep=1)")
+        if cfg.tpf != cfg.tpa:
+            return fail("tp ties attention and FFN widths")
+    elif cfg.strategy == "ep_dp":
+        if cfg.tpa != 1 or cfg.kvp != 1:
+            return fail("ep_dp replicates attention (tpa=1, kvp=1)")
+    elif cfg.strategy == "medha_kvp":
+        if cfg.tpf != cfg.tpa:
+            return fail("medha_kvp keeps the FFN on the tpa group")
+        if cfg.ep != 1:
+            return fail("medha_kvp does not shard experts (ep=1)")
+    if model.query_heads % cfg.tpa:
+        return fail("tpa must divide query_heads")
+    if cfg.strategy in ("helix", "medha_kvp") and model.hidden_dim % (cfg.kvp * cfg.tpa):
+        return fail("kvp*tpa must divide hidden_dim")
+    if model.moe is not None:
+        m = model.moe
+        if m.total_experts % cfg.ep:
+            return fail("ep must divide total_experts")
+        if m.expert_ffn_dim % cfg.tpf:
+            return fail("tpf must divide expert_ffn_dim")
+        if m.shared_expert_ffn_dim > 0 and m.shared_expert_ffn_dim % cfg.tpf:
+            return fail("tpf must divide shared_expert_ffn_dim")
+    else:
+        if cfg.ep != 1:
+            return fail("expert parallelism needs an MoE model")
+        if model.ffn_dim % cfg.tpf:
+            return fail("tpf must divide ffn_dim")
+    return Validity()
+
+
 class HelixDecoder(_Engine):
     """Full decode step of a decoder stack under Helix (tpa, kvp): GQA attention, or
     MLA (attention == "mla": one 2*kv_latent_dim-wide latent KV head, absorbed
@@ -186,6 +367,19 @@ class HelixDecoder(_Engine):
         self.n_ranks = tpa * kvp if pool else 1
         self.rank = rank
         self.vocab_local = -(-self.vocab // self.n_ranks)
+
+    @classmethod
+    def from_config(cls, spec, cfg, hw=None, **kw):
+        """Build from the reference's configuration objects: `cfg` must be a valid
+        Helix layout (validate_config against `hw`, default b200-measured); the
+        FFN runs on cfg.tpf x cfg.ep over the same pool (types.hpp:84-102)."""
+        hw = hw or HARDWARE_PRESETS["b200-measured"]
+        v = validate_config(cfg, spec, hw)
+        if not v:
+            raise ValueError(v.rule)
+        if cfg.strategy != "helix":
+            raise ValueError("the B200 decode engine runs the helix strategy")
+        return cls(spec, tpa=cfg.tpa, kvp=cfg.kvp, ep=cfg.ep, **kw)
 
     def init_weights(self, seed, qkv="mt19937"):
         if qkv == "mt19937":
