@@ -22,8 +22,6 @@
 // issue, warps 0-3 drain finished tiles (tcgen05.ld, TMEM lane = feature row)
 // into the split-K partials while the next tile accumulates in the other TMEM
 // buffer.
-#include <cstdlib>
-
 #include "common.cuh"
 #include "kernels.h"
 #include "tc05.cuh"
@@ -34,8 +32,7 @@ namespace hx {
 namespace {
 constexpr int kTcThreads = 224;
 constexpr int kTcDone = -1;
-// ring geometry: KSTEPS k-steps per stage x NSTAGE stages (4 x 4 by default;
-// HX_TC_RING=2 selects 2 x 8 -- the same bytes in flight at finer granularity)
+// ring geometry: KSTEPS k-steps per stage x NSTAGE stages
 struct TcMeta {
   int tile, pb, kc, gi, nks, first, last, k0;
 };
@@ -261,10 +258,10 @@ static cudaError_t launch_tc_t(const GemvParams& p, int grid, cudaStream_t strea
   return launch_k(gemv_tc_kernel<NB8, XS, KSTEPS, NSTAGE>, dim3(grid), dim3(kTcThreads), smem, stream, p);
 }
 
+// 4 k-steps x 4 stages (2 x 8 measured the same at B = 64)
 template <int NB8, int XS>
 static cudaError_t launch_tc_ring(const GemvParams& p, int grid, cudaStream_t stream) {
-  static const bool fine = std::getenv("HX_TC_RING") && std::getenv("HX_TC_RING")[0] == '2';
-  return fine ? launch_tc_t<NB8, XS, 2, 8>(p, grid, stream) : launch_tc_t<NB8, XS, 4, 4>(p, grid, stream);
+  return launch_tc_t<NB8, XS, 4, 4>(p, grid, stream);
 }
 
 cudaError_t launch_gemv_tc(const GemvParams& p, int nb8, int xs, int grid, cudaStream_t stream) {
