@@ -274,12 +274,13 @@ def kvp_slices(a):
     return out
 
 
-def fp8_kv_line(a):
+def fp8_kv_line(a, w_dtype="bf16"):
     """the configs[1] workload with FP8 (e4m3) KV pages
-    (kv_dtype="fp8"; weights stay bf16, attention MMAs in f16 on the exact
-    widened values). Same timing method as the headline (graph replay, CUDA
-    events on the engine stream); a separate key, never the headline number
-    (the headline stores KV in bf16)."""
+    (kv_dtype="fp8", attention MMAs in f16 on the exact widened values), and
+    with w_dtype="fp8" also e4m3 GEMV weights (per-output power-of-two scales).
+    Same timing method as the headline (graph replay, CUDA events on the engine
+    stream); separate keys, never the headline number (the headline stores KV
+    and weights in bf16)."""
     import ctypes
     import numpy as np
     import torch
@@ -287,7 +288,7 @@ def fp8_kv_line(a):
     spec = P.model.PRESETS["llama3-8b-like"]
     B, S, L = a.batch, a.context, a.layers
     eng = P.HelixDecoder(spec, tpa=1, kvp=1, batch=B, capacity=S + 4 * (a.warmup + a.steps + 16) + 64, layers=L,
-                         kv_dtype="fp8")
+                         kv_dtype="fp8", w_dtype=w_dtype)
     eng.init_weights(2507, qkv="hash")
     eng.fill_kv_hash(S, 2507)
     stream = torch.cuda.ExternalStream(eng.stream())
@@ -311,7 +312,8 @@ def fp8_kv_line(a):
     hbm, _ = peaks()
     info = eng.info()
     eng.close()
-    return {"kv_dtype": "fp8_e4m3", "ms_per_step": ms, "value": B / (ms * 1e-3), "unit": UNIT,
+    return {"kv_dtype": "fp8_e4m3", "w_dtype": "fp8_e4m3" if w_dtype == "fp8" else "bf16",
+            "weight_bytes_resident": info["weight_bytes_per_layer"] * L + info["head_bytes"], "ms_per_step": ms, "value": B / (ms * 1e-3), "unit": UNIT,
             "breakdown_ms": {k: float(v) for k, v in zip(
                 ["embed", "qkv", "attention", "split_reduce", "o_proj", "gate_up", "down", "lm_head", "merge"], prof)},
             "attention_roofline": {"bound": "hbm", "kernel": "attn_decode_kernel<128,8,4,1,fp8>",
@@ -544,6 +546,10 @@ def ours(a):
             line["fp8_kv"] = fp8_kv_line(a)
         except Exception as ex:  # reported, never fatal for the headline number
             line["fp8_kv"] = {"error": str(ex)[:300]}
+        try:
+            line["fp8_kv_w"] = fp8_kv_line(a, w_dtype="fp8")
+        except Exception as ex:  # reported, never fatal for the headline number
+            line["fp8_kv_w"] = {"error": str(ex)[:300]}
     if world == 1 and not a.no_slices:
         eng.close()  # free the 150 GB pool before the 8-GPU-pool slices
         try:

@@ -89,10 +89,16 @@ typedef struct hx_runtime_config {
   int32_t use_graphs;       /* capture the decode step in a CUDA graph */
   int32_t kv_dtype;         /* KV page storage: HX_KV_BF16, or HX_KV_FP8_E4M3 (GQA; e4m3 RNE,
                                saturating at +-448, unit scale -- SURVEY 8f rank 2) */
+  int32_t w_dtype;          /* GEMV weight storage: HX_W_BF16, or HX_W_FP8_E4M3 (dense GQA models,
+                               batch <= 16, hash init; e4m3 with a power-of-two scale per output
+                               feature, applied in the GEMV epilogue -- SURVEY 8f rank 2) */
+  int32_t reserved;
 } hx_runtime_config;
 
 #define HX_KV_BF16 0
 #define HX_KV_FP8_E4M3 1
+#define HX_W_BF16 0
+#define HX_W_FP8_E4M3 1
 
 typedef struct hx_engine_info {
   int64_t kv_bytes_per_layer;      /* resident KV pool bytes on this device, per layer */
@@ -103,6 +109,7 @@ typedef struct hx_engine_info {
   int64_t page_cap;
   int64_t head_dim_padded;
   int64_t kv_dtype;                /* HX_KV_BF16 / HX_KV_FP8_E4M3 */
+  int64_t w_dtype;                 /* HX_W_BF16 / HX_W_FP8_E4M3 */
 } hx_engine_info;
 
 const char* hx_version(void);

@@ -19,6 +19,24 @@ Mat hash_matrix(std::uint64_t seed, HashKind kind, i64 layer, i64 rows, i64 cols
   return m;
 }
 
+double fp8_pow2_scale(double absmax) {
+  if (!(absmax > 0.0)) return 1.0;
+  int e = 0;
+  const double f = std::frexp(absmax / 448.0, &e);  // absmax/448 = f * 2^e, f in [0.5, 1)
+  return std::ldexp(1.0, f == 0.5 ? e - 1 : e);     // smallest 2^j >= absmax / 448
+}
+
+Mat hash_matrix_fp8(std::uint64_t seed, HashKind kind, i64 layer, i64 rows, i64 cols, double scale) {
+  Mat m = hash_matrix(seed, kind, layer, rows, cols, scale, false);
+  for (i64 c = 0; c < cols; ++c) {
+    double mx = 0.0;
+    for (i64 r = 0; r < rows; ++r) mx = std::max(mx, std::fabs(m(r, c)));
+    const double s = fp8_pow2_scale(mx);
+    for (i64 r = 0; r < rows; ++r) m(r, c) = round_e4m3(m(r, c) / s) * s;
+  }
+  return m;
+}
+
 std::vector<double> rmsnorm(const std::vector<double>& x, double eps) {
   double ss = 0.0;
   for (double v : x) ss += v * v;
@@ -54,6 +72,11 @@ ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, st
   const i64 W = mla ? mla_width(d.kv_latent) : 0, DV = mla ? mla_value_width(d.kv_latent) : 0;
   const double sh = 1.0 / std::sqrt(static_cast<double>(d.hidden));
   const double sf = 1.0 / std::sqrt(static_cast<double>(std::max<i64>(d.ffn, 1)));
+  if (d.w_fp8 && (mla || d.n_experts > 0 || qkv_init != QkvInit::Hash))
+    throw std::invalid_argument("FP8 weights: dense GQA models with hash-initialised weights");
+  auto wmat = [&](HashKind kind, i64 l, i64 rows, i64 cols, double sc) {
+    return d.w_fp8 ? hash_matrix_fp8(seed, kind, l, rows, cols, sc) : hash_matrix(seed, kind, l, rows, cols, sc, bf16);
+  };
   h_.reserve(static_cast<std::size_t>(d.layers * batch));
   for (i64 l = 0; l < d.layers; ++l) {
     if (mla) {
@@ -69,16 +92,15 @@ ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, st
       h_.emplace_back(Dims{d.query_heads, d.kv_heads, d.head_size}, tpa, kvp, chunk,
                       seed + static_cast<std::uint64_t>(l), bf16);
       if (qkv_init == QkvInit::Hash)
-        h_.back().set_weights(
-            hash_matrix(seed, kWq, l, d.hidden, d.query_heads * d.head_size, 1.0, bf16),
-            hash_matrix(seed, kWk, l, d.hidden, d.kv_heads * d.head_size, 1.0, bf16),
-            hash_matrix(seed, kWv, l, d.hidden, d.kv_heads * d.head_size, 1.0, bf16));
+        h_.back().set_weights(wmat(kWq, l, d.hidden, d.query_heads * d.head_size, 1.0),
+                              wmat(kWk, l, d.hidden, d.kv_heads * d.head_size, 1.0),
+                              wmat(kWv, l, d.hidden, d.kv_heads * d.head_size, 1.0));
     }
-    wo_.push_back(hash_matrix(seed, kWo, l, d.hidden, d.hidden, sh, bf16));
+    wo_.push_back(wmat(kWo, l, d.hidden, d.hidden, sh));
     if (d.ffn > 0) {  // dense FFN, or the MoE shared expert
-      wg_.push_back(hash_matrix(seed, kWgate, l, d.hidden, d.ffn, sh, bf16));
-      wu_.push_back(hash_matrix(seed, kWup, l, d.hidden, d.ffn, sh, bf16));
-      wd_.push_back(hash_matrix(seed, kWdown, l, d.ffn, d.hidden, sf, bf16));
+      wg_.push_back(wmat(kWgate, l, d.hidden, d.ffn, sh));
+      wu_.push_back(wmat(kWup, l, d.hidden, d.ffn, sh));
+      wd_.push_back(wmat(kWdown, l, d.ffn, d.hidden, sf));
     } else {
       wg_.emplace_back();
       wu_.emplace_back();
@@ -110,7 +132,7 @@ ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, st
   routes_.assign(static_cast<std::size_t>(d.layers * batch), {});
   gaps_.assign(static_cast<std::size_t>(d.layers * batch), 1e30);
   emb_ = hash_matrix(seed, kEmb, 0, d.vocab, d.hidden, 1.0, bf16);
-  lm_ = hash_matrix(seed, kLm, 0, d.hidden, d.vocab, sh, bf16);
+  lm_ = wmat(kLm, 0, d.hidden, d.vocab, sh);
 }
 
 void ModelOracle::grow_random(i64 layer, i64 request, i64 n, std::mt19937_64& rng) {

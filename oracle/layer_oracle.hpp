@@ -63,6 +63,11 @@ struct ModelDims {
   i64 hidden, query_heads, kv_heads, head_size, ffn, layers, vocab;
   i64 n_experts = 0, top_k = 0, expert_ffn = 0;  // n_experts == 0: dense FFN of width `ffn`
   i64 kv_latent = 0;  // > 0: MLA attention (types.hpp:37-49), latent width W = 2 * kv_latent
+  // FP8 weights (dense GQA models, hash init): every GEMV
+  // weight W[k][n] (input k, output n) is stored as e4m3(W / s_n) * s_n with a
+  // power-of-two per-output scale s_n = 2^ceil(log2(max_k |W[k][n]| / 448));
+  // the embedding stays bf16 (a gather, not a GEMV).
+  bool w_fp8 = false;
 };
 
 // MLA attention in the weight-absorbed decode form (types.hpp:37-49: K_eff = 1,
@@ -147,6 +152,10 @@ class ModelOracle {
 // Hash-initialised matrix [rows x cols], row-major index r*cols + c, times scale.
 Mat hash_matrix(std::uint64_t seed, HashKind kind, i64 layer, i64 rows, i64 cols, double scale,
                 bool bf16);
+// The same values quantised per column (output feature) to e4m3 with a
+// power-of-two scale (ModelDims::w_fp8).
+Mat hash_matrix_fp8(std::uint64_t seed, HashKind kind, i64 layer, i64 rows, i64 cols, double scale);
+double fp8_pow2_scale(double absmax);
 std::vector<double> rmsnorm(const std::vector<double>& x, double eps = 1e-5);
 
 }  // namespace helix_oracle

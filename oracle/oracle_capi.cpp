@@ -208,6 +208,16 @@ int oracle_model_create(i64 hidden, i64 q, i64 k, i64 hsz, i64 ffn, i64 layers, 
   });
 }
 
+// Dense model with FP8 (e4m3, per-output power-of-two scale) GEMV weights.
+int oracle_model_create_w8(i64 hidden, i64 q, i64 k, i64 hsz, i64 ffn, i64 layers, i64 vocab, i64 tpa, i64 kvp,
+                           i64 chunk, i64 batch, std::uint64_t seed, void** out) {
+  return guard([&] {
+    ModelDims d{hidden, q, k, hsz, ffn, layers, vocab};
+    d.w_fp8 = true;
+    *out = new ModelOracle(d, tpa, kvp, chunk, batch, seed, QkvInit::Hash, true);
+  });
+}
+
 // MoE model: ffn = shared-expert width (0: none), n_experts / top_k / expert_ffn routed.
 int oracle_model_create_moe(i64 hidden, i64 q, i64 k, i64 hsz, i64 shared_ffn, i64 layers, i64 vocab,
                             i64 n_experts, i64 top_k, i64 expert_ffn, i64 tpa, i64 kvp, i64 chunk, i64 batch,

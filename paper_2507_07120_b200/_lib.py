@@ -31,16 +31,18 @@ class ParallelConfig(C.Structure):
 
 class RuntimeConfig(C.Structure):
     _fields_ = [("batch", i64), ("capacity_tokens", i64), ("device", i32), ("hopb", i32), ("use_graphs", i32),
-                ("kv_dtype", i32)]
+                ("kv_dtype", i32), ("w_dtype", i32), ("reserved", i32)]
 
 
 KV_DTYPES = {"bf16": 0, "fp8": 1, "fp8_e4m3": 1}
+W_DTYPES = {"bf16": 0, "fp8": 1, "fp8_e4m3": 1}
 
 
 class EngineInfo(C.Structure):
     _fields_ = [("kv_bytes_per_layer", i64), ("weight_bytes_per_layer", i64), ("head_bytes", i64),
                 ("attn_streams", i64), ("attn_splits", i64), ("attn_items", i64), ("attn_grid", i64),
-                ("kernels_per_step", i64), ("page_cap", i64), ("head_dim_padded", i64), ("kv_dtype", i64)]
+                ("kernels_per_step", i64), ("page_cap", i64), ("head_dim_padded", i64), ("kv_dtype", i64),
+                ("w_dtype", i64)]
 
 
 EXPORTS = {

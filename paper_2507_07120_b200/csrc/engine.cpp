@@ -130,6 +130,11 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
   if (rt.kv_dtype != HX_KV_BF16 && rt.kv_dtype != HX_KV_FP8_E4M3) throw std::invalid_argument("unknown kv_dtype");
   kv8_ = rt.kv_dtype == HX_KV_FP8_E4M3;
   if (kv8_ && mla_) throw std::invalid_argument("FP8 KV pages are implemented for GQA caches (MLA latents stay bf16)");
+  if (rt.w_dtype != HX_W_BF16 && rt.w_dtype != HX_W_FP8_E4M3) throw std::invalid_argument("unknown w_dtype");
+  w8_ = rt.w_dtype == HX_W_FP8_E4M3;
+  if (w8_ && (mla_ || m.n_experts > 0))
+    throw std::invalid_argument("FP8 weights are implemented for dense GQA models");
+  if (w8_ && B_ > 16) throw std::invalid_argument("FP8 weights run the mma.sync GEMV: batch <= 16");
   if (mla_) {
     // types.hpp:43-49: MLA keeps one latent KV head; Helix needs tpa <= K_eff = 1 (types.cpp:122-139)
     W_ = static_cast<int>(2 * m.kv_latent);
@@ -432,6 +437,8 @@ void Engine::plan_gemvs() {
     p.head_dim = static_cast<int>(D_);
     p.dp = DP_;
     p.tc = tc_ ? 1 : 0;
+    p.w8 = w8_ ? 1 : 0;  // wscale is wired by the weight init
+    p.xf16 = xf16_();
     g.xmode = norm;
     g.emode = em;
     ypart_elems_ = std::max(ypart_elems_, static_cast<size_t>(groups) * ksplit * B_ * Npad);
@@ -552,13 +559,22 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
   const int v0 = dist ? rank_ * V_local_ : 0;
   const int vrows = static_cast<int>(std::min<int64_t>(V_local_, V_ - v0));
   auto walloc = [&](const GemvPlan& g) {
-    return dalloc<uint4>(static_cast<size_t>(g.p.Npad) * g.p.K / 8, "weights");
+    return dalloc<uint4>(static_cast<size_t>(g.p.Npad) * g.p.K / (w8_ ? 16 : 8), "weights");
   };
-  auto init = [&](uint4* w, const GemvPlan& g, const std::vector<WSeg>& segs) {
+  // k_full: the input width of the whole (unsharded) matrix -- FP8 scales span it
+  auto init = [&](uint4* w, GemvPlan& g, const std::vector<WSeg>& segs, int k_full) {
     cuda_check(cudaMemcpyAsync(d_segs_, segs.data(), segs.size() * sizeof(WSeg), cudaMemcpyHostToDevice,
                                stream_), "segs");
-    cuda_check(launch_weight_init_hash(w, g.p.Npad, g.p.K, d_segs_, static_cast<int>(segs.size()), seed,
-                                       stream_, tc_ ? 1 : 0), "weight init");
+    if (w8_) {
+      float*& sc = wscale_[w];
+      if (!sc) sc = dalloc<float>(static_cast<size_t>(g.p.Npad), "weight scales");
+      cuda_check(launch_weight_init_hash_w8(reinterpret_cast<uint8_t*>(w), sc, g.p.Npad, g.p.K, k_full, d_segs_,
+                                            static_cast<int>(segs.size()), seed, stream_), "weight init");
+      g.p.wscale = sc;
+    } else {
+      cuda_check(launch_weight_init_hash(w, g.p.Npad, g.p.K, d_segs_, static_cast<int>(segs.size()), seed,
+                                         stream_, tc_ ? 1 : 0), "weight init");
+    }
     cuda_check(cudaStreamSynchronize(stream_), "weight init sync");
   };
   // WSeg: {stream, rows_begin, rows_end, cols_total, col_offset, interleave, scale, k_offset, col_limit}
@@ -570,7 +586,7 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
     if (mla_) {  // W_q [H x Q*Hsz] (kWq) and the latent down-projection (kWk), both 1/sqrt(H)
       init(w_qkv_[l], plan_qkv_[l],
            {{hash_stream(kWq, l), 0, nq, nq, 0, 0, sh, 0, 0},
-            {hash_stream(kWk, l), nq, nq + W_, W_, 0, 0, sh, 0, 0}});
+            {hash_stream(kWk, l), nq, nq + W_, W_, 0, 0, sh, 0, 0}}, Hh);
       // per-head absorptions: W_UK for every head, W_UV for the heads held here
       const long long uk = Qh_ * D_ * W_, uv = static_cast<long long>(uv_heads_) * DV_ * D_;
       if (w_uk_.size() <= static_cast<size_t>(l)) {
@@ -586,7 +602,7 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
       init(w_qkv_[l], plan_qkv_[l],
            {{hash_stream(kWq, l), 0, nq, Qall, q0, 0, 1.0, 0, 0},
             {hash_stream(kWk, l), nq, nq + nk, Kall, k0, 0, 1.0, 0, 0},
-            {hash_stream(kWv, l), nq + nk, nq + 2 * nk, Kall, k0, 0, 1.0, 0, 0}});
+            {hash_stream(kWv, l), nq + nk, nq + 2 * nk, Kall, k0, 0, 1.0, 0, 0}}, Hh);
     }
     plan_qkv_[l].p.w = w_qkv_[l];
     if (!attn_only_) {
@@ -600,13 +616,14 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
       // O-proj input rows: this rank's slice of its group's flattened heads
       // (MLA: the rows of the W_UV outputs of this rank's heads)
       const int ko = !dist ? 0 : (mla_ ? uv_h0_ * static_cast<int>(D_) : grp_ * q_per_slot_ * AD_ + r_ * slice_);
-      init(w_o_[l], plan_o_[l], {{hash_stream(kWo, l), 0, Hh, Hh, 0, 0, sh, ko, 0}});
+      init(w_o_[l], plan_o_[l], {{hash_stream(kWo, l), 0, Hh, Hh, 0, 0, sh, ko, 0}}, Hh);
       plan_o_[l].p.w = w_o_[l];
       if (F > 0) {
         init(w_gu_[l], plan_gu_[l],
              {{hash_stream(kWgate, l), 0, plan_gu_[l].p.Npad, static_cast<int>(F_), f0, 1, sh, 0, f0 + F},
-              {hash_stream(kWup, l), 0, plan_gu_[l].p.Npad, static_cast<int>(F_), f0, 2, sh, 0, f0 + F}});
-        init(w_down_[l], plan_down_[l], {{hash_stream(kWdown, l), 0, Hh, Hh, 0, 0, sf, f0, 0}});
+              {hash_stream(kWup, l), 0, plan_gu_[l].p.Npad, static_cast<int>(F_), f0, 2, sh, 0, f0 + F}}, Hh);
+        init(w_down_[l], plan_down_[l], {{hash_stream(kWdown, l), 0, Hh, Hh, 0, 0, sf, f0, 0}},
+             static_cast<int>(F_));
         plan_gu_[l].p.w = w_gu_[l];
         plan_down_[l].p.w = w_down_[l];
       }
@@ -624,14 +641,14 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
       }
       const int E = static_cast<int>(E_), Fe = Fe_local_, fe0 = tpf_rank_ * Fe_local_;
       const double se = 1.0 / std::sqrt(static_cast<double>(Fe_));
-      init(w_router_[l], r, {{hash_stream(kWrouter, l), 0, E, E, 0, 0, sh, 0, 0}});
+      init(w_router_[l], r, {{hash_stream(kWrouter, l), 0, E, E, 0, 0, sh, 0, 0}}, Hh);
       for (int el = 0; el < E_local_; ++el) {
         const int64_t e = e_begin_ + el;
         init(w_egu_[l] + static_cast<size_t>(el) * gu.p.Npad * gu.p.K / 8, gu,
              {{expert_stream(kEgate, l, e), 0, gu.p.Npad, static_cast<int>(Fe_), fe0, 1, sh, 0, fe0 + Fe},
-              {expert_stream(kEup, l, e), 0, gu.p.Npad, static_cast<int>(Fe_), fe0, 2, sh, 0, fe0 + Fe}});
+              {expert_stream(kEup, l, e), 0, gu.p.Npad, static_cast<int>(Fe_), fe0, 2, sh, 0, fe0 + Fe}}, Hh);
         init(w_edown_[l] + static_cast<size_t>(el) * dn.p.Npad * dn.p.K / 8, dn,
-             {{expert_stream(kEdown, l, e), 0, Hh, Hh, 0, 0, se, fe0, 0}});
+             {{expert_stream(kEdown, l, e), 0, Hh, Hh, 0, 0, se, fe0, 0}}, static_cast<int>(Fe_));
       }
       r.p.w = w_router_[l];
       gu.p.w = w_egu_[l];
@@ -640,7 +657,7 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
   }
   if (!attn_only_) {
     if (!w_lm_) w_lm_ = walloc(plan_lm_);
-    init(w_lm_, plan_lm_, {{hash_stream(kLm, 0), 0, vrows, static_cast<int>(V_), v0, 0, sh, 0, 0}});
+    init(w_lm_, plan_lm_, {{hash_stream(kLm, 0), 0, vrows, static_cast<int>(V_), v0, 0, sh, 0, 0}}, Hh);
     plan_lm_.p.w = w_lm_;
     if (!emb_) emb_ = dalloc<uint16_t>(static_cast<size_t>(V_) * H_, "embedding");
     cuda_check(launch_emb_init_hash(emb_, static_cast<int>(V_), Hh, seed, hash_stream(kEmb, 0), stream_),
@@ -776,6 +793,7 @@ void Engine::upload_qkv_host(int64_t layer, const std::vector<double>& wq, const
   // wq [H x Q*Hsz], wk/wv [H x K*Hsz] row-major (reference orientation); this
   // device keeps all columns (local pool) or its TPA group's heads.
   const bool dist = dist_mode_ != HX_POOL_LOCAL;
+  if (w8_) throw std::invalid_argument("FP8 weights are hash-initialised (hx_init_weights_hash)");
   const GemvPlan& g = plan_qkv_[layer];
   const int K = g.p.K, kst = K / 16;
   const int Qall = static_cast<int>(Qh_ * D_), Kall = static_cast<int>(Kh_ * D_);
@@ -1144,7 +1162,8 @@ void Engine::harness_step_device(int64_t layer, const float* x_dev, float* out_d
     throw StateError("the attention-only harness runs on a local pool; distributed pools use decode_step");
   if (!weights_ready_) throw StateError("weights are not initialised");
   require_context(layer);
-  cuda_check(launch_xprep_plain(x_dev, B_, static_cast<int>(H_), static_cast<int>(H_), d_xf_resid_, stream_),
+  cuda_check(launch_xprep_plain(x_dev, B_, static_cast<int>(H_), static_cast<int>(H_), d_xf_resid_, stream_,
+                                xf16_()),
              "xprep");
   enqueue_attention(layer);
   cuda_check(launch_merge_out(d_frag_o_, d_frag_lse_, B_, static_cast<int>(Qh_), q_per_slot_, kvp_,
@@ -1156,7 +1175,8 @@ void Engine::harness_step_device(int64_t layer, const float* x_dev, float* out_d
 }
 
 void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
-  cuda_check(launch_embed(emb_, tokens_dev, B_, static_cast<int>(H_), d_x_, d_ss_, d_xf_resid_, stream_), "embed");
+  cuda_check(launch_embed(emb_, tokens_dev, B_, static_cast<int>(H_), d_x_, d_ss_, d_xf_resid_, stream_, xf16_()),
+             "embed");
   mark(0);
   if (capture_hidden_)
     cuda_check(cudaMemcpyAsync(d_hidden_, d_x_, static_cast<size_t>(B_) * H_ * 4, cudaMemcpyDeviceToDevice, stream_),
@@ -1169,7 +1189,7 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
       // (a fused split+KVP merge kernel measured 0.2 ms/step slower than this pair)
       cuda_check(launch_xprep_merge_local(d_frag_o_, d_frag_lse_, B_, q_per_slot_, kvp_, AD_, ADP_,
                                           static_cast<int>(Qh_) * AD_, d_xf_attn_, d_total_ + l * B_, stream_,
-                                          mla_ ? d_att_ : nullptr),
+                                          mla_ ? d_att_ : nullptr, xf16_()),
                  "merge");
       if (mla_)
         cuda_check(launch_mla_uv(d_att_, w_uv_[l], B_, uv_heads_, static_cast<int>(D_), d_xf_attn_, stream_),
@@ -1181,7 +1201,7 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
       // merge of the exchanged slices, then TP O-proj over this rank's slice and
       // AllReduce over the pool (latency.cpp:85-94)
       cuda_check(launch_xprep_merge_recv(d_recv_, B_, kvp_, xchunk_, slice_, r_, AD_, d_xf_attn_,
-                                         d_total_ + l * B_, stream_, mla_ ? d_att_ : nullptr),
+                                         d_total_ + l * B_, stream_, mla_ ? d_att_ : nullptr, xf16_()),
                  "merge");
       if (mla_)
         cuda_check(launch_mla_uv(d_att_, w_uv_[l], B_, uv_heads_, static_cast<int>(D_), d_xf_attn_, stream_),
@@ -1189,13 +1209,15 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
       cuda_check(launch_gemv(plan_o_[l].p, 0, E_STORE, num_sms_, stream_), "o-proj");
       mark(4);
       if (!(skip_comm_ & 2)) transport_->all_reduce_sum(d_parth_, static_cast<size_t>(B_) * H_, stream_);
-      cuda_check(launch_residual_add(d_x_, d_parth_, B_, static_cast<int>(H_), d_ss_, d_xf_resid_, stream_),
+      cuda_check(launch_residual_add(d_x_, d_parth_, B_, static_cast<int>(H_), d_ss_, d_xf_resid_, stream_,
+                                     xf16_()),
                  "residual");
       mark(9);
       // TP FFN over F/N features (or EP x TPF experts), AllReduce (latency.cpp:110-144)
       enqueue_ffn(l);
       if (!(skip_comm_ & 2)) transport_->all_reduce_sum(d_parth_, static_cast<size_t>(B_) * H_, stream_);
-      cuda_check(launch_residual_add(d_x_, d_parth_, B_, static_cast<int>(H_), d_ss_, d_xf_resid_, stream_),
+      cuda_check(launch_residual_add(d_x_, d_parth_, B_, static_cast<int>(H_), d_ss_, d_xf_resid_, stream_,
+                                     xf16_()),
                  "residual");
       mark(9);
     }
@@ -1348,9 +1370,10 @@ void Engine::profile_step(int64_t reps, double* ms) {
 void Engine::info(hx_engine_info* o) const {
   std::memset(o, 0, sizeof(*o));
   o->kv_bytes_per_layer = static_cast<int64_t>(n_slots_) * B_ * kvh_per_slot_ * page_cap_ * page_bytes_;
-  int64_t wb = static_cast<int64_t>(plan_qkv_[0].p.Npad) * plan_qkv_[0].p.K * 2;
+  const int64_t wel = w8_ ? 1 : 2;  // GEMV weight element bytes
+  int64_t wb = static_cast<int64_t>(plan_qkv_[0].p.Npad) * plan_qkv_[0].p.K * wel;
   if (mla_) wb += (Qh_ * D_ * W_ + static_cast<int64_t>(uv_heads_) * DV_ * D_) * 2;  // W_UK + W_UV
-  auto bytes = [](const GemvPlan& g) { return static_cast<int64_t>(g.p.Npad) * g.p.K * 2; };
+  auto bytes = [wel](const GemvPlan& g) { return static_cast<int64_t>(g.p.Npad) * g.p.K * wel; };
   if (!attn_only_) {
     wb += bytes(plan_o_[0]);
     if (F_ > 0) wb += bytes(plan_gu_[0]) + bytes(plan_down_[0]);
@@ -1358,7 +1381,7 @@ void Engine::info(hx_engine_info* o) const {
       wb += bytes(plan_router_[0]) + static_cast<int64_t>(E_local_) * (bytes(plan_egu_[0]) + bytes(plan_edown_[0]));
   }
   o->weight_bytes_per_layer = wb;
-  o->head_bytes = attn_only_ ? 0 : static_cast<int64_t>(plan_lm_.p.Npad) * plan_lm_.p.K * 2 + V_ * H_ * 2;
+  o->head_bytes = attn_only_ ? 0 : static_cast<int64_t>(plan_lm_.p.Npad) * plan_lm_.p.K * wel + V_ * H_ * 2;
   o->attn_streams = n_streams_;
   o->attn_splits = splits_;
   o->attn_items = n_items_;
@@ -1369,6 +1392,7 @@ void Engine::info(hx_engine_info* o) const {
   o->page_cap = page_cap_;
   o->head_dim_padded = DP_;
   o->kv_dtype = kv8_ ? HX_KV_FP8_E4M3 : HX_KV_BF16;
+  o->w_dtype = w8_ ? HX_W_FP8_E4M3 : HX_W_BF16;
 }
 
 }  // namespace hx

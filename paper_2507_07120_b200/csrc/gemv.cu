@@ -20,6 +20,13 @@
 //   E_STORE  plain store (tensor-parallel partial products before AllReduce)
 // RMSNorm without a weight is a per-row scalar: (x * s) W = s * (x W), so
 // normalised consumers multiply y by s = rsqrt(mean(x^2) + eps) in the epilogue.
+//
+// FP8 weights (W8, hx_runtime_config.w_dtype = HX_W_FP8_E4M3): the same tile
+// order with 8 e4m3 bytes per lane (256 B per 16x16 tile, 2 KB per 128-row
+// k-step), widened exactly to f16 by cvt.rn.f16x2.e4m3x2 and multiplied by the
+// activation's two f16 terms (xfrag.cuh, xf16) on the f16 MMA; the per-output
+// power-of-two scale s_n is applied in the epilogue after the split-K sum
+// (exact: y_n = s_n * sum_k x_k q_kn).
 #include <algorithm>
 
 #include "common.cuh"
@@ -36,8 +43,8 @@ constexpr int kThreads = 256;     // consumer threads (+1 producer warp)
 constexpr int kStages = 4;        // ring depth (~150 KB in flight per SM)
 // k-steps per ring stage: 32 KB of weights (+ x slice) for B <= 16; fewer
 // k-steps when the x slice grows with the batch (B <= 64) so 4 stages fit.
-template <int NB8>
-constexpr int stage_steps() { return NB8 <= 2 ? 8 : (NB8 <= 4 ? 4 : 2); }
+template <int NB8, bool W8 = false>
+constexpr int stage_steps() { return W8 ? (NB8 == 1 ? 16 : 8) : (NB8 <= 2 ? 8 : (NB8 <= 4 ? 4 : 2)); }
 constexpr int kDone = -1;
 
 struct TileMeta {
@@ -57,18 +64,21 @@ __device__ __forceinline__ unsigned long long logit_key(float v, int n) {
   return (static_cast<unsigned long long>(u) << 32) | (0xFFFFFFFFu - static_cast<unsigned>(n));
 }
 
-__host__ __device__ __forceinline__ int stage_steps_rt(int nb8) { return nb8 <= 2 ? 8 : (nb8 <= 4 ? 4 : 2); }
-__host__ __device__ __forceinline__ size_t stage_bytes(int nb8) {
-  return static_cast<size_t>(stage_steps_rt(nb8)) * (4096 + xf_step_bytes(nb8));
+__host__ __device__ __forceinline__ int stage_steps_rt(int nb8, bool w8) {
+  return w8 ? (nb8 == 1 ? 16 : 8) : (nb8 <= 2 ? 8 : (nb8 <= 4 ? 4 : 2));
+}
+__host__ __device__ __forceinline__ size_t stage_bytes(int nb8, bool w8) {
+  return static_cast<size_t>(stage_steps_rt(nb8, w8)) * ((w8 ? 2048 : 4096) + xf_step_bytes(nb8));
 }
 
 }  // namespace
 
-template <int NB8, int EM, int XS, bool NORM>
+template <int NB8, int EM, int XS, bool NORM, bool W8>
 __global__ void __launch_bounds__(kThreads + 32, 1) gemv_kernel(const GemvParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int kStageSteps = stage_steps<NB8>();
-  constexpr size_t SW = kStageSteps * 4096;                   // weight bytes per stage
+  constexpr int kStageSteps = stage_steps<NB8, W8>();
+  constexpr uint32_t WB = W8 ? 2048 : 4096;                   // weight bytes per k-step (128 rows)
+  constexpr size_t SW = kStageSteps * WB;                     // weight bytes per stage
   constexpr size_t SX = kStageSteps * kXfTerms * NB8 * 256;   // x-fragment bytes per stage
   constexpr size_t SB = SW + SX;
   uint8_t* ring = smem;
@@ -136,8 +146,8 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemv_kernel(const GemvParams
           m.kc = kc;
           m.gi = gi;
           uint8_t* dst = ring + s * SB;
-          mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(n) * (4096u + kXfTerms * NB8 * 256u));
-          bulk_g2s(dst, wg + (static_cast<size_t>(nb) * KST + a) * 4096, static_cast<uint32_t>(n) * 4096u, &full[s]);
+          mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(n) * (WB + kXfTerms * NB8 * 256u));
+          bulk_g2s(dst, wg + (static_cast<size_t>(nb) * KST + a) * WB, static_cast<uint32_t>(n) * WB, &full[s]);
           if (!waited) {
             griddep_wait();
             waited = true;
@@ -159,11 +169,23 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemv_kernel(const GemvParams
       mbar_wait(&full[s], (st / kStages) & 1);
       const TileMeta m = meta[s];
       if (m.tile == kDone) break;
-      const uint32_t wbase = ring_base + s * SB + warp * 512 + lane * 16;
+      const uint32_t wbase = ring_base + s * SB + warp * (WB / 8) + lane * (WB / 256);
       const uint32_t xbase = ring_base + s * SB + SW + lane * 8;
 #pragma unroll
       for (int kk = 0; kk < kStageSteps; ++kk) {
-        if (kk < m.nks) {
+        if (W8 && kk < m.nks) {
+          const uint2 w8 = lds64(wbase + kk * WB);
+          uint32_t a0, a1, a2, a3;
+          e4m3x4_to_f16x2x2(w8.x, a0, a1);
+          e4m3x4_to_f16x2x2(w8.y, a2, a3);
+#pragma unroll
+          for (int t = 0; t < XS; ++t)
+#pragma unroll
+            for (int bg = 0; bg < NB8; ++bg) {
+              const uint2 bx = lds64(xbase + ((kk * kXfTerms + t) * NB8 + bg) * 256);
+              mma_f16_16816(acc[t * NB8 + bg], a0, a1, a2, a3, bx.x, bx.y);
+            }
+        } else if (kk < m.nks) {
           const uint4 wa = lds128(wbase + kk * 4096);
 #pragma unroll
           for (int t = 0; t < XS; ++t)
@@ -300,13 +322,17 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
         y[1] = yg[1];
       }
     }
+    if (p.wscale) {  // FP8 weights: per-output power-of-two scale (exact)
+      y[0] *= p.wscale[nb * kRows + r];
+      if (EM == E_SWIGLU) y[1] *= p.wscale[nb * kRows + r + kRows / 2];
+    }
     if (NORM) {
       y[0] *= s_inv[b];
       y[1] *= s_inv[b];
     }
     if (EM == E_SWIGLU) {
       const int f = nb * (kRows / 2) + r;
-      if (f < p.N / 2) xf_write(xf_out, NB8, b, f, y[0] / (1.f + __expf(-y[0])) * y[1]);
+      if (f < p.N / 2) xf_write(xf_out, NB8, b, f, y[0] / (1.f + __expf(-y[0])) * y[1], p.xf16);
       continue;
     }
     if (n >= p.N) continue;
@@ -317,7 +343,7 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
     } else if (EM == E_RESID) {
       const float keep = old + y[0];
       p.out[static_cast<size_t>(b) * p.out_stride + n] = keep;
-      xf_write(p.xf_out, NB8, b, n, keep);
+      xf_write(p.xf_out, NB8, b, n, keep, p.xf16);
       vt[b][r] = keep * keep;
     } else if (EM == E_LOGITS) {
       if (p.out) p.out[static_cast<size_t>(b) * p.out_stride + n] = y[0];
@@ -392,21 +418,22 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
 
 size_t gemv_smem_bytes(const GemvParams& p) {
   const int nb8 = xf_nb8(p.batch);
-  return static_cast<size_t>(kStages) * stage_bytes(nb8) + kStages * sizeof(TileMeta) + 2 * kStages * 8 + 64;
+  return static_cast<size_t>(kStages) * stage_bytes(nb8, p.w8 != 0) + kStages * sizeof(TileMeta) +
+         2 * kStages * 8 + 64;
 }
 
-template <int NB8, int EM, int XS, bool NORM>
+template <int NB8, int EM, int XS, bool NORM, bool W8 = false>
 static cudaError_t launch_t(const GemvParams& p, int grid, cudaStream_t stream) {
   const size_t smem = gemv_smem_bytes(p);
   static size_t configured = 0;  // opt in once per instantiation
   if (!p.tc && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemv_kernel<NB8, EM, XS, NORM>,
+    cudaError_t e = cudaFuncSetAttribute(gemv_kernel<NB8, EM, XS, NORM, W8>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = smem;
   }
   cudaError_t e = p.tc ? launch_gemv_tc(p, NB8, XS, grid, stream)
-                       : launch_k(gemv_kernel<NB8, EM, XS, NORM>, dim3(grid), dim3(kThreads + 32), smem, stream, p);
+                       : launch_k(gemv_kernel<NB8, EM, XS, NORM, W8>, dim3(grid), dim3(kThreads + 32), smem, stream, p);
   if (e != cudaSuccess) return e;
   const int rows_here = EM == E_SWIGLU ? kRows / 2 : kRows;
   const int gz = p.batch > 8 ? (p.batch + 7) / 8 : 1;  // one grid layer per 8 requests
@@ -418,6 +445,20 @@ static cudaError_t launch_t(const GemvParams& p, int grid, cudaStream_t stream) 
 
 template <int NB8>
 static cudaError_t dispatch_nb(const GemvParams& p, int norm, int em, int grid, cudaStream_t s) {
+  if constexpr (NB8 <= 2) {
+    if (p.w8) {  // FP8 weights: two f16 activation terms (22 bits) serve every projection
+#define HX_CASE8(E, NORMV) \
+  if (em == E && (norm != 0) == NORMV) return launch_t<NB8, E, 2, NORMV, true>(p, grid, s);
+      HX_CASE8(E_QKV, true)
+      HX_CASE8(E_QKV, false)
+      HX_CASE8(E_RESID, false)
+      HX_CASE8(E_STORE, false)
+      HX_CASE8(E_SWIGLU, true)
+      HX_CASE8(E_LOGITS, true)
+#undef HX_CASE8
+      return cudaErrorInvalidValue;
+    }
+  }
   // QKV feeds exp(q.k) with |logits| up to ~1e3 under the reference's unscaled
   // weights: carry x at fp32 precision there (3 bf16 terms), 2 terms elsewhere.
 #define HX_CASE(E, XS, NORMV) \
@@ -436,6 +477,7 @@ static cudaError_t dispatch_nb(const GemvParams& p, int norm, int em, int grid, 
 cudaError_t launch_gemv(const GemvParams& p, int norm, int emode, int grid, cudaStream_t stream) {
   if (p.batch < 1 || p.batch > 64 || (p.K & 15) || (p.Npad % kRows)) return cudaErrorInvalidValue;
   if (p.tc && p.batch <= 16) return cudaErrorInvalidValue;  // tcgen05 path: N = 32 or 64 batch rows
+  if (p.w8 && (p.tc || p.batch > 16 || !p.wscale || p.group_count)) return cudaErrorInvalidValue;
   if (p.batch <= 8) return dispatch_nb<1>(p, norm, emode, grid, stream);
   if (p.batch <= 16) return dispatch_nb<2>(p, norm, emode, grid, stream);
   if (p.batch <= 32) return dispatch_nb<4>(p, norm, emode, grid, stream);

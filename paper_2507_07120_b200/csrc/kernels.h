@@ -134,6 +134,11 @@ struct GemvParams {
   const float* route_w;      // [B][n_experts] routing weights: the epilogue combines groups
   int n_experts;
   const float* addend;       // optional [B][out_stride] added by E_RESID / E_STORE
+  // FP8 weights (B <= 16, ungrouped): w holds e4m3 bytes in the same tile order
+  // ([Npad/128][K/16][8][32 lanes][8 B]), wscale the per-output power-of-two scales
+  int w8;
+  const float* wscale;       // [Npad]
+  int xf16;                  // xf_out written as two f16 terms (the next GEMV has FP8 weights)
 };
 cudaError_t launch_gemv(const GemvParams& p, int norm, int emode, int grid, cudaStream_t stream);
 // tcgen05 inner product for p.tc plans (gemv_tc.cu); the epilogue kernel is shared.
@@ -141,7 +146,9 @@ cudaError_t launch_gemv_tc(const GemvParams& p, int nb8, int xs, int grid, cudaS
 size_t gemv_smem_bytes(const GemvParams& p);
 
 // x-fragment producers (xfrag.cuh layout; nb8 = ceil(batch / 8))
-cudaError_t launch_xprep_plain(const float* x, int batch, int K, int x_stride, uint8_t* xf, cudaStream_t s);
+// xf16: write the fragments as two f16 terms (consumer GEMV has FP8 weights, xfrag.cuh)
+cudaError_t launch_xprep_plain(const float* x, int batch, int K, int x_stride, uint8_t* xf, cudaStream_t s,
+                               int xf16 = 0);
 // Merged attention output (canonical LSE merge over KVP fragments, attention.hpp:90-137):
 //  local pool: frag_o [slot][B][q_per_slot][DP], frag_lse [slot][B][q_per_slot]; K = hidden
 //  exchanged:  recv [kvp src][B][chunk] (slice + lse slots); K = slice of rank exch_rank
@@ -150,17 +157,17 @@ cudaError_t launch_xprep_plain(const float* x, int batch, int K, int x_stride, u
 // plain != null: write the merged output as fp32 [B][K] there instead of x-fragments.
 cudaError_t launch_xprep_merge_local(const float* frag_o, const float* frag_lse, int batch, int q_per_slot,
                                      int kvp, int head_dim, int dp, int K, uint8_t* xf, int* bump_total,
-                                     cudaStream_t s, float* plain = nullptr);
+                                     cudaStream_t s, float* plain = nullptr, int xf16 = 0);
 cudaError_t launch_xprep_merge_recv(const float* recv, int batch, int kvp, int chunk, int slice, int exch_rank,
                                     int head_dim, uint8_t* xf, int* bump_total, cudaStream_t s,
-                                    float* plain = nullptr);
+                                    float* plain = nullptr, int xf16 = 0);
 
 // ---------------------------------------------------------------- misc
 cudaError_t launch_merge_out(const float* frag_o, const float* frag_lse, int batch, int q_heads,
                              int q_per_slot, int kvp, int head_dim, int dp, float* out,
                              float* out_lse, int* bump_total, cudaStream_t stream);
 cudaError_t launch_embed(const uint16_t* emb, const int* tokens, int batch, int hidden,
-                         float* x, float* ss_part, uint8_t* xf, cudaStream_t stream);
+                         float* x, float* ss_part, uint8_t* xf, cudaStream_t stream, int xf16 = 0);
 cudaError_t launch_argmax_finish(const unsigned long long* best, int batch, int* tokens_out,
                                  unsigned long long* best_reset, cudaStream_t stream);
 // Scatter n tokens (bf16 K/V rows [n][kv_heads][head_dim]) of request b at global
@@ -190,6 +197,9 @@ struct WSeg {
 };
 cudaError_t launch_weight_init_hash(uint4* w, int Npad, int K, const WSeg* segs, int nseg,
                                     uint64_t seed, cudaStream_t stream, int tc = 0);
+// FP8 weights: per-output power-of-two scales over the full input range k_full, then the e4m3 image.
+cudaError_t launch_weight_init_hash_w8(uint8_t* w, float* scale, int Npad, int K, int k_full, const WSeg* segs,
+                                       int nseg, uint64_t seed, cudaStream_t stream);
 cudaError_t launch_emb_init_hash(uint16_t* emb, int vocab, int hidden, uint64_t seed,
                                  uint64_t stream_id, cudaStream_t stream);
 // Plain row-major bf16: w[i] = bf16(hash_unit(seed, stream_id, idx0 + i) * scale), i < n.
@@ -209,6 +219,6 @@ cudaError_t launch_moe_route(const float* logits, int batch, int n_experts, int 
                              float* route_w, int* group_ids, int* group_count, cudaStream_t s);
 // Residual add of an all-reduced partial product + RMSNorm statistics.
 cudaError_t launch_residual_add(float* x, const float* part, int batch, int hidden, float* ss_part,
-                                uint8_t* xf, cudaStream_t s);
+                                uint8_t* xf, cudaStream_t s, int xf16 = 0);
 
 }  // namespace hx

@@ -71,7 +71,7 @@ cudaError_t launch_merge_out(const float* frag_o, const float* frag_lse, int bat
 // (128-column block, request), ss_part[blk][b] = sum of x^2 over the block --
 // the same RMSNorm partials the residual epilogues write.
 __global__ void embed_kernel(const __nv_bfloat16* emb, const int* tokens, int batch, int hidden,
-                             float* x, float* ss_part, uint8_t* xf) {
+                             float* x, float* ss_part, uint8_t* xf, int xf16) {
   griddep_wait();
   griddep_launch_dependents();
   const int nb = blockIdx.x, b = blockIdx.y;
@@ -80,7 +80,7 @@ __global__ void embed_kernel(const __nv_bfloat16* emb, const int* tokens, int ba
   if (col < hidden) {
     v = __bfloat162float(emb[static_cast<size_t>(tokens[b]) * hidden + col]);
     x[static_cast<size_t>(b) * hidden + col] = v;
-    xf_write(xf, xf_nb8(batch), b, col, v);
+    xf_write(xf, xf_nb8(batch), b, col, v, xf16);
   }
   float s = v * v;
   __shared__ float red[4];
@@ -92,9 +92,9 @@ __global__ void embed_kernel(const __nv_bfloat16* emb, const int* tokens, int ba
 }
 
 cudaError_t launch_embed(const uint16_t* emb, const int* tokens, int batch, int hidden, float* x,
-                         float* ss_part, uint8_t* xf, cudaStream_t stream) {
+                         float* ss_part, uint8_t* xf, cudaStream_t stream, int xf16) {
   return launch_k(embed_kernel, dim3((hidden + 127) / 128, batch), dim3(128), 0, stream,
-                  reinterpret_cast<const __nv_bfloat16*>(emb), tokens, batch, hidden, x, ss_part, xf);
+                  reinterpret_cast<const __nv_bfloat16*>(emb), tokens, batch, hidden, x, ss_part, xf, xf16);
 }
 
 __global__ void argmax_finish_kernel(const unsigned long long* best, int batch, int* tokens_out,
@@ -358,6 +358,67 @@ __global__ void weight_init_hash_kernel(uint4* w, int Npad, int K, const WSeg* s
   w[idx] = out;
 }
 
+// FP8 weights: the same chunk order with 8 e4m3 bytes per chunk, value / scale[n].
+__global__ void weight_init_hash_w8_kernel(uint2* w, int Npad, int K, const WSeg* segs, int nseg, uint64_t seed,
+                                           const float* scale) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int kst = K >> 4;
+  if (idx >= static_cast<long long>(Npad / 16) * kst * 32) return;
+  const int lane = static_cast<int>(idx & 31);
+  long long t = idx >> 5;
+  const int ntl = static_cast<int>(t & 7);
+  t >>= 3;
+  const int ks = static_cast<int>(t % kst), nb = static_cast<int>(t / kst);
+  const int nt = nb * 8 + ntl;
+  const int g = lane >> 2, c = lane & 3;
+  uint2 out;
+  uint8_t* o = reinterpret_cast<uint8_t*>(&out);
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    const int reg = e >> 1, elem = e & 1;
+    const int rowhalf = reg & 1, khalf = reg >> 1;
+    const int n = nt * 16 + rowhalf * 8 + g;
+    const int k = ks * 16 + khalf * 8 + 2 * c + elem;
+    o[e] = e4m3_from_double(wseg_value(segs, nseg, n, k, seed) / static_cast<double>(scale[n]));
+  }
+  w[idx] = out;
+}
+
+// scale[n] = the smallest power of two >= max over the FULL input range of
+// |W[k][n]| / 448 (oracle fp8_pow2_scale; k in [-k_offset, k_full - k_offset)
+// of a tensor-parallel input shard), 1 for an all-zero row. One warp per row.
+__global__ void weight_scale_hash_kernel(float* scale, int Npad, int k_full, const WSeg* segs, int nseg,
+                                         uint64_t seed) {
+  const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (n >= Npad) return;
+  int koff = 0;
+  for (int s = 0; s < nseg; ++s)
+    if (n >= segs[s].rows_begin && n < segs[s].rows_end) koff = segs[s].k_offset;
+  double mx = 0.0;
+  for (int k = lane; k < k_full; k += 32) mx = fmax(mx, fabs(wseg_value(segs, nseg, n, k - koff, seed)));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (lane == 0) {
+    double sc = 1.0;
+    if (mx > 0.0) {
+      int e;
+      const double f = frexp(mx / 448.0, &e);
+      sc = ldexp(1.0, f == 0.5 ? e - 1 : e);
+    }
+    scale[n] = static_cast<float>(sc);
+  }
+}
+
+cudaError_t launch_weight_init_hash_w8(uint8_t* w, float* scale, int Npad, int K, int k_full, const WSeg* segs,
+                                       int nseg, uint64_t seed, cudaStream_t stream) {
+  weight_scale_hash_kernel<<<static_cast<unsigned>((Npad + 7) / 8), 256, 0, stream>>>(scale, Npad, k_full, segs,
+                                                                                     nseg, seed);
+  const long long work = static_cast<long long>(Npad / 16) * (K / 16) * 32;
+  weight_init_hash_w8_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(
+      reinterpret_cast<uint2*>(w), Npad, K, segs, nseg, seed, scale);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_weight_init_hash(uint4* w, int Npad, int K, const WSeg* segs, int nseg,
                                     uint64_t seed, cudaStream_t stream, int tc) {
   const long long work = static_cast<long long>(Npad / 16) * (K / 16) * 32;
@@ -460,7 +521,7 @@ cudaError_t launch_pack_exchange(const float* frag_o, const float* frag_lse, int
 
 // x[b][n] += part[b][n]; ss_part[blk][b] = sum over the 128-column block of x^2 (deterministic).
 __global__ void residual_add_kernel(float* x, const float* part, int batch, int hidden, float* ss_part,
-                                    uint8_t* xf) {
+                                    uint8_t* xf, int xf16) {
   griddep_wait();
   griddep_launch_dependents();
   const int blk = blockIdx.x, b = blockIdx.y;
@@ -469,7 +530,7 @@ __global__ void residual_add_kernel(float* x, const float* part, int batch, int 
   if (n < hidden) {
     v = x[static_cast<size_t>(b) * hidden + n] + part[static_cast<size_t>(b) * hidden + n];
     x[static_cast<size_t>(b) * hidden + n] = v;
-    xf_write(xf, xf_nb8(batch), b, n, v);
+    xf_write(xf, xf_nb8(batch), b, n, v, xf16);
   }
   float s = v * v;
 #pragma unroll
@@ -480,32 +541,33 @@ __global__ void residual_add_kernel(float* x, const float* part, int batch, int 
   if (threadIdx.x == 0) ss_part[static_cast<size_t>(blk) * batch + b] = (red[0] + red[1]) + (red[2] + red[3]);
 }
 cudaError_t launch_residual_add(float* x, const float* part, int batch, int hidden, float* ss_part,
-                                uint8_t* xf, cudaStream_t s) {
+                                uint8_t* xf, cudaStream_t s, int xf16) {
   return launch_k(residual_add_kernel, dim3((hidden + 127) / 128, batch), dim3(128), 0, s, x, part, batch, hidden,
-                  ss_part, xf);
+                  ss_part, xf, xf16);
 }
 }  // namespace hx
 
 // ---------------------------------------------------------------- x-fragment producers
 namespace hx {
-__global__ void xprep_plain_kernel(const float* x, int batch, int K, int x_stride, uint8_t* xf) {
+__global__ void xprep_plain_kernel(const float* x, int batch, int K, int x_stride, uint8_t* xf, int xf16) {
   griddep_wait();
   griddep_launch_dependents();
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= static_cast<long long>(batch) * K) return;
   const int b = static_cast<int>(i / K), k = static_cast<int>(i % K);
-  xf_write(xf, xf_nb8(batch), b, k, x[static_cast<size_t>(b) * x_stride + k]);
+  xf_write(xf, xf_nb8(batch), b, k, x[static_cast<size_t>(b) * x_stride + k], xf16);
 }
-cudaError_t launch_xprep_plain(const float* x, int batch, int K, int x_stride, uint8_t* xf, cudaStream_t s) {
+cudaError_t launch_xprep_plain(const float* x, int batch, int K, int x_stride, uint8_t* xf, cudaStream_t s,
+                               int xf16) {
   const long long n = static_cast<long long>(batch) * K;
   return launch_k(xprep_plain_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, x, batch, K,
-                  x_stride, xf);
+                  x_stride, xf, xf16);
 }
 
 
 __global__ void xprep_merge_local_kernel(const float* frag_o, const float* frag_lse, int batch, int q_per_slot,
                                          int kvp, int head_dim, int dp, int K, uint8_t* xf, int* bump_total,
-                                         float* plain) {
+                                         float* plain, int xf16) {
   griddep_wait();
   griddep_launch_dependents();
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -528,18 +590,18 @@ __global__ void xprep_merge_local_kernel(const float* frag_o, const float* frag_
   if (plain)
     plain[i] = v;
   else
-    xf_write(xf, xf_nb8(batch), b, k, v);
+    xf_write(xf, xf_nb8(batch), b, k, v, xf16);
 }
 cudaError_t launch_xprep_merge_local(const float* frag_o, const float* frag_lse, int batch, int q_per_slot,
                                      int kvp, int head_dim, int dp, int K, uint8_t* xf, int* bump_total,
-                                     cudaStream_t s, float* plain) {
+                                     cudaStream_t s, float* plain, int xf16) {
   const long long n = static_cast<long long>(batch) * K;
   return launch_k(xprep_merge_local_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, frag_o,
-                  frag_lse, batch, q_per_slot, kvp, head_dim, dp, K, xf, bump_total, plain);
+                  frag_lse, batch, q_per_slot, kvp, head_dim, dp, K, xf, bump_total, plain, xf16);
 }
 
 __global__ void xprep_merge_recv_kernel(const float* recv, int batch, int kvp, int chunk, int slice, int exch_rank,
-                                        int head_dim, uint8_t* xf, int* bump_total, float* plain) {
+                                        int head_dim, uint8_t* xf, int* bump_total, float* plain, int xf16) {
   griddep_wait();
   griddep_launch_dependents();
   const long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
@@ -561,13 +623,14 @@ __global__ void xprep_merge_recv_kernel(const float* recv, int batch, int kvp, i
   if (plain)
     plain[i] = v;
   else
-    xf_write(xf, xf_nb8(batch), b, k, v);
+    xf_write(xf, xf_nb8(batch), b, k, v, xf16);
 }
 cudaError_t launch_xprep_merge_recv(const float* recv, int batch, int kvp, int chunk, int slice, int exch_rank,
-                                    int head_dim, uint8_t* xf, int* bump_total, cudaStream_t s, float* plain) {
+                                    int head_dim, uint8_t* xf, int* bump_total, cudaStream_t s, float* plain,
+                                    int xf16) {
   const long long n = static_cast<long long>(batch) * slice;
   return launch_k(xprep_merge_recv_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, recv,
-                  batch, kvp, chunk, slice, exch_rank, head_dim, xf, bump_total, plain);
+                  batch, kvp, chunk, slice, exch_rank, head_dim, xf, bump_total, plain, xf16);
 }
 }  // namespace hx
 

@@ -9,6 +9,9 @@
 //   u32 0 = (x[b][16ks+2c], x[b][16ks+2c+1]), u32 1 = (x[b][16ks+2c+8], x[b][16ks+2c+9])
 //   terms: hi = bf16(x), mid = bf16(x - hi), lo = bf16(x - hi - mid); a GEMV
 //   that needs ~16-bit activations reads hi+mid, the QKV projection all three.
+//   FP8-weight models (xf16 = 1) store two f16 terms instead (hi = f16(x),
+//   lo = f16(x - hi): 22 significant bits, absolute floor 2^-25; term 2 zero)
+//   for the f16 MMA that multiplies the widened e4m3 weights.
 //
 // Batches above 16 (nb8 >= 4) run the tcgen05 GEMV (gemv_tc.cu), whose B
 // operand is K-major in canonical core matrices: layout
@@ -30,19 +33,27 @@ __host__ __device__ __forceinline__ size_t xf_step_bytes(int nb8) {
 }
 
 // Write activation value v of (batch b, column k) into the fragment buffer.
-HX_DEV void xf_write(uint8_t* xf, int nb8, int b, int k, float v) {
+HX_DEV void xf_write(uint8_t* xf, int nb8, int b, int k, float v, int xf16 = 0) {
   const int ks = k >> 4, r = k & 15;
   const int half = r >> 3, c = (r & 7) >> 1, elem = r & 1;
   const int g = b & 7, bg = b >> 3;
   const int lane = g * 4 + c;
   float t[3];
-  split3(v, t[0], t[1], t[2]);
+  if (xf16) {
+    split2h(v, t[0], t[1]);
+    t[2] = 0.f;
+  } else {
+    split3(v, t[0], t[1], t[2]);
+  }
   const bool tc = nb8 >= 4;
 #pragma unroll
   for (int term = 0; term < kXfTerms; ++term) {
     const size_t blk = ((static_cast<size_t>(ks) * kXfTerms + term) * nb8 + bg) * 32 * 8;
     const size_t off = tc ? blk + half * 128 + g * 16 + (r & 7) * 2 : blk + lane * 8 + half * 4 + elem * 2;
-    *reinterpret_cast<__nv_bfloat16*>(xf + off) = __float2bfloat16_rn(t[term]);
+    if (xf16)
+      *reinterpret_cast<__half*>(xf + off) = __float2half_rn(t[term]);
+    else
+      *reinterpret_cast<__nv_bfloat16*>(xf + off) = __float2bfloat16_rn(t[term]);
   }
 }
 

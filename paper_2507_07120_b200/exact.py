@@ -12,7 +12,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from ._lib import (KV_DTYPES, EngineInfo, ModelConfig, ParallelConfig, RuntimeConfig, check, lib)
+from ._lib import (KV_DTYPES, W_DTYPES, EngineInfo, ModelConfig, ParallelConfig, RuntimeConfig, check, lib)
 
 _fp = C.POINTER(C.c_float)
 
@@ -61,7 +61,7 @@ class MsgKind:
 
 class _Engine:
     def __init__(self, model, tpa, kvp, chunk_size, batch, capacity, device=0, use_graphs=True, hopb=False,
-                 pool=0, rank=0, nccl_id=None, loopback=None, ep=1, kv_dtype="bf16"):
+                 pool=0, rank=0, nccl_id=None, loopback=None, ep=1, kv_dtype="bf16", w_dtype="bf16"):
         self.mc = model
         self._nccl_buf = C.create_string_buffer(bytes(nccl_id), 128) if nccl_id is not None else None
         self._loopback = loopback  # the group must outlive its engines
@@ -70,8 +70,10 @@ class _Engine:
                                  loopback=loopback._h if loopback is not None else None, ep=ep)
         if kv_dtype not in KV_DTYPES:
             raise ValueError(f"kv_dtype must be one of {sorted(KV_DTYPES)}")
+        if w_dtype not in W_DTYPES:
+            raise ValueError(f"w_dtype must be one of {sorted(W_DTYPES)}")
         self.rc = RuntimeConfig(batch=batch, capacity_tokens=capacity, device=device, hopb=int(hopb),
-                                use_graphs=int(use_graphs), kv_dtype=KV_DTYPES[kv_dtype])
+                                use_graphs=int(use_graphs), kv_dtype=KV_DTYPES[kv_dtype], w_dtype=W_DTYPES[w_dtype])
         h = C.c_void_p()
         check(lib().hx_engine_create(C.byref(self.mc), C.byref(self.pc), C.byref(self.rc), C.byref(h)))
         self._h = h

@@ -351,7 +351,7 @@ class HelixDecoder(_Engine):
 
     def __init__(self, spec, tpa=1, kvp=1, chunk_size=16, batch=8, capacity=4096, layers=None, vocab=None,
                  device=0, use_graphs=True, hopb=False, pool=0, rank=0, nccl_id=None, loopback=None, ep=1,
-                 kv_dtype="bf16"):
+                 kv_dtype="bf16", w_dtype="bf16"):
         self.spec = spec
         self.layers = layers or spec.layers
         self.vocab = vocab or spec.vocab
@@ -363,7 +363,8 @@ class HelixDecoder(_Engine):
                          expert_ffn=m.expert_ffn_dim if m else 0,
                          kv_latent=spec.kv_latent_dim if spec.attention == "mla" else 0)
         super().__init__(mc, tpa, kvp, chunk_size, batch, capacity, device, use_graphs=use_graphs, hopb=hopb,
-                         pool=pool, rank=rank, nccl_id=nccl_id, loopback=loopback, ep=ep, kv_dtype=kv_dtype)
+                         pool=pool, rank=rank, nccl_id=nccl_id, loopback=loopback, ep=ep, kv_dtype=kv_dtype,
+                         w_dtype=w_dtype)
         self.n_ranks = tpa * kvp if pool else 1
         self.rank = rank
         self.vocab_local = -(-self.vocab // self.n_ranks)

@@ -54,6 +54,7 @@ def lib():
             "oracle_model_create": (C.c_int, [i64] * 11 + [u64, C.c_int, C.c_int, C.POINTER(vp)]),
             "oracle_model_create_moe": (C.c_int, [i64] * 14 + [u64, C.c_int, C.c_int, C.POINTER(vp)]),
             "oracle_model_create_ex": (C.c_int, [i64] * 15 + [u64, C.c_int, C.c_int, C.POINTER(vp)]),
+            "oracle_model_create_w8": (C.c_int, [i64] * 11 + [u64, C.POINTER(vp)]),
             "oracle_model_routes": (C.c_int, [vp, ip]),
             "oracle_model_route_gaps": (C.c_int, [vp, dp]),
             "oracle_model_free": (None, [vp]),
@@ -243,15 +244,20 @@ class Model:
     WEIGHTS = {"wq": 0, "wk": 1, "wv": 2, "wo": 3, "wgate": 4, "wup": 5, "wdown": 6, "emb": 7, "lm": 8}
 
     def __init__(self, hidden, q, k, hsz, ffn, layers, vocab, tpa=1, kvp=1, chunk=16, batch=1,
-                 seed=0, qkv_hash=False, bf16=True, moe=None, kv_latent=0, kv_fp8=False):
+                 seed=0, qkv_hash=False, bf16=True, moe=None, kv_latent=0, kv_fp8=False, w_fp8=False):
         """moe = (n_experts, top_k, expert_ffn): every layer's FFN is routed MoE,
         `ffn` is then the shared expert width (0: none). kv_latent > 0: MLA
-        attention with latent width 2*kv_latent (layer_oracle.hpp)."""
+        attention with latent width 2*kv_latent (layer_oracle.hpp). w_fp8: e4m3
+        GEMV weights with per-output power-of-two scales (dense, hash init)."""
         self.dims = dict(hidden=hidden, q=q, k=k, hsz=hsz, ffn=ffn, layers=layers, vocab=vocab)
         self.batch = batch
         self.moe = moe
         h = C.c_void_p()
-        if kv_latent:
+        if w_fp8:
+            assert qkv_hash and not moe and not kv_latent
+            check(lib().oracle_model_create_w8(hidden, q, k, hsz, ffn, layers, vocab, tpa, kvp, chunk, batch, seed,
+                                               C.byref(h)))
+        elif kv_latent:
             m = moe or (0, 0, 0)
             check(lib().oracle_model_create_ex(hidden, q, k, hsz, ffn, layers, vocab, m[0], m[1], m[2], kv_latent,
                                                tpa, kvp, chunk, batch, seed, int(qkv_hash), int(bf16), C.byref(h)))

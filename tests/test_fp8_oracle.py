@@ -32,3 +32,19 @@ def test_round_e4m3_grid():
     vals = [v for v in vals if v <= 448.0]
     np.testing.assert_array_equal(O.round_e4m3(vals), np.array(vals))
     assert O.round_e4m3([1e30])[0] == 448.0 and O.round_e4m3([-1e30])[0] == -448.0
+
+
+def test_fp8_weights_oracle_quantisation():
+    """ModelDims::w_fp8 (layer_oracle.cpp hash_matrix_fp8): each GEMV weight column
+    (output feature) n is e4m3(W / s_n) * s_n with s_n the smallest power of two
+    >= max_k |W[k][n]| / 448; the unquantised draws come from the bf16=False oracle."""
+    H, Q, K, D, F, V = 64, 4, 2, 16, 96, 50
+    q8 = O.Model(H, Q, K, D, F, 1, V, seed=9, qkv_hash=True, w_fp8=True)
+    ref = O.Model(H, Q, K, D, F, 1, V, seed=9, qkv_hash=True, bf16=False)
+    for name in ("wq", "wk", "wv", "wo", "wgate", "wup", "wdown", "lm"):
+        w, w0 = q8.weight(name), ref.weight(name)
+        amax = np.abs(w0).max(axis=0)
+        s = np.exp2(np.ceil(np.log2(amax / 448.0)))
+        np.testing.assert_array_equal(w, O.round_e4m3(w0 / s) * s)
+        assert np.all(np.abs(w / s).max(axis=0) <= 448.0)
+        assert np.all(np.abs(w / s).max(axis=0) > 224.0 * 0.9)  # the scale is the smallest power of two

@@ -1,0 +1,124 @@
+"""GPU parity of FP8 (e4m3) GEMV weights (w_dtype="fp8").
+
+Every GEMV weight (QKV, O, gate/up, down, LM head) is stored as e4m3 with a
+power-of-two scale per output feature; the oracle quantises its double hash
+draws identically (layer_oracle.cpp hash_matrix_fp8, pinned on CPU in
+tests/test_fp8_oracle.py), so GPU and oracle multiply the SAME weights. The GPU
+widens e4m3 exactly to f16 and carries activations as two f16 terms (22 bits),
+so the comparison bounds are the bf16 path's: 2e-3 on the first step's hidden
+states / logits (fp32 accumulation over K, exact-weight operands).
+"""
+import threading
+
+import numpy as np
+import pytest
+
+from tests import oracle_py as O
+
+pytestmark = pytest.mark.gpu
+
+
+def rel_err(got, want):
+    return float(np.abs(got - want).max() / max(1e-12, np.abs(want).max()))
+
+
+@pytest.mark.parametrize("q,k,hsz,kvp,B,kv", [(8, 2, 32, 2, 3, "bf16"), (32, 2, 64, 1, 8, "bf16"),
+                                              (16, 1, 128, 4, 16, "bf16"), (8, 2, 64, 2, 5, "fp8")])
+def test_fp8_weights_decode_step_matches_oracle(q, k, hsz, kvp, B, kv):
+    import paper_2507_07120_b200 as P
+    H, F, L, V = q * hsz, 384, 2, 700
+    spec = P.model.ModelSpec("w8", L, H, q, k, hsz, F, 3, "gqa", 0, vocab=V)
+    g = P.HelixDecoder(spec, tpa=1, kvp=kvp, batch=B, capacity=2100, layers=L, vocab=V, kv_dtype=kv, w_dtype="fp8")
+    assert g.info()["w_dtype"] == 1
+    g.init_weights(17, qkv="hash")
+    g.fill_kv_hash(2000, 17)
+    o = O.Model(H, q, k, hsz, F, L, V, tpa=1, kvp=kvp, batch=B, seed=17, qkv_hash=True, kv_fp8=kv == "fp8",
+                w_fp8=True)
+    for l in range(L):
+        for b in range(B):
+            o.grow_hash(l, b, 2000)
+    tokens = (np.arange(B) * 131 + 1) % V
+    for step in range(2):
+        nxt, logits, hidden = g.step(tokens, want_logits=True, want_hidden=True)
+        lo, ho, no = o.step(tokens)
+        tol = 2e-3 if step == 0 else 2e-2
+        e_h, e_l = rel_err(hidden, ho), rel_err(logits, lo)
+        print(f"q={q} k={k} hsz={hsz} kvp={kvp} B={B} kv={kv} step={step} hidden={e_h:.2e} logits={e_l:.2e}")
+        assert e_h <= tol and e_l <= tol
+        tokens = no
+    g.close()
+
+
+def test_fp8_weights_loopback_pool():
+    """Distributed layout (TP-sharded O-proj rows / FFN columns / vocabulary): the
+    per-output scales span the FULL input range of each sharded matrix, so every
+    rank's shard carries the oracle's quantisation."""
+    import paper_2507_07120_b200 as P
+    from paper_2507_07120_b200.model import Loopback
+    H, Q, K, D, F, L, V, B, kvp = 512, 16, 2, 32, 512, 2, 400, 2, 2
+    spec = P.model.ModelSpec("w8d", L, H, Q, K, D, F, 3, "gqa", 0, vocab=V)
+    lb = Loopback(kvp)
+    engines = [P.HelixDecoder(spec, tpa=1, kvp=kvp, batch=B, capacity=3000, layers=L, vocab=V, use_graphs=False,
+                              pool=2, rank=r, loopback=lb, w_dtype="fp8") for r in range(kvp)]
+    for e in engines:
+        e.init_weights(3, qkv="hash")
+        e.fill_kv_hash(2500, 3)
+    o = O.Model(H, Q, K, D, F, L, V, tpa=1, kvp=kvp, batch=B, seed=3, qkv_hash=True, w_fp8=True)
+    for l in range(L):
+        for b in range(B):
+            o.grow_hash(l, b, 2500)
+    tokens = np.array([4, 399])
+    res = [None] * kvp
+    errors = []
+
+    def run(r):
+        try:
+            res[r] = engines[r].step(tokens, want_logits=True, want_hidden=True)
+        except Exception as ex:  # surfaced below
+            errors.append(ex)
+    th = [threading.Thread(target=run, args=(r,), daemon=True) for r in range(kvp)]
+    [t.start() for t in th]
+    [t.join(timeout=120) for t in th]
+    assert not errors, errors
+    lo, ho, no = o.step(tokens)
+    for r in range(kvp):
+        e_h = rel_err(res[r][2], ho)
+        print(f"rank {r}: hidden {e_h:.2e}")
+        assert e_h <= 2e-3
+        np.testing.assert_array_equal(res[r][0], no)
+    for e in engines:
+        e.close()
+
+
+def test_fp8_weights_halve_weight_bytes():
+    import paper_2507_07120_b200 as P
+    spec = P.model.ModelSpec("w8", 1, 1024, 8, 2, 128, 1024, 3, "gqa", 0, vocab=512)
+    a = P.HelixDecoder(spec, batch=2, capacity=64, layers=1, vocab=512)
+    b = P.HelixDecoder(spec, batch=2, capacity=64, layers=1, vocab=512, w_dtype="fp8")
+    assert b.info()["weight_bytes_per_layer"] * 2 == a.info()["weight_bytes_per_layer"]
+    a.close()
+    b.close()
+
+
+@pytest.mark.parametrize("what", ["mla", "moe", "batch", "mt19937"])
+def test_fp8_weights_rejections(what):
+    import paper_2507_07120_b200 as P
+    if what == "mla":
+        spec = P.model.ModelSpec("mla", 1, 256, 16, 1, 16, 256, 3, "mla", 288, vocab=300)
+        with pytest.raises(ValueError, match="FP8 weights"):
+            P.HelixDecoder(spec, batch=1, capacity=64, layers=1, vocab=300, w_dtype="fp8")
+    elif what == "moe":
+        spec = P.model.ModelSpec("moe", 1, 256, 8, 2, 32, 0, 3, "gqa", 0, vocab=300,
+                                 moe=P.model.MoESpec(8, 2, 128, 0))
+        with pytest.raises(ValueError, match="FP8 weights"):
+            P.HelixDecoder(spec, batch=1, capacity=64, layers=1, vocab=300, w_dtype="fp8")
+    elif what == "batch":
+        spec = P.model.ModelSpec("w8", 1, 256, 8, 2, 32, 256, 3, "gqa", 0, vocab=300)
+        with pytest.raises(ValueError, match="batch <= 16"):
+            P.HelixDecoder(spec, batch=32, capacity=64, layers=1, vocab=300, w_dtype="fp8")
+    else:
+        spec = P.model.ModelSpec("w8", 1, 256, 8, 2, 32, 256, 3, "gqa", 0, vocab=300)
+        g = P.HelixDecoder(spec, batch=1, capacity=64, layers=1, vocab=300, w_dtype="fp8")
+        with pytest.raises(Exception, match="hash"):
+            g.init_weights(1)
+        g.close()
