@@ -439,6 +439,8 @@ void Engine::plan_gemvs() {
     p.tc = tc_ ? 1 : 0;
     p.w8 = w8_ ? 1 : 0;  // wscale is wired by the weight init
     p.xf16 = xf16_();
+    p.prefetch_stages = 4;  // weight stages before griddepcontrol.wait; HX_GEMV_PREFETCH: A/B experiments
+    if (const char* e = std::getenv("HX_GEMV_PREFETCH")) p.prefetch_stages = std::atoi(e);
     g.xmode = norm;
     g.emode = em;
     ypart_elems_ = std::max(ypart_elems_, static_cast<size_t>(groups) * ksplit * B_ * Npad);

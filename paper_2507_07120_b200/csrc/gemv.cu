@@ -58,6 +58,11 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+__device__ __forceinline__ void cp_async4(float* smem_dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(smem_dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long logit_key(float v, int n) {
   unsigned u = __float_as_uint(v);
   u = (u & 0x80000000u) ? ~u : (u | 0x80000000u);
@@ -103,6 +108,21 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemv_kernel(const GemvParams
     if (lane == 0) {
       int st = 0;
       bool waited = false;  // x fragments come from the previous kernel; weights are constant
+      // Before griddepcontrol.wait the producer fills the WHOLE ring with weights
+      // (the x copies of those stages are deferred until the previous kernel has
+      // completed): with PDL this CTA streams ~kStages stages of weights while the
+      // previous GEMV's epilogue still runs.
+      const uint8_t* pend_src[kStages];
+      uint32_t pend_bytes[kStages];
+      int pend_stage[kStages];
+      int npend = 0;
+      auto flush_x = [&]() {
+        griddep_wait();
+        waited = true;
+        for (int i = 0; i < npend; ++i)
+          bulk_g2s(ring + pend_stage[i] * SB + SW, pend_src[i], pend_bytes[i], &full[pend_stage[i]]);
+        npend = 0;
+      };
       int n_tiles = p.n_tiles;
       if (p.group_count) {  // the active-expert list is produced by the routing kernel
         griddep_wait();
@@ -130,8 +150,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemv_kernel(const GemvParams
           if (st >= kStages) mbar_wait(&empty[s], ((st / kStages) & 1) ^ 1);
           TileMeta& m = meta[s];
           if (done) {
-            if (!waited) griddep_wait();
-            waited = true;
+            if (!waited) flush_x();
             m.tile = kDone;
             mbar_arrive(&full[s]);
             break;
@@ -148,12 +167,16 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemv_kernel(const GemvParams
           uint8_t* dst = ring + s * SB;
           mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(n) * (WB + kXfTerms * NB8 * 256u));
           bulk_g2s(dst, wg + (static_cast<size_t>(nb) * KST + a) * WB, static_cast<uint32_t>(n) * WB, &full[s]);
-          if (!waited) {
-            griddep_wait();
-            waited = true;
+          const uint8_t* xsrc = xg + static_cast<size_t>(a) * kXfTerms * NB8 * 256;
+          const uint32_t xbytes = static_cast<uint32_t>(n) * kXfTerms * NB8 * 256u;
+          if (waited) {
+            bulk_g2s(dst + SW, xsrc, xbytes, &full[s]);
+          } else {  // st < kStages here: no empty-slot wait can precede the flush
+            pend_src[npend] = xsrc;
+            pend_bytes[npend] = xbytes;
+            pend_stage[npend] = s;
+            if (++npend == min(max(p.prefetch_stages, 1), kStages)) flush_x();
           }
-          bulk_g2s(dst + SW, xg + static_cast<size_t>(a) * kXfTerms * NB8 * 256,
-                   static_cast<uint32_t>(n) * kXfTerms * NB8 * 256u, &full[s]);
         }
         if (done) break;
       }
@@ -249,6 +272,7 @@ template <int NB8, int EM, bool NORM>
 __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p) {
   // One thread per (row, request) element of a 128-row block; every global load
   // an element needs (its split partials, the old residual) is issued before use.
+  extern __shared__ float stage[];  // [NP * 16][blockDim] split partials in flight
   __shared__ float s_inv[64];
   __shared__ float vt[64][kRows];
   __shared__ unsigned long long s_best[64];
@@ -299,20 +323,31 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
     for (int gq = 0; gq < ngrp; ++gq) {
       const int gsl = combine ? gq : gi_epi;
       float yg[NP] = {0.f, 0.f};
+      // The split partials are staged through shared memory with cp.async: ptxas
+      // interleaved register loads with the adds that consume them (one L2 round
+      // trip per split; ncu: ~10 us for the O-proj epilogue's 16 splits), while
+      // cp.async has no destination register, so all of a thread's copies are in
+      // flight together. Slot (q, j) of thread t: stage[(q * 16 + j) * blockDim + t].
+      float* st = stage + threadIdx.x;
       for (int s0 = 0; s0 < p.ksplit; s0 += 16) {
-        float v[NP][16];
+        const int nj = min(16, p.ksplit - s0);
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
+          if (q >= np) continue;
           const float* base = p.ypart + static_cast<size_t>(gsl) * p.part_group_stride +
                               static_cast<size_t>(b) * p.Npad + nb * kRows + r + q * (kRows / 2);
 #pragma unroll
           for (int j = 0; j < 16; ++j)
-            v[q][j] = (q < np && s0 + j < p.ksplit) ? __ldcg(base + (s0 + j) * stride) : 0.f;
+            if (j < nj) cp_async4(st + (q * 16 + j) * blockDim.x, base + (s0 + j) * stride);
         }
+        cp_async_wait_all();
 #pragma unroll
-        for (int q = 0; q < NP; ++q)
+        for (int q = 0; q < NP; ++q) {
+          if (q >= np) continue;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) yg[q] += v[q][j];  // split order: deterministic
+          for (int j = 0; j < 16; ++j)
+            if (j < nj) yg[q] += st[(q * 16 + j) * blockDim.x];  // split order: deterministic
+        }
       }
       if (combine) {  // MoE combine in ascending expert order (deterministic)
         const float w = p.route_w[static_cast<size_t>(b) * p.n_experts + p.group_ids[gq]];
@@ -440,7 +475,16 @@ static cudaError_t launch_t(const GemvParams& p, int grid, cudaStream_t stream) 
   const int per = p.batch > 8 ? 8 : p.batch;
   const int threads = std::min(1024, (rows_here * per + 31) / 32 * 32);
   const int gy = (p.group_count && EM == E_SWIGLU) ? p.n_groups_max : 1;
-  return launch_k(gemv_epilogue_kernel<NB8, EM, NORM>, dim3(p.Npad / kRows, gy, gz), dim3(threads), 0, stream, p);
+  const size_t epi_smem = static_cast<size_t>(EM == E_SWIGLU ? 2 : 1) * 16 * threads * sizeof(float);
+  static size_t epi_configured = 0;
+  if (epi_smem > epi_configured) {
+    e = cudaFuncSetAttribute(gemv_epilogue_kernel<NB8, EM, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(epi_smem));
+    if (e != cudaSuccess) return e;
+    epi_configured = epi_smem;
+  }
+  return launch_k(gemv_epilogue_kernel<NB8, EM, NORM>, dim3(p.Npad / kRows, gy, gz), dim3(threads), epi_smem,
+                  stream, p);
 }
 
 template <int NB8>

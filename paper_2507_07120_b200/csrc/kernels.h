@@ -134,6 +134,7 @@ struct GemvParams {
   const float* route_w;      // [B][n_experts] routing weights: the epilogue combines groups
   int n_experts;
   const float* addend;       // optional [B][out_stride] added by E_RESID / E_STORE
+  int prefetch_stages;       // weight stages streamed before griddepcontrol.wait (<= ring depth)
   // FP8 weights (B <= 16, ungrouped): w holds e4m3 bytes in the same tile order
   // ([Npad/128][K/16][8][32 lanes][8 B]), wscale the per-output power-of-two scales
   int w8;
