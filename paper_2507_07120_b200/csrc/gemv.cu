@@ -284,6 +284,28 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
   // batches above 8: one grid layer per 8 requests (more CTAs in flight; every
   // per-request reduction below stays inside its layer)
   const int bz0 = static_cast<int>(blockIdx.z) * 8, bz1 = min(p.batch, bz0 + (gridDim.z > 1 ? 8 : p.batch));
+  const int rows_here = EM == E_SWIGLU ? kRows / 2 : kRows;
+  const size_t stride = static_cast<size_t>(p.batch) * p.Npad;
+  constexpr int NP = 2;  // partial streams per element (SwiGLU: gate + up)
+  const int np = EM == E_SWIGLU ? 2 : 1;
+  // grouped SwiGLU: one grid row per active expert slot
+  const int gi_epi = (p.group_count && EM == E_SWIGLU) ? static_cast<int>(blockIdx.y) : 0;
+  const bool combine = p.group_count && EM != E_SWIGLU;  // MoE combine (possibly of zero experts)
+  // One element per thread and one staging batch: issue the split copies FIRST,
+  // so their L2 round trip overlaps the RMSNorm / append-position loads below.
+  const bool pre = !combine && p.ksplit > 4 && p.ksplit <= 16 && rows_here * (bz1 - bz0) <= static_cast<int>(blockDim.x);
+  if (pre && static_cast<int>(threadIdx.x) < rows_here * (bz1 - bz0)) {
+    const int r = threadIdx.x % rows_here, b = bz0 + threadIdx.x / rows_here;
+#pragma unroll
+    for (int q = 0; q < NP; ++q) {
+      if (q >= np) continue;
+      const float* base = p.ypart + static_cast<size_t>(gi_epi) * p.part_group_stride +
+                          static_cast<size_t>(b) * p.Npad + nb * kRows + r + q * (kRows / 2);
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < p.ksplit) cp_async4(stage + threadIdx.x + (q * 16 + j) * blockDim.x, base + j * stride);
+    }
+  }
   if (NORM) {
     for (int b = bz0 + warp; b < bz1; b += nwarps) {
       float ss = 0.f;
@@ -303,18 +325,14 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
   if (EM == E_STORE || EM == E_RESID)
     for (int i = threadIdx.x; i < 64 * kRows; i += blockDim.x) vt[i / kRows][i % kRows] = 0.f;
   __syncthreads();
-  const int rows_here = EM == E_SWIGLU ? kRows / 2 : kRows;
-  const size_t stride = static_cast<size_t>(p.batch) * p.Npad;
-  constexpr int NP = 2;  // partial streams per element (SwiGLU: gate + up)
-  // grouped SwiGLU: one grid row per active expert slot
-  const int gi_epi = (p.group_count && EM == E_SWIGLU) ? static_cast<int>(blockIdx.y) : 0;
-  if (p.group_count && EM == E_SWIGLU && gi_epi >= *p.group_count) return;
-  const bool combine = p.group_count && EM != E_SWIGLU;  // MoE combine (possibly of zero experts)
+  if (p.group_count && EM == E_SWIGLU && gi_epi >= *p.group_count) {
+    cp_async_wait_all();  // no copies left in flight into this CTA's shared memory
+    return;
+  }
   const int n_comb = combine ? *p.group_count : 0;
   uint8_t* xf_out = p.xf_out + static_cast<size_t>(gi_epi) * p.xf_out_group_stride;
   for (int e = threadIdx.x; e < rows_here * (bz1 - bz0); e += blockDim.x) {
     const int r = e % rows_here, b = bz0 + e / rows_here;
-    const int np = EM == E_SWIGLU ? 2 : 1;
     float y[NP] = {0.f, 0.f};
     float old = 0.f;
     const int n = nb * kRows + r;
@@ -329,7 +347,31 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
       // cp.async has no destination register, so all of a thread's copies are in
       // flight together. Slot (q, j) of thread t: stage[(q * 16 + j) * blockDim + t].
       float* st = stage + threadIdx.x;
-      for (int s0 = 0; s0 < p.ksplit; s0 += 16) {
+      if (p.ksplit <= 4) {  // a few splits: direct loads (no staging round trip)
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          if (q >= np) continue;
+          const float* base = p.ypart + static_cast<size_t>(gsl) * p.part_group_stride +
+                              static_cast<size_t>(b) * p.Npad + nb * kRows + r + q * (kRows / 2);
+          float v[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) v[j] = j < p.ksplit ? __ldcg(base + j * stride) : 0.f;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (j < p.ksplit) yg[q] += v[j];  // split order: deterministic
+        }
+      }
+      if (pre) {  // copies issued at kernel entry
+        cp_async_wait_all();
+#pragma unroll
+        for (int q = 0; q < NP; ++q) {
+          if (q >= np) continue;
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (j < p.ksplit) yg[q] += st[(q * 16 + j) * blockDim.x];  // split order: deterministic
+        }
+      }
+      for (int s0 = 0; !pre && p.ksplit > 4 && s0 < p.ksplit; s0 += 16) {
         const int nj = min(16, p.ksplit - s0);
 #pragma unroll
         for (int q = 0; q < NP; ++q) {
@@ -475,7 +517,7 @@ static cudaError_t launch_t(const GemvParams& p, int grid, cudaStream_t stream) 
   const int per = p.batch > 8 ? 8 : p.batch;
   const int threads = std::min(1024, (rows_here * per + 31) / 32 * 32);
   const int gy = (p.group_count && EM == E_SWIGLU) ? p.n_groups_max : 1;
-  const size_t epi_smem = static_cast<size_t>(EM == E_SWIGLU ? 2 : 1) * 16 * threads * sizeof(float);
+  const size_t epi_smem = p.ksplit <= 4 ? 0 : static_cast<size_t>(EM == E_SWIGLU ? 2 : 1) * 16 * threads * sizeof(float);
   static size_t epi_configured = 0;
   if (epi_smem > epi_configured) {
     e = cudaFuncSetAttribute(gemv_epilogue_kernel<NB8, EM, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
