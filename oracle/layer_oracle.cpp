@@ -26,14 +26,18 @@ double fp8_pow2_scale(double absmax) {
   return std::ldexp(1.0, f == 0.5 ? e - 1 : e);     // smallest 2^j >= absmax / 448
 }
 
+void quantize_fp8_cols(Mat& m) {
+  for (i64 c = 0; c < m.cols; ++c) {
+    double mx = 0.0;
+    for (i64 r = 0; r < m.rows; ++r) mx = std::max(mx, std::fabs(m(r, c)));
+    const double s = fp8_pow2_scale(mx);
+    for (i64 r = 0; r < m.rows; ++r) m(r, c) = round_e4m3(m(r, c) / s) * s;
+  }
+}
+
 Mat hash_matrix_fp8(std::uint64_t seed, HashKind kind, i64 layer, i64 rows, i64 cols, double scale) {
   Mat m = hash_matrix(seed, kind, layer, rows, cols, scale, false);
-  for (i64 c = 0; c < cols; ++c) {
-    double mx = 0.0;
-    for (i64 r = 0; r < rows; ++r) mx = std::max(mx, std::fabs(m(r, c)));
-    const double s = fp8_pow2_scale(mx);
-    for (i64 r = 0; r < rows; ++r) m(r, c) = round_e4m3(m(r, c) / s) * s;
-  }
+  quantize_fp8_cols(m);
   return m;
 }
 
@@ -72,8 +76,8 @@ ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, st
   const i64 W = mla ? mla_width(d.kv_latent) : 0, DV = mla ? mla_value_width(d.kv_latent) : 0;
   const double sh = 1.0 / std::sqrt(static_cast<double>(d.hidden));
   const double sf = 1.0 / std::sqrt(static_cast<double>(std::max<i64>(d.ffn, 1)));
-  if (d.w_fp8 && (mla || d.n_experts > 0 || qkv_init != QkvInit::Hash))
-    throw std::invalid_argument("FP8 weights: dense GQA models with hash-initialised weights");
+  if (d.w_fp8 && qkv_init != QkvInit::Hash)
+    throw std::invalid_argument("FP8 weights: hash-initialised weights");
   auto wmat = [&](HashKind kind, i64 l, i64 rows, i64 cols, double sc) {
     return d.w_fp8 ? hash_matrix_fp8(seed, kind, l, rows, cols, sc) : hash_matrix(seed, kind, l, rows, cols, sc, bf16);
   };
@@ -81,10 +85,12 @@ ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, st
   for (i64 l = 0; l < d.layers; ++l) {
     if (mla) {
       for (i64 b = 0; b < batch; ++b) mla_.emplace_back(kvp, 1, W, chunk);
-      wq_mla_.push_back(hash_matrix(seed, kWq, l, d.hidden, d.query_heads * d.head_size, sh, bf16));
+      // W_q and the latent down-projection are GEMV weights (FP8 under w_fp8);
+      // the per-head absorptions W_UK / W_UV stay bf16
+      wq_mla_.push_back(wmat(kWq, l, d.hidden, d.query_heads * d.head_size, sh));
       wuk_.push_back(hash_matrix(seed, kWuk, l, d.query_heads * d.head_size, W,
                                  16.0 / std::sqrt(static_cast<double>(d.head_size)), bf16));
-      wdkv_.push_back(hash_matrix(seed, kWk, l, d.hidden, W, sh, bf16));
+      wdkv_.push_back(wmat(kWk, l, d.hidden, W, sh));
       wuv_.push_back(hash_matrix(seed, kWuv, l, d.query_heads * DV, d.head_size,
                                  1.0 / std::sqrt(static_cast<double>(DV)), bf16));
     }
@@ -107,7 +113,7 @@ ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, st
       wd_.emplace_back();
     }
     if (d.n_experts > 0) {
-      wr_.push_back(hash_matrix(seed, kWrouter, l, d.hidden, d.n_experts, sh, bf16));
+      wr_.push_back(wmat(kWrouter, l, d.hidden, d.n_experts, sh));
       const double se = 1.0 / std::sqrt(static_cast<double>(d.expert_ffn));
       eg_.emplace_back();
       eu_.emplace_back();
@@ -119,8 +125,9 @@ ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, st
           for (i64 r = 0; r < rows; ++r)
             for (i64 c = 0; c < cols; ++c) {
               const double v = hash_unit(seed, st, static_cast<std::uint64_t>(r * cols + c)) * sc;
-              m(r, c) = bf16 ? round_bf16(v) : v;
+              m(r, c) = (bf16 && !d.w_fp8) ? round_bf16(v) : v;
             }
+          if (d.w_fp8) quantize_fp8_cols(m);
           return m;
         };
         eg_.back().push_back(em(kEgate, d.hidden, d.expert_ffn, sh));

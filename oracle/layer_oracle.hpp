@@ -63,10 +63,10 @@ struct ModelDims {
   i64 hidden, query_heads, kv_heads, head_size, ffn, layers, vocab;
   i64 n_experts = 0, top_k = 0, expert_ffn = 0;  // n_experts == 0: dense FFN of width `ffn`
   i64 kv_latent = 0;  // > 0: MLA attention (types.hpp:37-49), latent width W = 2 * kv_latent
-  // FP8 weights (dense GQA models, hash init): every GEMV
+  // FP8 weights (hash init): every GEMV
   // weight W[k][n] (input k, output n) is stored as e4m3(W / s_n) * s_n with a
   // power-of-two per-output scale s_n = 2^ceil(log2(max_k |W[k][n]| / 448));
-  // the embedding stays bf16 (a gather, not a GEMV).
+  // the embedding (a gather) and the MLA per-head absorptions W_UK / W_UV stay bf16.
   bool w_fp8 = false;
 };
 
@@ -156,6 +156,7 @@ Mat hash_matrix(std::uint64_t seed, HashKind kind, i64 layer, i64 rows, i64 cols
 // power-of-two scale (ModelDims::w_fp8).
 Mat hash_matrix_fp8(std::uint64_t seed, HashKind kind, i64 layer, i64 rows, i64 cols, double scale);
 double fp8_pow2_scale(double absmax);
+void quantize_fp8_cols(Mat& m);  // per column: e4m3(m / s_c) * s_c
 std::vector<double> rmsnorm(const std::vector<double>& x, double eps = 1e-5);
 
 }  // namespace helix_oracle

@@ -218,6 +218,21 @@ int oracle_model_create_w8(i64 hidden, i64 q, i64 k, i64 hsz, i64 ffn, i64 layer
   });
 }
 
+// Any model (MoE and/or MLA as oracle_model_create_ex) with FP8 GEMV weights.
+int oracle_model_create_ex_w8(i64 hidden, i64 q, i64 k, i64 hsz, i64 ffn, i64 layers, i64 vocab, i64 n_experts,
+                              i64 top_k, i64 expert_ffn, i64 kv_latent, i64 tpa, i64 kvp, i64 chunk, i64 batch,
+                              std::uint64_t seed, void** out) {
+  return guard([&] {
+    ModelDims d{hidden, q, k, hsz, ffn, layers, vocab};
+    d.n_experts = n_experts;
+    d.top_k = top_k;
+    d.expert_ffn = expert_ffn;
+    d.kv_latent = kv_latent;
+    d.w_fp8 = true;
+    *out = new ModelOracle(d, tpa, kvp, chunk, batch, seed, QkvInit::Hash, true);
+  });
+}
+
 // MoE model: ffn = shared-expert width (0: none), n_experts / top_k / expert_ffn routed.
 int oracle_model_create_moe(i64 hidden, i64 q, i64 k, i64 hsz, i64 shared_ffn, i64 layers, i64 vocab,
                             i64 n_experts, i64 top_k, i64 expert_ffn, i64 tpa, i64 kvp, i64 chunk, i64 batch,

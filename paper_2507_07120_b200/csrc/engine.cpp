@@ -132,8 +132,6 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
   if (kv8_ && mla_) throw std::invalid_argument("FP8 KV pages are implemented for GQA caches (MLA latents stay bf16)");
   if (rt.w_dtype != HX_W_BF16 && rt.w_dtype != HX_W_FP8_E4M3) throw std::invalid_argument("unknown w_dtype");
   w8_ = rt.w_dtype == HX_W_FP8_E4M3;
-  if (w8_ && (mla_ || m.n_experts > 0))
-    throw std::invalid_argument("FP8 weights are implemented for dense GQA models");
   if (w8_ && B_ > 16) throw std::invalid_argument("FP8 weights run the mma.sync GEMV: batch <= 16");
   if (mla_) {
     // types.hpp:43-49: MLA keeps one latent KV head; Helix needs tpa <= K_eff = 1 (types.cpp:122-139)
@@ -500,7 +498,7 @@ void Engine::plan_gemvs() {
         p.tiles_per_group = p.n_tiles;
         p.n_groups_max = G;
         p.group_base = e_begin_;
-        p.w_group_stride = static_cast<long long>(p.Npad) * p.K * 2;
+        p.w_group_stride = static_cast<long long>(p.Npad) * p.K * (w8_ ? 1 : 2);
         p.part_group_stride = static_cast<long long>(p.ksplit) * B_ * p.Npad;
         p.n_experts = E;
       }
@@ -560,16 +558,22 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
   const int F = F_local_, f0 = dist ? rank_ * F_local_ : 0;
   const int v0 = dist ? rank_ * V_local_ : 0;
   const int vrows = static_cast<int>(std::min<int64_t>(V_local_, V_ - v0));
+  const size_t wdiv = w8_ ? 16 : 8;  // weight elements per uint4
   auto walloc = [&](const GemvPlan& g) {
     return dalloc<uint4>(static_cast<size_t>(g.p.Npad) * g.p.K / (w8_ ? 16 : 8), "weights");
   };
   // k_full: the input width of the whole (unsharded) matrix -- FP8 scales span it
-  auto init = [&](uint4* w, GemvPlan& g, const std::vector<WSeg>& segs, int k_full) {
+  // (grouped expert blocks pass their slice of one [E_local][Npad] scale array)
+  auto init = [&](uint4* w, GemvPlan& g, const std::vector<WSeg>& segs, int k_full, float* sc_slice = nullptr) {
     cuda_check(cudaMemcpyAsync(d_segs_, segs.data(), segs.size() * sizeof(WSeg), cudaMemcpyHostToDevice,
                                stream_), "segs");
     if (w8_) {
-      float*& sc = wscale_[w];
-      if (!sc) sc = dalloc<float>(static_cast<size_t>(g.p.Npad), "weight scales");
+      float* sc = sc_slice;
+      if (!sc) {
+        float*& slot = wscale_[w];
+        if (!slot) slot = dalloc<float>(static_cast<size_t>(g.p.Npad), "weight scales");
+        sc = slot;
+      }
       cuda_check(launch_weight_init_hash_w8(reinterpret_cast<uint8_t*>(w), sc, g.p.Npad, g.p.K, k_full, d_segs_,
                                             static_cast<int>(segs.size()), seed, stream_), "weight init");
       g.p.wscale = sc;
@@ -638,23 +642,33 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
       GemvPlan& dn = plan_edown_[l];
       if (w_router_.size() <= static_cast<size_t>(l)) {
         w_router_.push_back(walloc(r));
-        w_egu_.push_back(dalloc<uint4>(static_cast<size_t>(E_local_) * gu.p.Npad * gu.p.K / 8, "expert gate/up"));
-        w_edown_.push_back(dalloc<uint4>(static_cast<size_t>(E_local_) * dn.p.Npad * dn.p.K / 8, "expert down"));
+        w_egu_.push_back(dalloc<uint4>(static_cast<size_t>(E_local_) * gu.p.Npad * gu.p.K / wdiv, "expert gate/up"));
+        w_edown_.push_back(dalloc<uint4>(static_cast<size_t>(E_local_) * dn.p.Npad * dn.p.K / wdiv, "expert down"));
+        if (w8_) {
+          wscale_[w_egu_.back()] = dalloc<float>(static_cast<size_t>(E_local_) * gu.p.Npad, "expert scales");
+          wscale_[w_edown_.back()] = dalloc<float>(static_cast<size_t>(E_local_) * dn.p.Npad, "expert scales");
+        }
       }
       const int E = static_cast<int>(E_), Fe = Fe_local_, fe0 = tpf_rank_ * Fe_local_;
       const double se = 1.0 / std::sqrt(static_cast<double>(Fe_));
       init(w_router_[l], r, {{hash_stream(kWrouter, l), 0, E, E, 0, 0, sh, 0, 0}}, Hh);
       for (int el = 0; el < E_local_; ++el) {
         const int64_t e = e_begin_ + el;
-        init(w_egu_[l] + static_cast<size_t>(el) * gu.p.Npad * gu.p.K / 8, gu,
+        init(w_egu_[l] + static_cast<size_t>(el) * gu.p.Npad * gu.p.K / wdiv, gu,
              {{expert_stream(kEgate, l, e), 0, gu.p.Npad, static_cast<int>(Fe_), fe0, 1, sh, 0, fe0 + Fe},
-              {expert_stream(kEup, l, e), 0, gu.p.Npad, static_cast<int>(Fe_), fe0, 2, sh, 0, fe0 + Fe}}, Hh);
-        init(w_edown_[l] + static_cast<size_t>(el) * dn.p.Npad * dn.p.K / 8, dn,
-             {{expert_stream(kEdown, l, e), 0, Hh, Hh, 0, 0, se, fe0, 0}}, static_cast<int>(Fe_));
+              {expert_stream(kEup, l, e), 0, gu.p.Npad, static_cast<int>(Fe_), fe0, 2, sh, 0, fe0 + Fe}}, Hh,
+             w8_ ? wscale_[w_egu_[l]] + static_cast<size_t>(el) * gu.p.Npad : nullptr);
+        init(w_edown_[l] + static_cast<size_t>(el) * dn.p.Npad * dn.p.K / wdiv, dn,
+             {{expert_stream(kEdown, l, e), 0, Hh, Hh, 0, 0, se, fe0, 0}}, static_cast<int>(Fe_),
+             w8_ ? wscale_[w_edown_[l]] + static_cast<size_t>(el) * dn.p.Npad : nullptr);
       }
       r.p.w = w_router_[l];
       gu.p.w = w_egu_[l];
       dn.p.w = w_edown_[l];
+      if (w8_) {  // every expert's scales (indexed by expert id - group_base in the epilogue)
+        gu.p.wscale = wscale_[w_egu_[l]];
+        dn.p.wscale = wscale_[w_edown_[l]];
+      }
     }
   }
   if (!attn_only_) {
@@ -1194,7 +1208,7 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
                                           mla_ ? d_att_ : nullptr, xf16_()),
                  "merge");
       if (mla_)
-        cuda_check(launch_mla_uv(d_att_, w_uv_[l], B_, uv_heads_, static_cast<int>(D_), d_xf_attn_, stream_),
+        cuda_check(launch_mla_uv(d_att_, w_uv_[l], B_, uv_heads_, static_cast<int>(D_), d_xf_attn_, stream_, xf16_()),
                    "mla uv");
       cuda_check(launch_gemv(plan_o_[l].p, 0, E_RESID, num_sms_, stream_), "o-proj");
       mark(4);
@@ -1206,7 +1220,7 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
                                          d_total_ + l * B_, stream_, mla_ ? d_att_ : nullptr, xf16_()),
                  "merge");
       if (mla_)
-        cuda_check(launch_mla_uv(d_att_, w_uv_[l], B_, uv_heads_, static_cast<int>(D_), d_xf_attn_, stream_),
+        cuda_check(launch_mla_uv(d_att_, w_uv_[l], B_, uv_heads_, static_cast<int>(D_), d_xf_attn_, stream_, xf16_()),
                    "mla uv");
       cuda_check(launch_gemv(plan_o_[l].p, 0, E_STORE, num_sms_, stream_), "o-proj");
       mark(4);

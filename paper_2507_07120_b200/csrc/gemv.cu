@@ -391,6 +391,11 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
             if (j < nj) yg[q] += st[(q * 16 + j) * blockDim.x];  // split order: deterministic
         }
       }
+      if (p.wscale) {  // FP8 weights: this weight block's per-output power-of-two scale (exact)
+        const float* ws = p.wscale + (p.group_count ? static_cast<size_t>(p.group_ids[gsl] - p.group_base) * p.Npad : 0);
+        yg[0] *= ws[nb * kRows + r];
+        if (EM == E_SWIGLU) yg[1] *= ws[nb * kRows + r + kRows / 2];
+      }
       if (combine) {  // MoE combine in ascending expert order (deterministic)
         const float w = p.route_w[static_cast<size_t>(b) * p.n_experts + p.group_ids[gq]];
         y[0] += w * yg[0];
@@ -398,10 +403,6 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
         y[0] = yg[0];
         y[1] = yg[1];
       }
-    }
-    if (p.wscale) {  // FP8 weights: per-output power-of-two scale (exact)
-      y[0] *= p.wscale[nb * kRows + r];
-      if (EM == E_SWIGLU) y[1] *= p.wscale[nb * kRows + r + kRows / 2];
     }
     if (NORM) {
       y[0] *= s_inv[b];
@@ -539,6 +540,7 @@ static cudaError_t dispatch_nb(const GemvParams& p, int norm, int em, int grid, 
       HX_CASE8(E_QKV, false)
       HX_CASE8(E_RESID, false)
       HX_CASE8(E_STORE, false)
+      HX_CASE8(E_STORE, true)  // MoE router (f16 terms: 22 bits, like 3 bf16 terms' ~24)
       HX_CASE8(E_SWIGLU, true)
       HX_CASE8(E_LOGITS, true)
 #undef HX_CASE8
@@ -563,7 +565,7 @@ static cudaError_t dispatch_nb(const GemvParams& p, int norm, int em, int grid, 
 cudaError_t launch_gemv(const GemvParams& p, int norm, int emode, int grid, cudaStream_t stream) {
   if (p.batch < 1 || p.batch > 64 || (p.K & 15) || (p.Npad % kRows)) return cudaErrorInvalidValue;
   if (p.tc && p.batch <= 16) return cudaErrorInvalidValue;  // tcgen05 path: N = 32 or 64 batch rows
-  if (p.w8 && (p.tc || p.batch > 16 || !p.wscale || p.group_count)) return cudaErrorInvalidValue;
+  if (p.w8 && (p.tc || p.batch > 16 || !p.wscale)) return cudaErrorInvalidValue;
   if (p.batch <= 8) return dispatch_nb<1>(p, norm, emode, grid, stream);
   if (p.batch <= 16) return dispatch_nb<2>(p, norm, emode, grid, stream);
   if (p.batch <= 32) return dispatch_nb<4>(p, norm, emode, grid, stream);

@@ -73,7 +73,7 @@ cudaError_t launch_mla_split_reduce(const AttnParams& p, float* frag_o, float* f
 cudaError_t launch_mla_absorb_q(const float* n, const uint16_t* wuk, int batch, int q_heads, int hs, int dp,
                                 uint8_t* qimg, cudaStream_t stream);
 cudaError_t launch_mla_uv(const float* att, const uint16_t* wuv, int batch, int n_heads, int hs, uint8_t* xf,
-                          cudaStream_t stream);
+                          cudaStream_t stream, int xf16 = 0);
 cudaError_t launch_kv_fill_hash_mla(uint8_t* kv, int* total, int batch, int kvp, int chunk, int page_cap,
                                     int slot_base, int n_local_slots, long long n, uint64_t seed, uint64_t stream_k,
                                     cudaStream_t stream);

@@ -717,7 +717,7 @@ cudaError_t launch_kv_fill_hash_mla(uint8_t* kv, int* total, int batch, int kvp,
 template <bool ABSORB, int DS>
 __global__ void __launch_bounds__(512) mla_head_gemm_kernel(const float* in, int in_head_stride, int in_row_stride,
                                                              const __nv_bfloat16* w, int din, int dout, int batch,
-                                                             uint8_t* out) {
+                                                             uint8_t* out, int xf16) {
   constexpr int NB = 8;
   extern __shared__ __align__(16) float hsm[];
   float* s_in = hsm;                    // [din][NB]
@@ -803,7 +803,7 @@ __global__ void __launch_bounds__(512) mla_head_gemm_kernel(const float* in, int
         *reinterpret_cast<__nv_bfloat16*>(out + static_cast<size_t>(bc + b) * mla_q_bytes() + mla_q_offset(h, jj)) =
             __float2bfloat16_rn(v);
       else
-        xf_write(out, xf_nb8(batch), bc + b, h * dout + jj, v);
+        xf_write(out, xf_nb8(batch), bc + b, h * dout + jj, v, xf16);
     }
     __syncthreads();
   }
@@ -812,7 +812,7 @@ __global__ void __launch_bounds__(512) mla_head_gemm_kernel(const float* in, int
 template <bool ABSORB, int DS>
 static cudaError_t launch_head_gemm_t(const float* in, int in_head_stride, int in_row_stride, const uint16_t* w,
                                       int din, int dout, int batch, int heads, int col_chunks, uint8_t* out,
-                                      cudaStream_t stream) {
+                                      cudaStream_t stream, int xf16 = 0) {
   while (col_chunks > 1 && dout % (8 * col_chunks)) --col_chunks;
   const int cols = dout / col_chunks;
   if (cols % 8 || din % DS || (cols / 8) * DS > 512) return cudaErrorInvalidValue;
@@ -827,7 +827,7 @@ static cudaError_t launch_head_gemm_t(const float* in, int in_head_stride, int i
   const int threads = (cols / 8) * DS;
   return launch_k(mla_head_gemm_kernel<ABSORB, DS>, dim3(heads, col_chunks), dim3((threads + 31) / 32 * 32), smem,
                   stream, in,
-                  in_head_stride, in_row_stride, reinterpret_cast<const __nv_bfloat16*>(w), din, dout, batch, out);
+                  in_head_stride, in_row_stride, reinterpret_cast<const __nv_bfloat16*>(w), din, dout, batch, out, xf16);
 }
 
 cudaError_t launch_mla_absorb_q(const float* n, const uint16_t* wuk, int batch, int q_heads, int hs, int dp,
@@ -837,10 +837,10 @@ cudaError_t launch_mla_absorb_q(const float* n, const uint16_t* wuk, int batch, 
 }
 
 cudaError_t launch_mla_uv(const float* att, const uint16_t* wuv, int batch, int n_heads, int hs, uint8_t* xf,
-                          cudaStream_t stream) {
+                          cudaStream_t stream, int xf16) {
   if (hs > 128) return cudaErrorInvalidValue;  // 4 chunks of hs/32 column groups x 32 d-slices of 16
   return launch_head_gemm_t<false, 32>(att, kMlaDV, n_heads * kMlaDV, wuv, kMlaDV, hs, batch, n_heads, 4, xf,
-                                       stream);
+                                       stream, xf16);
 }
 
 }  // namespace hx

@@ -55,6 +55,7 @@ def lib():
             "oracle_model_create_moe": (C.c_int, [i64] * 14 + [u64, C.c_int, C.c_int, C.POINTER(vp)]),
             "oracle_model_create_ex": (C.c_int, [i64] * 15 + [u64, C.c_int, C.c_int, C.POINTER(vp)]),
             "oracle_model_create_w8": (C.c_int, [i64] * 11 + [u64, C.POINTER(vp)]),
+            "oracle_model_create_ex_w8": (C.c_int, [i64] * 15 + [u64, C.POINTER(vp)]),
             "oracle_model_routes": (C.c_int, [vp, ip]),
             "oracle_model_route_gaps": (C.c_int, [vp, dp]),
             "oracle_model_free": (None, [vp]),
@@ -253,8 +254,13 @@ class Model:
         self.batch = batch
         self.moe = moe
         h = C.c_void_p()
-        if w_fp8:
-            assert qkv_hash and not moe and not kv_latent
+        if w_fp8 and (moe or kv_latent):
+            assert qkv_hash
+            m = moe or (0, 0, 0)
+            check(lib().oracle_model_create_ex_w8(hidden, q, k, hsz, ffn, layers, vocab, m[0], m[1], m[2], kv_latent,
+                                                  tpa, kvp, chunk, batch, seed, C.byref(h)))
+        elif w_fp8:
+            assert qkv_hash
             check(lib().oracle_model_create_w8(hidden, q, k, hsz, ffn, layers, vocab, tpa, kvp, chunk, batch, seed,
                                                C.byref(h)))
         elif kv_latent:
