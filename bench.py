@@ -124,7 +124,7 @@ def peak_tensor():
         return 1393.0, "fallback"
 
 
-def pool_slice(a, preset, S, ep):
+def pool_slice(a, preset, S, ep, w_dtype="bf16"):
     """One GPU of an N=8 Helix pool (TPA=1, KVP=8; FFN TPF=8, or EP=8 x TPF=1 for
     MoE) measured alone: rank 0 of an 8-rank loopback pool with the collectives
     switched off (a single B200 here), so the number is this GPU's compute per
@@ -141,7 +141,7 @@ def pool_slice(a, preset, S, ep):
     mla = spec.attention == "mla"
     lb = Loopback(N)
     eng = P.HelixDecoder(spec, tpa=1, kvp=N, batch=B, capacity=S * N + 64 * N, layers=1, vocab=V,
-                         use_graphs=True, pool=2, rank=0, loopback=lb, ep=ep)
+                         use_graphs=True, pool=2, rank=0, loopback=lb, ep=ep, w_dtype=w_dtype)
     # HX_FLAG_SKIP_COMM: no a2a / all-reduce (no peers here) -- the step is then
     # CUDA-graph captured like the headline (and like the NCCL pool)
     P._lib.check(P.lib().hx_engine_set_flag(eng._h, 1, 3), eng._h)
@@ -563,10 +563,13 @@ def ours(a):
             line["kvp_slices"] = kvp_slices(a)
         except Exception as ex:  # reported, never fatal for the headline number
             line["kvp_slices"] = {"error": str(ex)[:300]}
-        for key, preset, ctx, ep in (("llama405b_slice", "llama405b-like", a.slice_context, 1),
-                                     ("deepseek_slice", "deepseek-r1-like", a.slice_context, 8)):
+        for key, preset, ctx, ep, wd in (("llama405b_slice", "llama405b-like", a.slice_context, 1, "bf16"),
+                                         ("deepseek_slice", "deepseek-r1-like", a.slice_context, 8, "bf16"),
+                                         ("llama405b_slice_fp8w", "llama405b-like", a.slice_context, 1, "fp8"),
+                                         ("deepseek_slice_fp8w", "deepseek-r1-like", a.slice_context, 8, "fp8")):
             try:
-                line[key] = pool_slice(a, preset, ctx, ep)
+                line[key] = pool_slice(a, preset, ctx, ep, wd)
+                line[key]["w_dtype"] = wd
             except Exception as ex:  # reported, never fatal for the headline number
                 line[key] = {"error": str(ex)[:300]}
     if rank == 0:
