@@ -316,7 +316,7 @@ def fp8_kv_line(a, w_dtype="bf16"):
             "weight_bytes_resident": info["weight_bytes_per_layer"] * L + info["head_bytes"], "ms_per_step": ms, "value": B / (ms * 1e-3), "unit": UNIT,
             "breakdown_ms": {k: float(v) for k, v in zip(
                 ["embed", "qkv", "attention", "split_reduce", "o_proj", "gate_up", "down", "lm_head", "merge"], prof)},
-            "attention_roofline": {"bound": "hbm", "kernel": "attn_decode_kernel<128,8,4,1,fp8>",
+            "attention_roofline": {"bound": "hbm", "kernel": "attn_decode_kernel<128,10,4,1,fp8>",
                                    "algorithmic_bytes_per_launch": kv_bytes, "launch_ms": att,
                                    "achieved": kv_bytes / (att * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                                    "frac": kv_bytes / (att * 1e-3) / 1e9 / hbm,
