@@ -28,6 +28,7 @@
 // power-of-two scale s_n is applied in the epilogue after the split-K sum
 // (exact: y_n = s_n * sum_k x_k q_kn).
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -44,7 +45,7 @@ constexpr int kStages = 4;        // ring depth (~150 KB in flight per SM)
 // k-steps per ring stage: 32 KB of weights (+ x slice) for B <= 16; fewer
 // k-steps when the x slice grows with the batch (B <= 64) so 4 stages fit.
 template <int NB8, bool W8 = false>
-constexpr int stage_steps() { return W8 ? (NB8 == 1 ? 16 : 8) : (NB8 <= 2 ? 8 : (NB8 <= 4 ? 4 : 2)); }
+constexpr int stage_steps() { return W8 ? (NB8 == 1 ? 8 : 4) : (NB8 <= 2 ? 8 : (NB8 <= 4 ? 4 : 2)); }
 constexpr int kDone = -1;
 
 struct TileMeta {
@@ -70,7 +71,7 @@ __device__ __forceinline__ unsigned long long logit_key(float v, int n) {
 }
 
 __host__ __device__ __forceinline__ int stage_steps_rt(int nb8, bool w8) {
-  return w8 ? (nb8 == 1 ? 16 : 8) : (nb8 <= 2 ? 8 : (nb8 <= 4 ? 4 : 2));
+  return w8 ? (nb8 == 1 ? 8 : 4) : (nb8 <= 2 ? 8 : (nb8 <= 4 ? 4 : 2));
 }
 __host__ __device__ __forceinline__ size_t stage_bytes(int nb8, bool w8) {
   return static_cast<size_t>(stage_steps_rt(nb8, w8)) * ((w8 ? 2048 : 4096) + xf_step_bytes(nb8));
@@ -510,8 +511,12 @@ static cudaError_t launch_t(const GemvParams& p, int grid, cudaStream_t stream) 
     if (e != cudaSuccess) return e;
     configured = smem;
   }
+  // FP8 weights: the consumer's per-k-step chain (e4m3 widening + 2 MMAs) is
+  // latency-bound at 8 warps per SM, so two CTAs per SM (half-size ring stages)
+  static const int w8_ctas = std::getenv("HX_W8_CTAS") ? std::atoi(std::getenv("HX_W8_CTAS")) : 2;
+  const int g = W8 ? grid * w8_ctas : grid;
   cudaError_t e = p.tc ? launch_gemv_tc(p, NB8, XS, grid, stream)
-                       : launch_k(gemv_kernel<NB8, EM, XS, NORM, W8>, dim3(grid), dim3(kThreads + 32), smem, stream, p);
+                       : launch_k(gemv_kernel<NB8, EM, XS, NORM, W8>, dim3(g), dim3(kThreads + 32), smem, stream, p);
   if (e != cudaSuccess) return e;
   const int rows_here = EM == E_SWIGLU ? kRows / 2 : kRows;
   const int gz = p.batch > 8 ? (p.batch + 7) / 8 : 1;  // one grid layer per 8 requests
