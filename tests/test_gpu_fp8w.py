@@ -50,26 +50,28 @@ def test_fp8_weights_decode_step_matches_oracle(q, k, hsz, kvp, B, kv):
     g.close()
 
 
-def test_fp8_weights_loopback_pool():
-    """Distributed layout (TP-sharded O-proj rows / FFN columns / vocabulary): the
-    per-output scales span the FULL input range of each sharded matrix, so every
-    rank's shard carries the oracle's quantisation."""
+@pytest.mark.parametrize("tpa,kvp", [(1, 2), (2, 2)])
+def test_fp8_weights_loopback_pool(tpa, kvp):
+    """Distributed layout (TPA-sharded QKV heads, TP-sharded O-proj rows / FFN
+    columns / vocabulary): the per-output scales span the FULL input range of
+    each sharded matrix, so every rank's shard carries the oracle's quantisation."""
     import paper_2507_07120_b200 as P
     from paper_2507_07120_b200.model import Loopback
-    H, Q, K, D, F, L, V, B, kvp = 512, 16, 2, 32, 512, 2, 400, 2, 2
+    H, Q, K, D, F, L, V, B = 512, 16, 2, 32, 512, 2, 400, 2
+    n = tpa * kvp
     spec = P.model.ModelSpec("w8d", L, H, Q, K, D, F, 3, "gqa", 0, vocab=V)
-    lb = Loopback(kvp)
-    engines = [P.HelixDecoder(spec, tpa=1, kvp=kvp, batch=B, capacity=3000, layers=L, vocab=V, use_graphs=False,
-                              pool=2, rank=r, loopback=lb, w_dtype="fp8") for r in range(kvp)]
+    lb = Loopback(n)
+    engines = [P.HelixDecoder(spec, tpa=tpa, kvp=kvp, batch=B, capacity=3000, layers=L, vocab=V, use_graphs=False,
+                              pool=2, rank=r, loopback=lb, w_dtype="fp8") for r in range(n)]
     for e in engines:
         e.init_weights(3, qkv="hash")
         e.fill_kv_hash(2500, 3)
-    o = O.Model(H, Q, K, D, F, L, V, tpa=1, kvp=kvp, batch=B, seed=3, qkv_hash=True, w_fp8=True)
+    o = O.Model(H, Q, K, D, F, L, V, tpa=tpa, kvp=kvp, batch=B, seed=3, qkv_hash=True, w_fp8=True)
     for l in range(L):
         for b in range(B):
             o.grow_hash(l, b, 2500)
     tokens = np.array([4, 399])
-    res = [None] * kvp
+    res = [None] * n
     errors = []
 
     def run(r):
@@ -77,12 +79,12 @@ def test_fp8_weights_loopback_pool():
             res[r] = engines[r].step(tokens, want_logits=True, want_hidden=True)
         except Exception as ex:  # surfaced below
             errors.append(ex)
-    th = [threading.Thread(target=run, args=(r,), daemon=True) for r in range(kvp)]
+    th = [threading.Thread(target=run, args=(r,), daemon=True) for r in range(n)]
     [t.start() for t in th]
     [t.join(timeout=120) for t in th]
     assert not errors, errors
     lo, ho, no = o.step(tokens)
-    for r in range(kvp):
+    for r in range(n):
         e_h = rel_err(res[r][2], ho)
         print(f"rank {r}: hidden {e_h:.2e}")
         assert e_h <= 2e-3
