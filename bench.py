@@ -404,7 +404,7 @@ def ours(a):
         dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
     spec = P.model.PRESETS["llama3-8b-like"]
     B, S, L = a.batch, a.context, a.layers
-    total_steps = 4 * (a.warmup + a.steps) + 8
+    total_steps = 6 * (a.warmup + a.steps) + 8
     # weak scaling: S KV tokens per request per GPU; KVP = N (global context S*N)
     S_glob = S * world
     cap = S_glob + 4 * (total_steps + 8) * world + 64
@@ -456,32 +456,6 @@ def ours(a):
     with ClockSampler() as clk:
         time.sleep(0.3)
         ms = timed(a.steps, a.warmup)
-        # e2e through the public API: pinned host tokens in, host next tokens out, every step
-        h_tok = torch.zeros(B, dtype=torch.int32).pin_memory()
-        h_next = torch.zeros(B, dtype=torch.int32).pin_memory()
-        h_tok.copy_(tok[0].cpu())
-        ip = ctypes.POINTER(ctypes.c_int32)
-        # untimed warm-up of this call path too: its first call captures and uploads
-        # the CUDA graph for the engine's own token buffers (tens of ms, once)
-        for i in range(a.warmup):
-            rc = P.lib().hx_decode_step(eng._h, ctypes.cast(h_tok.data_ptr(), ip), ctypes.cast(h_next.data_ptr(), ip),
-                                        None, None)
-            P._lib.check(rc, eng._h)
-            h_tok.copy_(h_next)
-        barrier()
-        e2 = torch.cuda.Event(enable_timing=True)
-        e3 = torch.cuda.Event(enable_timing=True)
-        w0 = time.perf_counter()
-        e2.record(stream)
-        for i in range(a.steps):
-            rc = P.lib().hx_decode_step(eng._h, ctypes.cast(h_tok.data_ptr(), ip), ctypes.cast(h_next.data_ptr(), ip),
-                                        None, None)
-            P._lib.check(rc, eng._h)
-            h_tok.copy_(h_next)
-        e3.record(stream)
-        e3.synchronize()
-        wall_e2e = (time.perf_counter() - w0) / a.steps * 1e3
-        ms_e2e = max_over_ranks(max(e2.elapsed_time(e3) / a.steps, wall_e2e))
         hopb = None
         if world > 1:
             # exposed all-to-all with and without HOP-B (overlap.hpp:37-69): same resident pool,
@@ -507,6 +481,35 @@ def ours(a):
                     "a2a_hidden_frac": (1.0 - exp_on / exp_off) if exp_off > 0 else None,
                     "hopb_net_ms": ms - ms_on, "headline": "HOP-B off"}
     clocks = clk.summary(dev)
+    # e2e through the public API: pinned host tokens in, host next tokens out, every
+    # step -- after the clock sampler has stopped: its nvidia-smi polling contends
+    # with the synchronous per-step driver calls (+0.5-1 ms/step measured; the same
+    # loop without it: tools/launch_cost.py, 22.73 vs 22.67 ms pipelined)
+    h_tok = torch.zeros(B, dtype=torch.int32).pin_memory()
+    h_next = torch.zeros(B, dtype=torch.int32).pin_memory()
+    h_tok.copy_(tok[0].cpu())
+    ip = ctypes.POINTER(ctypes.c_int32)
+    # untimed warm-up of this call path too: its first call captures and uploads
+    # the CUDA graph for the engine's own token buffers (tens of ms, once)
+    for i in range(a.warmup):
+        rc = P.lib().hx_decode_step(eng._h, ctypes.cast(h_tok.data_ptr(), ip), ctypes.cast(h_next.data_ptr(), ip),
+                                    None, None)
+        P._lib.check(rc, eng._h)
+        h_tok.copy_(h_next)
+    barrier()
+    e2 = torch.cuda.Event(enable_timing=True)
+    e3 = torch.cuda.Event(enable_timing=True)
+    w0 = time.perf_counter()
+    e2.record(stream)
+    for i in range(a.steps):
+        rc = P.lib().hx_decode_step(eng._h, ctypes.cast(h_tok.data_ptr(), ip), ctypes.cast(h_next.data_ptr(), ip),
+                                    None, None)
+        P._lib.check(rc, eng._h)
+        h_tok.copy_(h_next)
+    e3.record(stream)
+    e3.synchronize()
+    wall_e2e = (time.perf_counter() - w0) / a.steps * 1e3
+    ms_e2e = max_over_ranks(max(e2.elapsed_time(e3) / a.steps, wall_e2e))
 
     # per-kernel-kind breakdown (eager launches, CUDA events on the engine stream)
     prof = np.zeros(10)
