@@ -124,7 +124,7 @@ def peak_tensor():
         return 1393.0, "fallback"
 
 
-def pool_slice(a, preset, S, ep, w_dtype="bf16"):
+def pool_slice(a, preset, S, ep, w_dtype="bf16", kv_dtype="bf16"):
     """One GPU of an N=8 Helix pool (TPA=1, KVP=8; FFN TPF=8, or EP=8 x TPF=1 for
     MoE) measured alone: rank 0 of an 8-rank loopback pool with the collectives
     switched off (a single B200 here), so the number is this GPU's compute per
@@ -141,7 +141,7 @@ def pool_slice(a, preset, S, ep, w_dtype="bf16"):
     mla = spec.attention == "mla"
     lb = Loopback(N)
     eng = P.HelixDecoder(spec, tpa=1, kvp=N, batch=B, capacity=S * N + 64 * N, layers=1, vocab=V,
-                         use_graphs=True, pool=2, rank=0, loopback=lb, ep=ep, w_dtype=w_dtype)
+                         use_graphs=True, pool=2, rank=0, loopback=lb, ep=ep, w_dtype=w_dtype, kv_dtype=kv_dtype)
     # HX_FLAG_SKIP_COMM: no a2a / all-reduce (no peers here) -- the step is then
     # CUDA-graph captured like the headline (and like the NCCL pool)
     P._lib.check(P.lib().hx_engine_set_flag(eng._h, 1, 3), eng._h)
@@ -195,20 +195,22 @@ def pool_slice(a, preset, S, ep, w_dtype="bf16"):
                          "t_roof_ms": max(kv_bytes / hbm / 1e6, flops / tc / 1e9),
                          "traffic": ncu_traffic("mla")}}
         out["moe"] = {"local_experts": spec.moe.total_experts // ep, "active_local_experts_last_step": active,
-                      "expert_bytes_streamed": active * 3 * H * spec.moe.expert_ffn_dim * 2}
+                      "expert_bytes_streamed": active * 3 * H * spec.moe.expert_ffn_dim * (1 if w_dtype == "fp8" else 2)}
     else:
         K = spec.kv_heads
-        kv_bytes = B * 2 * K * Hsz * s_loc * 2
-        # roofline.hpp:17-48 at bf16: QKV duplicated per KVP rank, O and FFN sharded over N
-        w_bytes = H * (Q * Hsz + 2 * K * Hsz) * 2 + (H // N) * H * 2 + 3 * H * spec.ffn_dim // N * 2
+        ekv, ew = (1 if kv_dtype == "fp8" else 2), (1 if w_dtype == "fp8" else 2)
+        kv_bytes = B * 2 * K * Hsz * s_loc * ekv
+        # roofline.hpp:17-48: QKV duplicated per KVP rank, O and FFN sharded over N
+        w_bytes = (H * (Q * Hsz + 2 * K * Hsz) + (H // N) * H + 3 * H * spec.ffn_dim // N) * ew
         out["workload"] = ("llama405b-like layer, one GPU of TPA=1 x KVP=8 (TPF=8): %d KV heads x %d tokens x B=%d; "
                            "QKV replicated, W_O rows and FFN features 1/8; collectives off (1 GPU)" % (K, s_loc, B))
         out["attention"] = {
-            "kernel": "attn_decode_kernel<128,8,2> (TMA bulk-copy page ring, mma.sync)", "launch_ms": att_ms,
+            "kernel": ("attn_decode_kernel<128,8,4,2,fp8>" if kv_dtype == "fp8" else "attn_decode_kernel<128,8,2,2,W16>")
+                      + " (TMA bulk-copy page ring, mma.sync)", "launch_ms": att_ms,
             "algorithmic_kv_bytes": kv_bytes,
             "roofline": {"bound": "hbm", "achieved": kv_bytes / (att_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                          "frac": kv_bytes / (att_ms * 1e-3) / 1e9 / hbm,
-                         "traffic": ncu_traffic("attention_405b_slice")}}
+                         "traffic": None if kv_dtype == "fp8" else ncu_traffic("attention_405b_slice")}}
         out["layer_roofline"] = {"bound": "hbm", "algorithmic_bytes": kv_bytes + w_bytes, "weight_bytes": w_bytes,
                                  "t_roof_ms": (kv_bytes + w_bytes) / hbm / 1e6,
                                  "achieved_gbs": (kv_bytes + w_bytes) / (ms * 1e-3) / 1e9,
@@ -566,13 +568,16 @@ def ours(a):
             line["kvp_slices"] = kvp_slices(a)
         except Exception as ex:  # reported, never fatal for the headline number
             line["kvp_slices"] = {"error": str(ex)[:300]}
-        for key, preset, ctx, ep, wd in (("llama405b_slice", "llama405b-like", a.slice_context, 1, "bf16"),
-                                         ("deepseek_slice", "deepseek-r1-like", a.slice_context, 8, "bf16"),
-                                         ("llama405b_slice_fp8w", "llama405b-like", a.slice_context, 1, "fp8"),
-                                         ("deepseek_slice_fp8w", "deepseek-r1-like", a.slice_context, 8, "fp8")):
+        for key, preset, ctx, ep, wd, kd in (
+                ("llama405b_slice", "llama405b-like", a.slice_context, 1, "bf16", "bf16"),
+                ("deepseek_slice", "deepseek-r1-like", a.slice_context, 8, "bf16", "bf16"),
+                ("llama405b_slice_fp8w", "llama405b-like", a.slice_context, 1, "fp8", "bf16"),
+                ("deepseek_slice_fp8w", "deepseek-r1-like", a.slice_context, 8, "fp8", "bf16"),
+                ("llama405b_slice_fp8", "llama405b-like", a.slice_context, 1, "fp8", "fp8")):
             try:
-                line[key] = pool_slice(a, preset, ctx, ep, wd)
+                line[key] = pool_slice(a, preset, ctx, ep, wd, kd)
                 line[key]["w_dtype"] = wd
+                line[key]["kv_dtype"] = kd
             except Exception as ex:  # reported, never fatal for the headline number
                 line[key] = {"error": str(ex)[:300]}
     if rank == 0:
