@@ -104,7 +104,7 @@ template <int DP, int NWC, int NSTAGE, int QC, bool KV8, bool W16>
 __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const AttnParams p) {
   using Cfg = AttnCfg<DP, KV8>;
   static_assert(NWC % QC == 0, "query chunks must divide the consumer warps");
-  static_assert(!W16 || (QC == 2 && !KV8), "W16: 16 query rows of bf16 pages");
+  static_assert(!W16 || QC == 2, "W16: 16 query rows per warp");
   constexpr int QR = 8 * QC;           // query rows per item
   constexpr int WPC = NWC / QC;        // warps (pages per stage slot) per query chunk
   constexpr int SR = W16 ? 16 : 8;     // query rows per warp
@@ -211,6 +211,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
     }
   } else if constexpr (W16) {
     // ------------------------------------------------------------ consumers, 16 query rows per warp
+    constexpr int kQTerms = KV8 ? 2 : 3;
     const int g = lane >> 2, c = lane & 3;
     float acc[Cfg::ND][4];           // rows g (query g) and g+8 (query g+8)
     float m_ref[2] = {-INFINITY, -INFINITY}, l_sum[2] = {0.f, 0.f};
@@ -223,7 +224,8 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
       if (m.item == kItemDone) break;
       const uint32_t sbase = stage_base + s * STAGE_BYTES;
       if (m.first) {
-        // query fragment image: warp w builds k-steps w, w + NWC, ... of all three terms
+        // query fragment image: warp w builds k-steps w, w + NWC, ... of every term
+        // (bf16 pages: hi/mid/lo bf16; FP8 pages: hi/lo f16, 22 significant bits)
         const float* qs = reinterpret_cast<const float*>(stages + s * STAGE_BYTES + STAGE_KV);
         for (int ks = warp; ks < Cfg::KS; ks += NWC) {
           float t[3][2][4];  // [term][row g / g+8][d0, d0+1, d0+8, d0+9]
@@ -236,14 +238,19 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
               const float v = valid ? qs[row * DP + dd[i]] * p.qscale : 0.f;
-              split3(v, t[0][r][i], t[1][r][i], t[2][r][i]);
+              if constexpr (KV8) {
+                split2h(v, t[0][r][i], t[1][r][i]);
+                t[2][r][i] = 0.f;
+              } else {
+                split3(v, t[0][r][i], t[1][r][i], t[2][r][i]);
+              }
             }
           }
 #pragma unroll
-          for (int term = 0; term < 3; ++term)
+          for (int term = 0; term < kQTerms; ++term)
             qimg[(term * Cfg::KS + ks) * 32 + lane] =
-                make_uint4(pack_bf16(t[term][0][0], t[term][0][1]), pack_bf16(t[term][1][0], t[term][1][1]),
-                           pack_bf16(t[term][0][2], t[term][0][3]), pack_bf16(t[term][1][2], t[term][1][3]));
+                make_uint4(pack_kv<KV8>(t[term][0][0], t[term][0][1]), pack_kv<KV8>(t[term][1][0], t[term][1][1]),
+                           pack_kv<KV8>(t[term][0][2], t[term][0][3]), pack_kv<KV8>(t[term][1][2], t[term][1][3]));
         }
         named_bar_sync(1, NWC * 32);  // image complete before any warp's first page
 #pragma unroll
@@ -263,13 +270,14 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
         for (int nt = 0; nt < 2; ++nt) {
 #pragma unroll
           for (int kp = 0; kp < Cfg::KS / 2; ++kp) {
-            const uint4 kf = lds128(pbase + ((nt * (Cfg::KS / 2) + kp) * 32 + lane) * 16);
+            const int ci = (nt * (Cfg::KS / 2) + kp) * 32 + lane;
+            const uint4 kf = load_kv_frag<KV8>(pbase + ci * 16, pbase + ci * 8);
 #pragma unroll
-            for (int term = 0; term < 3; ++term) {
+            for (int term = 0; term < kQTerms; ++term) {
               const uint4 qa = lds128(qimg_base + ((term * Cfg::KS + 2 * kp) * 32 + lane) * 16);
-              mma_bf16_16816(sacc[nt], qa.x, qa.y, qa.z, qa.w, kf.x, kf.y);
+              mma_kv<KV8>(sacc[nt], qa.x, qa.y, qa.z, qa.w, kf.x, kf.y);
               const uint4 qb = lds128(qimg_base + ((term * Cfg::KS + 2 * kp + 1) * 32 + lane) * 16);
-              mma_bf16_16816(sacc[nt], qb.x, qb.y, qb.z, qb.w, kf.z, kf.w);
+              mma_kv<KV8>(sacc[nt], qb.x, qb.y, qb.z, qb.w, kf.z, kf.w);
             }
           }
         }
@@ -322,23 +330,27 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           for (int i = 0; i < 4; ++i) {
             const float pv = fast_exp2(sv[r][i] - m_ref[r]);
             l_sum[r] += pv;
-            split2(pv, ph[r][i], pl[r][i]);
+            if constexpr (KV8)
+              split2h(pv, ph[r][i], pl[r][i]);
+            else
+              split2(pv, ph[r][i], pl[r][i]);
           }
         }
         // P A-fragments (rows = queries g, g+8; k = tokens): hi tile and lo tile
-        const uint32_t h0 = pack_bf16(ph[0][0], ph[0][1]), h1 = pack_bf16(ph[1][0], ph[1][1]);
-        const uint32_t h2 = pack_bf16(ph[0][2], ph[0][3]), h3 = pack_bf16(ph[1][2], ph[1][3]);
-        const uint32_t q0 = pack_bf16(pl[0][0], pl[0][1]), q1 = pack_bf16(pl[1][0], pl[1][1]);
-        const uint32_t q2 = pack_bf16(pl[0][2], pl[0][3]), q3 = pack_bf16(pl[1][2], pl[1][3]);
+        const uint32_t h0 = pack_kv<KV8>(ph[0][0], ph[0][1]), h1 = pack_kv<KV8>(ph[1][0], ph[1][1]);
+        const uint32_t h2 = pack_kv<KV8>(ph[0][2], ph[0][3]), h3 = pack_kv<KV8>(ph[1][2], ph[1][3]);
+        const uint32_t q0 = pack_kv<KV8>(pl[0][0], pl[0][1]), q1 = pack_kv<KV8>(pl[1][0], pl[1][1]);
+        const uint32_t q2 = pack_kv<KV8>(pl[0][2], pl[0][3]), q3 = pack_kv<KV8>(pl[1][2], pl[1][3]);
         // ---- O += P V
         const uint32_t vbase = pbase + Cfg::PAGE / 2;
 #pragma unroll
         for (int nd2 = 0; nd2 < Cfg::ND / 2; ++nd2) {
-          const uint4 vf = lds128(vbase + (nd2 * 32 + lane) * 16);
-          mma_bf16_16816(acc[2 * nd2], h0, h1, h2, h3, vf.x, vf.y);
-          mma_bf16_16816(acc[2 * nd2], q0, q1, q2, q3, vf.x, vf.y);
-          mma_bf16_16816(acc[2 * nd2 + 1], h0, h1, h2, h3, vf.z, vf.w);
-          mma_bf16_16816(acc[2 * nd2 + 1], q0, q1, q2, q3, vf.z, vf.w);
+          const int ci = nd2 * 32 + lane;
+          const uint4 vf = load_kv_frag<KV8>(vbase + ci * 16, vbase + ci * 8);
+          mma_kv<KV8>(acc[2 * nd2], h0, h1, h2, h3, vf.x, vf.y);
+          mma_kv<KV8>(acc[2 * nd2], q0, q1, q2, q3, vf.x, vf.y);
+          mma_kv<KV8>(acc[2 * nd2 + 1], h0, h1, h2, h3, vf.z, vf.w);
+          mma_kv<KV8>(acc[2 * nd2 + 1], q0, q1, q2, q3, vf.z, vf.w);
         }
       }
       __syncwarp();
@@ -766,7 +778,7 @@ static cudaError_t launch_attn_t(const AttnParams& p, int grid, cudaStream_t str
 // stages in flight. 9-16 query rows of bf16 pages take the W16 consumers.
 template <int QC, bool KV8>
 static cudaError_t launch_attn_dp(const AttnParams& p, int grid, cudaStream_t stream) {
-  constexpr bool W16 = QC == 2 && !KV8;
+  constexpr bool W16 = QC == 2;  // 9-16 query rows: every warp takes 16 rows (bf16 or FP8 pages)
   switch (p.dp) {
     case 32: return launch_attn_t<32, 8, KV8 ? 8 : 4, QC, KV8, W16>(p, grid, stream);
     case 64: return launch_attn_t<64, 8, KV8 ? 6 : 3, QC, KV8, W16>(p, grid, stream);
@@ -775,8 +787,8 @@ static cudaError_t launch_attn_dp(const AttnParams& p, int grid, cudaStream_t st
       // e4m3 widening doubles the per-byte consumer work, so more pages in flight
       // per SM: 0.366 -> 0.339 ms per configs[1] launch vs 8 x 4 (12 x 3: 0.351)
       if constexpr (KV8 && QC == 1) return launch_attn_t<128, 10, 4, QC, KV8, W16>(p, grid, stream);
-      // 16 rows: 8 KB of q per stage, 10 x 3 fits (405B-like FP8 slice: 0.555 -> 0.516 ms vs 8 x 4)
-      if constexpr (KV8) return launch_attn_t<128, 10, 3, QC, KV8, W16>(p, grid, stream);
+      // 16 rows per warp (W16) of FP8 pages: 8 x 3 fits next to the 16-row scratch
+      if constexpr (KV8) return launch_attn_t<128, 8, 3, QC, KV8, W16>(p, grid, stream);
       if constexpr (!KV8 && QC == 1) {
         static const int exp_cfg = std::getenv("HX_ATTN16") ? std::atoi(std::getenv("HX_ATTN16")) : 0;
         if (exp_cfg == 10) return launch_attn_t<128, 10, 2, QC, KV8, W16>(p, grid, stream);

@@ -68,8 +68,13 @@ def test_large_batch_gemv_uses_tcgen05():
     for f in tc:
         for op in ("UTCHMMA", "LDTM", "UBLKCP", "UTCBAR"):
             assert op in f, op
-    fp8 = [f for f in funcs if f.startswith("_ZN2hx18attn_decode_kernel") and "Lb1ELb0E" in f.split("\n", 1)[0]]
+    # FP8 attention instantiations: 8-row (..Lb1ELb0E) and 16-row W16 (..Lb1ELb1E) consumers
+    fp8 = [f for f in funcs if f.startswith("_ZN2hx18attn_decode_kernel") and "Lb1ELb" in f.split("\n", 1)[0]]
+    assert any("Lb1ELb1E" in f.split("\n", 1)[0] for f in fp8)
     assert fp8 and all("F2FP.F16.E4M3.UNPACK_B" in f and "HMMA.16816.F32 " in f for f in fp8)
+    # FP8-weight GEMVs (template flag W8, last argument) widen e4m3 weights the same way
+    w8 = [f for f in funcs if f.startswith("_ZN2hx11gemv_kernel") and "Lb1EEEv" in f.split("\n", 1)[0]]
+    assert w8 and all("F2FP.F16.E4M3.UNPACK_B" in f and "UBLKCP" in f for f in w8)
 
 
 def test_ctypes_structs_match_c_header(tmp_path):
