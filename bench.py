@@ -205,7 +205,7 @@ def pool_slice(a, preset, S, ep, w_dtype="bf16", kv_dtype="bf16"):
         out["workload"] = ("llama405b-like layer, one GPU of TPA=1 x KVP=8 (TPF=8): %d KV heads x %d tokens x B=%d; "
                            "QKV replicated, W_O rows and FFN features 1/8; collectives off (1 GPU)" % (K, s_loc, B))
         out["attention"] = {
-            "kernel": ("attn_decode_kernel<128,8,4,2,fp8>" if kv_dtype == "fp8" else "attn_decode_kernel<128,8,2,2,W16>")
+            "kernel": ("attn_decode_kernel<128,12,2,2,fp8,W16>" if kv_dtype == "fp8" else "attn_decode_kernel<128,8,2,2,W16>")
                       + " (TMA bulk-copy page ring, mma.sync)", "launch_ms": att_ms,
             "algorithmic_kv_bytes": kv_bytes,
             "roofline": {"bound": "hbm", "achieved": kv_bytes / (att_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
