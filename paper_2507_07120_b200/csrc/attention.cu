@@ -23,7 +23,6 @@
 //   * per item, consumers combine their per-warp (m, l, O) through shared
 //     memory and write the split's normalised O and log2-sum-exp.
 // The KV stream is the roofline: 64*DP bytes per page, no re-reads.
-#include <cstdlib>
 
 #include "common.cuh"
 #include "kv_layout.cuh"
@@ -790,10 +789,6 @@ static cudaError_t launch_attn_dp(const AttnParams& p, int grid, cudaStream_t st
       // 16 rows per warp (W16) of FP8 pages: 12 warps x 2 stages next to the 16-row
       // scratch (224 KB; 405B-like FP8 slice 0.430 ms vs 0.450 at 8 x 3, 0.479 at 10 x 2)
       if constexpr (KV8) return launch_attn_t<128, 12, 2, QC, KV8, W16>(p, grid, stream);
-      if constexpr (!KV8 && QC == 1) {
-        static const int exp_cfg = std::getenv("HX_ATTN16") ? std::atoi(std::getenv("HX_ATTN16")) : 0;
-        if (exp_cfg == 10) return launch_attn_t<128, 10, 2, QC, KV8, W16>(p, grid, stream);
-      }
       return launch_attn_t<128, 8, 2, QC, KV8, W16>(p, grid, stream);
     default: return cudaErrorInvalidValue;
   }
