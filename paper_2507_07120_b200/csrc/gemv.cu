@@ -414,6 +414,22 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
       if (f < p.N / 2) xf_write(xf_out, NB8, b, f, y[0] / (1.f + __expf(-y[0])) * y[1], p.xf16);
       continue;
     }
+    if (EM == E_LOGITS) {
+      // argmax: one shared atomic per warp (a warp's 32 rows share the request b;
+      // 128 contending atomics per request made this epilogue ~30 us)
+      unsigned long long key = 0ull;
+      if (n < p.N) {
+        if (p.out) p.out[static_cast<size_t>(b) * p.out_stride + n] = y[0];
+        key = logit_key(y[0], n + p.n_offset);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, key, o);
+        key = other > key ? other : key;
+      }
+      if (lane == 0 && key) atomicMax(&s_best[b], key);
+      continue;
+    }
     if (n >= p.N) continue;
     if (p.addend) y[0] += p.addend[static_cast<size_t>(b) * p.out_stride + n];
     if (EM == E_STORE) {
@@ -424,9 +440,6 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
       p.out[static_cast<size_t>(b) * p.out_stride + n] = keep;
       xf_write(p.xf_out, NB8, b, n, keep, p.xf16);
       vt[b][r] = keep * keep;
-    } else if (EM == E_LOGITS) {
-      if (p.out) p.out[static_cast<size_t>(b) * p.out_stride + n] = y[0];
-      atomicMax(&s_best[b], logit_key(y[0], n + p.n_offset));
     } else if (EM == E_QKV && p.mla && n >= p.nq) {
       // MLA latent row -> its round-robin page (q heads: the GQA branch below,
       // then mla_absorb_q_kernel builds the tcgen05 query image)
