@@ -533,7 +533,7 @@ def ours(a):
         "e2e": {"value": B / (ms_e2e * 1e-3), "unit": UNIT, "h2d_bytes_per_step": 4 * B, "d2h_bytes_per_step": 4 * B,
                 "ms_per_step": ms_e2e},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": ncu_traffic(), "kernel": "attn_decode_kernel<128,8,2>",
+                     "frac": achieved / hbm_peak, "traffic": ncu_traffic(), "kernel": "attn_decode_kernel<128,7,3>",
                      "algorithmic_bytes_per_launch": attn_bytes, "launch_ms": attn_ms_launch, "peak_kind": peak_kind,
                      "step_hbm_frac": step_bytes / (ms * 1e-3) / 1e9 / hbm_peak,
                      "step_algorithmic_bytes": step_bytes},

@@ -24,6 +24,8 @@
 //     memory and write the split's normalised O and log2-sum-exp.
 // The KV stream is the roofline: 64*DP bytes per page, no re-reads.
 
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kv_layout.cuh"
 #include "xfrag.cuh"
@@ -789,6 +791,9 @@ static cudaError_t launch_attn_dp(const AttnParams& p, int grid, cudaStream_t st
       // 16 rows per warp (W16) of FP8 pages: 12 warps x 2 stages next to the 16-row
       // scratch (224 KB; 405B-like FP8 slice 0.430 ms vs 0.450 at 8 x 3, 0.479 at 10 x 2)
       if constexpr (KV8) return launch_attn_t<128, 12, 2, QC, KV8, W16>(p, grid, stream);
+      // bf16 pages, 8 query rows: 7 consumer warps x 3 stages (168 KB of KV in flight):
+      // configs[1] launch 0.606 -> 0.591 ms (7.27 TB/s) vs 8 x 2; 6 x 3 0.597, 5 x 4 0.603, 4 x 5 0.599
+      if constexpr (!KV8 && QC == 1) return launch_attn_t<128, 7, 3, QC, KV8, W16>(p, grid, stream);
       return launch_attn_t<128, 8, 2, QC, KV8, W16>(p, grid, stream);
     default: return cudaErrorInvalidValue;
   }
