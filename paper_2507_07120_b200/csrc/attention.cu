@@ -688,6 +688,13 @@ __global__ void __launch_bounds__(kSrWarps * 32) attn_split_reduce_kernel(const 
 #pragma unroll
     for (int i = 0; i < PER; ++i) frag_o[fo * DP + lane + 32 * i] = Lt > 0.f ? ot[i] / Lt : 0.f;
     if (lane == 0) frag_lse[fo] = Lt > 0.f ? (M + log2f(Lt)) * 0.69314718055994530942f : -INFINITY;
+    if (p.xf_out) {  // one-source pool: the merged attention output IS this fragment
+      const int head = ((slot_local + p.slot_base) / p.kvp) * p.q_per_slot + q_in_group;
+#pragma unroll
+      for (int i = 0; i < PER; ++i)
+        if (lane + 32 * i < p.hd)
+          xf_write(p.xf_out, xf_nb8(p.batch), b, head * p.hd + lane + 32 * i, Lt > 0.f ? ot[i] / Lt : 0.f, p.xf16);
+    }
   }
 }
 
@@ -742,6 +749,13 @@ __global__ void __launch_bounds__(256) attn_split_reduce_small_kernel(const Attn
 #pragma unroll
   for (int i = 0; i < PER; ++i) frag_o[fo * DP + lane + 32 * i] = L > 0.f ? o[i] / L : 0.f;
   if (lane == 0) frag_lse[fo] = L > 0.f ? (M + log2f(L)) * 0.69314718055994530942f : -INFINITY;
+  if (p.xf_out) {  // one-source pool: the merged attention output IS this fragment
+    const int head = ((slot_local + p.slot_base) / p.kvp) * p.q_per_slot + q_in_group;
+#pragma unroll
+    for (int i = 0; i < PER; ++i)
+      if (lane + 32 * i < p.hd)
+        xf_write(p.xf_out, xf_nb8(p.batch), b, head * p.hd + lane + 32 * i, L > 0.f ? o[i] / L : 0.f, p.xf16);
+  }
 }
 
 __global__ void bump_totals_kernel(int* total, int n) {

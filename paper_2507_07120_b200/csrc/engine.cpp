@@ -390,6 +390,8 @@ void Engine::alloc() {
 
 // ---------------------------------------------------------------------------
 void Engine::plan_gemvs() {
+  one_src_merge_ = dist_mode_ == HX_POOL_LOCAL && !mla_ && !attn_only_ && kvp_ == 1 &&
+                   !(std::getenv("HX_ONE_SRC_MERGE") && std::getenv("HX_ONE_SRC_MERGE")[0] == '0');
   d_plan_ctr_ = dalloc<int>(static_cast<size_t>(2 * (7 * L_ + 2)), "plan counters");
   int plan_idx = 0;
   // groups: expected concurrent weight blocks (MoE: active experts) for tile sizing
@@ -542,7 +544,7 @@ void Engine::plan_gemvs() {
   if (attn_only_)
     kernels_per_step_ = 6;  // xprep, qkv x2, attention, split-reduce, merge(+bump)
   else if (!dist)
-    kernels_per_step_ = 1 + (7 + ffn_k + (mla_ ? 2 : 0)) * L_ + 3;  // MLA: + absorb_q, uv
+    kernels_per_step_ = 1 + (7 - (one_src_merge_ ? 1 : 0) + ffn_k + (mla_ ? 2 : 0)) * L_ + 3;  // MLA: + absorb_q, uv
   else  // + pack and two residual adds per layer; per-request attention launches under HOP-B
     kernels_per_step_ = 1 + L_ * (9 + ffn_k + (mla_ ? 2 : 0) + (hopb_ ? 3 * (B_ - 1) : 0)) + 3;
 }
@@ -624,6 +626,7 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
       const int ko = !dist ? 0 : (mla_ ? uv_h0_ * static_cast<int>(D_) : grp_ * q_per_slot_ * AD_ + r_ * slice_);
       init(w_o_[l], plan_o_[l], {{hash_stream(kWo, l), 0, Hh, Hh, 0, 0, sh, ko, 0}}, Hh);
       plan_o_[l].p.w = w_o_[l];
+      plan_o_[l].p.bump_total = one_src_merge_ ? d_total_ + l * B_ : nullptr;
       if (F > 0) {
         init(w_gu_[l], plan_gu_[l],
              {{hash_stream(kWgate, l), 0, plan_gu_[l].p.Npad, static_cast<int>(F_), f0, 1, sh, 0, f0 + F},
@@ -1054,6 +1057,11 @@ AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) {
   a.q_chunks = q_chunks_;
   a.qrows = q_rows_;
   a.kv8 = kv8_ ? 1 : 0;
+  if (one_src_merge_) {
+    a.xf_out = d_xf_attn_;
+    a.xf16 = xf16_();
+    a.hd = static_cast<int>(D_);
+  }
   a.kvh_per_slot = kvh_per_slot_;
   a.q_per_slot = q_per_slot_;
   a.kvp = kvp_;
@@ -1203,10 +1211,11 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
     if (!dist) {
       // LSE-rescale combine of the KVP fragments -> O-proj activations (attention.hpp:118-175)
       // (a fused split+KVP merge kernel measured 0.2 ms/step slower than this pair)
-      cuda_check(launch_xprep_merge_local(d_frag_o_, d_frag_lse_, B_, q_per_slot_, kvp_, AD_, ADP_,
-                                          static_cast<int>(Qh_) * AD_, d_xf_attn_, d_total_ + l * B_, stream_,
-                                          mla_ ? d_att_ : nullptr, xf16_()),
-                 "merge");
+      if (!one_src_merge_)
+        cuda_check(launch_xprep_merge_local(d_frag_o_, d_frag_lse_, B_, q_per_slot_, kvp_, AD_, ADP_,
+                                            static_cast<int>(Qh_) * AD_, d_xf_attn_, d_total_ + l * B_, stream_,
+                                            mla_ ? d_att_ : nullptr, xf16_()),
+                   "merge");
       if (mla_)
         cuda_check(launch_mla_uv(d_att_, w_uv_[l], B_, uv_heads_, static_cast<int>(D_), d_xf_attn_, stream_, xf16_()),
                    "mla uv");

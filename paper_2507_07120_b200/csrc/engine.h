@@ -104,7 +104,11 @@ class Engine {
   bool loopback_ = false;
   bool kv8_ = false;  // FP8 e4m3 GQA pages (hx_runtime_config.kv_dtype)
   bool tc_ = false;   // batch > 16: tcgen05 GEMVs (weights / x-fragments in their operand images)
-  bool w8_ = false;   // FP8 e4m3 GEMV weights (hx_runtime_config.w_dtype), per-output pow2 scales
+  bool w8_ = false;
+  // local pool with KVP = 1 (one fragment per query head): the split reduce
+  // writes the O-projection's x-fragments itself, the O-proj epilogue bumps
+  // the token totals, and the merge kernel is not launched
+  bool one_src_merge_ = false;   // FP8 e4m3 GEMV weights (hx_runtime_config.w_dtype), per-output pow2 scales
   int xf16_() const { return w8_ ? 1 : 0; }  // x-fragments as f16 terms (xfrag.cuh)
   std::map<const void*, float*> wscale_;     // FP8 weight block -> its [Npad] scales
   int DP_, G_, q_rows_, q_chunks_, kvh_per_slot_, q_per_slot_, n_slots_, slot_base_;

@@ -323,6 +323,10 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
     s_pos[b][1] = rr_row(g, p.rr_chunk, p.kvp);
   }
   if (EM == E_LOGITS && threadIdx.x < 64) s_best[threadIdx.x] = 0ull;
+  // one-source pools: the attention's appended token counts from here on (the
+  // merge kernel that bumped it is skipped; nothing reads the totals in between)
+  if (p.bump_total && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && static_cast<int>(threadIdx.x) < p.batch)
+    p.bump_total[threadIdx.x] += 1;
   if (EM == E_STORE || EM == E_RESID)
     for (int i = threadIdx.x; i < 64 * kRows; i += blockDim.x) vt[i / kRows][i % kRows] = 0.f;
   __syncthreads();

@@ -55,6 +55,10 @@ struct AttnParams {
   int stream_batch;        // (HOP-B launches one request at a time)
   const uint8_t* qimg;     // MLA: [B] absorbed-query images (kv_layout.cuh mla_q_offset)
   int qrows;               // GQA: query rows per stream (8, or 16 when the group exceeds 8)
+  // one-source pools (local, KVP = 1): the split reduce also writes the merged
+  // output's x-fragments (the merge of one fragment is the identity) -- no merge kernel
+  uint8_t* xf_out;
+  int xf16, hd;
   int kv8;                 // GQA: FP8 (e4m3) pages (kv_layout.cuh), f16 MMAs
 };
 cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t stream);
@@ -134,6 +138,7 @@ struct GemvParams {
   const float* route_w;      // [B][n_experts] routing weights: the epilogue combines groups
   int n_experts;
   const float* addend;       // optional [B][out_stride] added by E_RESID / E_STORE
+  int* bump_total;           // optional [B]: token totals bumped by the epilogue (merge kernel skipped)
   int prefetch_stages;       // weight stages streamed before griddepcontrol.wait (<= ring depth)
   // FP8 weights (B <= 16, ungrouped): w holds e4m3 bytes in the same tile order
   // ([Npad/128][K/16][8][32 lanes][8 B]), wscale the per-output power-of-two scales
