@@ -42,7 +42,10 @@ def parse():
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--context", type=int, default=131072, help="KV tokens per request per GPU")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-context", type=int, default=131072)
+    ap.add_argument("--cpu-context", type=int, default=131072,
+                    help="context of the 1-thread cpu_baseline sample in our arm's line")
+    ap.add_argument("--ref-context", type=int, default=32768,
+                    help="context of the --impl reference sample (all host threads; scaled to the workload)")
     ap.add_argument("--profile-only", action="store_true", help="skip timing loops (for ncu)")
     ap.add_argument("--no-fp8", action="store_true", help="skip the FP8-KV variant of the headline workload")
     ap.add_argument("--no-slices", action="store_true",
@@ -337,18 +340,26 @@ def ncu_traffic(key="attention"):
 
 
 # ----------------------------------------------------------------------------- CPU reference
-def run_ref_bench(threads, context, steps, warmup, layers, batch):
+def run_ref_bench(threads, context, steps, warmup, layers, batch, kvp=1, context_full=None):
+    """The reference's DecodeHarness<double>::step (oracle/_ref/ref_bench) on
+    `threads` host threads, one request harness per thread, each step one layer's
+    attention of every thread's request at `context` tokens over a KVP=`kvp`
+    sharded cache. Returns the measured sample and the throughput it implies for
+    the full workload (batch requests x `layers` layers x `context_full` tokens;
+    attention cost is linear in the context -- acceptance.cpp:82-116)."""
+    context_full = context_full or context
     exe = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
     if os.path.exists(exe):
-        out = subprocess.run([exe, "32", "8", "128", "1", "1", str(context), str(steps), str(threads), str(warmup)],
-                             capture_output=True, text=True, check=True).stdout
+        out = subprocess.run([exe, "32", "8", "128", "1", str(kvp), str(context), str(steps), str(threads),
+                              str(warmup)], capture_output=True, text=True, check=True).stdout
         r = json.loads(out.strip().splitlines()[-1])
         t = r["seconds_per_step_per_request"]
+        wall_step = r["wall_s"] / max(1, steps)
         kind = "reference"
     else:
         # oracle port (clean-room restatement) when the reference could not be built
         from tests import oracle_py as O
-        h = O.Harness(32, 8, 128, 1, 1, 16, 42)
+        h = O.Harness(32, 8, 128, 1, kvp, 16, 42)
         h.grow_random(context, O.Rng(1000))
         x = O.Rng(7).draws(4096)
         for _ in range(warmup):
@@ -357,34 +368,44 @@ def run_ref_bench(threads, context, steps, warmup, layers, batch):
         for _ in range(steps):
             h.step(x)
         t = (time.time() - t0) / steps
+        wall_step = t
         threads, kind = 1, "port"
-    # one decode step = batch x layers reference harness steps; threads run requests in parallel
-    tok_s = threads / (t * layers)
-    sample = (f"DecodeHarness<double>::step, Q=32 K=8 Hsz=128, {context}-token context, {steps} timed steps "
-              f"x {threads} concurrent requests; extrapolated x{layers} layers (the reference has no "
-              f"O-proj/FFN/LM-head numerics, so this CPU figure covers attention only)")
+    scale = context_full / context
+    # request-layer attention steps per second at the sample context -> full decode steps
+    tok_s = threads / (t * layers * scale)
+    sample = (f"DecodeHarness<double>::step (attention.hpp:460-510), Q=32 K=8 Hsz=128 KVP={kvp}, {context}-token "
+              f"context, {steps} timed steps after {warmup} warm-up, {threads} request harnesses on {threads} host "
+              f"threads; one sample step = one layer's attention for each thread's request; throughput scaled x"
+              f"{layers} layers" + (f" and x{scale:g} to the {context_full}-token context" if scale != 1 else "") +
+              " (the reference has no O-proj/FFN/LM-head numerics, so the CPU figure covers attention only)")
     return {"value": tok_s, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample,
-            "seconds_per_request_layer_step": t}
+            "seconds_per_request_layer_step": t, "sample_ms_per_step": wall_step * 1e3,
+            "ms_per_full_step_extrapolated": batch / tok_s * 1e3}
 
 
 def reference_arm(a):
+    """--impl reference: the reference's own CPU path on this box's host cores,
+    rank 0 only (other ranks exit without work), exactly --steps timed sample
+    steps after --warmup untimed ones (run_ref_bench)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    n = a.gpus
     threads = os.cpu_count() or 1
-    ctx = a.cpu_context
-    # bound memory: ~16.8 KB of doubles per token per request (K,V x 8 heads x 128)
+    ctx_full = a.context * n
+    ctx = min(ctx_full, a.ref_context)
+    # bound memory: K and V doubles of 8 heads x 128 per token per request (+ chunk slack)
     try:
         mem = os.sysconf("SC_PAGE_SIZE") * os.sysconf("SC_PHYS_PAGES")
         threads = max(1, min(threads, int(mem * 0.5 // (ctx * 8 * 128 * 2 * 8 * 1.5))))
     except (ValueError, OSError):
         pass
-    steps = max(1, min(a.steps, 3))
-    cb = run_ref_bench(threads, ctx, steps, min(a.warmup, 1), a.layers, a.batch)
-    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": a.gpus, "steps": steps,
-            "warmup": min(a.warmup, 1), "ms_per_step": a.batch / cb["value"] * 1e3, "higher_is_better": True,
+    cb = run_ref_bench(threads, ctx, a.steps, a.warmup, a.layers, a.batch, kvp=n, context_full=ctx_full)
+    line = {"metric": METRIC, "value": cb["value"], "unit": UNIT, "n_gpus": n, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": cb["sample_ms_per_step"],
+            "ms_per_full_step_extrapolated": cb["ms_per_full_step_extrapolated"], "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": config_dict(a, a.gpus), "impl": "reference",
+            "config": config_dict(a, n), "impl": "reference",
             "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
             "e2e": {"value": cb["value"], "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -546,9 +567,28 @@ def ours(a):
     }
     if hopb is not None:
         line["hopb"] = hopb
+    if world > 1:
+        # one GPU of the KVP = N pool (TPA = 1, TPF = N): HBM bytes it reads per step and the
+        # NVLink bytes it sends (fp32 fragment slices to N-1 peers, two ring all-reduces of the
+        # [B x H] fp32 partials per layer, latency.cpp:77-146); combined roofline = HBM time at
+        # the measured peak + NVLink time at 900 GB/s per direction, nothing overlapped
+        H, Q, K, Hsz, F, V = (spec.hidden_dim, spec.query_heads, spec.kv_heads, spec.head_size, spec.ffn_dim,
+                              spec.vocab)
+        s_loc = int(P.lib().hx_effective_tokens(eng._h, 0, 0, rank % world))
+        kv = B * 2 * K * Hsz * s_loc * 2 * L
+        w = (H * (Q + 2 * K) * Hsz * 2 + (H // world) * H * 2 + 3 * H * F // world * 2) * L + (V // world) * H * 2
+        xchunk = int(P.lib().hx_exchange_layout(Q, Hsz, world, None))
+        a2a = (world - 1) * B * xchunk * 4 * L
+        ar = 2 * (2 * (world - 1) / world * B * H * 4) * L
+        t_hbm, t_nvl = (kv + w) / (hbm_peak * 1e9), (a2a + ar) / 900e9
+        line["pool"] = {"kvp": world, "tpa": 1, "tpf": world, "comm_ranks": info["comm_ranks"],
+                        "nccl_version": info["nccl_version"], "kv_tokens_per_request_per_gpu": s_loc,
+                        "global_context": s_loc * world, "ttl_ms": ms, "tokens_per_s_per_gpu": value / world,
+                        "hbm_bytes_per_gpu_per_step": kv + w, "nvlink_bytes_per_gpu_per_step": a2a + ar,
+                        "t_roof_ms": (t_hbm + t_nvl) * 1e3, "roofline_frac": (t_hbm + t_nvl) * 1e3 / ms}
     if not a.no_cpu_baseline and rank == 0 and world == 1:
         try:
-            cb = run_ref_bench(1, a.cpu_context, 2, 0, L, B)
+            cb = run_ref_bench(1, min(a.cpu_context, S), 2, 0, L, B, context_full=S)
             line["cpu_baseline"] = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
         except Exception as ex:  # reported, never fatal for the GPU number
             line["cpu_baseline"] = {"error": str(ex)[:200]}
@@ -588,13 +628,43 @@ def ours(a):
         dist.destroy_process_group()
 
 
+def relaunch_under_torchrun(a):
+    """`python bench.py --gpus N` (N > 1) outside torchrun: launch the N ranks
+    here, one process per GPU, exactly as the driver does (torch.distributed.run,
+    127.0.0.1 rendezvous), with NCCL's init log on so every communicator's
+    nranks is visible in stderr."""
+    import socket
+    import torch
+    have = torch.cuda.device_count()
+    if have < a.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {a.gpus} but {have} GPU(s) visible"}), flush=True)
+        return 1
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd, env=env)
+
+
 def main():
     a = parse()
     if a.impl == "reference":
         reference_arm(a)
-    else:
-        ours(a)
+        return 0
+    world = os.environ.get("WORLD_SIZE")
+    if world is None and a.gpus > 1:
+        return relaunch_under_torchrun(a)
+    if world is not None and int(world) != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}")
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    ours(a)
+    return 0
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

@@ -97,6 +97,7 @@ typedef struct hx_runtime_config {
 
 #define HX_KV_BF16 0
 #define HX_KV_FP8_E4M3 1
+#define HX_KV_F64 2 /* exact harness: fp64 shards, weights, projections and merges (DecodeHarness<double>) */
 #define HX_W_BF16 0
 #define HX_W_FP8_E4M3 1
 
@@ -110,6 +111,8 @@ typedef struct hx_engine_info {
   int64_t head_dim_padded;
   int64_t kv_dtype;                /* HX_KV_BF16 / HX_KV_FP8_E4M3 */
   int64_t w_dtype;                 /* HX_W_BF16 / HX_W_FP8_E4M3 */
+  int64_t comm_ranks;              /* ranks of the pool's world communicator (1: local pool) */
+  int64_t nccl_version;            /* ncclGetVersion of the linked NCCL (0: no NCCL pool) */
 } hx_engine_info;
 
 const char* hx_version(void);
@@ -163,6 +166,32 @@ int hx_decode_step_device(hx_engine* e, const int32_t* tokens_dev, int32_t* next
 /* Device-resident harness step (x/out device pointers, [batch][hidden] / [batch][Q][Hsz]). */
 int hx_harness_step_device(hx_engine* e, int64_t layer, const float* x_dev, float* out_dev);
 int hx_synchronize(hx_engine* e);
+
+/* --- exact harness (kv_dtype HX_KV_F64): DecodeHarness<double> in fp64 on the GPU ---
+ * The reference's own precision for callers holding its tolerances (1e-10 / 1e-12);
+ * attention-only local pools. x [batch][hidden]; out [batch][query_heads][head_size]. */
+int hx_harness_step_f64(hx_engine* e, int64_t layer, const double* x, int64_t x_len, double* out,
+                        double* lse);                                   /* step, attention.hpp:460-510 */
+int hx_harness_reference_f64(hx_engine* e, int64_t layer, const double* x, int64_t x_len,
+                             double* out);                              /* reference, :514-529 */
+int hx_append_projected_f64(hx_engine* e, int64_t layer, const double* x, int64_t x_len); /* :531-539 */
+/* append_round_robin of caller rows [n][kv_heads][head_size] (attention.hpp:262-282) */
+int hx_append_kv_f64(hx_engine* e, int64_t layer, int64_t request, int64_t n, const double* k,
+                     const double* v);
+int hx_read_kv_f64(hx_engine* e, int64_t layer, int64_t request, int64_t rank, int64_t head, double* k,
+                   double* v);                                          /* context, :303-309 */
+
+/* --- free functions on caller-supplied operands (fp64, current CUDA device) --- */
+/* partial_head_attention (attention.hpp:65-78) for n_queries queries [n_queries][width] over
+ * one K/V [tokens][width] (row-major): out [n_queries][width], lse [n_queries] (natural log;
+ * tokens == 0 gives the identity (0, -inf)). shard_attention (:375-396) is one call per KV
+ * head; reference_attention (:43-53) is the same call over the whole context. width <= 512. */
+int hx_attention_f64(const double* q, int64_t n_queries, const double* keys, const double* values,
+                     int64_t tokens, int64_t width, double* out, double* lse);
+/* merge_head_fragments (attention.hpp:118-137): canonical order (descending lse, ties by the
+ * first differing coefficient), outs [n][width], lses [n] -> out [width], lse. */
+int hx_merge_f64(int64_t n_fragments, int64_t width, const double* outs, const double* lses, double* out,
+                 double* lse);
 /* Profiling: `reps` eager steps (decode step, or one harness step per layer in
  * attention-only mode) with CUDA events after every launch on the engine
  * stream; ms[kind] = average milliseconds per step for kind

@@ -34,7 +34,7 @@ class RuntimeConfig(C.Structure):
                 ("kv_dtype", i32), ("w_dtype", i32), ("reserved", i32)]
 
 
-KV_DTYPES = {"bf16": 0, "fp8": 1, "fp8_e4m3": 1}
+KV_DTYPES = {"bf16": 0, "fp8": 1, "fp8_e4m3": 1, "f64": 2}
 W_DTYPES = {"bf16": 0, "fp8": 1, "fp8_e4m3": 1}
 
 
@@ -42,7 +42,7 @@ class EngineInfo(C.Structure):
     _fields_ = [("kv_bytes_per_layer", i64), ("weight_bytes_per_layer", i64), ("head_bytes", i64),
                 ("attn_streams", i64), ("attn_splits", i64), ("attn_items", i64), ("attn_grid", i64),
                 ("kernels_per_step", i64), ("page_cap", i64), ("head_dim_padded", i64), ("kv_dtype", i64),
-                ("w_dtype", i64)]
+                ("w_dtype", i64), ("comm_ranks", i64), ("nccl_version", i64)]
 
 
 EXPORTS = {
@@ -80,6 +80,13 @@ EXPORTS = {
     "hx_engine_set_flag": (C.c_int, [vp, i32, i32]),
     "hx_moe_active_experts": (i64, [vp]),
     "hx_loopback_destroy": (None, [vp]),
+    "hx_harness_step_f64": (C.c_int, [vp, i64, dp, i64, dp, dp]),
+    "hx_harness_reference_f64": (C.c_int, [vp, i64, dp, i64, dp]),
+    "hx_append_projected_f64": (C.c_int, [vp, i64, dp, i64]),
+    "hx_append_kv_f64": (C.c_int, [vp, i64, i64, i64, dp, dp]),
+    "hx_read_kv_f64": (C.c_int, [vp, i64, i64, i64, i64, dp, dp]),
+    "hx_attention_f64": (C.c_int, [dp, i64, dp, dp, i64, i64, dp, dp]),
+    "hx_merge_f64": (C.c_int, [i64, i64, dp, dp, dp, dp]),
 }
 
 _lib = None

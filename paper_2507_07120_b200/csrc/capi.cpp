@@ -128,6 +128,30 @@ int hx_decode_step_device(hx_engine* e, const int32_t* tokens_dev, int32_t* next
 int hx_profile_step(hx_engine* e, int64_t reps, double* ms) {
   return guard(e, [&] { e->e->profile_step(reps, ms); });
 }
+int hx_harness_step_f64(hx_engine* e, int64_t layer, const double* x, int64_t x_len, double* out, double* lse) {
+  return guard(e, [&] { e->e->harness_step_f64(layer, x, x_len, out, lse); });
+}
+int hx_harness_reference_f64(hx_engine* e, int64_t layer, const double* x, int64_t x_len, double* out) {
+  return guard(e, [&] { e->e->harness_reference_f64(layer, x, x_len, out); });
+}
+int hx_append_projected_f64(hx_engine* e, int64_t layer, const double* x, int64_t x_len) {
+  return guard(e, [&] { e->e->append_projected_f64(layer, x, x_len); });
+}
+int hx_append_kv_f64(hx_engine* e, int64_t layer, int64_t request, int64_t n, const double* k, const double* v) {
+  return guard(e, [&] { e->e->append_kv_f64(layer, request, n, k, v); });
+}
+int hx_read_kv_f64(hx_engine* e, int64_t layer, int64_t request, int64_t rank, int64_t head, double* k, double* v) {
+  return guard(e, [&] { e->e->read_kv_f64(layer, request, rank, head, k, v); });
+}
+int hx_attention_f64(const double* q, int64_t n_queries, const double* keys, const double* values, int64_t tokens,
+                     int64_t width, double* out, double* lse) {
+  return guard(nullptr, [&] { hx::attention_f64(q, n_queries, keys, values, tokens, width, out, lse); });
+}
+int hx_merge_f64(int64_t n_fragments, int64_t width, const double* outs, const double* lses, double* out,
+                 double* lse) {
+  return guard(nullptr, [&] { hx::merge_f64(n_fragments, width, outs, lses, out, lse); });
+}
+
 int hx_synchronize(hx_engine* e) {
   return guard(e, [&] { e->e->synchronize(); });
 }

@@ -122,7 +122,16 @@ class NcclTransport : public Transport {
     if (group_) ncclCommDestroy(group_);
     if (world_) ncclCommDestroy(world_);
   }
-  int world() const override { return n_; }
+  int world() const override {
+    int n = 0;
+    nccl_check(ncclCommCount(world_, &n), "ncclCommCount");
+    return n;
+  }
+  int64_t nccl_version() const override {
+    int v = 0;
+    ncclGetVersion(&v);
+    return v;
+  }
   void all_to_all(const float* send, float* recv, size_t count, size_t stride, cudaStream_t s) override {
     nccl_check(ncclGroupStart(), "ncclGroupStart");
     for (int p = 0; p < kvp_; ++p) {

@@ -31,6 +31,7 @@ class Transport {
   virtual void all_reduce_sum(float* buf, size_t n, cudaStream_t s) = 0;
   virtual void all_reduce_max_u64(unsigned long long* buf, size_t n, cudaStream_t s) = 0;
   virtual int world() const = 0;
+  virtual int64_t nccl_version() const { return 0; }
 };
 
 // Shared state of a loopback group (all ranks in one process, one device).

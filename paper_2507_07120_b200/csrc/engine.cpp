@@ -122,13 +122,21 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
       distributed_(par.distributed != 0), rank_(par.rank), B_(static_cast<int>(rt.batch)),
       cap_(rt.capacity_tokens), device_(rt.device), hopb_(rt.hopb != 0), graphs_(rt.use_graphs != 0) {
   validate_reference_dims();
+  // the merge kernels hold one (lse, coefficient) pair per KVP rank (merge.cuh);
+  // validate_config caps a Helix pool at max_gpus = 64 (types.hpp:63)
+  if (kvp_ > kMaxKvp) throw std::invalid_argument("kvp > 64 is not supported (validate_config max_gpus = 64)");
   if (H_ != Qh_ * D_) throw std::invalid_argument("hidden_dim must equal query_heads * head_size");
   if (L_ < 1) throw std::invalid_argument("layers must be >= 1");
   if (B_ < 1 || B_ > 64) throw std::invalid_argument("batch must be in [1, 64] for the B200 decode kernels");
   if (cap_ < 1) throw std::invalid_argument("capacity_tokens must be >= 1");
   mla_ = m.kv_latent > 0;
-  if (rt.kv_dtype != HX_KV_BF16 && rt.kv_dtype != HX_KV_FP8_E4M3) throw std::invalid_argument("unknown kv_dtype");
+  if (rt.kv_dtype != HX_KV_BF16 && rt.kv_dtype != HX_KV_FP8_E4M3 && rt.kv_dtype != HX_KV_F64)
+    throw std::invalid_argument("unknown kv_dtype");
   kv8_ = rt.kv_dtype == HX_KV_FP8_E4M3;
+  f64_ = rt.kv_dtype == HX_KV_F64;
+  if (f64_ && (!attn_only_ || par.distributed != HX_POOL_LOCAL))
+    throw std::invalid_argument("the exact fp64 harness (HX_KV_F64) is the attention-only local pool "
+                                "(DecodeHarness<double>)");
   if (kv8_ && mla_) throw std::invalid_argument("FP8 KV pages are implemented for GQA caches (MLA latents stay bf16)");
   if (rt.w_dtype != HX_W_BF16 && rt.w_dtype != HX_W_FP8_E4M3) throw std::invalid_argument("unknown w_dtype");
   w8_ = rt.w_dtype == HX_W_FP8_E4M3;
@@ -232,6 +240,10 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
     page_cap_ = static_cast<int>((per_rank_max + 15) / 16 + 1);
     page_bytes_ = page_bytes_kv(DP_, kv8_);
   }
+  if (f64_) {  // fp64 shards instead of bf16 pages (exact64.cu)
+    rows_cap64_ = per_rank_max;
+    page_cap_ = 1;
+  }
 
   if (std::getenv("HX_NO_PDL")) set_pdl(false);  // debugging: serialise every launch
   // batches above 16 make the GEMV contraction dense enough for tcgen05 (gemv_tc.cu);
@@ -285,6 +297,10 @@ Engine::~Engine() {
   f(d_frag_o_); f(d_frag_lse_); f(d_ypart_); f(d_counters_); f(d_x_); f(d_ss_); f(d_m_);
   f(d_logits_); f(d_best_); f(d_tokens_); f(d_next_); f(d_out_); f(d_out_lse_); f(d_hidden_);
   f(d_segs_); f(d_send_); f(d_recv_); f(d_parth_); f(d_xf_resid_); f(d_xf_attn_); f(d_xf_m_); f(d_plan_ctr_);
+  for (auto* p : k64_) f(p);
+  for (auto* p : v64_) f(p);
+  for (auto* p : w64_) f(p);
+  f(d_x64_); f(d_qkv64_); f(d_frag64_o_); f(d_frag64_lse_); f(d_out64_); f(d_lse64_);
   for (auto& e : hop_events_) cudaEventDestroy(e);
   delete transport_;
   if (comm_stream_) cudaStreamDestroy(comm_stream_);
@@ -386,6 +402,21 @@ void Engine::alloc() {
   d_next_ = dalloc<int>(B_, "next");
   d_best_ = dalloc<unsigned long long>(B_, "best");
   d_segs_ = dalloc<WSeg>(16, "segs");
+  if (f64_) {
+    const size_t shard = static_cast<size_t>(n_slots_) * B_ * kvh_per_slot_ * rows_cap64_ * D_;
+    const size_t ncols = static_cast<size_t>(Qh_ + 2 * Kh_) * D_;
+    for (int64_t l = 0; l < L_; ++l) {
+      k64_.push_back(dalloc<double>(shard, "f64 K shards"));
+      v64_.push_back(dalloc<double>(shard, "f64 V shards"));
+      w64_.push_back(dalloc<double>(static_cast<size_t>(H_) * ncols, "f64 qkv weights"));
+    }
+    d_x64_ = dalloc<double>(static_cast<size_t>(B_) * H_, "f64 x");
+    d_qkv64_ = dalloc<double>(static_cast<size_t>(B_) * ncols, "f64 qkv");
+    d_frag64_o_ = dalloc<double>(static_cast<size_t>(n_slots_) * B_ * q_per_slot_ * D_, "f64 frag_o");
+    d_frag64_lse_ = dalloc<double>(static_cast<size_t>(n_slots_) * B_ * q_per_slot_, "f64 frag_lse");
+    d_out64_ = dalloc<double>(static_cast<size_t>(B_) * Qh_ * D_, "f64 out");
+    d_lse64_ = dalloc<double>(static_cast<size_t>(B_) * Qh_, "f64 lse");
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -804,6 +835,18 @@ void Engine::init_weights_mt19937(uint64_t seed) {
     for (double& v : wk) v = unit_draw(rng);
     for (double& v : wv) v = unit_draw(rng);
     upload_qkv_host(l, wq, wk, wv);
+    if (f64_) {  // [H][q cols | k cols | v cols] in double, the reference's values exactly
+      const size_t ncols = static_cast<size_t>(nq + 2 * nk);
+      std::vector<double> w(static_cast<size_t>(H_) * ncols);
+      for (int64_t k = 0; k < H_; ++k) {
+        std::memcpy(&w[k * ncols], &wq[k * nq], nq * sizeof(double));
+        std::memcpy(&w[k * ncols + nq], &wk[k * nk], nk * sizeof(double));
+        std::memcpy(&w[k * ncols + nq + nk], &wv[k * nk], nk * sizeof(double));
+      }
+      cuda_check(cudaMemcpyAsync(w64_[l], w.data(), w.size() * sizeof(double), cudaMemcpyHostToDevice, stream_),
+                 "f64 weights");
+      cuda_check(cudaStreamSynchronize(stream_), "f64 weights sync");
+    }
   }
 }
 
@@ -848,6 +891,20 @@ void Engine::grow_random(int64_t layer, int64_t request, int64_t n, std::mt19937
   if (request < 0 || request >= B_) throw std::invalid_argument("request out of range");
   const int64_t per = Kh_ * D_;
   const int64_t block = 4096;
+  if (f64_) {  // the reference's doubles, unrounded
+    std::vector<double> k, v;
+    for (int64_t done = 0; done < n; done += block) {
+      const int64_t m = std::min(block, n - done);
+      k.resize(static_cast<size_t>(m * per));
+      v.resize(static_cast<size_t>(m * per));
+      for (int64_t i = 0; i < m; ++i) {  // attention.hpp:454-455 under g++: V drawn before K
+        for (int64_t j = 0; j < per; ++j) v[static_cast<size_t>(i * per + j)] = unit_draw(rng);
+        for (int64_t j = 0; j < per; ++j) k[static_cast<size_t>(i * per + j)] = unit_draw(rng);
+      }
+      append_kv_f64(layer, request, m, k.data(), v.data());
+    }
+    return;
+  }
   std::vector<float> k, v;
   for (int64_t done = 0; done < n; done += block) {
     const int64_t m = std::min(block, n - done);
@@ -873,6 +930,12 @@ void Engine::grow_random(int64_t layer, int64_t request, int64_t n, std::mt19937
 
 void Engine::append_kv(int64_t layer, int64_t request, int64_t n, const float* k, const float* v) {
   check_layer(layer);
+  if (f64_) {
+    const size_t cnt = static_cast<size_t>(std::max<int64_t>(n, 0) * Kh_ * D_);
+    std::vector<double> kd(k, k + cnt), vd(v, v + cnt);
+    append_kv_f64(layer, request, n, kd.data(), vd.data());
+    return;
+  }
   if (mla_) throw std::invalid_argument("append_kv takes GQA K/V rows; MLA caches hold latents");
   if (request < 0 || request >= B_) throw std::invalid_argument("request out of range");
   if (n < 0) throw std::invalid_argument("token count must be >= 0");
@@ -909,6 +972,7 @@ void Engine::append_kv(int64_t layer, int64_t request, int64_t n, const float* k
 }
 
 void Engine::fill_kv_hash(int64_t n, uint64_t seed) {
+  if (f64_) throw std::invalid_argument("the exact fp64 harness grows with grow_random / append");
   for (int64_t l = 0; l < L_; ++l)
     for (int b = 0; b < B_; ++b)
       if (h_total_[static_cast<size_t>(l * B_ + b)] + n > cap_) throw std::invalid_argument("KV capacity exceeded");
@@ -972,6 +1036,16 @@ void Engine::read_kv(int64_t layer, int64_t request, int64_t rank, int64_t head,
         k[t * W_ + d] = float_from_bf16_bits(kb);
         if (d < DV_) v[t * DV_ + d] = float_from_bf16_bits(kb);
       }
+    }
+    return;
+  }
+  if (f64_) {
+    const int64_t n = effective_tokens(layer, request, rank);
+    std::vector<double> kd(static_cast<size_t>(n * D_)), vd(static_cast<size_t>(n * D_));
+    read_kv_f64(layer, request, rank, head, kd.data(), vd.data());
+    for (size_t i = 0; i < kd.size(); ++i) {
+      k[i] = static_cast<float>(kd[i]);
+      v[i] = static_cast<float>(vd[i]);
     }
     return;
   }
@@ -1165,6 +1239,15 @@ void Engine::enqueue_exchange_and_attention_dist(int64_t layer) {
 
 void Engine::harness_step(int64_t layer, const float* x_host, int64_t x_len, float* out, float* lse) {
   check_layer(layer);
+  if (f64_) {
+    std::vector<double> xd(x_host, x_host + std::max<int64_t>(x_len, 0));
+    std::vector<double> od(static_cast<size_t>(B_ * Qh_ * D_)), ld(static_cast<size_t>(B_ * Qh_));
+    harness_step_f64(layer, xd.data(), x_len, od.data(), ld.data());
+    for (size_t i = 0; i < od.size(); ++i) out[i] = static_cast<float>(od[i]);
+    if (lse)
+      for (size_t i = 0; i < ld.size(); ++i) lse[i] = static_cast<float>(ld[i]);
+    return;
+  }
   if (x_len != static_cast<int64_t>(B_) * H_) throw std::invalid_argument("hidden state has wrong width");
   if (!weights_ready_) throw StateError("weights are not initialised");
   require_context(layer);
@@ -1181,6 +1264,7 @@ void Engine::harness_step(int64_t layer, const float* x_host, int64_t x_len, flo
 
 void Engine::harness_step_device(int64_t layer, const float* x_dev, float* out_dev) {
   check_layer(layer);
+  if (f64_) throw StateError("the exact fp64 harness takes host doubles (hx_harness_step_f64)");
   if (mla_) throw StateError("the attention-only harness is DecodeHarness (GQA); MLA runs through decode_step");
   if (dist_mode_ != HX_POOL_LOCAL)
     throw StateError("the attention-only harness runs on a local pool; distributed pools use decode_step");
@@ -1392,6 +1476,145 @@ void Engine::profile_step(int64_t reps, double* ms) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// Exact fp64 harness (HX_KV_F64; exact64.cu)
+F64HarnessParams Engine::f64_params(int64_t layer) const {
+  F64HarnessParams p{};
+  p.k = k64_[layer];
+  p.v = v64_[layer];
+  p.qkv = d_qkv64_;
+  p.total = d_total_ + layer * B_;
+  p.qkv_stride = static_cast<int>((Qh_ + 2 * Kh_) * D_);
+  p.batch = B_;
+  p.tpa = tpa_;
+  p.kvp = kvp_;
+  p.chunk = chunk_;
+  p.kvh_per_slot = kvh_per_slot_;
+  p.q_per_slot = q_per_slot_;
+  p.group = G_;
+  p.w = static_cast<int>(D_);
+  p.rows_cap = rows_cap64_;
+  p.scale = 1.0 / std::sqrt(static_cast<double>(D_));
+  return p;
+}
+
+// x [B][H] -> d_qkv64_ [B][(Q+2K)*Hsz] (x^T W_q | x^T W_k | x^T W_v, attention.hpp:479-484, 531-539)
+void Engine::qkv_f64(int64_t layer, const double* x, int64_t x_len) {
+  check_layer(layer);
+  if (!f64_) throw StateError("the fp64 entry points need an exact harness (kv_dtype HX_KV_F64)");
+  if (x_len != static_cast<int64_t>(B_) * H_) throw std::invalid_argument("hidden state has wrong width");
+  if (!weights_ready_) throw StateError("weights are not initialised");
+  cuda_check(cudaMemcpyAsync(d_x64_, x, static_cast<size_t>(x_len) * sizeof(double), cudaMemcpyHostToDevice,
+                             stream_),
+             "x h2d");
+  cuda_check(launch_gemv_f64(d_x64_, B_, w64_[layer], static_cast<int>(H_), static_cast<int>((Qh_ + 2 * Kh_) * D_),
+                             d_qkv64_, stream_),
+             "f64 qkv");
+}
+
+void Engine::harness_step_f64(int64_t layer, const double* x, int64_t x_len, double* out, double* lse) {
+  check_layer(layer);
+  if (x_len != static_cast<int64_t>(B_) * H_) throw std::invalid_argument("hidden state has wrong width");
+  require_context(layer);
+  qkv_f64(layer, x, x_len);
+  const F64HarnessParams p = f64_params(layer);
+  cuda_check(launch_attn_f64_harness(p, 0, d_frag64_o_, d_frag64_lse_, stream_), "f64 shard attention");
+  cuda_check(launch_merge_f64_harness(p, d_frag64_o_, d_frag64_lse_, d_out64_, d_lse64_, stream_), "f64 merge");
+  const size_t ncols = static_cast<size_t>(p.qkv_stride);
+  for (int b = 0; b < B_; ++b) {  // attend-then-append (attention.hpp:504-508)
+    const double* kp = d_qkv64_ + b * ncols + Qh_ * D_;
+    cuda_check(launch_append_f64(p, kp, kp + Kh_ * D_, ncols, b, 1, static_cast<int>(Kh_), stream_), "f64 append");
+  }
+  cuda_check(cudaMemcpyAsync(out, d_out64_, static_cast<size_t>(B_) * Qh_ * D_ * sizeof(double),
+                             cudaMemcpyDeviceToHost, stream_),
+             "out d2h");
+  if (lse)
+    cuda_check(cudaMemcpyAsync(lse, d_lse64_, static_cast<size_t>(B_) * Qh_ * sizeof(double), cudaMemcpyDeviceToHost,
+                               stream_),
+               "lse d2h");
+  cuda_check(cudaStreamSynchronize(stream_), "f64 step sync");
+  for (int b = 0; b < B_; ++b) h_total_[static_cast<size_t>(layer * B_ + b)] += 1;
+  record_transcript(1);
+}
+
+void Engine::harness_reference_f64(int64_t layer, const double* x, int64_t x_len, double* out) {
+  check_layer(layer);
+  for (int b = 0; b < B_; ++b)  // reference_attention (attention.hpp:45)
+    if (h_total_[static_cast<size_t>(layer * B_ + b)] == 0)
+      throw std::invalid_argument("attention needs >= 1 context token");
+  qkv_f64(layer, x, x_len);
+  const F64HarnessParams p = f64_params(layer);
+  // one softmax per query head over its KV head's whole global context ([tpa][B][q_per_slot] = [B][Q] for tpa 1)
+  cuda_check(launch_attn_f64_harness(p, 1, d_frag64_o_, d_frag64_lse_, stream_), "f64 reference attention");
+  std::vector<double> frag(static_cast<size_t>(tpa_) * B_ * q_per_slot_ * D_);
+  cuda_check(cudaMemcpyAsync(frag.data(), d_frag64_o_, frag.size() * sizeof(double), cudaMemcpyDeviceToHost, stream_),
+             "reference d2h");
+  cuda_check(cudaStreamSynchronize(stream_), "f64 reference sync");
+  for (int g = 0; g < tpa_; ++g)
+    for (int b = 0; b < B_; ++b)
+      std::memcpy(out + (static_cast<size_t>(b) * Qh_ + static_cast<size_t>(g) * q_per_slot_) * D_,
+                  frag.data() + (static_cast<size_t>(g) * B_ + b) * q_per_slot_ * D_,
+                  static_cast<size_t>(q_per_slot_) * D_ * sizeof(double));
+}
+
+void Engine::append_projected_f64(int64_t layer, const double* x, int64_t x_len) {
+  for (int b = 0; b < B_; ++b)
+    if (h_total_[static_cast<size_t>(layer * B_ + b)] + 1 > cap_) throw std::invalid_argument("KV capacity exceeded");
+  qkv_f64(layer, x, x_len);
+  const F64HarnessParams p = f64_params(layer);
+  const size_t ncols = static_cast<size_t>(p.qkv_stride);
+  for (int b = 0; b < B_; ++b) {
+    const double* kp = d_qkv64_ + b * ncols + Qh_ * D_;
+    cuda_check(launch_append_f64(p, kp, kp + Kh_ * D_, ncols, b, 1, static_cast<int>(Kh_), stream_), "f64 append");
+  }
+  cuda_check(cudaStreamSynchronize(stream_), "f64 append sync");
+  for (int b = 0; b < B_; ++b) h_total_[static_cast<size_t>(layer * B_ + b)] += 1;
+}
+
+void Engine::append_kv_f64(int64_t layer, int64_t request, int64_t n, const double* k, const double* v) {
+  check_layer(layer);
+  if (!f64_) throw StateError("the fp64 entry points need an exact harness (kv_dtype HX_KV_F64)");
+  if (request < 0 || request >= B_) throw std::invalid_argument("request out of range");
+  if (n < 0) throw std::invalid_argument("token count must be >= 0");
+  if (h_total_[static_cast<size_t>(layer * B_ + request)] + n > cap_)
+    throw std::invalid_argument("KV capacity exceeded");
+  if (n == 0) return;
+  const size_t cnt = static_cast<size_t>(n * Kh_ * D_);
+  double *dk = nullptr, *dv = nullptr;
+  cuda_check(cudaMalloc(&dk, cnt * sizeof(double)), "append staging");
+  cuda_check(cudaMalloc(&dv, cnt * sizeof(double)), "append staging");
+  cuda_check(cudaMemcpyAsync(dk, k, cnt * sizeof(double), cudaMemcpyHostToDevice, stream_), "append h2d");
+  cuda_check(cudaMemcpyAsync(dv, v, cnt * sizeof(double), cudaMemcpyHostToDevice, stream_), "append h2d");
+  cuda_check(launch_append_f64(f64_params(layer), dk, dv, static_cast<size_t>(Kh_ * D_), static_cast<int>(request), n,
+                               static_cast<int>(Kh_), stream_),
+             "f64 append");
+  cuda_check(cudaStreamSynchronize(stream_), "append sync");
+  cudaFree(dk);
+  cudaFree(dv);
+  h_total_[static_cast<size_t>(layer * B_ + request)] += n;
+}
+
+void Engine::read_kv_f64(int64_t layer, int64_t request, int64_t rank, int64_t head, double* k, double* v) {
+  check_layer(layer);
+  if (!f64_) throw StateError("the fp64 entry points need an exact harness (kv_dtype HX_KV_F64)");
+  if (head < 0 || head >= Kh_) throw std::invalid_argument("kv head out of range");
+  const int64_t n = effective_tokens(layer, request, rank);
+  const int grp = static_cast<int>(head / kvh_per_slot_), kvh = static_cast<int>(head % kvh_per_slot_);
+  if (n == 0) return;
+  double *dk = nullptr, *dv = nullptr;
+  const size_t cnt = static_cast<size_t>(n * D_);
+  cuda_check(cudaMalloc(&dk, cnt * sizeof(double)), "read staging");
+  cuda_check(cudaMalloc(&dv, cnt * sizeof(double)), "read staging");
+  cuda_check(launch_read_f64(f64_params(layer), grp * kvp_ + static_cast<int>(rank), static_cast<int>(request), kvh,
+                             n, dk, dv, stream_),
+             "f64 read");
+  cuda_check(cudaMemcpyAsync(k, dk, cnt * sizeof(double), cudaMemcpyDeviceToHost, stream_), "read d2h");
+  cuda_check(cudaMemcpyAsync(v, dv, cnt * sizeof(double), cudaMemcpyDeviceToHost, stream_), "read d2h");
+  cuda_check(cudaStreamSynchronize(stream_), "read sync");
+  cudaFree(dk);
+  cudaFree(dv);
+}
+
 void Engine::info(hx_engine_info* o) const {
   std::memset(o, 0, sizeof(*o));
   o->kv_bytes_per_layer = static_cast<int64_t>(n_slots_) * B_ * kvh_per_slot_ * page_cap_ * page_bytes_;
@@ -1418,6 +1641,66 @@ void Engine::info(hx_engine_info* o) const {
   o->head_dim_padded = DP_;
   o->kv_dtype = kv8_ ? HX_KV_FP8_E4M3 : HX_KV_BF16;
   o->w_dtype = w8_ ? HX_W_FP8_E4M3 : HX_W_BF16;
+  o->comm_ranks = transport_ ? transport_->world() : 1;
+  o->nccl_version = transport_ ? transport_->nccl_version() : 0;
 }
 
+}  // namespace hx
+
+// ---------------------------------------------------------------------------
+// Free functions (fp64, current device): the reference's primitives on
+// caller-supplied operands (attention.hpp:43-78, 118-137).
+namespace hx {
+namespace {
+struct DevBuf {
+  void* p = nullptr;
+  explicit DevBuf(size_t bytes) { cuda_check(cudaMalloc(&p, std::max<size_t>(bytes, 16)), "primitive buffer"); }
+  ~DevBuf() { cudaFree(p); }
+  double* d() const { return static_cast<double*>(p); }
+};
+void require_blackwell() {
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  cudaDeviceProp prop{};
+  cuda_check(cudaGetDeviceProperties(&prop, dev), "cudaGetDeviceProperties");
+  if (prop.major < 10) throw CudaError("device is not sm_100 class (Blackwell); this build targets sm_100a only");
+}
+}  // namespace
+
+void attention_f64(const double* q, int64_t nq, const double* keys, const double* values, int64_t tokens,
+                   int64_t width, double* out, double* lse) {
+  if (nq < 1 || tokens < 0 || width < 1) throw std::invalid_argument("attention operand sizes must be >= 1");
+  if (width > kF64MaxWidth) throw std::invalid_argument("attention width > 512 is not supported");
+  require_blackwell();
+  const size_t qn = static_cast<size_t>(nq * width), kn = static_cast<size_t>(tokens * width);
+  DevBuf dq(qn * 8), dk(kn * 8), dv(kn * 8), dout(qn * 8), dl(static_cast<size_t>(nq) * 8);
+  cuda_check(cudaMemcpy(dq.d(), q, qn * 8, cudaMemcpyHostToDevice), "q h2d");
+  if (kn) {
+    cuda_check(cudaMemcpy(dk.d(), keys, kn * 8, cudaMemcpyHostToDevice), "keys h2d");
+    cuda_check(cudaMemcpy(dv.d(), values, kn * 8, cudaMemcpyHostToDevice), "values h2d");
+  }
+  cuda_check(launch_attn_f64_plain(dq.d(), static_cast<int>(nq), dk.d(), dv.d(), tokens, static_cast<int>(width),
+                                   dout.d(), dl.d(), nullptr),
+             "f64 attention");
+  cuda_check(cudaMemcpy(out, dout.d(), qn * 8, cudaMemcpyDeviceToHost), "out d2h");
+  if (lse) cuda_check(cudaMemcpy(lse, dl.d(), static_cast<size_t>(nq) * 8, cudaMemcpyDeviceToHost), "lse d2h");
+}
+
+void merge_f64(int64_t nf, int64_t width, const double* outs, const double* lses, double* out, double* lse) {
+  if (nf < 1) throw std::invalid_argument("merge needs >= 1 fragment");
+  if (width < 0) throw std::invalid_argument("fragment widths differ");
+  bool any = false;
+  for (int64_t i = 0; i < nf; ++i) any |= lses[i] != -INFINITY;
+  if (!any) throw std::invalid_argument("all fragments empty: nothing to merge");
+  require_blackwell();
+  const size_t on = static_cast<size_t>(nf * width);
+  DevBuf dout(on * 8), dl(static_cast<size_t>(nf) * 8), dres(static_cast<size_t>(width) * 8), dlse(8);
+  if (on) cuda_check(cudaMemcpy(dout.d(), outs, on * 8, cudaMemcpyHostToDevice), "outs h2d");
+  cuda_check(cudaMemcpy(dl.d(), lses, static_cast<size_t>(nf) * 8, cudaMemcpyHostToDevice), "lses h2d");
+  cuda_check(launch_merge_f64_plain(dout.d(), dl.d(), static_cast<int>(nf), static_cast<int>(width), dres.d(),
+                                    dlse.d(), nullptr),
+             "f64 merge");
+  if (width) cuda_check(cudaMemcpy(out, dres.d(), static_cast<size_t>(width) * 8, cudaMemcpyDeviceToHost), "out d2h");
+  if (lse) cuda_check(cudaMemcpy(lse, dlse.d(), 8, cudaMemcpyDeviceToHost), "lse d2h");
+}
 }  // namespace hx

@@ -36,6 +36,12 @@ struct Message {
   int64_t kind, src, dst, payload, lse;
 };
 
+// Free-function numerics in fp64 on the current device (exact64.cu kernels):
+// partial_head_attention / merge_head_fragments on caller-supplied host operands.
+void attention_f64(const double* q, int64_t nq, const double* keys, const double* values, int64_t tokens,
+                   int64_t width, double* out, double* lse);
+void merge_f64(int64_t nf, int64_t width, const double* outs, const double* lses, double* out, double* lse);
+
 struct GemvPlan {
   GemvParams p{};
   int xmode = 0, emode = 0;  // xmode: 1 = RMSNorm consumer (scale y by the row's rsqrt(mean x^2))
@@ -60,6 +66,14 @@ class Engine {
   void read_kv(int64_t layer, int64_t request, int64_t rank, int64_t head, float* k, float* v);
 
   void harness_step(int64_t layer, const float* x_host, int64_t x_len, float* out, float* lse);
+  // Exact fp64 harness (kv_dtype HX_KV_F64, exact64.cu): DecodeHarness<double>
+  // step / reference / append_projected and caller rows in double.
+  void harness_step_f64(int64_t layer, const double* x, int64_t x_len, double* out, double* lse);
+  void harness_reference_f64(int64_t layer, const double* x, int64_t x_len, double* out);
+  void append_projected_f64(int64_t layer, const double* x, int64_t x_len);
+  void append_kv_f64(int64_t layer, int64_t request, int64_t n, const double* k, const double* v);
+  void read_kv_f64(int64_t layer, int64_t request, int64_t rank, int64_t head, double* k, double* v);
+  bool exact_f64() const { return f64_; }
   void harness_step_device(int64_t layer, const float* x_dev, float* out_dev);
   void decode_step(const int32_t* tokens, int32_t* next, float* logits, float* hidden);
   void decode_step_device(const int32_t* tokens_dev, int32_t* next_dev);
@@ -104,11 +118,19 @@ class Engine {
   bool loopback_ = false;
   bool kv8_ = false;  // FP8 e4m3 GQA pages (hx_runtime_config.kv_dtype)
   bool tc_ = false;   // batch > 16: tcgen05 GEMVs (weights / x-fragments in their operand images)
-  bool w8_ = false;
+  bool w8_ = false;   // FP8 e4m3 GEMV weights (hx_runtime_config.w_dtype), per-output pow2 scales
   // local pool with KVP = 1 (one fragment per query head): the split reduce
   // writes the O-projection's x-fragments itself, the O-proj epilogue bumps
   // the token totals, and the merge kernel is not launched
-  bool one_src_merge_ = false;   // FP8 e4m3 GEMV weights (hx_runtime_config.w_dtype), per-output pow2 scales
+  bool one_src_merge_ = false;
+  // exact fp64 harness (HX_KV_F64): fp64 shards, weights and projections (exact64.cu)
+  bool f64_ = false;
+  int64_t rows_cap64_ = 0;
+  std::vector<double*> k64_, v64_, w64_;  // per layer: K/V shards, [H][(Q+2K)*Hsz] weights
+  double *d_x64_ = nullptr, *d_qkv64_ = nullptr, *d_frag64_o_ = nullptr, *d_frag64_lse_ = nullptr;
+  double *d_out64_ = nullptr, *d_lse64_ = nullptr;
+  F64HarnessParams f64_params(int64_t layer) const;
+  void qkv_f64(int64_t layer, const double* x, int64_t x_len);
   int xf16_() const { return w8_ ? 1 : 0; }  // x-fragments as f16 terms (xfrag.cuh)
   std::map<const void*, float*> wscale_;     // FP8 weight block -> its [Npad] scales
   int DP_, G_, q_rows_, q_chunks_, kvh_per_slot_, q_per_slot_, n_slots_, slot_base_;

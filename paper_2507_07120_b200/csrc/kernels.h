@@ -16,6 +16,10 @@ namespace hx {
 // 1, 2, 4 or 8 groups, so writers, readers and allocations use the padded count.
 HX_HD inline int xf_nb8(int batch) { return batch <= 8 ? 1 : (batch <= 16 ? 2 : (batch <= 32 ? 4 : 8)); }
 
+// Largest KVP width the fragment merges handle (merge.cuh): validate_config's
+// max_gpus (types.hpp:63).
+constexpr int kMaxKvp = 64;
+
 
 // Programmatic dependent launch for the decode-step kernels (set by the engine).
 void set_pdl(bool on);
@@ -226,5 +230,35 @@ cudaError_t launch_moe_route(const float* logits, int batch, int n_experts, int 
 // Residual add of an all-reduced partial product + RMSNorm statistics.
 cudaError_t launch_residual_add(float* x, const float* part, int batch, int hidden, float* ss_part,
                                 uint8_t* xf, cudaStream_t s, int xf16 = 0);
+
+// ---------------------------------------------------------------- exact fp64 harness (exact64.cu)
+// DecodeHarness<double> numerics on the GPU for the drop-in C++ API: fp64 KV
+// shards [slot][request][kv head][rows_cap][w] (row-major), fp64 weights,
+// projections and merges. Widths up to kF64MaxWidth.
+constexpr int kF64MaxWidth = 512;
+struct F64HarnessParams {
+  double* k;            // K shards
+  double* v;            // V shards
+  const double* qkv;    // [batch][qkv_stride] projections: query heads at column head*w
+  int* total;           // [batch] tokens appended so far (this layer)
+  int qkv_stride, batch, tpa, kvp, chunk, kvh_per_slot, q_per_slot, group, w;
+  long long rows_cap;   // rows per (slot, request, kv head)
+  double scale;         // 1/sqrt(w) (logit_scale, attention.hpp:35-38)
+};
+cudaError_t launch_attn_f64_plain(const double* q, int nq, const double* K, const double* V, long long n, int w,
+                                  double* out, double* lse, cudaStream_t s);
+cudaError_t launch_merge_f64_plain(const double* outs, const double* lses, int nf, int w, double* out, double* lse,
+                                   cudaStream_t s);
+cudaError_t launch_gemv_f64(const double* x, int B, const double* W, int K, int N, double* y, cudaStream_t s);
+// mono = 0: per-rank fragments [tpa*kvp][batch][q_per_slot]; 1: one softmax over the group, [tpa][batch][q_per_slot]
+cudaError_t launch_attn_f64_harness(const F64HarnessParams& p, int mono, double* frag_o, double* frag_lse,
+                                    cudaStream_t s);
+cudaError_t launch_merge_f64_harness(const F64HarnessParams& p, const double* frag_o, const double* frag_lse,
+                                     double* out, double* lse, cudaStream_t s);
+// append n token rows (ksrc/vsrc + t*src_stride: [kv_heads][w]) to request b, then total[b] += n
+cudaError_t launch_append_f64(const F64HarnessParams& p, const double* ksrc, const double* vsrc, size_t src_stride,
+                              int b, long long n, int kv_heads, cudaStream_t s);
+cudaError_t launch_read_f64(const F64HarnessParams& p, int slot, int b, int kvh, long long n, double* k, double* v,
+                            cudaStream_t s);
 
 }  // namespace hx

@@ -15,6 +15,7 @@ namespace hx {
 // ---------------------------------------------------------------- merge (harness output)
 // out[b][head][d] = canonical LSE merge over kvp rank fragments
 // (merge_fragments / merge_head_fragments, attention.hpp:118-175).
+template <int MAXK>
 __global__ void merge_out_kernel(const float* frag_o, const float* frag_lse, int batch,
                                  int q_heads, int q_per_slot, int kvp, int head_dim, int dp,
                                  float* out, float* out_lse, int* bump_total) {
@@ -26,43 +27,46 @@ __global__ void merge_out_kernel(const float* frag_o, const float* frag_lse, int
   if (warp >= batch * q_heads) return;
   const int b = warp / q_heads, head = warp - b * q_heads;
   const int grp = head / q_per_slot, qi = head - grp * q_per_slot;
-  float lse[8];
-  int ord[8];
-  for (int r = 0; r < kvp; ++r) {
+  float lse[MAXK], o[MAXK];
+  for (int r = 0; r < kvp; ++r)
     lse[r] = frag_lse[(static_cast<size_t>(grp * kvp + r) * batch + b) * q_per_slot + qi];
-    ord[r] = r;
-  }
-  for (int i = 1; i < kvp; ++i) {
-    const int o = ord[i];
-    int j = i - 1;
-    while (j >= 0 && lse[ord[j]] < lse[o]) {
-      ord[j + 1] = ord[j];
-      --j;
-    }
-    ord[j + 1] = o;
-  }
-  const float m = lse[ord[0]];
-  float z = 0.f;
-  for (int i = 0; i < kvp; ++i)
-    if (lse[ord[i]] != -INFINITY) z += expf(lse[ord[i]] - m);
   for (int d = lane; d < head_dim; d += 32) {
-    float acc = 0.f;
-    for (int i = 0; i < kvp; ++i) {
-      const int r = ord[i];
-      if (lse[r] == -INFINITY) continue;
-      const float w = expf(lse[r] - m);
-      acc += w * frag_o[((static_cast<size_t>(grp * kvp + r) * batch + b) * q_per_slot + qi) * dp + d];
-    }
-    out[(static_cast<size_t>(b) * q_heads + head) * head_dim + d] = m == -INFINITY ? 0.f : acc / z;
+    for (int r = 0; r < kvp; ++r)
+      o[r] = frag_o[((static_cast<size_t>(grp * kvp + r) * batch + b) * q_per_slot + qi) * dp + d];
+    out[(static_cast<size_t>(b) * q_heads + head) * head_dim + d] = merge_sources<MAXK>(lse, o, kvp);
   }
-  if (lane == 0 && out_lse) out_lse[b * q_heads + head] = m == -INFINITY ? m : m + logf(z);
+  if (lane == 0 && out_lse) {
+    // lse = m + ln(sum of weights); the weights' sum does not depend on how lse ties are ordered
+    float m = -INFINITY;
+    for (int r = 0; r < kvp; ++r) m = fmaxf(m, lse[r]);
+    float z = 0.f;
+    if (m != -INFINITY) {
+      // same descending-lse order as merge_sources
+      int ord[MAXK];
+      for (int r = 0; r < kvp; ++r) ord[r] = r;
+      for (int i = 1; i < kvp; ++i) {
+        const int v = ord[i];
+        int j = i - 1;
+        while (j >= 0 && merge_before(lse[v], 0.f, v, lse[ord[j]], 0.f, ord[j])) {
+          ord[j + 1] = ord[j];
+          --j;
+        }
+        ord[j + 1] = v;
+      }
+      for (int i = 0; i < kvp; ++i)
+        if (lse[ord[i]] != -INFINITY) z += __expf(lse[ord[i]] - m);
+    }
+    out_lse[b * q_heads + head] = m == -INFINITY ? m : m + logf(z);
+  }
 }
 
 cudaError_t launch_merge_out(const float* frag_o, const float* frag_lse, int batch, int q_heads,
                              int q_per_slot, int kvp, int head_dim, int dp, float* out,
                              float* out_lse, int* bump_total, cudaStream_t stream) {
+  if (kvp > kMaxKvp) return cudaErrorInvalidValue;
   const int warps = batch * q_heads;
-  return launch_k(merge_out_kernel, dim3((warps * 32 + 255) / 256), dim3(256), 0, stream, frag_o, frag_lse,
+  auto k = kvp <= 8 ? merge_out_kernel<8> : merge_out_kernel<kMaxKvp>;
+  return launch_k(k, dim3((warps * 32 + 255) / 256), dim3(256), 0, stream, frag_o, frag_lse,
                   batch, q_heads, q_per_slot, kvp, head_dim, dp, out, out_lse, bump_total);
 }
 
@@ -565,6 +569,7 @@ cudaError_t launch_xprep_plain(const float* x, int batch, int K, int x_stride, u
 }
 
 
+template <int MAXK>
 __global__ void xprep_merge_local_kernel(const float* frag_o, const float* frag_lse, int batch, int q_per_slot,
                                          int kvp, int head_dim, int dp, int K, uint8_t* xf, int* bump_total,
                                          float* plain, int xf16) {
@@ -577,16 +582,16 @@ __global__ void xprep_merge_local_kernel(const float* frag_o, const float* frag_
   const int b = static_cast<int>(i / K), k = static_cast<int>(i % K);
   const int head = k / head_dim, d = k - head * head_dim;
   const int grp = head / q_per_slot, qi = head - grp * q_per_slot;
-  float lse[8], o[8];
+  float lse[MAXK], o[MAXK];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
+  for (int r = 0; r < MAXK; ++r) {
     if (r < kvp) {
       const size_t f = (static_cast<size_t>(grp * kvp + r) * batch + b) * q_per_slot + qi;
       lse[r] = frag_lse[f];
       o[r] = frag_o[f * dp + d];
     }
   }
-  const float v = merge_sources(lse, o, kvp);
+  const float v = merge_sources<MAXK>(lse, o, kvp);
   if (plain)
     plain[i] = v;
   else
@@ -595,11 +600,13 @@ __global__ void xprep_merge_local_kernel(const float* frag_o, const float* frag_
 cudaError_t launch_xprep_merge_local(const float* frag_o, const float* frag_lse, int batch, int q_per_slot,
                                      int kvp, int head_dim, int dp, int K, uint8_t* xf, int* bump_total,
                                      cudaStream_t s, float* plain, int xf16) {
+  if (kvp > kMaxKvp) return cudaErrorInvalidValue;
   const long long n = static_cast<long long>(batch) * K;
-  return launch_k(xprep_merge_local_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, frag_o,
+  return launch_k(kvp <= 8 ? xprep_merge_local_kernel<8> : xprep_merge_local_kernel<kMaxKvp>, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, frag_o,
                   frag_lse, batch, q_per_slot, kvp, head_dim, dp, K, xf, bump_total, plain, xf16);
 }
 
+template <int MAXK>
 __global__ void xprep_merge_recv_kernel(const float* recv, int batch, int kvp, int chunk, int slice, int exch_rank,
                                         int head_dim, uint8_t* xf, int* bump_total, float* plain, int xf16) {
   griddep_wait();
@@ -610,16 +617,16 @@ __global__ void xprep_merge_recv_kernel(const float* recv, int batch, int kvp, i
   const int b = static_cast<int>(i / slice), k = static_cast<int>(i % slice);
   const int first = (exch_rank * slice) / head_dim;
   const int head = (exch_rank * slice + k) / head_dim;
-  float lse[8], o[8];
+  float lse[MAXK], o[MAXK];
 #pragma unroll
-  for (int r = 0; r < 8; ++r) {
+  for (int r = 0; r < MAXK; ++r) {
     if (r < kvp) {
       const float* src = recv + (static_cast<size_t>(r) * batch + b) * chunk;
       lse[r] = src[slice + head - first];
       o[r] = src[k];
     }
   }
-  const float v = merge_sources(lse, o, kvp);
+  const float v = merge_sources<MAXK>(lse, o, kvp);
   if (plain)
     plain[i] = v;
   else
@@ -628,8 +635,9 @@ __global__ void xprep_merge_recv_kernel(const float* recv, int batch, int kvp, i
 cudaError_t launch_xprep_merge_recv(const float* recv, int batch, int kvp, int chunk, int slice, int exch_rank,
                                     int head_dim, uint8_t* xf, int* bump_total, cudaStream_t s, float* plain,
                                     int xf16) {
+  if (kvp > kMaxKvp) return cudaErrorInvalidValue;
   const long long n = static_cast<long long>(batch) * slice;
-  return launch_k(xprep_merge_recv_kernel, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, recv,
+  return launch_k(kvp <= 8 ? xprep_merge_recv_kernel<8> : xprep_merge_recv_kernel<kMaxKvp>, dim3(static_cast<unsigned>((n + 255) / 256)), dim3(256), 0, s, recv,
                   batch, kvp, chunk, slice, exch_rank, head_dim, xf, bump_total, plain, xf16);
 }
 }  // namespace hx

@@ -15,10 +15,49 @@ import numpy as np
 from ._lib import (KV_DTYPES, W_DTYPES, EngineInfo, ModelConfig, ParallelConfig, RuntimeConfig, check, lib)
 
 _fp = C.POINTER(C.c_float)
+_dp = C.POINTER(C.c_double)
 
 
 def _f32(a):
     return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def _f64(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+# ---------------------------------------------------------------------------- free functions (fp64, GPU)
+def partial_head_attention(q, keys, values):
+    """partial_head_attention (attention.hpp:65-78) for one query [w] or a group
+    [nq, w] over keys/values [tokens, w]: (partial_out, lse); empty -> (0, -inf)."""
+    q, k, v = _f64(q), _f64(keys), _f64(values)
+    single = q.ndim == 1
+    q2 = q.reshape(1, -1) if single else q
+    nq, w = q2.shape
+    n = k.shape[0] if k.size else 0
+    out, lse = np.zeros((nq, w)), np.zeros(nq)
+    check(lib().hx_attention_f64(q2.ctypes.data_as(_dp), nq, k.ctypes.data_as(_dp), v.ctypes.data_as(_dp), n, w,
+                                 out.ctypes.data_as(_dp), lse.ctypes.data_as(_dp)))
+    return (out[0], float(lse[0])) if single else (out, lse)
+
+
+def reference_attention(q, keys, values):
+    """reference_attention (attention.hpp:43-53): throws on an empty context."""
+    k = _f64(keys)
+    if k.shape[0] == 0:
+        raise ValueError("attention needs >= 1 context token")
+    return partial_head_attention(q, keys, values)[0]
+
+
+def merge_head_fragments(outs, lses):
+    """merge_head_fragments (attention.hpp:118-137): outs [n, w], lses [n] -> (out, lse)."""
+    o, l = _f64(outs), _f64(lses)
+    n = l.size
+    w = o.shape[1] if o.ndim == 2 else 0
+    out, lse = np.zeros(w), np.zeros(1)
+    check(lib().hx_merge_f64(n, w, o.ctypes.data_as(_dp), l.ctypes.data_as(_dp), out.ctypes.data_as(_dp),
+                             lse.ctypes.data_as(_dp)))
+    return out, float(lse[0])
 
 
 class Rng:
@@ -121,6 +160,7 @@ class DecodeHarness(_Engine):
                          attention_only=1)
         super().__init__(mc, tpa, kvp, chunk_size, batch, capacity, device, use_graphs=False, kv_dtype=kv_dtype)
         self._tpa, self._kvp = tpa, kvp
+        self.exact = kv_dtype == "f64"  # fp64 weights / shards / merges (DecodeHarness<double> precision)
         self._check(lib().hx_init_weights_mt19937(self._h, seed))
 
     def pool(self):
@@ -140,6 +180,15 @@ class DecodeHarness(_Engine):
         """DecodeHarness::step (attention.hpp:460-510) for every request.
 
         x: [hidden] (batch 1) or [batch, hidden]; returns [Q, Hsz] or [batch, Q, Hsz]."""
+        if self.exact:
+            x = _f64(x)
+            out = np.zeros((self.batch, self.dims.query_heads, self.dims.head_size))
+            lse = np.zeros((self.batch, self.dims.query_heads))
+            self._check(lib().hx_harness_step_f64(self._h, 0, x.ctypes.data_as(_dp), x.size,
+                                                  out.ctypes.data_as(_dp), lse.ctypes.data_as(_dp)))
+            if x.ndim == 1 and self.batch == 1:
+                out, lse = out[0], lse[0]
+            return (out, lse) if return_lse else out
         x = _f32(x)
         single = x.ndim == 1
         out = np.zeros((self.batch, self.dims.query_heads, self.dims.head_size), dtype=np.float32)
@@ -149,6 +198,19 @@ class DecodeHarness(_Engine):
         if single and self.batch == 1:
             out, lse = out[0], lse[0]
         return (out, lse) if return_lse else out
+
+    def reference(self, x):
+        """DecodeHarness::reference (attention.hpp:514-529): monolithic attention over
+        the global context, no append (exact harness)."""
+        x = _f64(x)
+        out = np.zeros((self.batch, self.dims.query_heads, self.dims.head_size))
+        self._check(lib().hx_harness_reference_f64(self._h, 0, x.ctypes.data_as(_dp), x.size, out.ctypes.data_as(_dp)))
+        return out[0] if x.ndim == 1 and self.batch == 1 else out
+
+    def append_projected(self, x):
+        """DecodeHarness::append_projected (attention.hpp:531-539) (exact harness)."""
+        x = _f64(x)
+        self._check(lib().hx_append_projected_f64(self._h, 0, x.ctypes.data_as(_dp), x.size))
 
     # ShardedKVCache views (attention.hpp:286-309)
     def total_tokens(self, request=0):
@@ -162,6 +224,11 @@ class DecodeHarness(_Engine):
 
     def context(self, rank, head, request=0):
         n = self.effective_tokens(rank, request)
+        if self.exact:
+            k, v = np.zeros((n, self.dims.head_size)), np.zeros((n, self.dims.head_size))
+            self._check(lib().hx_read_kv_f64(self._h, 0, request, rank, head, k.ctypes.data_as(_dp),
+                                             v.ctypes.data_as(_dp)))
+            return k, v
         k = np.zeros((n, self.dims.head_size), dtype=np.float32)
         v = np.zeros((n, self.dims.head_size), dtype=np.float32)
         self._check(lib().hx_read_kv(self._h, 0, request, rank, head, k.ctypes.data_as(_fp), v.ctypes.data_as(_fp)))

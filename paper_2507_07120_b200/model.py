@@ -399,6 +399,8 @@ class HelixDecoder(_Engine):
 
     def step(self, tokens, want_logits=False, want_hidden=False):
         t = np.ascontiguousarray(tokens, dtype=np.int32)
+        if t.shape != (self.batch,):  # hx_decode_step reads exactly `batch` ids from the pointer
+            raise ValueError(f"tokens must have shape ({self.batch},), got {t.shape}")
         nxt = np.zeros(self.batch, dtype=np.int32)
         logits = np.zeros((self.batch, self.vocab_local), dtype=np.float32) if want_logits else None
         hidden = np.zeros((self.layers + 1, self.batch, self.spec.hidden_dim), dtype=np.float32) \

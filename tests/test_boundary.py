@@ -106,6 +106,7 @@ int main(void) {
     ((4, 2, 8), 2, 3, "divide the hidden width"),
     ((4, 2, 8), 0, 1, "tpa and kvp must be >= 1"),
     ((4, 2, 8), 1, 0, "cache dimensions must be >= 1"),
+    ((32, 2, 8), 1, 128, "kvp > 64 is not supported"),
 ])
 def test_reference_validation_without_gpu(dims, tpa, kvp, msg):
     """Same checks, order and messages as attention.hpp:239-240, 431-437 --

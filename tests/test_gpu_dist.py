@@ -19,7 +19,8 @@ def rel_err(got, want):
     return float(np.abs(got - want).max() / max(1e-12, np.abs(want).max()))
 
 
-@pytest.mark.parametrize("tpa,kvp,hopb", [(1, 2, False), (2, 2, False), (1, 4, True), (2, 1, False), (2, 2, True)])
+@pytest.mark.parametrize("tpa,kvp,hopb", [(1, 2, False), (2, 2, False), (1, 4, True), (2, 1, False), (2, 2, True),
+                                              (1, 16, False)])
 def test_loopback_pool_matches_oracle(tpa, kvp, hopb):
     import paper_2507_07120_b200 as P
     from paper_2507_07120_b200.model import Loopback
@@ -184,3 +185,66 @@ def test_nccl_pool_single_rank_matches_local(hopb, graphs):
     assert rel_err(outs[1][2], outs[0][2]) <= 1e-5
     assert rel_err(outs[1][1], outs[0][1]) <= 1e-5
     np.testing.assert_array_equal(outs[1][0], outs[0][0])
+
+
+def _gpu_count():
+    try:
+        import torch
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def _nccl_pool_rank(rank, n, uid, hopb, graphs, q):
+    """One process = one GPU = one rank of the KVP = n pool (HX_POOL_NCCL)."""
+    try:
+        import paper_2507_07120_b200 as P
+        H, Q, K, D, F, L, V, B = 256, 8, 2, 32, 512, 2, 1000, 3
+        spec = P.model.ModelSpec("test", L, H, Q, K, D, F, 3, "gqa", 0, vocab=V)
+        g = P.HelixDecoder(spec, tpa=1, kvp=n, batch=B, capacity=400, layers=L, vocab=V, device=rank,
+                           use_graphs=graphs, hopb=hopb, pool=1, rank=rank, nccl_id=uid)
+        assert g.info()["comm_ranks"] == n
+        g.init_weights(77, qkv="hash")
+        g.fill_kv_hash(300, 77)
+        out = [g.step(np.array([3, 4, 5]), want_logits=True, want_hidden=True)]
+        out.append(g.step(out[0][0], want_logits=True, want_hidden=True))
+        g.close()
+        q.put((rank, out, None))
+    except Exception as ex:  # reported to the parent
+        q.put((rank, None, repr(ex)))
+
+
+@pytest.mark.skipif(_gpu_count() < 2, reason="needs >= 2 GPUs (one process per GPU)")
+@pytest.mark.parametrize("hopb,graphs", [(False, True), (True, False), (True, True)])
+def test_nccl_pool_two_gpus_matches_oracle(hopb, graphs):
+    """A real two-process NCCL pool (KVP = 2, TPF = 2): grouped send/recv
+    all-to-all of the fragment slices between GPUs, ncclAllReduce of the TP
+    partials, vocab-sharded argmax -- against the oracle's sharded decode."""
+    import multiprocessing as mp
+    from paper_2507_07120_b200.model import nccl_unique_id
+    n = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    uid = nccl_unique_id()
+    procs = [ctx.Process(target=_nccl_pool_rank, args=(r, n, uid, hopb, graphs, q)) for r in range(n)]
+    [p.start() for p in procs]
+    res = {}
+    for _ in range(n):
+        r, out, err = q.get(timeout=300)
+        assert err is None, (r, err)
+        res[r] = out
+    [p.join(timeout=60) for p in procs]
+    H, Q, K, D, F, L, V, B = 256, 8, 2, 32, 512, 2, 1000, 3
+    o = O.Model(H, Q, K, D, F, L, V, tpa=1, kvp=n, chunk=16, batch=B, seed=77, qkv_hash=True, bf16=True)
+    for l in range(L):
+        for b in range(B):
+            o.grow_hash(l, b, 300)
+    tokens = np.array([3, 4, 5])
+    for step in range(2):
+        lo, ho, no = o.step(tokens)
+        tol = 2e-3 if step == 0 else 2e-2
+        for r in range(n):
+            nxt, logits, hidden = res[r][step]
+            assert rel_err(hidden, ho) <= tol, (r, step, rel_err(hidden, ho))
+        np.testing.assert_array_equal(res[1][step][2], res[0][step][2])
+        tokens = no

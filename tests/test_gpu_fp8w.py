@@ -161,16 +161,19 @@ def test_fp8_weights_mla_matches_oracle(moe):
         for b in range(B):
             o.grow_hash(l, b, ctx)
     tokens = np.array([1, 2, 3])
+    compared = 0
     for step in range(2):
         nxt, logits, hidden = g.step(tokens, want_logits=True, want_hidden=True)
         lo, ho, no = o.step(tokens)
         if moe and not o.route_gaps().min() > 1e-4:
-            break
+            break  # a router near-tie: the two sides may legally diverge from here
         tol = 5e-3 if step == 0 else 2e-2
         e_h, e_l = rel_err(hidden, ho), rel_err(logits, lo)
         print(f"mla moe={moe} step={step} hidden={e_h:.2e} logits={e_l:.2e}")
         assert e_h <= tol and e_l <= tol
+        compared += 1
         tokens = no
+    assert compared >= 1, "router near-tie on the first step at this seed; pick another"
     g.close()
 
 

@@ -138,3 +138,27 @@ def test_batched_requests_are_independent(P):
             k_gpu, v_gpu = appended_rows(g, case, b)
             want, _ = oracles[b].step_append(x[b].astype(np.float64), k_gpu, v_gpu)
             assert rel_err(got[b], want) <= TOL_ARITH
+
+
+@pytest.mark.parametrize("dims,tpa,kvp,chunk,ctx", [
+    ((16, 4, 16), 1, 16, 4, 300),     # kvp = 16: past the register-resident merge (MAXK = 8)
+    ((32, 8, 16), 2, 16, 16, 700),    # two TPA groups x 16 KVP ranks = 32 slots
+    ((64, 2, 8), 1, 64, 1, 200),      # kvp = 64 = validate_config max_gpus, chunk 1, empty ranks
+])
+def test_wide_kvp_local_pool_matches_oracle(P, dims, tpa, kvp, chunk, ctx):
+    """kvp > 8 merges (local memory, merge.cuh MAXK = 64) against the oracle,
+    including ranks whose shard is still empty (lse = -inf)."""
+    g = P.DecodeHarness(dims, tpa, kvp, chunk, 77, batch=1, capacity=ctx + 8)
+    o = O.Harness(*dims, tpa, kvp, chunk, 77, bf16=True)
+    rg, ro = P.Rng(5), O.Rng(5)
+    g.grow_random(ctx, rg)
+    o.grow_random(ctx, ro)
+    case = {"chunk": chunk, "kvp": kvp, "kv_heads": dims[1]}
+    rx = np.random.default_rng(11)
+    for _ in range(3):
+        x = rx.uniform(-1, 1, size=dims[0] * dims[2]).astype(np.float32).astype(np.float64)
+        got = g.step(x)
+        k_gpu, v_gpu = appended_rows(g, case)
+        want, _ = o.step_append(x, k_gpu, v_gpu)
+        assert rel_err(got, want) <= TOL_ARITH
+    assert [g.effective_tokens(r) for r in range(kvp)] == [o.effective_tokens(r) for r in range(kvp)]

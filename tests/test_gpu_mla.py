@@ -94,8 +94,9 @@ def test_mla_with_moe_matches_oracle():
     tokens = np.array([1, 2, 3])
     nxt, logits, hidden = g.step(tokens, want_logits=True, want_hidden=True)
     lo, ho, no = o.step(tokens)
-    if o.route_gaps().min() > 1e-4:
-        assert rel_err(hidden, ho) <= 5e-3 and rel_err(logits, lo) <= 5e-3
+    # seed 11 has clear router margins (min top-k gap 0.11): the comparison always runs
+    assert o.route_gaps().min() > 1e-4, "router near-tie at this seed; pick another"
+    assert rel_err(hidden, ho) <= 5e-3 and rel_err(logits, lo) <= 5e-3
 
 
 @pytest.mark.parametrize("kvp", [2, 4])
