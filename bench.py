@@ -109,6 +109,20 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(rows)}
 
 
+def step_bytes_per_gpu(spec, batch, seq_global, kvp, layers, kv_elem=2, w_elem=2):
+    """Algorithmic HBM bytes one GPU of a TPA = 1 x KVP = kvp Helix pool (TPF = kvp)
+    streams for `layers` layers: KV = the reference's kv_read_time x mem_bw
+    (roofline.hpp:17-27); weights = weight_read_time x mem_bw (roofline.hpp:33-48:
+    QKV replicated per KVP rank, FFN over TPF) with the O-projection sharded over
+    the pool as latency.cpp:85-94 has it (the roofline header counts it whole).
+    Pinned to the reference's library by tests/test_analytic.py."""
+    from paper_2507_07120_b200 import analytic as A
+    kv = A.kv_bytes(spec, batch, seq_global, 1, kvp, kv_elem) * layers
+    o_full = spec.hidden_dim * spec.query_heads * spec.head_size * w_elem
+    w = (A.weight_bytes(spec, 1, kvp, w_elem) - o_full + o_full / kvp) * layers
+    return kv, w
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -202,9 +216,8 @@ def pool_slice(a, preset, S, ep, w_dtype="bf16", kv_dtype="bf16"):
     else:
         K = spec.kv_heads
         ekv, ew = (1 if kv_dtype == "fp8" else 2), (1 if w_dtype == "fp8" else 2)
-        kv_bytes = B * 2 * K * Hsz * s_loc * ekv
         # roofline.hpp:17-48: QKV duplicated per KVP rank, O and FFN sharded over N
-        w_bytes = (H * (Q * Hsz + 2 * K * Hsz) + (H // N) * H + 3 * H * spec.ffn_dim // N) * ew
+        kv_bytes, w_bytes = step_bytes_per_gpu(spec, B, s_loc * N, N, 1, ekv, ew)
         out["workload"] = ("llama405b-like layer, one GPU of TPA=1 x KVP=8 (TPF=8): %d KV heads x %d tokens x B=%d; "
                            "QKV replicated, W_O rows and FFN features 1/8; collectives off (1 GPU)" % (K, s_loc, B))
         out["attention"] = {
@@ -263,8 +276,8 @@ def kvp_slices(a):
         ms = e0.elapsed_time(e1) / a.steps
         s_loc = int(P.lib().hx_effective_tokens(eng._h, 0, 0, 0))
         eng.close()
-        kv = B * 2 * K * Hsz * s_loc * 2 * L
-        w = (H * (Q + 2 * K) * Hsz * 2 + (H // n) * H * 2 + 3 * H * F // n * 2) * L + (V // n) * H * 2
+        kv, w = step_bytes_per_gpu(spec, B, s_loc * n, n, L)
+        w += (V // n) * H * 2  # LM-head rows of this rank
         # reference comm model per layer: all-to-all of the fragment slices + two TP all-reduces
         per_dest = B * H / n * (1 + 1 / Hsz) * 4
         a2a = 1e-7 + per_dest * n * (n - 1) / n / 9e11
@@ -575,8 +588,8 @@ def ours(a):
         H, Q, K, Hsz, F, V = (spec.hidden_dim, spec.query_heads, spec.kv_heads, spec.head_size, spec.ffn_dim,
                               spec.vocab)
         s_loc = int(P.lib().hx_effective_tokens(eng._h, 0, 0, rank % world))
-        kv = B * 2 * K * Hsz * s_loc * 2 * L
-        w = (H * (Q + 2 * K) * Hsz * 2 + (H // world) * H * 2 + 3 * H * F // world * 2) * L + (V // world) * H * 2
+        kv, w = step_bytes_per_gpu(spec, B, s_loc * world, world, L)
+        w += (V // world) * H * 2  # LM-head rows of this rank
         xchunk = int(P.lib().hx_exchange_layout(Q, Hsz, world, None))
         a2a = (world - 1) * B * xchunk * 4 * L
         ar = 2 * (2 * (world - 1) / world * B * H * 4) * L

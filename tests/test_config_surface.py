@@ -73,3 +73,19 @@ def test_from_config_rejects_invalid_layouts_before_touching_the_gpu():
         M.HelixDecoder.from_config(spec, M.ParallelismConfig("helix", 1, 8, 4, 1, 1))
     with pytest.raises(ValueError, match="helix strategy"):
         M.HelixDecoder.from_config(spec, M.ParallelismConfig("tp", 8, 1, 8, 1, 1))
+
+
+def test_cpp_config_surface_matches_reference():
+    """include/helixsim/config_b200.hpp (the C++ L0/L1 surface: specs, JSON
+    schema, presets, validate_config, lowering onto the C ABI) -- the C++
+    test tests/cpp/test_config_b200.cpp against the same reference golden."""
+    import subprocess
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    subprocess.check_call(["make", "-s", "-C", os.path.join(root, "tests", "cpp"), "test_config_b200"])
+    env = dict(os.environ, HX_GOLDEN_DIR=os.path.join(root, "tests", "golden"))
+    if os.path.isdir("/root/reference/proj/presets"):
+        env["HX_REF_PRESETS"] = "/root/reference/proj/presets"
+    out = subprocess.run([os.path.join(root, "tests", "cpp", "test_config_b200")], capture_output=True, text=True,
+                         env=env, timeout=120)
+    assert out.returncode == 0, out.stdout[-3000:]
+    assert "failed: 0" in out.stdout.splitlines()[-1]

@@ -36,27 +36,25 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
-LINK_BW, LINK_LAT = 9e11, 1e-7  # reference presets/gb200-like.json:5-6
+from types import SimpleNamespace
+
+from paper_2507_07120_b200 import analytic as A  # pinned to the reference library (tests/test_analytic.py)
+from paper_2507_07120_b200.model import HARDWARE_PRESETS
 
 
 def hopb_schedule(requests, compute, comm, enabled):
     """overlap.hpp:37-69: total span of R requests' compute + comm."""
-    if not enabled:
-        return requests * (compute + comm)
-    prev = 0.0
-    for i in range(requests):
-        ce = (i + 1) * compute
-        ms = ce if i == 0 else max(ce, prev)
-        prev = ms + comm
-    return prev
+    return A.hopb_schedule(requests, compute, comm, enabled).total
 
 
 def a2a_time(hidden, head_size, batch, kvp, bytes_per_elem=4):
-    """comm_time(AllToAll, kvp, per_dest * kvp) with the reference payload (comm.hpp)."""
-    if kvp == 1:
-        return 0.0
-    per_dest = batch * hidden / kvp * (1.0 + 1.0 / head_size) * bytes_per_elem
-    return LINK_LAT + per_dest * kvp * (kvp - 1) / kvp / LINK_BW
+    """comm_time(AllToAll, kvp, per_dest * kvp) with the reference payload (comm.hpp:28-69)
+    on the reference's gb200-like link (presets/gb200-like.json: 900 GB/s, 0.1 us)."""
+    hw = HARDWARE_PRESETS["gb200-like"]
+    hw = SimpleNamespace(**{**hw.__dict__, "bytes_per_param": bytes_per_elem})
+    per_dest = A.a2a_payload_per_destination(SimpleNamespace(hidden_dim=hidden, head_size=head_size), batch, kvp, 1,
+                                             hw)
+    return A.comm_time("all_to_all", kvp, per_dest * kvp, hw)
 
 
 def point(P, Loopback, spec, kvp, S, B, steps=5):
