@@ -94,6 +94,99 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 
 }  // namespace
 
+// ------------------------------------------------------------------------
+// Fused split reduce + device-initiated exchange (AttnParams::fused / push)
+
+// Stream `stream`'s split partials -> the rank's fragment rows (HeadFragment,
+// attention.hpp:56-59), in split order; threads tid, tid + nthr, ... over the
+// stream's rows x DP elements. Partials are read at L2 (ld.cg): other CTAs
+// wrote them in this launch.
+template <int DP>
+__device__ void reduce_stream(const AttnParams& p, int stream, int rows, int tid, int nthr) {
+  int t = stream;
+  const int qc = t % p.q_chunks;
+  t /= p.q_chunks;
+  const int kvh = t % p.kvh_per_slot;
+  t /= p.kvh_per_slot;
+  const int b = t % p.stream_batch + p.b_begin;
+  const int sl = t / p.stream_batch;
+  const int slot = sl + p.slot_base;
+  const int rank = slot % p.kvp;
+  const int QR = p.qrows;
+  const int pages = (static_cast<int>(rr_count(p.total[b], rank, p.chunk, p.kvp)) + 15) >> 4;
+  const int q0 = kvh * p.group + qc * QR;  // first query row of the stream within the slot's group
+  const size_t fbase = (static_cast<size_t>(sl) * p.batch + b) * p.q_per_slot + q0;
+  const size_t ibase = static_cast<size_t>(stream) * p.splits;
+  auto nonempty = [&](int s) {
+    return (static_cast<long long>(s + 1) * pages) / p.splits > (static_cast<long long>(s) * pages) / p.splits;
+  };
+  for (int idx = tid; idx < rows * DP; idx += nthr) {
+    const int q = idx / DP, d = idx - q * DP;
+    float M = -INFINITY;
+    for (int s = 0; s < p.splits; ++s)
+      if (nonempty(s)) M = fmaxf(M, __ldcg(p.part_lse2 + (ibase + s) * QR + q));
+    float L = 0.f, O = 0.f;
+    for (int s = 0; s < p.splits; ++s) {
+      if (!nonempty(s)) continue;
+      const float e = fast_exp2(__ldcg(p.part_lse2 + (ibase + s) * QR + q) - M);
+      L += e;
+      O += __ldcg(p.part_o + ((ibase + s) * QR + q) * DP + d) * e;
+    }
+    const float o = L > 0.f ? O / L : 0.f;
+    const float lse = L > 0.f ? (M + __log2f(L)) * 0.69314718055994530942f : -INFINITY;
+    p.frag_o[(fbase + q) * DP + d] = o;
+    if (d == 0) p.frag_lse[fbase + q] = lse;
+    if (d >= p.hd) continue;
+    const int qg = q0 + q;  // query head within the slot's group
+    if (p.xf_out)           // one-source pool: this fragment IS the merged output
+      xf_write(p.xf_out, xf_nb8(p.batch), b, (slot / p.kvp) * p.q_per_slot * p.hd + qg * p.hd + d, o, p.xf16);
+    if (p.push) {
+      // element e of the group's flattened (heads x hd) output -> peer e / slice (attention.hpp:495-502)
+      const int e = qg * p.hd + d;
+      const int dst = e / p.xslice;
+      const size_t row = (static_cast<size_t>(p.xrank) * p.batch + b) * p.xchunk;
+      p.peer_recv[dst][row + (e - dst * p.xslice)] = o;
+      if (d == 0) {  // the head's lse rides with every slice that touches the head
+        const int p0 = (qg * p.hd) / p.xslice, p1 = ((qg + 1) * p.hd - 1) / p.xslice;
+        for (int pd = p0; pd <= p1; ++pd) p.peer_recv[pd][row + p.xslice + (qg - (pd * p.xslice) / p.hd)] = lse;
+      }
+    }
+  }
+}
+
+// One more stream is out; the launch's last raises this rank's flag in every peer.
+__device__ __forceinline__ void signal_pushed(const AttnParams& p) {
+  __threadfence_system();  // this CTA's peer stores before the count
+  if (atomicAdd(p.pushed, 1) == p.n_streams - 1) {
+    __threadfence_system();
+    for (int r = 0; r < p.kvp; ++r) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.peer_flag[r]), "r"(1u)
+                                                 : "memory");
+    *p.pushed = 0;
+  }
+}
+
+// Consumer warps after an item's partial is stored: count the stream's
+// completed splits; the CTA completing the last one reduces (and pushes) it.
+template <int DP, int NWC>
+__device__ __forceinline__ void fused_stream_done(const AttnParams& p, int stream, int rows, int ntok) {
+  __shared__ int s_last;
+  if (threadIdx.x == 0) {
+    __threadfence();  // the item's partial (all consumer threads, ordered by the barrier) before the count
+    const int pages = (ntok + 15) >> 4;
+    const int need = pages < p.splits ? pages : p.splits;  // non-empty splits of the stream
+    s_last = atomicAdd(p.stream_done + stream, 1) == need - 1;
+    if (s_last) __threadfence();
+  }
+  named_bar_sync(1, NWC * 32);
+  if (!s_last) return;
+  reduce_stream<DP>(p, stream, rows, threadIdx.x, NWC * 32);
+  named_bar_sync(1, NWC * 32);
+  if (threadIdx.x == 0) {
+    p.stream_done[stream] = 0;  // for the next launch / graph replay
+    if (p.push) signal_pushed(p);
+  }
+}
+
 // W16 (bf16 pages, 9-16 query heads per KV head): every consumer warp takes
 // one page per stage for ALL 16 query rows. The three bf16 terms of the query
 // (hi/mid/lo) are three 16-row M-tiles accumulated into ONE S fragment (rows =
@@ -146,9 +239,11 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
         const uint8_t* kv_base = nullptr;
         const float* q_src = nullptr;
         if (!done) {
-          // decode the item once: (split, stream) -> (slot, request, kv head, query chunk)
-          const int split = item / p.n_streams;
-          stream = item - split * p.n_streams;
+          // decode the item once: stream-major (the splits of a stream are adjacent, so
+          // streams -- and requests -- complete in order), then
+          // stream -> (slot, request, kv head, query chunk)
+          stream = item / p.splits;
+          const int split = item - stream * p.splits;
           int t = stream;
           const int qc = t % p.q_chunks;
           t /= p.q_chunks;
@@ -165,7 +260,19 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           pg1 = static_cast<int>((static_cast<long long>(split + 1) * pages) / p.splits);
           const int g_rows = p.group - qc * QR;
           rows = g_rows < QR ? g_rows : QR;
-          if (pg1 <= pg0) continue;  // empty split: nothing to emit
+          if (pg1 <= pg0) {  // empty split: nothing to emit
+            if (p.fused && pages == 0 && split == 0) {
+              // no tokens on this rank for the stream: its fragment is the identity (0, -inf)
+              // (attention.hpp:69-70); the producer thread writes / pushes it
+              if (!waited) {
+                griddep_wait();
+                waited = true;
+              }
+              reduce_stream<DP>(p, stream, rows, 0, 1);
+              if (p.push) signal_pushed(p);
+            }
+            continue;
+          }
           const size_t pool_stream = (static_cast<size_t>(sl) * p.batch + b) * p.kvh_per_slot + kvh;
           kv_base = p.kv + pool_stream * p.page_cap * static_cast<size_t>(Cfg::PAGE);
           const int grp = slot / p.kvp;
@@ -399,6 +506,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           if (d == 0) p.part_lse2[static_cast<size_t>(m.item) * QR + q] = M + __log2f(L);
         }
         named_bar_sync(1, NWC * 32);
+        if (p.fused) fused_stream_done<DP, NWC>(p, m.stream, m.rows, m.ntok);
         m_ref[0] = m_ref[1] = -INFINITY;
         l_sum[0] = l_sum[1] = 0.f;
 #pragma unroll
@@ -579,6 +687,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           if (d == 0) p.part_lse2[static_cast<size_t>(m.item) * QR + qi] = M + __log2f(L);
         }
         named_bar_sync(1, NWC * 32);
+        if (p.fused) fused_stream_done<DP, NWC>(p, m.stream, m.rows, m.ntok);
         // the next item re-initialises state on its first stage
         m_ref = -INFINITY;
         l_sum = 0.f;
@@ -637,7 +746,7 @@ __global__ void __launch_bounds__(kSrWarps * 32) attn_split_reduce_kernel(const 
   // pass 1: max lse over the non-empty splits
   float M = -INFINITY;
   for (int s = warp * 32 + lane; s < p.splits; s += kSrWarps * 32)
-    if (valid(s)) M = fmaxf(M, p.part_lse2[(static_cast<size_t>(s) * p.n_streams + stream) * QR + row]);
+    if (valid(s)) M = fmaxf(M, p.part_lse2[(static_cast<size_t>(stream) * p.splits + s) * QR + row]);
 #pragma unroll
   for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
   if (lane == 0) s_m[warp] = M;
@@ -655,7 +764,7 @@ __global__ void __launch_bounds__(kSrWarps * 32) attn_split_reduce_kernel(const 
     for (int j = 0; j < 4; ++j) {
       const int s = s0 + j * kSrWarps;
       const bool ok = s < p.splits && valid(s);
-      const size_t item = static_cast<size_t>(s) * p.n_streams + stream;
+      const size_t item = static_cast<size_t>(stream) * p.splits + s;
       w4[j] = ok ? p.part_lse2[item * QR + row] : -INFINITY;
 #pragma unroll
       for (int i = 0; i < PER; ++i) v[j][i] = ok ? p.part_o[(item * QR + row) * DP + lane + 32 * i] : 0.f;
@@ -728,7 +837,7 @@ __global__ void __launch_bounds__(256) attn_split_reduce_small_kernel(const Attn
     const int pg0 = static_cast<int>((static_cast<long long>(j) * pages) / p.splits);
     const int pg1 = static_cast<int>((static_cast<long long>(j + 1) * pages) / p.splits);
     const bool ok = j < p.splits && pg1 > pg0;
-    const size_t item = static_cast<size_t>(j) * p.n_streams + stream;
+    const size_t item = static_cast<size_t>(stream) * p.splits + j;
     w[j] = ok ? p.part_lse2[item * QR + row] : -INFINITY;
 #pragma unroll
     for (int i = 0; i < PER; ++i) v[j][i] = ok ? p.part_o[(item * QR + row) * DP + lane + 32 * i] : 0.f;

@@ -11,7 +11,7 @@
 namespace hx {
 
 // ---------------------------------------------------------------------------- loopback
-LoopbackHub::LoopbackHub(int n) : send(n), recv(n), bufs(n), n_(n) {}
+LoopbackHub::LoopbackHub(int n) : send(n), recv(n), bufs(n), reg_recv(n), reg_flags(n), n_(n) {}
 
 void LoopbackHub::barrier() {
   std::unique_lock<std::mutex> lk(mu);
@@ -57,6 +57,23 @@ class LoopbackTransport : public Transport {
     }
     cuda_check(cudaStreamSynchronize(s), "loopback sync");
     hub_->barrier();  // send buffers may be reused
+  }
+
+  // one device: the peers' buffers are directly addressable
+  void map_peers(void* recv, void* flags, std::vector<void*>& recv_out, std::vector<void*>& flags_out) override {
+    {
+      std::lock_guard<std::mutex> lk(hub_->mu);
+      hub_->reg_recv[static_cast<size_t>(rank_)] = recv;
+      hub_->reg_flags[static_cast<size_t>(rank_)] = flags;
+    }
+    hub_->barrier();
+    recv_out.assign(static_cast<size_t>(kvp_), nullptr);
+    flags_out.assign(static_cast<size_t>(kvp_), nullptr);
+    for (int p = 0; p < kvp_; ++p) {
+      recv_out[static_cast<size_t>(p)] = hub_->reg_recv[static_cast<size_t>(group_base_ + p)];
+      flags_out[static_cast<size_t>(p)] = hub_->reg_flags[static_cast<size_t>(group_base_ + p)];
+    }
+    hub_->barrier();
   }
 
   template <class T, class Launch>
@@ -111,7 +128,7 @@ void nccl_check(ncclResult_t r, const char* what) {
 
 class NcclTransport : public Transport {
  public:
-  NcclTransport(const void* uid, int rank, int tpa, int kvp) : kvp_(kvp), n_(tpa * kvp) {
+  NcclTransport(const void* uid, int rank, int tpa, int kvp) : kvp_(kvp), n_(tpa * kvp), my_(rank % kvp) {
     ncclUniqueId id;
     std::memcpy(&id, uid, sizeof(id));
     nccl_check(ncclCommInitRank(&world_, n_, id, rank), "ncclCommInitRank");
@@ -119,8 +136,45 @@ class NcclTransport : public Transport {
     nccl_check(ncclCommSplit(world_, rank / kvp, rank % kvp, &group_, nullptr), "ncclCommSplit");
   }
   ~NcclTransport() override {
+    for (void* p : opened_) cudaIpcCloseMemHandle(p);
     if (group_) ncclCommDestroy(group_);
     if (world_) ncclCommDestroy(world_);
+  }
+  // CUDA IPC over NVLink/NVSwitch: all-gather the group's memory handles through
+  // NCCL, open the peers' (lazy peer access) -- their buffers become plain
+  // device pointers the attention kernel stores into.
+  void map_peers(void* recv, void* flags, std::vector<void*>& recv_out, std::vector<void*>& flags_out) override {
+    constexpr size_t kH = sizeof(cudaIpcMemHandle_t);
+    cudaIpcMemHandle_t mine[2];
+    cuda_check(cudaIpcGetMemHandle(&mine[0], recv), "cudaIpcGetMemHandle(recv)");
+    cuda_check(cudaIpcGetMemHandle(&mine[1], flags), "cudaIpcGetMemHandle(flags)");
+    char* dbuf = nullptr;
+    cuda_check(cudaMalloc(&dbuf, 2 * kH * static_cast<size_t>(kvp_ + 1)), "ipc staging");
+    cudaStream_t s;
+    cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "ipc stream");
+    cuda_check(cudaMemcpyAsync(dbuf, mine, 2 * kH, cudaMemcpyHostToDevice, s), "ipc h2d");
+    nccl_check(ncclAllGather(dbuf, dbuf + 2 * kH, 2 * kH, ncclChar, group_, s), "ncclAllGather(ipc handles)");
+    std::vector<cudaIpcMemHandle_t> all(static_cast<size_t>(2 * kvp_));
+    cuda_check(cudaMemcpyAsync(all.data(), dbuf + 2 * kH, 2 * kH * kvp_, cudaMemcpyDeviceToHost, s), "ipc d2h");
+    cuda_check(cudaStreamSynchronize(s), "ipc sync");
+    cudaStreamDestroy(s);
+    cudaFree(dbuf);
+    recv_out.assign(static_cast<size_t>(kvp_), nullptr);
+    flags_out.assign(static_cast<size_t>(kvp_), nullptr);
+    for (int p = 0; p < kvp_; ++p) {
+      if (p == my_) {
+        recv_out[static_cast<size_t>(p)] = recv;
+        flags_out[static_cast<size_t>(p)] = flags;
+        continue;
+      }
+      for (int k = 0; k < 2; ++k) {
+        void* ptr = nullptr;
+        cuda_check(cudaIpcOpenMemHandle(&ptr, all[static_cast<size_t>(2 * p + k)], cudaIpcMemLazyEnablePeerAccess),
+                   "cudaIpcOpenMemHandle");
+        opened_.push_back(ptr);
+        (k ? flags_out : recv_out)[static_cast<size_t>(p)] = ptr;
+      }
+    }
   }
   int world() const override {
     int n = 0;
@@ -148,8 +202,9 @@ class NcclTransport : public Transport {
   }
 
  private:
-  int kvp_, n_;
+  int kvp_, n_, my_;
   ncclComm_t world_ = nullptr, group_ = nullptr;
+  std::vector<void*> opened_;
 };
 
 }  // namespace

@@ -32,6 +32,11 @@ class Transport {
   virtual void all_reduce_max_u64(unsigned long long* buf, size_t n, cudaStream_t s) = 0;
   virtual int world() const = 0;
   virtual int64_t nccl_version() const { return 0; }
+  // Device-initiated exchange: make every KVP-group peer's receive buffer and
+  // flag array addressable from this device. recv_out / flags_out get the
+  // group's kvp pointers in group-rank order (own buffers at this rank's index).
+  // Collective over the group (call on every rank, outside stream capture).
+  virtual void map_peers(void* recv, void* flags, std::vector<void*>& recv_out, std::vector<void*>& flags_out) = 0;
 };
 
 // Shared state of a loopback group (all ranks in one process, one device).
@@ -44,6 +49,7 @@ class LoopbackHub {
   std::vector<const void*> send;
   std::vector<void*> recv;
   std::vector<void*> bufs;
+  std::vector<void*> reg_recv, reg_flags;  // map_peers registration
   float* scratch = nullptr;            // [n][max elems] for sum reductions
   unsigned long long* scratch_u64 = nullptr;
   size_t scratch_elems = 0;

@@ -296,6 +296,7 @@ Engine::~Engine() {
   f(w_lm_); f(emb_); f(d_total_); f(d_q_); f(d_part_o_); f(d_part_lse_); f(d_work_);
   f(d_frag_o_); f(d_frag_lse_); f(d_ypart_); f(d_counters_); f(d_x_); f(d_ss_); f(d_m_);
   f(d_logits_); f(d_best_); f(d_tokens_); f(d_next_); f(d_out_); f(d_out_lse_); f(d_hidden_);
+  f(d_stream_done_); f(d_pushed_); f(d_flags_); f(d_peer_recv_); f(d_peer_flag_); f(d_self_recv_); f(d_self_flag_);
   f(d_segs_); f(d_send_); f(d_recv_); f(d_parth_); f(d_xf_resid_); f(d_xf_attn_); f(d_xf_m_); f(d_plan_ctr_);
   for (auto* p : k64_) f(p);
   for (auto* p : v64_) f(p);
@@ -383,7 +384,15 @@ void Engine::alloc() {
     n_items_ = std::max(n_streams_ * splits_, req_streams * splits_req_);
   }
   attn_grid_ = std::min(mla_ ? num_sms_ / 2 : num_sms_, n_items_);  // MLA: CTA pairs
+  if (std::getenv("HX_FUSED_REDUCE") && std::getenv("HX_FUSED_REDUCE")[0] == '0') fused_ = false;
+  d_stream_done_ = dalloc<int>(static_cast<size_t>(std::max(n_streams_, 1)), "stream done counters");
+  d_pushed_ = dalloc<int>(1, "pushed counter");
   if (dist_mode_ != HX_POOL_LOCAL) {
+    d_flags_ = dalloc<unsigned>(static_cast<size_t>(kvp_), "exchange flags");
+    d_peer_recv_ = dalloc<float*>(static_cast<size_t>(kvp_), "peer recv table");
+    d_peer_flag_ = dalloc<unsigned*>(static_cast<size_t>(kvp_), "peer flag table");
+    d_self_recv_ = dalloc<float*>(static_cast<size_t>(kvp_), "self recv table");
+    d_self_flag_ = dalloc<unsigned*>(static_cast<size_t>(kvp_), "self flag table");
     d_send_ = dalloc<float>(static_cast<size_t>(kvp_) * B_ * xchunk_, "exchange send");
     d_recv_ = dalloc<float>(static_cast<size_t>(kvp_) * B_ * xchunk_, "exchange recv");
     d_parth_ = dalloc<float>(static_cast<size_t>(B_) * H_, "tp partial");
@@ -569,15 +578,21 @@ void Engine::plan_gemvs() {
     d_logits_ = dalloc<float>(static_cast<size_t>(B_) * V_local_, "logits");
     d_hidden_ = dalloc<float>(static_cast<size_t>(L_ + 1) * B_ * H_, "hidden");
   }
-  // launches per step (each GEMV = streaming kernel + epilogue kernel)
-  // FFN per layer: dense 4; MoE router 2 + route 1 + experts 4 (+ shared 4)
-  const int64_t ffn_k = moe_ ? 7 + (F_ > 0 ? 4 : 0) : 4;
-  if (attn_only_)
-    kernels_per_step_ = 6;  // xprep, qkv x2, attention, split-reduce, merge(+bump)
-  else if (!dist)
-    kernels_per_step_ = 1 + (7 - (one_src_merge_ ? 1 : 0) + ffn_k + (mla_ ? 2 : 0)) * L_ + 3;  // MLA: + absorb_q, uv
-  else  // + pack and two residual adds per layer; per-request attention launches under HOP-B
-    kernels_per_step_ = 1 + L_ * (9 + ffn_k + (mla_ ? 2 : 0) + (hopb_ ? 3 * (B_ - 1) : 0)) + 3;
+}
+
+// Kernel launches of one step as the engine enqueues it now (each GEMV =
+// streaming kernel + epilogue kernel; NCCL's own kernels not counted).
+int64_t Engine::launches_per_step() const {
+  const int64_t ffn_k = moe_ ? 7 + (F_ > 0 ? 4 : 0) : 4;  // dense 4; MoE router 2 + route + experts 4 (+ shared 4)
+  const int64_t sr = (mla_ || !fused_) ? 1 : 0;           // split-reduce kernel (fused into GQA attention)
+  if (attn_only_) return f64_ ? 3 + 2 * B_ : 4 + sr + 1;  // xprep, qkv x2, attention, [split-reduce], merge
+  const int64_t head = 1 + 3;                              // embed; LM head x2 + argmax finish
+  const int64_t mla_k = mla_ ? 2 : 0;                      // W_UK absorption, W_UV
+  if (dist_mode_ == HX_POOL_LOCAL)
+    return head + L_ * (2 + 1 + sr + (one_src_merge_ ? 0 : 1) + mla_k + 2 + ffn_k);
+  const int64_t attn = device_exchange() ? 2                       // attention (+ push) and the flag wait
+                                         : (hopb_ ? B_ : 1) * (2 + sr);  // [per request] attention, [sr], pack
+  return head + L_ * (2 + attn + 1 + mla_k + 2 + 1 + ffn_k + 1);  // + merge, O x2, residual, FFN, residual
 }
 
 // ---------------------------------------------------------------------------
@@ -1149,6 +1164,14 @@ AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) {
   a.splits = b_count == B_ ? splits_ : splits_req_;
   a.n_items = a.n_streams * a.splits;  // HOP-B (one request): splits_req_ balanced page ranges
   a.qscale = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(mla_ ? W_ : D_)));
+  if (!mla_ && fused_) {
+    a.fused = 1;
+    a.stream_done = d_stream_done_;
+    a.frag_o = d_frag_o_;
+    a.frag_lse = d_frag_lse_;
+    a.pushed = d_pushed_;
+    a.hd = static_cast<int>(D_);
+  }
   if (mla_) {
     a.qimg = d_qimg_;
     a.dp = DV_;
@@ -1169,7 +1192,7 @@ void Engine::launch_attention_kernels(const AttnParams& a) {
   } else {
     cuda_check(launch_attn_decode(a, std::min(attn_grid_, a.n_items), stream_), "attention");
     mark(2);
-    cuda_check(launch_attn_split_reduce(a, d_frag_o_, d_frag_lse_, stream_), "split reduce");
+    if (!a.fused) cuda_check(launch_attn_split_reduce(a, d_frag_o_, d_frag_lse_, stream_), "split reduce");
   }
 }
 
@@ -1198,6 +1221,26 @@ void Engine::enqueue_attention(int64_t layer) {
 // HOP-B (overlap.hpp:37-69): request b's exchange runs on the comm stream while
 // request b+1's attention runs on the compute stream.
 void Engine::enqueue_exchange_and_attention_dist(int64_t layer) {
+  if (device_exchange()) {
+    // HOP-B, device-initiated (overlap.hpp:37-69 at stream granularity): ONE
+    // attention launch in request order whose CTAs reduce each finished stream
+    // and store its slices straight into the peers' receive buffers while the
+    // later requests are still streaming; the last CTA raises this rank's flag
+    // in every peer. No per-request launches, no exchange kernel, no NCCL.
+    AttnParams a = attn_params(layer, 0, B_);
+    const bool skip = skip_comm_ & 1;  // measurement: every slice stays on this rank
+    a.push = 1;
+    a.peer_recv = skip ? d_self_recv_ : d_peer_recv_;
+    a.peer_flag = skip ? d_self_flag_ : d_peer_flag_;
+    a.xchunk = xchunk_;
+    a.xslice = slice_;
+    a.xrank = r_;
+    launch_attention_kernels(a);
+    mark(3);
+    cuda_check(launch_wait_flags(skip ? d_flags_ + r_ : d_flags_, skip ? 1 : kvp_, stream_), "exchange wait");
+    mark(9);
+    return;
+  }
   const size_t stride = static_cast<size_t>(B_) * xchunk_;
   const int rounds = hopb_ ? B_ : 1;
   const int per = hopb_ ? 1 : B_;
@@ -1235,6 +1278,25 @@ void Engine::enqueue_exchange_and_attention_dist(int64_t layer) {
     cuda_check(cudaStreamWaitEvent(stream_, hop_events_.back(), 0), "hopb join wait");
   }
   mark(9);
+}
+
+// Map the KVP group's receive buffers and flags (device-initiated exchange):
+// once, collectively, before the first distributed step (outside capture).
+void Engine::ensure_peers() {
+  if (peers_mapped_ || dist_mode_ == HX_POOL_LOCAL) return;
+  std::vector<void*> recv, flags;
+  transport_->map_peers(d_recv_, d_flags_, recv, flags);
+  std::vector<float*> pr(static_cast<size_t>(kvp_)), sr(static_cast<size_t>(kvp_), d_recv_);
+  std::vector<unsigned*> pf(static_cast<size_t>(kvp_)), sf(static_cast<size_t>(kvp_), d_flags_ + r_);
+  for (int p = 0; p < kvp_; ++p) {
+    pr[static_cast<size_t>(p)] = static_cast<float*>(recv[static_cast<size_t>(p)]);
+    pf[static_cast<size_t>(p)] = static_cast<unsigned*>(flags[static_cast<size_t>(p)]) + r_;  // my word in peer p
+  }
+  cuda_check(cudaMemcpy(d_peer_recv_, pr.data(), pr.size() * sizeof(float*), cudaMemcpyHostToDevice), "peer table");
+  cuda_check(cudaMemcpy(d_peer_flag_, pf.data(), pf.size() * sizeof(unsigned*), cudaMemcpyHostToDevice), "peer table");
+  cuda_check(cudaMemcpy(d_self_recv_, sr.data(), sr.size() * sizeof(float*), cudaMemcpyHostToDevice), "self table");
+  cuda_check(cudaMemcpy(d_self_flag_, sf.data(), sf.size() * sizeof(unsigned*), cudaMemcpyHostToDevice), "self table");
+  peers_mapped_ = true;
 }
 
 void Engine::harness_step(int64_t layer, const float* x_host, int64_t x_len, float* out, float* lse) {
@@ -1379,6 +1441,7 @@ void Engine::decode_step_device(const int32_t* tokens_dev, int32_t* next_dev) {
   if (attn_only_) throw StateError("decode_step needs a full model (attention_only = 0)");
   if (!weights_ready_) throw StateError("weights are not initialised");
   for (int64_t l = 0; l < L_; ++l) require_context(l);
+  if (device_exchange()) ensure_peers();
   if (graphs_ && !(loopback_ && skip_comm_ != 3) && !prof_) {
     cudaGraphExec_t exec = nullptr;
     for (auto& g : graphs_cache_)
@@ -1634,9 +1697,7 @@ void Engine::info(hx_engine_info* o) const {
   o->attn_splits = splits_;
   o->attn_items = n_items_;
   o->attn_grid = attn_grid_;
-  o->kernels_per_step = kernels_per_step_;
-  if (!attn_only_ && dist_mode_ != HX_POOL_LOCAL)  // + pack and two residual adds per layer
-    o->kernels_per_step = 1 + L_ * (13 + (hopb_ ? 3 * (B_ - 1) : 0)) + 3;
+  o->kernels_per_step = launches_per_step();
   o->page_cap = page_cap_;
   o->head_dim_padded = DP_;
   o->kv_dtype = kv8_ ? HX_KV_FP8_E4M3 : HX_KV_BF16;

@@ -180,7 +180,7 @@ class Engine {
   GemvPlan plan_lm_;
   size_t ypart_elems_ = 0;
   int max_counters_ = 0;
-  int64_t kernels_per_step_ = 0;
+  int64_t launches_per_step() const;
 
   struct GraphEntry {
     const int32_t* tokens;
@@ -206,6 +206,18 @@ class Engine {
   float* d_recv_ = nullptr;
   float* d_parth_ = nullptr;   // [B][H] partial products before the TP AllReduce
   cudaStream_t comm_stream_ = nullptr;
+  // fused split reduce (GQA) and the device-initiated exchange (HOP-B on)
+  bool fused_ = true;            // HX_FUSED_REDUCE=0: separate split-reduce kernel (A/B)
+  int* d_stream_done_ = nullptr;
+  int* d_pushed_ = nullptr;
+  unsigned* d_flags_ = nullptr;  // [kvp] raised by the peer that pushed to this rank
+  float** d_peer_recv_ = nullptr;       // [kvp] group receive buffers (peer pointers)
+  unsigned** d_peer_flag_ = nullptr;    // [kvp] this rank's flag word in each peer
+  float** d_self_recv_ = nullptr;       // HX_FLAG_SKIP_COMM stand-ins: everything to this rank
+  unsigned** d_self_flag_ = nullptr;
+  bool peers_mapped_ = false;
+  void ensure_peers();
+  bool device_exchange() const { return hopb_ && !mla_ && fused_ && dist_mode_ != HX_POOL_LOCAL; }
   std::vector<cudaEvent_t> hop_events_;
   void enqueue_exchange_and_attention_dist(int64_t layer);
   void init_dist_weights(uint64_t seed, bool qkv_hash);

@@ -64,8 +64,29 @@ struct AttnParams {
   uint8_t* xf_out;
   int xf16, hd;
   int kv8;                 // GQA: FP8 (e4m3) pages (kv_layout.cuh), f16 MMAs
+  // Fused split reduce (GQA): the CTA that completes a stream's last non-empty
+  // split merges the stream's partials (split order) into frag_o / frag_lse
+  // [slot_local][b][q][DP] (natural-log lse) -- no split-reduce launch.
+  int fused;
+  int* stream_done;        // [n_streams] completed splits per stream (self-resetting)
+  float* frag_o;
+  float* frag_lse;
+  // Device-initiated fragment exchange (HOP-B, distributed GQA pools): each
+  // reduced stream is stored straight into the KVP peers' receive buffers
+  // [src rank][batch][xchunk] (slice + lse slots, attention.hpp:492-502); once
+  // every stream of the launch is out, the last CTA raises this rank's flag in
+  // every peer (system-scope release). Exchange of request b overlaps the
+  // attention of the requests after it.
+  int push;
+  float* const* peer_recv; // [kvp] receive buffers of this rank's KVP group (own included)
+  unsigned* const* peer_flag; // [kvp] this rank's flag word in each peer
+  int* pushed;             // streams pushed in this launch (self-resetting)
+  int xchunk, xslice, xrank;
 };
 cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t stream);
+// Spin (one CTA) until every flag is raised, then lower it: the receive side
+// of the device-initiated exchange (flags written by the peers' attention kernels).
+cudaError_t launch_wait_flags(unsigned* flags, int n, cudaStream_t stream);
 // MLA (tcgen05): items = (split, stream, value half); part_o [n_items][128][256],
 // part_lse2 [n_items][128]; the split reduce writes frag_o [slot][b][q][512].
 // tm_s / tm_v: CUtensorMap (128 B each) over the layer's latent pool viewed as

@@ -523,6 +523,26 @@ cudaError_t launch_pack_exchange(const float* frag_o, const float* frag_lse, int
                   q_per_slot, head_dim, dp, kvp, slice, chunk, send);
 }
 
+// Receive side of the device-initiated exchange: one CTA waits until every
+// peer's attention kernel has raised its flag (system-scope acquire), then
+// lowers it for the next layer. The merge that follows reads the pushed slices.
+__global__ void wait_flags_kernel(unsigned* flags, int n) {
+  griddep_wait();  // after this rank's own attention: never holds an SM the attention needs
+  griddep_launch_dependents();
+  const int i = threadIdx.x;
+  if (i >= n) return;
+  unsigned v = 0;
+  for (;;) {
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + i) : "memory");
+    if (v) break;
+    __nanosleep(64);
+  }
+  flags[i] = 0u;
+}
+cudaError_t launch_wait_flags(unsigned* flags, int n, cudaStream_t s) {
+  return launch_k(wait_flags_kernel, dim3(1), dim3(32 * ((n + 31) / 32)), 0, s, flags, n);
+}
+
 // x[b][n] += part[b][n]; ss_part[blk][b] = sum over the 128-column block of x^2 (deterministic).
 __global__ void residual_add_kernel(float* x, const float* part, int batch, int hidden, float* ss_part,
                                     uint8_t* xf, int xf16) {
