@@ -50,6 +50,7 @@ def build(verbose=False, force=False):
                 "-I", CSRC, "-I", os.path.join(ROOT, "include"), "-I", nccl_inc]
     if verbose:
         cu_flags += ["-Xptxas", "-v"]
+    cu_flags += os.environ.get("HX_NVCC_FLAGS", "").split()  # e.g. -DHX_DEBUG_PUSH (debug builds)
     jobs = []
     for src in sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp"))):
         obj = os.path.join(BUILD, os.path.basename(src) + ".o")

@@ -24,6 +24,7 @@
 //     memory and write the split's normalised O and log2-sum-exp.
 // The KV stream is the roofline: 64*DP bytes per page, no re-reads.
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -92,17 +93,59 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
+// Work item of (stream, split): split-major (every stream advances together --
+// the faster order for one batched launch) or stream-major (the splits of a
+// stream are adjacent, so streams and requests complete in order: HOP-B).
+__device__ __forceinline__ size_t attn_item(const AttnParams& p, int stream, int split) {
+  return p.stream_major ? static_cast<size_t>(stream) * p.splits + split
+                        : static_cast<size_t>(split) * p.n_streams + stream;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------------
 // Fused split reduce + device-initiated exchange (AttnParams::fused / push)
 
 // Stream `stream`'s split partials -> the rank's fragment rows (HeadFragment,
-// attention.hpp:56-59), in split order; threads tid, tid + nthr, ... over the
-// stream's rows x DP elements. Partials are read at L2 (ld.cg): other CTAs
-// wrote them in this launch.
+// attention.hpp:56-59), splits merged in order. Warp `warp` of `nwarps` takes
+// rows warp, warp + nwarps, ...; lanes hold dims lane + 32 i, and each batch of
+// 16 splits issues all its loads before using any (the partials are L2-resident:
+// other CTAs wrote them in this launch, so ld.cg). nwarps = 0: a single thread
+// (the producer, for an empty stream: the identity fragment).
+// Device-initiated exchange (AttnParams::push): element d of query head qg of
+// this rank's group output for request b goes to peer e / slice at offset
+// e % slice of its [this rank][b] chunk, e = qg * hd + d; the head's lse rides
+// in the lse slots of every slice that touches the head (attention.hpp:495-502).
+__device__ __forceinline__ void push_value(const AttnParams& p, int b, int qg, int d, float o) {
+  const int e = qg * p.hd + d;
+  const int dst = e / p.xslice;
+  p.peer_recv[dst][(static_cast<size_t>(p.xrank) * p.batch + b) * p.xchunk + (e - dst * p.xslice)] = o;
+}
+__device__ __forceinline__ void push_lse(const AttnParams& p, int b, int qg, float lse) {
+  const size_t row = (static_cast<size_t>(p.xrank) * p.batch + b) * p.xchunk;
+  const int p0 = (qg * p.hd) / p.xslice, p1 = ((qg + 1) * p.hd - 1) / p.xslice;
+  for (int pd = p0; pd <= p1; ++pd) p.peer_recv[pd][row + p.xslice + (qg - (pd * p.xslice) / p.hd)] = lse;
+}
+// One more unit (stream / reduce CTA) is out; the `total`-th raises this
+// rank's flag in every peer (system-scope release after a system fence).
+__device__ __forceinline__ void signal_pushed(const AttnParams& p, int total) {
+  __threadfence_system();  // this unit's peer stores before the count
+  const int cnt = atomicAdd(p.pushed, 1);
+#ifdef HX_DEBUG_PUSH
+  printf("push rank %d unit %d/%d\n", p.xrank, cnt, total);
+#endif
+  if (cnt == total - 1) {
+    __threadfence_system();
+    for (int r = 0; r < p.kvp; ++r) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.peer_flag[r]), "r"(1u)
+                                                 : "memory");
+    *p.pushed = 0;
+  }
+}
+
+constexpr int kRedBatch = 16;  // splits whose loads are in flight together
 template <int DP>
-__device__ void reduce_stream(const AttnParams& p, int stream, int rows, int tid, int nthr) {
+__device__ void reduce_stream(const AttnParams& p, int stream, int rows, int warp, int nwarps) {
+  constexpr int PER = DP / 32;
   int t = stream;
   const int qc = t % p.q_chunks;
   t /= p.q_chunks;
@@ -116,52 +159,61 @@ __device__ void reduce_stream(const AttnParams& p, int stream, int rows, int tid
   const int pages = (static_cast<int>(rr_count(p.total[b], rank, p.chunk, p.kvp)) + 15) >> 4;
   const int q0 = kvh * p.group + qc * QR;  // first query row of the stream within the slot's group
   const size_t fbase = (static_cast<size_t>(sl) * p.batch + b) * p.q_per_slot + q0;
-  const size_t ibase = static_cast<size_t>(stream) * p.splits;
+  const bool single = nwarps == 0;
+  const int lane = single ? 0 : (threadIdx.x & 31);
+  const bool all_full = pages >= p.splits;  // every split holds >= 1 page (the usual case)
   auto nonempty = [&](int s) {
-    return (static_cast<long long>(s + 1) * pages) / p.splits > (static_cast<long long>(s) * pages) / p.splits;
+    return all_full ||
+           (static_cast<long long>(s + 1) * pages) / p.splits > (static_cast<long long>(s) * pages) / p.splits;
   };
-  for (int idx = tid; idx < rows * DP; idx += nthr) {
-    const int q = idx / DP, d = idx - q * DP;
+  for (int q = single ? 0 : warp; q < rows; q += single ? 1 : nwarps) {
     float M = -INFINITY;
-    for (int s = 0; s < p.splits; ++s)
-      if (nonempty(s)) M = fmaxf(M, __ldcg(p.part_lse2 + (ibase + s) * QR + q));
-    float L = 0.f, O = 0.f;
-    for (int s = 0; s < p.splits; ++s) {
-      if (!nonempty(s)) continue;
-      const float e = fast_exp2(__ldcg(p.part_lse2 + (ibase + s) * QR + q) - M);
-      L += e;
-      O += __ldcg(p.part_o + ((ibase + s) * QR + q) * DP + d) * e;
+    if (!single) {
+      for (int s = lane; s < p.splits; s += 32)
+        if (nonempty(s)) M = fmaxf(M, __ldcg(p.part_lse2 + attn_item(p, stream, s) * QR + q));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     }
-    const float o = L > 0.f ? O / L : 0.f;
-    const float lse = L > 0.f ? (M + __log2f(L)) * 0.69314718055994530942f : -INFINITY;
-    p.frag_o[(fbase + q) * DP + d] = o;
-    if (d == 0) p.frag_lse[fbase + q] = lse;
-    if (d >= p.hd) continue;
-    const int qg = q0 + q;  // query head within the slot's group
-    if (p.xf_out)           // one-source pool: this fragment IS the merged output
-      xf_write(p.xf_out, xf_nb8(p.batch), b, (slot / p.kvp) * p.q_per_slot * p.hd + qg * p.hd + d, o, p.xf16);
-    if (p.push) {
-      // element e of the group's flattened (heads x hd) output -> peer e / slice (attention.hpp:495-502)
-      const int e = qg * p.hd + d;
-      const int dst = e / p.xslice;
-      const size_t row = (static_cast<size_t>(p.xrank) * p.batch + b) * p.xchunk;
-      p.peer_recv[dst][row + (e - dst * p.xslice)] = o;
-      if (d == 0) {  // the head's lse rides with every slice that touches the head
-        const int p0 = (qg * p.hd) / p.xslice, p1 = ((qg + 1) * p.hd - 1) / p.xslice;
-        for (int pd = p0; pd <= p1; ++pd) p.peer_recv[pd][row + p.xslice + (qg - (pd * p.xslice) / p.hd)] = lse;
+    float L = 0.f, acc[PER];
+#pragma unroll
+    for (int i = 0; i < PER; ++i) acc[i] = 0.f;
+    if (M != -INFINITY) {
+      for (int s0 = 0; s0 < p.splits; s0 += kRedBatch) {
+        float e[kRedBatch], v[kRedBatch][PER];
+#pragma unroll
+        for (int j = 0; j < kRedBatch; ++j) {
+          const int s = s0 + j;
+          const bool ok = s < p.splits && nonempty(s);
+          const size_t it = attn_item(p, stream, ok ? s : 0);
+          e[j] = ok ? __ldcg(p.part_lse2 + it * QR + q) : -INFINITY;
+          const float* po = p.part_o + (it * QR + q) * DP + lane;
+#pragma unroll
+          for (int i = 0; i < PER; ++i) v[j][i] = ok ? __ldcg(po + 32 * i) : 0.f;
+        }
+#pragma unroll
+        for (int j = 0; j < kRedBatch; ++j) {
+          const float w = e[j] == -INFINITY ? 0.f : fast_exp2(e[j] - M);
+          L += w;
+#pragma unroll
+          for (int i = 0; i < PER; ++i) acc[i] += v[j][i] * w;
+        }
       }
     }
-  }
-}
-
-// One more stream is out; the launch's last raises this rank's flag in every peer.
-__device__ __forceinline__ void signal_pushed(const AttnParams& p) {
-  __threadfence_system();  // this CTA's peer stores before the count
-  if (atomicAdd(p.pushed, 1) == p.n_streams - 1) {
-    __threadfence_system();
-    for (int r = 0; r < p.kvp; ++r) asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p.peer_flag[r]), "r"(1u)
-                                                 : "memory");
-    *p.pushed = 0;
+    const float lse = L > 0.f ? (M + __log2f(L)) * 0.69314718055994530942f : -INFINITY;
+    const int qg = q0 + q;  // query head within the slot's group
+    for (int i = 0; i < (single ? DP : PER); ++i) {
+      const int d = single ? i : lane + 32 * i;
+      const float o = single ? 0.f : (L > 0.f ? acc[i] / L : 0.f);  // single: empty stream
+      p.frag_o[(fbase + q) * DP + d] = o;
+      if (d >= p.hd) continue;
+      if (p.xf_out)  // one-source pool: this fragment IS the merged output
+        xf_write(p.xf_out, xf_nb8(p.batch), b, (slot / p.kvp) * p.q_per_slot * p.hd + qg * p.hd + d, o, p.xf16);
+      if (p.push) push_value(p, b, qg, d, o);
+    }
+    if (lane == 0) {
+      p.frag_lse[fbase + q] = lse;
+      if (p.push) push_lse(p, b, qg, lse);
+    }
   }
 }
 
@@ -179,11 +231,11 @@ __device__ __forceinline__ void fused_stream_done(const AttnParams& p, int strea
   }
   named_bar_sync(1, NWC * 32);
   if (!s_last) return;
-  reduce_stream<DP>(p, stream, rows, threadIdx.x, NWC * 32);
+  reduce_stream<DP>(p, stream, rows, threadIdx.x >> 5, NWC);
   named_bar_sync(1, NWC * 32);
   if (threadIdx.x == 0) {
     p.stream_done[stream] = 0;  // for the next launch / graph replay
-    if (p.push) signal_pushed(p);
+    if (p.push) signal_pushed(p, p.n_streams);
   }
 }
 
@@ -239,11 +291,16 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
         const uint8_t* kv_base = nullptr;
         const float* q_src = nullptr;
         if (!done) {
-          // decode the item once: stream-major (the splits of a stream are adjacent, so
-          // streams -- and requests -- complete in order), then
+          // decode the item once: (stream, split) (attn_item), then
           // stream -> (slot, request, kv head, query chunk)
-          stream = item / p.splits;
-          const int split = item - stream * p.splits;
+          int split;
+          if (p.stream_major) {
+            stream = item / p.splits;
+            split = item - stream * p.splits;
+          } else {
+            split = item / p.n_streams;
+            stream = item - split * p.n_streams;
+          }
           int t = stream;
           const int qc = t % p.q_chunks;
           t /= p.q_chunks;
@@ -268,8 +325,8 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
                 griddep_wait();
                 waited = true;
               }
-              reduce_stream<DP>(p, stream, rows, 0, 1);
-              if (p.push) signal_pushed(p);
+              reduce_stream<DP>(p, stream, rows, 0, 0);
+              if (p.push) signal_pushed(p, p.n_streams);
             }
             continue;
           }
@@ -734,7 +791,10 @@ __global__ void __launch_bounds__(kSrWarps * 32) attn_split_reduce_kernel(const 
   const int slot = slot_local + p.slot_base;
   const int rank = slot % p.kvp;
   const int qrow = qc * QR + row;
-  if (qrow >= p.group) return;  // whole CTA
+  if (qrow >= p.group) {  // whole CTA: nothing to reduce, still one unit of the exchange count
+    if (p.push && threadIdx.x == 0) signal_pushed(p, gridDim.x);
+    return;
+  }
   const int ntok = static_cast<int>(rr_count(p.total[b], rank, p.chunk, p.kvp));
   const int pages = (ntok + 15) >> 4;
   constexpr int PER = DP / 32;
@@ -746,7 +806,7 @@ __global__ void __launch_bounds__(kSrWarps * 32) attn_split_reduce_kernel(const 
   // pass 1: max lse over the non-empty splits
   float M = -INFINITY;
   for (int s = warp * 32 + lane; s < p.splits; s += kSrWarps * 32)
-    if (valid(s)) M = fmaxf(M, p.part_lse2[(static_cast<size_t>(stream) * p.splits + s) * QR + row]);
+    if (valid(s)) M = fmaxf(M, p.part_lse2[attn_item(p, stream, s) * QR + row]);
 #pragma unroll
   for (int o2 = 16; o2 > 0; o2 >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o2));
   if (lane == 0) s_m[warp] = M;
@@ -764,7 +824,7 @@ __global__ void __launch_bounds__(kSrWarps * 32) attn_split_reduce_kernel(const 
     for (int j = 0; j < 4; ++j) {
       const int s = s0 + j * kSrWarps;
       const bool ok = s < p.splits && valid(s);
-      const size_t item = static_cast<size_t>(stream) * p.splits + s;
+      const size_t item = attn_item(p, stream, ok ? s : 0);
       w4[j] = ok ? p.part_lse2[item * QR + row] : -INFINITY;
 #pragma unroll
       for (int i = 0; i < PER; ++i) v[j][i] = ok ? p.part_o[(item * QR + row) * DP + lane + 32 * i] : 0.f;
@@ -804,6 +864,16 @@ __global__ void __launch_bounds__(kSrWarps * 32) attn_split_reduce_kernel(const 
         if (lane + 32 * i < p.hd)
           xf_write(p.xf_out, xf_nb8(p.batch), b, head * p.hd + lane + 32 * i, Lt > 0.f ? ot[i] / Lt : 0.f, p.xf16);
     }
+    if (p.push) {  // device-initiated exchange straight from the reduce (no pack, no collective)
+#pragma unroll
+      for (int i = 0; i < PER; ++i)
+        if (lane + 32 * i < p.hd) push_value(p, b, q_in_group, lane + 32 * i, Lt > 0.f ? ot[i] / Lt : 0.f);
+      if (lane == 0) push_lse(p, b, q_in_group, Lt > 0.f ? (M + log2f(Lt)) * 0.69314718055994530942f : -INFINITY);
+    }
+  }
+  if (p.push) {
+    __syncthreads();
+    if (threadIdx.x == 0) signal_pushed(p, gridDim.x);
   }
 }
 
@@ -818,7 +888,7 @@ __global__ void __launch_bounds__(256) attn_split_reduce_small_kernel(const Attn
   const int QR = p.qrows;
   const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int row = wg % QR, stream = wg / QR;
-  if (stream >= p.n_streams) return;
+  if (stream < p.n_streams && (stream % p.q_chunks) * QR + row < p.group) {
   int t = stream;
   const int qc = t % p.q_chunks; t /= p.q_chunks;
   const int kvh = t % p.kvh_per_slot; t /= p.kvh_per_slot;
@@ -826,7 +896,6 @@ __global__ void __launch_bounds__(256) attn_split_reduce_small_kernel(const Attn
   const int slot_local = t / p.stream_batch;
   const int rank = (slot_local + p.slot_base) % p.kvp;
   const int qrow = qc * QR + row;
-  if (qrow >= p.group) return;
   const int ntok = static_cast<int>(rr_count(p.total[b], rank, p.chunk, p.kvp));
   const int pages = (ntok + 15) >> 4;
   constexpr int PER = DP / 32;
@@ -837,7 +906,7 @@ __global__ void __launch_bounds__(256) attn_split_reduce_small_kernel(const Attn
     const int pg0 = static_cast<int>((static_cast<long long>(j) * pages) / p.splits);
     const int pg1 = static_cast<int>((static_cast<long long>(j + 1) * pages) / p.splits);
     const bool ok = j < p.splits && pg1 > pg0;
-    const size_t item = static_cast<size_t>(stream) * p.splits + j;
+    const size_t item = attn_item(p, stream, ok ? j : 0);
     w[j] = ok ? p.part_lse2[item * QR + row] : -INFINITY;
 #pragma unroll
     for (int i = 0; i < PER; ++i) v[j][i] = ok ? p.part_o[(item * QR + row) * DP + lane + 32 * i] : 0.f;
@@ -864,6 +933,17 @@ __global__ void __launch_bounds__(256) attn_split_reduce_small_kernel(const Attn
     for (int i = 0; i < PER; ++i)
       if (lane + 32 * i < p.hd)
         xf_write(p.xf_out, xf_nb8(p.batch), b, head * p.hd + lane + 32 * i, L > 0.f ? o[i] / L : 0.f, p.xf16);
+  }
+  if (p.push) {  // device-initiated exchange straight from the reduce
+#pragma unroll
+    for (int i = 0; i < PER; ++i)
+      if (lane + 32 * i < p.hd) push_value(p, b, q_in_group, lane + 32 * i, L > 0.f ? o[i] / L : 0.f);
+    if (lane == 0) push_lse(p, b, q_in_group, L > 0.f ? (M + log2f(L)) * 0.69314718055994530942f : -INFINITY);
+  }
+  }  // active warp
+  if (p.push) {
+    __syncthreads();
+    if (threadIdx.x == 0) signal_pushed(p, gridDim.x);
   }
 }
 

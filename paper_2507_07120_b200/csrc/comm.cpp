@@ -59,6 +59,9 @@ class LoopbackTransport : public Transport {
     hub_->barrier();  // send buffers may be reused
   }
 
+  void host_barrier() override { hub_->barrier(); }
+  void reserve(size_t bytes) override { ensure_tmp(bytes); }
+
   // one device: the peers' buffers are directly addressable
   void map_peers(void* recv, void* flags, std::vector<void*>& recv_out, std::vector<void*>& flags_out) override {
     {

@@ -37,6 +37,12 @@ class Transport {
   // group's kvp pointers in group-rank order (own buffers at this rank's index).
   // Collective over the group (call on every rank, outside stream capture).
   virtual void map_peers(void* recv, void* flags, std::vector<void*>& recv_out, std::vector<void*>& flags_out) = 0;
+  // In-process pools (loopback) only: a host barrier over the ranks, and the
+  // reduction scratch allocated up front. A rank's host thread must never sit
+  // in a device-synchronising call (cudaMalloc / cudaFree / pageable cudaMemcpy)
+  // while another rank's flag-wait kernel spins on the same device waiting for it.
+  virtual void host_barrier() {}
+  virtual void reserve(size_t /*bytes*/) {}
 };
 
 // Shared state of a loopback group (all ranks in one process, one device).

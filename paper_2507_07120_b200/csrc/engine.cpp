@@ -267,6 +267,8 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
     loopback_ = true;
   }
   if (dist_mode_ != HX_POOL_LOCAL) {
+    // the largest collective: the [B x H] fp32 TP partials (loopback scratch allocated now, not mid-step)
+    transport_->reserve(static_cast<size_t>(B_) * H_ * sizeof(float));
     cuda_check(cudaStreamCreateWithFlags(&comm_stream_, cudaStreamNonBlocking), "comm stream");
     hop_events_.resize(static_cast<size_t>(B_) + 1);
     for (auto& e : hop_events_) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -385,6 +387,7 @@ void Engine::alloc() {
   }
   attn_grid_ = std::min(mla_ ? num_sms_ / 2 : num_sms_, n_items_);  // MLA: CTA pairs
   if (std::getenv("HX_FUSED_REDUCE") && std::getenv("HX_FUSED_REDUCE")[0] == '0') fused_ = false;
+  if (std::getenv("HX_A2A_NCCL") && std::getenv("HX_A2A_NCCL")[0] == '1') nccl_a2a_ = true;
   d_stream_done_ = dalloc<int>(static_cast<size_t>(std::max(n_streams_, 1)), "stream done counters");
   d_pushed_ = dalloc<int>(1, "pushed counter");
   if (dist_mode_ != HX_POOL_LOCAL) {
@@ -395,6 +398,11 @@ void Engine::alloc() {
     d_self_flag_ = dalloc<unsigned*>(static_cast<size_t>(kvp_), "self flag table");
     d_send_ = dalloc<float>(static_cast<size_t>(kvp_) * B_ * xchunk_, "exchange send");
     d_recv_ = dalloc<float>(static_cast<size_t>(kvp_) * B_ * xchunk_, "exchange recv");
+    // HX_FLAG_SKIP_COMM stand-ins of the peer tables: every slice and flag stays on this rank
+    const std::vector<float*> sr(static_cast<size_t>(kvp_), d_recv_);
+    const std::vector<unsigned*> sf(static_cast<size_t>(kvp_), d_flags_ + r_);
+    cuda_check(cudaMemcpy(d_self_recv_, sr.data(), sr.size() * sizeof(float*), cudaMemcpyHostToDevice), "self table");
+    cuda_check(cudaMemcpy(d_self_flag_, sf.data(), sf.size() * sizeof(unsigned*), cudaMemcpyHostToDevice), "self table");
     d_parth_ = dalloc<float>(static_cast<size_t>(B_) * H_, "tp partial");
   }
   const size_t part_rows = mla_ ? static_cast<size_t>(kMlaHeads) : static_cast<size_t>(q_rows_);  // rows per item
@@ -584,14 +592,14 @@ void Engine::plan_gemvs() {
 // streaming kernel + epilogue kernel; NCCL's own kernels not counted).
 int64_t Engine::launches_per_step() const {
   const int64_t ffn_k = moe_ ? 7 + (F_ > 0 ? 4 : 0) : 4;  // dense 4; MoE router 2 + route + experts 4 (+ shared 4)
-  const int64_t sr = (mla_ || !fused_) ? 1 : 0;           // split-reduce kernel (fused into GQA attention)
-  if (attn_only_) return f64_ ? 3 + 2 * B_ : 4 + sr + 1;  // xprep, qkv x2, attention, [split-reduce], merge
+  const int64_t sr = 1;                                    // split-reduce kernel (fused under device_exchange())
+  if (attn_only_) return f64_ ? 3 + 2 * B_ : 4 + sr + 1;  // xprep, qkv x2, attention, split-reduce, merge
   const int64_t head = 1 + 3;                              // embed; LM head x2 + argmax finish
   const int64_t mla_k = mla_ ? 2 : 0;                      // W_UK absorption, W_UV
   if (dist_mode_ == HX_POOL_LOCAL)
     return head + L_ * (2 + 1 + sr + (one_src_merge_ ? 0 : 1) + mla_k + 2 + ffn_k);
-  const int64_t attn = device_exchange() ? 2                       // attention (+ push) and the flag wait
-                                         : (hopb_ ? B_ : 1) * (2 + sr);  // [per request] attention, [sr], pack
+  const int64_t attn = device_exchange() ? (hopb_ && fused_ ? 2 : 3)  // attention, [reduce + push], flag wait
+                                         : (hopb_ ? B_ : 1) * (2 + sr);  // [per request] attention, sr, pack
   return head + L_ * (2 + attn + 1 + mla_k + 2 + 1 + ffn_k + 1);  // + merge, O x2, residual, FFN, residual
 }
 
@@ -1164,8 +1172,14 @@ AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) {
   a.splits = b_count == B_ ? splits_ : splits_req_;
   a.n_items = a.n_streams * a.splits;  // HOP-B (one request): splits_req_ balanced page ranges
   a.qscale = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(mla_ ? W_ : D_)));
-  if (!mla_ && fused_) {
+  a.stream_major = std::getenv("HX_STREAM_MAJOR") && std::getenv("HX_STREAM_MAJOR")[0] == '1';  // A/B
+  a.hd = static_cast<int>(D_);
+  a.pushed = d_pushed_;
+  if (fused_ && hopb_ && device_exchange()) {
+    // HOP-B: request-ordered work, each stream reduced (and pushed) in-kernel as
+    // it completes, overlapping the attention of the streams after it
     a.fused = 1;
+    a.stream_major = 1;
     a.stream_done = d_stream_done_;
     a.frag_o = d_frag_o_;
     a.frag_lse = d_frag_lse_;
@@ -1222,11 +1236,12 @@ void Engine::enqueue_attention(int64_t layer) {
 // request b+1's attention runs on the compute stream.
 void Engine::enqueue_exchange_and_attention_dist(int64_t layer) {
   if (device_exchange()) {
-    // HOP-B, device-initiated (overlap.hpp:37-69 at stream granularity): ONE
-    // attention launch in request order whose CTAs reduce each finished stream
-    // and store its slices straight into the peers' receive buffers while the
-    // later requests are still streaming; the last CTA raises this rank's flag
-    // in every peer. No per-request launches, no exchange kernel, no NCCL.
+    // Device-initiated exchange: the split reduce stores each rank's slices
+    // straight into the peers' receive buffers (NVLink P2P / CUDA IPC) and the
+    // last CTA raises this rank's flag in every peer -- no pack kernel, no
+    // collective. HOP-B on (overlap.hpp:37-69, at stream granularity): ONE
+    // request-ordered attention launch whose CTAs reduce and push each stream
+    // as it completes, while the later requests are still streaming.
     AttnParams a = attn_params(layer, 0, B_);
     const bool skip = skip_comm_ & 1;  // measurement: every slice stays on this rank
     a.push = 1;
@@ -1237,6 +1252,14 @@ void Engine::enqueue_exchange_and_attention_dist(int64_t layer) {
     a.xrank = r_;
     launch_attention_kernels(a);
     mark(3);
+    if (loopback_ && !skip) {
+      // in-process pool: every rank's pushes land before any rank's flag wait
+      // runs. A kernel spinning on a flag that another thread's not-yet-launched
+      // kernel raises can deadlock one shared context (lazy module loading
+      // synchronises it); across processes (NCCL pools) the wait spins on the device.
+      cuda_check(cudaStreamSynchronize(stream_), "loopback exchange sync");
+      transport_->host_barrier();
+    }
     cuda_check(launch_wait_flags(skip ? d_flags_ + r_ : d_flags_, skip ? 1 : kvp_, stream_), "exchange wait");
     mark(9);
     return;
@@ -1286,16 +1309,19 @@ void Engine::ensure_peers() {
   if (peers_mapped_ || dist_mode_ == HX_POOL_LOCAL) return;
   std::vector<void*> recv, flags;
   transport_->map_peers(d_recv_, d_flags_, recv, flags);
-  std::vector<float*> pr(static_cast<size_t>(kvp_)), sr(static_cast<size_t>(kvp_), d_recv_);
-  std::vector<unsigned*> pf(static_cast<size_t>(kvp_)), sf(static_cast<size_t>(kvp_), d_flags_ + r_);
+  std::vector<float*> pr(static_cast<size_t>(kvp_));
+  std::vector<unsigned*> pf(static_cast<size_t>(kvp_));
   for (int p = 0; p < kvp_; ++p) {
     pr[static_cast<size_t>(p)] = static_cast<float*>(recv[static_cast<size_t>(p)]);
     pf[static_cast<size_t>(p)] = static_cast<unsigned*>(flags[static_cast<size_t>(p)]) + r_;  // my word in peer p
   }
-  cuda_check(cudaMemcpy(d_peer_recv_, pr.data(), pr.size() * sizeof(float*), cudaMemcpyHostToDevice), "peer table");
-  cuda_check(cudaMemcpy(d_peer_flag_, pf.data(), pf.size() * sizeof(unsigned*), cudaMemcpyHostToDevice), "peer table");
-  cuda_check(cudaMemcpy(d_self_recv_, sr.data(), sr.size() * sizeof(float*), cudaMemcpyHostToDevice), "self table");
-  cuda_check(cudaMemcpy(d_self_flag_, sf.data(), sf.size() * sizeof(unsigned*), cudaMemcpyHostToDevice), "self table");
+  cuda_check(cudaMemcpyAsync(d_peer_recv_, pr.data(), pr.size() * sizeof(float*), cudaMemcpyHostToDevice, stream_),
+             "peer table");
+  cuda_check(cudaMemcpyAsync(d_peer_flag_, pf.data(), pf.size() * sizeof(unsigned*), cudaMemcpyHostToDevice, stream_),
+             "peer table");
+  cuda_check(cudaStreamSynchronize(stream_), "peer table");
+  // in-process pools: nobody launches a flag wait before every rank is past its uploads
+  transport_->host_barrier();
   peers_mapped_ = true;
 }
 
@@ -1441,7 +1467,7 @@ void Engine::decode_step_device(const int32_t* tokens_dev, int32_t* next_dev) {
   if (attn_only_) throw StateError("decode_step needs a full model (attention_only = 0)");
   if (!weights_ready_) throw StateError("weights are not initialised");
   for (int64_t l = 0; l < L_; ++l) require_context(l);
-  if (device_exchange()) ensure_peers();
+  if (device_exchange() && !(skip_comm_ & 1)) ensure_peers();  // skip: the self tables (alloc) suffice
   if (graphs_ && !(loopback_ && skip_comm_ != 3) && !prof_) {
     cudaGraphExec_t exec = nullptr;
     for (auto& g : graphs_cache_)

@@ -207,7 +207,8 @@ class Engine {
   float* d_parth_ = nullptr;   // [B][H] partial products before the TP AllReduce
   cudaStream_t comm_stream_ = nullptr;
   // fused split reduce (GQA) and the device-initiated exchange (HOP-B on)
-  bool fused_ = true;            // HX_FUSED_REDUCE=0: separate split-reduce kernel (A/B)
+  bool fused_ = true;            // HX_FUSED_REDUCE=0: HOP-B keeps the split-reduce kernel (A/B)
+  bool nccl_a2a_ = false;        // HX_A2A_NCCL=1: pack + NCCL grouped send/recv instead of the device exchange
   int* d_stream_done_ = nullptr;
   int* d_pushed_ = nullptr;
   unsigned* d_flags_ = nullptr;  // [kvp] raised by the peer that pushed to this rank
@@ -217,7 +218,9 @@ class Engine {
   unsigned** d_self_flag_ = nullptr;
   bool peers_mapped_ = false;
   void ensure_peers();
-  bool device_exchange() const { return hopb_ && !mla_ && fused_ && dist_mode_ != HX_POOL_LOCAL; }
+  // GQA pools exchange device-initiated: the split reduce (or, under HOP-B, the
+  // attention kernel itself) stores the slices into the peers' receive buffers
+  bool device_exchange() const { return !mla_ && !nccl_a2a_ && dist_mode_ != HX_POOL_LOCAL; }
   std::vector<cudaEvent_t> hop_events_;
   void enqueue_exchange_and_attention_dist(int64_t layer);
   void init_dist_weights(uint64_t seed, bool qkv_hash);

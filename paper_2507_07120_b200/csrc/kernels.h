@@ -68,6 +68,7 @@ struct AttnParams {
   // split merges the stream's partials (split order) into frag_o / frag_lse
   // [slot_local][b][q][DP] (natural-log lse) -- no split-reduce launch.
   int fused;
+  int stream_major;        // work order (attention.cu attn_item): 1 = the splits of a stream adjacent
   int* stream_done;        // [n_streams] completed splits per stream (self-resetting)
   float* frag_o;
   float* frag_lse;

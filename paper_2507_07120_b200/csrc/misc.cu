@@ -3,6 +3,8 @@
 // the round-robin page pool, and hash-RNG weight init directly into the
 // fragment-major layout (values identical to oracle/layer_oracle.hpp).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -526,21 +528,24 @@ cudaError_t launch_pack_exchange(const float* frag_o, const float* frag_lse, int
 // Receive side of the device-initiated exchange: one CTA waits until every
 // peer's attention kernel has raised its flag (system-scope acquire), then
 // lowers it for the next layer. The merge that follows reads the pushed slices.
-__global__ void wait_flags_kernel(unsigned* flags, int n) {
+__global__ void wait_flags_kernel(unsigned* flags, int n, long long max_spin) {
   griddep_wait();  // after this rank's own attention: never holds an SM the attention needs
   griddep_launch_dependents();
   const int i = threadIdx.x;
   if (i >= n) return;
   unsigned v = 0;
-  for (;;) {
+  for (long long it = 0;; ++it) {
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(flags + i) : "memory");
     if (v) break;
+    if (max_spin > 0 && it == max_spin)  // HX_DEBUG_WAIT: report a long wait (keeps waiting)
+      printf("wait_flags: flag %d of %d (%p) not raised after %lld polls\n", i, n, flags + i, it);
     __nanosleep(64);
   }
   flags[i] = 0u;
 }
 cudaError_t launch_wait_flags(unsigned* flags, int n, cudaStream_t s) {
-  return launch_k(wait_flags_kernel, dim3(1), dim3(32 * ((n + 31) / 32)), 0, s, flags, n);
+  static const long long max_spin = std::getenv("HX_DEBUG_WAIT") ? std::atoll(std::getenv("HX_DEBUG_WAIT")) : 0;
+  return launch_k(wait_flags_kernel, dim3(1), dim3(32 * ((n + 31) / 32)), 0, s, flags, n, max_spin);
 }
 
 // x[b][n] += part[b][n]; ss_part[blk][b] = sum over the 128-column block of x^2 (deterministic).

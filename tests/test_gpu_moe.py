@@ -76,10 +76,10 @@ def test_moe_info_counts_expert_weights():
     # qkv + o + router + 8 experts x (gate/up + down), no shared expert
     want = (384 * 256 + 256 * 256 + 128 * 256 + 8 * (128 * 256 + 256 * 64)) * 2
     assert info["weight_bytes_per_layer"] == want
-    # embed + LM head (2) + argmax; per layer qkv (2), attention (its fused split
-    # reduce also writes the O-proj input of this one-source local pool: no
-    # split-reduce or merge kernel), o (2), router (2) + route + 2 x 2 grouped expert launches
-    assert info["kernels_per_step"] == 1 + (5 + 7) * 1 + 3
+    # embed + LM head (2) + argmax; per layer qkv (2), attention, split reduce (which
+    # also writes the O-proj input of this one-source local pool: no merge kernel),
+    # o (2), router (2) + route + 2 x 2 grouped expert launches
+    assert info["kernels_per_step"] == 1 + (6 + 7) * 1 + 3
 
 
 def test_moe_rejects_bad_shapes():

@@ -8,11 +8,13 @@ One GPU of a KVP-sharded Helix pool (TPA = 1, TPF = KVP; one layer of the
 model) is measured alone: rank 0 of a KVP-rank loopback pool with the
 collectives switched off, so every number here is this GPU's real compute:
 
-  * attn_batched_ms -- attention + split-reduce + exchange pack for the whole
-    batch in one launch (HOP-B off);
-  * attn_hopb_ms    -- the same work launched per request (HOP-B on: request
-    b's exchange would overlap request b+1's attention, overlap.hpp:37-69);
-    the difference is the compute-side price of HOP-B's finer launches;
+  * attn_ms_off -- attention + split-reduce + exchange pack for the whole
+    batch (HOP-B off: the exchange follows, fully exposed);
+  * attn_ms_on  -- HOP-B on as this engine implements it: ONE request-ordered
+    attention launch whose CTAs reduce each finished stream and store its
+    slices straight into the peers' receive buffers while later requests
+    stream (overlap.hpp:37-69 at stream granularity; here the slices stay on
+    this rank), plus the receive-side flag wait;
   * layer_ms_off / layer_ms_on -- the whole layer (QKV .. FFN), eager launches.
 
 The all-to-all itself needs peers (one B200 here), so its duration comes from
@@ -70,7 +72,7 @@ def point(P, Loopback, spec, kvp, S, B, steps=5):
     eng = P.HelixDecoder(spec, tpa=1, kvp=kvp, batch=B, capacity=S + 64 * kvp, layers=1, vocab=4096,
                          use_graphs=False, pool=2, rank=0, loopback=lb, hopb=True)
     lib = P.lib()
-    lib.hx_engine_set_flag(eng._h, 1, 3)  # collectives off (no peers on one GPU)
+    lib.hx_engine_set_flag(eng._h, 1, 3)  # no peers on one GPU: slices stay on this rank, all-reduces off
     eng.init_weights(2507, qkv="hash")
     eng.fill_kv_hash(S, 2507)
     tok = torch.randint(0, 4096, (B,), dtype=torch.int32, device="cuda")
@@ -91,23 +93,26 @@ def point(P, Loopback, spec, kvp, S, B, steps=5):
         e1.record(stream)
         e1.synchronize()
         key = "on" if hopb else "off"
-        # attention kernel + split reduce + pack (kinds 2, 3): the compute HOP-B overlaps
-        out[f"attn_{'hopb' if hopb else 'batched'}_ms"] = float(prof[2] + prof[3])
+        # off: batched attention + split reduce + pack (kinds 2, 3); on: ONE request-ordered
+        # attention launch that reduces each stream and pushes its slices as it completes
+        # (kinds 2, 3), then the flag wait (kind 9)
+        out[f"attn_ms_{key}"] = float(prof[2] + prof[3])
+        out[f"flag_wait_ms_{key}"] = float(prof[9])
         out[f"layer_ms_{key}"] = e0.elapsed_time(e1) / steps
+    streams = eng.info()["attn_streams"]
     eng.close()
-    t = a2a_time(H, Hsz, B, kvp) * 1e3  # ms, whole batch
-    c_on = out["attn_hopb_ms"] / B
-    c_off = out["attn_batched_ms"] / B
-    span_on = hopb_schedule(B, c_on, t / B, True)
-    span_off = hopb_schedule(B, c_off, t / B, False)
+    t = a2a_time(H, Hsz, B, kvp) * 1e3  # ms, whole batch, reference alpha-beta model
+    # off: the exchange follows the whole batch's attention (fully exposed);
+    # on: each stream's slices leave as the stream completes -- the reference's
+    # hopb_schedule at the kernel's exchange granularity (R = streams)
+    span_on = hopb_schedule(streams, out["attn_ms_on"] / streams, t / streams, True)
+    exp_on = max(0.0, span_on - out["attn_ms_on"]) + out["flag_wait_ms_on"]
     out.update({
-        "a2a_ms_modeled": t,
-        "exposed_a2a_ms_off": max(0.0, span_off - out["attn_batched_ms"]),
-        "exposed_a2a_ms_on": max(0.0, span_on - out["attn_hopb_ms"]),
-        # what HOP-B buys end to end at this point: (off span) - (on span), incl. its launch price
-        "hopb_gain_ms": span_off - span_on,
+        "streams": streams, "a2a_ms_modeled": t, "exposed_a2a_ms_off": t, "exposed_a2a_ms_on": exp_on,
+        "a2a_hidden_frac": (1.0 - max(0.0, span_on - out["attn_ms_on"]) / t) if t > 0 else None,
+        # what HOP-B buys end to end at this point, its compute price included
+        "hopb_gain_ms": (out["attn_ms_off"] + t) - (out["attn_ms_on"] + exp_on),
     })
-    out["a2a_hidden_frac"] = 1.0 - out["exposed_a2a_ms_on"] / t if t > 0 else None
     return out
 
 
