@@ -494,28 +494,31 @@ def ours(a):
         ms = timed(a.steps, a.warmup)
         hopb = None
         if world > 1:
-            # exposed all-to-all with and without HOP-B (overlap.hpp:37-69): same resident pool,
-            # runtime switches; "no a2a" replaces the exchange by a local copy (measurement only)
+            # exposed KVP exchange per mode (overlap.hpp:37-69): same resident pool, runtime
+            # switches; "no a2a" keeps every slice on its rank (measurement only)
             def setf(flag, v):
                 P._lib.check(P.lib().hx_engine_set_flag(eng._h, flag, v), eng._h)
             off = a.warmup + a.steps
 
-            def run_mode(hopb_on, skip_a2a):
+            def run_mode(collective, hopb_on, skip_a2a):
+                setf(3, int(collective))
                 setf(2, int(hopb_on))
                 setf(1, int(skip_a2a))
                 for i in range(a.warmup):
                     dev_step(off + i)
                 return timed(a.steps, off + a.warmup)
-            ms_on = run_mode(True, False)
-            ms_on_noa2a = run_mode(True, True)   # same per-request launches, exchange replaced by a local copy
-            ms_off_noa2a = run_mode(False, True)
+            hopb = {"headline": "device exchange, HOP-B off (the line's ms_per_step)"}
+            for name, coll, hb in (("collective_a2a", 1, 0), ("device", 0, 0), ("device_hopb", 0, 1)):
+                with_x = ms if name == "device" else run_mode(coll, hb, 0)
+                no_x = run_mode(coll, hb, 1)
+                hopb[name] = {"ms_per_step": with_x, "ms_per_step_no_a2a": no_x,
+                              "exposed_a2a_ms": max(0.0, with_x - no_x)}
             setf(1, 0)
             setf(2, 0)
-            exp_on, exp_off = max(0.0, ms_on - ms_on_noa2a), max(0.0, ms - ms_off_noa2a)
-            hopb = {"ms_per_step_off": ms, "ms_per_step_on": ms_on, "ms_per_step_no_a2a_off": ms_off_noa2a,
-                    "ms_per_step_no_a2a_on": ms_on_noa2a, "exposed_a2a_ms_on": exp_on, "exposed_a2a_ms_off": exp_off,
-                    "a2a_hidden_frac": (1.0 - exp_on / exp_off) if exp_off > 0 else None,
-                    "hopb_net_ms": ms - ms_on, "headline": "HOP-B off"}
+            setf(3, 0)
+            e_c, e_h = hopb["collective_a2a"]["exposed_a2a_ms"], hopb["device_hopb"]["exposed_a2a_ms"]
+            hopb["hopb_hidden_frac_vs_collective"] = (1.0 - e_h / e_c) if e_c > 0 else None
+            hopb["hopb_net_ms_vs_device"] = hopb["device"]["ms_per_step"] - hopb["device_hopb"]["ms_per_step"]
     clocks = clk.summary(dev)
     # e2e through the public API: pinned host tokens in, host next tokens out, every
     # step -- after the clock sampler has stopped: its nvidia-smi polling contends

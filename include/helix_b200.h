@@ -113,7 +113,13 @@ typedef struct hx_engine_info {
   int64_t w_dtype;                 /* HX_W_BF16 / HX_W_FP8_E4M3 */
   int64_t comm_ranks;              /* ranks of the pool's world communicator (1: local pool) */
   int64_t nccl_version;            /* ncclGetVersion of the linked NCCL (0: no NCCL pool) */
+  int64_t exchange;                /* KVP fragment exchange: HX_EXCHANGE_* (distributed pools) */
 } hx_engine_info;
+
+#define HX_EXCHANGE_NONE 0      /* local pool: the merge reads every rank's fragment */
+#define HX_EXCHANGE_COLLECTIVE 1 /* pack + grouped send/recv all-to-all (NCCL, or loopback copies) */
+#define HX_EXCHANGE_DEVICE 2    /* split reduce stores into the peers' receive buffers, flag-signalled */
+#define HX_EXCHANGE_DEVICE_HOPB 3 /* attention kernel reduces + pushes each stream as it completes */
 
 const char* hx_version(void);
 const char* hx_last_error(const hx_engine* e); /* e may be NULL: last create/global error */
@@ -223,6 +229,7 @@ int64_t hx_exchange_layout(int64_t q_per_group, int64_t head_size, int64_t kvp, 
  * copy, 2 = skip the all-reduces -- exposed-communication measurement. */
 #define HX_FLAG_SKIP_COMM 1
 #define HX_FLAG_HOPB 2
+#define HX_FLAG_COLLECTIVE_A2A 3 /* 1: exchange through the collective transport instead of device stores */
 int hx_engine_set_flag(hx_engine* e, int32_t flag, int32_t value);
 /* MoE: experts held by this device that the last step's router selected in the
  * last layer (the grouped GEMVs streamed exactly these weight blocks); 0 for

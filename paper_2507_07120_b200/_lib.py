@@ -42,7 +42,8 @@ class EngineInfo(C.Structure):
     _fields_ = [("kv_bytes_per_layer", i64), ("weight_bytes_per_layer", i64), ("head_bytes", i64),
                 ("attn_streams", i64), ("attn_splits", i64), ("attn_items", i64), ("attn_grid", i64),
                 ("kernels_per_step", i64), ("page_cap", i64), ("head_dim_padded", i64), ("kv_dtype", i64),
-                ("w_dtype", i64), ("comm_ranks", i64), ("nccl_version", i64)]
+                ("w_dtype", i64), ("comm_ranks", i64), ("nccl_version", i64),
+                ("exchange", i64)]
 
 
 EXPORTS = {

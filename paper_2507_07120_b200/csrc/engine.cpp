@@ -1308,7 +1308,15 @@ void Engine::enqueue_exchange_and_attention_dist(int64_t layer) {
 void Engine::ensure_peers() {
   if (peers_mapped_ || dist_mode_ == HX_POOL_LOCAL) return;
   std::vector<void*> recv, flags;
-  transport_->map_peers(d_recv_, d_flags_, recv, flags);
+  try {
+    transport_->map_peers(d_recv_, d_flags_, recv, flags);
+  } catch (const std::exception& ex) {
+    // no peer mapping on this system (e.g. CUDA IPC unavailable): exchange through the collective
+    std::fprintf(stderr, "helix-b200: device exchange unavailable (%s); using the collective all-to-all\n",
+                 ex.what());
+    nccl_a2a_ = true;
+    return;
+  }
   std::vector<float*> pr(static_cast<size_t>(kvp_));
   std::vector<unsigned*> pf(static_cast<size_t>(kvp_));
   for (int p = 0; p < kvp_; ++p) {
@@ -1521,6 +1529,9 @@ void Engine::set_flag(int flag, int value) {
   } else if (flag == HX_FLAG_HOPB) {
     hopb_ = value != 0;
     drop_graphs();
+  } else if (flag == HX_FLAG_COLLECTIVE_A2A) {
+    nccl_a2a_ = value != 0;
+    drop_graphs();
   } else {
     throw std::invalid_argument("unknown engine flag");
   }
@@ -1730,6 +1741,10 @@ void Engine::info(hx_engine_info* o) const {
   o->w_dtype = w8_ ? HX_W_FP8_E4M3 : HX_W_BF16;
   o->comm_ranks = transport_ ? transport_->world() : 1;
   o->nccl_version = transport_ ? transport_->nccl_version() : 0;
+  o->exchange = dist_mode_ == HX_POOL_LOCAL ? HX_EXCHANGE_NONE
+                : !device_exchange()       ? HX_EXCHANGE_COLLECTIVE
+                : (hopb_ && fused_)        ? HX_EXCHANGE_DEVICE_HOPB
+                                           : HX_EXCHANGE_DEVICE;
 }
 
 }  // namespace hx
