@@ -215,18 +215,19 @@ def pool_slice(a, preset, S, ep, w_dtype="bf16", kv_dtype="bf16"):
                       "expert_bytes_streamed": active * 3 * H * spec.moe.expert_ffn_dim * (1 if w_dtype == "fp8" else 2)}
     else:
         K = spec.kv_heads
-        ekv, ew = (1 if kv_dtype == "fp8" else 2), (1 if w_dtype == "fp8" else 2)
+        ekv, ew = KV_ELEM_BYTES[kv_dtype], (1 if w_dtype == "fp8" else 2)
         # roofline.hpp:17-48: QKV duplicated per KVP rank, O and FFN sharded over N
         kv_bytes, w_bytes = step_bytes_per_gpu(spec, B, s_loc * N, N, 1, ekv, ew)
         out["workload"] = ("llama405b-like layer, one GPU of TPA=1 x KVP=8 (TPF=8): %d KV heads x %d tokens x B=%d; "
                            "QKV replicated, W_O rows and FFN features 1/8; collectives off (1 GPU)" % (K, s_loc, B))
         out["attention"] = {
-            "kernel": ("attn_decode_kernel<128,12,2,2,fp8,W16>" if kv_dtype == "fp8" else "attn_decode_kernel<128,8,2,2,W16>")
+            "kernel": {"fp8": "attn_decode_kernel<128,12,2,2,fp8,W16>", "fp4": "attn_decode_kernel<128,8,4,2,fp4,W16>",
+                       "bf16": "attn_decode_kernel<128,8,2,2,W16>"}[kv_dtype]
                       + " (TMA bulk-copy page ring, mma.sync)", "launch_ms": att_ms,
             "algorithmic_kv_bytes": kv_bytes,
             "roofline": {"bound": "hbm", "achieved": kv_bytes / (att_ms * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                          "frac": kv_bytes / (att_ms * 1e-3) / 1e9 / hbm,
-                         "traffic": None if kv_dtype == "fp8" else ncu_traffic("attention_405b_slice")}}
+                         "traffic": ncu_traffic("attention_405b_slice" + ("" if kv_dtype == "bf16" else "_" + kv_dtype))}}
         out["layer_roofline"] = {"bound": "hbm", "algorithmic_bytes": kv_bytes + w_bytes, "weight_bytes": w_bytes,
                                  "t_roof_ms": (kv_bytes + w_bytes) / hbm / 1e6,
                                  "achieved_gbs": (kv_bytes + w_bytes) / (ms * 1e-3) / 1e9,
@@ -292,7 +293,12 @@ def kvp_slices(a):
     return out
 
 
-def fp8_kv_line(a, w_dtype="bf16"):
+KV_ELEM_BYTES = {"bf16": 2.0, "fp8": 1.0, "fp4": 17.0 / 32.0}  # fp4: e2m1 nibble + one exponent byte per 32
+KV_KERNEL = {"bf16": "attn_decode_kernel<128,7,3,1,bf16>", "fp8": "attn_decode_kernel<128,10,4,1,fp8>",
+             "fp4": "attn_decode_kernel<128,10,6,1,fp4>"}
+
+
+def fp8_kv_line(a, w_dtype="bf16", kv_dtype="fp8"):
     """the configs[1] workload with FP8 (e4m3) KV pages
     (kv_dtype="fp8", attention MMAs in f16 on the exact widened values), and
     with w_dtype="fp8" also e4m3 GEMV weights (per-output power-of-two scales).
@@ -306,7 +312,7 @@ def fp8_kv_line(a, w_dtype="bf16"):
     spec = P.model.PRESETS["llama3-8b-like"]
     B, S, L = a.batch, a.context, a.layers
     eng = P.HelixDecoder(spec, tpa=1, kvp=1, batch=B, capacity=S + 4 * (a.warmup + a.steps + 16) + 64, layers=L,
-                         kv_dtype="fp8", w_dtype=w_dtype)
+                         kv_dtype=kv_dtype, w_dtype=w_dtype)
     eng.init_weights(2507, qkv="hash")
     eng.fill_kv_hash(S, 2507)
     stream = torch.cuda.ExternalStream(eng.stream())
@@ -326,19 +332,20 @@ def fp8_kv_line(a, w_dtype="bf16"):
     P.lib().hx_profile_step(eng._h, 2, prof.ctypes.data_as(ctypes.POINTER(ctypes.c_double)))
     att = prof[2] / L
     s_now = eng.total_tokens(0, 0)
-    kv_bytes = B * spec.kv_heads * s_now * spec.head_size * 2 * 1  # K+V, 1 byte per element
+    kv_bytes = B * spec.kv_heads * s_now * spec.head_size * 2 * KV_ELEM_BYTES[kv_dtype]  # K+V, algorithmic
     hbm, _ = peaks()
     info = eng.info()
     eng.close()
-    return {"kv_dtype": "fp8_e4m3", "w_dtype": "fp8_e4m3" if w_dtype == "fp8" else "bf16",
+    return {"kv_dtype": {"fp8": "fp8_e4m3", "fp4": "fp4_e2m1 (32-dim blocks, pow2 scales)"}[kv_dtype],
+            "w_dtype": "fp8_e4m3" if w_dtype == "fp8" else "bf16",
             "weight_bytes_resident": info["weight_bytes_per_layer"] * L + info["head_bytes"], "ms_per_step": ms, "value": B / (ms * 1e-3), "unit": UNIT,
             "breakdown_ms": {k: float(v) for k, v in zip(
                 ["embed", "qkv", "attention", "split_reduce", "o_proj", "gate_up", "down", "lm_head", "merge"], prof)},
-            "attention_roofline": {"bound": "hbm", "kernel": "attn_decode_kernel<128,10,4,1,fp8>",
+            "attention_roofline": {"bound": "hbm", "kernel": KV_KERNEL[kv_dtype],
                                    "algorithmic_bytes_per_launch": kv_bytes, "launch_ms": att,
                                    "achieved": kv_bytes / (att * 1e-3) / 1e9, "peak": hbm, "unit": "GB/s",
                                    "frac": kv_bytes / (att * 1e-3) / 1e9 / hbm,
-                                   "traffic": ncu_traffic("attention_fp8")},
+                                   "traffic": ncu_traffic("attention_" + kv_dtype)},
             "kv_bytes_per_layer": info["kv_bytes_per_layer"]}
 
 
@@ -618,6 +625,10 @@ def ours(a):
             line["fp8_kv_w"] = fp8_kv_line(a, w_dtype="fp8")
         except Exception as ex:  # reported, never fatal for the headline number
             line["fp8_kv_w"] = {"error": str(ex)[:300]}
+        try:  # FP4 (e2m1) KV -- the paper's evaluation precision -- with FP8 weights
+            line["fp4_kv_fp8_w"] = fp8_kv_line(a, w_dtype="fp8", kv_dtype="fp4")
+        except Exception as ex:  # reported, never fatal for the headline number
+            line["fp4_kv_fp8_w"] = {"error": str(ex)[:300]}
     if world == 1 and not a.no_slices:
         eng.close()  # free the 150 GB pool before the 8-GPU-pool slices
         try:
@@ -629,7 +640,8 @@ def ours(a):
                 ("deepseek_slice", "deepseek-r1-like", a.slice_context, 8, "bf16", "bf16"),
                 ("llama405b_slice_fp8w", "llama405b-like", a.slice_context, 1, "fp8", "bf16"),
                 ("deepseek_slice_fp8w", "deepseek-r1-like", a.slice_context, 8, "fp8", "bf16"),
-                ("llama405b_slice_fp8", "llama405b-like", a.slice_context, 1, "fp8", "fp8")):
+                ("llama405b_slice_fp8", "llama405b-like", a.slice_context, 1, "fp8", "fp8"),
+                ("llama405b_slice_fp4", "llama405b-like", a.slice_context, 1, "fp8", "fp4")):
             try:
                 line[key] = pool_slice(a, preset, ctx, ep, wd, kd)
                 line[key]["w_dtype"] = wd

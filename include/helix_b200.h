@@ -98,6 +98,8 @@ typedef struct hx_runtime_config {
 #define HX_KV_BF16 0
 #define HX_KV_FP8_E4M3 1
 #define HX_KV_F64 2 /* exact harness: fp64 shards, weights, projections and merges (DecodeHarness<double>) */
+#define HX_KV_FP4_E2M1 3 /* GQA: e2m1 codes, one power-of-two scale per 32 dims of a token's K or V row
+                            (MX-style blocks; head_size 32/64/128) -- the paper's FP4 */
 #define HX_W_BF16 0
 #define HX_W_FP8_E4M3 1
 

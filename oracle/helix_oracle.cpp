@@ -40,6 +40,37 @@ double round_e4m3(double x) {
   return std::copysign(r, x);
 }
 
+void round_e2m1_block(double* x, i64 n) {
+  double amax = 0.0;
+  for (i64 i = 0; i < n; ++i) amax = std::max(amax, std::fabs(x[i]));
+  int e = 0;
+  if (amax > 0.0) {
+    int k = 0;
+    const double m = std::frexp(amax / 6.0, &k);  // amax / 6 = m 2^k, m in [0.5, 1)
+    e = (m == 0.5) ? k - 1 : k;                   // smallest e with 6 2^e >= amax
+    e = std::min(13, std::max(-20, e));
+  }
+  static const double grid[8] = {0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0};
+  for (i64 i = 0; i < n; ++i) {
+    const double t = std::ldexp(std::fabs(x[i]), -e);
+    int best = 0;
+    for (int c = 1; c < 8; ++c) {  // nearest grid point; a tie goes to the even code
+      const double dc = std::fabs(t - grid[c]), db = std::fabs(t - grid[best]);
+      if (dc < db || (dc == db && (c & 1) == 0)) best = c;
+    }
+    x[i] = std::copysign(std::ldexp(grid[best], e), x[i]);
+  }
+}
+
+void DecodeHarness::round_kv_rows(Mat& m) const {
+  if (!kv_fp4_) {
+    for (double& e : m.a) e = round_kv(e);
+    return;
+  }
+  for (i64 r = 0; r < m.rows; ++r)
+    for (i64 c0 = 0; c0 < m.cols; c0 += 32) round_e2m1_block(m.row(r) + c0, std::min<i64>(32, m.cols - c0));
+}
+
 double logit_scale(i64 width) { return 1.0 / std::sqrt(static_cast<double>(width)); }
 
 namespace {
@@ -298,8 +329,8 @@ void DecodeHarness::grow_random(i64 n, std::mt19937_64& rng) {
   for (i64 i = 0; i < n; ++i) {
     Mat v = random_matrix(rng, dims_.kv_heads, dims_.head_size);
     Mat k = random_matrix(rng, dims_.kv_heads, dims_.head_size);
-    for (double& e : k.a) e = round_kv(e);
-    for (double& e : v.a) e = round_kv(e);
+    round_kv_rows(k);
+    round_kv_rows(v);
     cache_.append_round_robin(k, v);
   }
 }
@@ -337,8 +368,8 @@ void DecodeHarness::project_kv(const std::vector<double>& x, Mat& k, Mat& v) con
 void DecodeHarness::append_projected(const std::vector<double>& x) {
   Mat k, v;
   project_kv(x, k, v);
-  for (double& e : k.a) e = round_kv(e);
-  for (double& e : v.a) e = round_kv(e);
+  round_kv_rows(k);
+  round_kv_rows(v);
   cache_.append_round_robin(k, v);
 }
 

@@ -55,6 +55,12 @@ double round_bf16(double x);
 // 448, no infinities) value, ties to even, saturating at +-448 -- the B200
 // path's optional FP8 KV storage.
 double round_e4m3(double x);
+// FP4 E2M1 block storage (PAPER.md:158 evaluates at FP4): the n values of one
+// block share a power-of-two scale 2^e, e = the smallest exponent with
+// 6 * 2^e >= max |x| (clamped to [-20, 13]); each value is rounded to the
+// nearest e2m1 grid point {0, 0.5, 1, 1.5, 2, 3, 4, 6} * 2^e, ties to the even
+// code, saturating at 6 * 2^e. In place; blocks are 32 dims of one token's row.
+void round_e2m1_block(double* x, i64 n);
 
 // ---- single-head primitives (attention.hpp:35-78) ----
 struct HeadFragment {
@@ -170,7 +176,11 @@ class DecodeHarness {
   // weights stay bf16. Applies to KV grown or appended after the call.
   void set_kv_fp8(bool on) { kv_fp8_ = on; }
   bool kv_fp8() const { return kv_fp8_; }
+  // FP4 (e2m1, blocks of 32 dims of a token's K or V row per KV head)
+  void set_kv_fp4(bool on) { kv_fp4_ = on; }
   double round_kv(double x) const { return kv_fp8_ ? round_e4m3(x) : (bf16_ ? round_bf16(x) : x); }
+  // Storage rounding of one token's K or V rows [kv heads x width].
+  void round_kv_rows(Mat& m) const;
   // Last step's merged lse per query head (natural log), for kernel parity.
   const std::vector<double>& last_lse() const { return last_lse_; }
 
@@ -180,6 +190,7 @@ class DecodeHarness {
   i64 tpa_, kvp_;
   bool bf16_;
   bool kv_fp8_ = false;
+  bool kv_fp4_ = false;
   Mat wq_, wk_, wv_;
   ShardedKVCache cache_;
   std::vector<Message> transcript_;

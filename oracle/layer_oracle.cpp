@@ -179,9 +179,11 @@ void ModelOracle::grow_hash(i64 layer, i64 request, i64 n) {
             static_cast<std::uint64_t>(dd);
         const double kv = hash_unit(seed_, hash_stream(kCacheK, layer), idx);
         const double vv = hash_unit(seed_, hash_stream(kCacheV, layer), idx);
-        k(kh, dd) = kv_fp8_ ? round_e4m3(kv) : (bf16_ ? round_bf16(kv) : kv);
-        v(kh, dd) = kv_fp8_ ? round_e4m3(vv) : (bf16_ ? round_bf16(vv) : vv);
+        k(kh, dd) = kv;
+        v(kh, dd) = vv;
       }
+    h.round_kv_rows(k);  // the harness's storage rounding (bf16 / e4m3 / e2m1 blocks)
+    h.round_kv_rows(v);
     h.cache().append_round_robin(k, v);
   }
 }

@@ -130,6 +130,10 @@ class ModelOracle {
     kv_fp8_ = on;
     for (auto& h : h_) h.set_kv_fp8(on);
   }
+  // FP4 (e2m1 blocks) KV storage for the GQA caches (DecodeHarness::set_kv_fp4).
+  void set_kv_fp4(bool on) {
+    for (auto& h : h_) h.set_kv_fp4(on);
+  }
 
  private:
   ModelDims d_;

@@ -46,6 +46,8 @@ int oracle_harness_create(i64 q, i64 k, i64 hsz, i64 tpa, i64 kvp, i64 chunk, st
 }
 void oracle_harness_free(void* h) { delete static_cast<DecodeHarness*>(h); }
 void oracle_harness_set_kv_fp8(void* h, int on) { static_cast<DecodeHarness*>(h)->set_kv_fp8(on != 0); }
+void oracle_harness_set_kv_fp4(void* h, int on) { static_cast<DecodeHarness*>(h)->set_kv_fp4(on != 0); }
+void oracle_round_e2m1_block(double* x, i64 n) { round_e2m1_block(x, n); }
 
 int oracle_harness_grow_random(void* h, i64 n, void* rng) {
   return guard([&] {
@@ -280,6 +282,7 @@ int oracle_model_route_gaps(void* mp, double* out) {
 }
 void oracle_model_free(void* m) { delete static_cast<ModelOracle*>(m); }
 void oracle_model_set_kv_fp8(void* m, int on) { static_cast<ModelOracle*>(m)->set_kv_fp8(on != 0); }
+void oracle_model_set_kv_fp4(void* m, int on) { static_cast<ModelOracle*>(m)->set_kv_fp4(on != 0); }
 
 int oracle_model_grow_random(void* m, i64 layer, i64 request, i64 n, void* rng) {
   return guard([&] {

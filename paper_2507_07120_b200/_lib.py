@@ -34,7 +34,7 @@ class RuntimeConfig(C.Structure):
                 ("kv_dtype", i32), ("w_dtype", i32), ("reserved", i32)]
 
 
-KV_DTYPES = {"bf16": 0, "fp8": 1, "fp8_e4m3": 1, "f64": 2}
+KV_DTYPES = {"bf16": 0, "fp8": 1, "fp8_e4m3": 1, "f64": 2, "fp4": 3, "fp4_e2m1": 3}
 W_DTYPES = {"bf16": 0, "fp8": 1, "fp8_e4m3": 1}
 
 

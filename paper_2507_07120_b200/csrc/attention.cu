@@ -50,27 +50,98 @@ struct StageMeta {
   int rows;         // valid query rows in this stream (<= 8 * QC)
 };
 
-template <int DP, bool KV8>
+template <int DP, int KVF>
 struct AttnCfg {
   static constexpr int KS = DP / 16;     // k-steps over the head dim
   static constexpr int ND = DP / 8;      // PV n-tiles
-  static constexpr uint32_t PAGE = (KV8 ? 32u : 64u) * DP;  // kv_layout.cuh
+  // kv_layout.cuh: bf16 64*DP, fp8 32*DP, fp4 17*DP bytes per page
+  static constexpr uint32_t PAGE = KVF == 2 ? 17u * DP : (KVF == 1 ? 32u : 64u) * DP;
 };
 
-// KV8: FP8 e4m3 pages; each lane's 8-byte chunk widens to the f16 register image
-// of the bf16 path's 16-byte chunk, and the MMAs run in f16 (q and P split into
-// f16 terms) -- e4m3 values are exact in f16, so the only rounding is the e4m3
-// storage itself.
-template <bool KV8>
-__device__ __forceinline__ uint4 load_kv_frag(uint32_t addr16, uint32_t addr8) {
-  if constexpr (KV8) {
-    const uint2 b = lds64(addr8);
+// KVF = 1: FP8 e4m3 pages; each lane's 8-byte chunk widens to the f16 register
+// image of the bf16 path's 16-byte chunk. KVF = 2: FP4 e2m1 pages; each lane's
+// 4-byte chunk widens (cvt e2m1x2 -> f16x2) and is scaled by its block's 2^e in
+// f16 (exact, fp8.cuh). Either way the MMAs run in f16 (q and P split into f16
+// terms); the only rounding is the storage itself.
+__device__ __forceinline__ void e2m1x8_to_f16x2x4(uint32_t w, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm("{\n .reg .b8 b0, b1, b2, b3;\n mov.b32 {b0, b1, b2, b3}, %4;\n"
+      " cvt.rn.f16x2.e2m1x2 %0, b0;\n cvt.rn.f16x2.e2m1x2 %1, b1;\n"
+      " cvt.rn.f16x2.e2m1x2 %2, b2;\n cvt.rn.f16x2.e2m1x2 %3, b3;\n}"
+      : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+      : "r"(w));
+}
+// f16 bits of 2^e for a stored block exponent byte (e + 127), e in [-20, 13]
+__device__ __forceinline__ uint32_t f16_pow2(uint32_t ebyte) {
+  const int e = static_cast<int>(ebyte) - 127;
+  return e >= -14 ? static_cast<uint32_t>(e + 15) << 10 : 1u << (e + 24);
+}
+__device__ __forceinline__ uint32_t hmul2(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+__device__ __forceinline__ uint32_t lds8(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t lds32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+// Lane chunk ci of the page's K region (tokens 8 nt + g, 32-dim group kp):
+// the register image of the bf16 chunk (kv_layout.cuh).
+template <int DP, int KVF>
+__device__ __forceinline__ uint4 load_k(uint32_t pbase, int ci) {
+  if constexpr (KVF == 0) {
+    return lds128(pbase + ci * 16);
+  } else if constexpr (KVF == 1) {
+    const uint2 b = lds64(pbase + ci * 8);
     uint4 r;
     e4m3x4_to_f16x2x2(b.x, r.x, r.y);
     e4m3x4_to_f16x2x2(b.y, r.z, r.w);
     return r;
   } else {
-    return lds128(addr16);
+    uint4 r;
+    e2m1x8_to_f16x2x4(lds32(pbase + ci * 4), r.x, r.y, r.z, r.w);
+    const int grp = ci >> 5, kp = grp % (DP / 32), nt = grp / (DP / 32);
+    const int t = nt * 8 + ((ci & 31) >> 2);
+    const uint32_t s = f16_pow2(lds8(pbase + 16 * DP + t * (DP / 32) + kp));
+    const uint32_t ss = s | (s << 16);
+    r.x = hmul2(r.x, ss);
+    r.y = hmul2(r.y, ss);
+    r.z = hmul2(r.z, ss);
+    r.w = hmul2(r.w, ss);
+    return r;
+  }
+}
+// Lane chunk ci of the page's V region (dims 16 nd2 + g, 16 nd2 + 8 + g; tokens
+// 2c, 2c+1 in .x/.z and 2c+8, 2c+9 in .y/.w).
+template <int DP, int KVF>
+__device__ __forceinline__ uint4 load_v(uint32_t pbase, int ci) {
+  if constexpr (KVF == 0) {
+    return lds128(pbase + 32 * DP + ci * 16);
+  } else if constexpr (KVF == 1) {
+    const uint2 b = lds64(pbase + 16 * DP + ci * 8);
+    uint4 r;
+    e4m3x4_to_f16x2x2(b.x, r.x, r.y);
+    e4m3x4_to_f16x2x2(b.y, r.z, r.w);
+    return r;
+  } else {
+    uint4 r;
+    e2m1x8_to_f16x2x4(lds32(pbase + 8 * DP + ci * 4), r.x, r.y, r.z, r.w);
+    const int c = ci & 3, grp = (ci >> 5) >> 1;
+    const uint32_t sb = pbase + 16 * DP + DP / 2 + grp;  // V exponents [16 tokens][DP/32]
+    const uint32_t lo = f16_pow2(lds8(sb + (2 * c) * (DP / 32))) | (f16_pow2(lds8(sb + (2 * c + 1) * (DP / 32))) << 16);
+    const uint32_t hi =
+        f16_pow2(lds8(sb + (2 * c + 8) * (DP / 32))) | (f16_pow2(lds8(sb + (2 * c + 9) * (DP / 32))) << 16);
+    r.x = hmul2(r.x, lo);
+    r.y = hmul2(r.y, hi);
+    r.z = hmul2(r.z, lo);
+    r.w = hmul2(r.w, hi);
+    return r;
   }
 }
 template <bool KV8>
@@ -246,9 +317,10 @@ __device__ __forceinline__ void fused_stream_done(const AttnParams& p, int strea
 // 3·2·KS + 2·ND MMAs (80 at Hsz 128) instead of two 8-row passes (96); the
 // per-item query fragment image (3 terms x KS k-steps x 32 lanes x 16 B) lives
 // in shared memory, keeping registers at the 8-row path's level.
-template <int DP, int NWC, int NSTAGE, int QC, bool KV8, bool W16>
+template <int DP, int NWC, int NSTAGE, int QC, int KVF, bool W16>
 __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const AttnParams p) {
-  using Cfg = AttnCfg<DP, KV8>;
+  using Cfg = AttnCfg<DP, KVF>;
+  constexpr bool KV8 = KVF != 0;  // f16 MMAs on the widened FP8 / FP4 operands
   static_assert(NWC % QC == 0, "query chunks must divide the consumer warps");
   static_assert(!W16 || QC == 2, "W16: 16 query rows per warp");
   constexpr int QR = 8 * QC;           // query rows per item
@@ -436,7 +508,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
 #pragma unroll
           for (int kp = 0; kp < Cfg::KS / 2; ++kp) {
             const int ci = (nt * (Cfg::KS / 2) + kp) * 32 + lane;
-            const uint4 kf = load_kv_frag<KV8>(pbase + ci * 16, pbase + ci * 8);
+            const uint4 kf = load_k<DP, KVF>(pbase, ci);
 #pragma unroll
             for (int term = 0; term < kQTerms; ++term) {
               const uint4 qa = lds128(qimg_base + ((term * Cfg::KS + 2 * kp) * 32 + lane) * 16);
@@ -507,11 +579,10 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
         const uint32_t q0 = pack_kv<KV8>(pl[0][0], pl[0][1]), q1 = pack_kv<KV8>(pl[1][0], pl[1][1]);
         const uint32_t q2 = pack_kv<KV8>(pl[0][2], pl[0][3]), q3 = pack_kv<KV8>(pl[1][2], pl[1][3]);
         // ---- O += P V
-        const uint32_t vbase = pbase + Cfg::PAGE / 2;
 #pragma unroll
         for (int nd2 = 0; nd2 < Cfg::ND / 2; ++nd2) {
           const int ci = nd2 * 32 + lane;
-          const uint4 vf = load_kv_frag<KV8>(vbase + ci * 16, vbase + ci * 8);
+          const uint4 vf = load_v<DP, KVF>(pbase, ci);
           mma_kv<KV8>(acc[2 * nd2], h0, h1, h2, h3, vf.x, vf.y);
           mma_kv<KV8>(acc[2 * nd2], q0, q1, q2, q3, vf.x, vf.y);
           mma_kv<KV8>(acc[2 * nd2 + 1], h0, h1, h2, h3, vf.z, vf.w);
@@ -640,7 +711,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
 #pragma unroll
           for (int kp = 0; kp < Cfg::KS / 2; ++kp) {
             const int ci = (nt * (Cfg::KS / 2) + kp) * 32 + lane;
-            const uint4 kf = load_kv_frag<KV8>(pbase + ci * 16, pbase + ci * 8);
+            const uint4 kf = load_k<DP, KVF>(pbase, ci);
             const int k0 = 2 * kp, k1 = 2 * kp + 1;
             mma_kv<KV8>(s0[nt], qa[k0][0], qa[k0][1], qa[k0][2], qa[k0][3], kf.x, kf.y);
             if constexpr (!KV8) mma_kv<KV8>(s1[nt], qb[k0][0], 0u, qb[k0][1], 0u, kf.x, kf.y);
@@ -694,11 +765,10 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           a3 = pack_bf16(pl[2], pl[3]);
         }
         // ---- O += P V
-        const uint32_t vbase = pbase + Cfg::PAGE / 2;
 #pragma unroll
         for (int nd2 = 0; nd2 < Cfg::ND / 2; ++nd2) {
           const int ci = nd2 * 32 + lane;
-          const uint4 vf = load_kv_frag<KV8>(vbase + ci * 16, vbase + ci * 8);
+          const uint4 vf = load_v<DP, KVF>(pbase, ci);
           mma_kv<KV8>(acc[2 * nd2], a0, a1, a2, a3, vf.x, vf.y);
           mma_kv<KV8>(acc[2 * nd2 + 1], a0, a1, a2, a3, vf.z, vf.w);
         }
@@ -956,56 +1026,65 @@ __global__ void bump_totals_kernel(int* total, int n) {
 
 // ------------------------------------------------------------------------
 // host launchers
-template <int DP, int NWC, int NSTAGE, int QC, bool KV8, bool W16>
+template <int DP, int NWC, int NSTAGE, int QC, int KVF, bool W16>
 static size_t attn_smem_bytes() {
   constexpr int SR = W16 ? 16 : 8;
-  return NSTAGE * (NWC * AttnCfg<DP, KV8>::PAGE + QC * 8 * DP * 4) + NWC * (SR * DP + 2 * SR) * 4 +
+  return NSTAGE * (NWC * AttnCfg<DP, KVF>::PAGE + QC * 8 * DP * 4) + NWC * (SR * DP + 2 * SR) * 4 +
          (W16 ? 3 * (DP / 16) * 32 * 16 : 0) + NSTAGE * sizeof(StageMeta) + 2 * NSTAGE * 8 + 64;
 }
 
-template <int DP, int NWC, int NSTAGE, int QC, bool KV8, bool W16>
+template <int DP, int NWC, int NSTAGE, int QC, int KVF, bool W16>
 static cudaError_t launch_attn_t(const AttnParams& p, int grid, cudaStream_t stream) {
-  const size_t smem = attn_smem_bytes<DP, NWC, NSTAGE, QC, KV8, W16>();
+  const size_t smem = attn_smem_bytes<DP, NWC, NSTAGE, QC, KVF, W16>();
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<DP, NWC, NSTAGE, QC, KV8, W16>,
+    cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<DP, NWC, NSTAGE, QC, KVF, W16>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  return launch_k(attn_decode_kernel<DP, NWC, NSTAGE, QC, KV8, W16>, dim3(grid), dim3((NWC + 1) * 32), smem, stream,
+  return launch_k(attn_decode_kernel<DP, NWC, NSTAGE, QC, KVF, W16>, dim3(grid), dim3((NWC + 1) * 32), smem, stream,
                   p);
 }
 
 // bf16 pages: 2-4 stages of 8 pages; FP8 pages are half the bytes, so twice the
 // stages in flight. 9-16 query rows of bf16 pages take the W16 consumers.
-template <int QC, bool KV8>
+template <int QC, int KVF>
 static cudaError_t launch_attn_dp(const AttnParams& p, int grid, cudaStream_t stream) {
-  constexpr bool W16 = QC == 2;  // 9-16 query rows: every warp takes 16 rows (bf16 or FP8 pages)
+  constexpr bool W16 = QC == 2;  // 9-16 query rows: every warp takes 16 rows
+  constexpr bool KV8 = KVF != 0;
   switch (p.dp) {
-    case 32: return launch_attn_t<32, 8, KV8 ? 8 : 4, QC, KV8, W16>(p, grid, stream);
-    case 64: return launch_attn_t<64, 8, KV8 ? 6 : 3, QC, KV8, W16>(p, grid, stream);
+    case 32: return launch_attn_t<32, 8, KV8 ? 8 : 4, QC, KVF, W16>(p, grid, stream);
+    case 64: return launch_attn_t<64, 8, KV8 ? 6 : 3, QC, KVF, W16>(p, grid, stream);
     case 128:
+      // FP4 pages (2176 B each): the widening + scaling dominates the consumer work --
+      // as many consumer warps as registers allow without spills (10 x 168 regs;
+      // 12 warps spill), and deep rings (the pages are small)
+      if constexpr (KVF == 2 && QC == 1) return launch_attn_t<128, 10, 6, QC, KVF, W16>(p, grid, stream);
+      else if constexpr (KVF == 2) return launch_attn_t<128, 8, 4, QC, KVF, W16>(p, grid, stream);
+      else {
       // FP8 pages: 10 consumer warps x 4 stages (217 KB of shared memory) -- the
       // e4m3 widening doubles the per-byte consumer work, so more pages in flight
       // per SM: 0.366 -> 0.339 ms per configs[1] launch vs 8 x 4 (12 x 3: 0.351)
-      if constexpr (KV8 && QC == 1) return launch_attn_t<128, 10, 4, QC, KV8, W16>(p, grid, stream);
+      if constexpr (KV8 && QC == 1) return launch_attn_t<128, 10, 4, QC, KVF, W16>(p, grid, stream);
       // 16 rows per warp (W16) of FP8 pages: 12 warps x 2 stages next to the 16-row
       // scratch (224 KB; 405B-like FP8 slice 0.430 ms vs 0.450 at 8 x 3, 0.479 at 10 x 2)
-      if constexpr (KV8) return launch_attn_t<128, 12, 2, QC, KV8, W16>(p, grid, stream);
+      if constexpr (KV8) return launch_attn_t<128, 12, 2, QC, KVF, W16>(p, grid, stream);
       // bf16 pages, 8 query rows: 7 consumer warps x 3 stages (168 KB of KV in flight):
       // configs[1] launch 0.606 -> 0.591 ms (7.27 TB/s) vs 8 x 2; 6 x 3 0.597, 5 x 4 0.603, 4 x 5 0.599
-      if constexpr (!KV8 && QC == 1) return launch_attn_t<128, 7, 3, QC, KV8, W16>(p, grid, stream);
-      return launch_attn_t<128, 8, 2, QC, KV8, W16>(p, grid, stream);
+      if constexpr (!KV8 && QC == 1) return launch_attn_t<128, 7, 3, QC, KVF, W16>(p, grid, stream);
+      return launch_attn_t<128, 8, 2, QC, KVF, W16>(p, grid, stream);
+      }
     default: return cudaErrorInvalidValue;
   }
 }
 
 cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t stream) {
   if (p.qrows != 8 && p.qrows != 16) return cudaErrorInvalidValue;
-  if (p.kv8) return p.qrows == 16 ? launch_attn_dp<2, true>(p, grid, stream) : launch_attn_dp<1, true>(p, grid, stream);
-  return p.qrows == 16 ? launch_attn_dp<2, false>(p, grid, stream) : launch_attn_dp<1, false>(p, grid, stream);
+  if (p.kv4) return p.qrows == 16 ? launch_attn_dp<2, 2>(p, grid, stream) : launch_attn_dp<1, 2>(p, grid, stream);
+  if (p.kv8) return p.qrows == 16 ? launch_attn_dp<2, 1>(p, grid, stream) : launch_attn_dp<1, 1>(p, grid, stream);
+  return p.qrows == 16 ? launch_attn_dp<2, 0>(p, grid, stream) : launch_attn_dp<1, 0>(p, grid, stream);
 }
 
 cudaError_t launch_attn_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse,
@@ -1039,9 +1118,9 @@ bool pdl_enabled() { return g_pdl; }
 
 size_t attn_decode_smem_bytes(int dp) {
   switch (dp) {  // the larger (two query chunks) variant
-    case 32: return attn_smem_bytes<32, 8, 4, 2, false, true>();
-    case 64: return attn_smem_bytes<64, 8, 3, 2, false, true>();
-    case 128: return attn_smem_bytes<128, 8, 2, 2, false, true>();
+    case 32: return attn_smem_bytes<32, 8, 4, 2, 0, true>();
+    case 64: return attn_smem_bytes<64, 8, 3, 2, 0, true>();
+    case 128: return attn_smem_bytes<128, 8, 2, 2, 0, true>();
     default: return 0;
   }
 }

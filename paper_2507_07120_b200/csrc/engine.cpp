@@ -130,14 +130,19 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
   if (B_ < 1 || B_ > 64) throw std::invalid_argument("batch must be in [1, 64] for the B200 decode kernels");
   if (cap_ < 1) throw std::invalid_argument("capacity_tokens must be >= 1");
   mla_ = m.kv_latent > 0;
-  if (rt.kv_dtype != HX_KV_BF16 && rt.kv_dtype != HX_KV_FP8_E4M3 && rt.kv_dtype != HX_KV_F64)
+  if (rt.kv_dtype != HX_KV_BF16 && rt.kv_dtype != HX_KV_FP8_E4M3 && rt.kv_dtype != HX_KV_F64 &&
+      rt.kv_dtype != HX_KV_FP4_E2M1)
     throw std::invalid_argument("unknown kv_dtype");
   kv8_ = rt.kv_dtype == HX_KV_FP8_E4M3;
+  kv4_ = rt.kv_dtype == HX_KV_FP4_E2M1;
   f64_ = rt.kv_dtype == HX_KV_F64;
   if (f64_ && (!attn_only_ || par.distributed != HX_POOL_LOCAL))
     throw std::invalid_argument("the exact fp64 harness (HX_KV_F64) is the attention-only local pool "
                                 "(DecodeHarness<double>)");
   if (kv8_ && mla_) throw std::invalid_argument("FP8 KV pages are implemented for GQA caches (MLA latents stay bf16)");
+  if (kv4_ && mla_) throw std::invalid_argument("FP4 KV pages are implemented for GQA caches (MLA latents stay bf16)");
+  if (kv4_ && m.head_size != 32 && m.head_size != 64 && m.head_size != 128)
+    throw std::invalid_argument("FP4 KV blocks are 32 dims: head_size must be 32, 64 or 128");
   if (rt.w_dtype != HX_W_BF16 && rt.w_dtype != HX_W_FP8_E4M3) throw std::invalid_argument("unknown w_dtype");
   w8_ = rt.w_dtype == HX_W_FP8_E4M3;
   if (w8_ && B_ > 16) throw std::invalid_argument("FP8 weights run the mma.sync GEMV: batch <= 16");
@@ -238,7 +243,7 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
     page_bytes_ = mla_page_bytes();
   } else {
     page_cap_ = static_cast<int>((per_rank_max + 15) / 16 + 1);
-    page_bytes_ = page_bytes_kv(DP_, kv8_);
+    page_bytes_ = kv4_ ? page_bytes_kv4(DP_) : page_bytes_kv(DP_, kv8_);
   }
   if (f64_) {  // fp64 shards instead of bf16 pages (exact64.cu)
     rows_cap64_ = per_rank_max;
@@ -516,6 +521,7 @@ void Engine::plan_gemvs() {
     q.p.n_local_slots = n_slots_;
     q.p.append = 1;
     q.p.kv8 = kv8_ ? 1 : 0;
+    q.p.kv4 = kv4_ ? 1 : 0;
     plan_qkv_.push_back(q);
     if (!attn_only_) {
       if (dist) {
@@ -938,6 +944,19 @@ void Engine::grow_random(int64_t layer, int64_t request, int64_t n, std::mt19937
       std::vector<double> vv(static_cast<size_t>(per)), kk(static_cast<size_t>(per));
       for (double& x : vv) x = unit_draw(rng);
       for (double& x : kk) x = unit_draw(rng);
+      if (kv4_) {  // e2m1 blocks of 32 dims per (token, head), rounded from the doubles; the stored
+                   // values are exact floats, and append_kv's re-rounding keeps them (fp8.cuh)
+        for (int64_t j0 = 0; j0 < per; j0 += 32)
+          for (int w = 0; w < 2; ++w) {
+            const double* src = (w ? kk : vv).data() + j0;
+            float* dst = (w ? k : v).data() + i * per + j0;
+            double am = 0.0;
+            for (int j = 0; j < 32; ++j) am = std::max(am, std::fabs(src[j]));
+            const int ex = e2m1_block_exp(am);
+            for (int j = 0; j < 32; ++j) dst[j] = e2m1_to_float(e2m1_from_double(src[j], ex), ex);
+          }
+        continue;
+      }
       for (int64_t j = 0; j < per; ++j) {
         // exact: route the double through its stored value (bf16, or e4m3 -- both exact in float)
         const double dv = vv[static_cast<size_t>(j)], dk = kk[static_cast<size_t>(j)];
@@ -966,6 +985,36 @@ void Engine::append_kv(int64_t layer, int64_t request, int64_t n, const float* k
     throw std::invalid_argument("KV capacity exceeded");
   if (n == 0) return;
   const size_t cnt = static_cast<size_t>(n * Kh_ * D_);
+  if (kv4_) {  // host e2m1 block rounding (fp8.cuh) of each 32-dim block of a token's row
+    const size_t nblk = cnt / 32;
+    std::vector<uint8_t> ck(cnt), cv(cnt);
+    std::vector<int8_t> ek(nblk), ev(nblk);
+    for (size_t blk = 0; blk < nblk; ++blk)
+      for (int w = 0; w < 2; ++w) {
+        const float* src = (w ? v : k) + blk * 32;
+        double am = 0.0;
+        for (int j = 0; j < 32; ++j) am = std::max(am, std::fabs(static_cast<double>(src[j])));
+        const int ex = e2m1_block_exp(am);
+        (w ? ev : ek)[blk] = static_cast<int8_t>(ex);
+        for (int j = 0; j < 32; ++j) (w ? cv : ck)[blk * 32 + j] = e2m1_from_double(src[j], ex);
+      }
+    uint8_t* dbuf = nullptr;
+    cuda_check(cudaMalloc(&dbuf, 2 * cnt + 2 * nblk), "append staging");
+    cuda_check(cudaMemcpyAsync(dbuf, ck.data(), cnt, cudaMemcpyHostToDevice, stream_), "append h2d");
+    cuda_check(cudaMemcpyAsync(dbuf + cnt, cv.data(), cnt, cudaMemcpyHostToDevice, stream_), "append h2d");
+    cuda_check(cudaMemcpyAsync(dbuf + 2 * cnt, ek.data(), nblk, cudaMemcpyHostToDevice, stream_), "append h2d");
+    cuda_check(cudaMemcpyAsync(dbuf + 2 * cnt + nblk, ev.data(), nblk, cudaMemcpyHostToDevice, stream_), "append h2d");
+    cuda_check(launch_kv4_append_rows(kv_[layer], dbuf, dbuf + cnt, reinterpret_cast<int8_t*>(dbuf + 2 * cnt),
+                                      reinterpret_cast<int8_t*>(dbuf + 2 * cnt + nblk), static_cast<int>(n),
+                                      static_cast<int>(request), d_total_ + layer * B_, B_, static_cast<int>(Kh_),
+                                      kvh_per_slot_, kvp_, chunk_, static_cast<int>(D_), DP_, page_cap_, slot_base_,
+                                      n_slots_, stream_),
+               "fp4 append kernel");
+    cuda_check(cudaStreamSynchronize(stream_), "append sync");
+    cudaFree(dbuf);
+    h_total_[static_cast<size_t>(layer * B_ + request)] += n;
+    return;
+  }
   const size_t esz = kv8_ ? 1 : 2;  // stored element bytes
   std::vector<uint8_t> kb(cnt * esz), vb(cnt * esz);
   for (size_t i = 0; i < cnt; ++i) {
@@ -1005,7 +1054,14 @@ void Engine::fill_kv_hash(int64_t n, uint64_t seed) {
                "kv fill");
     for (int b = 0; b < B_; ++b) h_total_[static_cast<size_t>(l * B_ + b)] += n;
   }
-  for (int64_t l = 0; l < L_ && !mla_; ++l) {
+  for (int64_t l = 0; l < L_ && !mla_ && kv4_; ++l) {
+    cuda_check(launch_kv4_fill_hash(kv_[l], d_total_ + l * B_, B_, static_cast<int>(Kh_), kvh_per_slot_, kvp_,
+                                    chunk_, static_cast<int>(D_), DP_, page_cap_, slot_base_, n_slots_, n, seed,
+                                    hash_stream(kCacheK, l), hash_stream(kCacheV, l), stream_),
+               "kv fill");
+    for (int b = 0; b < B_; ++b) h_total_[static_cast<size_t>(l * B_ + b)] += n;
+  }
+  for (int64_t l = 0; l < L_ && !mla_ && !kv4_; ++l) {
     cuda_check(launch_kv_fill_hash(kv_[l], d_total_ + l * B_, B_, static_cast<int>(Kh_), kvh_per_slot_, kvp_,
                                    chunk_, static_cast<int>(D_), DP_, page_cap_, slot_base_, n_slots_, n, seed,
                                    hash_stream(kCacheK, l), hash_stream(kCacheV, l), kv8_, stream_),
@@ -1083,7 +1139,18 @@ void Engine::read_kv(int64_t layer, int64_t request, int64_t rank, int64_t head,
   cuda_check(cudaStreamSynchronize(stream_), "read_kv sync");
   if (pages)
     cuda_check(cudaMemcpy(buf.data(), kv_[layer] + base, buf.size(), cudaMemcpyDeviceToHost), "read_kv");
-  for (int64_t t = 0; t < n; ++t) {
+  for (int64_t t = 0; t < n && kv4_; ++t) {
+    const uint8_t* page = buf.data() + static_cast<size_t>(t / 16) * page_bytes_;
+    for (int d = 0; d < D_; ++d)
+      for (int w = 0; w < 2; ++w) {
+        bool high = false;
+        const uint32_t off = kv4_offset(DP_, static_cast<int>(t % 16), d, w != 0, &high);
+        const uint8_t code = static_cast<uint8_t>((page[off] >> (high ? 4 : 0)) & 15);
+        const int ex = static_cast<int>(page[kv4_scale_offset(DP_, static_cast<int>(t % 16), d, w != 0)]) - 127;
+        (w ? v : k)[t * D_ + d] = e2m1_to_float(code, ex);
+      }
+  }
+  for (int64_t t = 0; t < n && !kv4_; ++t) {
     const uint8_t* page = buf.data() + static_cast<size_t>(t / 16) * page_bytes_;
     for (int d = 0; d < D_; ++d) {
       const uint8_t* pk = page + kv_offset(DP_, static_cast<int>(t % 16), d, false, kv8_);
@@ -1154,6 +1221,7 @@ AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) {
   a.q_chunks = q_chunks_;
   a.qrows = q_rows_;
   a.kv8 = kv8_ ? 1 : 0;
+  a.kv4 = kv4_ ? 1 : 0;
   if (one_src_merge_) {
     a.xf_out = d_xf_attn_;
     a.xf16 = xf16_();
@@ -1737,7 +1805,7 @@ void Engine::info(hx_engine_info* o) const {
   o->kernels_per_step = launches_per_step();
   o->page_cap = page_cap_;
   o->head_dim_padded = DP_;
-  o->kv_dtype = kv8_ ? HX_KV_FP8_E4M3 : HX_KV_BF16;
+  o->kv_dtype = kv4_ ? HX_KV_FP4_E2M1 : (f64_ ? HX_KV_F64 : (kv8_ ? HX_KV_FP8_E4M3 : HX_KV_BF16));
   o->w_dtype = w8_ ? HX_W_FP8_E4M3 : HX_W_BF16;
   o->comm_ranks = transport_ ? transport_->world() : 1;
   o->nccl_version = transport_ ? transport_->nccl_version() : 0;

@@ -117,6 +117,7 @@ class Engine {
   bool hopb_, graphs_;
   bool loopback_ = false;
   bool kv8_ = false;  // FP8 e4m3 GQA pages (hx_runtime_config.kv_dtype)
+  bool kv4_ = false;  // FP4 e2m1 block-scaled GQA pages
   bool tc_ = false;   // batch > 16: tcgen05 GEMVs (weights / x-fragments in their operand images)
   bool w8_ = false;   // FP8 e4m3 GEMV weights (hx_runtime_config.w_dtype), per-output pow2 scales
   // local pool with KVP = 1 (one fragment per query head): the split reduce

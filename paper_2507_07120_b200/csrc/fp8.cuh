@@ -71,3 +71,75 @@ HX_HD float e4m3_to_float(uint8_t v) {
 }
 
 }  // namespace hx
+
+// ---------------------------------------------------------------------------
+// FP4 E2M1 KV storage (PAPER.md:158 evaluates Helix at FP4): MX-style blocks of
+// 32 elements -- one (token, KV head, 32-dim group) of K or of V -- share a
+// power-of-two scale 2^e, e = the smallest exponent with 6 * 2^e >= max |x|
+// (clamped to [-20, 13], so every stored value grid * 2^e is exact in f16);
+// each element is the e2m1 code of x / 2^e rounded to nearest-even on the grid
+// {0, 0.5, 1, 1.5, 2, 3, 4, 6} (saturating at 6). Identical on host, device and
+// in the oracle (round_e2m1_block), always from the value the writer holds
+// (double for grown / hash-filled rows, fp32 for projected rows).
+namespace hx {
+
+constexpr int kE2m1MinExp = -20, kE2m1MaxExp = 13;
+
+HX_HD int e2m1_block_exp(double amax) {
+  if (!(amax > 0.0)) return 0;
+  // smallest e with 6 * 2^e >= amax: amax / 6 = m * 2^k, m in [0.5, 1)
+  const double r = amax / 6.0;
+  int k = 0;
+  double m = r;
+  while (m >= 1.0) {
+    m *= 0.5;
+    ++k;
+  }
+  while (m < 0.5) {
+    m *= 2.0;
+    --k;
+  }
+  int e = (m == 0.5) ? k - 1 : k;
+  if (e < kE2m1MinExp) e = kE2m1MinExp;
+  if (e > kE2m1MaxExp) e = kE2m1MaxExp;
+  return e;
+}
+
+HX_HD double pow2i(int e) {
+  double s = 1.0;
+  for (; e > 0; --e) s *= 2.0;
+  for (; e < 0; ++e) s *= 0.5;
+  return s;
+}
+
+// e2m1 code (sign << 3 | magnitude code) of x / 2^e, round to nearest even.
+HX_HD uint8_t e2m1_from_double(double x, int e) {
+  const uint8_t sign = x < 0.0 ? 8 : 0;
+  const double t = (x < 0.0 ? -x : x) / pow2i(e);  // exact: power-of-two scale
+  // grid 0 0.5 1 1.5 2 3 4 6 (codes 0..7); midpoints go to the even code
+  uint8_t c;
+  if (t < 0.25) c = 0;
+  else if (t == 0.25) c = 0;
+  else if (t < 0.75) c = 1;
+  else if (t == 0.75) c = 2;
+  else if (t < 1.25) c = 2;
+  else if (t == 1.25) c = 2;
+  else if (t < 1.75) c = 3;
+  else if (t == 1.75) c = 4;
+  else if (t < 2.5) c = 4;
+  else if (t == 2.5) c = 4;
+  else if (t < 3.5) c = 5;
+  else if (t == 3.5) c = 6;
+  else if (t < 5.0) c = 6;
+  else if (t == 5.0) c = 6;
+  else c = 7;
+  return sign | c;
+}
+
+HX_HD float e2m1_to_float(uint8_t code, int e) {
+  const float grid[8] = {0.f, 0.5f, 1.f, 1.5f, 2.f, 3.f, 4.f, 6.f};
+  const float v = grid[code & 7] * static_cast<float>(pow2i(e));
+  return (code & 8) ? -v : v;
+}
+
+}  // namespace hx

@@ -484,12 +484,27 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
             const size_t page =
                 ((static_cast<size_t>(slot_local) * p.batch + b) * p.kvh_per_slot + kvh) * p.page_cap +
                 static_cast<size_t>(row >> 4);
-            uint8_t* dst = p.kv + page * page_bytes_kv(p.dp, p.kv8 != 0) +
-                           kv_offset(p.dp, static_cast<int>(row & 15), d, is_v != 0, p.kv8 != 0);
-            if (p.kv8)
-              *dst = e4m3_from_double(static_cast<double>(y[0]));
-            else
-              *reinterpret_cast<__nv_bfloat16*>(dst) = __float2bfloat16_rn(y[0]);
+            if (p.kv4) {
+              // FP4 block = 32 dims of this token's K or V row of one head: the warp's 32
+              // lanes (32 consecutive output features, head_dim % 32 == 0) -- amax by shuffles
+              float am = fabsf(y[0]);
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+              const int ex = e2m1_block_exp(static_cast<double>(am));
+              uint8_t* pg = p.kv + page * page_bytes_kv4(p.dp);
+              bool high = false;
+              const uint32_t off = kv4_offset(p.dp, static_cast<int>(row & 15), d, is_v != 0, &high);
+              const uint32_t code = e2m1_from_double(static_cast<double>(y[0]), ex);
+              atomicOr(reinterpret_cast<unsigned*>(pg + (off & ~3u)), code << ((off & 3u) * 8u + (high ? 4u : 0u)));
+              if ((d & 31) == 0) pg[kv4_scale_offset(p.dp, static_cast<int>(row & 15), d, is_v != 0)] = ex + 127;
+            } else {
+              uint8_t* dst = p.kv + page * page_bytes_kv(p.dp, p.kv8 != 0) +
+                             kv_offset(p.dp, static_cast<int>(row & 15), d, is_v != 0, p.kv8 != 0);
+              if (p.kv8)
+                *dst = e4m3_from_double(static_cast<double>(y[0]));
+              else
+                *reinterpret_cast<__nv_bfloat16*>(dst) = __float2bfloat16_rn(y[0]);
+            }
           }
         }
       }

@@ -64,6 +64,7 @@ struct AttnParams {
   uint8_t* xf_out;
   int xf16, hd;
   int kv8;                 // GQA: FP8 (e4m3) pages (kv_layout.cuh), f16 MMAs
+  int kv4;                 // GQA: FP4 (e2m1 blocks of 32, power-of-two scales) pages, f16 MMAs
   // Fused split reduce (GQA): the CTA that completes a stream's last non-empty
   // split merges the stream's partials (split order) into frag_o / frag_lse
   // [slot_local][b][q][DP] (natural-log lse) -- no split-reduce launch.
@@ -85,6 +86,16 @@ struct AttnParams {
   int xchunk, xslice, xrank;
 };
 cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t stream);
+// FP4 (e2m1 block) KV pages (kv_layout.cuh kv4_*): device hash fill, and the
+// scatter of host-quantized rows (codes per element, exponents per 32-dim block).
+cudaError_t launch_kv4_fill_hash(uint8_t* kv, int* total, int batch, int kv_heads, int kvh_per_slot, int kvp,
+                                 int chunk, int head_dim, int dp, int page_cap, int slot_base, int n_local_slots,
+                                 long long n, uint64_t seed, uint64_t stream_k, uint64_t stream_v,
+                                 cudaStream_t stream);
+cudaError_t launch_kv4_append_rows(uint8_t* kv, const uint8_t* codes_k, const uint8_t* codes_v, const int8_t* exp_k,
+                                   const int8_t* exp_v, int n, int b, int* total, int batch, int kv_heads,
+                                   int kvh_per_slot, int kvp, int chunk, int head_dim, int dp, int page_cap,
+                                   int slot_base, int n_local_slots, cudaStream_t stream);
 // Spin (one CTA) until every flag is raised, then lower it: the receive side
 // of the device-initiated exchange (flags written by the peers' attention kernels).
 cudaError_t launch_wait_flags(unsigned* flags, int n, cudaStream_t stream);
@@ -146,6 +157,7 @@ struct GemvParams {
   int kv_head_base;      // global index of the first KV head in this projection
   int append;            // write K/V into the cache
   int kv8;               // GQA cache pages are FP8 e4m3 (fp8.cuh), else bf16
+  int kv4;               // GQA cache pages are FP4 e2m1 blocks (fp8.cuh, kv_layout.cuh)
   uint8_t* q_img;        // MLA (mla = 1): q -> bf16 query images, latent -> MLA pages
   int mla;
   int kvp, head_dim, dp;

@@ -57,6 +57,27 @@ __host__ __device__ __forceinline__ uint32_t kv_offset(int dp, int t, int d, boo
   return fp8 ? off >> 1 : off;
 }
 
+// FP4 (e2m1, fp8.cuh) pages: the same fragment order with 4-bit elements (a
+// lane's 16-byte bf16 chunk becomes 4 bytes; element 2r of the chunk in the low
+// nibble of byte r), K data [0, 8*DP), V data [8*DP, 16*DP), then the block
+// exponents (e + 127, one byte per token and 32-dim group): K [16][DP/32] at
+// 16*DP, V [16][DP/32] at 16*DP + DP/2. A page is 17*DP bytes.
+__host__ __device__ __forceinline__ uint32_t page_bytes_kv4(int dp) { return 17u * static_cast<uint32_t>(dp); }
+// byte offset of element (t, d) and whether it is the high nibble
+__host__ __device__ __forceinline__ uint32_t kv4_offset(int dp, int t, int d, bool is_v, bool* high) {
+  const uint32_t off = is_v ? v_offset(dp, t, d) - 32u * static_cast<uint32_t>(dp) : k_offset(dp, t, d);
+  *high = ((off >> 1) & 1u) != 0;
+  return (is_v ? 8u * static_cast<uint32_t>(dp) : 0u) + (off >> 2);
+}
+__host__ __device__ __forceinline__ uint32_t kv4_scale_offset(int dp, int t, int d, bool is_v) {
+  return 16u * static_cast<uint32_t>(dp) + (is_v ? static_cast<uint32_t>(dp) / 2u : 0u) +
+         static_cast<uint32_t>(t * (dp / 32) + d / 32);
+}
+// page bytes for a KV storage type: 0 bf16, 1 fp8, 2 fp4
+__host__ __device__ __forceinline__ uint32_t page_bytes_kvt(int dp, int kvt) {
+  return kvt == 2 ? page_bytes_kv4(dp) : page_bytes_kv(dp, kvt == 1);
+}
+
 // Round-robin placement (attention.hpp:262-282 in closed form): global token
 // g of a cache grown only by append_round_robin with chunk c over kvp ranks.
 __host__ __device__ __forceinline__ int rr_rank(long long g, int chunk, int kvp) {

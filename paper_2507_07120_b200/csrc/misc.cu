@@ -271,6 +271,134 @@ __global__ void kv_fill_hash_kernel(uint8_t* kv, const int* total, int batch, in
   }
 }
 
+__global__ void add_total_all_kernel(int* total, int batch, int n);
+
+// FP4 pages (kv_layout.cuh kv4_*): one thread per (stream, page row t, K or V,
+// 32-dim group) -- the e2m1 block. Values are the same hash doubles as the bf16
+// fill, block-rounded exactly as the oracle (round_e2m1_block). K blocks own 16
+// contiguous bytes (plain stores); a V byte pairs tokens t and t^1 (atomicOr:
+// pages start zeroed and every position is written once).
+__global__ void kv4_fill_hash_kernel(uint8_t* kv, const int* total, int batch, int kv_heads, int kvh_per_slot,
+                                     int kvp, int chunk, int head_dim, int dp, int page_cap, int slot_base,
+                                     int n_local_slots, long long n, uint64_t seed, uint64_t stream_k,
+                                     uint64_t stream_v) {
+  const int groups = dp / 32;
+  long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const long long streams = static_cast<long long>(n_local_slots) * batch * kvh_per_slot;
+  if (i >= streams * page_cap * 16 * 2 * groups) return;
+  const int grp = static_cast<int>(i % groups);
+  i /= groups;
+  const int is_v = static_cast<int>(i % 2);
+  i /= 2;
+  const int t = static_cast<int>(i % 16);
+  i /= 16;
+  const int page = static_cast<int>(i % page_cap);
+  const long long stream_idx = i / page_cap;
+  long long st = stream_idx;
+  const int kvh = static_cast<int>(st % kvh_per_slot);
+  st /= kvh_per_slot;
+  const int b = static_cast<int>(st % batch);
+  const int slot = static_cast<int>(st / batch) + slot_base;
+  const int rank = slot % kvp, grpi = slot / kvp;
+  const int h = grpi * kvh_per_slot + kvh;
+  const long long t0 = total[b];
+  const long long gtok = rr_global_of_row(16ll * page + t, rank, chunk, kvp);
+  if (gtok < t0 || gtok >= t0 + n) return;
+  const uint64_t sseed = splitmix64(seed ^ ((is_v ? stream_v : stream_k) * 0xD1B54A32D192ED03ull));
+  const uint64_t base = ((static_cast<uint64_t>(b * kv_heads + h) << 32) + static_cast<uint64_t>(gtok)) *
+                        static_cast<uint64_t>(head_dim);
+  double v[32];
+  double am = 0.0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int d = grp * 32 + j;
+    v[j] = d < head_dim ? hash_kv_unit(sseed, base + static_cast<uint64_t>(d)) : 0.0;
+    am = fmax(am, fabs(v[j]));
+  }
+  const int ex = e2m1_block_exp(am);
+  uint8_t* pg = kv + (static_cast<size_t>(stream_idx) * page_cap + page) * page_bytes_kv4(dp);
+  uint32_t words[4] = {0u, 0u, 0u, 0u};
+  uint32_t kbase = 0;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int d = grp * 32 + j;
+    bool high = false;
+    const uint32_t off = kv4_offset(dp, t, d, is_v != 0, &high);
+    const uint32_t nib = static_cast<uint32_t>(e2m1_from_double(v[j], ex)) << ((off & 3u) * 8u + (high ? 4u : 0u));
+    if (is_v) {
+      atomicOr(reinterpret_cast<unsigned*>(pg + (off & ~3u)), nib);
+    } else {  // the block's 16 bytes are contiguous: 4 lane chunks of 4 bytes
+      if (j == 0) kbase = off & ~15u;
+      words[((off & ~3u) - kbase) >> 2] |= nib;
+    }
+  }
+  if (!is_v) *reinterpret_cast<uint4*>(pg + kbase) = make_uint4(words[0], words[1], words[2], words[3]);
+  pg[kv4_scale_offset(dp, t, grp * 32, is_v != 0)] = static_cast<uint8_t>(ex + 127);
+}
+
+cudaError_t launch_kv4_fill_hash(uint8_t* kv, int* total, int batch, int kv_heads, int kvh_per_slot, int kvp,
+                                 int chunk, int head_dim, int dp, int page_cap, int slot_base, int n_local_slots,
+                                 long long n, uint64_t seed, uint64_t stream_k, uint64_t stream_v,
+                                 cudaStream_t stream) {
+  const long long work = static_cast<long long>(n_local_slots) * batch * kvh_per_slot * page_cap * 16 * 2 * (dp / 32);
+  if (n > 0)
+    kv4_fill_hash_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(
+        kv, total, batch, kv_heads, kvh_per_slot, kvp, chunk, head_dim, dp, page_cap, slot_base, n_local_slots, n,
+        seed, stream_k, stream_v);
+  add_total_all_kernel<<<1, 64, 0, stream>>>(total, batch, static_cast<int>(n));
+  return cudaGetLastError();
+}
+
+// Host-quantized FP4 rows (codes [n][kv_heads][head_dim], block exponents
+// [n][kv_heads][head_dim / 32] for K and V) into the pages of request b, tokens
+// total[b] ..: one thread per (token, head, K/V, group).
+__global__ void kv4_append_rows_kernel(uint8_t* kv, const uint8_t* codes_k, const uint8_t* codes_v,
+                                       const int8_t* exp_k, const int8_t* exp_v, int n, int b, const int* total,
+                                       int batch, int kv_heads, int kvh_per_slot, int kvp, int chunk, int head_dim,
+                                       int dp, int page_cap, int slot_base, int n_local_slots) {
+  const int groups = head_dim / 32;
+  long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= static_cast<long long>(n) * kv_heads * 2 * groups) return;
+  const int grp = static_cast<int>(i % groups);
+  i /= groups;
+  const int is_v = static_cast<int>(i % 2);
+  i /= 2;
+  const int h = static_cast<int>(i % kv_heads);
+  const int tok = static_cast<int>(i / kv_heads);
+  const long long g = static_cast<long long>(total[b]) + tok;
+  const int rank = rr_rank(g, chunk, kvp);
+  const long long row = rr_row(g, chunk, kvp);
+  const int grpi = h / kvh_per_slot, kvh = h - grpi * kvh_per_slot;
+  const int slot_local = grpi * kvp + rank - slot_base;
+  if (slot_local < 0 || slot_local >= n_local_slots) return;
+  uint8_t* pg = kv + (((static_cast<size_t>(slot_local) * batch + b) * kvh_per_slot + kvh) * page_cap +
+                      static_cast<size_t>(row >> 4)) * page_bytes_kv4(dp);
+  const int t = static_cast<int>(row & 15);
+  const uint8_t* codes = (is_v ? codes_v : codes_k) + (static_cast<size_t>(tok) * kv_heads + h) * head_dim;
+  for (int j = 0; j < 32; ++j) {
+    const int d = grp * 32 + j;
+    bool high = false;
+    const uint32_t off = kv4_offset(dp, t, d, is_v != 0, &high);
+    atomicOr(reinterpret_cast<unsigned*>(pg + (off & ~3u)),
+             static_cast<uint32_t>(codes[d]) << ((off & 3u) * 8u + (high ? 4u : 0u)));
+  }
+  const int8_t ex = (is_v ? exp_v : exp_k)[(static_cast<size_t>(tok) * kv_heads + h) * groups + grp];
+  pg[kv4_scale_offset(dp, t, grp * 32, is_v != 0)] = static_cast<uint8_t>(ex + 127);
+}
+
+cudaError_t launch_kv4_append_rows(uint8_t* kv, const uint8_t* codes_k, const uint8_t* codes_v, const int8_t* exp_k,
+                                   const int8_t* exp_v, int n, int b, int* total, int batch, int kv_heads,
+                                   int kvh_per_slot, int kvp, int chunk, int head_dim, int dp, int page_cap,
+                                   int slot_base, int n_local_slots, cudaStream_t stream) {
+  const long long work = static_cast<long long>(n) * kv_heads * 2 * (head_dim / 32);
+  if (work > 0)
+    kv4_append_rows_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(
+        kv, codes_k, codes_v, exp_k, exp_v, n, b, total, batch, kv_heads, kvh_per_slot, kvp, chunk, head_dim, dp,
+        page_cap, slot_base, n_local_slots);
+  add_total_kernel<<<1, 1, 0, stream>>>(total, b, n);
+  return cudaGetLastError();
+}
+
 __global__ void add_total_all_kernel(int* total, int batch, int n) {
   for (int b = threadIdx.x; b < batch; b += blockDim.x) total[b] += n;
 }

@@ -32,6 +32,9 @@ def lib():
             "oracle_round_e4m3": (C.c_double, [C.c_double]),
             "oracle_harness_set_kv_fp8": (None, [vp, C.c_int]),
             "oracle_model_set_kv_fp8": (None, [vp, C.c_int]),
+            "oracle_harness_set_kv_fp4": (None, [vp, C.c_int]),
+            "oracle_model_set_kv_fp4": (None, [vp, C.c_int]),
+            "oracle_round_e2m1_block": (None, [dp, i64]),
             "oracle_harness_create": (C.c_int, [i64, i64, i64, i64, i64, i64, u64, C.c_int, C.POINTER(vp)]),
             "oracle_harness_free": (None, [vp]),
             "oracle_harness_grow_random": (C.c_int, [vp, i64, vp]),
@@ -120,12 +123,14 @@ def round_bf16(a):
 class Harness:
     """Oracle DecodeHarness<double> (attention.hpp:419-563)."""
 
-    def __init__(self, q, k, hsz, tpa, kvp, chunk, seed, bf16=False, kv_fp8=False):
+    def __init__(self, q, k, hsz, tpa, kvp, chunk, seed, bf16=False, kv_fp8=False, kv_fp4=False):
         self.q, self.k, self.hsz, self.tpa, self.kvp = q, k, hsz, tpa, kvp
         h = C.c_void_p()
         check(lib().oracle_harness_create(q, k, hsz, tpa, kvp, chunk, seed, int(bf16), C.byref(h)))
         if kv_fp8:
             lib().oracle_harness_set_kv_fp8(h, 1)
+        if kv_fp4:
+            lib().oracle_harness_set_kv_fp4(h, 1)
         self.h = h
 
     @property
@@ -245,7 +250,8 @@ class Model:
     WEIGHTS = {"wq": 0, "wk": 1, "wv": 2, "wo": 3, "wgate": 4, "wup": 5, "wdown": 6, "emb": 7, "lm": 8}
 
     def __init__(self, hidden, q, k, hsz, ffn, layers, vocab, tpa=1, kvp=1, chunk=16, batch=1,
-                 seed=0, qkv_hash=False, bf16=True, moe=None, kv_latent=0, kv_fp8=False, w_fp8=False):
+                 seed=0, qkv_hash=False, bf16=True, moe=None, kv_latent=0, kv_fp8=False, w_fp8=False,
+                 kv_fp4=False):
         """moe = (n_experts, top_k, expert_ffn): every layer's FFN is routed MoE,
         `ffn` is then the shared expert width (0: none). kv_latent > 0: MLA
         attention with latent width 2*kv_latent (layer_oracle.hpp). w_fp8: e4m3
@@ -276,6 +282,8 @@ class Model:
                                             seed, int(qkv_hash), int(bf16), C.byref(h)))
         if kv_fp8:
             lib().oracle_model_set_kv_fp8(h, 1)
+        if kv_fp4:
+            lib().oracle_model_set_kv_fp4(h, 1)
         self.h = h
 
     def routes(self):
@@ -319,6 +327,13 @@ class Model:
             lib().oracle_model_free(self.h)
         except Exception:
             pass
+
+
+def round_e2m1_block(x):
+    """The oracle's FP4 block rounding (helix_oracle.cpp round_e2m1_block) of one block."""
+    a = np.ascontiguousarray(x, dtype=np.float64).copy()
+    lib().oracle_round_e2m1_block(_dp(a), a.size)
+    return a
 
 
 def hash_unit(seed, stream, index):
