@@ -59,7 +59,8 @@ def test_mla_kernel_uses_tcgen05():
 def test_large_batch_gemv_uses_tcgen05():
     """Batches above 16 run the weight-streaming GEMV on tcgen05 (UTCHMMA with
     TMEM drains, LDTM) fed by TMA bulk copies (UBLKCP); FP8 KV pages widen with
-    the e4m3 -> f16 converter (F2FP.F16.E4M3.UNPACK_B)."""
+    the e4m3 -> f16 converter (F2FP.F16.E4M3.UNPACK_B), FP4 pages with the
+    e2m1 -> f16 converter (F2FP.F16.E2M1.UNPACK_B) and an f16 scale (HMUL2)."""
     so = os.path.join(ROOT, "paper_2507_07120_b200", "libhelix_b200.so")
     sass = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
     funcs = sass.split("Function : ")
@@ -68,10 +69,14 @@ def test_large_batch_gemv_uses_tcgen05():
     for f in tc:
         for op in ("UTCHMMA", "LDTM", "UBLKCP", "UTCBAR"):
             assert op in f, op
-    # FP8 attention instantiations: 8-row (..Lb1ELb0E) and 16-row W16 (..Lb1ELb1E) consumers
-    fp8 = [f for f in funcs if f.startswith("_ZN2hx18attn_decode_kernel") and "Lb1ELb" in f.split("\n", 1)[0]]
-    assert any("Lb1ELb1E" in f.split("\n", 1)[0] for f in fp8)
+    # FP8 (KV type 1) attention instantiations: 8-row (..Li1ELb0E) and 16-row W16 (..Li1ELb1E) consumers
+    att = [f for f in funcs if f.startswith("_ZN2hx18attn_decode_kernel")]
+    fp8 = [f for f in att if "ELi1ELb" in f.split("\n", 1)[0]]
+    assert any("ELi1ELb1E" in f.split("\n", 1)[0] for f in fp8)
     assert fp8 and all("F2FP.F16.E4M3.UNPACK_B" in f and "HMMA.16816.F32 " in f for f in fp8)
+    fp4 = [f for f in att if "ELi2ELb" in f.split("\n", 1)[0]]
+    assert any("ELi2ELb1E" in f.split("\n", 1)[0] for f in fp4)
+    assert fp4 and all("F2FP.F16.E2M1.UNPACK_B" in f and "HMUL2" in f and "HMMA.16816.F32 " in f for f in fp4)
     # FP8-weight GEMVs (template flag W8, last argument) widen e4m3 weights the same way
     w8 = [f for f in funcs if f.startswith("_ZN2hx11gemv_kernel") and "Lb1EEEv" in f.split("\n", 1)[0]]
     assert w8 and all("F2FP.F16.E4M3.UNPACK_B" in f and "UBLKCP" in f for f in w8)
