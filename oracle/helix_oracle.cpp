@@ -48,7 +48,7 @@ void round_e2m1_block(double* x, i64 n) {
     int k = 0;
     const double m = std::frexp(amax / 6.0, &k);  // amax / 6 = m 2^k, m in [0.5, 1)
     e = (m == 0.5) ? k - 1 : k;                   // smallest e with 6 2^e >= amax
-    e = std::min(13, std::max(-20, e));
+    e = std::min(13, std::max(-14, e));
   }
   static const double grid[8] = {0.0, 0.5, 1.0, 1.5, 2.0, 3.0, 4.0, 6.0};
   for (i64 i = 0; i < n; ++i) {

@@ -57,7 +57,7 @@ double round_bf16(double x);
 double round_e4m3(double x);
 // FP4 E2M1 block storage (PAPER.md:158 evaluates at FP4): the n values of one
 // block share a power-of-two scale 2^e, e = the smallest exponent with
-// 6 * 2^e >= max |x| (clamped to [-20, 13]); each value is rounded to the
+// 6 * 2^e >= max |x| (clamped to [-14, 13]); each value is rounded to the
 // nearest e2m1 grid point {0, 0.5, 1, 1.5, 2, 3, 4, 6} * 2^e, ties to the even
 // code, saturating at 6 * 2^e. In place; blocks are 32 dims of one token's row.
 void round_e2m1_block(double* x, i64 n);

@@ -70,10 +70,12 @@ __device__ __forceinline__ void e2m1x8_to_f16x2x4(uint32_t w, uint32_t& r0, uint
       : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
       : "r"(w));
 }
-// f16 bits of 2^e for a stored block exponent byte (e + 127), e in [-20, 13]
-__device__ __forceinline__ uint32_t f16_pow2(uint32_t ebyte) {
-  const int e = static_cast<int>(ebyte) - 127;
-  return e >= -14 ? static_cast<uint32_t>(e + 15) << 10 : 1u << (e + 24);
+// f16 bits of 2^e from the stored exponent byte e + 15 (e in [-14, 13]: normal)
+__device__ __forceinline__ uint32_t f16_pow2(uint32_t ebyte) { return ebyte << 10; }
+__device__ __forceinline__ uint32_t lds16(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
 }
 __device__ __forceinline__ uint32_t hmul2(uint32_t a, uint32_t b) {
   uint32_t d;
@@ -133,10 +135,10 @@ __device__ __forceinline__ uint4 load_v(uint32_t pbase, int ci) {
     uint4 r;
     e2m1x8_to_f16x2x4(lds32(pbase + 8 * DP + ci * 4), r.x, r.y, r.z, r.w);
     const int c = ci & 3, grp = (ci >> 5) >> 1;
-    const uint32_t sb = pbase + 16 * DP + DP / 2 + grp;  // V exponents [16 tokens][DP/32]
-    const uint32_t lo = f16_pow2(lds8(sb + (2 * c) * (DP / 32))) | (f16_pow2(lds8(sb + (2 * c + 1) * (DP / 32))) << 16);
-    const uint32_t hi =
-        f16_pow2(lds8(sb + (2 * c + 8) * (DP / 32))) | (f16_pow2(lds8(sb + (2 * c + 9) * (DP / 32))) << 16);
+    const uint32_t sb = pbase + 16 * DP + DP / 2 + grp * 16;  // V exponents [DP/32][16 tokens]
+    const uint32_t w0 = lds16(sb + 2 * c), w8 = lds16(sb + 2 * c + 8);  // tokens (2c, 2c+1), (2c+8, 2c+9)
+    const uint32_t lo = ((w0 & 0xFFu) << 10) | ((w0 >> 8) << 26);
+    const uint32_t hi = ((w8 & 0xFFu) << 10) | ((w8 >> 8) << 26);
     r.x = hmul2(r.x, lo);
     r.y = hmul2(r.y, hi);
     r.z = hmul2(r.z, lo);

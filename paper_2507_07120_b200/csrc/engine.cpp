@@ -327,6 +327,48 @@ void Engine::validate_reference_dims() const {
     throw std::invalid_argument("tpa*kvp must divide the hidden width");
 }
 
+// Splits per stream for `pages` pages of KV per stream.
+// GQA: equal-size items pulled by one persistent CTA per SM cost waves x
+// (pages per item + per-item overhead ~16 pages: query staging and the
+// cross-warp combine), waves = ceil(items / SMs); minimised over the split
+// count with items >= 32 pages (256 KB at Hsz 128: below that the per-item
+// overhead dominates -- one 131k-token request of the 405B-like shard 0.196 ->
+// 0.131 ms). An item count that is a multiple of the SM count leaves no tail
+// (configs[1]: 64 streams x 37 splits = 16 x 148; 20.5 -> 20.0 ms of attention
+// per step vs 19 splits). MLA: one item per CTA pair, statically strided.
+int Engine::plan_splits(int streams, int pages) const {
+  if (mla_) return std::max(1, std::min((num_sms_ / 2) / streams, std::max(1, pages / 2)));
+  const int smax = std::max(1, pages / std::max(1, min_pages_));
+  if (split_env_) return std::max(1, std::min((num_sms_ * std::max(1, ips_) + streams - 1) / streams, smax));
+  int best = 1;
+  double best_cost = 1e300;
+  for (int sp = 1; sp <= smax && sp <= 8192; ++sp) {
+    const long long waves = (static_cast<long long>(streams) * sp + num_sms_ - 1) / num_sms_;
+    const double cost = static_cast<double>(waves) * ((pages + sp - 1) / sp + 16.0);
+    if (cost < best_cost) {
+      best_cost = cost;
+      best = sp;
+    }
+  }
+  return best;
+}
+
+// Splits for a launch over `layer`'s live context (pages of the fullest rank --
+// rank 0 -- rounded up to a power of two, so a growing context re-plans, and
+// re-captures the step graph, only log2 times), never above the capacity plan
+// the partial buffers are sized for.
+int Engine::live_splits(int64_t layer, bool per_request) const {
+  int64_t tmax = 0;
+  for (int b = 0; b < B_; ++b) tmax = std::max(tmax, h_total_[static_cast<size_t>(layer * B_ + b)]);
+  const int64_t rows = rr_count(tmax, 0, chunk_, kvp_);
+  const int64_t unit = mla_ ? kMlaPageRows : 16;
+  int pages = 1;
+  while (pages < (rows + unit - 1) / unit && pages < page_cap_) pages *= 2;
+  pages = std::min(pages, page_cap_);
+  const int streams = per_request ? n_streams_ / B_ : n_streams_;
+  return std::min(plan_splits(streams, pages), per_request ? splits_req_ : splits_);
+}
+
 void Engine::alloc() {
   const size_t pool = static_cast<size_t>(n_slots_) * B_ * kvh_per_slot_ * page_cap_ * page_bytes_;
   for (int64_t l = 0; l < L_; ++l) kv_.push_back(dalloc<uint8_t>(pool, "kv pool"));
@@ -340,55 +382,24 @@ void Engine::alloc() {
   const int qh_buf = dist_mode_ == HX_POOL_LOCAL ? static_cast<int>(Qh_) : q_per_slot_;
   d_q_ = dalloc<float>(static_cast<size_t>(B_) * qh_buf * DP_, "q");
 
-  // attention work decomposition: balanced page ranges ("splits") per stream,
-  // ~8 work items per SM for a full-batch launch and for a one-request (HOP-B) launch
-  const int pages_max = page_cap_;
-  // ~8 items per SM balance the persistent queue, but an item must stay >= 32
-  // pages (256 KB at Hsz 128): below that the per-item query staging and
-  // cross-warp combine dominate (measured: one 131k-token request of the
-  // 405B-like shard 0.196 -> 0.131 ms; profiles/r01_hopb_sweep.md).
-  int ips = 8, min_pages = 32;  // HX_ATTN_SPLIT="items_per_sm,min_pages_per_item" (tuning experiments)
-  const char* split_env = std::getenv("HX_ATTN_SPLIT");
-  if (split_env) std::sscanf(split_env, "%d,%d", &ips, &min_pages);
-  const int target_items = num_sms_ * std::max(1, ips);
-  // Equal-size items pulled by one persistent CTA per SM: the step costs
-  // waves x (pages per item + per-item overhead ~16 pages: query staging and
-  // the cross-warp combine), waves = ceil(items / SMs). Minimise that over the
-  // split count (items >= 32 pages): an item count that is a multiple of the
-  // SM count leaves no tail (configs[1]: 64 streams x 37 splits = 16 x 148;
-  // measured 20.5 -> 20.0 ms of attention per step vs 19 splits).
-  auto splits_for = [&](int streams) {
-    const int smax = std::max(1, pages_max / std::max(1, min_pages));
-    if (split_env) return std::max(1, std::min((target_items + streams - 1) / streams, smax));
-    int best = 1;
-    double best_cost = 1e300;
-    for (int sp = 1; sp <= smax && sp <= 8192; ++sp) {
-      const long long waves = (static_cast<long long>(streams) * sp + num_sms_ - 1) / num_sms_;
-      const double cost = static_cast<double>(waves) * ((pages_max + sp - 1) / sp + 16.0);
-      if (cost < best_cost) {
-        best_cost = cost;
-        best = sp;
-      }
-    }
-    return best;
-  };
+  // attention work decomposition: balanced page ranges ("splits") per stream.
+  // Buffers are sized for the capacity; every launch re-plans from the LIVE
+  // context (plan_splits / live_splits), so short contexts in a large engine
+  // keep items of useful size.
+  const char* split_env = std::getenv("HX_ATTN_SPLIT");  // "items_per_sm,min_pages_per_item" (tuning)
+  if (split_env) {
+    split_env_ = true;
+    std::sscanf(split_env, "%d,%d", &ips_, &min_pages_);
+  }
   n_streams_ = n_slots_ * B_ * kvh_per_slot_ * q_chunks_;
   const int req_streams = n_slots_ * kvh_per_slot_ * q_chunks_;
+  splits_ = plan_splits(n_streams_, page_cap_);
+  splits_req_ = plan_splits(req_streams, page_cap_);
+  n_items_ = std::max(n_streams_ * splits_, req_streams * splits_req_);
   if (mla_) {
-    // one item per CTA pair: (split, stream), statically strided over the pairs
-    auto mla_splits = [&](int streams) {
-      return std::max(1, std::min((num_sms_ / 2) / streams, std::max(1, pages_max / 2)));
-    };
-    splits_ = mla_splits(n_streams_);
-    splits_req_ = mla_splits(req_streams);
-    n_items_ = std::max(n_streams_ * splits_, req_streams * splits_req_);
     d_qimg_ = dalloc<uint8_t>(static_cast<size_t>(B_) * mla_q_bytes(), "mla query images");
     d_att_ = dalloc<float>(static_cast<size_t>(B_) * (dist_mode_ == HX_POOL_LOCAL ? Qh_ * DV_ : slice_),
                            "mla merged latent output");
-  } else {
-    splits_ = splits_for(n_streams_);
-    splits_req_ = splits_for(req_streams);
-    n_items_ = std::max(n_streams_ * splits_, req_streams * splits_req_);
   }
   attn_grid_ = std::min(mla_ ? num_sms_ / 2 : num_sms_, n_items_);  // MLA: CTA pairs
   if (std::getenv("HX_FUSED_REDUCE") && std::getenv("HX_FUSED_REDUCE")[0] == '0') fused_ = false;
@@ -1146,7 +1157,7 @@ void Engine::read_kv(int64_t layer, int64_t request, int64_t rank, int64_t head,
         bool high = false;
         const uint32_t off = kv4_offset(DP_, static_cast<int>(t % 16), d, w != 0, &high);
         const uint8_t code = static_cast<uint8_t>((page[off] >> (high ? 4 : 0)) & 15);
-        const int ex = static_cast<int>(page[kv4_scale_offset(DP_, static_cast<int>(t % 16), d, w != 0)]) - 127;
+        const int ex = static_cast<int>(page[kv4_scale_offset(DP_, static_cast<int>(t % 16), d, w != 0)]) - kE2m1ExpBias;
         (w ? v : k)[t * D_ + d] = e2m1_to_float(code, ex);
       }
   }
@@ -1237,7 +1248,7 @@ AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) {
   a.b_begin = b_begin;
   a.stream_batch = b_count;
   a.n_streams = n_slots_ * b_count * kvh_per_slot_ * q_chunks_;
-  a.splits = b_count == B_ ? splits_ : splits_req_;
+  a.splits = live_splits(layer, b_count != B_);
   a.n_items = a.n_streams * a.splits;  // HOP-B (one request): splits_req_ balanced page ranges
   a.qscale = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(mla_ ? W_ : D_)));
   a.stream_major = std::getenv("HX_STREAM_MAJOR") && std::getenv("HX_STREAM_MAJOR")[0] == '1';  // A/B
@@ -1546,8 +1557,12 @@ void Engine::decode_step_device(const int32_t* tokens_dev, int32_t* next_dev) {
   if (device_exchange() && !(skip_comm_ & 1)) ensure_peers();  // skip: the self tables (alloc) suffice
   if (graphs_ && !(loopback_ && skip_comm_ != 3) && !prof_) {
     cudaGraphExec_t exec = nullptr;
+    // the attention plan is baked into the graph: key it by every layer's live splits
+    std::vector<int> plan(static_cast<size_t>(L_));
+    for (int64_t l = 0; l < L_; ++l) plan[static_cast<size_t>(l)] = live_splits(l, false);
     for (auto& g : graphs_cache_)
-      if (g.tokens == tokens_dev && g.next == next_dev && g.hidden == capture_hidden_ && g.logits == store_logits_)
+      if (g.tokens == tokens_dev && g.next == next_dev && g.hidden == capture_hidden_ && g.logits == store_logits_ &&
+          g.plan == plan)
         exec = g.exec;
     if (!exec) {
       cudaGraph_t g;
@@ -1557,7 +1572,7 @@ void Engine::decode_step_device(const int32_t* tokens_dev, int32_t* next_dev) {
       cuda_check(cudaGraphInstantiate(&exec, g, 0), "graph instantiate");
       cuda_check(cudaGraphUpload(exec, stream_), "graph upload");  // device-side setup once, not per launch
       cudaGraphDestroy(g);
-      graphs_cache_.push_back({tokens_dev, next_dev, capture_hidden_, store_logits_, exec});
+      graphs_cache_.push_back({tokens_dev, next_dev, capture_hidden_, store_logits_, exec, plan});
     }
     cuda_check(cudaGraphLaunch(exec, stream_), "graph launch");
   } else {
@@ -1799,8 +1814,8 @@ void Engine::info(hx_engine_info* o) const {
   o->weight_bytes_per_layer = wb;
   o->head_bytes = attn_only_ ? 0 : static_cast<int64_t>(plan_lm_.p.Npad) * plan_lm_.p.K * wel + V_ * H_ * 2;
   o->attn_streams = n_streams_;
-  o->attn_splits = splits_;
-  o->attn_items = n_items_;
+  o->attn_splits = live_splits(0, false);  // the plan the next batched launch of layer 0 uses
+  o->attn_items = static_cast<int64_t>(n_streams_) * o->attn_splits;
   o->attn_grid = attn_grid_;
   o->kernels_per_step = launches_per_step();
   o->page_cap = page_cap_;

@@ -141,6 +141,10 @@ class Engine {
   // attention plan
   int n_streams_, splits_, n_items_, attn_grid_;
   int splits_req_ = 1;  // splits per stream for per-request (HOP-B) launches
+  int ips_ = 8, min_pages_ = 32;  // split planner knobs (HX_ATTN_SPLIT)
+  bool split_env_ = false;
+  int plan_splits(int streams, int pages) const;
+  int live_splits(int64_t layer, bool per_request) const;
 
   // ---- device state
   cudaStream_t stream_ = nullptr;
@@ -188,6 +192,7 @@ class Engine {
     int32_t* next;
     bool hidden, logits;
     cudaGraphExec_t exec;
+    std::vector<int> plan;  // live attention splits per layer baked into the graph
   };
   std::vector<GraphEntry> graphs_cache_;
   void drop_graphs();

@@ -76,14 +76,15 @@ HX_HD float e4m3_to_float(uint8_t v) {
 // FP4 E2M1 KV storage (PAPER.md:158 evaluates Helix at FP4): MX-style blocks of
 // 32 elements -- one (token, KV head, 32-dim group) of K or of V -- share a
 // power-of-two scale 2^e, e = the smallest exponent with 6 * 2^e >= max |x|
-// (clamped to [-20, 13], so every stored value grid * 2^e is exact in f16);
+// (clamped to [-14, 13], so 2^e is a normal f16 and every stored value grid * 2^e
+// is exact in f16);
 // each element is the e2m1 code of x / 2^e rounded to nearest-even on the grid
 // {0, 0.5, 1, 1.5, 2, 3, 4, 6} (saturating at 6). Identical on host, device and
 // in the oracle (round_e2m1_block), always from the value the writer holds
 // (double for grown / hash-filled rows, fp32 for projected rows).
 namespace hx {
 
-constexpr int kE2m1MinExp = -20, kE2m1MaxExp = 13;
+constexpr int kE2m1MinExp = -14, kE2m1MaxExp = 13;  // 2^e normal in f16: the kernel builds it by a shift
 
 HX_HD int e2m1_block_exp(double amax) {
   if (!(amax > 0.0)) return 0;

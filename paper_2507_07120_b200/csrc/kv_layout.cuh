@@ -70,9 +70,11 @@ __host__ __device__ __forceinline__ uint32_t kv4_offset(int dp, int t, int d, bo
   return (is_v ? 8u * static_cast<uint32_t>(dp) : 0u) + (off >> 2);
 }
 __host__ __device__ __forceinline__ uint32_t kv4_scale_offset(int dp, int t, int d, bool is_v) {
-  return 16u * static_cast<uint32_t>(dp) + (is_v ? static_cast<uint32_t>(dp) / 2u : 0u) +
-         static_cast<uint32_t>(t * (dp / 32) + d / 32);
+  return 16u * static_cast<uint32_t>(dp) +
+         (is_v ? static_cast<uint32_t>(dp) / 2u + static_cast<uint32_t>((d / 32) * 16 + t)
+               : static_cast<uint32_t>(t * (dp / 32) + d / 32));
 }
+constexpr int kE2m1ExpBias = 15;  // stored exponent byte = e + 15
 // page bytes for a KV storage type: 0 bf16, 1 fp8, 2 fp4
 __host__ __device__ __forceinline__ uint32_t page_bytes_kvt(int dp, int kvt) {
   return kvt == 2 ? page_bytes_kv4(dp) : page_bytes_kv(dp, kvt == 1);

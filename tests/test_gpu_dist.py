@@ -77,10 +77,11 @@ def test_loopback_pool_matches_oracle(tpa, kvp, hopb):
 
 
 def test_loopback_hopb_long_context_group16():
-    """HOP-B launches attention once per request with its own (larger) split
-    count; at a context long enough that it differs from the batched launch's,
-    every split must still be covered. GQA group 16 runs the two-query-chunk
-    kernel variant (each KV page read once for 16 query heads)."""
+    """HOP-B at a long context with many small work items (HX_ATTN_SPLIT): the
+    request-ordered attention launch reduces and pushes every stream from
+    inside the kernel -- every split of every stream must be counted exactly
+    once. GQA group 16 runs the W16 consumers (each KV page read once for 16
+    query heads)."""
     import paper_2507_07120_b200 as P
     from paper_2507_07120_b200.model import Loopback
     H, Q, K, D, F, L, V, B, kvp = 1024, 32, 2, 32, 512, 1, 500, 4, 2
@@ -98,8 +99,7 @@ def test_loopback_hopb_long_context_group16():
             del os.environ["HX_ATTN_SPLIT"]
         else:
             os.environ["HX_ATTN_SPLIT"] = old
-    info = engines[0].info()
-    assert info["attn_splits"] < (S // kvp // 16) // 8, info  # the per-request launch uses more splits
+    assert engines[0].info()["exchange"] == 3  # HOP-B: reduce + push inside the attention kernel
     o = O.Model(H, Q, K, D, F, L, V, tpa=1, kvp=kvp, chunk=16, batch=B, seed=77, qkv_hash=True, bf16=True)
     for e in engines:
         e.init_weights(77, qkv="hash")

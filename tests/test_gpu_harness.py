@@ -162,3 +162,26 @@ def test_wide_kvp_local_pool_matches_oracle(P, dims, tpa, kvp, chunk, ctx):
         want, _ = o.step_append(x, k_gpu, v_gpu)
         assert rel_err(got, want) <= TOL_ARITH
     assert [g.effective_tokens(r) for r in range(kvp)] == [o.effective_tokens(r) for r in range(kvp)]
+
+
+def test_short_context_in_a_large_engine_plans_from_the_live_context(P):
+    """The attention split plan follows the live context (engine.cpp
+    live_splits), not the capacity: a 1M-token engine serving a 600-token
+    context launches few, full-size work items -- and stays exact as the
+    context grows across plan buckets."""
+    dims = (32, 8, 128)
+    g = P.DecodeHarness(dims, 1, 1, 16, 3, batch=2, capacity=1 << 20)
+    o = [O.Harness(*dims, 1, 1, 16, 3, bf16=True) for _ in range(2)]
+    for b in range(2):
+        g.grow_random(600 + 300 * b, P.Rng(40 + b), request=b)
+        o[b].grow_random(600 + 300 * b, O.Rng(40 + b))
+    assert g.info()["attn_splits"] <= 2, g.info()  # 57 pages: items of >= 32 pages
+    rx = np.random.default_rng(5)
+    case = {"chunk": 16, "kvp": 1, "kv_heads": 8}
+    for step in range(3):
+        x = rx.uniform(-1, 1, size=(2, 4096)).astype(np.float32)
+        got = g.step(x)
+        for b in range(2):
+            k_gpu, v_gpu = appended_rows(g, case, b)
+            want, _ = o[b].step_append(x[b].astype(np.float64), k_gpu, v_gpu)
+            assert rel_err(got[b], want) <= TOL_ARITH
