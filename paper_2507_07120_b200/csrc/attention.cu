@@ -1038,14 +1038,8 @@ static size_t attn_smem_bytes() {
 template <int DP, int NWC, int NSTAGE, int QC, int KVF, bool W16>
 static cudaError_t launch_attn_t(const AttnParams& p, int grid, cudaStream_t stream) {
   const size_t smem = attn_smem_bytes<DP, NWC, NSTAGE, QC, KVF, W16>();
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_decode_kernel<DP, NWC, NSTAGE, QC, KVF, W16>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  const cudaError_t e = smem_optin<attn_decode_kernel<DP, NWC, NSTAGE, QC, KVF, W16>>(smem);
+  if (e != cudaSuccess) return e;
   return launch_k(attn_decode_kernel<DP, NWC, NSTAGE, QC, KVF, W16>, dim3(grid), dim3((NWC + 1) * 32), smem, stream,
                   p);
 }

@@ -536,12 +536,9 @@ size_t gemv_smem_bytes(const GemvParams& p) {
 template <int NB8, int EM, int XS, bool NORM, bool W8 = false>
 static cudaError_t launch_t(const GemvParams& p, int grid, cudaStream_t stream) {
   const size_t smem = gemv_smem_bytes(p);
-  static size_t configured = 0;  // opt in once per instantiation
-  if (!p.tc && smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemv_kernel<NB8, EM, XS, NORM, W8>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (!p.tc) {
+    cudaError_t e = smem_optin<gemv_kernel<NB8, EM, XS, NORM, W8>>(smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   // FP8 weights: the consumer's per-k-step chain (e4m3 widening + 2 MMAs) is
   // latency-bound at 8 warps per SM, so two CTAs per SM (half-size ring stages)
@@ -556,12 +553,9 @@ static cudaError_t launch_t(const GemvParams& p, int grid, cudaStream_t stream) 
   const int threads = std::min(1024, (rows_here * per + 31) / 32 * 32);
   const int gy = (p.group_count && EM == E_SWIGLU) ? p.n_groups_max : 1;
   const size_t epi_smem = p.ksplit <= 4 ? 0 : static_cast<size_t>(EM == E_SWIGLU ? 2 : 1) * 16 * threads * sizeof(float);
-  static size_t epi_configured = 0;
-  if (epi_smem > epi_configured) {
-    e = cudaFuncSetAttribute(gemv_epilogue_kernel<NB8, EM, NORM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(epi_smem));
+  if (epi_smem > 0) {
+    e = smem_optin<gemv_epilogue_kernel<NB8, EM, NORM>>(epi_smem);
     if (e != cudaSuccess) return e;
-    epi_configured = epi_smem;
   }
   return launch_k(gemv_epilogue_kernel<NB8, EM, NORM>, dim3(p.Npad / kRows, gy, gz), dim3(threads), epi_smem,
                   stream, p);

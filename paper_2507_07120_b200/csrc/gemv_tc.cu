@@ -248,13 +248,8 @@ template <int NB8, int XS, int KSTEPS, int NSTAGE>
 static cudaError_t launch_tc_t(const GemvParams& p, int grid, cudaStream_t stream) {
   constexpr size_t smem = tc_smem_bytes<NB8, KSTEPS, NSTAGE>();
   static_assert(smem <= 227 * 1024, "tcgen05 GEMV ring exceeds shared memory");
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemv_tc_kernel<NB8, XS, KSTEPS, NSTAGE>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  const cudaError_t e = smem_optin<gemv_tc_kernel<NB8, XS, KSTEPS, NSTAGE>>(smem);
+  if (e != cudaSuccess) return e;
   return launch_k(gemv_tc_kernel<NB8, XS, KSTEPS, NSTAGE>, dim3(grid), dim3(kTcThreads), smem, stream, p);
 }
 

@@ -5,6 +5,8 @@
 #include <stddef.h>
 #include <stdint.h>
 
+#include <mutex>
+
 namespace hx {
 
 #ifdef __CUDACC__
@@ -20,6 +22,25 @@ HX_HD inline int xf_nb8(int batch) { return batch <= 8 ? 1 : (batch <= 16 ? 2 : 
 // max_gpus (types.hpp:63).
 constexpr int kMaxKvp = 64;
 
+
+// Dynamic shared memory opt-in (cudaFuncAttributeMaxDynamicSharedMemorySize)
+// lives in each device's context: remembered per (kernel, device) with the
+// largest size set so far, under a lock (loopback pools launch from several
+// host threads; engines may sit on different devices of one process).
+template <auto Kernel>
+cudaError_t smem_optin(size_t bytes) {
+  static std::mutex mu;
+  static size_t done[64] = {};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const int slot = dev >= 0 && dev < 64 ? dev : 63;
+  std::lock_guard<std::mutex> lk(mu);
+  if (bytes <= done[slot] && dev < 64) return cudaSuccess;
+  e = cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes));
+  if (e == cudaSuccess) done[slot] = bytes;
+  return e;
+}
 
 // Programmatic dependent launch for the decode-step kernels (set by the engine).
 void set_pdl(bool on);

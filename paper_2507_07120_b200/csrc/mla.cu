@@ -577,12 +577,9 @@ size_t mla_smem_bytes() { return kSmem; }
 
 cudaError_t launch_mla_decode(const AttnParams& p, int grid, cudaStream_t stream, const void* tm_s, const void* tm_v) {
   if (p.q_heads > kMlaHeads || p.q_heads < 1) return cudaErrorInvalidValue;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(mla_decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmem));
+  {
+    const cudaError_t e = smem_optin<mla_decode_kernel>(kSmem);
     if (e != cudaSuccess) return e;
-    configured = true;
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(static_cast<unsigned>(2 * grid));  // grid = number of CTA pairs
@@ -817,12 +814,9 @@ static cudaError_t launch_head_gemm_t(const float* in, int in_head_stride, int i
   const int cols = dout / col_chunks;
   if (cols % 8 || din % DS || (cols / 8) * DS > 512) return cudaErrorInvalidValue;
   const size_t smem = (static_cast<size_t>(din) * 8 + static_cast<size_t>(DS) * 8 * cols) * sizeof(float);
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaError_t e = cudaFuncSetAttribute(mla_head_gemm_kernel<ABSORB, DS>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  {
+    const cudaError_t e = smem_optin<mla_head_gemm_kernel<ABSORB, DS>>(smem);
     if (e != cudaSuccess) return e;
-    configured = smem;
   }
   const int threads = (cols / 8) * DS;
   return launch_k(mla_head_gemm_kernel<ABSORB, DS>, dim3(heads, col_chunks), dim3((threads + 31) / 32 * 32), smem,

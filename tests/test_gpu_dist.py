@@ -31,6 +31,12 @@ def test_loopback_pool_matches_oracle(tpa, kvp, hopb):
     engines = [P.HelixDecoder(spec, tpa=tpa, kvp=kvp, chunk_size=16, batch=B, capacity=400, layers=L, vocab=V,
                               use_graphs=False, hopb=hopb, pool=2, rank=r, loopback=lb) for r in range(n)]
     o = O.Model(H, Q, K, D, F, L, V, tpa=tpa, kvp=kvp, chunk=16, batch=B, seed=4321, bf16=True)
+    # launches per step (engine.cpp launches_per_step): embed + LM head x2 + argmax; per layer
+    # QKV x2, attention [+ split reduce with the device push under HOP-B off], flag wait,
+    # merge, O x2, residual, gate/up x2, down x2, residual
+    info = engines[0].info()
+    assert info["exchange"] == (3 if hopb else 2)
+    assert info["kernels_per_step"] == 4 + L * (11 + (2 if hopb else 3))
     for e in engines:
         e.init_weights(4321, qkv="mt19937")
     for l in range(L):
