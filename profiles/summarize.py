@@ -63,14 +63,14 @@ def full(rep, out, summary=None):
 
 def hopb(path, out):
     rows = [json.loads(l) for l in open(path) if l.strip()]
-    ok = [r for r in rows if "attn_batched_ms" in r]
-    lines = ["| KVP | context | B | KV tok/GPU | attn batched (ms) | attn per-request (ms) | layer off (ms) | "
+    ok = [r for r in rows if "attn_ms_off" in r]
+    lines = ["| KVP | context | B | KV tok/GPU | attn+reduce off (ms) | attn, in-kernel push on (ms) | layer off (ms) | "
              "layer on (ms) | a2a modeled (us) | exposed off (us) | exposed on (us) | hidden | HOP-B net (us) |",
              "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in ok:
         hf = r.get("a2a_hidden_frac")
         lines.append(f"| {r['kvp']} | {r['context']} | {r['batch']} | {r['kv_tokens_per_gpu']} | "
-                     f"{r['attn_batched_ms']:.3f} | {r['attn_hopb_ms']:.3f} | {r['layer_ms_off']:.3f} | "
+                     f"{r['attn_ms_off']:.3f} | {r['attn_ms_on']:.3f} | {r['layer_ms_off']:.3f} | "
                      f"{r['layer_ms_on']:.3f} | {r['a2a_ms_modeled'] * 1e3:.2f} | {r['exposed_a2a_ms_off'] * 1e3:.2f} | "
                      f"{r['exposed_a2a_ms_on'] * 1e3:.2f} | {'-' if hf is None else f'{hf:.2f}'} | "
                      f"{r['hopb_gain_ms'] * 1e3:+.1f} |")
