@@ -64,6 +64,10 @@ def full(rep, out, summary=None):
 def hopb(path, out):
     rows = [json.loads(l) for l in open(path) if l.strip()]
     ok = [r for r in rows if "attn_ms_off" in r]
+    for r in ok:  # both modes end with the same flag wait (older records counted it on one side only)
+        if abs(r["exposed_a2a_ms_off"] - r["a2a_ms_modeled"]) < 1e-12:
+            r["exposed_a2a_ms_off"] += r["flag_wait_ms_off"]
+            r["hopb_gain_ms"] = (r["attn_ms_off"] + r["exposed_a2a_ms_off"]) - (r["attn_ms_on"] + r["exposed_a2a_ms_on"])
     lines = ["| KVP | context | B | KV tok/GPU | attn+reduce off (ms) | attn, in-kernel push on (ms) | layer off (ms) | "
              "layer on (ms) | a2a modeled (us) | exposed off (us) | exposed on (us) | hidden | HOP-B net (us) |",
              "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]

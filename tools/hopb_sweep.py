@@ -106,12 +106,14 @@ def point(P, Loopback, spec, kvp, S, B, steps=5):
     # on: each stream's slices leave as the stream completes -- the reference's
     # hopb_schedule at the kernel's exchange granularity (R = streams)
     span_on = hopb_schedule(streams, out["attn_ms_on"] / streams, t / streams, True)
+    # both modes end with the same one-CTA flag wait (device-initiated exchange)
     exp_on = max(0.0, span_on - out["attn_ms_on"]) + out["flag_wait_ms_on"]
+    exp_off = t + out["flag_wait_ms_off"]
     out.update({
-        "streams": streams, "a2a_ms_modeled": t, "exposed_a2a_ms_off": t, "exposed_a2a_ms_on": exp_on,
+        "streams": streams, "a2a_ms_modeled": t, "exposed_a2a_ms_off": exp_off, "exposed_a2a_ms_on": exp_on,
         "a2a_hidden_frac": (1.0 - max(0.0, span_on - out["attn_ms_on"]) / t) if t > 0 else None,
         # what HOP-B buys end to end at this point, its compute price included
-        "hopb_gain_ms": (out["attn_ms_off"] + t) - (out["attn_ms_on"] + exp_on),
+        "hopb_gain_ms": (out["attn_ms_off"] + exp_off) - (out["attn_ms_on"] + exp_on),
     })
     return out
 
