@@ -293,7 +293,7 @@ def kvp_slices(a):
     return out
 
 
-KV_ELEM_BYTES = {"bf16": 2.0, "fp8": 1.0, "fp4": 17.0 / 32.0}  # fp4: e2m1 nibble + one exponent byte per 32
+KV_ELEM_BYTES = {"bf16": 2.0, "fp8": 1.0, "fp4": 17.5 / 32.0}  # fp4: e2m1 nibble + a K exponent byte / V f16 scale per 32
 KV_KERNEL = {"bf16": "attn_decode_kernel<128,7,3,1,bf16>", "fp8": "attn_decode_kernel<128,10,4,1,fp8>",
              "fp4": "attn_decode_kernel<128,10,6,1,fp4>"}
 

@@ -54,8 +54,8 @@ template <int DP, int KVF>
 struct AttnCfg {
   static constexpr int KS = DP / 16;     // k-steps over the head dim
   static constexpr int ND = DP / 8;      // PV n-tiles
-  // kv_layout.cuh: bf16 64*DP, fp8 32*DP, fp4 17*DP bytes per page
-  static constexpr uint32_t PAGE = KVF == 2 ? 17u * DP : (KVF == 1 ? 32u : 64u) * DP;
+  // kv_layout.cuh: bf16 64*DP, fp8 32*DP, fp4 17.5*DP bytes per page
+  static constexpr uint32_t PAGE = KVF == 2 ? 35u * DP / 2u : (KVF == 1 ? 32u : 64u) * DP;
 };
 
 // KVF = 1: FP8 e4m3 pages; each lane's 8-byte chunk widens to the f16 register
@@ -135,10 +135,8 @@ __device__ __forceinline__ uint4 load_v(uint32_t pbase, int ci) {
     uint4 r;
     e2m1x8_to_f16x2x4(lds32(pbase + 8 * DP + ci * 4), r.x, r.y, r.z, r.w);
     const int c = ci & 3, grp = (ci >> 5) >> 1;
-    const uint32_t sb = pbase + 16 * DP + DP / 2 + grp * 16;  // V exponents [DP/32][16 tokens]
-    const uint32_t w0 = lds16(sb + 2 * c), w8 = lds16(sb + 2 * c + 8);  // tokens (2c, 2c+1), (2c+8, 2c+9)
-    const uint32_t lo = ((w0 & 0xFFu) << 10) | ((w0 >> 8) << 26);
-    const uint32_t hi = ((w8 & 0xFFu) << 10) | ((w8 >> 8) << 26);
+    const uint32_t sb = pbase + 16 * DP + DP / 2 + grp * 32;  // V scales, f16 [DP/32][16 tokens]
+    const uint32_t lo = lds32(sb + 4 * c), hi = lds32(sb + 4 * c + 16);  // tokens (2c, 2c+1), (2c+8, 2c+9)
     r.x = hmul2(r.x, lo);
     r.y = hmul2(r.y, hi);
     r.z = hmul2(r.z, lo);

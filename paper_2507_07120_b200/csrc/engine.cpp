@@ -391,6 +391,11 @@ void Engine::alloc() {
     split_env_ = true;
     std::sscanf(split_env, "%d,%d", &ips_, &min_pages_);
   }
+  // tcgen05 kernel for quantised pages: opt-in (HX_ATTN_TC=1) -- the e4m3 / e2m1
+  // widening it still pays on the CUDA cores keeps it behind the legacy kernel
+  // (K1-TC)
+  attn_tc_ = !mla_ && (kv8_ || kv4_) && DP_ == 128 && q_chunks_ == 1 && std::getenv("HX_ATTN_TC") &&
+             std::getenv("HX_ATTN_TC")[0] == '1';
   n_streams_ = n_slots_ * B_ * kvh_per_slot_ * q_chunks_;
   const int req_streams = n_slots_ * kvh_per_slot_ * q_chunks_;
   splits_ = plan_splits(n_streams_, page_cap_);
@@ -1157,7 +1162,7 @@ void Engine::read_kv(int64_t layer, int64_t request, int64_t rank, int64_t head,
         bool high = false;
         const uint32_t off = kv4_offset(DP_, static_cast<int>(t % 16), d, w != 0, &high);
         const uint8_t code = static_cast<uint8_t>((page[off] >> (high ? 4 : 0)) & 15);
-        const int ex = static_cast<int>(page[kv4_scale_offset(DP_, static_cast<int>(t % 16), d, w != 0)]) - kE2m1ExpBias;
+        const int ex = kv4_scale_exp(page[kv4_scale_offset(DP_, static_cast<int>(t % 16), d, w != 0)], w != 0);
         (w ? v : k)[t * D_ + d] = e2m1_to_float(code, ex);
       }
   }
@@ -1283,7 +1288,10 @@ void Engine::launch_attention_kernels(const AttnParams& a) {
     mark(2);
     cuda_check(launch_mla_split_reduce(a, d_frag_o_, d_frag_lse_, stream_), "mla split reduce");
   } else {
-    cuda_check(launch_attn_decode(a, std::min(attn_grid_, a.n_items), stream_), "attention");
+    if (attn_tc_ && attn_tc_supported(a))
+      cuda_check(launch_attn_tc(a, std::min(attn_grid_, a.n_items), stream_), "attention (tcgen05)");
+    else
+      cuda_check(launch_attn_decode(a, std::min(attn_grid_, a.n_items), stream_), "attention");
     mark(2);
     if (!a.fused) cuda_check(launch_attn_split_reduce(a, d_frag_o_, d_frag_lse_, stream_), "split reduce");
   }

@@ -144,6 +144,7 @@ class Engine {
   int ips_ = 8, min_pages_ = 32;  // split planner knobs (HX_ATTN_SPLIT)
   bool split_env_ = false;
   int plan_splits(int streams, int pages) const;
+  bool attn_tc_ = false;  // quantised pages on the tcgen05 kernel (attention_tc.cu)
   int live_splits(int64_t layer, bool per_request) const;
 
   // ---- device state

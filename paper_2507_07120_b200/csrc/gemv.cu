@@ -496,7 +496,7 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
               const uint32_t off = kv4_offset(p.dp, static_cast<int>(row & 15), d, is_v != 0, &high);
               const uint32_t code = e2m1_from_double(static_cast<double>(y[0]), ex);
               atomicOr(reinterpret_cast<unsigned*>(pg + (off & ~3u)), code << ((off & 3u) * 8u + (high ? 4u : 0u)));
-              if ((d & 31) == 0) pg[kv4_scale_offset(p.dp, static_cast<int>(row & 15), d, is_v != 0)] = static_cast<uint8_t>(ex + kE2m1ExpBias);
+              if ((d & 31) == 0) pg[kv4_scale_offset(p.dp, static_cast<int>(row & 15), d, is_v != 0)] = kv4_scale_byte(ex, is_v != 0);
             } else {
               uint8_t* dst = p.kv + page * page_bytes_kv(p.dp, p.kv8 != 0) +
                              kv_offset(p.dp, static_cast<int>(row & 15), d, is_v != 0, p.kv8 != 0);

@@ -107,6 +107,11 @@ struct AttnParams {
   int xchunk, xslice, xrank;
 };
 cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t stream);
+// Quantised (FP8 / FP4) pages at DP = 128, <= 16 query rows, no fused reduce:
+// the tcgen05 kernel (attention_tc.cu). grid = CTAs; items are statically
+// assigned (item = CTA + n * grid).
+bool attn_tc_supported(const AttnParams& p);
+cudaError_t launch_attn_tc(const AttnParams& p, int grid, cudaStream_t stream);
 // FP4 (e2m1 block) KV pages (kv_layout.cuh kv4_*): device hash fill, and the
 // scatter of host-quantized rows (codes per element, exponents per 32-dim block).
 cudaError_t launch_kv4_fill_hash(uint8_t* kv, int* total, int batch, int kv_heads, int kvh_per_slot, int kvp,

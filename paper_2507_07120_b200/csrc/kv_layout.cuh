@@ -60,21 +60,32 @@ __host__ __device__ __forceinline__ uint32_t kv_offset(int dp, int t, int d, boo
 // FP4 (e2m1, fp8.cuh) pages: the same fragment order with 4-bit elements (a
 // lane's 16-byte bf16 chunk becomes 4 bytes; element 2r of the chunk in the low
 // nibble of byte r), K data [0, 8*DP), V data [8*DP, 16*DP), then the block
-// exponents (e + 127, one byte per token and 32-dim group): K [16][DP/32] at
-// 16*DP, V [16][DP/32] at 16*DP + DP/2. A page is 17*DP bytes.
-__host__ __device__ __forceinline__ uint32_t page_bytes_kv4(int dp) { return 17u * static_cast<uint32_t>(dp); }
+// scales 2^e (one per token and 32-dim group): K as exponent bytes e + 15,
+// [16][DP/32] at 16*DP; V as ready-made f16 values, [DP/32][16 tokens] x 2 B
+// at 16*DP + DP/2 -- so the V converters of the tcgen05 kernel load the f16x2
+// scale of tokens (2c, 2c+1) as one word (attention_tc.cu). The f16 of 2^e is
+// (e + 15) << 10: low byte 0, high byte (e + 15) << 2. A page is 17.5*DP bytes.
+__host__ __device__ __forceinline__ uint32_t page_bytes_kv4(int dp) { return 35u * static_cast<uint32_t>(dp) / 2u; }
 // byte offset of element (t, d) and whether it is the high nibble
 __host__ __device__ __forceinline__ uint32_t kv4_offset(int dp, int t, int d, bool is_v, bool* high) {
   const uint32_t off = is_v ? v_offset(dp, t, d) - 32u * static_cast<uint32_t>(dp) : k_offset(dp, t, d);
   *high = ((off >> 1) & 1u) != 0;
   return (is_v ? 8u * static_cast<uint32_t>(dp) : 0u) + (off >> 2);
 }
+// the byte that carries the block scale of (t, d): K its exponent byte, V the
+// high byte of its f16 (the low byte stays 0)
 __host__ __device__ __forceinline__ uint32_t kv4_scale_offset(int dp, int t, int d, bool is_v) {
   return 16u * static_cast<uint32_t>(dp) +
-         (is_v ? static_cast<uint32_t>(dp) / 2u + static_cast<uint32_t>((d / 32) * 16 + t)
+         (is_v ? static_cast<uint32_t>(dp) / 2u + static_cast<uint32_t>((d / 32) * 32 + 2 * t + 1)
                : static_cast<uint32_t>(t * (dp / 32) + d / 32));
 }
-constexpr int kE2m1ExpBias = 15;  // stored exponent byte = e + 15
+constexpr int kE2m1ExpBias = 15;  // K: stored exponent byte = e + 15
+__host__ __device__ __forceinline__ uint8_t kv4_scale_byte(int e, bool is_v) {
+  return static_cast<uint8_t>(is_v ? (e + kE2m1ExpBias) << 2 : e + kE2m1ExpBias);
+}
+__host__ __device__ __forceinline__ int kv4_scale_exp(uint8_t byte, bool is_v) {
+  return (is_v ? byte >> 2 : byte) - kE2m1ExpBias;
+}
 // page bytes for a KV storage type: 0 bf16, 1 fp8, 2 fp4
 __host__ __device__ __forceinline__ uint32_t page_bytes_kvt(int dp, int kvt) {
   return kvt == 2 ? page_bytes_kv4(dp) : page_bytes_kv(dp, kvt == 1);

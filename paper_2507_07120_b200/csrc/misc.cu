@@ -333,7 +333,7 @@ __global__ void kv4_fill_hash_kernel(uint8_t* kv, const int* total, int batch, i
     }
   }
   if (!is_v) *reinterpret_cast<uint4*>(pg + kbase) = make_uint4(words[0], words[1], words[2], words[3]);
-  pg[kv4_scale_offset(dp, t, grp * 32, is_v != 0)] = static_cast<uint8_t>(ex + kE2m1ExpBias);
+  pg[kv4_scale_offset(dp, t, grp * 32, is_v != 0)] = kv4_scale_byte(ex, is_v != 0);
 }
 
 cudaError_t launch_kv4_fill_hash(uint8_t* kv, int* total, int batch, int kv_heads, int kvh_per_slot, int kvp,
@@ -383,7 +383,7 @@ __global__ void kv4_append_rows_kernel(uint8_t* kv, const uint8_t* codes_k, cons
              static_cast<uint32_t>(codes[d]) << ((off & 3u) * 8u + (high ? 4u : 0u)));
   }
   const int8_t ex = (is_v ? exp_v : exp_k)[(static_cast<size_t>(tok) * kv_heads + h) * groups + grp];
-  pg[kv4_scale_offset(dp, t, grp * 32, is_v != 0)] = static_cast<uint8_t>(ex + kE2m1ExpBias);
+  pg[kv4_scale_offset(dp, t, grp * 32, is_v != 0)] = kv4_scale_byte(ex, is_v != 0);
 }
 
 cudaError_t launch_kv4_append_rows(uint8_t* kv, const uint8_t* codes_k, const uint8_t* codes_v, const int8_t* exp_k,

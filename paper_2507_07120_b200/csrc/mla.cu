@@ -250,10 +250,12 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
         ++qcount;
         mbar_arrive_cluster_relaxed(l_pq);
       }
-    } else if (lane == 0 && leader) {
+    } else if (leader) {
       // ---------------------------------------------------------- leader: MMA issue
       // order S(0) S(1) V(0) S(2) V(1) ... (a non-blocking scheduler interleaving
-      // the two streams measured slower: both rings are latency-bound anyway)
+      // the two streams measured slower: both rings are latency-bound anyway).
+      // The whole warp walks the loop and waits; one elected lane issues (a
+      // lone-lane issue loop cost ~145 cycles per tcgen05.mma, tc05.cuh elect_one).
       int us = 0, uv = 0, qcount = 0, g0 = 0, items = 0;
       for (int item = cluster_id; item < p.n_items; item += n_clusters) {
         const MlaItem it = decode_item(p, item);
@@ -276,16 +278,22 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
               const int s = us % kSSlots;
               mbar_wait(&full_s[s], (us / kSSlots) & 1);  // both CTAs' chunks (2-SM TMA)
               tc_fence_after();
+              const uint64_t a0 = umma_desc(sbase + kOffS + s * kSChunk, 2048, 128);
+              const uint64_t b0 = umma_desc(sbase + kOffQ + 4 * j * 2048, 1024, 128);
+              if (elect_one()) {
 #pragma unroll
-              for (int kk = 0; kk < 4; ++kk) {
-                const uint64_t a = umma_desc(sbase + kOffS + s * kSChunk + kk * 4096, 2048, 128);
-                const uint64_t bd = umma_desc(sbase + kOffQ + (4 * j + kk) * 2048, 1024, 128);
-                umma_ss_pair(d, a, bd, kIdescST, (j | kk) != 0);
+                for (int kk = 0; kk < 4; ++kk)
+                  umma_ss_pair(d, a0 + static_cast<uint64_t>((kk * 4096) >> 4),
+                               b0 + static_cast<uint64_t>((kk * 2048) >> 4), kIdescST, (j | kk) != 0);
+                umma_commit_pair(&empty_s[s]);
               }
-              umma_commit_pair(&empty_s[s]);
+              __syncwarp();
             }
-            if (tile == n - 1) umma_commit_pair(q_free);
-            umma_commit_pair(&s_full[g & 1]);
+            if (elect_one()) {
+              if (tile == n - 1) umma_commit_pair(q_free);
+              umma_commit_pair(&s_full[g & 1]);
+            }
+            __syncwarp();
           } else {
             mbar_wait(pt_full, g & 1);
             if (tile == 0 && items > 0) mbar_wait_cluster(o_free, (items - 1) & 1);
@@ -296,15 +304,20 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
                 const int s = uv % kVSlots;
                 mbar_wait(&full_v[s], (uv / kVSlots) & 1);  // both CTAs' blocks (2-SM TMA)
                 tc_fence_after();
+                const uint64_t a0 = umma_desc(sbase + kOffV + s * kVBlock, 128, 2048);
+                const uint64_t b0 = umma_desc(sbase + kOffPT + 8 * pp * 2048, 1024, 128);
+                const bool acc0 = tile > 0 || pp > 0;
+                if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < kMlaPageRows / 16; ++kk) {
-                  const uint64_t a = umma_desc(sbase + kOffV + s * kVBlock + kk * 256, 128, 2048);
-                  const uint64_t bd = umma_desc(sbase + kOffPT + (8 * pp + kk) * 2048, 1024, 128);
-                  umma_ss_pair(tbase + 256 + 128 * jb, a, bd, kIdescOT, (tile > 0 || pp > 0 || kk > 0) ? 1u : 0u);
+                  for (int kk = 0; kk < kMlaPageRows / 16; ++kk)
+                    umma_ss_pair(tbase + 256 + 128 * jb, a0 + static_cast<uint64_t>((kk * 256) >> 4),
+                                 b0 + static_cast<uint64_t>((kk * 2048) >> 4), kIdescOT, (acc0 || kk > 0) ? 1u : 0u);
+                  umma_commit_pair(&empty_v[s]);
                 }
-                umma_commit_pair(&empty_v[s]);
+                __syncwarp();
               }
-            umma_commit_pair(pv_done);
+            if (elect_one()) umma_commit_pair(pv_done);
+            __syncwarp();
           }
         }
         g0 += n;

@@ -45,6 +45,15 @@ HX_DEV void tmem_alloc(uint32_t* smem_result, uint32_t ncols) {
 HX_DEV void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
   asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(taddr), "r"(ncols) : "memory");
 }
+// One lane of a converged warp (elect.sync). Issue tcgen05.mma from a
+// converged warp through this rather than from a lone lane: in a lone-lane
+// branch the per-lane descriptor values go through R2UR / waterfall code and
+// each MMA costs ~145 cycles to issue; converged, ~21 (tools/tc_issue_probe.cu).
+HX_DEV bool elect_one() {
+  uint32_t pred;
+  asm volatile("{\n.reg .pred P;\nelect.sync _|P, 0xffffffff;\nselp.u32 %0, 1, 0, P;\n}" : "=r"(pred));
+  return pred != 0;
+}
 HX_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 HX_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 

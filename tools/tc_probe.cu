@@ -1,0 +1,137 @@
+// Probe of the tcgen05 operand forms the quantised GQA decode kernel
+// (attention_tc.cu) relies on, checked against a host product:
+//   test 0: D[128 x N] = A[128 x 128] . B^T, A f16 in TMEM (lane = row m,
+//           column j = elements k = 2j, 2j+1), B f16 K-major in shared memory
+//   test 1: same A, B f16 MN-major in shared memory ([n/8][k/8][k%8][n%8])
+//   test 2: A f16 K-major in shared memory (control)
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O2 -I paper_2507_07120_b200/csrc tools/tc_probe.cu -o tools/tc_probe
+#include <cuda_fp16.h>
+#include <cstdio>
+#include <cstdlib>
+#include <cmath>
+
+#include "common.cuh"
+#include "tc05.cuh"
+
+using namespace hx;
+
+constexpr int M = 128, K = 128;
+
+__host__ __device__ constexpr uint32_t idesc_f16(int m, int n, bool a_mn, bool b_mn) {
+  return (1u << 4) | (static_cast<uint32_t>(a_mn) << 15) | (static_cast<uint32_t>(b_mn) << 16) |
+         (static_cast<uint32_t>(n >> 3) << 17) | (static_cast<uint32_t>(m >> 4) << 24);
+}
+
+__host__ __device__ float aval(int m, int k) { return (((m * 7 + k * 3) % 9) - 4) * 0.25f; }
+__host__ __device__ float bval(int n, int k) { return (((n * 5 + k) % 7) - 3) * 0.5f; }
+
+template <int N>
+__global__ void probe(int test, float* out) {
+  __shared__ __align__(1024) __half bs[N * K];
+  __shared__ __align__(1024) __half as[M * K];
+  __shared__ uint32_t tbase;
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) tmem_alloc(&tbase, 256);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  // B image
+  for (int i = tid; i < N * K; i += 128) {
+    const int n = i / K, k = i % K;
+    int off;
+    if (test == 1)
+      off = (((n >> 3) * (K / 8) + (k >> 3)) * 8 + (k & 7)) * 8 + (n & 7);  // MN-major
+    else
+      off = (((k >> 3) * (N / 8) + (n >> 3)) * 8 + (n & 7)) * 8 + (k & 7);  // K-major
+    bs[off] = __float2half(bval(n, k));
+  }
+  for (int i = tid; i < M * K; i += 128) {  // A K-major smem image (test 2)
+    const int m = i / K, k = i % K;
+    as[(((k >> 3) * (M / 8) + (m >> 3)) * 8 + (m & 7)) * 8 + (k & 7)] = __float2half(aval(m, k));
+  }
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tbase;
+  // A into TMEM columns [0, 64): lane = row
+  {
+    const int m = tid;
+    uint32_t r[16];
+    for (int c0 = 0; c0 < 64; c0 += 16) {
+      for (int j = 0; j < 16; ++j) {
+        const int k = 2 * (c0 + j);
+        __half2 h = __floats2half2_rn(aval(m, k), aval(m, k + 1));
+        r[j] = *reinterpret_cast<uint32_t*>(&h);
+      }
+      tmem_st16(tm + (static_cast<uint32_t>(warp * 32) << 16) + c0, r);
+    }
+    tmem_wait_st();
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (tid == 0) {
+    const uint32_t d = tm + 128;
+    for (int ks = 0; ks < K / 16; ++ks) {
+      if (test == 2) {
+        const uint64_t a = umma_desc(smem_u32(as) + ks * 2 * (M / 8) * 128, (M / 8) * 128, 128);
+        const uint64_t b = umma_desc(smem_u32(bs) + ks * 2 * (N / 8) * 128, (N / 8) * 128, 128);
+        umma_ss(d, a, b, idesc_f16(M, N, false, false), ks > 0);
+      } else if (test == 1) {
+        const uint64_t b = umma_desc(smem_u32(bs) + ks * 2 * 128, 128, (K / 8) * 128);
+        umma_ts(d, tm + ks * 8, b, idesc_f16(M, N, false, true), ks > 0);
+      } else {
+        const uint64_t b = umma_desc(smem_u32(bs) + ks * 2 * (N / 8) * 128, (N / 8) * 128, 128);
+        umma_ts(d, tm + ks * 8, b, idesc_f16(M, N, false, false), ks > 0);
+      }
+    }
+    umma_commit(&bar);
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  float v[32];
+  tmem_ld32(tm + (static_cast<uint32_t>(warp * 32) << 16) + 128, v);
+  for (int n = 0; n < N; ++n) out[tid * N + n] = v[n];
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tm, 256);
+}
+
+template <int N>
+int run(int test) {
+  float* d;
+  cudaMalloc(&d, M * N * 4);
+  cudaMemset(d, 0, M * N * 4);
+  probe<N><<<1, 128>>>(test, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    printf("test %d N=%d: CUDA error %s\n", test, N, cudaGetErrorString(e));
+    return 1;
+  }
+  float h[M * N];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double err = 0;
+  for (int m = 0; m < M; ++m)
+    for (int n = 0; n < N; ++n) {
+      double r = 0;
+      for (int k = 0; k < K; ++k) r += static_cast<double>(aval(m, k)) * bval(n, k);
+      err = fmax(err, fabs(r - h[m * N + n]));
+    }
+  printf("test %d N=%d: max |err| = %g  (D[0][0..3] = %g %g %g %g)\n", test, N, err, h[0], h[1], h[2], h[3]);
+  cudaFree(d);
+  return err > 1e-3;
+}
+
+int main() {
+  int bad = 0;
+  bad += run<16>(2);
+  bad += run<32>(2);
+  bad += run<16>(0);
+  bad += run<32>(0);
+  bad += run<16>(1);
+  bad += run<32>(1);
+  printf(bad ? "PROBE FAILED\n" : "PROBE OK\n");
+  return bad;
+}
