@@ -578,11 +578,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
             const uint32_t s1w[4] = {v2[pq].x, v2[pq].y, v2[pq].z, v2[pq].w};  // tokens 2c+8, 2c+9
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
-              const uint32_t h = have ? __byte_perm(wd[c], 0u, sub ? 0x3232u : 0x1010u) : 0u;
               uint32_t a0, a1;
-              e2m1x4_to_f16x2x2(h, a0, a1);
-              w[8 * pq + c] = hmul2_(a0, s0w[c]);
-              w[8 * pq + 4 + c] = hmul2_(a1, s1w[c]);
+              e2m1x4_to_f16x2x2(__byte_perm(wd[c], 0u, sub ? 0x3232u : 0x1010u), a0, a1);
+              // pages past np: stale bytes (a stale scale may be inf / nan) -> exact zeros
+              w[8 * pq + c] = have ? hmul2_(a0, s0w[c]) : 0u;
+              w[8 * pq + 4 + c] = have ? hmul2_(a1, s1w[c]) : 0u;
             }
           }
         }

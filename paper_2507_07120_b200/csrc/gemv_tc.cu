@@ -162,8 +162,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvParams
       }
     }
   } else if (warp == 5) {
-    // ------------------------------------------------------------ MMA issue (one thread)
-    if (lane == 0) {
+    // ------------------------------------------------------------ MMA issue (one elected lane of
+    // the converged warp: tc05.cuh elect_one -- a lone-lane issue loop costs ~145 cycles per MMA)
+    {
       const uint32_t ring = smem_u32(smem);
       int uses = 0;  // accumulator buffer uses (tile t -> buffer t & 1)
       for (int st = 0;; ++st) {
@@ -173,30 +174,36 @@ __global__ void __launch_bounds__(kTcThreads, 1) gemv_tc_kernel(const GemvParams
         const int buf = uses & 1;
         if (m.tile == kTcDone || m.first) {
           if (uses >= 2) mbar_wait(&acc_empty[buf], ((uses >> 1) - 1) & 1);  // drained two tiles ago
-          acc_meta[buf * 4 + 0] = m.pb;
-          acc_meta[buf * 4 + 1] = m.kc;
-          acc_meta[buf * 4 + 2] = m.gi;
-          acc_meta[buf * 4 + 3] = m.tile == kTcDone;
-          mbar_arrive(&acc_ready[buf]);
+          if (lane == 0) {
+            acc_meta[buf * 4 + 0] = m.pb;
+            acc_meta[buf * 4 + 1] = m.kc;
+            acc_meta[buf * 4 + 2] = m.gi;
+            acc_meta[buf * 4 + 3] = m.tile == kTcDone;
+            mbar_arrive(&acc_ready[buf]);
+          }
+          __syncwarp();
           if (m.tile == kTcDone) break;
         }
         tc_fence_after();
         const uint32_t sw = ring + s * SB, sx = sw + 2 * SW;
-        for (int kk = 0; kk < m.nks; ++kk) {
+        const uint64_t a0 = umma_desc(sw, 128, 256), x0 = umma_desc(sx, 128, 256);
+        const uint32_t d0 = tbase + static_cast<uint32_t>(2 * buf * NC);
+        if (elect_one()) {
+          for (int kk = 0; kk < m.nks; ++kk) {
 #pragma unroll
-          for (int r2 = 0; r2 < 2; ++r2) {
-            const uint32_t d = tbase + static_cast<uint32_t>((2 * buf + r2) * NC);
-            const uint64_t a = umma_desc(sw + r2 * SW + kk * 4096u, 128, 256);
-            const uint32_t acc = (m.first && kk == 0) ? 0u : 1u;
-            umma_ss(d, a, umma_desc(sx + kk * XSTEP, 128, 256), IDESC2, acc);           // [hi | mid]
-            if (XS == 3) umma_ss(d, a, umma_desc(sx + kk * XSTEP + 2 * XT, 128, 256), IDESC1, 1u);  // lo -> hi half
+            for (int r2 = 0; r2 < 2; ++r2) {
+              const uint64_t a = a0 + static_cast<uint64_t>((r2 * SW + kk * 4096u) >> 4);
+              const uint64_t x = x0 + static_cast<uint64_t>((kk * XSTEP) >> 4);
+              const uint32_t acc = (m.first && kk == 0) ? 0u : 1u;
+              umma_ss(d0 + r2 * NC, a, x, IDESC2, acc);  // [hi | mid]
+              if (XS == 3) umma_ss(d0 + r2 * NC, a, x + static_cast<uint64_t>((2 * XT) >> 4), IDESC1, 1u);  // lo -> hi
+            }
           }
+          umma_commit(&empty[s]);  // the stage is free once these MMAs have read it
+          if (m.last) umma_commit(&acc_full[buf]);
         }
-        umma_commit(&empty[s]);  // the stage is free once these MMAs have read it
-        if (m.last) {
-          umma_commit(&acc_full[buf]);
-          ++uses;
-        }
+        __syncwarp();
+        if (m.last) ++uses;
       }
     }
   } else {
