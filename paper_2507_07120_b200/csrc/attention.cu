@@ -165,11 +165,27 @@ __device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
 }
 
 // Work item of (stream, split): split-major (every stream advances together --
-// the faster order for one batched launch) or stream-major (the splits of a
-// stream are adjacent, so streams and requests complete in order: HOP-B).
+// the faster order for one batched launch), or in groups of stream_major
+// consecutive streams, split-major inside a group and the groups in order
+// (1 = stream-major): streams, hence requests, complete group by group (HOP-B).
 __device__ __forceinline__ size_t attn_item(const AttnParams& p, int stream, int split) {
-  return p.stream_major ? static_cast<size_t>(stream) * p.splits + split
-                        : static_cast<size_t>(split) * p.n_streams + stream;
+  if (!p.stream_major) return static_cast<size_t>(split) * p.n_streams + stream;
+  const int G = p.stream_major, g0 = (stream / G) * G;
+  const int gs = min(G, p.n_streams - g0);  // streams in this (possibly short, last) group
+  return static_cast<size_t>(g0) * p.splits + static_cast<size_t>(split) * gs + (stream - g0);
+}
+__device__ __forceinline__ void attn_item_decode(const AttnParams& p, int item, int& stream, int& split) {
+  if (!p.stream_major) {
+    split = item / p.n_streams;
+    stream = item - split * p.n_streams;
+    return;
+  }
+  const int G = p.stream_major, per_group = G * p.splits;
+  const int g0 = (item / per_group) * G;
+  const int gs = min(G, p.n_streams - g0);
+  const int r = item - g0 * p.splits;
+  split = r / gs;
+  stream = g0 + (r - split * gs);
 }
 
 }  // namespace
@@ -215,7 +231,8 @@ __device__ __forceinline__ void signal_pushed(const AttnParams& p, int total) {
 
 constexpr int kRedBatch = 16;  // splits whose loads are in flight together
 template <int DP>
-__device__ void reduce_stream(const AttnParams& p, int stream, int rows, int warp, int nwarps) {
+__device__ void reduce_stream(const AttnParams& p, int stream, int rows, int warp, int nwarps, int q_begin = 0,
+                              int q_end = 1 << 30) {
   constexpr int PER = DP / 32;
   int t = stream;
   const int qc = t % p.q_chunks;
@@ -237,7 +254,8 @@ __device__ void reduce_stream(const AttnParams& p, int stream, int rows, int war
     return all_full ||
            (static_cast<long long>(s + 1) * pages) / p.splits > (static_cast<long long>(s) * pages) / p.splits;
   };
-  for (int q = single ? 0 : warp; q < rows; q += single ? 1 : nwarps) {
+  if (q_end > rows) q_end = rows;
+  for (int q = q_begin + (single ? 0 : warp); q < q_end; q += single ? 1 : nwarps) {
     float M = -INFINITY;
     if (!single) {
       for (int s = lane; s < p.splits; s += 32)
@@ -289,10 +307,19 @@ __device__ void reduce_stream(const AttnParams& p, int stream, int rows, int war
 }
 
 // Consumer warps after an item's partial is stored: count the stream's
-// completed splits; the CTA completing the last one reduces (and pushes) it.
+// completed splits; the CTA completing the last one reduces (and pushes) it
+// (fused == 1), or -- fused == 2 -- only the count is published and the
+// co-resident stream reducer (attn_stream_reduce_kernel) does the rest.
 template <int DP, int NWC>
 __device__ __forceinline__ void fused_stream_done(const AttnParams& p, int stream, int rows, int ntok) {
   __shared__ int s_last;
+  if (p.fused == 2) {
+    if (threadIdx.x == 0) {
+      __threadfence();  // the item's partial (all consumer threads, ordered by the barrier) before the count
+      atomicAdd(p.stream_done + stream, 1);
+    }
+    return;
+  }
   if (threadIdx.x == 0) {
     __threadfence();  // the item's partial (all consumer threads, ordered by the barrier) before the count
     const int pages = (ntok + 15) >> 4;
@@ -366,13 +393,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           // decode the item once: (stream, split) (attn_item), then
           // stream -> (slot, request, kv head, query chunk)
           int split;
-          if (p.stream_major) {
-            stream = item / p.splits;
-            split = item - stream * p.splits;
-          } else {
-            split = item / p.n_streams;
-            stream = item - split * p.n_streams;
-          }
+          attn_item_decode(p, item, stream, split);
           int t = stream;
           const int qc = t % p.q_chunks;
           t /= p.q_chunks;
@@ -390,7 +411,7 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           const int g_rows = p.group - qc * QR;
           rows = g_rows < QR ? g_rows : QR;
           if (pg1 <= pg0) {  // empty split: nothing to emit
-            if (p.fused && pages == 0 && split == 0) {
+            if (p.fused == 1 && pages == 0 && split == 0) {
               // no tokens on this rank for the stream: its fragment is the identity (0, -inf)
               // (attention.hpp:69-70); the producer thread writes / pushes it
               if (!waited) {
@@ -1014,6 +1035,73 @@ __global__ void __launch_bounds__(256) attn_split_reduce_small_kernel(const Attn
   if (p.push) {
     __syncthreads();
     if (threadIdx.x == 0) signal_pushed(p, gridDim.x);
+  }
+}
+
+// HOP-B without stalling the KV stream (AttnParams::fused == 2, overlap.hpp:37-69
+// at stream granularity): the attention kernel only publishes each stream's
+// finished-split count; this kernel, launched right behind it with
+// programmatic dependent launch and small enough (128 threads, no shared
+// memory) to sit next to the attention CTAs on their SMs, reduces and pushes
+// every stream as soon as its last split has landed -- request b's slices
+// travel while the requests after it are still streaming KV, and no attention
+// CTA ever pauses its stream for a reduce. Streams in request order (the
+// attention's work order is stream-major under HOP-B).
+__device__ __forceinline__ int ld_acquire_gpu(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+constexpr int kSrRowsPerCta = 4;  // one warp per query row
+template <int DP>
+__global__ void __launch_bounds__(128) attn_stream_reduce_kernel(const AttnParams p) {
+  const int warp = threadIdx.x >> 5;
+  const int chunks = (p.qrows + kSrRowsPerCta - 1) / kSrRowsPerCta;
+  // CTA = (stream, chunk of 4 query rows), dispatched in stream (= completion) order
+  {
+    const int stream = blockIdx.x / chunks, q0 = (blockIdx.x % chunks) * kSrRowsPerCta;
+    int t = stream;
+    const int qc = t % p.q_chunks;
+    t /= p.q_chunks;
+    t /= p.kvh_per_slot;
+    const int b = t % p.stream_batch + p.b_begin;
+    const int rank = (t / p.stream_batch + p.slot_base) % p.kvp;
+    const int pages = (static_cast<int>(rr_count(p.total[b], rank, p.chunk, p.kvp)) + 15) >> 4;
+    const int need = pages < p.splits ? pages : p.splits;  // non-empty splits of the stream
+    const int g_rows = p.group - qc * p.qrows;
+    const int rows = g_rows < p.qrows ? g_rows : p.qrows;
+    if (threadIdx.x == 0) {
+      while (ld_acquire_gpu(p.stream_done + stream) < need) __nanosleep(64);
+    }
+    __syncthreads();
+    if (need == 0) {
+      if (threadIdx.x == 0) reduce_stream<DP>(p, stream, rows, 0, 0, q0, q0 + kSrRowsPerCta);  // identity (0, -inf)
+    } else {
+      reduce_stream<DP>(p, stream, rows, warp, 4, q0, q0 + kSrRowsPerCta);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      // the stream's counter is reset by its last chunk (the others have read it)
+      if (atomicAdd(p.stream_done + p.n_streams + stream, 1) == chunks - 1) {
+        p.stream_done[stream] = 0;  // for the next launch / graph replay
+        p.stream_done[p.n_streams + stream] = 0;
+      }
+      if (p.push) signal_pushed(p, gridDim.x);
+    }
+  }
+  // completion of this grid implies the attention grid's (the next kernel's
+  // griddepcontrol.wait sees only this one)
+  griddep_wait();
+  griddep_launch_dependents();
+}
+
+cudaError_t launch_attn_stream_reduce(const AttnParams& p, cudaStream_t stream) {
+  const int grid = p.n_streams * ((p.qrows + kSrRowsPerCta - 1) / kSrRowsPerCta);
+  switch (p.dp) {
+    case 32: return launch_k(attn_stream_reduce_kernel<32>, dim3(grid), dim3(128), 0, stream, p);
+    case 64: return launch_k(attn_stream_reduce_kernel<64>, dim3(grid), dim3(128), 0, stream, p);
+    case 128: return launch_k(attn_stream_reduce_kernel<128>, dim3(grid), dim3(128), 0, stream, p);
+    default: return cudaErrorInvalidValue;
   }
 }
 

@@ -120,14 +120,9 @@ struct TcSeq {
         return;
       }
       const int iti = static_cast<int>(it);
-      int stream, split;
-      if (p->stream_major) {
-        stream = iti / p->splits;
-        split = iti - stream * p->splits;
-      } else {
-        split = iti / p->n_streams;
-        stream = iti - split * p->n_streams;
-      }
+      // split-major (the tcgen05 kernel never runs the HOP-B order: attn_tc_supported)
+      const int split = iti / p->n_streams;
+      const int stream = iti - split * p->n_streams;
       int t = stream;
       const int qc = t % p->q_chunks;
       t /= p->q_chunks;

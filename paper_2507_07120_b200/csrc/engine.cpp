@@ -408,8 +408,11 @@ void Engine::alloc() {
   }
   attn_grid_ = std::min(mla_ ? num_sms_ / 2 : num_sms_, n_items_);  // MLA: CTA pairs
   if (std::getenv("HX_FUSED_REDUCE") && std::getenv("HX_FUSED_REDUCE")[0] == '0') fused_ = false;
+  hopb_inkernel_ = std::getenv("HX_HOPB_INKERNEL") && std::getenv("HX_HOPB_INKERNEL")[0] == '1';
+  if (std::getenv("HX_HOPB_GROUP")) hopb_group_ = std::max(1, std::atoi(std::getenv("HX_HOPB_GROUP")));
   if (std::getenv("HX_A2A_NCCL") && std::getenv("HX_A2A_NCCL")[0] == '1') nccl_a2a_ = true;
-  d_stream_done_ = dalloc<int>(static_cast<size_t>(std::max(n_streams_, 1)), "stream done counters");
+  // [n_streams] finished splits, [n_streams] finished reducer chunks (HOP-B stream reducer)
+  d_stream_done_ = dalloc<int>(2 * static_cast<size_t>(std::max(n_streams_, 1)), "stream done counters");
   d_pushed_ = dalloc<int>(1, "pushed counter");
   if (dist_mode_ != HX_POOL_LOCAL) {
     d_flags_ = dalloc<unsigned>(static_cast<size_t>(kvp_), "exchange flags");
@@ -620,7 +623,7 @@ int64_t Engine::launches_per_step() const {
   const int64_t mla_k = mla_ ? 2 : 0;                      // W_UK absorption, W_UV
   if (dist_mode_ == HX_POOL_LOCAL)
     return head + L_ * (2 + 1 + sr + (one_src_merge_ ? 0 : 1) + mla_k + 2 + ffn_k);
-  const int64_t attn = device_exchange() ? (hopb_ && fused_ ? 2 : 3)  // attention, [reduce + push], flag wait
+  const int64_t attn = device_exchange() ? (hopb_ && fused_ && hopb_inkernel_ ? 2 : 3)  // attention, reduce + push, flag wait
                                          : (hopb_ ? B_ : 1) * (2 + sr);  // [per request] attention, sr, pack
   return head + L_ * (2 + attn + 1 + mla_k + 2 + 1 + ffn_k + 1);  // + merge, O x2, residual, FFN, residual
 }
@@ -1260,10 +1263,16 @@ AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) {
   a.hd = static_cast<int>(D_);
   a.pushed = d_pushed_;
   if (fused_ && hopb_ && device_exchange()) {
-    // HOP-B: request-ordered work, each stream reduced (and pushed) in-kernel as
-    // it completes, overlapping the attention of the streams after it
-    a.fused = 1;
-    a.stream_major = 1;
+    // HOP-B: request-ordered work, each stream reduced (and pushed) as it
+    // completes, overlapping the attention of the streams after it -- by the
+    // co-resident stream reducer (2, the attention CTAs never pause their KV
+    // stream) or, with HX_HOPB_INKERNEL=1, by the attention CTA that finished
+    // the stream's last split (1)
+    a.fused = hopb_inkernel_ ? 1 : 2;
+    // work in groups of hopb_group_ requests (split-major inside a group): the
+    // groups' exchanges overlap the attention of the groups after them, while
+    // each group keeps the batched launch's split-major KV order
+    a.stream_major = hopb_inkernel_ ? 1 : std::max(1, a.n_streams / b_count * hopb_group_);
     a.stream_done = d_stream_done_;
     a.frag_o = d_frag_o_;
     a.frag_lse = d_frag_lse_;
@@ -1294,6 +1303,7 @@ void Engine::launch_attention_kernels(const AttnParams& a) {
       cuda_check(launch_attn_decode(a, std::min(attn_grid_, a.n_items), stream_), "attention");
     mark(2);
     if (!a.fused) cuda_check(launch_attn_split_reduce(a, d_frag_o_, d_frag_lse_, stream_), "split reduce");
+    if (a.fused == 2) cuda_check(launch_attn_stream_reduce(a, stream_), "hop-b stream reduce");
   }
 }
 

@@ -144,7 +144,9 @@ class Engine {
   int ips_ = 8, min_pages_ = 32;  // split planner knobs (HX_ATTN_SPLIT)
   bool split_env_ = false;
   int plan_splits(int streams, int pages) const;
-  bool attn_tc_ = false;  // quantised pages on the tcgen05 kernel (attention_tc.cu)
+  bool attn_tc_ = false;
+  bool hopb_inkernel_ = false;
+  int hopb_group_ = 1;  // HOP-B: requests per work group (HX_HOPB_GROUP; 1 = stream-major)  // HOP-B reduce inside the attention kernel (HX_HOPB_INKERNEL=1) vs the stream reducer  // quantised pages on the tcgen05 kernel (attention_tc.cu)
   int live_splits(int64_t layer, bool per_request) const;
 
   // ---- device state

@@ -88,9 +88,11 @@ struct AttnParams {
   int kv4;                 // GQA: FP4 (e2m1 blocks of 32, power-of-two scales) pages, f16 MMAs
   // Fused split reduce (GQA): the CTA that completes a stream's last non-empty
   // split merges the stream's partials (split order) into frag_o / frag_lse
-  // [slot_local][b][q][DP] (natural-log lse) -- no split-reduce launch.
+  // [slot_local][b][q][DP] (natural-log lse) -- no split-reduce launch (1); or
+  // the attention kernel only counts the stream's finished splits and the
+  // co-resident stream reducer merges and pushes (2).
   int fused;
-  int stream_major;        // work order (attention.cu attn_item): 1 = the splits of a stream adjacent
+  int stream_major;        // work order (attention.cu attn_item): 0 split-major, G > 0 groups of G streams
   int* stream_done;        // [n_streams] completed splits per stream (self-resetting)
   float* frag_o;
   float* frag_lse;
@@ -107,6 +109,9 @@ struct AttnParams {
   int xchunk, xslice, xrank;
 };
 cudaError_t launch_attn_decode(const AttnParams& p, int grid, cudaStream_t stream);
+// HOP-B stream reducer (fused == 2): reduce + push each stream as its splits land,
+// next to the running attention kernel (attention.cu).
+cudaError_t launch_attn_stream_reduce(const AttnParams& p, cudaStream_t stream);
 // Quantised (FP8 / FP4) pages at DP = 128, <= 16 query rows, no fused reduce:
 // the tcgen05 kernel (attention_tc.cu). grid = CTAs; items are statically
 // assigned (item = CTA + n * grid).

@@ -36,7 +36,7 @@ def test_loopback_pool_matches_oracle(tpa, kvp, hopb):
     # merge, O x2, residual, gate/up x2, down x2, residual
     info = engines[0].info()
     assert info["exchange"] == (3 if hopb else 2)
-    assert info["kernels_per_step"] == 4 + L * (11 + (2 if hopb else 3))
+    assert info["kernels_per_step"] == 4 + L * (11 + 3)  # attention, split reduce or HOP-B stream reducer, flag wait
     for e in engines:
         e.init_weights(4321, qkv="mt19937")
     for l in range(L):
