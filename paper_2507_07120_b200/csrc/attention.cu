@@ -1071,7 +1071,7 @@ __global__ void __launch_bounds__(128) attn_stream_reduce_kernel(const AttnParam
     const int g_rows = p.group - qc * p.qrows;
     const int rows = g_rows < p.qrows ? g_rows : p.qrows;
     if (threadIdx.x == 0) {
-      while (ld_acquire_gpu(p.stream_done + stream) < need) __nanosleep(64);
+      while (ld_acquire_gpu(p.stream_done + stream) < need) __nanosleep(512);  // light polling: L2 stays with the KV stream
     }
     __syncthreads();
     if (need == 0) {

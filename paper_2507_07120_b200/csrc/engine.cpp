@@ -409,6 +409,7 @@ void Engine::alloc() {
   attn_grid_ = std::min(mla_ ? num_sms_ / 2 : num_sms_, n_items_);  // MLA: CTA pairs
   if (std::getenv("HX_FUSED_REDUCE") && std::getenv("HX_FUSED_REDUCE")[0] == '0') fused_ = false;
   hopb_inkernel_ = std::getenv("HX_HOPB_INKERNEL") && std::getenv("HX_HOPB_INKERNEL")[0] == '1';
+  local_stream_reduce_ = std::getenv("HX_LOCAL_STREAM_REDUCE") && std::getenv("HX_LOCAL_STREAM_REDUCE")[0] == '1';
   if (std::getenv("HX_HOPB_GROUP")) hopb_group_ = std::max(1, std::atoi(std::getenv("HX_HOPB_GROUP")));
   if (std::getenv("HX_A2A_NCCL") && std::getenv("HX_A2A_NCCL")[0] == '1') nccl_a2a_ = true;
   // [n_streams] finished splits, [n_streams] finished reducer chunks (HOP-B stream reducer)
@@ -1278,6 +1279,16 @@ AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) {
     a.frag_lse = d_frag_lse_;
     a.pushed = d_pushed_;
     a.hd = static_cast<int>(D_);
+  }
+  if (local_stream_reduce_ && dist_mode_ == HX_POOL_LOCAL && !mla_ && !(attn_tc_ && attn_tc_supported(a))) {
+    // local pools: the same co-resident stream reducer replaces the split-reduce
+    // kernel -- streams are merged while the attention of later streams runs,
+    // instead of one reduce launch after the whole attention kernel
+    a.fused = 2;
+    a.stream_major = std::max(1, a.n_streams / b_count * hopb_group_);
+    a.stream_done = d_stream_done_;
+    a.frag_o = d_frag_o_;
+    a.frag_lse = d_frag_lse_;
   }
   if (mla_) {
     a.qimg = d_qimg_;

@@ -146,6 +146,7 @@ class Engine {
   int plan_splits(int streams, int pages) const;
   bool attn_tc_ = false;
   bool hopb_inkernel_ = false;
+  bool local_stream_reduce_ = false;  // local pools: stream reducer instead of the split-reduce kernel (HX_LOCAL_STREAM_REDUCE=1; measured slower: DESIGN)
   int hopb_group_ = 1;  // HOP-B: requests per work group (HX_HOPB_GROUP; 1 = stream-major)  // HOP-B reduce inside the attention kernel (HX_HOPB_INKERNEL=1) vs the stream reducer  // quantised pages on the tcgen05 kernel (attention_tc.cu)
   int live_splits(int64_t layer, bool per_request) const;
 
