@@ -313,11 +313,12 @@ __device__ void reduce_stream(const AttnParams& p, int stream, int rows, int war
 template <int DP, int NWC>
 __device__ __forceinline__ void fused_stream_done(const AttnParams& p, int stream, int rows, int ntok) {
   __shared__ int s_last;
+  if (p.fused == 3) return;  // timing experiment only (no count; the reducer does not wait)
   if (p.fused == 2) {
-    if (threadIdx.x == 0) {
-      __threadfence();  // the item's partial (all consumer threads, ordered by the barrier) before the count
-      atomicAdd(p.stream_done + stream, 1);
-    }
+    // the item's partial (every consumer thread's stores, ordered before this by
+    // the named barrier) released with the count: a cumulative gpu-scope release
+    // instead of a full fence + atomic
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.stream_done + stream) : "memory");
     return;
   }
   if (threadIdx.x == 0) {
@@ -1056,6 +1057,9 @@ constexpr int kSrRowsPerCta = 4;  // one warp per query row
 template <int DP>
 __global__ void __launch_bounds__(128) attn_stream_reduce_kernel(const AttnParams p) {
   const int warp = threadIdx.x >> 5;
+#ifdef HX_SR_SERIAL
+  griddep_wait();
+#endif
   const int chunks = (p.qrows + kSrRowsPerCta - 1) / kSrRowsPerCta;
   // CTA = (stream, chunk of 4 query rows), dispatched in stream (= completion) order
   {
@@ -1067,7 +1071,7 @@ __global__ void __launch_bounds__(128) attn_stream_reduce_kernel(const AttnParam
     const int b = t % p.stream_batch + p.b_begin;
     const int rank = (t / p.stream_batch + p.slot_base) % p.kvp;
     const int pages = (static_cast<int>(rr_count(p.total[b], rank, p.chunk, p.kvp)) + 15) >> 4;
-    const int need = pages < p.splits ? pages : p.splits;  // non-empty splits of the stream
+    const int need = p.fused == 3 ? 0 : (pages < p.splits ? pages : p.splits);  // non-empty splits of the stream
     const int g_rows = p.group - qc * p.qrows;
     const int rows = g_rows < p.qrows ? g_rows : p.qrows;
     if (threadIdx.x == 0) {

@@ -1269,7 +1269,7 @@ AttnParams Engine::attn_params(int64_t layer, int b_begin, int b_count) {
     // co-resident stream reducer (2, the attention CTAs never pause their KV
     // stream) or, with HX_HOPB_INKERNEL=1, by the attention CTA that finished
     // the stream's last split (1)
-    a.fused = hopb_inkernel_ ? 1 : 2;
+    a.fused = hopb_inkernel_ ? 1 : (std::getenv("HX_HOPB_DEBUG_NOCOUNT") ? 3 : 2);
     // work in groups of hopb_group_ requests (split-major inside a group): the
     // groups' exchanges overlap the attention of the groups after them, while
     // each group keeps the batched launch's split-major KV order
@@ -1314,7 +1314,7 @@ void Engine::launch_attention_kernels(const AttnParams& a) {
       cuda_check(launch_attn_decode(a, std::min(attn_grid_, a.n_items), stream_), "attention");
     mark(2);
     if (!a.fused) cuda_check(launch_attn_split_reduce(a, d_frag_o_, d_frag_lse_, stream_), "split reduce");
-    if (a.fused == 2) cuda_check(launch_attn_stream_reduce(a, stream_), "hop-b stream reduce");
+    if (a.fused >= 2) cuda_check(launch_attn_stream_reduce(a, stream_), "hop-b stream reduce");
   }
 }
 
