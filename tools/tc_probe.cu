@@ -124,6 +124,92 @@ int run(int test) {
   return err > 1e-3;
 }
 
+// test 3: kind::f8f6f4, A e4m3 K-major [128 x 128] and B e4m3 K-major [N x 128]
+// from shared memory (core matrix = 8 rows x 16 bytes), 4 MMAs of K = 32
+__host__ __device__ float a8(int m, int k) { return (((m * 5 + k * 3) % 7) - 3) * 0.5f; }
+__host__ __device__ float b8(int n, int k) { return (((n * 3 + k) % 5) - 2) * 0.25f; }
+__device__ uint8_t to_e4m3(float x) {
+  uint16_t r;
+  asm("{\n.reg .b16 t;\ncvt.rn.satfinite.e4m3x2.f32 t, %1, %1;\nmov.b16 %0, t;\n}" : "=h"(r) : "f"(x));
+  return static_cast<uint8_t>(r & 0xFF);
+}
+template <int N>
+__global__ void probe8(float* out) {
+  __shared__ __align__(1024) uint8_t as[128 * 128];
+  __shared__ __align__(1024) uint8_t bs[N * 128];
+  __shared__ uint32_t tbase;
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) tmem_alloc(&tbase, 256);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  // K-major 8-bit: [k/16][row/8][row%8][k%16]
+  for (int i = tid; i < 128 * 128; i += 128) {
+    const int m = i / 128, k = i % 128;
+    as[(((k >> 4) * 16 + (m >> 3)) * 8 + (m & 7)) * 16 + (k & 15)] = to_e4m3(a8(m, k));
+  }
+  for (int i = tid; i < N * 128; i += 128) {
+    const int n = i / 128, k = i % 128;
+    bs[(((k >> 4) * (N / 8) + (n >> 3)) * 8 + (n & 7)) * 16 + (k & 15)] = to_e4m3(b8(n, k));
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tbase;
+  // idesc kind::f8f6f4: D f32 (bit 4), A/B format E4M3 = 0, K-major both, N>>3 at 17, M>>4 at 24
+  const uint32_t id = (1u << 4) | (static_cast<uint32_t>(N >> 3) << 17) | (128u >> 4 << 24);
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int ks = 0; ks < 4; ++ks) {  // K = 32 per MMA: two 16-byte core matrices along K
+        const uint64_t a = umma_desc(smem_u32(as) + ks * 2 * 16 * 128, 16 * 128, 128);
+        const uint64_t b = umma_desc(smem_u32(bs) + ks * 2 * (N / 8) * 128, (N / 8) * 128, 128);
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(tm + 128),
+            "l"(a), "l"(b), "r"(id), "r"(ks > 0 ? 1u : 0u)
+            : "memory");
+      }
+      umma_commit(&bar);
+    }
+    __syncwarp();
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  for (int n0 = 0; n0 < N; n0 += 32) {
+    float v[32];
+    tmem_ld32(tm + (static_cast<uint32_t>(warp * 32) << 16) + 128 + n0, v);
+    for (int n = 0; n < 32; ++n) out[tid * N + n0 + n] = v[n];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tm, 256);
+}
+template <int N>
+int run8() {
+  float* d;
+  cudaMalloc(&d, 128 * N * 4);
+  probe8<N><<<1, 128>>>(d);
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    printf("f8 test N=%d: CUDA error\n", N);
+    return 1;
+  }
+  float h[128 * N];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double err = 0;
+  for (int m = 0; m < 128; ++m)
+    for (int n = 0; n < N; ++n) {
+      double r = 0;
+      for (int k = 0; k < 128; ++k) r += static_cast<double>(a8(m, k)) * b8(n, k);
+      err = fmax(err, fabs(r - h[m * N + n]));
+    }
+  printf("f8f6f4 e4m3 K-major N=%d: max |err| = %g (D[0][0..1] = %g %g)\n", N, err, h[0], h[1]);
+  cudaFree(d);
+  return err > 1e-3;
+}
+
 int main() {
   int bad = 0;
   bad += run<16>(2);
@@ -132,6 +218,8 @@ int main() {
   bad += run<32>(0);
   bad += run<16>(1);
   bad += run<32>(1);
+  bad += run8<32>();
+  bad += run8<64>();
   printf(bad ? "PROBE FAILED\n" : "PROBE OK\n");
   return bad;
 }
