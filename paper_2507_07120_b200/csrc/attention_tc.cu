@@ -1,5 +1,7 @@
-// K1-TC: GQA flash-decode partial attention over QUANTISED KV pages (FP8 e4m3,
-// FP4 e2m1 blocks) on the 5th-generation tensor cores (tcgen05 + TMEM).
+// K1-TC: GQA flash-decode partial attention over FP8 (e4m3) KV pages on the
+// 5th-generation tensor cores (tcgen05 + TMEM). Opt-in (HX_ATTN_TC=1): the
+// engine then stores its FP8 pages in the tensor-core layout
+// (kv_layout.cuh kv8tc_offset), which only this kernel reads.
 //
 // Same contract as attn_decode_kernel (attention.cu): per work item (stream =
 // (rank slot, request, KV head), split = page range) the locally normalised
@@ -7,38 +9,38 @@
 // HeadFragment of partial_head_attention (reference attention.hpp:56-78,
 // :375-396) -- so the split reduce / merge / exchange path is unchanged.
 //
-// Why a second kernel: the legacy-HMMA kernel widens every KV element into
-// mma.sync operands on the consumer warps, and with 16 query rows (405B-like
-// G = 16) or 4-bit pages the widen + MMA issue chain, not HBM, bounds it
-// (FP8 G16 66%, FP4 33-47% of the copy bandwidth; K1-FP4).
-// Here the tensor core does all the MACs and each KV byte is widened once:
+// Why: the legacy-HMMA kernel widens every e4m3 element into mma.sync operands
+// on the consumer warps, and with 16 query rows (405B-like G = 16) that widen
+// + MMA chain, not HBM, bounds it (66% of the copy bandwidth). Here
 //
 //   tile = 128 tokens (8 pages), transposed formulation (token = TMEM lane):
-//   S^T [128 tok x NC] = K [128 tok x 128 dim] . Q^T        (A = K f16 in TMEM)
-//   O^T [128 dim x NC] += V^T [128 dim x 128 tok] . P^T     (A = V^T f16 in TMEM)
-//   NC = 2 * NQ columns: (term, query) -- q and P each split into f16 hi + lo
-//   (22 significant bits), so as in the legacy kernel the only rounding is the
-//   KV storage itself (e4m3 / e2m1 x 2^e values are exact in f16).
+//   S^T [128 tok x NS] = K [128 tok x 128 dim] . Q8^T   kind::f8f6f4: K is the
+//       A operand STRAIGHT FROM THE PAGES (e4m3, K-major core matrices), Q8 the
+//       query split into T = 4 e4m3 terms, q ~ s0 * sum_j 16^-j * c_j (s0 a
+//       power of two per query), so the only rounding is K's storage (~2^-16
+//       relative in q; S = s0 * sum_j 16^-j S_j in the softmax)
+//   O^T [128 dim x NC] += V^T [128 dim x 128 tok] . P^T  kind::f16: V widened to
+//       f16 into TMEM by converter warps (one cvt per 2 elements), P split into
+//       f16 hi + lo (22 bits); NC = 2 * NQ
 //
-// One CTA per SM, two ITEM SLOTS whose tiles alternate through the shared converters:
-//   warps 0-3 / 4-7   softmax of slot 0 / 1 (thread = token lane of S^T, = dim
-//                     lane of O^T): lazy online softmax (rescale only when a
-//                     query's max grows by > 8 in log2 units, found with one
-//                     barrier.red.or), P^T hi/lo into shared memory, the rare
-//                     O^T rescale in TMEM, the item's partial at its end
-//   warps 8-11        K converters: thread = token t; K's 128 dims (FP8 8-byte /
-//                     FP4 4-byte fragment chunks of the page) widen to f16 and go
-//                     to TMEM lane t (tcgen05.st) (+ the item's query image)
-//   warps 12-15       V converters: thread = dim d; d's 16 tokens per page -> lane d
-//   warp 16           producer: cp.async.bulk of each tile's 8 pages (+ the
-//                     item's query rows) into a shared-memory ring
-//   warp 17           MMA issue (elected lane of the converged warp): S(i+1), PV(i)
-// (18 warps: the sub-partitions holding 5 cap registers at 96 per thread)
-// MMAs are issued from converged warps by one elected lane (descriptors stay
-// warp-uniform: ~21 cycles per tcgen05.mma, tools/tc_issue_probe.cu).
-// Work is statically assigned (item = unit + n * units, unit = 2 CTA + slot):
-// every role walks the same deterministic tile sequence, so only mbarrier
-// phases pass between roles.
+// Roles (448 threads = 14 warps: <= 4 per SM sub-partition, 128 registers):
+//   warps 0-3 / 4-7  softmax of item slot 0 / 1 (thread = token lane of S^T,
+//                    = dim lane of O^T): lazy online softmax (rescale only when
+//                    a query's max grows by > 8 in log2 units, found with one
+//                    barrier.red.or), P^T hi/lo into shared memory, the rare O^T
+//                    rescale in TMEM, the item's partial at its end
+//   warps 8-11       V converters (thread = dim d: d's 8-token words of the
+//                    page -> f16 pairs -> TMEM lane d) + the item's e4m3 query
+//                    image
+//   warp 12          producer: cp.async.bulk of each tile's 8 pages (+ the
+//                    item's query rows) into a shared-memory ring
+//   warp 13          MMA issue (one elected lane of the converged warp): S(i+1)
+//                    before PV(i)
+// Two item slots per CTA: their tiles alternate through the shared converters
+// and tensor core, so one slot's softmax overlaps the other's MMAs. Work is
+// statically assigned (item = unit + n * units, unit = 2 CTA + slot): every
+// role walks the same deterministic tile sequence; only mbarrier phases pass
+// between roles.
 #include <cstdio>
 
 #include "common.cuh"
@@ -51,45 +53,59 @@ namespace hx {
 namespace {
 
 constexpr int kTcDP = 128;  // head dim (padded) this kernel serves
-constexpr int kTcThreads = 576;
-constexpr int kWarpKConv = 8, kWarpVConv = 12, kWarpProd = 16, kWarpMma = 17;
+constexpr int kTcThreads = 448;
+constexpr int kWarpVConv = 8, kWarpProd = 12, kWarpMma = 13;
+constexpr int kQTerms = 4;  // e4m3 terms of the query
+// Lazy online softmax: the reference max of a query moves only when a logit
+// exceeds it by more than this (log2 units); P <= 2^14 keeps its f16 hi term
+// finite. A group-wide max update costs a barrier + shared-memory exchange and
+// an O^T rescale in TMEM, so the threshold is set as high as f16 allows (the
+// legacy kernel's per-warp update uses 8).
+constexpr float kGrow = 14.f;
 
-template <int NQ, int KVF, int NST>
+template <int NQ, int NST>
 struct TcCfg {
-  static constexpr int NC = 2 * NQ;                                   // MMA N
-  static constexpr int NV = NC == 32 ? 3 : 4;                         // V buffers in TMEM
-  static constexpr uint32_t PAGE = KVF == 2 ? 35u * kTcDP / 2u : 32u * kTcDP;
+  static constexpr int NC = 2 * NQ;                                   // PV MMA N: P hi/lo x query
+  static constexpr int NS = kQTerms * NQ;                             // S MMA N: term x query
+  // TMEM budget (512 columns): NQ = 16 keeps one S buffer per slot to afford 5 V
+  // buffers (the converters run further ahead of the PV MMAs); NQ = 8 double-buffers S
+  static constexpr int SB = NS == 64 ? 1 : 2;                         // S buffers per slot
+  static constexpr int NV = NS == 64 ? 5 : 4;                         // V buffers in TMEM
+  static constexpr uint32_t PAGE = 32u * kTcDP;                       // FP8 page, tensor-core layout
   static constexpr uint32_t STAGE = 8 * PAGE;                          // 8 pages = 128 tokens
   static constexpr uint32_t QRAW = NQ * kTcDP * 4;                    // fp32 query rows
-  static constexpr uint32_t QIMG = NC * kTcDP * 2;                    // Q^T f16, K-major core matrices
+  static constexpr uint32_t QIMG = NS * kTcDP;                        // Q8^T e4m3, K-major core matrices
   static constexpr uint32_t PBUF = 128 * NC * 2;                      // P^T f16, MN-major core matrices
-  static constexpr uint32_t OFF_QIMG = NST * STAGE;                   // (STAGE % 128 == 0)
+  static constexpr uint32_t OFF_QIMG = NST * STAGE;
   static constexpr uint32_t OFF_PBUF = OFF_QIMG + 2 * QIMG;           // [slot][2]
   static constexpr uint32_t OFF_QRAW = OFF_PBUF + 4 * PBUF;           // [slot]
-  static constexpr uint32_t OFF_RED = OFF_QRAW + 2 * QRAW;            // float [slot][4 warps][NQ]
+  static constexpr uint32_t OFF_QS0 = OFF_QRAW + 2 * QRAW;            // float [slot][NQ]: q term-0 scales
+  static constexpr uint32_t OFF_RED = OFF_QS0 + 2 * NQ * 4;           // float [slot][4 warps][NQ]
   static constexpr uint32_t OFF_BAR = OFF_RED + 2 * 4 * NQ * 4;
-  static constexpr int NBAR = 2 * NST + 2 * NV + 28;
+  static constexpr int NBAR = 2 * NST + 2 * NV + 30;
   static constexpr uint32_t SMEM = OFF_BAR + NBAR * 8 + 16;
-  // TMEM columns: K x2 | V x NV | S [slot][2] | O [slot]
-  static constexpr uint32_t COL_K = 0, COL_V = 128, COL_S = 128 + 64 * NV, COL_O = COL_S + 4 * NC;
+  // TMEM columns: V x NV | S [slot][2] | O [slot]
+  static constexpr uint32_t COL_V = 0, COL_S = 64 * NV, COL_O = COL_S + 2 * SB * NS;
   static_assert(COL_O + 2 * NC <= 512, "TMEM columns");
-  // instruction descriptors (kind::f16, f16 x f16 -> f32): S^T (B = Q^T K-major), O^T (B = P^T MN-major)
-  static constexpr uint32_t IDESC_S = (1u << 4) | (static_cast<uint32_t>(NC >> 3) << 17) | (128u >> 4 << 24);
-  static constexpr uint32_t IDESC_O = IDESC_S | (1u << 16);
+  // S^T: kind::f8f6f4, e4m3 x e4m3 -> f32, both K-major
+  static constexpr uint32_t IDESC_S = (1u << 4) | (static_cast<uint32_t>(NS >> 3) << 17) | (128u >> 4 << 24);
+  // O^T: kind::f16, f16 x f16 -> f32, B (P^T) MN-major
+  static constexpr uint32_t IDESC_O =
+      (1u << 4) | (1u << 16) | (static_cast<uint32_t>(NC >> 3) << 17) | (128u >> 4 << 24);
 };
 
 // barrier indices
 template <int NST, int NV>
 struct TcBars {
   static constexpr int RAW_FULL = 0, RAW_EMPTY = NST;
-  static constexpr int KFULL = 2 * NST, KFREE = KFULL + 2, VFULL = KFREE + 2, VFREE = VFULL + NV;
+  static constexpr int VFULL = 2 * NST, VFREE = VFULL + NV;
   static constexpr int SFULL = VFREE + NV, SFREE = SFULL + 4;  // [slot][buffer]
   static constexpr int PFULL = SFREE + 4, ODONE = PFULL + 4;   // [slot][P buffer]
-  static constexpr int QFREE = ODONE + 4, QRAWFREE = QFREE + 2;  // [slot]
+  static constexpr int QFULL = ODONE + 4, QFREE = QFULL + 2, QRAWFREE = QFREE + 2;  // [slot]
 };
 
 struct TcTile {
-  int slot, item, np, ntok, rows, first, last;
+  int slot, item, stream, np, ntok, rows, first, last;
   int tok0;           // first token (within the stream's shard) of the tile
   const uint8_t* kv;  // the tile's first page
   const float* q;     // the item's query rows
@@ -101,7 +117,7 @@ struct TcTile {
 // the L1 left for a local-memory stack is tiny, and a stack round trip to L2
 // per tile costs ~0.3 us).
 struct TcSlot {
-  int kord, item, tile, ntiles, pg0, pg1, ntok, rows;
+  int kord, item, stream, tile, ntiles, pg0, pg1, ntok, rows;
   const uint8_t* kvs;
   const float* q;
   bool act;
@@ -139,6 +155,7 @@ struct TcSeq {
       const int e = static_cast<int>((static_cast<long long>(split + 1) * pages) / p->splits);
       if (e <= a) continue;  // empty split: nothing to emit (the split reduce skips it)
       S.item = iti;
+      S.stream = stream;
       S.tile = 0;
       S.ntiles = (e - a + 7) >> 3;
       S.pg0 = a;
@@ -169,6 +186,7 @@ struct TcSeq {
     last = g;
     t.slot = g;
     t.item = S.item;
+    t.stream = S.stream;
     const int a = S.pg0 + 8 * S.tile;
     t.np = min(8, S.pg1 - a);
     t.ntok = S.ntok;
@@ -236,22 +254,6 @@ HX_DEV void tmem_stn(uint32_t taddr, float (&v)[N]) {
   }
 }
 
-HX_DEV uint32_t lds32_(uint32_t a) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
-  return v;
-}
-HX_DEV void e2m1x4_to_f16x2x2(uint32_t two_bytes, uint32_t& lo, uint32_t& hi) {
-  asm("{\n .reg .b8 b0, b1, b2, b3;\n mov.b32 {b0, b1, b2, b3}, %2;\n"
-      " cvt.rn.f16x2.e2m1x2 %0, b0;\n cvt.rn.f16x2.e2m1x2 %1, b1;\n}"
-      : "=r"(lo), "=r"(hi)
-      : "r"(two_bytes));
-}
-HX_DEV uint32_t hmul2_(uint32_t a, uint32_t b) {
-  uint32_t d;
-  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
-  return d;
-}
 HX_DEV uint32_t pack_f16x2(float lo, float hi) {
   uint32_t d;
   asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
@@ -263,10 +265,25 @@ HX_DEV float2 unpack_f16x2(uint32_t v) {
 }
 
 
+HX_DEV uint32_t e4m3x2_from_f32(float lo, float hi) {  // RNE, saturating (cvt.rn.satfinite)
+  uint16_t r;
+  asm("{\n.reg .b16 t;\ncvt.rn.satfinite.e4m3x2.f32 t, %1, %2;\nmov.b16 %0, t;\n}" : "=h"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+HX_DEV float2 f32x2_from_e4m3x2(uint32_t two) {
+  uint32_t h;
+  asm("{\n.reg .b16 t;\ncvt.u16.u32 t, %1;\ncvt.rn.f16x2.e4m3x2 %0, t;\n}" : "=r"(h) : "r"(two));
+  return unpack_f16x2(h);
+}
+// smallest power of two >= x (x > 0, normal)
+HX_DEV float pow2_ceil(float x) {
+  const uint32_t b = __float_as_uint(x);
+  return (b & 0x007FFFFFu) ? __uint_as_float((b & 0x7F800000u) + 0x00800000u) : x;
+}
 #ifdef HX_TC_TRACE
 __device__ unsigned long long g_tc_trace[64][8];
-__device__ unsigned long long g_tc_v[64][4];
-__device__ unsigned long long g_tc_k[64][6];
+__device__ unsigned long long g_tc_sm[64][4];
+__device__ unsigned long long g_tc_mma[64][6];
 HX_DEV unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -277,14 +294,23 @@ HX_DEV unsigned long long gtime() {
 #else
 #define TC_TRACE(i, ev) do {} while (0)
 #endif
+#ifdef HX_TC_TRACE
+#define TC_SM(i, ev) do { if (blockIdx.x == 0 && (i) < 64 && threadIdx.x == 0) g_tc_sm[i][ev] = gtime(); } while (0)
+#else
+#define TC_SM(i, ev) do {} while (0)
+#endif
+#ifdef HX_TC_TRACE
+#define TC_M(i, ev) do { if (blockIdx.x == 0 && (i) < 64 && lane == 0) g_tc_mma[i][ev] = gtime(); } while (0)
+#else
+#define TC_M(i, ev) do {} while (0)
+#endif
 }  // namespace
 
-template <int NQ, int KVF, int NST>
+template <int NQ, int NST>
 __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_constant__ AttnParams p) {
-  using C = TcCfg<NQ, KVF, NST>;
-  constexpr int NV = C::NV;
+  using C = TcCfg<NQ, NST>;
+  constexpr int NV = C::NV, NS = C::NS, NC = C::NC;
   using Bn = TcBars<NST, NV>;
-  constexpr int NC = C::NC;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(smem + C::OFF_BAR + C::NBAR * 8);
@@ -293,23 +319,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
   if (threadIdx.x == 0) {
     for (int s = 0; s < NST; ++s) {
       mbar_init(&bars[Bn::RAW_FULL + s], 1);
-      mbar_init(&bars[Bn::RAW_EMPTY + s], 8);  // 4 K + 4 V converter warps
+      mbar_init(&bars[Bn::RAW_EMPTY + s], 5);  // 4 V converter warps + the S MMAs (they read K in place)
     }
     for (int v = 0; v < NV; ++v) {
       mbar_init(&bars[Bn::VFULL + v], 4);
       mbar_init(&bars[Bn::VFREE + v], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&bars[Bn::KFULL + i], 4);
-      mbar_init(&bars[Bn::KFREE + i], 1);
-      mbar_init(&bars[Bn::QFREE + i], 1);
-      mbar_init(&bars[Bn::QRAWFREE + i], 4);
     }
     for (int i = 0; i < 4; ++i) {
       mbar_init(&bars[Bn::SFULL + i], 1);
       mbar_init(&bars[Bn::SFREE + i], 4);
       mbar_init(&bars[Bn::PFULL + i], 4);
       mbar_init(&bars[Bn::ODONE + i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&bars[Bn::QFULL + i], 4);
+      mbar_init(&bars[Bn::QFREE + i], 1);
+      mbar_init(&bars[Bn::QRAWFREE + i], 4);
     }
     fence_mbar_init();
   }
@@ -325,131 +350,28 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
   seq.init(p, C::PAGE);
   TcTile t;
 
-  if (warp >= kWarpKConv && warp < kWarpVConv) {
-    // ---------------------------------------------------------------- K converters (thread = token) + S issue
-    const int tl = threadIdx.x - kWarpKConv * 32;
-    const int page = tl >> 4, r = tl & 15, nt = r >> 3, g8 = r & 7;
-    const uint32_t lane_addr = tm_lane(tbase, warp);
-    int nitem0 = 0, nitem1 = 0;
-    for (int i = 0; seq.next(t); ++i) {
-      const int s = i % NST, kb = i & 1, g = t.slot;
-#ifdef HX_TC_TRACE
-      if (blockIdx.x == 0 && i < 64 && threadIdx.x == kWarpKConv * 32) g_tc_k[i][0] = gtime();
-#endif
-      mbar_wait(&bars[Bn::RAW_FULL + s], (i / NST) & 1);
-#ifdef HX_TC_TRACE
-      if (blockIdx.x == 0 && i < 64 && threadIdx.x == kWarpKConv * 32) g_tc_k[i][1] = gtime();
-#endif
-      if (t.first) {
-        // the slot's query image: previous item's S MMAs done, then this item's rows
-        const int ni = g ? nitem1++ : nitem0++;
-        if (ni > 0) mbar_wait(&bars[Bn::QFREE + g], (ni - 1) & 1);
-        const float* qs = reinterpret_cast<const float*>(smem + C::OFF_QRAW + g * C::QRAW);
-        uint8_t* qi = smem + C::OFF_QIMG + g * C::QIMG;
-        for (int u = tl; u < NQ * 16; u += 128) {
-          const int q = u % NQ, dg = u / NQ;
-          uint32_t h[4], l[4];
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float x0 = q < t.rows ? qs[q * kTcDP + dg * 8 + 2 * e] * p.qscale : 0.f;
-            const float x1 = q < t.rows ? qs[q * kTcDP + dg * 8 + 2 * e + 1] * p.qscale : 0.f;
-            h[e] = pack_f16x2(x0, x1);
-            const float2 hf = unpack_f16x2(h[e]);
-            l[e] = pack_f16x2(x0 - hf.x, x1 - hf.y);
-          }
-          // [dg][cg][c%8][d%8]: hi term in column q, lo term in column NQ + q
-          *reinterpret_cast<uint4*>(qi + (dg * (NC / 8) + (q >> 3)) * 128 + (q & 7) * 16) =
-              make_uint4(h[0], h[1], h[2], h[3]);
-          *reinterpret_cast<uint4*>(qi + (dg * (NC / 8) + ((NQ + q) >> 3)) * 128 + (q & 7) * 16) =
-              make_uint4(l[0], l[1], l[2], l[3]);
-        }
-        fence_proxy_async();  // generic-proxy image writes -> the tensor core's async proxy
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[Bn::QRAWFREE + g]);
-      }
-      if (i >= 2) mbar_wait(&bars[Bn::KFREE + kb], ((i >> 1) - 1) & 1);
-      tc_fence_after();
-      TC_TRACE(i, 1);
-      // this token's K row: every load issued first (rows of pages past np hold
-      // stale bytes; their logits are masked by the softmax, so no zeroing)
-      const uint32_t pbase = sbase + s * C::STAGE + page * C::PAGE;
-      uint4 kv[8];
-      uint32_t ex = 0;
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        if constexpr (KVF == 1) {
-          kv[j] = lds128(pbase + (((nt * 4 + (j >> 1)) * 32 + g8 * 4 + 2 * (j & 1)) * 8));  // kp = j/2, chunks 2(j%2)..+1
-        } else if (j < 4) {
-          kv[j] = lds128(pbase + (((nt * 4 + j) * 32 + g8 * 4) * 4));  // kp = j: chunks c = 0..3
-        }
-      }
-      if constexpr (KVF == 2) ex = lds32_(pbase + 16 * kTcDP + r * 4);  // this token's 4 block exponents
-#pragma unroll
-      for (int half = 0; half < 2; ++half) {  // dims [64 half, 64 half + 64) -> columns [32 half, +32)
-        uint32_t w[32];
-#pragma unroll
-        for (int kq = 0; kq < 2; ++kq) {
-          const int kp = 2 * half + kq;
-          if constexpr (KVF == 1) {
-#pragma unroll
-            for (int c2 = 0; c2 < 2; ++c2) {  // chunks c = 2 c2, 2 c2 + 1
-              const uint4 v = kv[2 * kp + c2];
-              const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-              for (int cc = 0; cc < 2; ++cc) {
-                const int c = 2 * c2 + cc;
-                uint32_t a0, a1, a2, a3;
-                e4m3x4_to_f16x2x2(wd[2 * cc], a0, a1);
-                e4m3x4_to_f16x2x2(wd[2 * cc + 1], a2, a3);
-                w[16 * kq + c] = a0;       // dims 32kp + 2c, +1
-                w[16 * kq + 4 + c] = a1;   // +8, +9
-                w[16 * kq + 8 + c] = a2;   // +16, +17
-                w[16 * kq + 12 + c] = a3;  // +24, +25
-              }
-            }
-          } else {
-            const uint32_t sc = ((ex >> (8 * kp)) & 0xFFu) << 10;
-            const uint32_t ss = sc | (sc << 16);
-            const uint4 v = kv[kp];
-            const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint32_t a0, a1, a2, a3;
-              e2m1x4_to_f16x2x2(wd[c] & 0xFFFFu, a0, a1);
-              e2m1x4_to_f16x2x2(wd[c] >> 16, a2, a3);
-              w[16 * kq + c] = hmul2_(a0, ss);
-              w[16 * kq + 4 + c] = hmul2_(a1, ss);
-              w[16 * kq + 8 + c] = hmul2_(a2, ss);
-              w[16 * kq + 12 + c] = hmul2_(a3, ss);
-            }
-          }
-        }
-        tmem_st32u(lane_addr + C::COL_K + kb * 64 + 32 * half, w);
-      }
-      tmem_wait_st();
-      tc_fence_before();
-      __syncwarp();
-      TC_TRACE(i, 2);
-      if (lane == 0) {
-        mbar_arrive(&bars[Bn::KFULL + kb]);
-        mbar_arrive(&bars[Bn::RAW_EMPTY + s]);
-      }
-    }
-  } else if (warp == kWarpMma) {
+  if (warp == kWarpMma) {
     // ---------------------------------------------------------------- MMA issue: S(i+1) before PV(i)
     // The whole warp walks the sequence and waits (converged, so descriptors stay
-    // warp-uniform); one elected lane issues each batch (a lone-lane issue loop
-    // costs ~145 cycles per tcgen05.mma in R2UR / waterfall code; converged, 8
-    // unrolled MMAs issue at ~21 cycles each: tools/tc_issue_probe.cu).
-    const uint64_t qdesc0 = umma_desc(sbase + C::OFF_QIMG, (NC / 8) * 128, 128);
+    // warp-uniform); one elected lane issues each batch (tc05.cuh elect_one).
+    const uint64_t qdesc0 = umma_desc(sbase + C::OFF_QIMG, (NS / 8) * 128, 128);
     const uint64_t pdesc0 = umma_desc(sbase + C::OFF_PBUF, 128, 16 * 128);
-    int jslot0 = 0, jslot1 = 0;
-    bool pend = false;
-    int pi = 0, pg = 0, pj = 0, pfirst = 0;
+    // K of a 128-token tile, as landed: core matrices (8 tokens x 16 dims) 128 B
+    // apart along the dims, 2 KB apart along the tokens (kv_layout.cuh kv8tc_offset)
+    const uint64_t kdesc0 = umma_desc(sbase, 128, 2048);
+    int jslot0 = 0, jslot1 = 0, nit0 = 0, nit1 = 0;
+    // PV lags S by two tiles (S(i), then PV(i-2)): S runs ahead of the softmax
+    // instead of queueing behind the previous tile's P, and the raw stages
+    // holding K are released early
+    int npend = 0;  // pending PVs (scalars, not arrays: no local memory)
+    int ai = 0, ag = 0, aj = 0, af = 0, bi = 0, bg = 0, bj = 0, bf = 0;
     auto issue_pv = [&](int i, int g, int j, int first) {
       const int vb = i % NV, pb = j & 1;
+      TC_M(i, 3);
       mbar_wait(&bars[Bn::VFULL + vb], (i / NV) & 1);
+      TC_M(i, 4);
       mbar_wait(&bars[Bn::PFULL + 2 * g + pb], (j >> 1) & 1);
+      TC_M(i, 5);
       tc_fence_after();
       const uint32_t acol = tbase + C::COL_V + vb * 64, dcol = tbase + C::COL_O + g * NC;
       const uint64_t pdesc = pdesc0 + static_cast<uint64_t>(((2 * g + pb) * C::PBUF) >> 4);
@@ -464,32 +386,55 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
       __syncwarp();
     };
     for (int i = 0; seq.next(t); ++i) {
-      const int kb = i & 1, g = t.slot, j = g ? jslot1++ : jslot0++, sb = j & 1;
-      mbar_wait(&bars[Bn::KFULL + kb], (i >> 1) & 1);
-      if (j >= 2) mbar_wait(&bars[Bn::SFREE + 2 * g + sb], ((j >> 1) - 1) & 1);
+      const int s = i % NST, g = t.slot, j = g ? jslot1++ : jslot0++, sb = C::SB == 2 ? (j & 1) : 0;
+      TC_M(i, 0);
+      mbar_wait(&bars[Bn::RAW_FULL + s], (i / NST) & 1);
+      TC_M(i, 1);
+      if (t.first) {
+        const int ni = g ? nit1++ : nit0++;
+        mbar_wait(&bars[Bn::QFULL + g], ni & 1);  // this item's query image
+      }
+      if (j >= C::SB) mbar_wait(&bars[Bn::SFREE + 2 * g + sb], ((j / C::SB) - 1) & 1);
+      TC_M(i, 2);
       tc_fence_after();
-      const uint32_t dcol = tbase + C::COL_S + (2 * g + sb) * NC, acol = tbase + C::COL_K + kb * 64;
+      const uint32_t dcol = tbase + C::COL_S + (C::SB * g + sb) * NS;
+      const uint64_t kdesc = kdesc0 + static_cast<uint64_t>((s * C::STAGE) >> 4);
       const uint64_t qdesc = qdesc0 + static_cast<uint64_t>((g * C::QIMG) >> 4);
       const bool lst = t.last;
       if (elect_one()) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k)
-          umma_ts(dcol, acol + k * 8, qdesc + static_cast<uint64_t>((k * NC * 32) >> 4), C::IDESC_S,
-                  k > 0 ? 1u : 0u);
+        for (int k = 0; k < 4; ++k)  // K = 32 dims per MMA: two core matrices along the dims
+          umma_ss_f8(dcol, kdesc + static_cast<uint64_t>((k * 256) >> 4),
+                     qdesc + static_cast<uint64_t>((k * 2 * (NS / 8) * 128) >> 4), C::IDESC_S, k > 0 ? 1u : 0u);
         umma_commit(&bars[Bn::SFULL + 2 * g + sb]);
-        umma_commit(&bars[Bn::KFREE + kb]);
+        umma_commit(&bars[Bn::RAW_EMPTY + s]);  // K read: the stage may refill once V is converted too
         if (lst) umma_commit(&bars[Bn::QFREE + g]);
       }
       __syncwarp();
       TC_TRACE(i, 5);
-      if (pend) issue_pv(pi, pg, pj, pfirst);
-      pend = true;
-      pi = i;
-      pg = g;
-      pj = j;
-      pfirst = t.first;
+      if (npend == 2) {
+        issue_pv(ai, ag, aj, af);
+        ai = bi;
+        ag = bg;
+        aj = bj;
+        af = bf;
+        npend = 1;
+      }
+      if (npend == 0) {
+        ai = i;
+        ag = g;
+        aj = j;
+        af = t.first;
+      } else {
+        bi = i;
+        bg = g;
+        bj = j;
+        bf = t.first;
+      }
+      ++npend;
     }
-    if (pend) issue_pv(pi, pg, pj, pfirst);
+    if (npend >= 1) issue_pv(ai, ag, aj, af);
+    if (npend == 2) issue_pv(bi, bg, bj, bf);
   } else if (warp == kWarpProd) {
     // ---------------------------------------------------------------- producer (one lane; a bulk-copy
     // issue blocks its warp ~0.3 us, so it has a warp of its own)
@@ -517,71 +462,81 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
       if (!waited) griddep_wait();
     }
   } else if (warp >= kWarpVConv) {
-    // ---------------------------------------------------------------- V converters (thread = dim)
-    const int d = threadIdx.x - kWarpVConv * 32;
-    const int vnd = d >> 3, vg8 = d & 7, nd2 = vnd >> 1, sub = vnd & 1;
+    // ---------------------------------------------------------------- V converters (thread = dim) + query image
+    const int d = threadIdx.x - kWarpVConv * 32, vw = warp - kWarpVConv;
     const uint32_t lane_addr = tm_lane(tbase, warp);
+    int nitem0 = 0, nitem1 = 0;
     for (int i = 0; seq.next(t); ++i) {
-      const int s = i % NST, vb = i % NV;
-#ifdef HX_TC_TRACE
-      if (blockIdx.x == 0 && i < 64 && threadIdx.x == kWarpVConv * 32) g_tc_v[i][0] = gtime();
-#endif
+      const int s = i % NST, vb = i % NV, g = t.slot;
       mbar_wait(&bars[Bn::RAW_FULL + s], (i / NST) & 1);
-#ifdef HX_TC_TRACE
-      if (blockIdx.x == 0 && i < 64 && threadIdx.x == kWarpVConv * 32) g_tc_v[i][1] = gtime();
-#endif
+      if (t.first) {
+        // The item's query as T e4m3 terms: q * qscale = s0 * sum_j 16^-j c_j, s0 the
+        // smallest power of two with max|q| <= 448 s0 (per query; every scaling exact).
+        // Image: Q8^T K-major core matrices [dim/16][row/8][row%8][16 dims], row = j NQ + q.
+        const int ni = g ? nitem1++ : nitem0++;
+        if (ni > 0) mbar_wait(&bars[Bn::QFREE + g], (ni - 1) & 1);  // previous item's S MMAs done
+        const float* qs = reinterpret_cast<const float*>(smem + C::OFF_QRAW + g * C::QRAW);
+        uint8_t* qi = smem + C::OFF_QIMG + g * C::QIMG;
+        float* qs0 = reinterpret_cast<float*>(smem + C::OFF_QS0) + g * NQ;
+        for (int q = vw; q < NQ; q += 4) {
+          float x[4];
+          float am = 0.f;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            x[e] = q < t.rows ? qs[q * kTcDP + 4 * lane + e] * p.qscale : 0.f;
+            am = fmaxf(am, fabsf(x[e]));
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) am = fmaxf(am, __shfl_xor_sync(0xffffffffu, am, o));
+          const float s0 = am > 0.f ? pow2_ceil(am / 448.f) : 1.f;
+#pragma unroll
+          for (int e = 0; e < 4; ++e) x[e] /= s0;  // exact
+          float sc = 1.f;
+#pragma unroll
+          for (int jt = 0; jt < kQTerms; ++jt, sc *= 16.f) {
+            const uint32_t c01 = e4m3x2_from_f32(x[0] * sc, x[1] * sc), c23 = e4m3x2_from_f32(x[2] * sc, x[3] * sc);
+            const float2 d01 = f32x2_from_e4m3x2(c01), d23 = f32x2_from_e4m3x2(c23);
+            x[0] -= d01.x / sc;
+            x[1] -= d01.y / sc;
+            x[2] -= d23.x / sc;
+            x[3] -= d23.y / sc;
+            const int row = jt * NQ + q;
+            *reinterpret_cast<uint32_t*>(qi + ((lane >> 2) * (NS / 8) + (row >> 3)) * 128 + (row & 7) * 16 +
+                                         4 * (lane & 3)) = c01 | (c23 << 16);
+          }
+          if (lane == 0) qs0[q] = s0;
+        }
+        fence_proxy_async();  // generic-proxy image writes -> the tensor core's async proxy
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&bars[Bn::QRAWFREE + g]);
+          mbar_arrive(&bars[Bn::QFULL + g]);
+        }
+      }
       if (i >= NV) mbar_wait(&bars[Bn::VFREE + vb], ((i / NV) - 1) & 1);
       tc_fence_after();
       TC_TRACE(i, 3);
-      const uint32_t stage = sbase + s * C::STAGE;
+      const uint32_t vbase = sbase + s * C::STAGE + 1024 + d * 8;  // this dim's 8-token word, first half
 #pragma unroll
       for (int half = 0; half < 2; ++half) {  // pages [4 half, 4 half + 4) -> columns [32 half, +32)
-        // all of the half's shared-memory loads first (pages past np read stale
-        // bytes and are zeroed below), then the widening
-        uint4 v0[4], v1[4], v2[4];
+        uint2 w[4][2];
 #pragma unroll
         for (int pq = 0; pq < 4; ++pq) {
-          const uint32_t pbase = stage + (4 * half + pq) * C::PAGE;
-          if constexpr (KVF == 1) {
-            // chunks c = 0..3 of (nd2, g8): 32 contiguous bytes; this dim's 4 bytes of each
-            const uint32_t cb = pbase + 16 * kTcDP + (nd2 * 32 + vg8 * 4) * 8;
-            v0[pq] = lds128(cb);
-            v1[pq] = lds128(cb + 16);
-          } else {
-            v0[pq] = lds128(pbase + 8 * kTcDP + (nd2 * 32 + vg8 * 4) * 4);
-            v1[pq] = lds128(pbase + 16 * kTcDP + kTcDP / 2 + (d >> 5) * 32);  // f16x2 scales, tokens 0..7
-            v2[pq] = lds128(pbase + 16 * kTcDP + kTcDP / 2 + (d >> 5) * 32 + 16);  // tokens 8..15
-          }
+          const uint32_t pb = vbase + (4 * half + pq) * C::PAGE;
+          w[pq][0] = lds64(pb);         // tokens 0..7
+          w[pq][1] = lds64(pb + 2048);  // tokens 8..15
         }
-        uint32_t w[32];
+        uint32_t r[32];
 #pragma unroll
         for (int pq = 0; pq < 4; ++pq) {
-          const bool have = 4 * half + pq < t.np;
-          if constexpr (KVF == 1) {
-            const uint32_t wd[4] = {sub ? v0[pq].y : v0[pq].x, sub ? v0[pq].w : v0[pq].z, sub ? v1[pq].y : v1[pq].x,
-                                    sub ? v1[pq].w : v1[pq].z};
+          const bool have = 4 * half + pq < t.np;  // pages past np: stale bytes (maybe nan) -> zeros
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {  // tokens (2c, 2c+1) and (2c+8, 2c+9)
-              uint32_t lo, hi;
-              e4m3x4_to_f16x2x2(have ? wd[c] : 0u, lo, hi);
-              w[8 * pq + c] = lo;
-              w[8 * pq + 4 + c] = hi;
-            }
-          } else {
-            const uint32_t wd[4] = {v0[pq].x, v0[pq].y, v0[pq].z, v0[pq].w};
-            const uint32_t s0w[4] = {v1[pq].x, v1[pq].y, v1[pq].z, v1[pq].w};  // (2^e_2c, 2^e_2c+1)
-            const uint32_t s1w[4] = {v2[pq].x, v2[pq].y, v2[pq].z, v2[pq].w};  // tokens 2c+8, 2c+9
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint32_t a0, a1;
-              e2m1x4_to_f16x2x2(__byte_perm(wd[c], 0u, sub ? 0x3232u : 0x1010u), a0, a1);
-              // pages past np: stale bytes (a stale scale may be inf / nan) -> exact zeros
-              w[8 * pq + c] = have ? hmul2_(a0, s0w[c]) : 0u;
-              w[8 * pq + 4 + c] = have ? hmul2_(a1, s1w[c]) : 0u;
-            }
+          for (int hh = 0; hh < 2; ++hh) {
+            e4m3x4_to_f16x2x2(have ? w[pq][hh].x : 0u, r[8 * pq + 4 * hh], r[8 * pq + 4 * hh + 1]);
+            e4m3x4_to_f16x2x2(have ? w[pq][hh].y : 0u, r[8 * pq + 4 * hh + 2], r[8 * pq + 4 * hh + 3]);
           }
         }
-        tmem_st32u(lane_addr + C::COL_V + vb * 64 + 32 * half, w);
+        tmem_st32u(lane_addr + C::COL_V + vb * 64 + 32 * half, r);
       }
       tmem_wait_st();
       tc_fence_before();
@@ -591,32 +546,48 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
         mbar_arrive(&bars[Bn::VFULL + vb]);
         mbar_arrive(&bars[Bn::RAW_EMPTY + s]);
       }
-#ifdef HX_TC_TRACE
-      if (blockIdx.x == 0 && i < 64 && threadIdx.x == kWarpVConv * 32) g_tc_v[i][2] = gtime();
-#endif
     }
   } else {
-    // ---------------------------------------------------------------- softmax + PV (slot g)
+    // ---------------------------------------------------------------- softmax (slot g)
     const int g = warp >> 2, wq = warp & 3;
     const int tl = threadIdx.x - g * 128;  // token lane of S^T, dim lane of O^T
     const uint32_t lane_addr = tm_lane(tbase, warp);
     const int barid = 1 + g;
     float* red = reinterpret_cast<float*>(smem + C::OFF_RED) + g * 4 * NQ;
+    const float* qs0 = reinterpret_cast<const float*>(smem + C::OFF_QS0) + g * NQ;
     const uint32_t prow = sbase + C::OFF_PBUF + (2 * g) * C::PBUF + (tl >> 3) * 128 + (tl & 7) * 16;
-    const uint64_t pdesc0 = umma_desc(sbase + C::OFF_PBUF + (2 * g) * C::PBUF, 128, 16 * 128);
     float m[NQ], l[NQ];
     int j = 0;
     for (int i = 0; seq.next(t); ++i) {
       if (t.slot != g) continue;
-      const int sb = j & 1;
-      mbar_wait(&bars[Bn::SFULL + 2 * g + sb], (j >> 1) & 1);
+      const int sb = j & 1;                               // P^T buffer
+      const int ss = C::SB == 2 ? sb : 0;                 // S buffer
+      mbar_wait(&bars[Bn::SFULL + 2 * g + ss], (j / C::SB) & 1);
       tc_fence_after();
       TC_TRACE(i, 6);
-      float sv[NC];
-      tmem_ldn<NC>(lane_addr + C::COL_S + (2 * g + sb) * NC, sv);
+      // S = s0 * (S_0 + S_1 / 16 + S_2 / 256 + S_3 / 4096), columns jt * NQ + q
+      float part[NQ];
+      {
+        const uint32_t scol = lane_addr + C::COL_S + (C::SB * g + ss) * NS;
+        float sv[32];
+        tmem_ld32(scol, sv);  // NQ = 8: all four terms; NQ = 16: terms 0, 1
+        if constexpr (NQ == 8) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            part[q] = ((sv[24 + q] * (1.f / 16.f) + sv[16 + q]) * (1.f / 16.f) + sv[8 + q]) * (1.f / 16.f) + sv[q];
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) part[q] = sv[16 + q] * (1.f / 16.f) + sv[q];
+          tmem_ld32(scol + 32, sv);  // terms 2, 3
+#pragma unroll
+          for (int q = 0; q < 16; ++q)
+            part[q] += (sv[16 + q] * (1.f / 16.f) + sv[q]) * (1.f / 256.f);
+        }
+      }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[Bn::SFREE + 2 * g + sb]);
+      if (lane == 0) mbar_arrive(&bars[Bn::SFREE + 2 * g + ss]);
+      TC_SM(i, 0);
       if (t.first) {
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
@@ -629,12 +600,14 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
       bool grow = false;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        s[q] = valid ? sv[q] + sv[NQ + q] : -INFINITY;
-        grow |= s[q] > m[q] + 8.f;
+        s[q] = valid ? qs0[q] * part[q] : -INFINITY;
+        grow |= s[q] > m[q] + kGrow;
       }
       bool rescale = false;
       float alpha[NQ];
-      if (bar_red_or(barid, 128, grow)) {
+      const bool any_grow = bar_red_or(barid, 128, grow);
+      TC_SM(i, 1);
+      if (any_grow) {
         // tile maxima per query over the 128 token lanes
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
@@ -642,10 +615,23 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
           if (lane == 0) red[wq * NQ + q] = mx;
         }
         named_bar(barid, 128);
+        float tmx[NQ];
+#pragma unroll
+        for (int q = 0; q < NQ; ++q) tmx[q] = -INFINITY;
+#pragma unroll
+        for (int w4 = 0; w4 < 4; ++w4)
+#pragma unroll
+          for (int q4 = 0; q4 < NQ / 4; ++q4) {
+            const float4 v4 = *reinterpret_cast<const float4*>(red + w4 * NQ + 4 * q4);
+            tmx[4 * q4] = fmaxf(tmx[4 * q4], v4.x);
+            tmx[4 * q4 + 1] = fmaxf(tmx[4 * q4 + 1], v4.y);
+            tmx[4 * q4 + 2] = fmaxf(tmx[4 * q4 + 2], v4.z);
+            tmx[4 * q4 + 3] = fmaxf(tmx[4 * q4 + 3], v4.w);
+          }
 #pragma unroll
         for (int q = 0; q < NQ; ++q) {
-          const float tm = fmaxf(fmaxf(red[q], red[NQ + q]), fmaxf(red[2 * NQ + q], red[3 * NQ + q]));
-          const float mn = tm > m[q] + 8.f ? tm : m[q];
+          const float tm = tmx[q];
+          const float mn = tm > m[q] + kGrow ? tm : m[q];
           alpha[q] = fast_exp2(m[q] - mn);  // 0 when m = -inf
           rescale |= mn != m[q];
           l[q] *= alpha[q];
@@ -655,6 +641,22 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
       }
       // P^T buffer sb of this slot: PV(j-2) done
       if (j >= 2) mbar_wait(&bars[Bn::ODONE + 2 * g + sb], ((j >> 1) - 1) & 1);
+      TC_SM(i, 2);
+      if (rescale) {  // rare: some query's max grew by > kGrow (log2): wait for PV(j-1), rescale O^T
+        mbar_wait(&bars[Bn::ODONE + 2 * g + (sb ^ 1)], ((j - 1) >> 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int h = 0; h < NC / 16; ++h) {  // columns [16h, 16h + 16): query (16h + c) % NQ
+          float ov[16];
+          const uint32_t col = lane_addr + C::COL_O + g * NC + 16 * h;
+          tmem_ld16(col, ov);
+          uint32_t rr[16];
+#pragma unroll
+          for (int c = 0; c < 16; ++c) rr[c] = __float_as_uint(ov[c] * alpha[(16 * h + c) % NQ]);
+          tmem_st16(col, rr);
+        }
+        tmem_wait_st();
+      }
       {
         uint32_t ph[NQ / 2], pl[NQ / 2];
 #pragma unroll
@@ -673,21 +675,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
           sts128(pr + cg * 2048, make_uint4(ph[4 * cg], ph[4 * cg + 1], ph[4 * cg + 2], ph[4 * cg + 3]));
           sts128(pr + (NQ / 8 + cg) * 2048, make_uint4(pl[4 * cg], pl[4 * cg + 1], pl[4 * cg + 2], pl[4 * cg + 3]));
         }
-      }
-      if (rescale) {  // rare: some query's max grew by > 8 (log2): wait for PV(j-1), rescale O^T
-        mbar_wait(&bars[Bn::ODONE + 2 * g + (sb ^ 1)], ((j - 1) >> 1) & 1);
-        tc_fence_after();
-#pragma unroll
-        for (int h = 0; h < NC / 16; ++h) {  // columns [16h, 16h + 16): query (16h + c) % NQ
-          float ov[16];
-          const uint32_t col = lane_addr + C::COL_O + g * NC + 16 * h;
-          tmem_ld16(col, ov);
-          uint32_t rr[16];
-#pragma unroll
-          for (int c = 0; c < 16; ++c) rr[c] = __float_as_uint(ov[c] * alpha[(16 * h + c) % NQ]);
-          tmem_st16(col, rr);
-        }
-        tmem_wait_st();
       }
       fence_proxy_async();
       tc_fence_before();
@@ -738,7 +725,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
             if (tl == q) p.part_lse2[obase + q] = m[q] + __log2f(L);
           }
         }
-        named_bar(barid, 128);  // red reads done before the next item's grow path
+        named_bar(barid, 128);  // red reads and the partial's stores done
+        // HOP-B stream reducer (fused == 2): publish the finished split (cumulative
+        // gpu-scope release of the whole group's stores, ordered by the barrier)
+        if (p.fused == 2 && tl == 0)
+          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.stream_done + t.stream) : "memory");
       }
       ++j;
     }
@@ -753,36 +744,35 @@ __global__ void __launch_bounds__(kTcThreads, 1) attn_tc_kernel(const __grid_con
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     const unsigned long long t0 = g_tc_trace[0][0];
     for (int i = 0; i < 40; ++i)
-      printf("tile %2d tma %6llu  k %6llu-%6llu S %6llu  v %6llu-%6llu  sm %6llu-%6llu\n", i, g_tc_trace[i][0] - t0,
-             g_tc_trace[i][1] - t0, g_tc_trace[i][2] - t0, g_tc_trace[i][5] - t0, g_tc_trace[i][3] - t0,
-             g_tc_trace[i][4] - t0, g_tc_trace[i][6] - t0, g_tc_trace[i][7] - t0);
-    for (int i = 10; i < 24; ++i)
-      printf("k %2d top %6llu rawfull %6llu | kfull %6llu sfree %6llu\n", i, g_tc_k[i][0] - t0, g_tc_k[i][1] - t0,
-             g_tc_k[i][2] - t0, g_tc_k[i][3] - t0);
-    for (int i = 0; i < 30; ++i)
-      printf("v %2d top %6llu rawfull %6llu produced %6llu\n", i, g_tc_v[i][0] - t0, g_tc_v[i][1] - t0, g_tc_v[i][2] - t0);
+      printf("tile %2d tma %6llu  v %6llu-%6llu  S %6llu  sm %6llu ld %6llu vote %6llu odone %6llu end %6llu\n", i,
+             g_tc_trace[i][0] - t0, g_tc_trace[i][3] - t0, g_tc_trace[i][4] - t0, g_tc_trace[i][5] - t0,
+             g_tc_trace[i][6] - t0, g_tc_sm[i][0] - t0, g_tc_sm[i][1] - t0, g_tc_sm[i][2] - t0, g_tc_trace[i][7] - t0);
+    for (int i = 14; i < 26; ++i)
+      printf("mma %2d top %6llu rawfull %6llu sfree %6llu | pv top %6llu vfull %6llu pfull %6llu\n", i,
+             g_tc_mma[i][0] - t0, g_tc_mma[i][1] - t0, g_tc_mma[i][2] - t0, g_tc_mma[i][3] - t0, g_tc_mma[i][4] - t0,
+             g_tc_mma[i][5] - t0);
   }
 #endif
 }
 
-template <int NQ, int KVF, int NST>
+template <int NQ, int NST>
 static cudaError_t launch_tc_t(const AttnParams& p, int grid, cudaStream_t stream) {
-  using C = TcCfg<NQ, KVF, NST>;
-  const cudaError_t e = smem_optin<attn_tc_kernel<NQ, KVF, NST>>(C::SMEM);
+  using C = TcCfg<NQ, NST>;
+  const cudaError_t e = smem_optin<attn_tc_kernel<NQ, NST>>(C::SMEM);
   if (e != cudaSuccess) return e;
-  return launch_k(attn_tc_kernel<NQ, KVF, NST>, dim3(grid), dim3(kTcThreads), C::SMEM, stream, p);
+  return launch_k(attn_tc_kernel<NQ, NST>, dim3(grid), dim3(kTcThreads), C::SMEM, stream, p);
 }
 
 bool attn_tc_supported(const AttnParams& p) {
-  return (p.kv8 || p.kv4) && p.dp == kTcDP && p.q_chunks == 1 && (p.qrows == 8 || p.qrows == 16) && !p.fused;
+  return p.kv8 && !p.kv4 && p.dp == kTcDP && p.q_chunks == 1 && (p.qrows == 8 || p.qrows == 16) &&
+         (p.fused == 0 || p.fused == 2);
 }
 
 // grid: CTAs; two item slots each, items statically assigned (item = unit + n *
 // 2 grid for unit = 2 CTA + slot)
 cudaError_t launch_attn_tc(const AttnParams& p, int grid, cudaStream_t stream) {
   if (!attn_tc_supported(p)) return cudaErrorInvalidValue;
-  if (p.kv4) return p.qrows == 16 ? launch_tc_t<16, 2, 9>(p, grid, stream) : launch_tc_t<8, 2, 11>(p, grid, stream);
-  return p.qrows == 16 ? launch_tc_t<16, 1, 4>(p, grid, stream) : launch_tc_t<8, 1, 5>(p, grid, stream);
+  return p.qrows == 16 ? launch_tc_t<16, 5>(p, grid, stream) : launch_tc_t<8, 6>(p, grid, stream);
 }
 
 }  // namespace hx

@@ -394,8 +394,11 @@ void Engine::alloc() {
   // tcgen05 kernel for quantised pages: opt-in (HX_ATTN_TC=1) -- the e4m3 / e2m1
   // widening it still pays on the CUDA cores keeps it behind the legacy kernel
   // (K1-TC)
-  attn_tc_ = !mla_ && (kv8_ || kv4_) && DP_ == 128 && q_chunks_ == 1 && std::getenv("HX_ATTN_TC") &&
+  attn_tc_ = !mla_ && kv8_ && DP_ == 128 && q_chunks_ == 1 && std::getenv("HX_ATTN_TC") &&
              std::getenv("HX_ATTN_TC")[0] == '1';
+  // the tcgen05 kernel reads K straight from its pages (kind::f8f6f4): FP8 pages
+  // in the tensor-core layout, which only it reads -- so no in-kernel HOP-B reduce
+  kv8tc_ = attn_tc_;
   n_streams_ = n_slots_ * B_ * kvh_per_slot_ * q_chunks_;
   const int req_streams = n_slots_ * kvh_per_slot_ * q_chunks_;
   splits_ = plan_splits(n_streams_, page_cap_);
@@ -408,7 +411,7 @@ void Engine::alloc() {
   }
   attn_grid_ = std::min(mla_ ? num_sms_ / 2 : num_sms_, n_items_);  // MLA: CTA pairs
   if (std::getenv("HX_FUSED_REDUCE") && std::getenv("HX_FUSED_REDUCE")[0] == '0') fused_ = false;
-  hopb_inkernel_ = std::getenv("HX_HOPB_INKERNEL") && std::getenv("HX_HOPB_INKERNEL")[0] == '1';
+  hopb_inkernel_ = !kv8tc_ && std::getenv("HX_HOPB_INKERNEL") && std::getenv("HX_HOPB_INKERNEL")[0] == '1';
   local_stream_reduce_ = std::getenv("HX_LOCAL_STREAM_REDUCE") && std::getenv("HX_LOCAL_STREAM_REDUCE")[0] == '1';
   if (std::getenv("HX_HOPB_GROUP")) hopb_group_ = std::max(1, std::atoi(std::getenv("HX_HOPB_GROUP")));
   if (std::getenv("HX_A2A_NCCL") && std::getenv("HX_A2A_NCCL")[0] == '1') nccl_a2a_ = true;
@@ -540,7 +543,7 @@ void Engine::plan_gemvs() {
     q.p.slot_base = slot_base_;
     q.p.n_local_slots = n_slots_;
     q.p.append = 1;
-    q.p.kv8 = kv8_ ? 1 : 0;
+    q.p.kv8 = kv8_fmt();
     q.p.kv4 = kv4_ ? 1 : 0;
     plan_qkv_.push_back(q);
     if (!attn_only_) {
@@ -1054,7 +1057,7 @@ void Engine::append_kv(int64_t layer, int64_t request, int64_t n, const float* k
   cuda_check(cudaMemcpyAsync(dv, vb.data(), cnt * esz, cudaMemcpyHostToDevice, stream_), "append h2d");
   cuda_check(launch_kv_append_rows(kv_[layer], dk, dv, static_cast<int>(n), static_cast<int>(request),
                                    d_total_ + layer * B_, B_, static_cast<int>(Kh_), kvh_per_slot_, kvp_,
-                                   chunk_, static_cast<int>(D_), DP_, page_cap_, slot_base_, n_slots_, kv8_,
+                                   chunk_, static_cast<int>(D_), DP_, page_cap_, slot_base_, n_slots_, kv8_fmt(),
                                    stream_),
              "append kernel");
   cuda_check(cudaStreamSynchronize(stream_), "append sync");
@@ -1084,7 +1087,7 @@ void Engine::fill_kv_hash(int64_t n, uint64_t seed) {
   for (int64_t l = 0; l < L_ && !mla_ && !kv4_; ++l) {
     cuda_check(launch_kv_fill_hash(kv_[l], d_total_ + l * B_, B_, static_cast<int>(Kh_), kvh_per_slot_, kvp_,
                                    chunk_, static_cast<int>(D_), DP_, page_cap_, slot_base_, n_slots_, n, seed,
-                                   hash_stream(kCacheK, l), hash_stream(kCacheV, l), kv8_, stream_),
+                                   hash_stream(kCacheK, l), hash_stream(kCacheV, l), kv8_fmt(), stream_),
                "kv fill");
     for (int b = 0; b < B_; ++b) h_total_[static_cast<size_t>(l * B_ + b)] += n;
   }
@@ -1173,8 +1176,8 @@ void Engine::read_kv(int64_t layer, int64_t request, int64_t rank, int64_t head,
   for (int64_t t = 0; t < n && !kv4_; ++t) {
     const uint8_t* page = buf.data() + static_cast<size_t>(t / 16) * page_bytes_;
     for (int d = 0; d < D_; ++d) {
-      const uint8_t* pk = page + kv_offset(DP_, static_cast<int>(t % 16), d, false, kv8_);
-      const uint8_t* pv = page + kv_offset(DP_, static_cast<int>(t % 16), d, true, kv8_);
+      const uint8_t* pk = page + kv_offset(DP_, static_cast<int>(t % 16), d, false, kv8_fmt());
+      const uint8_t* pv = page + kv_offset(DP_, static_cast<int>(t % 16), d, true, kv8_fmt());
       if (kv8_) {
         k[t * D_ + d] = e4m3_to_float(*pk);
         v[t * D_ + d] = e4m3_to_float(*pv);
@@ -1308,8 +1311,10 @@ void Engine::launch_attention_kernels(const AttnParams& a) {
     mark(2);
     cuda_check(launch_mla_split_reduce(a, d_frag_o_, d_frag_lse_, stream_), "mla split reduce");
   } else {
+    if (kv8tc_ && !attn_tc_supported(a))  // tensor-core FP8 pages: only the tcgen05 kernel reads them
+      throw std::runtime_error("attention: FP8 tensor-core pages need the tcgen05 kernel (unsupported launch)");
     if (attn_tc_ && attn_tc_supported(a))
-      cuda_check(launch_attn_tc(a, std::min(attn_grid_, a.n_items), stream_), "attention (tcgen05)");
+      cuda_check(launch_attn_tc(a, std::min(attn_grid_, (a.n_items + 1) / 2), stream_), "attention (tcgen05)");
     else
       cuda_check(launch_attn_decode(a, std::min(attn_grid_, a.n_items), stream_), "attention");
     mark(2);

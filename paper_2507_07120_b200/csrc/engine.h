@@ -145,6 +145,8 @@ class Engine {
   bool split_env_ = false;
   int plan_splits(int streams, int pages) const;
   bool attn_tc_ = false;
+  bool kv8tc_ = false;  // FP8 pages in the tensor-core layout (kv_layout.cuh kv8tc_offset)
+  int kv8_fmt() const { return kv8_ ? (kv8tc_ ? 2 : 1) : 0; }
   bool hopb_inkernel_ = false;
   bool local_stream_reduce_ = false;  // local pools: stream reducer instead of the split-reduce kernel (HX_LOCAL_STREAM_REDUCE=1; measured slower: DESIGN)
   int hopb_group_ = 1;  // HOP-B: requests per work group (HX_HOPB_GROUP; 1 = stream-major)  // HOP-B reduce inside the attention kernel (HX_HOPB_INKERNEL=1) vs the stream reducer  // quantised pages on the tcgen05 kernel (attention_tc.cu)

@@ -499,7 +499,7 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
               if ((d & 31) == 0) pg[kv4_scale_offset(p.dp, static_cast<int>(row & 15), d, is_v != 0)] = kv4_scale_byte(ex, is_v != 0);
             } else {
               uint8_t* dst = p.kv + page * page_bytes_kv(p.dp, p.kv8 != 0) +
-                             kv_offset(p.dp, static_cast<int>(row & 15), d, is_v != 0, p.kv8 != 0);
+                             kv_offset(p.dp, static_cast<int>(row & 15), d, is_v != 0, p.kv8);
               if (p.kv8)
                 *dst = e4m3_from_double(static_cast<double>(y[0]));
               else

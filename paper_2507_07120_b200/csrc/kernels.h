@@ -187,7 +187,7 @@ struct GemvParams {
   int nq, nk, kv_heads, kvh_per_slot, rr_chunk, page_cap, slot_base, n_local_slots;
   int kv_head_base;      // global index of the first KV head in this projection
   int append;            // write K/V into the cache
-  int kv8;               // GQA cache pages are FP8 e4m3 (fp8.cuh), else bf16
+  int kv8;               // GQA cache pages: 0 bf16, 1 FP8 e4m3 fragment-major, 2 FP8 tensor-core layout (kv_layout.cuh)
   int kv4;               // GQA cache pages are FP4 e2m1 blocks (fp8.cuh, kv_layout.cuh)
   uint8_t* q_img;        // MLA (mla = 1): q -> bf16 query images, latent -> MLA pages
   int mla;
@@ -250,13 +250,13 @@ cudaError_t launch_argmax_finish(const unsigned long long* best, int batch, int*
 cudaError_t launch_kv_append_rows(uint8_t* kv, const void* k_rows, const void* v_rows,
                                   int n, int b, int* total, int batch, int kv_heads,
                                   int kvh_per_slot, int kvp, int chunk, int head_dim, int dp,
-                                  int page_cap, int slot_base, int n_local_slots, bool fp8,
+                                  int page_cap, int slot_base, int n_local_slots, int fp8,
                                   cudaStream_t stream);
 // Device-side synthetic fill: tokens [t0, t0+n) of every request from the hash RNG.
 cudaError_t launch_kv_fill_hash(uint8_t* kv, int* total, int batch, int kv_heads,
                                 int kvh_per_slot, int kvp, int chunk, int head_dim, int dp,
                                 int page_cap, int slot_base, int n_local_slots, long long n,
-                                uint64_t seed, uint64_t stream_k, uint64_t stream_v, bool fp8,
+                                uint64_t seed, uint64_t stream_k, uint64_t stream_v, int fp8,
                                 cudaStream_t stream);
 // Weight init from the hash RNG straight into the fragment-major layout.
 // Segment list maps combined rows to (hash stream, column count, column offset).

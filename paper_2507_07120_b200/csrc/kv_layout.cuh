@@ -52,7 +52,23 @@ __host__ __device__ __forceinline__ uint32_t v_offset(int dp, int t, int d) {
 __host__ __device__ __forceinline__ uint32_t page_bytes_kv(int dp, bool fp8) {
   return (fp8 ? 32u : 64u) * static_cast<uint32_t>(dp);
 }
-__host__ __device__ __forceinline__ uint32_t kv_offset(int dp, int t, int d, bool is_v, bool fp8) {
+// FP8 pages in the tensor-core layout (fp8 mode 2; DP = 128, the tcgen05 GQA
+// kernel, attention_tc.cu): two 8-token halves of 2 KB, each
+//   K [dim/16 : 8][token : 8][16 dims]   -- the K-major UMMA core matrices
+//                                           (8 rows x 16 B) of kind::f8f6f4, so
+//                                           a 128-token tile of 8 pages is the A
+//                                           operand of S^T = K . Q^T as loaded
+//                                           (LBO 128 B, SBO 2 KB), no conversion
+//   V [dim : 128][token : 8]             -- a converter thread (= dim) reads its
+//                                           8 tokens as one 8-byte word
+__host__ __device__ __forceinline__ uint32_t kv8tc_offset(int t, int d, bool is_v) {
+  const uint32_t half = static_cast<uint32_t>(t >> 3) * 2048u, r = static_cast<uint32_t>(t & 7);
+  return is_v ? half + 1024u + static_cast<uint32_t>(d) * 8u + r
+              : half + static_cast<uint32_t>(d >> 4) * 128u + r * 16u + static_cast<uint32_t>(d & 15);
+}
+// fp8: 0 bf16 pages, 1 FP8 fragment-major pages, 2 FP8 tensor-core layout
+__host__ __device__ __forceinline__ uint32_t kv_offset(int dp, int t, int d, bool is_v, int fp8) {
+  if (fp8 == 2) return kv8tc_offset(t, d, is_v);
   const uint32_t off = is_v ? v_offset(dp, t, d) : k_offset(dp, t, d);
   return fp8 ? off >> 1 : off;
 }

@@ -124,7 +124,7 @@ cudaError_t launch_argmax_finish(const unsigned long long* best, int batch, int*
 __device__ __forceinline__ uint8_t* kv_elem_ptr(uint8_t* kv, long long g, int b, int h, int d,
                                                 int is_v, int batch, int kvh_per_slot, int kvp,
                                                 int chunk, int dp, int page_cap, int slot_base,
-                                                int n_local_slots, bool fp8) {
+                                                int n_local_slots, int fp8) {
   const int rank = rr_rank(g, chunk, kvp);
   const long long row = rr_row(g, chunk, kvp);
   const int grp = h / kvh_per_slot, kvh = h - grp * kvh_per_slot;
@@ -140,7 +140,7 @@ __device__ __forceinline__ uint8_t* kv_elem_ptr(uint8_t* kv, long long g, int b,
 __global__ void kv_append_rows_kernel(uint8_t* kv, const void* k_rows, const void* v_rows,
                                       int n, int b, const int* total, int batch, int kv_heads,
                                       int kvh_per_slot, int kvp, int chunk, int head_dim, int dp,
-                                      int page_cap, int slot_base, int n_local_slots, bool fp8) {
+                                      int page_cap, int slot_base, int n_local_slots, int fp8) {
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
   const long long per_tok = static_cast<long long>(kv_heads) * head_dim;
   if (idx >= n * per_tok) return;
@@ -167,7 +167,7 @@ __global__ void add_total_kernel(int* total, int b, int n) { total[b] += n; }
 cudaError_t launch_kv_append_rows(uint8_t* kv, const void* k_rows, const void* v_rows,
                                   int n, int b, int* total, int batch, int kv_heads,
                                   int kvh_per_slot, int kvp, int chunk, int head_dim, int dp,
-                                  int page_cap, int slot_base, int n_local_slots, bool fp8,
+                                  int page_cap, int slot_base, int n_local_slots, int fp8,
                                   cudaStream_t stream) {
   const long long work = static_cast<long long>(n) * kv_heads * head_dim;
   if (work > 0) {
@@ -200,7 +200,7 @@ __device__ __forceinline__ uint16_t hash_bf16_bits(uint64_t sseed, uint64_t inde
 __global__ void kv_fill_hash_kernel(uint8_t* kv, const int* total, int batch, int kv_heads,
                                     int kvh_per_slot, int kvp, int chunk, int head_dim, int dp,
                                     int page_cap, int slot_base, int n_local_slots, long long n,
-                                    uint64_t seed, uint64_t stream_k, uint64_t stream_v, bool fp8) {
+                                    uint64_t seed, uint64_t stream_k, uint64_t stream_v, int fp8) {
   const long long warp = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   const long long streams = static_cast<long long>(n_local_slots) * batch * kvh_per_slot;
@@ -230,7 +230,10 @@ __global__ void kv_fill_hash_kernel(uint8_t* kv, const int* total, int batch, in
     uint4 old = full ? make_uint4(0, 0, 0, 0) : (fp8 ? make_uint4(dst8->x, dst8->y, 0, 0) : *dst);
     uint16_t* ov = reinterpret_cast<uint16_t*>(&old);
     uint8_t* ov8 = reinterpret_cast<uint8_t*>(&old);
-    const int is_v = ci >= chunks / 2;
+    // tensor-core FP8 layout (fp8 == 2, kv_layout.cuh kv8tc_offset): a chunk is
+    // 8 dims of one token (K) or 8 tokens of one dim (V)
+    const int tco = ci * 8 & 2047, tch = ci * 8 >> 11;
+    const int is_v = fp8 == 2 ? tco >= 1024 : ci >= chunks / 2;
     const int cl = is_v ? ci - chunks / 2 : ci;
     const int ln = cl & 31, grpi = cl >> 5;
     const int g = ln >> 2, c = ln & 3;
@@ -239,7 +242,15 @@ __global__ void kv_fill_hash_kernel(uint8_t* kv, const int* total, int batch, in
       // e = sub*4 + half*2 + elem  (see kv_layout.cuh)
       const int sub = e >> 2, half = (e >> 1) & 1, elem = e & 1;
       int t, d;
-      if (!is_v) {  // grpi = nt*(dp/32) + kp
+      if (fp8 == 2) {
+        if (!is_v) {
+          t = tch * 8 + ((tco & 127) >> 4);
+          d = (tco >> 7) * 16 + (tco & 15) + e;
+        } else {
+          t = tch * 8 + e;
+          d = (tco - 1024) >> 3;
+        }
+      } else if (!is_v) {  // grpi = nt*(dp/32) + kp
         const int nt = grpi / (dp / 32), kp = grpi % (dp / 32);
         t = nt * 8 + g;
         d = (2 * kp + sub) * 16 + half * 8 + 2 * c + elem;
@@ -406,7 +417,7 @@ __global__ void add_total_all_kernel(int* total, int batch, int n) {
 cudaError_t launch_kv_fill_hash(uint8_t* kv, int* total, int batch, int kv_heads,
                                 int kvh_per_slot, int kvp, int chunk, int head_dim, int dp,
                                 int page_cap, int slot_base, int n_local_slots, long long n,
-                                uint64_t seed, uint64_t stream_k, uint64_t stream_v, bool fp8,
+                                uint64_t seed, uint64_t stream_k, uint64_t stream_v, int fp8,
                                 cudaStream_t stream) {
   const long long work = static_cast<long long>(n_local_slots) * batch * kvh_per_slot * page_cap * 32;
   if (n > 0)

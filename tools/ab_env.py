@@ -24,10 +24,13 @@ def main():
     ap.add_argument("--w", default="bf16")
     ap.add_argument("--rounds", type=int, default=6)
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--g16", action="store_true", help="the C3 per-GPU attention shape: 128 query / 8 KV heads")
     a = ap.parse_args()
     import torch
     import paper_2507_07120_b200 as P
     spec = P.model.PRESETS["llama3-8b-like"]
+    if a.g16:
+        spec = P.model.ModelSpec("g16", 1, 16384, 128, 8, 128, 1024, 3, "gqa", 0, vocab=4096)
     B = 8
     engines = []
     for v in ("0", a.value):

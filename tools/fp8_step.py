@@ -19,9 +19,12 @@ def main():
     ap.add_argument("--kv", default="fp8")
     ap.add_argument("--w", default="fp8")
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--g16", action="store_true", help="405B-like attention shard: 128 query / 8 KV heads (G = 16)")
     a = ap.parse_args()
     import paper_2507_07120_b200 as P
     spec = P.model.PRESETS["llama3-8b-like"]
+    if a.g16:  # the C3 per-GPU attention shape (one GPU of KVP = 8: 8 KV heads, G = 16), small FFN
+        spec = P.model.ModelSpec("g16", 1, 16384, 128, 8, 128, 1024, 3, "gqa", 0, vocab=4096)
     B = 8
     eng = P.HelixDecoder(spec, tpa=1, kvp=1, batch=B, capacity=a.context + 64, layers=a.layers,
                          kv_dtype=a.kv, w_dtype=a.w)
