@@ -89,9 +89,11 @@ typedef struct hx_runtime_config {
   int32_t use_graphs;       /* capture the decode step in a CUDA graph */
   int32_t kv_dtype;         /* KV page storage: HX_KV_BF16, or HX_KV_FP8_E4M3 (GQA; e4m3 RNE,
                                saturating at +-448, unit scale -- SURVEY 8f rank 2) */
-  int32_t w_dtype;          /* GEMV weight storage: HX_W_BF16, or HX_W_FP8_E4M3 (dense GQA models,
-                               batch <= 16, hash init; e4m3 with a power-of-two scale per output
-                               feature, applied in the GEMV epilogue -- SURVEY 8f rank 2) */
+  int32_t w_dtype;          /* GEMV weight storage: HX_W_BF16, HX_W_FP8_E4M3 (batch <= 16, hash init;
+                               e4m3 with a power-of-two scale per output feature, applied in the
+                               GEMV epilogue -- SURVEY 8f rank 2) or HX_W_FP4_E2M1 (batch <= 16,
+                               hash init; e2m1 in MX-style blocks of 32 inputs per output feature
+                               with a power-of-two scale -- the paper's FP4) */
   int32_t reserved;
 } hx_runtime_config;
 
@@ -102,6 +104,7 @@ typedef struct hx_runtime_config {
                             (MX-style blocks; head_size 32/64/128) -- the paper's FP4 */
 #define HX_W_BF16 0
 #define HX_W_FP8_E4M3 1
+#define HX_W_FP4_E2M1 2
 
 typedef struct hx_engine_info {
   int64_t kv_bytes_per_layer;      /* resident KV pool bytes on this device, per layer */
@@ -112,7 +115,7 @@ typedef struct hx_engine_info {
   int64_t page_cap;
   int64_t head_dim_padded;
   int64_t kv_dtype;                /* HX_KV_BF16 / HX_KV_FP8_E4M3 */
-  int64_t w_dtype;                 /* HX_W_BF16 / HX_W_FP8_E4M3 */
+  int64_t w_dtype;                 /* HX_W_BF16 / HX_W_FP8_E4M3 / HX_W_FP4_E2M1 */
   int64_t comm_ranks;              /* ranks of the pool's world communicator (1: local pool) */
   int64_t nccl_version;            /* ncclGetVersion of the linked NCCL (0: no NCCL pool) */
   int64_t exchange;                /* KVP fragment exchange: HX_EXCHANGE_* (distributed pools) */

@@ -35,6 +35,17 @@ void quantize_fp8_cols(Mat& m) {
   }
 }
 
+void quantize_fp4_cols(Mat& m) {
+  double blk[32];
+  for (i64 c = 0; c < m.cols; ++c)
+    for (i64 r0 = 0; r0 < m.rows; r0 += 32) {
+      const i64 n = std::min<i64>(32, m.rows - r0);
+      for (i64 i = 0; i < n; ++i) blk[i] = m(r0 + i, c);
+      round_e2m1_block(blk, n);
+      for (i64 i = 0; i < n; ++i) m(r0 + i, c) = blk[i];
+    }
+}
+
 Mat hash_matrix_fp8(std::uint64_t seed, HashKind kind, i64 layer, i64 rows, i64 cols, double scale) {
   Mat m = hash_matrix(seed, kind, layer, rows, cols, scale, false);
   quantize_fp8_cols(m);
@@ -76,9 +87,14 @@ ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, st
   const i64 W = mla ? mla_width(d.kv_latent) : 0, DV = mla ? mla_value_width(d.kv_latent) : 0;
   const double sh = 1.0 / std::sqrt(static_cast<double>(d.hidden));
   const double sf = 1.0 / std::sqrt(static_cast<double>(std::max<i64>(d.ffn, 1)));
-  if (d.w_fp8 && qkv_init != QkvInit::Hash)
-    throw std::invalid_argument("FP8 weights: hash-initialised weights");
+  if ((d.w_fp8 || d.w_fp4) && qkv_init != QkvInit::Hash)
+    throw std::invalid_argument("FP8 / FP4 weights: hash-initialised weights");
   auto wmat = [&](HashKind kind, i64 l, i64 rows, i64 cols, double sc) {
+    if (d.w_fp4) {
+      Mat m = hash_matrix(seed, kind, l, rows, cols, sc, false);
+      quantize_fp4_cols(m);
+      return m;
+    }
     return d.w_fp8 ? hash_matrix_fp8(seed, kind, l, rows, cols, sc) : hash_matrix(seed, kind, l, rows, cols, sc, bf16);
   };
   h_.reserve(static_cast<std::size_t>(d.layers * batch));
@@ -125,9 +141,10 @@ ModelOracle::ModelOracle(ModelDims d, i64 tpa, i64 kvp, i64 chunk, i64 batch, st
           for (i64 r = 0; r < rows; ++r)
             for (i64 c = 0; c < cols; ++c) {
               const double v = hash_unit(seed, st, static_cast<std::uint64_t>(r * cols + c)) * sc;
-              m(r, c) = (bf16 && !d.w_fp8) ? round_bf16(v) : v;
+              m(r, c) = (bf16 && !d.w_fp8 && !d.w_fp4) ? round_bf16(v) : v;
             }
           if (d.w_fp8) quantize_fp8_cols(m);
+          if (d.w_fp4) quantize_fp4_cols(m);
           return m;
         };
         eg_.back().push_back(em(kEgate, d.hidden, d.expert_ffn, sh));

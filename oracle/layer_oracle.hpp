@@ -68,6 +68,11 @@ struct ModelDims {
   // power-of-two per-output scale s_n = 2^ceil(log2(max_k |W[k][n]| / 448));
   // the embedding (a gather) and the MLA per-head absorptions W_UK / W_UV stay bf16.
   bool w_fp8 = false;
+  // FP4 weights (the paper's setting; hash init): every GEMV
+  // weight column n is stored in MX-style e2m1 blocks of 32 consecutive inputs k
+  // (k0 = 32 i) sharing a power-of-two scale -- round_e2m1_block (helix_oracle.hpp)
+  // over W[k0 .. k0+31][n]; same exclusions as w_fp8.
+  bool w_fp4 = false;
 };
 
 // MLA attention in the weight-absorbed decode form (types.hpp:37-49: K_eff = 1,
@@ -160,6 +165,8 @@ Mat hash_matrix(std::uint64_t seed, HashKind kind, i64 layer, i64 rows, i64 cols
 // power-of-two scale (ModelDims::w_fp8).
 Mat hash_matrix_fp8(std::uint64_t seed, HashKind kind, i64 layer, i64 rows, i64 cols, double scale);
 double fp8_pow2_scale(double absmax);
+// ModelDims::w_fp4: e2m1 blocks of 32 along the rows (inputs k) of every column.
+void quantize_fp4_cols(Mat& m);
 void quantize_fp8_cols(Mat& m);  // per column: e4m3(m / s_c) * s_c
 std::vector<double> rmsnorm(const std::vector<double>& x, double eps = 1e-5);
 

@@ -220,6 +220,23 @@ int oracle_model_create_w8(i64 hidden, i64 q, i64 k, i64 hsz, i64 ffn, i64 layer
   });
 }
 
+// Any model (dense, MoE and/or MLA as oracle_model_create_ex) with FP8 (wq = 1)
+// or FP4 (wq = 2) GEMV weights.
+int oracle_model_create_wq(i64 hidden, i64 q, i64 k, i64 hsz, i64 ffn, i64 layers, i64 vocab, i64 n_experts,
+                           i64 top_k, i64 expert_ffn, i64 kv_latent, i64 tpa, i64 kvp, i64 chunk, i64 batch,
+                           std::uint64_t seed, int wq, void** out) {
+  return guard([&] {
+    ModelDims d{hidden, q, k, hsz, ffn, layers, vocab};
+    d.n_experts = n_experts;
+    d.top_k = top_k;
+    d.expert_ffn = expert_ffn;
+    d.kv_latent = kv_latent;
+    d.w_fp8 = wq == 1;
+    d.w_fp4 = wq == 2;
+    *out = new ModelOracle(d, tpa, kvp, chunk, batch, seed, QkvInit::Hash, true);
+  });
+}
+
 // Any model (MoE and/or MLA as oracle_model_create_ex) with FP8 GEMV weights.
 int oracle_model_create_ex_w8(i64 hidden, i64 q, i64 k, i64 hsz, i64 ffn, i64 layers, i64 vocab, i64 n_experts,
                               i64 top_k, i64 expert_ffn, i64 kv_latent, i64 tpa, i64 kvp, i64 chunk, i64 batch,

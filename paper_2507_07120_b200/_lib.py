@@ -35,7 +35,7 @@ class RuntimeConfig(C.Structure):
 
 
 KV_DTYPES = {"bf16": 0, "fp8": 1, "fp8_e4m3": 1, "f64": 2, "fp4": 3, "fp4_e2m1": 3}
-W_DTYPES = {"bf16": 0, "fp8": 1, "fp8_e4m3": 1}
+W_DTYPES = {"bf16": 0, "fp8": 1, "fp8_e4m3": 1, "fp4": 2, "fp4_e2m1": 2}
 
 
 class EngineInfo(C.Structure):

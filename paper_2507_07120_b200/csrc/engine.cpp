@@ -143,9 +143,11 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
   if (kv4_ && mla_) throw std::invalid_argument("FP4 KV pages are implemented for GQA caches (MLA latents stay bf16)");
   if (kv4_ && m.head_size != 32 && m.head_size != 64 && m.head_size != 128)
     throw std::invalid_argument("FP4 KV blocks are 32 dims: head_size must be 32, 64 or 128");
-  if (rt.w_dtype != HX_W_BF16 && rt.w_dtype != HX_W_FP8_E4M3) throw std::invalid_argument("unknown w_dtype");
+  if (rt.w_dtype != HX_W_BF16 && rt.w_dtype != HX_W_FP8_E4M3 && rt.w_dtype != HX_W_FP4_E2M1)
+    throw std::invalid_argument("unknown w_dtype");
   w8_ = rt.w_dtype == HX_W_FP8_E4M3;
-  if (w8_ && B_ > 16) throw std::invalid_argument("FP8 weights run the mma.sync GEMV: batch <= 16");
+  w4_ = rt.w_dtype == HX_W_FP4_E2M1;
+  if ((w8_ || w4_) && B_ > 16) throw std::invalid_argument("FP8 / FP4 weights run the mma.sync GEMV: batch <= 16");
   if (mla_) {
     // types.hpp:43-49: MLA keeps one latent KV head; Helix needs tpa <= K_eff = 1 (types.cpp:122-139)
     W_ = static_cast<int>(2 * m.kv_latent);
@@ -503,6 +505,10 @@ void Engine::plan_gemvs() {
     while (kr > 8 && (!tc_ || (kr / 2) % 4 == 0) && (kst + kr / 2 - 1) / (kr / 2) <= max_ks &&
            static_cast<int64_t>(tile_blks) * groups * ((kst + kr - 1) / kr) < target)
       kr /= 2;
+    if (w4_) {  // FP4 weights stream in 32-input blocks (2 k-steps): even chunks
+      if (K % 32) throw std::invalid_argument("FP4 weights: GEMV input widths must be multiples of 32");
+      kr += kr & 1;
+    }
     const int ksplit = (kst + kr - 1) / kr;
     p.ksplit = ksplit;
     p.kr_steps = kr;
@@ -513,7 +519,7 @@ void Engine::plan_gemvs() {
     p.head_dim = static_cast<int>(D_);
     p.dp = DP_;
     p.tc = tc_ ? 1 : 0;
-    p.w8 = w8_ ? 1 : 0;  // wscale is wired by the weight init
+    p.w8 = w4_ ? 2 : (w8_ ? 1 : 0);  // FP8: wscale is wired by the weight init
     p.xf16 = xf16_();
     p.prefetch_stages = 4;  // weight stages before griddepcontrol.wait; HX_GEMV_PREFETCH: A/B experiments
     if (const char* e = std::getenv("HX_GEMV_PREFETCH")) p.prefetch_stages = std::atoi(e);
@@ -577,7 +583,7 @@ void Engine::plan_gemvs() {
         p.tiles_per_group = p.n_tiles;
         p.n_groups_max = G;
         p.group_base = e_begin_;
-        p.w_group_stride = static_cast<long long>(p.Npad) * p.K * (w8_ ? 1 : 2);
+        p.w_group_stride = static_cast<long long>(weight_bytes(p.Npad, p.K));
         p.part_group_stride = static_cast<long long>(p.ksplit) * B_ * p.Npad;
         p.n_experts = E;
       }
@@ -643,16 +649,17 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
   const int F = F_local_, f0 = dist ? rank_ * F_local_ : 0;
   const int v0 = dist ? rank_ * V_local_ : 0;
   const int vrows = static_cast<int>(std::min<int64_t>(V_local_, V_ - v0));
-  const size_t wdiv = w8_ ? 16 : 8;  // weight elements per uint4
-  auto walloc = [&](const GemvPlan& g) {
-    return dalloc<uint4>(static_cast<size_t>(g.p.Npad) * g.p.K / (w8_ ? 16 : 8), "weights");
-  };
+  auto wchunks = [&](const GemvPlan& g) { return weight_bytes(g.p.Npad, g.p.K) / 16; };  // uint4 per matrix
+  auto walloc = [&](const GemvPlan& g) { return dalloc<uint4>(wchunks(g), "weights"); };
   // k_full: the input width of the whole (unsharded) matrix -- FP8 scales span it
   // (grouped expert blocks pass their slice of one [E_local][Npad] scale array)
   auto init = [&](uint4* w, GemvPlan& g, const std::vector<WSeg>& segs, int k_full, float* sc_slice = nullptr) {
     cuda_check(cudaMemcpyAsync(d_segs_, segs.data(), segs.size() * sizeof(WSeg), cudaMemcpyHostToDevice,
                                stream_), "segs");
-    if (w8_) {
+    if (w4_) {  // e2m1 blocks of 32 inputs with their scales inline (gemv.cu FP4 tile image)
+      cuda_check(launch_weight_init_hash_w4(reinterpret_cast<uint8_t*>(w), g.p.Npad, g.p.K, d_segs_,
+                                            static_cast<int>(segs.size()), seed, stream_), "weight init");
+    } else if (w8_) {
       float* sc = sc_slice;
       if (!sc) {
         float*& slot = wscale_[w];
@@ -728,8 +735,8 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
       GemvPlan& dn = plan_edown_[l];
       if (w_router_.size() <= static_cast<size_t>(l)) {
         w_router_.push_back(walloc(r));
-        w_egu_.push_back(dalloc<uint4>(static_cast<size_t>(E_local_) * gu.p.Npad * gu.p.K / wdiv, "expert gate/up"));
-        w_edown_.push_back(dalloc<uint4>(static_cast<size_t>(E_local_) * dn.p.Npad * dn.p.K / wdiv, "expert down"));
+        w_egu_.push_back(dalloc<uint4>(static_cast<size_t>(E_local_) * wchunks(gu), "expert gate/up"));
+        w_edown_.push_back(dalloc<uint4>(static_cast<size_t>(E_local_) * wchunks(dn), "expert down"));
         if (w8_) {
           wscale_[w_egu_.back()] = dalloc<float>(static_cast<size_t>(E_local_) * gu.p.Npad, "expert scales");
           wscale_[w_edown_.back()] = dalloc<float>(static_cast<size_t>(E_local_) * dn.p.Npad, "expert scales");
@@ -740,11 +747,11 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
       init(w_router_[l], r, {{hash_stream(kWrouter, l), 0, E, E, 0, 0, sh, 0, 0}}, Hh);
       for (int el = 0; el < E_local_; ++el) {
         const int64_t e = e_begin_ + el;
-        init(w_egu_[l] + static_cast<size_t>(el) * gu.p.Npad * gu.p.K / wdiv, gu,
+        init(w_egu_[l] + static_cast<size_t>(el) * wchunks(gu), gu,
              {{expert_stream(kEgate, l, e), 0, gu.p.Npad, static_cast<int>(Fe_), fe0, 1, sh, 0, fe0 + Fe},
               {expert_stream(kEup, l, e), 0, gu.p.Npad, static_cast<int>(Fe_), fe0, 2, sh, 0, fe0 + Fe}}, Hh,
              w8_ ? wscale_[w_egu_[l]] + static_cast<size_t>(el) * gu.p.Npad : nullptr);
-        init(w_edown_[l] + static_cast<size_t>(el) * dn.p.Npad * dn.p.K / wdiv, dn,
+        init(w_edown_[l] + static_cast<size_t>(el) * wchunks(dn), dn,
              {{expert_stream(kEdown, l, e), 0, Hh, Hh, 0, 0, se, fe0, 0}}, static_cast<int>(Fe_),
              w8_ ? wscale_[w_edown_[l]] + static_cast<size_t>(el) * dn.p.Npad : nullptr);
       }
@@ -907,7 +914,7 @@ void Engine::upload_qkv_host(int64_t layer, const std::vector<double>& wq, const
   // wq [H x Q*Hsz], wk/wv [H x K*Hsz] row-major (reference orientation); this
   // device keeps all columns (local pool) or its TPA group's heads.
   const bool dist = dist_mode_ != HX_POOL_LOCAL;
-  if (w8_) throw std::invalid_argument("FP8 weights are hash-initialised (hx_init_weights_hash)");
+  if (w8_ || w4_) throw std::invalid_argument("FP8 / FP4 weights are hash-initialised (hx_init_weights_hash)");
   const GemvPlan& g = plan_qkv_[layer];
   const int K = g.p.K, kst = K / 16;
   const int Qall = static_cast<int>(Qh_ * D_), Kall = static_cast<int>(Kh_ * D_);
@@ -1835,10 +1842,9 @@ void Engine::read_kv_f64(int64_t layer, int64_t request, int64_t rank, int64_t h
 void Engine::info(hx_engine_info* o) const {
   std::memset(o, 0, sizeof(*o));
   o->kv_bytes_per_layer = static_cast<int64_t>(n_slots_) * B_ * kvh_per_slot_ * page_cap_ * page_bytes_;
-  const int64_t wel = w8_ ? 1 : 2;  // GEMV weight element bytes
-  int64_t wb = static_cast<int64_t>(plan_qkv_[0].p.Npad) * plan_qkv_[0].p.K * wel;
+  int64_t wb = static_cast<int64_t>(weight_bytes(plan_qkv_[0].p.Npad, plan_qkv_[0].p.K));
   if (mla_) wb += (Qh_ * D_ * W_ + static_cast<int64_t>(uv_heads_) * DV_ * D_) * 2;  // W_UK + W_UV
-  auto bytes = [wel](const GemvPlan& g) { return static_cast<int64_t>(g.p.Npad) * g.p.K * wel; };
+  auto bytes = [this](const GemvPlan& g) { return static_cast<int64_t>(weight_bytes(g.p.Npad, g.p.K)); };
   if (!attn_only_) {
     wb += bytes(plan_o_[0]);
     if (F_ > 0) wb += bytes(plan_gu_[0]) + bytes(plan_down_[0]);
@@ -1846,7 +1852,7 @@ void Engine::info(hx_engine_info* o) const {
       wb += bytes(plan_router_[0]) + static_cast<int64_t>(E_local_) * (bytes(plan_egu_[0]) + bytes(plan_edown_[0]));
   }
   o->weight_bytes_per_layer = wb;
-  o->head_bytes = attn_only_ ? 0 : static_cast<int64_t>(plan_lm_.p.Npad) * plan_lm_.p.K * wel + V_ * H_ * 2;
+  o->head_bytes = attn_only_ ? 0 : bytes(plan_lm_) + V_ * H_ * 2;
   o->attn_streams = n_streams_;
   o->attn_splits = live_splits(0, false);  // the plan the next batched launch of layer 0 uses
   o->attn_items = static_cast<int64_t>(n_streams_) * o->attn_splits;
@@ -1855,7 +1861,7 @@ void Engine::info(hx_engine_info* o) const {
   o->page_cap = page_cap_;
   o->head_dim_padded = DP_;
   o->kv_dtype = kv4_ ? HX_KV_FP4_E2M1 : (f64_ ? HX_KV_F64 : (kv8_ ? HX_KV_FP8_E4M3 : HX_KV_BF16));
-  o->w_dtype = w8_ ? HX_W_FP8_E4M3 : HX_W_BF16;
+  o->w_dtype = w4_ ? HX_W_FP4_E2M1 : (w8_ ? HX_W_FP8_E4M3 : HX_W_BF16);
   o->comm_ranks = transport_ ? transport_->world() : 1;
   o->nccl_version = transport_ ? transport_->nccl_version() : 0;
   o->exchange = dist_mode_ == HX_POOL_LOCAL ? HX_EXCHANGE_NONE

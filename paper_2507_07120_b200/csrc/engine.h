@@ -132,7 +132,14 @@ class Engine {
   double *d_out64_ = nullptr, *d_lse64_ = nullptr;
   F64HarnessParams f64_params(int64_t layer) const;
   void qkv_f64(int64_t layer, const double* x, int64_t x_len);
-  int xf16_() const { return w8_ ? 1 : 0; }  // x-fragments as f16 terms (xfrag.cuh)
+  bool w4_ = false;   // FP4 e2m1 GEMV weights: MX blocks of 32 inputs, pow2 scales inline (gemv.cu)
+  int xf16_() const { return (w8_ || w4_) ? 1 : 0; }  // x-fragments as f16 terms (xfrag.cuh)
+  // GEMV weight image bytes of an [Npad x K] matrix: bf16 2 B, e4m3 1 B, e2m1 17/32 B per
+  // element (per 128 rows x 32 inputs: 2 KB of codes + 128 exponent bytes)
+  size_t weight_bytes(int Npad, int K) const {
+    const size_t n = static_cast<size_t>(Npad) * static_cast<size_t>(K);
+    return w4_ ? n / 32 * 17 : (w8_ ? n : 2 * n);
+  }
   std::map<const void*, float*> wscale_;     // FP8 weight block -> its [Npad] scales
   int DP_, G_, q_rows_, q_chunks_, kvh_per_slot_, q_per_slot_, n_slots_, slot_base_;
   int page_cap_;

@@ -44,8 +44,11 @@ constexpr int kThreads = 256;     // consumer threads (+1 producer warp)
 constexpr int kStages = 4;        // ring depth (~150 KB in flight per SM)
 // k-steps per ring stage: 32 KB of weights (+ x slice) for B <= 16; fewer
 // k-steps when the x slice grows with the batch (B <= 64) so 4 stages fit.
-template <int NB8, bool W8 = false>
-constexpr int stage_steps() { return W8 ? (NB8 == 1 ? 8 : 4) : (NB8 <= 2 ? 8 : (NB8 <= 4 ? 4 : 2)); }
+// WQ: weight storage 0 bf16, 1 e4m3 (FP8), 2 e2m1 blocks (FP4; stages of whole 32-input pairs)
+template <int NB8, int WQ = 0>
+constexpr int stage_steps() { return WQ ? (NB8 == 1 ? 8 : 4) : (NB8 <= 2 ? 8 : (NB8 <= 4 ? 4 : 2)); }
+// weight bytes per k-step and 128 rows (FP4: 2176 B per pair of k-steps)
+__host__ __device__ constexpr uint32_t weight_step_bytes(int wq) { return wq == 2 ? 1088u : (wq ? 2048u : 4096u); }
 constexpr int kDone = -1;
 
 struct TileMeta {
@@ -70,20 +73,40 @@ __device__ __forceinline__ unsigned long long logit_key(float v, int n) {
   return (static_cast<unsigned long long>(u) << 32) | (0xFFFFFFFFu - static_cast<unsigned>(n));
 }
 
-__host__ __device__ __forceinline__ int stage_steps_rt(int nb8, bool w8) {
-  return w8 ? (nb8 == 1 ? 8 : 4) : (nb8 <= 2 ? 8 : (nb8 <= 4 ? 4 : 2));
+__host__ __device__ __forceinline__ int stage_steps_rt(int nb8, int wq) {
+  return wq ? (nb8 == 1 ? 8 : 4) : (nb8 <= 2 ? 8 : (nb8 <= 4 ? 4 : 2));
 }
-__host__ __device__ __forceinline__ size_t stage_bytes(int nb8, bool w8) {
-  return static_cast<size_t>(stage_steps_rt(nb8, w8)) * ((w8 ? 2048 : 4096) + xf_step_bytes(nb8));
+__host__ __device__ __forceinline__ size_t stage_bytes(int nb8, int wq) {
+  return static_cast<size_t>(stage_steps_rt(nb8, wq)) * (weight_step_bytes(wq) + xf_step_bytes(nb8));
+}
+// four e2m1 pairs (bytes 0..3 of w) -> f16x2 each, low nibble = first element
+__device__ __forceinline__ void e2m1x8_to_f16x2x4_w(uint32_t w, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                                     uint32_t& r3) {
+  asm("{\n .reg .b8 b0, b1, b2, b3;\n mov.b32 {b0, b1, b2, b3}, %4;\n"
+      " cvt.rn.f16x2.e2m1x2 %0, b0;\n cvt.rn.f16x2.e2m1x2 %1, b1;\n"
+      " cvt.rn.f16x2.e2m1x2 %2, b2;\n cvt.rn.f16x2.e2m1x2 %3, b3;\n}"
+      : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+      : "r"(w));
+}
+__device__ __forceinline__ uint32_t lds32_w(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint32_t hmul2_w(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("mul.rn.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
 }
 
 }  // namespace
 
-template <int NB8, int EM, int XS, bool NORM, bool W8>
+template <int NB8, int EM, int XS, bool NORM, int WQ>
 __global__ void __launch_bounds__(kThreads + 32, 1) gemv_kernel(const GemvParams p) {
   extern __shared__ __align__(128) uint8_t smem[];
-  constexpr int kStageSteps = stage_steps<NB8, W8>();
-  constexpr uint32_t WB = W8 ? 2048 : 4096;                   // weight bytes per k-step (128 rows)
+  constexpr bool W8 = WQ != 0;  // e4m3 or e2m1: f16 MMAs on the widened weights
+  constexpr int kStageSteps = stage_steps<NB8, WQ>();
+  constexpr uint32_t WB = weight_step_bytes(WQ);              // weight bytes per k-step (128 rows)
   constexpr size_t SW = kStageSteps * WB;                     // weight bytes per stage
   constexpr size_t SX = kStageSteps * kXfTerms * NB8 * 256;   // x-fragment bytes per stage
   constexpr size_t SB = SW + SX;
@@ -197,7 +220,28 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemv_kernel(const GemvParams
       const uint32_t xbase = ring_base + s * SB + SW + lane * 8;
 #pragma unroll
       for (int kk = 0; kk < kStageSteps; ++kk) {
-        if (W8 && kk < m.nks) {
+        if (WQ == 2 && kk < m.nks) {
+          // FP4: the lane's 8 codes (rows g / g+8, inputs 2c, 2c+1, 2c+8, 2c+9 -- the bf16
+          // chunk's order) widen exactly to f16 and take their block's 2^e (rows g, g+8)
+          const uint32_t pb = ring_base + s * SB + (kk >> 1) * 2176;
+          const uint32_t wv = lds32_w(pb + (kk & 1) * 1024 + warp * 128 + lane * 4);
+          const uint8_t* sc = ring + s * SB + (kk >> 1) * 2176 + 2048 + warp * 16 + (lane >> 2);
+          const uint32_t eg = sc[0], eg8 = sc[8];
+          const uint32_t sg = (eg << 10) | (eg << 26), sg8 = (eg8 << 10) | (eg8 << 26);
+          uint32_t a0, a1, a2, a3;
+          e2m1x8_to_f16x2x4_w(wv, a0, a1, a2, a3);
+          a0 = hmul2_w(a0, sg);
+          a1 = hmul2_w(a1, sg8);
+          a2 = hmul2_w(a2, sg);
+          a3 = hmul2_w(a3, sg8);
+#pragma unroll
+          for (int t = 0; t < XS; ++t)
+#pragma unroll
+            for (int bg = 0; bg < NB8; ++bg) {
+              const uint2 bx = lds64(xbase + ((kk * kXfTerms + t) * NB8 + bg) * 256);
+              mma_f16_16816(acc[t * NB8 + bg], a0, a1, a2, a3, bx.x, bx.y);
+            }
+        } else if (W8 && kk < m.nks) {
           const uint2 w8 = lds64(wbase + kk * WB);
           uint32_t a0, a1, a2, a3;
           e4m3x4_to_f16x2x2(w8.x, a0, a1);
@@ -529,11 +573,11 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
 
 size_t gemv_smem_bytes(const GemvParams& p) {
   const int nb8 = xf_nb8(p.batch);
-  return static_cast<size_t>(kStages) * stage_bytes(nb8, p.w8 != 0) + kStages * sizeof(TileMeta) +
+  return static_cast<size_t>(kStages) * stage_bytes(nb8, p.w8) + kStages * sizeof(TileMeta) +
          2 * kStages * 8 + 64;
 }
 
-template <int NB8, int EM, int XS, bool NORM, bool W8 = false>
+template <int NB8, int EM, int XS, bool NORM, int W8 = 0>
 static cudaError_t launch_t(const GemvParams& p, int grid, cudaStream_t stream) {
   const size_t smem = gemv_smem_bytes(p);
   if (!p.tc) {
@@ -564,9 +608,10 @@ static cudaError_t launch_t(const GemvParams& p, int grid, cudaStream_t stream) 
 template <int NB8>
 static cudaError_t dispatch_nb(const GemvParams& p, int norm, int em, int grid, cudaStream_t s) {
   if constexpr (NB8 <= 2) {
-    if (p.w8) {  // FP8 weights: two f16 activation terms (22 bits) serve every projection
-#define HX_CASE8(E, NORMV) \
-  if (em == E && (norm != 0) == NORMV) return launch_t<NB8, E, 2, NORMV, true>(p, grid, s);
+    if (p.w8) {  // FP8 / FP4 weights: two f16 activation terms (22 bits) serve every projection
+#define HX_CASE8(E, NORMV)                                                                       \
+  if (em == E && (norm != 0) == NORMV)                                                           \
+    return p.w8 == 2 ? launch_t<NB8, E, 2, NORMV, 2>(p, grid, s) : launch_t<NB8, E, 2, NORMV, 1>(p, grid, s);
       HX_CASE8(E_QKV, true)
       HX_CASE8(E_QKV, false)
       HX_CASE8(E_RESID, false)
@@ -596,7 +641,8 @@ static cudaError_t dispatch_nb(const GemvParams& p, int norm, int em, int grid, 
 cudaError_t launch_gemv(const GemvParams& p, int norm, int emode, int grid, cudaStream_t stream) {
   if (p.batch < 1 || p.batch > 64 || (p.K & 15) || (p.Npad % kRows)) return cudaErrorInvalidValue;
   if (p.tc && p.batch <= 16) return cudaErrorInvalidValue;  // tcgen05 path: N = 32 or 64 batch rows
-  if (p.w8 && (p.tc || p.batch > 16 || !p.wscale)) return cudaErrorInvalidValue;
+  if (p.w8 && (p.tc || p.batch > 16 || (p.w8 == 1 && !p.wscale) || (p.w8 == 2 && (p.K & 31))))
+    return cudaErrorInvalidValue;
   if (p.batch <= 8) return dispatch_nb<1>(p, norm, emode, grid, stream);
   if (p.batch <= 16) return dispatch_nb<2>(p, norm, emode, grid, stream);
   if (p.batch <= 32) return dispatch_nb<4>(p, norm, emode, grid, stream);

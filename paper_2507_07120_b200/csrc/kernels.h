@@ -209,8 +209,11 @@ struct GemvParams {
   const float* addend;       // optional [B][out_stride] added by E_RESID / E_STORE
   int* bump_total;           // optional [B]: token totals bumped by the epilogue (merge kernel skipped)
   int prefetch_stages;       // weight stages streamed before griddepcontrol.wait (<= ring depth)
-  // FP8 weights (B <= 16, ungrouped): w holds e4m3 bytes in the same tile order
-  // ([Npad/128][K/16][8][32 lanes][8 B]), wscale the per-output power-of-two scales
+  // FP8 weights (w8 = 1; B <= 16): w holds e4m3 bytes in the same tile order
+  // ([Npad/128][K/16][8][32 lanes][8 B]), wscale the per-output power-of-two scales.
+  // FP4 weights (w8 = 2; B <= 16): per (128-row block, pair of k-steps = 32 inputs)
+  // 2 x [8 n-tiles][32 lanes][4 B] e2m1 codes (nibbles in the bf16 chunk's element
+  // order) then 128 exponent bytes (e + 15, one per row), 2176 B; no wscale.
   int w8;
   const float* wscale;       // [Npad]
   int xf16;                  // xf_out written as two f16 terms (the next GEMV has FP8 weights)
@@ -275,6 +278,11 @@ cudaError_t launch_weight_init_hash(uint4* w, int Npad, int K, const WSeg* segs,
 // FP8 weights: per-output power-of-two scales over the full input range k_full, then the e4m3 image.
 cudaError_t launch_weight_init_hash_w8(uint8_t* w, float* scale, int Npad, int K, int k_full, const WSeg* segs,
                                        int nseg, uint64_t seed, cudaStream_t stream);
+// FP4 weights: e2m1 blocks of 32 inputs per output row with a power-of-two
+// scale (oracle quantize_fp4_cols), image per (128-row block, 32-input pair of
+// k-steps): 2 x 1 KB fragment-major codes + 128 exponent bytes (gemv.cu).
+cudaError_t launch_weight_init_hash_w4(uint8_t* w, int Npad, int K, const WSeg* segs, int nseg, uint64_t seed,
+                                       cudaStream_t stream);
 cudaError_t launch_emb_init_hash(uint16_t* emb, int vocab, int hidden, uint64_t seed,
                                  uint64_t stream_id, cudaStream_t stream);
 // Plain row-major bf16: w[i] = bf16(hash_unit(seed, stream_id, idx0 + i) * scale), i < n.

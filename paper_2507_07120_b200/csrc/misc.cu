@@ -564,6 +564,43 @@ cudaError_t launch_weight_init_hash_w8(uint8_t* w, float* scale, int Npad, int K
   return cudaGetLastError();
 }
 
+// FP4 weights: one thread per (output row n, 32-input block): the block's 32
+// values, its power-of-two scale (e2m1_block_exp: the oracle's round_e2m1_block)
+// and 16 code bytes at their fragment positions (a byte holds elements k, k+1
+// of one row: both nibbles from this thread) + the exponent byte.
+__global__ void weight_init_hash_w4_kernel(uint8_t* w, int Npad, int K, const WSeg* segs, int nseg, uint64_t seed) {
+  const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int kblocks = K >> 5;
+  if (idx >= static_cast<long long>(Npad) * kblocks) return;
+  const int n = static_cast<int>(idx % Npad), kb = static_cast<int>(idx / Npad);
+  double v[32];
+  double am = 0.0;
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    v[i] = wseg_value(segs, nseg, n, kb * 32 + i, seed);
+    am = fmax(am, fabs(v[i]));
+  }
+  const int ex = e2m1_block_exp(am);
+  const int nb = n >> 7, r = n & 127, warp = r >> 4, rr = r & 15, g = rr & 7, rowhalf = rr >> 3;
+  uint8_t* blk = w + (static_cast<size_t>(nb) * kblocks + kb) * 2176;
+#pragma unroll
+  for (int i = 0; i < 32; i += 2) {  // k = 32 kb + i: (k-step half, khalf, c) ; elements i, i+1 share a byte
+    const int sub = i >> 4, kk = i & 15, khalf = kk >> 3, c = (kk & 7) >> 1;
+    const int lane = g * 4 + c, reg = khalf * 2 + rowhalf;
+    blk[sub * 1024 + warp * 128 + lane * 4 + reg] =
+        static_cast<uint8_t>(e2m1_from_double(v[i], ex) | (e2m1_from_double(v[i + 1], ex) << 4));
+  }
+  blk[2048 + r] = static_cast<uint8_t>(ex + 15);
+}
+
+cudaError_t launch_weight_init_hash_w4(uint8_t* w, int Npad, int K, const WSeg* segs, int nseg, uint64_t seed,
+                                       cudaStream_t stream) {
+  const long long work = static_cast<long long>(Npad) * (K / 32);
+  weight_init_hash_w4_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(w, Npad, K, segs, nseg,
+                                                                                           seed);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_weight_init_hash(uint4* w, int Npad, int K, const WSeg* segs, int nseg,
                                     uint64_t seed, cudaStream_t stream, int tc) {
   const long long work = static_cast<long long>(Npad / 16) * (K / 16) * 32;

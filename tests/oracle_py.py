@@ -58,6 +58,7 @@ def lib():
             "oracle_model_create_moe": (C.c_int, [i64] * 14 + [u64, C.c_int, C.c_int, C.POINTER(vp)]),
             "oracle_model_create_ex": (C.c_int, [i64] * 15 + [u64, C.c_int, C.c_int, C.POINTER(vp)]),
             "oracle_model_create_w8": (C.c_int, [i64] * 11 + [u64, C.POINTER(vp)]),
+            "oracle_model_create_wq": (C.c_int, [i64] * 15 + [u64, C.c_int, C.POINTER(vp)]),
             "oracle_model_create_ex_w8": (C.c_int, [i64] * 15 + [u64, C.POINTER(vp)]),
             "oracle_model_routes": (C.c_int, [vp, ip]),
             "oracle_model_route_gaps": (C.c_int, [vp, dp]),
@@ -251,7 +252,7 @@ class Model:
 
     def __init__(self, hidden, q, k, hsz, ffn, layers, vocab, tpa=1, kvp=1, chunk=16, batch=1,
                  seed=0, qkv_hash=False, bf16=True, moe=None, kv_latent=0, kv_fp8=False, w_fp8=False,
-                 kv_fp4=False):
+                 kv_fp4=False, w_fp4=False):
         """moe = (n_experts, top_k, expert_ffn): every layer's FFN is routed MoE,
         `ffn` is then the shared expert width (0: none). kv_latent > 0: MLA
         attention with latent width 2*kv_latent (layer_oracle.hpp). w_fp8: e4m3
@@ -260,7 +261,12 @@ class Model:
         self.batch = batch
         self.moe = moe
         h = C.c_void_p()
-        if w_fp8 and (moe or kv_latent):
+        if w_fp4:
+            assert qkv_hash
+            m = moe or (0, 0, 0)
+            check(lib().oracle_model_create_wq(hidden, q, k, hsz, ffn, layers, vocab, m[0], m[1], m[2], kv_latent,
+                                               tpa, kvp, chunk, batch, seed, 2, C.byref(h)))
+        elif w_fp8 and (moe or kv_latent):
             assert qkv_hash
             m = moe or (0, 0, 0)
             check(lib().oracle_model_create_ex_w8(hidden, q, k, hsz, ffn, layers, vocab, m[0], m[1], m[2], kv_latent,

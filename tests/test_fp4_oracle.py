@@ -55,3 +55,22 @@ def test_e2m1_values_are_exact_in_f16():
     for e in range(-14, 14):
         v = GRID * 2.0 ** e
         np.testing.assert_array_equal(v.astype(np.float16).astype(np.float64), v)
+
+
+def test_fp4_weights_oracle_quantisation():
+    """ModelDims::w_fp4 (layer_oracle.cpp quantize_fp4_cols): every GEMV weight
+    column (output feature) n is stored in e2m1 blocks of 32 consecutive inputs
+    k = 32 i .. 32 i + 31 with a power-of-two block scale -- the same MX rounding
+    as the KV pages, checked here against the independent restatement over the
+    unquantised draws of the bf16=False oracle."""
+    H, Q, K, D, F, V = 64, 4, 2, 16, 96, 50
+    q4 = O.Model(H, Q, K, D, F, 1, V, seed=9, qkv_hash=True, w_fp4=True)
+    ref = O.Model(H, Q, K, D, F, 1, V, seed=9, qkv_hash=True, bf16=False)
+    for name in ("wq", "wk", "wv", "wo", "wgate", "wup", "wdown", "lm"):
+        w, w0 = q4.weight(name), ref.weight(name)
+        assert w.shape == w0.shape and w.shape[0] % 32 == 0
+        want = np.empty_like(w0)
+        for n in range(w0.shape[1]):
+            for k0 in range(0, w0.shape[0], 32):
+                want[k0:k0 + 32, n] = independent(w0[k0:k0 + 32, n])
+        np.testing.assert_array_equal(w, want)
