@@ -212,10 +212,10 @@ def pool_slice(a, preset, S, ep, w_dtype="bf16", kv_dtype="bf16"):
                          "t_roof_ms": max(kv_bytes / hbm / 1e6, flops / tc / 1e9),
                          "traffic": ncu_traffic("mla")}}
         out["moe"] = {"local_experts": spec.moe.total_experts // ep, "active_local_experts_last_step": active,
-                      "expert_bytes_streamed": active * 3 * H * spec.moe.expert_ffn_dim * (1 if w_dtype == "fp8" else 2)}
+                      "expert_bytes_streamed": active * 3 * H * spec.moe.expert_ffn_dim * W_ELEM_BYTES[w_dtype]}
     else:
         K = spec.kv_heads
-        ekv, ew = KV_ELEM_BYTES[kv_dtype], (1 if w_dtype == "fp8" else 2)
+        ekv, ew = KV_ELEM_BYTES[kv_dtype], W_ELEM_BYTES[w_dtype]
         # roofline.hpp:17-48: QKV duplicated per KVP rank, O and FFN sharded over N
         kv_bytes, w_bytes = step_bytes_per_gpu(spec, B, s_loc * N, N, 1, ekv, ew)
         out["workload"] = ("llama405b-like layer, one GPU of TPA=1 x KVP=8 (TPF=8): %d KV heads x %d tokens x B=%d; "
@@ -293,6 +293,7 @@ def kvp_slices(a):
     return out
 
 
+W_ELEM_BYTES = {"bf16": 2.0, "fp8": 1.0, "fp4": 17.0 / 32.0}  # fp4: e2m1 nibble + one exponent byte per 32 inputs
 KV_ELEM_BYTES = {"bf16": 2.0, "fp8": 1.0, "fp4": 17.5 / 32.0}  # fp4: e2m1 nibble + a K exponent byte / V f16 scale per 32
 KV_KERNEL = {"bf16": "attn_decode_kernel<128,7,3,1,bf16>", "fp8": "attn_decode_kernel<128,10,4,1,fp8>",
              "fp4": "attn_decode_kernel<128,10,6,1,fp4>"}
@@ -337,7 +338,7 @@ def fp8_kv_line(a, w_dtype="bf16", kv_dtype="fp8"):
     info = eng.info()
     eng.close()
     return {"kv_dtype": {"fp8": "fp8_e4m3", "fp4": "fp4_e2m1 (32-dim blocks, pow2 scales)"}[kv_dtype],
-            "w_dtype": "fp8_e4m3" if w_dtype == "fp8" else "bf16",
+            "w_dtype": {"fp8": "fp8_e4m3", "fp4": "fp4_e2m1 (32-input blocks, pow2 scales)"}.get(w_dtype, "bf16"),
             "weight_bytes_resident": info["weight_bytes_per_layer"] * L + info["head_bytes"], "ms_per_step": ms, "value": B / (ms * 1e-3), "unit": UNIT,
             "breakdown_ms": {k: float(v) for k, v in zip(
                 ["embed", "qkv", "attention", "split_reduce", "o_proj", "gate_up", "down", "lm_head", "merge"], prof)},
@@ -629,6 +630,10 @@ def ours(a):
             line["fp4_kv_fp8_w"] = fp8_kv_line(a, w_dtype="fp8", kv_dtype="fp4")
         except Exception as ex:  # reported, never fatal for the headline number
             line["fp4_kv_fp8_w"] = {"error": str(ex)[:300]}
+        try:  # the paper's setting: weights AND KV in FP4
+            line["fp4_kv_fp4_w"] = fp8_kv_line(a, w_dtype="fp4", kv_dtype="fp4")
+        except Exception as ex:  # reported, never fatal for the headline number
+            line["fp4_kv_fp4_w"] = {"error": str(ex)[:300]}
     if world == 1 and not a.no_slices:
         eng.close()  # free the 150 GB pool before the 8-GPU-pool slices
         try:
@@ -641,7 +646,9 @@ def ours(a):
                 ("llama405b_slice_fp8w", "llama405b-like", a.slice_context, 1, "fp8", "bf16"),
                 ("deepseek_slice_fp8w", "deepseek-r1-like", a.slice_context, 8, "fp8", "bf16"),
                 ("llama405b_slice_fp8", "llama405b-like", a.slice_context, 1, "fp8", "fp8"),
-                ("llama405b_slice_fp4", "llama405b-like", a.slice_context, 1, "fp8", "fp4")):
+                ("llama405b_slice_fp4", "llama405b-like", a.slice_context, 1, "fp8", "fp4"),
+                ("llama405b_slice_fp4w", "llama405b-like", a.slice_context, 1, "fp4", "fp4"),
+                ("deepseek_slice_fp4w", "deepseek-r1-like", a.slice_context, 8, "fp4", "bf16")):
             try:
                 line[key] = pool_slice(a, preset, ctx, ep, wd, kd)
                 line[key]["w_dtype"] = wd

@@ -68,7 +68,9 @@ def hopb(path, out):
         if abs(r["exposed_a2a_ms_off"] - r["a2a_ms_modeled"]) < 1e-12:
             r["exposed_a2a_ms_off"] += r["flag_wait_ms_off"]
             r["hopb_gain_ms"] = (r["attn_ms_off"] + r["exposed_a2a_ms_off"]) - (r["attn_ms_on"] + r["exposed_a2a_ms_on"])
-    lines = ["| KVP | context | B | KV tok/GPU | attn+reduce off (ms) | attn, in-kernel push on (ms) | layer off (ms) | "
+    on_hdr = "attn + stream reducer on (ms, serialised)" if any("attn_kernel_ms_on" in r for r in ok) \
+        else "attn, in-kernel push on (ms)"
+    lines = [f"| KVP | context | B | KV tok/GPU | attn+reduce off (ms) | {on_hdr} | layer off (ms) | "
              "layer on (ms) | a2a modeled (us) | exposed off (us) | exposed on (us) | hidden | HOP-B net (us) |",
              "|---|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in ok:
