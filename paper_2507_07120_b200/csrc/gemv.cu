@@ -584,10 +584,12 @@ static cudaError_t launch_t(const GemvParams& p, int grid, cudaStream_t stream) 
     cudaError_t e = smem_optin<gemv_kernel<NB8, EM, XS, NORM, W8>>(smem);
     if (e != cudaSuccess) return e;
   }
-  // FP8 weights: the consumer's per-k-step chain (e4m3 widening + 2 MMAs) is
-  // latency-bound at 8 warps per SM, so two CTAs per SM (half-size ring stages)
-  static const int w8_ctas = std::getenv("HX_W8_CTAS") ? std::atoi(std::getenv("HX_W8_CTAS")) : 2;
-  const int g = W8 ? grid * w8_ctas : grid;
+  // FP8 / FP4 weights: the consumer's per-k-step chain (widening (+ block scale)
+  // + 2 MMAs) is latency-bound at 8 warps per SM, so two (e4m3) or three (e2m1,
+  // smaller stages) CTAs per SM: FP4 step -3.8% vs two, FP8 best at two
+  // (tools/time_step.py across processes, HX_W8_CTAS)
+  static const int w8_ctas = std::getenv("HX_W8_CTAS") ? std::atoi(std::getenv("HX_W8_CTAS")) : 0;
+  const int g = W8 ? grid * (w8_ctas > 0 ? w8_ctas : (W8 == 2 ? 3 : 2)) : grid;
   cudaError_t e = p.tc ? launch_gemv_tc(p, NB8, XS, grid, stream)
                        : launch_k(gemv_kernel<NB8, EM, XS, NORM, W8>, dim3(g), dim3(kThreads + 32), smem, stream, p);
   if (e != cudaSuccess) return e;
