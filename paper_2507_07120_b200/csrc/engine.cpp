@@ -470,7 +470,10 @@ void Engine::alloc() {
 void Engine::plan_gemvs() {
   one_src_merge_ = dist_mode_ == HX_POOL_LOCAL && !mla_ && !attn_only_ && kvp_ == 1 &&
                    !(std::getenv("HX_ONE_SRC_MERGE") && std::getenv("HX_ONE_SRC_MERGE")[0] == '0');
-  d_plan_ctr_ = dalloc<int>(static_cast<size_t>(2 * (7 * L_ + 2)), "plan counters");
+  // fused LSE combine in the O-projection (GQA; the tcgen05 GEMV and MLA keep the merge kernel)
+  fused_combine_ = !mla_ && !attn_only_ && !tc_ && !one_src_merge_ &&
+                   !(std::getenv("HX_FUSED_COMBINE") && std::getenv("HX_FUSED_COMBINE")[0] == '0');
+  d_plan_ctr_ = dalloc<int>(static_cast<size_t>(2 * (7 * L_ + 2) + L_), "plan counters");
   int plan_idx = 0;
   // groups: expected concurrent weight blocks (MoE: active experts) for tile sizing
   auto make = [&](int N, int Npad, int K, int norm, int em, int groups = 1) {
@@ -632,10 +635,10 @@ int64_t Engine::launches_per_step() const {
   const int64_t head = 1 + 3;                              // embed; LM head x2 + argmax finish
   const int64_t mla_k = mla_ ? 2 : 0;                      // W_UK absorption, W_UV
   if (dist_mode_ == HX_POOL_LOCAL)
-    return head + L_ * (2 + 1 + sr + (one_src_merge_ ? 0 : 1) + mla_k + 2 + ffn_k);
+    return head + L_ * (2 + 1 + sr + (one_src_merge_ || fused_combine_ ? 0 : 1) + mla_k + 2 + ffn_k);
   const int64_t attn = device_exchange() ? (hopb_ && fused_ && hopb_inkernel_ ? 2 : 3)  // attention, reduce + push, flag wait
                                          : (hopb_ ? B_ : 1) * (2 + sr);  // [per request] attention, sr, pack
-  return head + L_ * (2 + attn + 1 + mla_k + 2 + 1 + ffn_k + 1);  // + merge, O x2, residual, FFN, residual
+  return head + L_ * (2 + attn + (fused_combine_ ? 0 : 1) + mla_k + 2 + 1 + ffn_k + 1);  // + merge, O x2, residual, FFN, residual
 }
 
 // ---------------------------------------------------------------------------
@@ -716,7 +719,7 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
       const int ko = !dist ? 0 : (mla_ ? uv_h0_ * static_cast<int>(D_) : grp_ * q_per_slot_ * AD_ + r_ * slice_);
       init(w_o_[l], plan_o_[l], {{hash_stream(kWo, l), 0, Hh, Hh, 0, 0, sh, ko, 0}}, Hh);
       plan_o_[l].p.w = w_o_[l];
-      plan_o_[l].p.bump_total = one_src_merge_ ? d_total_ + l * B_ : nullptr;
+      plan_o_[l].p.bump_total = (one_src_merge_ || fused_combine_) ? d_total_ + l * B_ : nullptr;
       if (F > 0) {
         init(w_gu_[l], plan_gu_[l],
              {{hash_stream(kWgate, l), 0, plan_gu_[l].p.Npad, static_cast<int>(F_), f0, 1, sh, 0, f0 + F},
@@ -795,6 +798,21 @@ void Engine::build_weights_common(uint64_t seed, bool qkv_hash) {
       o.out_stride = static_cast<int>(H_);
       o.ss_out = dist ? nullptr : d_ss_;
       o.xf_out = d_xf_resid_;
+      if (fused_combine_) {
+        o.merge = dist ? 1 : 2;
+        if (const char* e = std::getenv("HX_FUSED_COMBINE_DEBUG")) o.merge |= std::atoi(e);  // 4: no wait, 8: no merge (timing only)
+        o.merge_ctr = d_plan_ctr_ + 2 * (7 * L_ + 2) + l;
+        o.m_kvp = kvp_;
+        o.m_head_dim = AD_;
+        o.m_recv = d_recv_;
+        o.m_chunk = xchunk_;
+        o.m_slice = slice_;
+        o.m_rank = r_;
+        o.m_frag_o = d_frag_o_;
+        o.m_frag_lse = d_frag_lse_;
+        o.m_q_per_slot = q_per_slot_;
+        o.m_dp = ADP_;
+      }
       // the FFN's last GEMV writes the residual (local) or the TP partial (dist)
       float* ffn_out = dist ? d_parth_ : d_x_;
       float* ffn_ss = dist ? nullptr : d_ss_;
@@ -1511,7 +1529,7 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
     if (!dist) {
       // LSE-rescale combine of the KVP fragments -> O-proj activations (attention.hpp:118-175)
       // (a fused split+KVP merge kernel measured 0.2 ms/step slower than this pair)
-      if (!one_src_merge_)
+      if (!one_src_merge_ && !fused_combine_)
         cuda_check(launch_xprep_merge_local(d_frag_o_, d_frag_lse_, B_, q_per_slot_, kvp_, AD_, ADP_,
                                             static_cast<int>(Qh_) * AD_, d_xf_attn_, d_total_ + l * B_, stream_,
                                             mla_ ? d_att_ : nullptr, xf16_()),
@@ -1525,9 +1543,10 @@ void Engine::enqueue_decode(const int32_t* tokens_dev, int32_t* next_dev) {
     } else {
       // merge of the exchanged slices, then TP O-proj over this rank's slice and
       // AllReduce over the pool (latency.cpp:85-94)
-      cuda_check(launch_xprep_merge_recv(d_recv_, B_, kvp_, xchunk_, slice_, r_, AD_, d_xf_attn_,
-                                         d_total_ + l * B_, stream_, mla_ ? d_att_ : nullptr, xf16_()),
-                 "merge");
+      if (!fused_combine_)
+        cuda_check(launch_xprep_merge_recv(d_recv_, B_, kvp_, xchunk_, slice_, r_, AD_, d_xf_attn_,
+                                           d_total_ + l * B_, stream_, mla_ ? d_att_ : nullptr, xf16_()),
+                   "merge");
       if (mla_)
         cuda_check(launch_mla_uv(d_att_, w_uv_[l], B_, uv_heads_, static_cast<int>(D_), d_xf_attn_, stream_, xf16_()),
                    "mla uv");

@@ -124,6 +124,7 @@ class Engine {
   // writes the O-projection's x-fragments itself, the O-proj epilogue bumps
   // the token totals, and the merge kernel is not launched
   bool one_src_merge_ = false;
+  bool fused_combine_ = false;   // LSE combine fused into the O-projection GEMV (HX_FUSED_COMBINE=0: merge kernel)
   // exact fp64 harness (HX_KV_F64): fp64 shards, weights and projections (exact64.cu)
   bool f64_ = false;
   int64_t rows_cap64_ = 0;

@@ -33,6 +33,7 @@
 #include "common.cuh"
 #include "kernels.h"
 #include "kv_layout.cuh"
+#include "merge.cuh"
 #include "xfrag.cuh"
 
 namespace hx {
@@ -88,6 +89,63 @@ __device__ __forceinline__ void e2m1x8_to_f16x2x4_w(uint32_t w, uint32_t& r0, ui
       : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
       : "r"(w));
 }
+__device__ __forceinline__ int ld_acquire_gpu_i(const int* ptr) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(ptr) : "memory");
+  return v;
+}
+
+// Fused LSE combine (GemvParams::merge): the KVP fragments of each input element
+// merged in the reference's canonical order (merge.cuh merge_sources,
+// attention.hpp:90-137) -- the work xprep_merge_recv / xprep_merge_local do as a
+// separate kernel -- by the 256 consumer threads of every CTA, grid-strided,
+// written into p.xf; then a gpu-scope release of this CTA's share.
+template <int MAXK>
+__device__ __forceinline__ void merge_elems(const GemvParams& p) {
+  const long long n = static_cast<long long>(p.batch) * p.K;
+  uint8_t* xf = const_cast<uint8_t*>(p.xf);
+  for (long long i = static_cast<long long>(blockIdx.x) * kThreads + threadIdx.x; i < n;
+       i += static_cast<long long>(gridDim.x) * kThreads) {
+    const int b = static_cast<int>(i / p.K), k = static_cast<int>(i % p.K);
+    float lse[MAXK], o[MAXK];
+    if ((p.merge & 3) == 1) {  // received slices [src][b][chunk]: values, then the lse of every head the slice touches
+      const int first = (p.m_rank * p.m_slice) / p.m_head_dim;
+      const int head = (p.m_rank * p.m_slice + k) / p.m_head_dim;
+#pragma unroll
+      for (int r = 0; r < MAXK; ++r)
+        if (r < p.m_kvp) {
+          const float* src = p.m_recv + (static_cast<size_t>(r) * p.batch + b) * p.m_chunk;
+          lse[r] = src[p.m_slice + head - first];
+          o[r] = src[k];
+        }
+    } else {  // local fragments [grp * kvp + r][b][q][dp]
+      const int head = k / p.m_head_dim, d = k - head * p.m_head_dim;
+      const int grp = head / p.m_q_per_slot, qi = head - grp * p.m_q_per_slot;
+#pragma unroll
+      for (int r = 0; r < MAXK; ++r)
+        if (r < p.m_kvp) {
+          const size_t f = (static_cast<size_t>(grp * p.m_kvp + r) * p.batch + b) * p.m_q_per_slot + qi;
+          lse[r] = p.m_frag_lse[f];
+          o[r] = p.m_frag_o[f * p.m_dp + d];
+        }
+    }
+    xf_write(xf, xf_nb8(p.batch), b, k, merge_sources<MAXK>(lse, o, p.m_kvp), p.xf16);
+  }
+}
+__device__ void merge_prologue(const GemvParams& p) {
+  griddep_wait();  // the fragments / received slices come from the previous kernels
+  if (p.merge & 8) {
+  } else if (p.m_kvp <= 8)
+    merge_elems<8>(p);
+  else
+    merge_elems<kMaxKvp>(p);
+  // generic-proxy stores of p.xf -> the producers' bulk (async-proxy) reads, then the release
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __threadfence();
+  asm volatile("bar.sync 1, %0;" ::"r"(kThreads) : "memory");
+  if (threadIdx.x == 0) atomicAdd(p.merge_ctr, 1);
+}
+
 __device__ __forceinline__ uint32_t lds32_w(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -143,6 +201,8 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemv_kernel(const GemvParams
       auto flush_x = [&]() {
         griddep_wait();
         waited = true;
+        if (p.merge && !(p.merge & 4))  // every CTA's share of the fused LSE combine is in p.xf (see the consumers)
+          while (ld_acquire_gpu_i(p.merge_ctr) < static_cast<int>(gridDim.x)) __nanosleep(32);
         for (int i = 0; i < npend; ++i)
           bulk_g2s(ring + pend_stage[i] * SB + SW, pend_src[i], pend_bytes[i], &full[pend_stage[i]]);
         npend = 0;
@@ -207,6 +267,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemv_kernel(const GemvParams
     }
   } else {
     // ------------------------------------------------------------ consumers
+    if (p.merge) merge_prologue(p);  // fused LSE combine -> this GEMV's input fragments
     float acc[XS * NB8][4];
 #pragma unroll
     for (int j = 0; j < XS * NB8; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.f;
@@ -304,6 +365,7 @@ __global__ void __launch_bounds__(kThreads + 32, 1) gemv_kernel(const GemvParams
     if (atomicAdd(p.work_counter + 1, 1) == static_cast<int>(gridDim.x) - 1) {
       p.work_counter[0] = 0;  // every CTA drained the queue: reset for the next launch
       p.work_counter[1] = 0;
+      if (p.merge) *p.merge_ctr = 0;
       __threadfence();
     }
   }
@@ -590,6 +652,16 @@ static cudaError_t launch_t(const GemvParams& p, int grid, cudaStream_t stream) 
   // (tools/time_step.py across processes, HX_W8_CTAS)
   static const int w8_ctas = std::getenv("HX_W8_CTAS") ? std::atoi(std::getenv("HX_W8_CTAS")) : 0;
   const int g = W8 ? grid * (w8_ctas > 0 ? w8_ctas : (W8 == 2 ? 3 : 2)) : grid;
+  if (p.merge && p.tc) return cudaErrorInvalidValue;  // the tcgen05 GEMV has no merge prologue
+  if (p.merge) {
+    // the fused combine needs every CTA of the grid resident at once (CTAs wait
+    // for each other's share): refuse a grid that cannot be
+    int per_sm = 0, dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gemv_kernel<NB8, EM, XS, NORM, W8>, kThreads + 32, smem);
+    if (per_sm * sms < g) return cudaErrorCooperativeLaunchTooLarge;
+  }
   cudaError_t e = p.tc ? launch_gemv_tc(p, NB8, XS, grid, stream)
                        : launch_k(gemv_kernel<NB8, EM, XS, NORM, W8>, dim3(g), dim3(kThreads + 32), smem, stream, p);
   if (e != cudaSuccess) return e;

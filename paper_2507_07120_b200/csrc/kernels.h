@@ -217,6 +217,22 @@ struct GemvParams {
   int w8;
   const float* wscale;       // [Npad]
   int xf16;                  // xf_out written as two f16 terms (the next GEMV has FP8 weights)
+  // Fused LSE combine (the O-projection, north star item 2; attention.hpp:118-175):
+  // before its first x copy the GEMV's consumer warps merge the KVP fragments
+  // into this GEMV's own input fragments (xf, in the xf16 image the weights
+  // need), every CTA a slice, then raise merge_ctr; the producer streams weights
+  // meanwhile and issues the x copies once all CTAs have merged. 0: off,
+  // 1: received slices (distributed pools: merge_recv layout), 2: local fragments.
+  // Needs the whole grid resident (launch_gemv refuses otherwise) and p.tc == 0;
+  // the token-total bump of the skipped merge kernel moves to bump_total.
+  int merge;
+  const float* m_recv;        // merge 1: [kvp][B][xchunk] (slice values + lse slots)
+  int m_chunk, m_slice, m_rank;
+  const float* m_frag_o;      // merge 2: [slots][B][q_per_slot][dp]
+  const float* m_frag_lse;    // merge 2: [slots][B][q_per_slot]
+  int m_q_per_slot, m_dp;
+  int m_kvp, m_head_dim;
+  int* merge_ctr;             // arrivals (self-resetting)
 };
 cudaError_t launch_gemv(const GemvParams& p, int norm, int emode, int grid, cudaStream_t stream);
 // tcgen05 inner product for p.tc plans (gemv_tc.cu); the epilogue kernel is shared.

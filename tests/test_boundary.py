@@ -77,9 +77,13 @@ def test_large_batch_gemv_uses_tcgen05():
     fp4 = [f for f in att if "ELi2ELb" in f.split("\n", 1)[0]]
     assert any("ELi2ELb1E" in f.split("\n", 1)[0] for f in fp4)
     assert fp4 and all("F2FP.F16.E2M1.UNPACK_B" in f and "HMUL2" in f and "HMMA.16816.F32 " in f for f in fp4)
-    # FP8-weight GEMVs (template flag W8, last argument) widen e4m3 weights the same way
-    w8 = [f for f in funcs if f.startswith("_ZN2hx11gemv_kernel") and "Lb1EEEv" in f.split("\n", 1)[0]]
+    # FP8-weight GEMVs (template argument WQ = 1, last) widen e4m3 weights the same
+    # way; FP4-weight GEMVs (WQ = 2) widen e2m1 and apply the block scale (HMUL2)
+    gemv = [f for f in funcs if f.startswith("_ZN2hx11gemv_kernel")]
+    w8 = [f for f in gemv if "Li1EEEv" in f.split("\n", 1)[0]]
     assert w8 and all("F2FP.F16.E4M3.UNPACK_B" in f and "UBLKCP" in f for f in w8)
+    w4 = [f for f in gemv if "Li2EEEv" in f.split("\n", 1)[0]]
+    assert w4 and all("F2FP.F16.E2M1.UNPACK_B" in f and "HMUL2" in f and "UBLKCP" in f for f in w4)
 
 
 def test_ctypes_structs_match_c_header(tmp_path):

@@ -33,10 +33,10 @@ def test_loopback_pool_matches_oracle(tpa, kvp, hopb):
     o = O.Model(H, Q, K, D, F, L, V, tpa=tpa, kvp=kvp, chunk=16, batch=B, seed=4321, bf16=True)
     # launches per step (engine.cpp launches_per_step): embed + LM head x2 + argmax; per layer
     # QKV x2, attention [+ split reduce with the device push under HOP-B off], flag wait,
-    # merge, O x2, residual, gate/up x2, down x2, residual
+    # O x2 (the LSE combine fused into the O-projection GEMV), residual, gate/up x2, down x2, residual
     info = engines[0].info()
     assert info["exchange"] == (3 if hopb else 2)
-    assert info["kernels_per_step"] == 4 + L * (11 + 3)  # attention, split reduce or HOP-B stream reducer, flag wait
+    assert info["kernels_per_step"] == 4 + L * (10 + 3)  # attention, split reduce or HOP-B stream reducer, flag wait
     for e in engines:
         e.init_weights(4321, qkv="mt19937")
     for l in range(L):
