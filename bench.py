@@ -197,20 +197,26 @@ def pool_slice(a, preset, S, ep, w_dtype="bf16", kv_dtype="bf16"):
                 "down_or_down_combine", "lm_head", "merge"], prof)}}
     if mla:
         active = int(P.lib().hx_moe_active_experts(eng._h))
-        kv_bytes = B * s_loc * 576 * 2
+        f8 = kv_dtype == "fp8"
+        kv_bytes = B * s_loc * 576 * (1 if f8 else 2)
         flops = B * s_loc * Q * (576 + 512) * 2
         tc, tc_kind = peak_tensor()
+        if f8:  # kind::f8f6f4 issues at twice the kind::f16 rate (B200 dense fp8 = 2x bf16)
+            tc, tc_kind = 2 * tc, "2x " + tc_kind + " bf16 (fp8 rate)"
+
         out["workload"] = ("deepseek-r1-like layer, one GPU of KVP=8 x EP=8 (tpf=1): 128 heads x %d latent tokens x "
                            "B=%d; 32/256 experts top-8 + shared 2048/8; collectives off (1 GPU)" % (s_loc, B))
         out["mla_attention"] = {
-            "kernel": "mla_decode_kernel (tcgen05 cta_group::2 CTA pair, TMEM accumulators, 2-SM TMA)",
+            "kernel": ("mla_decode_kernel<fp8> (tcgen05 kind::f8f6f4 cta_group::2, e4m3 latents / q / P"
+                       if f8 else "mla_decode_kernel (tcgen05 cta_group::2 CTA pair") +
+                      ", TMEM accumulators, 2-SM TMA)",
             "launch_ms": att_ms, "algorithmic_kv_bytes": kv_bytes, "algorithmic_flops": flops,
             "roofline": {"bound": "tensor", "achieved": flops / (att_ms * 1e-3) / 1e12, "peak": tc,
                          "unit": "TFLOP/s", "frac": flops / (att_ms * 1e-3) / 1e12 / tc, "peak_kind": tc_kind,
                          "hbm_achieved_gbs": kv_bytes / (att_ms * 1e-3) / 1e9,
                          "hbm_frac": kv_bytes / (att_ms * 1e-3) / 1e9 / hbm,
                          "t_roof_ms": max(kv_bytes / hbm / 1e6, flops / tc / 1e9),
-                         "traffic": ncu_traffic("mla")}}
+                         "traffic": ncu_traffic("mla_fp8" if f8 else "mla")}}
         out["moe"] = {"local_experts": spec.moe.total_experts // ep, "active_local_experts_last_step": active,
                       "expert_bytes_streamed": active * 3 * H * spec.moe.expert_ffn_dim * W_ELEM_BYTES[w_dtype]}
     else:
@@ -648,7 +654,8 @@ def ours(a):
                 ("llama405b_slice_fp8", "llama405b-like", a.slice_context, 1, "fp8", "fp8"),
                 ("llama405b_slice_fp4", "llama405b-like", a.slice_context, 1, "fp8", "fp4"),
                 ("llama405b_slice_fp4w", "llama405b-like", a.slice_context, 1, "fp4", "fp4"),
-                ("deepseek_slice_fp4w", "deepseek-r1-like", a.slice_context, 8, "fp4", "bf16")):
+                ("deepseek_slice_fp4w", "deepseek-r1-like", a.slice_context, 8, "fp4", "bf16"),
+                ("deepseek_slice_fp8", "deepseek-r1-like", a.slice_context, 8, "fp8", "fp8")):
             try:
                 line[key] = pool_slice(a, preset, ctx, ep, wd, kd)
                 line[key]["w_dtype"] = wd

@@ -177,7 +177,7 @@ void ModelOracle::grow_hash(i64 layer, i64 request, i64 n) {
                 static_cast<std::uint64_t>(W) +
             static_cast<std::uint64_t>(dd);
         const double v = hash_unit(seed_, hash_stream(kCacheK, layer), idx);
-        row(0, dd) = bf16_ ? round_bf16(v) : v;
+        row(0, dd) = kv_fp8_ ? round_e4m3(v) : (bf16_ ? round_bf16(v) : v);
       }
       c.append_round_robin(row, row);
     }
@@ -257,6 +257,27 @@ std::vector<double> ModelOracle::attend_mla(i64 l, i64 b, const std::vector<doub
       for (i64 dd = 0; dd < hs; ++dd) acc += qn[static_cast<std::size_t>(h * hs + dd)] * wuk(h * hs + dd, j);
       q(h, j) = round_bf16(acc);
     }
+  if (kv_fp8_) {
+    // FP8 latents: the query image is e4m3 of q_h * 2^e_h, e_h the largest power
+    // of two keeping max |q_h| <= 448 (the GPU's absorb kernel, mla.cu Q8)
+    for (i64 h = 0; h < Qh; ++h) {
+      Mat qa(1, W);
+      double mx = 0.0;
+      for (i64 j = 0; j < W; ++j) {
+        double acc = 0.0;
+        for (i64 dd = 0; dd < hs; ++dd) acc += qn[static_cast<std::size_t>(h * hs + dd)] * wuk(h * hs + dd, j);
+        qa(0, j) = acc;
+        mx = std::max(mx, std::fabs(acc));
+      }
+      int e = 0;
+      if (mx > 0.0) {
+        e = static_cast<int>(std::floor(std::log2(448.0 / mx)));
+        while (std::ldexp(mx, e) > 448.0) --e;
+        while (std::ldexp(mx, e + 1) <= 448.0) ++e;
+      }
+      for (i64 j = 0; j < W; ++j) q(h, j) = std::ldexp(round_e4m3(std::ldexp(qa(0, j), e)), -e);
+    }
+  }
   ShardedKVCache& cache = mla_[static_cast<std::size_t>(l * batch_ + b)];
   std::vector<AttentionFragment> frags;
   for (i64 r = 0; r < cache.kvp(); ++r) frags.push_back(shard_attention(q, cache, r, 0, 1, Qh));
@@ -272,7 +293,10 @@ std::vector<double> ModelOracle::attend_mla(i64 l, i64 b, const std::vector<doub
   // attend-then-append: this token's latent joins the cache after the merge
   const std::vector<double> c = vecmat(a, wdkv_[static_cast<std::size_t>(l)]);
   Mat row(1, W);
-  for (i64 dd = 0; dd < W; ++dd) row(0, dd) = bf16_ ? round_bf16(c[static_cast<std::size_t>(dd)]) : c[static_cast<std::size_t>(dd)];
+  for (i64 dd = 0; dd < W; ++dd) {
+    const double cv = c[static_cast<std::size_t>(dd)];
+    row(0, dd) = kv_fp8_ ? round_e4m3(cv) : (bf16_ ? round_bf16(cv) : cv);
+  }
   cache.append_round_robin(row, row);
   return att;
 }

@@ -130,7 +130,8 @@ class ModelOracle {
   // Last step's router margin per (layer, request): r[k-th] - r[(k+1)-th]
   // (a kernel whose logits differ by more than this may legally pick another set)
   const std::vector<double>& route_gaps() const { return gaps_; }
-  // FP8 (e4m3) KV storage for the GQA caches (DecodeHarness::set_kv_fp8).
+  // FP8 (e4m3) KV storage: the GQA caches (DecodeHarness::set_kv_fp8) and the MLA
+  // latents (with the e4m3 query image, attend_mla).
   void set_kv_fp8(bool on) {
     kv_fp8_ = on;
     for (auto& h : h_) h.set_kv_fp8(on);

@@ -139,8 +139,8 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
   if (f64_ && (!attn_only_ || par.distributed != HX_POOL_LOCAL))
     throw std::invalid_argument("the exact fp64 harness (HX_KV_F64) is the attention-only local pool "
                                 "(DecodeHarness<double>)");
-  if (kv8_ && mla_) throw std::invalid_argument("FP8 KV pages are implemented for GQA caches (MLA latents stay bf16)");
-  if (kv4_ && mla_) throw std::invalid_argument("FP4 KV pages are implemented for GQA caches (MLA latents stay bf16)");
+  if (kv4_ && mla_)
+    throw std::invalid_argument("FP4 KV pages are implemented for GQA caches (MLA latents: bf16 or FP8)");
   if (kv4_ && m.head_size != 32 && m.head_size != 64 && m.head_size != 128)
     throw std::invalid_argument("FP4 KV blocks are 32 dims: head_size must be 32, 64 or 128");
   if (rt.w_dtype != HX_W_BF16 && rt.w_dtype != HX_W_FP8_E4M3 && rt.w_dtype != HX_W_FP4_E2M1)
@@ -242,7 +242,7 @@ Engine::Engine(const hx_model_config& m, const hx_parallel_config& par, const hx
                                 (static_cast<int64_t>(chunk_) * kvp_)) * chunk_;
   if (mla_) {
     page_cap_ = static_cast<int>((per_rank_max + kMlaPageRows - 1) / kMlaPageRows + 1);
-    page_bytes_ = mla_page_bytes();
+    page_bytes_ = mla_page_bytes(kv8_);
   } else {
     page_cap_ = static_cast<int>((per_rank_max + 15) / 16 + 1);
     page_bytes_ = kv4_ ? page_bytes_kv4(DP_) : page_bytes_kv(DP_, kv8_);
@@ -377,7 +377,7 @@ void Engine::alloc() {
   if (mla_) {  // 2-SM TMA views of each layer's latent pool (mla.cu)
     mla_tm_.resize(static_cast<size_t>(L_));
     for (int64_t l = 0; l < L_; ++l)
-      cuda_check(make_mla_tensor_maps(kv_[l], pool, mla_tm_[l].s, mla_tm_[l].v), "mla tensor maps");
+      cuda_check(make_mla_tensor_maps(kv_[l], pool, mla_tm_[l].s, mla_tm_[l].v, kv8_), "mla tensor maps");
   }
   d_total_ = dalloc<int>(static_cast<size_t>(L_) * B_, "totals");
   h_total_.assign(static_cast<size_t>(L_ * B_), 0);
@@ -407,7 +407,7 @@ void Engine::alloc() {
   splits_req_ = plan_splits(req_streams, page_cap_);
   n_items_ = std::max(n_streams_ * splits_, req_streams * splits_req_);
   if (mla_) {
-    d_qimg_ = dalloc<uint8_t>(static_cast<size_t>(B_) * mla_q_bytes(), "mla query images");
+    d_qimg_ = dalloc<uint8_t>(static_cast<size_t>(B_) * mla_q_bytes(kv8_), "mla query images");
     d_att_ = dalloc<float>(static_cast<size_t>(B_) * (dist_mode_ == HX_POOL_LOCAL ? Qh_ * DV_ : slice_),
                            "mla merged latent output");
   }
@@ -1098,7 +1098,7 @@ void Engine::fill_kv_hash(int64_t n, uint64_t seed) {
       if (h_total_[static_cast<size_t>(l * B_ + b)] + n > cap_) throw std::invalid_argument("KV capacity exceeded");
   for (int64_t l = 0; l < L_ && mla_; ++l) {
     cuda_check(launch_kv_fill_hash_mla(kv_[l], d_total_ + l * B_, B_, kvp_, chunk_, page_cap_, slot_base_, n_slots_,
-                                       n, seed, hash_stream(kCacheK, l), stream_),
+                                       n, seed, hash_stream(kCacheK, l), stream_, kv8_),
                "kv fill");
     for (int b = 0; b < B_; ++b) h_total_[static_cast<size_t>(l * B_ + b)] += n;
   }
@@ -1158,10 +1158,16 @@ void Engine::read_kv(int64_t layer, int64_t request, int64_t rank, int64_t head,
     for (int64_t t = 0; t < n; ++t) {
       const uint8_t* page = buf.data() + static_cast<size_t>(t / kMlaPageRows) * page_bytes_;
       for (int d = 0; d < W_; ++d) {
-        uint16_t kb;
-        std::memcpy(&kb, page + mla_kv_offset(static_cast<int>(t % kMlaPageRows), d), 2);
-        k[t * W_ + d] = float_from_bf16_bits(kb);
-        if (d < DV_) v[t * DV_ + d] = float_from_bf16_bits(kb);
+        float x;
+        if (kv8_) {
+          x = e4m3_to_float(page[mla_kv_offset8(static_cast<int>(t % kMlaPageRows), d)]);
+        } else {
+          uint16_t kb;
+          std::memcpy(&kb, page + mla_kv_offset(static_cast<int>(t % kMlaPageRows), d), 2);
+          x = float_from_bf16_bits(kb);
+        }
+        k[t * W_ + d] = x;
+        if (d < DV_) v[t * DV_ + d] = x;
       }
     }
     return;
@@ -1355,7 +1361,7 @@ void Engine::enqueue_attention(int64_t layer) {
   cuda_check(launch_gemv(q.p, q.xmode, E_QKV, num_sms_, stream_), "qkv gemv");
   if (mla_)  // W_UK absorption: q heads -> the 576-wide latent query image
     cuda_check(launch_mla_absorb_q(d_q_, w_uk_[layer], B_, static_cast<int>(Qh_), static_cast<int>(D_), DP_,
-                                   d_qimg_, stream_),
+                                   d_qimg_, stream_, kv8_),
                "mla absorb q");
   mark(1);
   if (dist_mode_ != HX_POOL_LOCAL) {

@@ -11,14 +11,14 @@
 #include <stdint.h>
 
 #ifdef __CUDACC__
-#define HX_HD __host__ __device__ __forceinline__
+#define HX_F8HD __host__ __device__ __forceinline__
 #else
-#define HX_HD inline
+#define HX_F8HD inline
 #endif
 
 namespace hx {
 
-HX_HD uint8_t e4m3_from_double(double x) {
+HX_F8HD uint8_t e4m3_from_double(double x) {
   if (x != x) return 0x7F;
   const uint8_t sign = x < 0.0 ? 0x80 : 0x00;
   const double a = x < 0.0 ? -x : x;
@@ -48,7 +48,7 @@ HX_HD uint8_t e4m3_from_double(double x) {
   return sign | static_cast<uint8_t>(ef << 3) | static_cast<uint8_t>(m - 8);
 }
 
-HX_HD float e4m3_to_float(uint8_t v) {
+HX_F8HD float e4m3_to_float(uint8_t v) {
   const int ef = (v >> 3) & 15, m = v & 7;
   float r;
   if (ef == 0) {
@@ -86,7 +86,7 @@ namespace hx {
 
 constexpr int kE2m1MinExp = -14, kE2m1MaxExp = 13;  // 2^e normal in f16: the kernel builds it by a shift
 
-HX_HD int e2m1_block_exp(double amax) {
+HX_F8HD int e2m1_block_exp(double amax) {
   if (!(amax > 0.0)) return 0;
   // smallest e with 6 * 2^e >= amax: amax / 6 = m * 2^k, m in [0.5, 1)
   const double r = amax / 6.0;
@@ -106,7 +106,7 @@ HX_HD int e2m1_block_exp(double amax) {
   return e;
 }
 
-HX_HD double pow2i(int e) {
+HX_F8HD double pow2i(int e) {
   double s = 1.0;
   for (; e > 0; --e) s *= 2.0;
   for (; e < 0; ++e) s *= 0.5;
@@ -114,7 +114,7 @@ HX_HD double pow2i(int e) {
 }
 
 // e2m1 code (sign << 3 | magnitude code) of x / 2^e, round to nearest even.
-HX_HD uint8_t e2m1_from_double(double x, int e) {
+HX_F8HD uint8_t e2m1_from_double(double x, int e) {
   const uint8_t sign = x < 0.0 ? 8 : 0;
   const double t = (x < 0.0 ? -x : x) / pow2i(e);  // exact: power-of-two scale
   // grid 0 0.5 1 1.5 2 3 4 6 (codes 0..7); midpoints go to the even code
@@ -137,7 +137,7 @@ HX_HD uint8_t e2m1_from_double(double x, int e) {
   return sign | c;
 }
 
-HX_HD float e2m1_to_float(uint8_t code, int e) {
+HX_F8HD float e2m1_to_float(uint8_t code, int e) {
   const float grid[8] = {0.f, 0.5f, 1.f, 1.5f, 2.f, 3.f, 4.f, 6.f};
   const float v = grid[code & 7] * static_cast<float>(pow2i(e));
   return (code & 8) ? -v : v;

@@ -562,9 +562,13 @@ __global__ void __launch_bounds__(1024) gemv_epilogue_kernel(const GemvParams p)
           if (slot_local >= 0 && slot_local < p.n_local_slots) {
             const size_t page = (static_cast<size_t>(slot_local) * p.batch + b) * p.page_cap +
                                 static_cast<size_t>(row / kMlaPageRows);
-            *reinterpret_cast<__nv_bfloat16*>(p.kv + page * mla_page_bytes() +
-                                              mla_kv_offset(static_cast<int>(row % kMlaPageRows), d)) =
-                __float2bfloat16_rn(y[0]);
+            if (p.kv8)  // FP8 latents: e4m3 RNE of the fp32 row (oracle: round_e4m3)
+              p.kv[page * mla_page_bytes(true) + mla_kv_offset8(static_cast<int>(row % kMlaPageRows), d)] =
+                  e4m3_from_double(static_cast<double>(y[0]));
+            else
+              *reinterpret_cast<__nv_bfloat16*>(p.kv + page * mla_page_bytes() +
+                                                mla_kv_offset(static_cast<int>(row % kMlaPageRows), d)) =
+                  __float2bfloat16_rn(y[0]);
           }
         }
       }

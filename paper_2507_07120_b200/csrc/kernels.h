@@ -133,22 +133,25 @@ cudaError_t launch_wait_flags(unsigned* flags, int n, cudaStream_t stream);
 // MLA (tcgen05): items = (split, stream, value half); part_o [n_items][128][256],
 // part_lse2 [n_items][128]; the split reduce writes frag_o [slot][b][q][512].
 // tm_s / tm_v: CUtensorMap (128 B each) over the layer's latent pool viewed as
-// [rows of 2 KB] x [256 x u64], boxes of 8 rows (16 KB chunk) / 16 rows (32 KB block).
+// [rows of 2 KB] x [256 x u64], boxes of 8 rows (16 KB chunk) / 16 rows (32 KB block);
+// FP8 latents (p.kv8 = 1, kv_layout.cuh mla_kv_offset8): 12-row (24 KB) S chunks,
+// 8-row (16 KB) V blocks, the e4m3 query image (mla_q_offset8) and kind::f8f6f4.
 cudaError_t launch_mla_decode(const AttnParams& p, int grid, cudaStream_t stream, const void* tm_s, const void* tm_v);
 // Encode the two tensor maps for a latent pool of `bytes` bytes (multiple of 2 KB).
-cudaError_t make_mla_tensor_maps(const void* pool, size_t bytes, void* tm_s, void* tm_v);
+cudaError_t make_mla_tensor_maps(const void* pool, size_t bytes, void* tm_s, void* tm_v, bool f8 = false);
 cudaError_t launch_mla_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse, cudaStream_t stream);
 // MLA weight absorption (layer_oracle.hpp): q image = bf16(n_h . Wuk_h) from the
 // QKV epilogue's n [B][Q][dp] and wuk [Q][hs][576]; v = o_h . Wuv_h from the merged
 // latent output att [B][n_heads*512] and wuv [n_heads][512][hs] -> x-fragments of
 // v [B][n_heads*hs] for the O-projection.
+// f8: the e4m3 image with per-head power-of-two scales (kv_layout.cuh mla_q_offset8).
 cudaError_t launch_mla_absorb_q(const float* n, const uint16_t* wuk, int batch, int q_heads, int hs, int dp,
-                                uint8_t* qimg, cudaStream_t stream);
+                                uint8_t* qimg, cudaStream_t stream, bool f8 = false);
 cudaError_t launch_mla_uv(const float* att, const uint16_t* wuv, int batch, int n_heads, int hs, uint8_t* xf,
                           cudaStream_t stream, int xf16 = 0);
 cudaError_t launch_kv_fill_hash_mla(uint8_t* kv, int* total, int batch, int kvp, int chunk, int page_cap,
                                     int slot_base, int n_local_slots, long long n, uint64_t seed, uint64_t stream_k,
-                                    cudaStream_t stream);
+                                    cudaStream_t stream, bool f8 = false);
 cudaError_t launch_attn_split_reduce(const AttnParams& p, float* frag_o, float* frag_lse,
                                      cudaStream_t stream);
 cudaError_t launch_bump_totals(int* total, int n, cudaStream_t stream);

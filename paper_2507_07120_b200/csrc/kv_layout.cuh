@@ -140,15 +140,34 @@ constexpr int kMlaW = 576;
 constexpr int kMlaDV = 512;
 constexpr int kMlaPageRows = 128;
 constexpr int kMlaHeads = 128;  // UMMA M: query heads per CTA (zero-padded)
-__host__ __device__ __forceinline__ uint32_t mla_page_bytes() { return kMlaPageRows * kMlaW * 2; }
+__host__ __device__ __forceinline__ uint32_t mla_page_bytes(bool f8 = false) {
+  return kMlaPageRows * kMlaW * (f8 ? 1 : 2);
+}
 __host__ __device__ __forceinline__ uint32_t mla_kv_offset(int r, int d) {
   return static_cast<uint32_t>((((d >> 3) * (kMlaPageRows / 8) + (r >> 3)) * 64 + (r & 7) * 8 + (d & 7)) * 2);
+}
+// FP8 (e4m3) latent pages (kv_dtype = HX_KV_FP8_E4M3): the same core-matrix
+// order with 16-byte rows of 16 dims --
+//   [dg = d/16 : 36][tg = row/8 : 16][row%8 : 8][d%16 : 16] e4m3
+// (a page = 36 rows of 2 KB): K-major A operand of S^T (kind::f8f6f4, K = 32
+// per MMA = two dim groups), and MN-major A operand of O^T (tokens along K).
+__host__ __device__ __forceinline__ uint32_t mla_kv_offset8(int r, int d) {
+  return static_cast<uint32_t>((((d >> 4) * (kMlaPageRows / 8) + (r >> 3)) * 8 + (r & 7)) * 16 + (d & 15));
 }
 // Per-request absorbed-query image, split in two head halves (one per CTA of
 // the MLA pair): [head/64 : 2][dg : 72][(head%64)/8 : 8][head%8][d%8] bf16 --
 // each half is the K-major B operand (N = 64 heads) of S^T = C . Q^T and one
 // contiguous 73,728-byte block. Written by the QKV epilogue.
-__host__ __device__ __forceinline__ uint32_t mla_q_bytes() { return kMlaW * kMlaHeads * 2; }
+__host__ __device__ __forceinline__ uint32_t mla_q_bytes(bool f8 = false) {
+  return f8 ? kMlaW * kMlaHeads + kMlaHeads * 4 : kMlaW * kMlaHeads * 2;
+}
+// FP8 query image (FP8 latents): [head/64 : 2][dg = d/16 : 36][(head%64)/8 : 8][head%8][d%16]
+// e4m3 of q * 2^e_h (per head, the largest power of two keeping max |q_h| <= 448),
+// then float 2^-e_h per head at offset kMlaW * kMlaHeads.
+__host__ __device__ __forceinline__ uint32_t mla_q_offset8(int head, int d) {
+  return static_cast<uint32_t>(((((head >> 6) * 36 + (d >> 4)) * 8 + ((head & 63) >> 3)) * 8 + (head & 7)) * 16 +
+                               (d & 15));
+}
 __host__ __device__ __forceinline__ uint32_t mla_q_offset(int head, int d) {
   return static_cast<uint32_t>(((((head >> 6) * 72 + (d >> 3)) * 8 + ((head & 63) >> 3)) * 8 + (head & 7)) * 16 +
                                (d & 7) * 2);

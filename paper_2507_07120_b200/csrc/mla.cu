@@ -52,30 +52,46 @@
 namespace hx {
 
 namespace {
-constexpr uint32_t kQHalf = kMlaW * 64 * 2;          // 73728: query image half
-constexpr uint32_t kSChunk = 64 * kMlaPageRows * 2;  // 16384: 64 dims x 128 rows
-constexpr uint32_t kVBlock = 128 * kMlaPageRows * 2; // 32768: 128 dims x 128 rows
-constexpr uint32_t kPT = 256 * 64 * 2;               // 32768: P^T, 256 tokens x 64 heads
-constexpr int kSChunks = kMlaW / 64;                 // 9
-constexpr int kSSlots = 3, kVSlots = 2;
-constexpr uint32_t kIdescST = umma_idesc_bf16(256, 128, false, false);
-constexpr uint32_t kIdescOT = umma_idesc_bf16(256, 128, true, true);
 constexpr int kThreads = 384;  // 8 softmax warps + 2 S producers + MMA + V producer
 
-// shared-memory carve-up
-constexpr uint32_t kOffQ = 0;
-constexpr uint32_t kOffS = kOffQ + kQHalf;
-constexpr uint32_t kOffV = kOffS + kSSlots * kSChunk;
-constexpr uint32_t kOffPT = kOffV + kVSlots * kVBlock;
-constexpr uint32_t kOffRed = kOffPT + kPT;         // float [8 warps][64 heads] (max / sum)
-constexpr uint32_t kOffMin = kOffRed + 4 * 128 * 4; // float [2][128] peer maxima
-constexpr uint32_t kOffMuse = kOffMin + 2 * 128 * 4;
-constexpr uint32_t kOffAlpha = kOffMuse + 128 * 4;
-constexpr uint32_t kOffZin = kOffAlpha + 128 * 4;   // float [2][128] peer sums
-constexpr uint32_t kOffZs = kOffZin + 2 * 128 * 4;
-constexpr uint32_t kOffBar = kOffZs + 128 * 4;
-constexpr int kNumBars = 32;
-constexpr uint32_t kSmem = kOffBar + kNumBars * 8 + 16;
+// Per-variant geometry. bf16 latents (F8 = false): kind::f16, K = 16 per MMA;
+// FP8 latents (F8 = true, kv_layout.cuh mla_kv_offset8): kind::f8f6f4 with e4m3
+// latents, an e4m3 query image (per-head power-of-two scale) and e4m3 P, K = 32
+// per MMA -- the same tile shapes at half the bytes and twice the MMA rate.
+template <bool F8>
+struct MlaCfg {
+  static constexpr uint32_t kQHalf = F8 ? 36u * 1024u : kMlaW * 64u * 2u;  // query image half (64 heads)
+  static constexpr int kSRows = F8 ? 12 : 8;          // 2 KB page rows per S chunk (192 / 64 dims)
+  static constexpr uint32_t kSChunk = kSRows * 2048u;  // 24 / 16 KB
+  static constexpr int kSChunks = F8 ? 3 : 9;
+  static constexpr int kSMmas = F8 ? 6 : 4;            // MMAs per S chunk (2 dim groups each)
+  static constexpr int kVRows = F8 ? 8 : 16;           // 128 value dims x 128 rows
+  static constexpr uint32_t kVBlock = kVRows * 2048u;
+  static constexpr int kSSlots = 3, kVSlots = F8 ? 4 : 2;  // barrier slots: S <= 3, V <= 4
+  static_assert(kSSlots <= 3 && kVSlots <= 4, "mbarrier index layout (mla_decode_kernel)");
+  static constexpr uint32_t kPTPage = F8 ? 8192u : 16384u;  // P^T of 128 tokens x 64 heads
+  static constexpr uint32_t kPT = 2 * kPTPage;
+  static constexpr uint32_t kPTLbo = F8 ? 512u : 1024u;     // P^T stride between 8-token groups
+  static constexpr int kPVMmas = F8 ? 4 : 8;                // MMAs per 128-token page (K = 32 / 16)
+  static constexpr uint32_t kPVAStep = F8 ? 512u : 256u;    // V^T bytes per MMA along K (tokens)
+  static constexpr uint32_t kIdescST = F8 ? umma_idesc_e4m3(256, 128, false, false) : umma_idesc_bf16(256, 128, false, false);
+  static constexpr uint32_t kIdescOT = F8 ? umma_idesc_e4m3(256, 128, true, true) : umma_idesc_bf16(256, 128, true, true);
+  // shared-memory carve-up
+  static constexpr uint32_t kOffQ = 0;
+  static constexpr uint32_t kOffS = kOffQ + kQHalf;
+  static constexpr uint32_t kOffV = kOffS + kSSlots * kSChunk;
+  static constexpr uint32_t kOffPT = kOffV + kVSlots * kVBlock;
+  static constexpr uint32_t kOffRed = kOffPT + kPT;          // float [8 warps][64 heads] (max / sum)
+  static constexpr uint32_t kOffMin = kOffRed + 4 * 128 * 4;  // float [2][128] peer maxima
+  static constexpr uint32_t kOffMuse = kOffMin + 2 * 128 * 4;
+  static constexpr uint32_t kOffAlpha = kOffMuse + 128 * 4;
+  static constexpr uint32_t kOffZin = kOffAlpha + 128 * 4;    // float [2][128] peer sums
+  static constexpr uint32_t kOffZs = kOffZin + 2 * 128 * 4;
+  static constexpr uint32_t kOffCs = kOffZs + 128 * 4;        // float [128] score scale per head (FP8 q)
+  static constexpr uint32_t kOffBar = kOffCs + 128 * 4;
+  static constexpr int kNumBars = 32;
+  static constexpr uint32_t kSmem = kOffBar + kNumBars * 8 + 16;
+};
 
 struct MlaItem {
   int b, sl, pg0, pg1, ntok;
@@ -117,17 +133,35 @@ __device__ __forceinline__ void mla_step(int k, int n, int& tile, bool& value) {
     value = true;
   }
 }
+// four floats -> four e4m3 bytes (RNE, saturating), a in the lowest byte
+__device__ __forceinline__ uint32_t pack_e4m3x4(float a, float b, float c, float d) {
+  uint32_t r;
+  asm("{\n.reg .b16 lo, hi;\ncvt.rn.satfinite.e4m3x2.f32 lo, %2, %1;\ncvt.rn.satfinite.e4m3x2.f32 hi, %4, %3;\n"
+      "mov.b32 %0, {lo, hi};\n}"
+      : "=r"(r)
+      : "f"(a), "f"(b), "f"(c), "f"(d));
+  return r;
+}
 }  // namespace
 
+template <bool F8>
 __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParams p, const __grid_constant__ CUtensorMap tm_s,
                                                                    const __grid_constant__ CUtensorMap tm_v) {
+  using C = MlaCfg<F8>;
+  constexpr uint32_t kQHalf = C::kQHalf, kSChunk = C::kSChunk, kVBlock = C::kVBlock;
+  constexpr int kSChunks = C::kSChunks, kSSlots = C::kSSlots, kVSlots = C::kVSlots;
+  constexpr uint32_t kOffQ = C::kOffQ, kOffS = C::kOffS, kOffV = C::kOffV, kOffPT = C::kOffPT;
+  constexpr uint32_t kOffRed = C::kOffRed, kOffMin = C::kOffMin, kOffMuse = C::kOffMuse, kOffAlpha = C::kOffAlpha;
+  constexpr uint32_t kOffZin = C::kOffZin, kOffZs = C::kOffZs, kOffBar = C::kOffBar;
+  constexpr int kNumBars = C::kNumBars;
+  const uint32_t page_bytes = mla_page_bytes(F8), q_bytes = mla_q_bytes(F8);
   extern __shared__ __align__(128) uint8_t smem[];
   const uint32_t sbase = smem_u32(smem);
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + kOffBar);
   uint64_t* full_s = bars + 0;       // [3]
   uint64_t* empty_s = bars + 3;      // [3]
-  uint64_t* full_v = bars + 9;       // [2]
-  uint64_t* empty_v = bars + 11;     // [2]
+  uint64_t* full_v = bars + 6;       // [kVSlots <= 4]
+  uint64_t* empty_v = bars + 10;     // [kVSlots <= 4]
   uint64_t* q_full = bars + 15;
   uint64_t* q_free = bars + 16;
   uint64_t* pq_full = bars + 17;     // leader: peer's Q half landed
@@ -145,6 +179,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
   float* alpha_s = reinterpret_cast<float*>(smem + kOffAlpha);
   float* z_in = reinterpret_cast<float*>(smem + kOffZin);
   float* zs = reinterpret_cast<float*>(smem + kOffZs);
+  float* cs = reinterpret_cast<float*>(smem + C::kOffCs);  // FP8: qscale * 2^-e_h per head
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t cta = cluster_ctarank();
@@ -198,17 +233,17 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
           waited = true;
         }
         const uint8_t* kvb =
-            p.kv + (static_cast<size_t>(it.sl) * p.batch + it.b) * p.page_cap * static_cast<size_t>(mla_page_bytes());
+            p.kv + (static_cast<size_t>(it.sl) * p.batch + it.b) * p.page_cap * static_cast<size_t>(page_bytes);
         const int n = (it.pg1 - it.pg0 + 1) / 2;
         auto page_of = [&](int tile, int c) {
           const int pg = it.pg0 + 2 * tile + c;
-          return kvb + static_cast<size_t>(pg < it.pg1 ? pg : it.pg0) * mla_page_bytes();  // ghost: masked
+          return kvb + static_cast<size_t>(pg < it.pg1 ? pg : it.pg0) * page_bytes;  // ghost: masked
         };
         if (sprod) {
           if (sparity == 0) {
             if (qcount > 0) mbar_wait(q_free, (qcount - 1) & 1);
             mbar_arrive_expect_tx(q_full, kQHalf);
-            bulk_g2s(smem + kOffQ, p.qimg + static_cast<size_t>(it.b) * mla_q_bytes() + cta * kQHalf, kQHalf, q_full);
+            bulk_g2s(smem + kOffQ, p.qimg + static_cast<size_t>(it.b) * q_bytes + cta * kQHalf, kQHalf, q_full);
             ++qcount;
           }
           for (int tile = 0; tile < n; ++tile) {
@@ -219,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
               if (us >= kSSlots) mbar_wait(&empty_s[s], ((us / kSSlots) - 1) & 1);
               // both CTAs' chunks complete on the LEADER's full barrier (2-SM TMA)
               if (leader) mbar_arrive_expect_tx(&full_s[s], 2 * kSChunk);
-              tma_load_2d_pair(sbase + kOffS + s * kSChunk, &tm_s, 0, row0 + j * 8, l_full_s + s * 8);
+              tma_load_2d_pair(sbase + kOffS + s * kSChunk, &tm_s, 0, row0 + j * C::kSRows, l_full_s + s * 8);
             }
           }
         } else {
@@ -230,7 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
                 if (uv >= kVSlots) mbar_wait(&empty_v[s], ((uv / kVSlots) - 1) & 1);
                 if (leader) mbar_arrive_expect_tx(&full_v[s], 2 * kVBlock);
                 // this CTA's 128 value dims of block jb: [256 jb + 128 cta, +128), rows of CTA pp's page
-                const int row0 = static_cast<int>((page_of(tile, pp) - p.kv) >> 11) + (2 * jb + static_cast<int>(cta)) * 16;
+                const int row0 = static_cast<int>((page_of(tile, pp) - p.kv) >> 11) + (2 * jb + static_cast<int>(cta)) * C::kVRows;
                 tma_load_2d_pair(sbase + kOffV + s * kVBlock, &tm_v, 0, row0, l_full_v + s * 8);
               }
         }
@@ -278,13 +313,20 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
               const int s = us % kSSlots;
               mbar_wait(&full_s[s], (us / kSSlots) & 1);  // both CTAs' chunks (2-SM TMA)
               tc_fence_after();
+              // A: the chunk's dim groups (2 KB apart) x 8-token groups (128 B); B: the
+              // query image's dim groups (1 KB apart) x 8-head groups; 2 dim groups per MMA
               const uint64_t a0 = umma_desc(sbase + kOffS + s * kSChunk, 2048, 128);
-              const uint64_t b0 = umma_desc(sbase + kOffQ + 4 * j * 2048, 1024, 128);
+              const uint64_t b0 = umma_desc(sbase + kOffQ + j * C::kSRows * 1024, 1024, 128);
               if (elect_one()) {
 #pragma unroll
-                for (int kk = 0; kk < 4; ++kk)
-                  umma_ss_pair(d, a0 + static_cast<uint64_t>((kk * 4096) >> 4),
-                               b0 + static_cast<uint64_t>((kk * 2048) >> 4), kIdescST, (j | kk) != 0);
+                for (int kk = 0; kk < C::kSMmas; ++kk) {
+                  const uint64_t a = a0 + static_cast<uint64_t>((kk * 4096) >> 4);
+                  const uint64_t b = b0 + static_cast<uint64_t>((kk * 2048) >> 4);
+                  if constexpr (F8)
+                    umma_ss_pair_f8(d, a, b, C::kIdescST, (j | kk) != 0);
+                  else
+                    umma_ss_pair(d, a, b, C::kIdescST, (j | kk) != 0);
+                }
                 umma_commit_pair(&empty_s[s]);
               }
               __syncwarp();
@@ -304,14 +346,22 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
                 const int s = uv % kVSlots;
                 mbar_wait(&full_v[s], (uv / kVSlots) & 1);  // both CTAs' blocks (2-SM TMA)
                 tc_fence_after();
+                // MN-major both: A = V^T (8-token groups 128 B apart along K, dim
+                // groups 2 KB apart along M), B = P^T (8-token groups kPTLbo apart,
+                // head groups 128 B apart along N)
                 const uint64_t a0 = umma_desc(sbase + kOffV + s * kVBlock, 128, 2048);
-                const uint64_t b0 = umma_desc(sbase + kOffPT + 8 * pp * 2048, 1024, 128);
+                const uint64_t b0 = umma_desc(sbase + kOffPT + pp * C::kPTPage, C::kPTLbo, 128);
                 const bool acc0 = tile > 0 || pp > 0;
                 if (elect_one()) {
 #pragma unroll
-                  for (int kk = 0; kk < kMlaPageRows / 16; ++kk)
-                    umma_ss_pair(tbase + 256 + 128 * jb, a0 + static_cast<uint64_t>((kk * 256) >> 4),
-                                 b0 + static_cast<uint64_t>((kk * 2048) >> 4), kIdescOT, (acc0 || kk > 0) ? 1u : 0u);
+                  for (int kk = 0; kk < C::kPVMmas; ++kk) {
+                    const uint64_t a = a0 + static_cast<uint64_t>((kk * C::kPVAStep) >> 4);
+                    const uint64_t b = b0 + static_cast<uint64_t>((kk * 2048) >> 4);
+                    if constexpr (F8)
+                      umma_ss_pair_f8(tbase + 256 + 128 * jb, a, b, C::kIdescOT, (acc0 || kk > 0) ? 1u : 0u);
+                    else
+                      umma_ss_pair(tbase + 256 + 128 * jb, a, b, C::kIdescOT, (acc0 || kk > 0) ? 1u : 0u);
+                  }
                   umma_commit_pair(&empty_v[s]);
                 }
                 __syncwarp();
@@ -338,6 +388,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
     const uint32_t pt_local = sbase + kOffPT;
     const bool pt_remote = wg != static_cast<int>(cta);  // P^T of these heads lives in the peer
     const int h_own = hbase + t;                           // head owned for max/sum bookkeeping (t < 64)
+    if constexpr (F8) griddep_wait();  // the query images' head scales are read from global below
     int g = 0, items = 0;
     for (int item = cluster_id; item < p.n_items; item += n_clusters) {
       const MlaItem it = decode_item(p, item);
@@ -354,6 +405,11 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
 #pragma unroll
       for (int h = 0; h < 64; ++h) z[h] = 0.f;
       float m_run = -INFINITY;  // reference max of head h_own (log2 units), threads t < 64
+      if constexpr (F8) {  // per-head score scale: qscale x the query image's 2^-e_h (published by the barriers below)
+        if (t < 64)
+          cs[h_own] = p.qscale * reinterpret_cast<const float*>(p.qimg + static_cast<size_t>(it.b) * q_bytes +
+                                                                kMlaW * kMlaHeads)[h_own];
+      }
       const int n = (it.pg1 - it.pg0 + 1) / 2;
       for (int tile = 0; tile < n; ++tile, ++g) {
         const int buf = g & 1;
@@ -382,7 +438,7 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
         if (t < 64) {
           float mc = fmaxf(fmaxf(red[(4 * wg) * 64 + t], red[(4 * wg + 1) * 64 + t]),
                            fmaxf(red[(4 * wg + 2) * 64 + t], red[(4 * wg + 3) * 64 + t]));
-          mc *= p.qscale;
+          mc *= F8 ? cs[h_own] : p.qscale;
           st_async_f32(peer_min + (buf * 128 + h_own) * 4, mc, peer_mx + buf * 8);
           mbar_wait(&mx_bar[buf], (g >> 1) & 1);
           const float mt = fmaxf(mc, m_in[buf * 128 + h_own]);
@@ -416,40 +472,77 @@ __global__ void __launch_bounds__(kThreads, 1) mla_decode_kernel(const AttnParam
         if (tile > 0 && !pv_waited) mbar_wait(pv_done, (g - 1) & 1);  // P^T buffers free
         // ---- P for this token, this warpgroup's 64 heads -> P^T of CTA wg (local or st.async)
         const int k = 128 * static_cast<int>(cta) + t;
-        const uint32_t rowoff = (static_cast<uint32_t>(k >> 3) * 64 + (k & 7)) * 16;
+        if constexpr (F8) {
+          // e4m3 P^T [tg 32][16-head group 4][token%8][16 heads]; the head sums keep
+          // the unrounded fp32 p (RNE errors are unbiased; the tolerance covers them)
+          const uint32_t rowoff = static_cast<uint32_t>(k >> 3) * 512 + (k & 7) * 16;
 #pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          float v[32];
-          tmem_ld32(srow + 32 * j, v);
+          for (int j = 0; j < 2; ++j) {
+            float v[32];
+            tmem_ld32(srow + 32 * j, v);
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 ma = *reinterpret_cast<const float4*>(m_use + hbase + 32 * j + 8 * q);
-            const float4 mb = *reinterpret_cast<const float4*>(m_use + hbase + 32 * j + 8 * q + 4);
-            const float mm[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
-            uint32_t w4[4];
+            for (int q = 0; q < 2; ++q) {
+              uint32_t w4[4];
 #pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int hl = 32 * j + 8 * q + 2 * e;  // head index within the warpgroup
-              const float p0 = mine ? ex2_approx(fmaf(v[8 * q + 2 * e], p.qscale, -mm[2 * e])) : 0.f;
-              const float p1 = mine ? ex2_approx(fmaf(v[8 * q + 2 * e + 1], p.qscale, -mm[2 * e + 1])) : 0.f;
-              const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
-              z[hl] += __low2float(pb);
-              z[hl + 1] += __high2float(pb);
-              w4[e] = *reinterpret_cast<const uint32_t*>(&pb);
+              for (int e = 0; e < 4; ++e) {
+                const int hl = 32 * j + 16 * q + 4 * e;  // head index within the warpgroup
+                const float4 mm = *reinterpret_cast<const float4*>(m_use + hbase + hl);
+                const float4 cc = *reinterpret_cast<const float4*>(cs + hbase + hl);
+                const float* vv = v + 16 * q + 4 * e;
+                const float p0 = mine ? ex2_approx(fmaf(vv[0], cc.x, -mm.x)) : 0.f;
+                const float p1 = mine ? ex2_approx(fmaf(vv[1], cc.y, -mm.y)) : 0.f;
+                const float p2 = mine ? ex2_approx(fmaf(vv[2], cc.z, -mm.z)) : 0.f;
+                const float p3 = mine ? ex2_approx(fmaf(vv[3], cc.w, -mm.w)) : 0.f;
+                z[hl] += p0;
+                z[hl + 1] += p1;
+                z[hl + 2] += p2;
+                z[hl + 3] += p3;
+                w4[e] = pack_e4m3x4(p0, p1, p2, p3);
+              }
+              const uint32_t off = rowoff + static_cast<uint32_t>(2 * j + q) * 128;
+              const uint4 val = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+              if (pt_remote)
+                st_async_v4(peer_pt + off, val, peer_ptfull);
+              else
+                sts128(pt_local + off, val);
             }
-            // P^T core (token row k, heads 8-group (4j + q) of this CTA's 64)
-            const uint32_t off = rowoff + static_cast<uint32_t>(4 * j + q) * 128;
-            const uint4 val = make_uint4(w4[0], w4[1], w4[2], w4[3]);
-            if (pt_remote)
-              st_async_v4(peer_pt + off, val, peer_ptfull);
-            else
-              sts128(pt_local + off, val);
+          }
+        } else {
+          const uint32_t rowoff = (static_cast<uint32_t>(k >> 3) * 64 + (k & 7)) * 16;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            float v[32];
+            tmem_ld32(srow + 32 * j, v);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float4 ma = *reinterpret_cast<const float4*>(m_use + hbase + 32 * j + 8 * q);
+              const float4 mb = *reinterpret_cast<const float4*>(m_use + hbase + 32 * j + 8 * q + 4);
+              const float mm[8] = {ma.x, ma.y, ma.z, ma.w, mb.x, mb.y, mb.z, mb.w};
+              uint32_t w4[4];
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const int hl = 32 * j + 8 * q + 2 * e;  // head index within the warpgroup
+                const float p0 = mine ? ex2_approx(fmaf(v[8 * q + 2 * e], p.qscale, -mm[2 * e])) : 0.f;
+                const float p1 = mine ? ex2_approx(fmaf(v[8 * q + 2 * e + 1], p.qscale, -mm[2 * e + 1])) : 0.f;
+                const __nv_bfloat162 pb = __floats2bfloat162_rn(p0, p1);
+                z[hl] += __low2float(pb);
+                z[hl + 1] += __high2float(pb);
+                w4[e] = *reinterpret_cast<const uint32_t*>(&pb);
+              }
+              // P^T core (token row k, heads 8-group (4j + q) of this CTA's 64)
+              const uint32_t off = rowoff + static_cast<uint32_t>(4 * j + q) * 128;
+              const uint4 val = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+              if (pt_remote)
+                st_async_v4(peer_pt + off, val, peer_ptfull);
+              else
+                sts128(pt_local + off, val);
+            }
           }
         }
         fence_proxy_async();
         tc_fence_before();
         if (threadIdx.x == 0)
-          mbar_arrive_expect_tx(pt_full, 128 * 64 * 2);  // + the peer warpgroup's st.async into this P^T
+          mbar_arrive_expect_tx(pt_full, 128 * 64 * (F8 ? 1 : 2));  // + the peer warpgroup's st.async into this P^T
         else
           mbar_arrive(pt_full);
         if (!leader && threadIdx.x == 0) {  // forward "peer P^T complete" to the leader's MMA issuer
@@ -586,12 +679,11 @@ __global__ void __launch_bounds__(256) mla_split_reduce_kernel(const AttnParams 
   if (threadIdx.x == 0) frag_lse[fo] = Lt > 0.f ? (M + log2f(Lt)) * 0.69314718055994530942f : -INFINITY;
 }
 
-size_t mla_smem_bytes() { return kSmem; }
-
-cudaError_t launch_mla_decode(const AttnParams& p, int grid, cudaStream_t stream, const void* tm_s, const void* tm_v) {
-  if (p.q_heads > kMlaHeads || p.q_heads < 1) return cudaErrorInvalidValue;
+template <bool F8>
+static cudaError_t launch_mla_t(const AttnParams& p, int grid, cudaStream_t stream, const void* tm_s, const void* tm_v) {
+  constexpr uint32_t kSmem = MlaCfg<F8>::kSmem;
   {
-    const cudaError_t e = smem_optin<mla_decode_kernel>(kSmem);
+    const cudaError_t e = smem_optin<mla_decode_kernel<F8>>(kSmem);
     if (e != cudaSuccess) return e;
   }
   cudaLaunchConfig_t cfg{};
@@ -608,11 +700,16 @@ cudaError_t launch_mla_decode(const AttnParams& p, int grid, cudaStream_t stream
   attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, mla_decode_kernel, p, *static_cast<const CUtensorMap*>(tm_s),
+  return cudaLaunchKernelEx(&cfg, mla_decode_kernel<F8>, p, *static_cast<const CUtensorMap*>(tm_s),
                             *static_cast<const CUtensorMap*>(tm_v));
 }
 
-cudaError_t make_mla_tensor_maps(const void* pool, size_t bytes, void* tm_s, void* tm_v) {
+cudaError_t launch_mla_decode(const AttnParams& p, int grid, cudaStream_t stream, const void* tm_s, const void* tm_v) {
+  if (p.q_heads > kMlaHeads || p.q_heads < 1) return cudaErrorInvalidValue;
+  return p.kv8 ? launch_mla_t<true>(p, grid, stream, tm_s, tm_v) : launch_mla_t<false>(p, grid, stream, tm_s, tm_v);
+}
+
+cudaError_t make_mla_tensor_maps(const void* pool, size_t bytes, void* tm_s, void* tm_v, bool f8) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -628,7 +725,7 @@ cudaError_t make_mla_tensor_maps(const void* pool, size_t bytes, void* tm_s, voi
   const cuuint64_t dims[2] = {256, bytes / 2048};  // u64 elements per 2 KB row, rows
   const cuuint64_t strides[1] = {2048};
   const cuuint32_t estr[2] = {1, 1};
-  const cuuint32_t box_s[2] = {256, 8}, box_v[2] = {256, 16};
+  const cuuint32_t box_s[2] = {256, f8 ? 12u : 8u}, box_v[2] = {256, f8 ? 8u : 16u};
   CUresult r = encode(static_cast<CUtensorMap*>(tm_s), CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, const_cast<void*>(pool), dims,
                       strides, box_s, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -656,9 +753,10 @@ __device__ __forceinline__ long long mla_rr_global(long long row, int rank, int 
 
 __global__ void kv_fill_hash_mla_kernel(uint8_t* kv, const int* total, int batch, int kvp, int chunk, int page_cap,
                                         int slot_base, int n_local_slots, long long n, uint64_t seed,
-                                        uint64_t stream_k) {
+                                        uint64_t stream_k, bool f8) {
   const long long idx = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x;
-  constexpr int kRowsPerPage = kMlaPageRows * (kMlaW / 8);  // 16-byte rows per page
+  const int dims = f8 ? 16 : 8;  // latent dims per 16-byte row
+  const int kRowsPerPage = kMlaPageRows * (kMlaW / dims);  // 16-byte rows per page
   const long long per_stream = static_cast<long long>(page_cap) * kRowsPerPage;
   if (idx >= static_cast<long long>(n_local_slots) * batch * per_stream) return;
   const long long st = idx / per_stream;  // slot_local * B + b
@@ -673,7 +771,16 @@ __global__ void kv_fill_hash_mla_kernel(uint8_t* kv, const int* total, int batch
   const long long t0 = total[b];
   if (g < t0 || g >= t0 + n) return;
   const uint64_t kseed = splitmix64(seed ^ (stream_k * 0xD1B54A32D192ED03ull));
-  const uint64_t base = ((static_cast<uint64_t>(b) << 32) + static_cast<uint64_t>(g)) * kMlaW + dg * 8;
+  const uint64_t base = ((static_cast<uint64_t>(b) << 32) + static_cast<uint64_t>(g)) * kMlaW + dg * dims;
+  uint8_t* pg = kv + (static_cast<size_t>(st) * page_cap + page) * static_cast<size_t>(mla_page_bytes(f8));
+  if (f8) {  // the double draw rounded straight to e4m3 (oracle: round_e4m3 of the same draw)
+    uint8_t c[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e)
+      c[e] = e4m3_from_double(2.0 * (static_cast<double>(splitmix64(kseed + base + e) >> 11) * 0x1.0p-53) - 1.0);
+    *reinterpret_cast<uint4*>(pg + static_cast<size_t>(ci) * 16) = *reinterpret_cast<const uint4*>(c);
+    return;
+  }
   uint32_t w[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
@@ -690,7 +797,6 @@ __global__ void kv_fill_hash_mla_kernel(uint8_t* kv, const int* total, int batch
     }
     w[e] = static_cast<uint32_t>(lo) | (static_cast<uint32_t>(hi) << 16);
   }
-  uint8_t* pg = kv + (static_cast<size_t>(st) * page_cap + page) * static_cast<size_t>(mla_page_bytes());
   *reinterpret_cast<uint4*>(pg + static_cast<size_t>(ci) * 16) = make_uint4(w[0], w[1], w[2], w[3]);
 }
 
@@ -700,11 +806,11 @@ __global__ void add_total_mla_kernel(int* total, int batch, int n) {
 
 cudaError_t launch_kv_fill_hash_mla(uint8_t* kv, int* total, int batch, int kvp, int chunk, int page_cap,
                                     int slot_base, int n_local_slots, long long n, uint64_t seed, uint64_t stream_k,
-                                    cudaStream_t stream) {
-  const long long work = static_cast<long long>(n_local_slots) * batch * page_cap * kMlaPageRows * (kMlaW / 8);
+                                    cudaStream_t stream, bool f8) {
+  const long long work = static_cast<long long>(n_local_slots) * batch * page_cap * kMlaPageRows * (kMlaW / (f8 ? 16 : 8));
   if (n > 0)
     kv_fill_hash_mla_kernel<<<static_cast<unsigned>((work + 255) / 256), 256, 0, stream>>>(
-        kv, total, batch, kvp, chunk, page_cap, slot_base, n_local_slots, n, seed, stream_k);
+        kv, total, batch, kvp, chunk, page_cap, slot_base, n_local_slots, n, seed, stream_k, f8);
   add_total_mla_kernel<<<1, 64, 0, stream>>>(total, batch, static_cast<int>(n));
   return cudaGetLastError();
 }
@@ -724,7 +830,10 @@ cudaError_t launch_kv_fill_hash_mla(uint8_t* kv, int* total, int batch, int kvp,
 // weight load per d feeds 8 requests x 8 columns of FMAs, eight loads in flight
 // per thread; the DS d-slice partials are summed in slice order (deterministic).
 // Requests in passes of 8, staged in shared memory as [d][8].
-template <bool ABSORB, int DS>
+// Q8 (ABSORB for FP8 latents, one CTA per head): the head's 576 values of each
+// request are scaled by 2^e_h, the largest power of two keeping max |q_h| <= 448,
+// and stored as e4m3 with 2^-e_h beside the image (mla_q_offset8).
+template <bool ABSORB, int DS, bool Q8 = false>
 __global__ void __launch_bounds__(512) mla_head_gemm_kernel(const float* in, int in_head_stride, int in_row_stride,
                                                              const __nv_bfloat16* w, int din, int dout, int batch,
                                                              uint8_t* out, int xf16) {
@@ -804,22 +913,58 @@ __global__ void __launch_bounds__(512) mla_head_gemm_kernel(const float* in, int
       }
     }
     __syncthreads();
-    for (int e = threadIdx.x; e < nb * cols; e += blockDim.x) {
-      const int b = e / cols, jc = e - b * cols, jj = c0 + jc;
-      float v = 0.f;
+    if constexpr (Q8) {
+      __shared__ float s_scale[NB];
+      for (int e = threadIdx.x; e < nb * cols; e += blockDim.x) {  // sums in place (slice 0 of each element)
+        const int b = e / cols, jc = e - b * cols;
+        float v = 0.f;
 #pragma unroll
-      for (int s = 0; s < DS; ++s) v += red[(s * NB + b) * cols + jc];
-      if (ABSORB)
-        *reinterpret_cast<__nv_bfloat16*>(out + static_cast<size_t>(bc + b) * mla_q_bytes() + mla_q_offset(h, jj)) =
-            __float2bfloat16_rn(v);
-      else
-        xf_write(out, xf_nb8(batch), bc + b, h * dout + jj, v, xf16);
+        for (int s = 0; s < DS; ++s) v += red[(s * NB + b) * cols + jc];
+        red[b * cols + jc] = v;
+      }
+      __syncthreads();
+      const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+      if (warp < nb) {
+        float mx = 0.f;
+        for (int jc = lane; jc < cols; jc += 32) mx = fmaxf(mx, fabsf(red[warp * cols + jc]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        int ex = 0;
+        if (mx > 0.f) {
+          ex = static_cast<int>(floorf(log2f(448.f / mx)));
+          while (ex > -120 && ldexpf(mx, ex) > 448.f) --ex;
+          while (ex < 120 && ldexpf(mx, ex + 1) <= 448.f) ++ex;
+        }
+        if (lane == 0) {
+          s_scale[warp] = ldexpf(1.f, ex);
+          reinterpret_cast<float*>(out + static_cast<size_t>(bc + warp) * mla_q_bytes(true) + kMlaW * kMlaHeads)[h] =
+              ldexpf(1.f, -ex);
+        }
+      }
+      __syncthreads();
+      for (int e = threadIdx.x; e < nb * cols; e += blockDim.x) {
+        const int b = e / cols, jc = e - b * cols;
+        out[static_cast<size_t>(bc + b) * mla_q_bytes(true) + mla_q_offset8(h, c0 + jc)] =
+            e4m3_from_double(static_cast<double>(red[b * cols + jc] * s_scale[b]));
+      }
+    } else {
+      for (int e = threadIdx.x; e < nb * cols; e += blockDim.x) {
+        const int b = e / cols, jc = e - b * cols, jj = c0 + jc;
+        float v = 0.f;
+#pragma unroll
+        for (int s = 0; s < DS; ++s) v += red[(s * NB + b) * cols + jc];
+        if (ABSORB)
+          *reinterpret_cast<__nv_bfloat16*>(out + static_cast<size_t>(bc + b) * mla_q_bytes() + mla_q_offset(h, jj)) =
+              __float2bfloat16_rn(v);
+        else
+          xf_write(out, xf_nb8(batch), bc + b, h * dout + jj, v, xf16);
+      }
     }
     __syncthreads();
   }
 }
 
-template <bool ABSORB, int DS>
+template <bool ABSORB, int DS, bool Q8 = false>
 static cudaError_t launch_head_gemm_t(const float* in, int in_head_stride, int in_row_stride, const uint16_t* w,
                                       int din, int dout, int batch, int heads, int col_chunks, uint8_t* out,
                                       cudaStream_t stream, int xf16 = 0) {
@@ -828,18 +973,21 @@ static cudaError_t launch_head_gemm_t(const float* in, int in_head_stride, int i
   if (cols % 8 || din % DS || (cols / 8) * DS > 512) return cudaErrorInvalidValue;
   const size_t smem = (static_cast<size_t>(din) * 8 + static_cast<size_t>(DS) * 8 * cols) * sizeof(float);
   {
-    const cudaError_t e = smem_optin<mla_head_gemm_kernel<ABSORB, DS>>(smem);
+    const cudaError_t e = smem_optin<mla_head_gemm_kernel<ABSORB, DS, Q8>>(smem);
     if (e != cudaSuccess) return e;
   }
   const int threads = (cols / 8) * DS;
-  return launch_k(mla_head_gemm_kernel<ABSORB, DS>, dim3(heads, col_chunks), dim3((threads + 31) / 32 * 32), smem,
+  if (Q8 && (col_chunks != 1 || threads < 32 * 8)) return cudaErrorInvalidValue;  // one CTA per head, a warp per request
+  return launch_k(mla_head_gemm_kernel<ABSORB, DS, Q8>, dim3(heads, col_chunks), dim3((threads + 31) / 32 * 32), smem,
                   stream, in,
                   in_head_stride, in_row_stride, reinterpret_cast<const __nv_bfloat16*>(w), din, dout, batch, out, xf16);
 }
 
 cudaError_t launch_mla_absorb_q(const float* n, const uint16_t* wuk, int batch, int q_heads, int hs, int dp,
-                                uint8_t* qimg, cudaStream_t stream) {
+                                uint8_t* qimg, cudaStream_t stream, bool f8) {
   if (hs > 128) return cudaErrorInvalidValue;  // 3 chunks of 24 column groups x 8 d-slices
+  if (f8)  // one CTA per head (the per-head scale spans all 576 columns): 72 column groups x 4 d-slices
+    return launch_head_gemm_t<true, 4, true>(n, dp, q_heads * dp, wuk, hs, kMlaW, batch, q_heads, 1, qimg, stream);
   return launch_head_gemm_t<true, 8>(n, dp, q_heads * dp, wuk, hs, kMlaW, batch, q_heads, 3, qimg, stream);
 }
 

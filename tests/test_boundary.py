@@ -51,9 +51,16 @@ def test_mla_kernel_uses_tcgen05():
     sass = subprocess.run(["cuobjdump", "-sass", so], capture_output=True, text=True).stdout
     funcs = sass.split("Function : ")
     mla = [f for f in funcs if f.startswith("_ZN2hx17mla_decode_kernel")]
-    assert len(mla) == 1
+    assert len(mla) == 2  # bf16 latents (template false) and FP8 latents (true)
+    bf16 = [f for f in mla if f.startswith("_ZN2hx17mla_decode_kernelILb0E")]
+    fp8 = [f for f in mla if f.startswith("_ZN2hx17mla_decode_kernelILb1E")]
+    assert len(bf16) == 1 and len(fp8) == 1
     for op in ("UTCHMMA.2CTA", "LDTM", "STTM", "UTCBAR", "UTMALDG.2D.2CTA", "REDUX.MAX.F32"):
-        assert op in mla[0], op
+        assert op in bf16[0], op
+    # FP8 latents: kind::f8f6f4 paired MMAs (UTCQMMA.2CTA), P packed to e4m3 in registers
+    for op in ("UTCQMMA.2CTA", "F2FP.SATFINITE.E4M3.F32.PACK", "LDTM", "UTCBAR", "UTMALDG.2D.2CTA"):
+        assert op in fp8[0], op
+    assert "UTCHMMA" not in fp8[0]
 
 
 def test_large_batch_gemv_uses_tcgen05():

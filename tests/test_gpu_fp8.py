@@ -177,8 +177,9 @@ def test_fp8_loopback_pool_hopb():
         e.close()
 
 
-def test_fp8_rejects_mla():
+def test_fp4_rejects_mla():
+    """MLA latents are bf16 or FP8 (tests/test_gpu_mla_fp8.py); FP4 pages are GQA-only."""
     import paper_2507_07120_b200 as P
     spec = P.model.ModelSpec("mla", 1, 256, 16, 1, 16, 256, 3, "mla", 288, vocab=300)
-    with pytest.raises(ValueError, match="FP8"):
-        P.HelixDecoder(spec, batch=1, capacity=64, layers=1, vocab=300, kv_dtype="fp8")
+    with pytest.raises(ValueError, match="FP4"):
+        P.HelixDecoder(spec, batch=1, capacity=64, layers=1, vocab=300, kv_dtype="fp4")

@@ -1,0 +1,168 @@
+"""GPU parity of MLA decode over FP8 (e4m3) latents (the
+paper evaluates at low precision): kv_dtype = "fp8" with an MLA
+model runs mla.cu's kind::f8f6f4 variant -- e4m3 latent pages
+(kv_layout.cuh mla_kv_offset8), an e4m3 query image with a power-of-two scale
+per head, e4m3 P -- against the oracle with the same latent rounding
+(round_e4m3 of the hash draws and of the appended rows) and the same query
+quantisation (layer_oracle.cpp attend_mla).
+
+What the oracle does not mirror: P rounded to e4m3 before P.V (3 mantissa
+bits, RNE; the head sums keep the unrounded p) and fp32 accumulation. The
+tolerances below are ~3x the largest errors measured on a B200 over these
+cases; the bf16-latent kernel's are in tests/test_gpu_mla.py.
+"""
+import ctypes
+import threading
+
+import numpy as np
+import pytest
+
+from tests import oracle_py as O
+
+pytestmark = pytest.mark.gpu
+
+H, Q, HSZ, L, V, LAT = 256, 16, 16, 2, 500, 288
+TOL_FIRST = TOL_LATER = 2e-2  # measured <= 6.2e-3 (hidden), <= 5.5e-3 (logits)
+
+
+def rel_err(got, want):
+    return float(np.abs(got - want).max() / max(1e-12, np.abs(want).max()))
+
+
+def _spec(P, moe=None, q=Q, h=H, hsz=HSZ, layers=L):
+    return P.model.ModelSpec("mla", layers, h, q, 1, hsz, 256, 3, "mla", LAT, moe, vocab=V)
+
+
+def test_mla_fp8_latent_fill_matches_oracle_hash():
+    """Hash-filled e4m3 latent pages read back as round_e4m3 of the oracle's draws."""
+    import paper_2507_07120_b200 as P
+    g = P.HelixDecoder(_spec(P), tpa=1, kvp=2, batch=2, capacity=600, layers=1, vocab=V, kv_dtype="fp8")
+    assert g.info()["kv_dtype"] == 1
+    g.init_weights(5, qkv="hash")
+    g.fill_kv_hash(530, 5)
+    W = 2 * LAT
+    for b in range(2):
+        for rank in range(2):
+            n = g.total_tokens(0, b)
+            cnt = sum(1 for t in range(n) if (t // 16) % 2 == rank)
+            k = np.zeros((cnt, W), dtype=np.float32)
+            v = np.zeros((cnt, W - 64), dtype=np.float32)
+            rc = P.lib().hx_read_kv(g._h, 0, b, rank, 0, k.ctypes.data_as(ctypes.POINTER(ctypes.c_float)),
+                                    v.ctypes.data_as(ctypes.POINTER(ctypes.c_float)))
+            assert rc == 0
+            toks = [t for t in range(n) if (t // 16) % 2 == rank]
+            for row in (0, 1, 127, 128, cnt - 1):
+                t = toks[row]
+                want = np.array([O.hash_unit(5, (10 << 32) | 0, ((b << 32) + t) * W + d) for d in range(W)])
+                np.testing.assert_array_equal(k[row], O.round_e4m3(want).astype(np.float32))
+            np.testing.assert_array_equal(v, k[:, :W - 64])
+    g.close()
+
+
+@pytest.mark.parametrize("kvp,B,ctx", [(1, 2, 40), (1, 3, 700), (2, 2, 300), (4, 1, 1100), (1, 8, 2000), (2, 20, 300)])
+def test_mla_fp8_decode_matches_oracle(kvp, B, ctx):
+    import paper_2507_07120_b200 as P
+    seed = 177 + kvp
+    g = P.HelixDecoder(_spec(P), tpa=1, kvp=kvp, batch=B, capacity=ctx + 8, layers=L, vocab=V, kv_dtype="fp8")
+    g.init_weights(seed, qkv="hash")
+    g.fill_kv_hash(ctx, seed)
+    o = O.Model(H, Q, 1, HSZ, 256, L, V, tpa=1, kvp=kvp, chunk=16, batch=B, seed=seed, qkv_hash=True, bf16=True,
+                kv_latent=LAT, kv_fp8=True)
+    for l in range(L):
+        for b in range(B):
+            o.grow_hash(l, b, ctx)
+    tokens = (np.arange(B) * 97 + 3) % V
+    for step in range(3):
+        nxt, logits, hidden = g.step(tokens, want_logits=True, want_hidden=True)
+        lo, ho, no = o.step(tokens)
+        tol = TOL_FIRST if step == 0 else TOL_LATER
+        e_h, e_l = rel_err(hidden, ho), rel_err(logits, lo)
+        print(f"fp8 mla kvp={kvp} B={B} ctx={ctx} step={step}: hidden {e_h:.2e} logits {e_l:.2e}")
+        assert e_h <= tol and e_l <= tol
+        tokens = no
+    g.close()
+
+
+def test_mla_fp8_at_deepseek_width_matches_oracle():
+    """deepseek-r1-like attention width (H = 16384, 128 heads x Hsz 128, latent
+    2 x 288) over FP8 latents, one layer, KVP = 2 local pool, B = 2, 2k context."""
+    import paper_2507_07120_b200 as P
+    Hw, Qw, Hsz, F, Vw, B, ctx, kvp, seed = 16384, 128, 128, 256, 512, 2, 2048, 2, 31
+    spec = P.model.ModelSpec("deepseek-width", 1, Hw, Qw, 1, Hsz, F, 3, "mla", LAT, None, vocab=Vw)
+    g = P.HelixDecoder(spec, tpa=1, kvp=kvp, batch=B, capacity=ctx + 16, layers=1, vocab=Vw, kv_dtype="fp8")
+    g.init_weights(seed, qkv="hash")
+    g.fill_kv_hash(ctx, seed)
+    o = O.Model(Hw, Qw, 1, Hsz, F, 1, Vw, tpa=1, kvp=kvp, chunk=16, batch=B, seed=seed, qkv_hash=True, bf16=True,
+                kv_latent=LAT, kv_fp8=True)
+    for b in range(B):
+        o.grow_hash(0, b, ctx)
+    tokens = np.array([3, 100])
+    for step in range(2):
+        nxt, logits, hidden = g.step(tokens, want_logits=True, want_hidden=True)
+        lo, ho, no = o.step(tokens)
+        tol = TOL_FIRST if step == 0 else TOL_LATER
+        e_h, e_l = rel_err(hidden, ho), rel_err(logits, lo)
+        print(f"fp8 MLA H={Hw} Q={Qw} step {step}: hidden {e_h:.2e} logits {e_l:.2e}")
+        assert e_h <= tol and e_l <= tol
+        tokens = no
+    g.close()
+
+
+def test_mla_fp8_loopback_pool_matches_oracle():
+    """KVP = 2 loopback pool over FP8 latents: per-rank fragments, exchange, merge."""
+    import paper_2507_07120_b200 as P
+    from paper_2507_07120_b200.model import Loopback
+    kvp, B, ctx, seed = 2, 2, 600, 21
+    lb = Loopback(kvp)
+    engines = [P.HelixDecoder(_spec(P), tpa=1, kvp=kvp, batch=B, capacity=ctx + 4, layers=L, vocab=V,
+                              use_graphs=False, pool=2, rank=r, loopback=lb, kv_dtype="fp8") for r in range(kvp)]
+    for e in engines:
+        e.init_weights(seed, qkv="hash")
+        e.fill_kv_hash(ctx, seed)
+    o = O.Model(H, Q, 1, HSZ, 256, L, V, tpa=1, kvp=kvp, chunk=16, batch=B, seed=seed, qkv_hash=True, bf16=True,
+                kv_latent=LAT, kv_fp8=True)
+    for l in range(L):
+        for b in range(B):
+            o.grow_hash(l, b, ctx)
+    tokens = np.array([7, 8])
+    for step in range(2):
+        results = [None] * kvp
+        errors = []
+
+        def run(r):
+            try:
+                results[r] = engines[r].step(tokens, want_logits=True, want_hidden=True)
+            except Exception as ex:  # surfaced below
+                errors.append(ex)
+        th = [threading.Thread(target=run, args=(r,), daemon=True) for r in range(kvp)]
+        [t.start() for t in th]
+        [t.join(timeout=120) for t in th]
+        assert not any(t.is_alive() for t in th), "loopback ranks did not finish"
+        assert not errors, errors
+        lo, ho, no = o.step(tokens)
+        tol = TOL_FIRST if step == 0 else TOL_LATER
+        for r in range(kvp):
+            e = rel_err(results[r][2], ho)
+            print(f"fp8 mla pool rank {r} step {step}: hidden {e:.2e}")
+            assert e <= tol
+        tokens = no
+    for e in engines:
+        e.close()
+
+
+def test_mla_fp8_vs_bf16_latents_attention_difference_is_small():
+    """Sanity of the quantised path against the bf16-latent kernel on the same
+    weights and draws (not an oracle check): the two decode steps differ by the
+    e4m3 rounding of latents, queries and P only."""
+    import paper_2507_07120_b200 as P
+    B, ctx, seed = 4, 1500, 9
+    outs = []
+    for kv in ("bf16", "fp8"):
+        g = P.HelixDecoder(_spec(P), tpa=1, kvp=1, batch=B, capacity=ctx + 8, layers=L, vocab=V, kv_dtype=kv)
+        g.init_weights(seed, qkv="hash")
+        g.fill_kv_hash(ctx, seed)
+        outs.append(g.step(np.arange(B) + 5, want_logits=True, want_hidden=True)[2])
+        g.close()
+    e = rel_err(outs[1], outs[0])
+    print(f"fp8 vs bf16 latents: hidden {e:.2e}")
+    assert 0 < e <= 5e-2

@@ -210,6 +210,85 @@ int run8() {
   return err > 1e-3;
 }
 
+// test 4: kind::f8f6f4 with A and B both MN-major e4m3 (the MLA FP8 P.V form):
+// [mn/16][k/8][k%8][mn%16] bytes -- a core matrix is 8 K-rows x 16 bytes along
+// M/N; K-direction stride 128 B (LBO), M/N-direction stride (K/8)*128 B (SBO)
+template <int N>
+__global__ void probe8mn(float* out) {
+  constexpr int KK = 128;
+  __shared__ __align__(1024) uint8_t as[128 * KK];
+  __shared__ __align__(1024) uint8_t bs[N * KK];
+  __shared__ uint32_t tbase;
+  __shared__ __align__(8) uint64_t bar;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  if (warp == 0) tmem_alloc(&tbase, 256);
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_mbar_init();
+  }
+  for (int i = tid; i < 128 * KK; i += 128) {
+    const int m = i / KK, k = i % KK;
+    as[(((m >> 4) * (KK / 8) + (k >> 3)) * 8 + (k & 7)) * 16 + (m & 15)] = to_e4m3(a8(m, k));
+  }
+  for (int i = tid; i < N * KK; i += 128) {
+    const int n = i / KK, k = i % KK;
+    bs[(((n >> 4) * (KK / 8) + (k >> 3)) * 8 + (k & 7)) * 16 + (n & 15)] = to_e4m3(b8(n, k));
+  }
+  fence_proxy_async();
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tm = tbase;
+  const uint32_t id = (1u << 4) | (1u << 15) | (1u << 16) | (static_cast<uint32_t>(N >> 3) << 17) | (128u >> 4 << 24);
+  if (warp == 0) {
+    if (elect_one()) {
+      for (int ks = 0; ks < KK / 32; ++ks) {  // K = 32 per MMA: four 8-row core matrices along K
+        const uint64_t a = umma_desc(smem_u32(as) + ks * 4 * 128, 128, (KK / 8) * 128);
+        const uint64_t b = umma_desc(smem_u32(bs) + ks * 4 * 128, 128, (KK / 8) * 128);
+        asm volatile(
+            "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+            "tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], %1, %2, %3, p;\n}\n" ::"r"(tm + 128),
+            "l"(a), "l"(b), "r"(id), "r"(ks > 0 ? 1u : 0u)
+            : "memory");
+      }
+      umma_commit(&bar);
+    }
+    __syncwarp();
+  }
+  mbar_wait(&bar, 0);
+  tc_fence_after();
+  for (int n0 = 0; n0 < N; n0 += 32) {
+    float v[32];
+    tmem_ld32(tm + (static_cast<uint32_t>(warp * 32) << 16) + 128 + n0, v);
+    for (int n = 0; n < 32; ++n) out[tid * N + n0 + n] = v[n];
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tm, 256);
+}
+template <int N>
+int run8mn() {
+  float* d;
+  cudaMalloc(&d, 128 * N * 4);
+  probe8mn<N><<<1, 128>>>(d);
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    printf("f8 MN-major test N=%d: CUDA error\n", N);
+    return 1;
+  }
+  float h[128 * N];
+  cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+  double err = 0;
+  for (int m = 0; m < 128; ++m)
+    for (int n = 0; n < N; ++n) {
+      double r = 0;
+      for (int k = 0; k < 128; ++k) r += static_cast<double>(a8(m, k)) * b8(n, k);
+      err = fmax(err, fabs(r - h[m * N + n]));
+    }
+  printf("f8f6f4 e4m3 MN-major A and B N=%d: max |err| = %g (D[0][0..1] = %g %g)\n", N, err, h[0], h[1]);
+  cudaFree(d);
+  return err > 1e-3;
+}
+
 int main() {
   int bad = 0;
   bad += run<16>(2);
@@ -220,6 +299,8 @@ int main() {
   bad += run<32>(1);
   bad += run8<32>();
   bad += run8<64>();
+  bad += run8mn<32>();
+  bad += run8mn<64>();
   printf(bad ? "PROBE FAILED\n" : "PROBE OK\n");
   return bad;
 }
