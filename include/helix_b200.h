@@ -87,8 +87,9 @@ typedef struct hx_runtime_config {
   int32_t device;
   int32_t hopb;             /* HOP-B batch-wise comm/compute overlap (overlap.hpp:37-69) */
   int32_t use_graphs;       /* capture the decode step in a CUDA graph */
-  int32_t kv_dtype;         /* KV page storage: HX_KV_BF16, or HX_KV_FP8_E4M3 (GQA; e4m3 RNE,
-                               saturating at +-448, unit scale -- SURVEY 8f rank 2) */
+  int32_t kv_dtype;         /* KV page storage: HX_KV_BF16, or HX_KV_FP8_E4M3 (e4m3 RNE, saturating
+                               at +-448, unit scale -- SURVEY 8f rank 2; GQA K/V pages, or MLA
+                               latents on kind::f8f6f4 with an e4m3 query image and e4m3 P) */
   int32_t w_dtype;          /* GEMV weight storage: HX_W_BF16, HX_W_FP8_E4M3 (batch <= 16, hash init;
                                e4m3 with a power-of-two scale per output feature, applied in the
                                GEMV epilogue -- SURVEY 8f rank 2) or HX_W_FP4_E2M1 (batch <= 16,
