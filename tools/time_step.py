@@ -24,7 +24,8 @@ def main():
     import paper_2507_07120_b200 as P
     spec = P.model.PRESETS["llama3-8b-like"]
     B = 8
-    g = P.HelixDecoder(spec, batch=B, capacity=a.context + 64, layers=a.layers, kv_dtype=a.kv, w_dtype=a.w)
+    g = P.HelixDecoder(spec, batch=B, capacity=a.context + a.rounds * a.steps + 64, layers=a.layers, kv_dtype=a.kv,
+                       w_dtype=a.w)
     g.init_weights(2507, qkv="hash")
     g.fill_kv_hash(a.context, 2507)
     tok = torch.randint(0, spec.vocab, (B,), dtype=torch.int32, device="cuda")
