@@ -254,3 +254,51 @@ def test_nccl_pool_two_gpus_matches_oracle(hopb, graphs):
             assert rel_err(hidden, ho) <= tol, (r, step, rel_err(hidden, ho))
         np.testing.assert_array_equal(res[1][step][2], res[0][step][2])
         tokens = no
+
+
+@pytest.mark.parametrize("pool,kvp,hopb", [(0, 2, False), (0, 4, False), (2, 2, False), (2, 2, True), (2, 4, False)])
+def test_fused_combine_is_bit_identical_to_merge_kernel(pool, kvp, hopb, monkeypatch):
+    """The LSE combine inside the O-projection GEMV (GemvParams::merge, gemv.cu
+    merge_prologue) merges in the same canonical order as the merge kernels it
+    replaces (misc.cu xprep_merge_local / xprep_merge_recv): decode steps are
+    bit-identical with HX_FUSED_COMBINE=0, and one launch per layer shorter."""
+    import paper_2507_07120_b200 as P
+    from paper_2507_07120_b200.model import Loopback
+    H, Q, K, D, F, L, V, B = 256, 8, 2, 32, 512, 2, 1000, 3
+    spec = P.model.ModelSpec("test", L, H, Q, K, D, F, 3, "gqa", 0, vocab=V)
+    out, launches = {}, {}
+    for mode in ("0", "1"):
+        monkeypatch.setenv("HX_FUSED_COMBINE", mode)
+        n = kvp if pool else 1
+        lb = Loopback(n) if pool else None
+        kw = dict(pool=2, loopback=lb) if pool else {}
+        engines = [P.HelixDecoder(spec, tpa=1, kvp=kvp, chunk_size=16, batch=B, capacity=400, layers=L, vocab=V,
+                                  use_graphs=False, hopb=hopb, rank=r, **kw) for r in range(n)]
+        launches[mode] = engines[0].info()["kernels_per_step"]
+        for e in engines:
+            e.init_weights(77, qkv="hash")
+            e.fill_kv_hash(150 + 17 * kvp, 77)
+        tokens = np.array([5, 17, 999])
+        res = []
+        for step in range(2):
+            results = [None] * n
+            errors = []
+
+            def run(r):
+                try:
+                    results[r] = engines[r].step(tokens, want_logits=True, want_hidden=True)
+                except Exception as ex:  # surfaced below
+                    errors.append(ex)
+            th = [threading.Thread(target=run, args=(r,), daemon=True) for r in range(n)]
+            [t.start() for t in th]
+            [t.join(timeout=120) for t in th]
+            assert not any(t.is_alive() for t in th) and not errors, errors
+            res.append(results[0])
+            tokens = results[0][0]
+        out[mode] = res
+        for e in engines:
+            e.close()
+    assert launches["0"] == launches["1"] + L
+    for a, b in zip(out["0"], out["1"]):
+        for x, y in zip(a, b):
+            np.testing.assert_array_equal(x, y)
