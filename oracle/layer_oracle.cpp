@@ -245,6 +245,19 @@ std::vector<double> ModelOracle::ffn(i64 l, i64 b, const std::vector<double>& f)
   return y;
 }
 
+int quantize_q_e4m3_pow2(double* q, i64 n) {
+  double mx = 0.0;
+  for (i64 j = 0; j < n; ++j) mx = std::max(mx, std::fabs(q[j]));
+  int e = 0;
+  if (mx > 0.0) {
+    e = static_cast<int>(std::floor(std::log2(448.0 / mx)));
+    while (std::ldexp(mx, e) > 448.0) --e;
+    while (std::ldexp(mx, e + 1) <= 448.0) ++e;
+  }
+  for (i64 j = 0; j < n; ++j) q[j] = std::ldexp(round_e4m3(std::ldexp(q[j], e)), -e);
+  return e;
+}
+
 std::vector<double> ModelOracle::attend_mla(i64 l, i64 b, const std::vector<double>& a) {
   const i64 Qh = d_.query_heads, W = mla_width(d_.kv_latent), DV = mla_value_width(d_.kv_latent);
   const i64 hs = d_.head_size;
@@ -269,13 +282,9 @@ std::vector<double> ModelOracle::attend_mla(i64 l, i64 b, const std::vector<doub
         qa(0, j) = acc;
         mx = std::max(mx, std::fabs(acc));
       }
-      int e = 0;
-      if (mx > 0.0) {
-        e = static_cast<int>(std::floor(std::log2(448.0 / mx)));
-        while (std::ldexp(mx, e) > 448.0) --e;
-        while (std::ldexp(mx, e + 1) <= 448.0) ++e;
-      }
-      for (i64 j = 0; j < W; ++j) q(h, j) = std::ldexp(round_e4m3(std::ldexp(qa(0, j), e)), -e);
+      (void)mx;
+      quantize_q_e4m3_pow2(&qa(0, 0), W);
+      for (i64 j = 0; j < W; ++j) q(h, j) = qa(0, j);
     }
   }
   ShardedKVCache& cache = mla_[static_cast<std::size_t>(l * batch_ + b)];

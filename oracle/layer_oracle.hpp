@@ -97,6 +97,10 @@ struct ModelDims {
 // Cache fill: latent element d of token g of (layer, request) =
 //   hash_unit(seed, (kCacheK<<32)|layer, ((request << 32) + g) * W + d).
 inline i64 mla_width(i64 kv_latent) { return 2 * kv_latent; }
+// FP8-latent MLA query image (the GPU's absorb kernel, mla.cu Q8): one head's
+// values scaled by 2^e, e the largest exponent keeping max |q| <= 448, rounded to
+// e4m3 (round_e4m3) and scaled back; in place. Returns e.
+int quantize_q_e4m3_pow2(double* q, i64 n);
 inline i64 mla_value_width(i64 kv_latent) { return 2 * kv_latent - 64; }
 
 enum class QkvInit { MT19937 = 0, Hash = 1 };

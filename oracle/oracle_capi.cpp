@@ -37,6 +37,7 @@ double oracle_rng_unit_draw(void* r) { return unit_draw(*static_cast<std::mt1993
 std::uint64_t oracle_rng_next(void* r) { return (*static_cast<std::mt19937_64*>(r))(); }
 double oracle_round_bf16(double x) { return round_bf16(x); }
 double oracle_round_e4m3(double x) { return round_e4m3(x); }
+int oracle_quantize_q_e4m3_pow2(double* q, long long n) { return quantize_q_e4m3_pow2(q, n); }
 
 int oracle_harness_create(i64 q, i64 k, i64 hsz, i64 tpa, i64 kvp, i64 chunk, std::uint64_t seed,
                           int bf16, void** out) {

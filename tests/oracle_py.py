@@ -30,6 +30,7 @@ def lib():
             "oracle_rng_next": (u64, [vp]),
             "oracle_round_bf16": (C.c_double, [C.c_double]),
             "oracle_round_e4m3": (C.c_double, [C.c_double]),
+            "oracle_quantize_q_e4m3_pow2": (C.c_int, [C.POINTER(C.c_double), C.c_longlong]),
             "oracle_harness_set_kv_fp8": (None, [vp, C.c_int]),
             "oracle_model_set_kv_fp8": (None, [vp, C.c_int]),
             "oracle_harness_set_kv_fp4": (None, [vp, C.c_int]),
@@ -114,6 +115,13 @@ class Rng:
 def round_e4m3(a):
     f = np.vectorize(lib().oracle_round_e4m3)
     return f(np.asarray(a, dtype=np.float64))
+
+
+def quantize_q_e4m3_pow2(q):
+    """FP8-latent MLA query quantisation (layer_oracle.cpp quantize_q_e4m3_pow2): returns (values, e)."""
+    a = np.ascontiguousarray(np.asarray(q, dtype=np.float64)).copy()
+    e = lib().oracle_quantize_q_e4m3_pow2(a.ctypes.data_as(C.POINTER(C.c_double)), a.size)
+    return a, e
 
 
 def round_bf16(a):

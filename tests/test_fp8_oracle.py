@@ -48,3 +48,20 @@ def test_fp8_weights_oracle_quantisation():
         np.testing.assert_array_equal(w, O.round_e4m3(w0 / s) * s)
         assert np.all(np.abs(w / s).max(axis=0) <= 448.0)
         assert np.all(np.abs(w / s).max(axis=0) > 224.0 * 0.9)  # the scale is the smallest power of two
+
+
+def test_mla_query_quantisation_matches_torch():
+    """The FP8-latent MLA query image (layer_oracle.cpp quantize_q_e4m3_pow2, the
+    rule of the GPU's absorb kernel, mla.cu Q8): per head, e = the largest exponent
+    with max |q| * 2^e <= 448, values e4m3(q * 2^e) * 2^-e -- against torch.float8_e4m3fn."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(3)
+    for scale in (1e-6, 3e-3, 0.7, 1.0, 5.0, 448.0, 1e3, 2.0 ** 20):
+        q = (rng.standard_normal(576) * scale).astype(np.float32).astype(np.float64)
+        got, e = O.quantize_q_e4m3_pow2(q)
+        mx = np.abs(q).max()
+        assert mx * 2.0 ** e <= 448.0 < mx * 2.0 ** (e + 1)
+        want = torch_e4m3(q * 2.0 ** e) * 2.0 ** -e
+        np.testing.assert_array_equal(got, want)
+    got, e = O.quantize_q_e4m3_pow2(np.zeros(576))
+    assert e == 0 and not got.any()
