@@ -588,11 +588,17 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
             const float pv = fast_exp2(sv[r][i] - m_ref[r]);
-            l_sum[r] += pv;
-            if constexpr (KV8)
-              split2h(pv, ph[r][i], pl[r][i]);
-            else
+            if constexpr (KV8) {
+              // quantised pages: P as ONE f16 term (11 significant bits) -- the row sum
+              // takes the same rounded weights, so the output stays an exact weighted
+              // mean of V; half the P.V MMAs of the hi/lo split
+              ph[r][i] = __half2float(__float2half_rn(pv));
+              pl[r][i] = 0.f;
+              l_sum[r] += ph[r][i];
+            } else {
+              l_sum[r] += pv;
               split2(pv, ph[r][i], pl[r][i]);
+            }
           }
         }
         // P A-fragments (rows = queries g, g+8; k = tokens): hi tile and lo tile
@@ -606,9 +612,9 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
           const int ci = nd2 * 32 + lane;
           const uint4 vf = load_v<DP, KVF>(pbase, ci);
           mma_kv<KV8>(acc[2 * nd2], h0, h1, h2, h3, vf.x, vf.y);
-          mma_kv<KV8>(acc[2 * nd2], q0, q1, q2, q3, vf.x, vf.y);
+          if constexpr (!KV8) mma_kv<KV8>(acc[2 * nd2], q0, q1, q2, q3, vf.x, vf.y);
           mma_kv<KV8>(acc[2 * nd2 + 1], h0, h1, h2, h3, vf.z, vf.w);
-          mma_kv<KV8>(acc[2 * nd2 + 1], q0, q1, q2, q3, vf.z, vf.w);
+          if constexpr (!KV8) mma_kv<KV8>(acc[2 * nd2 + 1], q0, q1, q2, q3, vf.z, vf.w);
         }
       }
       __syncwarp();
