@@ -166,3 +166,37 @@ def test_mla_fp8_vs_bf16_latents_attention_difference_is_small():
     e = rel_err(outs[1], outs[0])
     print(f"fp8 vs bf16 latents: hidden {e:.2e}")
     assert 0 < e <= 5e-2
+
+
+@pytest.mark.parametrize("moe", [False, True])
+def test_mla_fp8_latents_and_fp8_weights_match_oracle(moe):
+    """The deepseek_slice_fp8 setting in miniature: FP8 latents AND FP8 GEMV weights
+    (W_q and the latent projection in e4m3; W_UK / W_UV bf16), alone and with a
+    routed MoE FFN plus shared expert."""
+    import paper_2507_07120_b200 as P
+    m = P.model.MoESpec(8, 2, 64, 64) if moe else None
+    spec = P.model.ModelSpec("mla", L, H, Q, 1, HSZ, 256, 3, "mla", LAT, m, vocab=V)
+    B, ctx, seed = 3, 333, 11
+    g = P.HelixDecoder(spec, tpa=1, kvp=2, batch=B, capacity=ctx + 8, layers=L, vocab=V, w_dtype="fp8",
+                       kv_dtype="fp8")
+    g.init_weights(seed, qkv="hash")
+    g.fill_kv_hash(ctx, seed)
+    o = O.Model(H, Q, 1, HSZ, 64 if moe else 256, L, V, tpa=1, kvp=2, chunk=16, batch=B, seed=seed, qkv_hash=True,
+                moe=(8, 2, 64) if moe else None, kv_latent=LAT, w_fp8=True, kv_fp8=True)
+    for l in range(L):
+        for b in range(B):
+            o.grow_hash(l, b, ctx)
+    tokens = np.array([1, 2, 3])
+    compared = 0
+    for step in range(2):
+        nxt, logits, hidden = g.step(tokens, want_logits=True, want_hidden=True)
+        lo, ho, no = o.step(tokens)
+        if moe and not o.route_gaps().min() > 1e-4:
+            break  # a router near-tie: the two sides may legally diverge from here
+        e_h, e_l = rel_err(hidden, ho), rel_err(logits, lo)
+        print(f"fp8 latents + fp8 weights moe={moe} step={step}: hidden {e_h:.2e} logits {e_l:.2e}")
+        assert e_h <= TOL_LATER and e_l <= TOL_LATER
+        compared += 1
+        tokens = no
+    assert compared >= 1
+    g.close()
