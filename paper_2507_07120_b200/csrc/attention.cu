@@ -1154,7 +1154,10 @@ static cudaError_t launch_attn_dp(const AttnParams& p, int grid, cudaStream_t st
       // as many consumer warps as registers allow without spills (10 x 168 regs;
       // 12 warps spill), and deep rings (the pages are small)
       if constexpr (KVF == 2 && QC == 1) return launch_attn_t<128, 10, 6, QC, KVF, W16>(p, grid, stream);
-      else if constexpr (KVF == 2) return launch_attn_t<128, 8, 4, QC, KVF, W16>(p, grid, stream);
+      // 16-row (W16) FP4 consumers, single-term P (128 registers): 12 warps x 3 stages,
+      // 405B-like FP4 slice 0.406 ms vs 0.463 at 8 x 4, 0.444 at 10 x 4, 0.419 at 14 x 2
+      // (14 x 3 and 12 x 4 exceed the shared memory)
+      else if constexpr (KVF == 2) return launch_attn_t<128, 12, 3, QC, KVF, W16>(p, grid, stream);
       else {
       // FP8 pages: 10 consumer warps x 4 stages (217 KB of shared memory) -- the
       // e4m3 widening doubles the per-byte consumer work, so more pages in flight
