@@ -358,7 +358,10 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
   constexpr uint32_t Q_BYTES = QR * DP * 4;
   constexpr uint32_t STAGE_BYTES = STAGE_KV + Q_BYTES;
   constexpr int WS = SR * DP + 2 * SR; // per-warp combine scratch (floats): O rows, m, l
-  constexpr uint32_t QIMG_BYTES = W16 ? 3u * Cfg::KS * 32u * 16u : 0u;
+  // FP4 pages, 8 query rows: the query fragments live in shared memory (one image per
+  // query chunk) instead of 32 registers per thread, so more consumer warps fit
+  constexpr bool QSM = KVF == 2 && !W16;
+  constexpr uint32_t QIMG_BYTES = W16 ? 3u * Cfg::KS * 32u * 16u : (QSM ? QC * Cfg::KS * 32u * 16u : 0u);
 
   extern __shared__ __align__(128) uint8_t smem[];
   uint8_t* stages = smem;                                                     // NSTAGE * STAGE_BYTES
@@ -709,13 +712,22 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
               split3(v[i], hi[i], mid[i], lo[i]);
             }
           }
-          qa[ks][0] = pack_kv<KV8>(hi[0], hi[1]);
-          qa[ks][1] = pack_kv<KV8>(mid[0], mid[1]);
-          qa[ks][2] = pack_kv<KV8>(hi[2], hi[3]);
-          qa[ks][3] = pack_kv<KV8>(mid[2], mid[3]);
-          qb[ks][0] = pack_kv<KV8>(lo[0], lo[1]);
-          qb[ks][1] = pack_kv<KV8>(lo[2], lo[3]);
+          if constexpr (QSM) {
+            if (ks % WPC == wpg)  // the chunk's warps split the k-steps of its image
+              qimg[(qch * Cfg::KS + ks) * 32 + lane] =
+                  make_uint4(pack_kv<KV8>(hi[0], hi[1]), pack_kv<KV8>(mid[0], mid[1]), pack_kv<KV8>(hi[2], hi[3]),
+                             pack_kv<KV8>(mid[2], mid[3]));
+          } else {
+            qa[ks][0] = pack_kv<KV8>(hi[0], hi[1]);
+            qa[ks][1] = pack_kv<KV8>(mid[0], mid[1]);
+            qa[ks][2] = pack_kv<KV8>(hi[2], hi[3]);
+            qa[ks][3] = pack_kv<KV8>(mid[2], mid[3]);
+            qb[ks][0] = pack_kv<KV8>(lo[0], lo[1]);
+            qb[ks][1] = pack_kv<KV8>(lo[2], lo[3]);
+          }
         }
+        // (every warp finished the previous item: its combine ended with a barrier)
+        if constexpr (QSM) named_bar_sync(1, NWC * 32);
 #pragma unroll
         for (int nd = 0; nd < Cfg::ND; ++nd) acc[nd][0] = acc[nd][1] = acc[nd][2] = acc[nd][3] = 0.f;
         m_ref = -INFINITY;
@@ -741,10 +753,17 @@ __global__ void __launch_bounds__((NWC + 1) * 32, 1) attn_decode_kernel(const At
             const int ci = (nt * (Cfg::KS / 2) + kp) * 32 + lane;
             const uint4 kf = load_k<DP, KVF>(pbase, ci);
             const int k0 = 2 * kp, k1 = 2 * kp + 1;
-            mma_kv<KV8>(s0[nt], qa[k0][0], qa[k0][1], qa[k0][2], qa[k0][3], kf.x, kf.y);
-            if constexpr (!KV8) mma_kv<KV8>(s1[nt], qb[k0][0], 0u, qb[k0][1], 0u, kf.x, kf.y);
-            mma_kv<KV8>(s0[nt], qa[k1][0], qa[k1][1], qa[k1][2], qa[k1][3], kf.z, kf.w);
-            if constexpr (!KV8) mma_kv<KV8>(s1[nt], qb[k1][0], 0u, qb[k1][1], 0u, kf.z, kf.w);
+            if constexpr (QSM) {
+              const uint32_t qb0 = smem_u32(qimg) + ((qch * Cfg::KS + k0) * 32 + lane) * 16;
+              const uint4 a0 = lds128(qb0), a1 = lds128(qb0 + 32 * 16);
+              mma_kv<KV8>(s0[nt], a0.x, a0.y, a0.z, a0.w, kf.x, kf.y);
+              mma_kv<KV8>(s0[nt], a1.x, a1.y, a1.z, a1.w, kf.z, kf.w);
+            } else {
+              mma_kv<KV8>(s0[nt], qa[k0][0], qa[k0][1], qa[k0][2], qa[k0][3], kf.x, kf.y);
+              if constexpr (!KV8) mma_kv<KV8>(s1[nt], qb[k0][0], 0u, qb[k0][1], 0u, kf.x, kf.y);
+              mma_kv<KV8>(s0[nt], qa[k1][0], qa[k1][1], qa[k1][2], qa[k1][3], kf.z, kf.w);
+              if constexpr (!KV8) mma_kv<KV8>(s1[nt], qb[k1][0], 0u, qb[k1][1], 0u, kf.z, kf.w);
+            }
           }
         }
         // logits (log2 units) for query row g, tokens 2c, 2c+1, 8+2c, 9+2c
@@ -1128,7 +1147,8 @@ template <int DP, int NWC, int NSTAGE, int QC, int KVF, bool W16>
 static size_t attn_smem_bytes() {
   constexpr int SR = W16 ? 16 : 8;
   return NSTAGE * (NWC * AttnCfg<DP, KVF>::PAGE + QC * 8 * DP * 4) + NWC * (SR * DP + 2 * SR) * 4 +
-         (W16 ? 3 * (DP / 16) * 32 * 16 : 0) + NSTAGE * sizeof(StageMeta) + 2 * NSTAGE * 8 + 64;
+         (W16 ? 3 * (DP / 16) * 32 * 16 : (KVF == 2 ? QC * (DP / 16) * 32 * 16 : 0)) + NSTAGE * sizeof(StageMeta) +
+         2 * NSTAGE * 8 + 64;
 }
 
 template <int DP, int NWC, int NSTAGE, int QC, int KVF, bool W16>
@@ -1150,10 +1170,12 @@ static cudaError_t launch_attn_dp(const AttnParams& p, int grid, cudaStream_t st
     case 32: return launch_attn_t<32, 8, KV8 ? 8 : 4, QC, KVF, W16>(p, grid, stream);
     case 64: return launch_attn_t<64, 8, KV8 ? 6 : 3, QC, KVF, W16>(p, grid, stream);
     case 128:
-      // FP4 pages (2176 B each): the widening + scaling dominates the consumer work --
-      // as many consumer warps as registers allow without spills (10 x 168 regs;
-      // 12 warps spill), and deep rings (the pages are small)
-      if constexpr (KVF == 2 && QC == 1) return launch_attn_t<128, 10, 6, QC, KVF, W16>(p, grid, stream);
+      // FP4 pages (2240 B each): the widening + scaling dominates the consumer work --
+      // as many consumer warps as registers allow: with the query fragments in shared
+      // memory (QSM) 12 warps x 4 stages at 128 registers (configs[1] FP4 KV, 8 layers:
+      // 3.43 ms vs 3.56 at 10 x 6, 3.46 at 12 x 5, 3.48 at 14 x 4; registers-held
+      // query at 10 x 6: 3.66 ms)
+      if constexpr (KVF == 2 && QC == 1) return launch_attn_t<128, 12, 4, QC, KVF, W16>(p, grid, stream);
       // 16-row (W16) FP4 consumers, single-term P (128 registers): 12 warps x 3 stages,
       // 405B-like FP4 slice 0.406 ms vs 0.463 at 8 x 4, 0.444 at 10 x 4, 0.419 at 14 x 2
       // (14 x 3 and 12 x 4 exceed the shared memory)
