@@ -227,7 +227,7 @@ def pool_slice(a, preset, S, ep, w_dtype="bf16", kv_dtype="bf16"):
         out["workload"] = ("llama405b-like layer, one GPU of TPA=1 x KVP=8 (TPF=8): %d KV heads x %d tokens x B=%d; "
                            "QKV replicated, W_O rows and FFN features 1/8; collectives off (1 GPU)" % (K, s_loc, B))
         out["attention"] = {
-            "kernel": {"fp8": "attn_decode_kernel<128,12,2,2,fp8,W16>", "fp4": "attn_decode_kernel<128,8,4,2,fp4,W16>",
+            "kernel": {"fp8": "attn_decode_kernel<128,12,2,2,fp8,W16>", "fp4": "attn_decode_kernel<128,12,3,2,fp4,W16>",
                        "bf16": "attn_decode_kernel<128,8,2,2,W16>"}[kv_dtype]
                       + " (TMA bulk-copy page ring, mma.sync)", "launch_ms": att_ms,
             "algorithmic_kv_bytes": kv_bytes,
@@ -302,7 +302,7 @@ def kvp_slices(a):
 W_ELEM_BYTES = {"bf16": 2.0, "fp8": 1.0, "fp4": 17.0 / 32.0}  # fp4: e2m1 nibble + one exponent byte per 32 inputs
 KV_ELEM_BYTES = {"bf16": 2.0, "fp8": 1.0, "fp4": 17.5 / 32.0}  # fp4: e2m1 nibble + a K exponent byte / V f16 scale per 32
 KV_KERNEL = {"bf16": "attn_decode_kernel<128,7,3,1,bf16>", "fp8": "attn_decode_kernel<128,10,4,1,fp8>",
-             "fp4": "attn_decode_kernel<128,10,6,1,fp4>"}
+             "fp4": "attn_decode_kernel<128,12,4,1,fp4> (query image in shared memory)"}
 
 
 def fp8_kv_line(a, w_dtype="bf16", kv_dtype="fp8"):
